@@ -1,0 +1,181 @@
+/* knnj_c.h — the drop-in C ABI of the B200 KNN self-join engine.
+ *
+ * Replaces the hot path of the reference HybridKNN-Join library
+ * (/root/reference/proj, arXiv 1810.04758) at PHASE granularity: every entry
+ * point below names the reference function/class it stands in for
+ * (file:line, relative to /root/reference/). Plain pointers and sizes only; no
+ * C++ or torch types cross this boundary. Host buffers are caller-owned; all
+ * device memory is owned by the knnj_ctx (allocated lazily, freed by
+ * knnj_destroy). Calls on one ctx are synchronous and not re-entrant; use one
+ * ctx per GPU (one process per GPU for multi-GPU runs).
+ *
+ * Arithmetic contract: every distance that decides an output is the FP64
+ * squared Euclidean distance accumulated in the reference SCALAR kernel's
+ * order (proj/src/kernels_scalar.cpp:9-27: d=a-b; sum += d*d, separately
+ * rounded, dimensions in order), over the variance-reordered columns.
+ * Output distances are sqrt of that sum, so they are bit-identical to the
+ * reference run with kernel "scalar". FP32/FP16 is used only as a screen whose
+ * error is bounded rigorously; anything inside the bound is re-decided in FP64.
+ *
+ * Return codes mirror the reference exception types
+ * (proj/include/knnjoin/errors.hpp:11-62). */
+#ifndef KNNJ_C_H
+#define KNNJ_C_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KNNJ_ABI_VERSION 1
+
+enum knnj_status {
+    KNNJ_OK = 0,
+    KNNJ_E_USAGE = 1,             /* UsageError              errors.hpp:11-15 */
+    KNNJ_E_INGEST = 2,            /* IngestError             errors.hpp:17-21 */
+    KNNJ_E_INDEXING = 3,          /* IndexingError           errors.hpp:23-27 */
+    KNNJ_E_DEGENERATE = 4,        /* DegenerateProfileError  errors.hpp:29-34 */
+    KNNJ_E_TARGET_UNREACHABLE = 5,/* TargetUnreachableError  errors.hpp:36-42 */
+    KNNJ_E_BATCH_OVERFLOW = 6,    /* BatchOverflowError      errors.hpp:44-50 (never raised: no pair buffer) */
+    KNNJ_E_SAMPLE_TOO_SMALL = 7,  /* SampleTooSmallError     errors.hpp:52-56 */
+    KNNJ_E_ORACLE_CAP = 8,        /* OracleCapError          errors.hpp:58-62 */
+    KNNJ_E_CUDA = 9               /* device / runtime failure (no reference analogue) */
+};
+
+/* EngineMode, proj/include/knnjoin/orchestrator.hpp:15 */
+enum knnj_mode { KNNJ_HYBRID = 0, KNNJ_SPARSE_ONLY = 1, KNNJ_DENSE_ONLY = 2, KNNJ_BRUTE_ORACLE = 3 };
+/* Provenance, proj/include/knnjoin/orchestrator.hpp:43 */
+enum knnj_provenance { KNNJ_PROV_DENSE = 0, KNNJ_PROV_SPARSE = 1, KNNJ_PROV_DENSE_FAILED = 2 };
+
+typedef struct knnj_ctx knnj_ctx;
+
+/* ---- context ---------------------------------------------------------- */
+int knnj_abi_version(void);
+int knnj_create(int device, knnj_ctx** out);
+void knnj_destroy(knnj_ctx* ctx);
+/* Message of the last failed call on ctx (same text as the reference exception's what()). */
+const char* knnj_last_error(const knnj_ctx* ctx);
+/* Page-locked host buffers for the end-to-end path (H2D/D2H at full PCIe rate). */
+void* knnj_alloc_pinned(size_t bytes);
+void knnj_free_pinned(void* p);
+
+/* ---- dataset (Dataset, proj/include/knnjoin/dataset.hpp:14-40) --------- */
+/* Uploads |D| x n row-major FP64 points; rejects non-finite values like
+ * proj/src/dataset.cpp:22-33 ("non-finite coordinate at point i, dimension j"). */
+int knnj_set_points(knnj_ctx* ctx, const double* rowmajor, uint64_t n_points, uint32_t dims);
+/* reorder_by_variance, proj/src/dataset.cpp:87-111. perm[j] = original column of
+ * working column j; var (optional) = population variances of the ORIGINAL columns
+ * (Dataset::column_variances, dataset.cpp:58-74). Must precede the phases below. */
+int knnj_reorder_by_variance(knnj_ctx* ctx, uint32_t m, uint32_t* perm, double* var);
+/* Working (reordered) coordinates back to the host, |D| x n row-major. */
+int knnj_get_points(knnj_ctx* ctx, double* out);
+
+/* ---- distance (kernels::sq_dist_limited, proj/include/knnjoin/kernels.hpp:33-40) */
+/* out[i] = scalar-order squared distance of working points ij[2i], ij[2i+1], or
+ * +inf when it exceeds limit_sq (pass +inf for kernels::sq_dist). */
+int knnj_pair_sq(knnj_ctx* ctx, const uint64_t* ij, uint64_t n_pairs, double limit_sq,
+                 double* out);
+
+/* ---- epsilon selection (proj/src/epsilon.cpp) -------------------------- */
+/* estimate_eps_mean, epsilon.cpp:14-44 (pairs drawn with the reference RNG). */
+int knnj_eps_mean(knnj_ctx* ctx, uint64_t sample_pairs, uint64_t seed, double* out);
+/* build_distance_histogram, epsilon.cpp:46-120: integer bin counts (divide by
+ * *query_count for EpsilonProfile::counts). Queries are sampled on the host with
+ * the reference sampler (util.hpp:70-92); the all-pairs binning runs on the GPU. */
+int knnj_histogram(knnj_ctx* ctx, double eps_mean, uint32_t n_bins, double query_fraction,
+                   uint64_t seed, uint64_t* raw_counts, uint64_t* query_count);
+/* Same binning over an explicit query-id list (used for sharding). raw_counts
+ * is ACCUMULATED into (caller zeroes it). */
+int knnj_histogram_queries(knnj_ctx* ctx, const uint64_t* query_ids, uint64_t n_queries,
+                           double eps_mean, uint32_t n_bins, uint64_t* raw_counts);
+
+/* ---- grid index (GridIndex, proj/include/knnjoin/grid_index.hpp:34-84) -- */
+typedef struct {
+    uint32_t m;
+    double eps;
+    uint64_t n_cells;              /* |B| */
+    double mins[64], maxs[64];     /* first m working dims */
+    uint64_t cells_per_dim[64];
+} knnj_grid_info;
+/* GridIndex::build, grid_index.cpp:13-75 (IndexingError on 64-bit overflow). */
+int knnj_grid_build(knnj_ctx* ctx, uint32_t m, double eps, knnj_grid_info* info);
+/* B (n_cells), G (2*n_cells: begin,end), A (|D|), slot (|D|); any may be NULL. */
+int knnj_grid_export(knnj_ctx* ctx, uint64_t* B, uint64_t* G, uint32_t* A, uint32_t* slot);
+/* range_query sizes (self included) and candidates examined per query:
+ * grid_index.cpp:149-167 — what estimate_batches (dense_engine.cpp:48-75) sums. */
+int knnj_range_count(knnj_ctx* ctx, const uint32_t* queries, uint64_t n_queries,
+                     uint64_t* in_eps, uint64_t* candidates);
+
+/* ---- split (split_work, proj/src/partition.cpp:30-75) ------------------- */
+typedef struct {
+    double n_min, n_thresh;
+    uint64_t q_gpu, q_cpu, demoted;
+} knnj_split_info;
+int knnj_split(knnj_ctx* ctx, const uint32_t* queries, uint64_t n_queries, uint32_t k,
+               double beta, double gamma, double rho, uint8_t* is_dense, uint64_t* cell_pop,
+               knnj_split_info* info);
+
+/* ---- joins -------------------------------------------------------------- */
+typedef struct {
+    uint64_t candidates_examined; /* DenseJoinStats::candidates_examined (dense_engine.hpp:86-92) */
+    uint64_t solved, failed;
+    double kernel_ms;             /* device time of the fused join kernels (CUDA events) */
+} knnj_join_stats;
+/* run_dense_join (dense_engine.cpp:229-303) with filter_keys fused
+ * (dense_engine.cpp:165-196): per query solved[i] = 1 and k (dist,id)-ordered
+ * neighbours, or solved[i] = 0 (failed; row contents unspecified). */
+int knnj_dense_join(knnj_ctx* ctx, const uint32_t* queries, uint64_t n_queries, uint32_t k,
+                    uint32_t* ids, double* dist, uint8_t* solved, knnj_join_stats* stats);
+/* Exact KNN, self excluded, (dist,id) order: the contract of KdTree::knn_query
+ * (proj/src/kdtree.cpp:109-159) and brute_force_knn (dense_engine.cpp:322-346).
+ * Needs only knnj_set_points (+ optional reorder). k <= |D|-1. */
+int knnj_exact_knn(knnj_ctx* ctx, const uint32_t* queries, uint64_t n_queries, uint32_t k,
+                   uint32_t* ids, double* dist);
+
+/* ---- full pipeline (run_hybrid, proj/src/orchestrator.cpp:67-250) ------- */
+typedef struct {
+    uint32_t k;                   /* RunConfig::k */
+    uint32_t m;                   /* 0 -> min(6, n) */
+    double beta, gamma, rho;
+    uint32_t mode;                /* enum knnj_mode */
+    uint32_t n_bins;              /* 100 */
+    double hist_query_fraction;   /* 0.01 */
+    uint64_t eps_mean_pair_cap;   /* 1e6 */
+    uint64_t seed;
+    const uint32_t* query_subset; /* NULL = all points */
+    uint64_t n_query_subset;
+} knnj_config;
+
+typedef struct {
+    uint64_t n_queries;
+    uint32_t k_effective, m_used;
+    uint32_t k_clamped, eps_fallback;
+    double eps_mean, bin_width, eps_default, eps_beta, eps_final, eps_used;
+    uint64_t hist_query_count, hist_bin;
+    double n_min, n_thresh;
+    uint64_t q_gpu, q_cpu, demoted, failed_count;
+    uint64_t candidates_examined;
+    uint64_t fallback_queries, fallback_passes, slow_path_queries;
+    uint64_t grid_cells;
+    /* device-event timings (ms) */
+    double ms_upload, ms_reorder, ms_eps_mean, ms_histogram, ms_grid, ms_split, ms_join,
+        ms_fallback, ms_download, ms_total;
+    double ms_join_kernel, ms_hist_kernel;
+    uint32_t perm[1024];
+} knnj_run_info;
+
+/* Runs Alg. 1 over the points set by knnj_set_points (which it reorders in place).
+ * Outputs (caller-allocated, n_queries rows in ascending query-id order):
+ *   ids, dist : n_queries * k_effective   (row stride k_effective)
+ *   prov      : n_queries                 (enum knnj_provenance)
+ *   raw_hist  : n_bins (may be NULL)      integer histogram counts
+ * k_effective = min(k, |D|-1) (orchestrator.cpp:77-82). */
+int knnj_run(knnj_ctx* ctx, const knnj_config* cfg, uint32_t* ids, double* dist, uint8_t* prov,
+             uint64_t* raw_hist, knnj_run_info* info);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KNNJ_C_H */

@@ -1,0 +1,1509 @@
+// Host runtime and C ABI of the B200 KNN self-join engine.
+//
+// Mirrors the reference's phase functions (see include/knnj_c.h for the
+// file:line each entry point replaces) and its orchestrator run_hybrid
+// (proj/src/orchestrator.cpp:67-250). Host code does only what must stay
+// sequential to be bit-identical with the reference (the mt19937_64 sampling
+// streams, the sequential eps_mean sum, the O(n_bins) selection arithmetic);
+// all per-point and per-pair work runs on the GPU.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <memory>
+#include <numeric>
+#include <random>
+#include <string>
+#include <vector>
+
+#include <cub/cub.cuh>
+
+#include "knnj_c.h"
+#include "knnj_internal.cuh"
+
+using namespace kj;
+
+namespace {
+
+constexpr double kInf = std::numeric_limits<double>::infinity();
+constexpr double U64 = 1.1102230246251565e-16;  // 2^-53
+
+// ---------------------------------------------------------------- CUB helpers
+struct Scratch {
+    DBuf<unsigned char> tmp;
+    void* get(size_t bytes) { return tmp.ensure(bytes); }
+};
+
+void sort_pairs_u64_u32(Scratch& sc, const uint64_t* kin, uint64_t* kout, const uint32_t* vin,
+                        uint32_t* vout, uint64_t n, int end_bit, cudaStream_t s) {
+    size_t bytes = 0;
+    KJ_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, kin, kout, vin, vout, (int64_t)n, 0,
+                                            end_bit, s));
+    KJ_CUDA(cub::DeviceRadixSort::SortPairs(sc.get(bytes), bytes, kin, kout, vin, vout,
+                                            (int64_t)n, 0, end_bit, s));
+}
+void sort_pairs_u32_u32(Scratch& sc, const uint32_t* kin, uint32_t* kout, const uint32_t* vin,
+                        uint32_t* vout, uint64_t n, int end_bit, cudaStream_t s) {
+    size_t bytes = 0;
+    KJ_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, kin, kout, vin, vout, (int64_t)n, 0,
+                                            end_bit, s));
+    KJ_CUDA(cub::DeviceRadixSort::SortPairs(sc.get(bytes), bytes, kin, kout, vin, vout,
+                                            (int64_t)n, 0, end_bit, s));
+}
+void sort_desc_u64_u32(Scratch& sc, const unsigned long long* kin, unsigned long long* kout,
+                       const uint32_t* vin, uint32_t* vout, uint64_t n, cudaStream_t s) {
+    size_t bytes = 0;
+    KJ_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, bytes, kin, kout, vin, vout,
+                                                      (int64_t)n, 0, 64, s));
+    KJ_CUDA(cub::DeviceRadixSort::SortPairsDescending(sc.get(bytes), bytes, kin, kout, vin, vout,
+                                                      (int64_t)n, 0, 64, s));
+}
+template <class T>
+void inclusive_sum(Scratch& sc, const T* in, T* out, uint64_t n, cudaStream_t s) {
+    size_t bytes = 0;
+    KJ_CUDA(cub::DeviceScan::InclusiveSum(nullptr, bytes, in, out, (int64_t)n, s));
+    KJ_CUDA(cub::DeviceScan::InclusiveSum(sc.get(bytes), bytes, in, out, (int64_t)n, s));
+}
+template <class T>
+void exclusive_sum(Scratch& sc, const T* in, T* out, uint64_t n, cudaStream_t s) {
+    size_t bytes = 0;
+    KJ_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, (int64_t)n, s));
+    KJ_CUDA(cub::DeviceScan::ExclusiveSum(sc.get(bytes), bytes, in, out, (int64_t)n, s));
+}
+// run-length encode: unique, counts, number of runs (device)
+void rle(Scratch& sc, const uint32_t* in, uint32_t* uniq, uint32_t* counts, uint64_t* nruns,
+         uint64_t n, cudaStream_t s) {
+    size_t bytes = 0;
+    KJ_CUDA(cub::DeviceRunLengthEncode::Encode(nullptr, bytes, in, uniq, counts, nruns,
+                                               (int64_t)n, s));
+    KJ_CUDA(cub::DeviceRunLengthEncode::Encode(sc.get(bytes), bytes, in, uniq, counts, nruns,
+                                               (int64_t)n, s));
+}
+template <class T>
+void reduce_sum(Scratch& sc, const T* in, T* out, uint64_t n, cudaStream_t s) {
+    size_t bytes = 0;
+    KJ_CUDA(cub::DeviceReduce::Sum(nullptr, bytes, in, out, (int64_t)n, s));
+    KJ_CUDA(cub::DeviceReduce::Sum(sc.get(bytes), bytes, in, out, (int64_t)n, s));
+}
+
+int bits_for(uint64_t maxval) {
+    int b = 0;
+    while (b < 64 && (maxval >> b) != 0) ++b;
+    return std::max(b, 1);
+}
+
+float f32_round_up(double v) {
+    float f = (float)v;
+    if ((double)f < v) f = std::nextafter(f, std::numeric_limits<float>::infinity());
+    return f;
+}
+float f32_round_down(double v) {
+    float f = (float)v;
+    if ((double)f > v) f = std::nextafter(f, -std::numeric_limits<float>::infinity());
+    return f;
+}
+
+// Sampler with the reference's exact output (proj/include/knnjoin/util.hpp:70-92):
+// partial Fisher-Yates over an index map, same libstdc++ distribution calls.
+std::vector<uint64_t> sample_without_replacement(uint64_t n, uint64_t k, std::mt19937_64& rng) {
+    std::vector<uint64_t> out;
+    if (k >= n) {
+        out.resize(n);
+        std::iota(out.begin(), out.end(), 0ull);
+        return out;
+    }
+    out.reserve(k);
+    uint64_t cap = 16;
+    while (cap < 2 * k + 16) cap <<= 1;
+    std::vector<uint64_t> keys(cap, ~0ull), vals(cap);
+    auto slot = [&](uint64_t key) {
+        uint64_t h = (key * 0x9E3779B97F4A7C15ull) >> 17;
+        h &= cap - 1;
+        while (keys[h] != ~0ull && keys[h] != key) h = (h + 1) & (cap - 1);
+        return h;
+    };
+    for (uint64_t i = 0; i < k; ++i) {
+        std::uniform_int_distribution<uint64_t> dist(i, n - 1);
+        uint64_t j = dist(rng);
+        uint64_t sj = slot(j);
+        uint64_t jv = keys[sj] == j ? vals[sj] : j;
+        uint64_t si = slot(i);
+        uint64_t iv = keys[si] == i ? vals[si] : i;
+        out.push_back(jv);
+        sj = slot(j);
+        keys[sj] = j;
+        vals[sj] = iv;
+    }
+    std::sort(out.begin(), out.end());
+    return out;
+}
+
+uint64_t splitmix64(uint64_t x) {
+    x += 0x9e3779b97f4a7c15ull;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+    return x ^ (x >> 31);
+}
+uint64_t derive_seed(uint64_t master, uint64_t tag) { return splitmix64(master ^ splitmix64(tag)); }
+
+struct Timer {
+    cudaEvent_t a, b;
+    cudaStream_t s;
+    explicit Timer(cudaStream_t st) : s(st) {
+        KJ_CUDA(cudaEventCreate(&a));
+        KJ_CUDA(cudaEventCreate(&b));
+        KJ_CUDA(cudaEventRecord(a, s));
+    }
+    ~Timer() {
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+    }
+    double ms() {
+        KJ_CUDA(cudaEventRecord(b, s));
+        KJ_CUDA(cudaEventSynchronize(b));
+        float f = 0;
+        KJ_CUDA(cudaEventElapsedTime(&f, a, b));
+        return f;
+    }
+};
+
+}  // namespace
+
+// ============================================================================ context
+struct knnj_ctx {
+    int dev = 0;
+    cudaStream_t s = nullptr;
+    std::string err;
+    Scratch sc;
+
+    uint64_t N = 0;
+    uint32_t n = 0;
+    uint64_t Npad = 0;
+    bool have_points = false, working_ready = false;
+    std::vector<uint32_t> perm;
+    std::vector<double> var;  // original-column variances
+    std::vector<double> g;    // working-column means (float centre)
+    double Rg = 0.0;          // max ||x - g||
+
+    DBuf<double> X0, X64;
+    DBuf<float> Xf;           // SoA id order
+    DBuf<double> d_g;
+
+    Level levels[40];
+    double eps0 = 0.0;
+    uint32_t m0 = 0;
+
+    // small device scratch
+    DBuf<unsigned long long> d_u64a, d_u64b;
+    DBuf<double> d_part;
+
+    ~knnj_ctx() {
+        if (s) cudaStreamDestroy(s);
+    }
+
+    void sync() { KJ_CUDA(cudaStreamSynchronize(s)); }
+
+    // ------------------------------------------------------------ screen constants
+    void screen_consts(float& gam, float& erg, float& eab, float& e64) const {
+        const double u = 5.9604644775390625e-08;  // 2^-24
+        const double gamma = (n + 2) * u / (1.0 - (n + 2) * u);
+        gam = (float)(2.02 * gamma * 1.01);
+        const double u1 = u * (1.0 + 1e-6);
+        erg = (float)(2.0 * u1 * Rg * 1.01 + 1e-30);
+        eab = (float)(u * (1.0 + 2.0 * u) * 1.01);
+        e64 = (float)((n + 4) * 2.0 * U64 * 1.01);
+    }
+
+    // ------------------------------------------------------------ working set
+    // Working coordinates from a column order; builds the FP32 SoA copy
+    // centred at the working-column means.
+    void make_working(const std::vector<uint32_t>& order, const std::vector<double>& mean0) {
+        X64.ensure(N * n);
+        DBuf<uint32_t> d_ord;
+        d_ord.ensure(n);
+        KJ_CUDA(cudaMemcpyAsync(d_ord.p, order.data(), n * 4, cudaMemcpyHostToDevice, s));
+        launch_permute_cols(X0.p, X64.p, N, n, d_ord.p, s);
+        g.resize(n);
+        for (uint32_t j = 0; j < n; ++j) g[j] = mean0[order[j]];
+        d_g.ensure(n);
+        KJ_CUDA(cudaMemcpyAsync(d_g.p, g.data(), n * 8, cudaMemcpyHostToDevice, s));
+        Npad = ((N + 127) / 128) * 128 + 128;
+        Xf.ensure((uint64_t)n * Npad);
+        d_u64a.ensure(1);
+        KJ_CUDA(cudaMemsetAsync(d_u64a.p, 0, 8, s));
+        launch_to_float_soa(X64.p, N, n, d_g.p, Xf.p, Npad, d_u64a.p, s);
+        unsigned long long bits = 0;
+        KJ_CUDA(cudaMemcpyAsync(&bits, d_u64a.p, 8, cudaMemcpyDeviceToHost, s));
+        sync();
+        double r2;
+        std::memcpy(&r2, &bits, 8);
+        Rg = std::sqrt(r2) * (1.0 + 1e-12);
+        perm = order;
+        working_ready = true;
+        for (auto& lv : levels) lv.built = false;
+    }
+
+    // column means (and variances when want_var) of X0, deterministic on device
+    void column_stats(std::vector<double>& mean, std::vector<double>* varp) {
+        const uint32_t nblk = (uint32_t)std::min<uint64_t>(1024, std::max<uint64_t>(1, N / 64));
+        d_part.ensure((uint64_t)nblk * n);
+        std::vector<double> part((uint64_t)nblk * n);
+        launch_col_sums(X0.p, N, n, nullptr, d_part.p, nblk, s);
+        KJ_CUDA(cudaMemcpyAsync(part.data(), d_part.p, part.size() * 8, cudaMemcpyDeviceToHost, s));
+        sync();
+        mean.assign(n, 0.0);
+        for (uint32_t b = 0; b < nblk; ++b)
+            for (uint32_t j = 0; j < n; ++j) mean[j] += part[(uint64_t)b * n + j];
+        for (uint32_t j = 0; j < n; ++j) mean[j] /= double(N);
+        if (!varp) return;
+        DBuf<double> d_mean;
+        d_mean.ensure(n);
+        KJ_CUDA(cudaMemcpyAsync(d_mean.p, mean.data(), n * 8, cudaMemcpyHostToDevice, s));
+        launch_col_sums(X0.p, N, n, d_mean.p, d_part.p, nblk, s);
+        KJ_CUDA(cudaMemcpyAsync(part.data(), d_part.p, part.size() * 8, cudaMemcpyDeviceToHost, s));
+        sync();
+        varp->assign(n, 0.0);
+        for (uint32_t b = 0; b < nblk; ++b)
+            for (uint32_t j = 0; j < n; ++j) (*varp)[j] += part[(uint64_t)b * n + j];
+        for (uint32_t j = 0; j < n; ++j) (*varp)[j] /= double(N);
+    }
+
+    // Exact reference arithmetic for selected columns (dataset.cpp:58-74): used only
+    // when two device variances are too close to order safely.
+    void exact_column_variance(const std::vector<uint32_t>& cols, std::vector<double>& var_out) {
+        std::vector<double> col(N);
+        for (uint32_t j : cols) {
+            KJ_CUDA(cudaMemcpy2DAsync(col.data(), 8, X0.p + j, (size_t)n * 8, 8, N,
+                                      cudaMemcpyDeviceToHost, s));
+            sync();
+            double mean = 0.0;
+            for (uint64_t i = 0; i < N; ++i) mean += col[i];
+            mean /= double(N);
+            double v = 0.0;
+            for (uint64_t i = 0; i < N; ++i) {
+                double d = col[i] - mean;
+                v += d * d;
+            }
+            var_out[j] = v / double(N);
+        }
+    }
+
+    // ------------------------------------------------------------ reorder
+    // reorder_by_variance (dataset.cpp:87-111)
+    void reorder(uint32_t m) {
+        if (m < 1 || m > n) throw Error(1, "indexed dimension count m must satisfy 1 <= m <= n");
+        std::vector<double> mean, v;
+        column_stats(mean, &v);
+        // guard band: the reference sums sequentially (relative error <= ~N*2^-53);
+        // ties or near-ties are re-decided with the reference's own arithmetic.
+        const double tau = 8.0 * double(N) * U64 + 1e-12;
+        std::vector<uint32_t> order(n);
+        std::iota(order.begin(), order.end(), 0u);
+        std::sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) {
+            if (v[a] != v[b]) return v[a] > v[b];
+            return a < b;
+        });
+        std::vector<uint32_t> close;
+        for (uint32_t i = 0; i + 1 < n; ++i) {
+            double a = v[order[i]], b = v[order[i + 1]];
+            if (std::fabs(a - b) <= tau * std::max(std::fabs(a), std::fabs(b))) {
+                close.push_back(order[i]);
+                close.push_back(order[i + 1]);
+            }
+        }
+        if (!close.empty()) {
+            std::sort(close.begin(), close.end());
+            close.erase(std::unique(close.begin(), close.end()), close.end());
+            exact_column_variance(close, v);
+            std::sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) {
+                if (v[a] != v[b]) return v[a] > v[b];
+                return a < b;
+            });
+        }
+        var = v;
+        make_working(order, mean);
+    }
+
+    void ensure_working() {
+        if (working_ready) return;
+        std::vector<double> mean;
+        column_stats(mean, nullptr);
+        std::vector<uint32_t> id(n);
+        std::iota(id.begin(), id.end(), 0u);
+        make_working(id, mean);
+    }
+
+    // ------------------------------------------------------------ eps_mean
+    double eps_mean(uint64_t sample_pairs, uint64_t seed) {
+        if (N < 2) throw Error(1, "eps_mean estimation needs at least two points");
+        if (sample_pairs < 1) throw Error(1, "sample_pairs must be at least 1");
+        const uint64_t all = N * (N - 1);
+        std::vector<uint64_t> ij;
+        uint64_t used;
+        if (sample_pairs >= all) {
+            ij.reserve(2 * all);
+            for (uint64_t i = 0; i < N; ++i)
+                for (uint64_t j = 0; j < N; ++j)
+                    if (i != j) {
+                        ij.push_back(i);
+                        ij.push_back(j);
+                    }
+            used = all;
+        } else {
+            ij.resize(2 * sample_pairs);
+            std::mt19937_64 rng(seed);
+            std::uniform_int_distribution<uint64_t> pick(0, N - 1);
+            for (uint64_t p = 0; p < sample_pairs; ++p) {
+                uint64_t i = pick(rng);
+                uint64_t j = pick(rng);
+                while (j == i) j = pick(rng);
+                ij[2 * p] = i;
+                ij[2 * p + 1] = j;
+            }
+            used = sample_pairs;
+        }
+        std::vector<double> sq = pair_sq(ij.data(), used, kInf);
+        double sum = 0.0;
+        for (uint64_t p = 0; p < used; ++p) sum += std::sqrt(sq[p]);
+        return sum / double(used);
+    }
+
+    std::vector<double> pair_sq(const uint64_t* ij, uint64_t np, double limit) {
+        DBuf<uint64_t> d_ij;
+        DBuf<double> d_out;
+        d_ij.ensure(2 * np);
+        d_out.ensure(np);
+        KJ_CUDA(cudaMemcpyAsync(d_ij.p, ij, 16 * np, cudaMemcpyHostToDevice, s));
+        launch_pair_sq(X64.p, n, d_ij.p, np, limit, d_out.p, s);
+        std::vector<double> out(np);
+        KJ_CUDA(cudaMemcpyAsync(out.data(), d_out.p, 8 * np, cudaMemcpyDeviceToHost, s));
+        sync();
+        return out;
+    }
+
+    // ------------------------------------------------------------ histogram
+    // bin of an exact sq, as epsilon.cpp:86-95 computes it (n_bins = uncounted)
+    static uint64_t ref_bin(double sq, double eps_mean, double inv_width, uint32_t nb) {
+        if (sq > eps_mean * eps_mean) return nb;
+        double dist = std::sqrt(sq);
+        if (dist >= eps_mean) return nb;
+        uint64_t b = (uint64_t)(dist * inv_width);
+        if (b >= nb) b = nb - 1;
+        return b;
+    }
+    // smallest double sq >= 0 whose bin is >= b (monotone in sq)
+    static double bin_threshold(uint64_t b, double eps_mean, double inv_width, uint32_t nb) {
+        uint64_t lo = 0, hi = 0x7FF0000000000000ull;  // +inf bits
+        while (lo < hi) {
+            uint64_t mid = lo + (hi - lo) / 2;
+            double v;
+            std::memcpy(&v, &mid, 8);
+            if (ref_bin(v, eps_mean, inv_width, nb) >= b) hi = mid;
+            else lo = mid + 1;
+        }
+        double r;
+        std::memcpy(&r, &lo, 8);
+        return r;
+    }
+
+    double last_hist_kernel_ms = 0.0;
+    void histogram_queries(const uint64_t* qids, uint64_t nq, double em, uint32_t nb,
+                           uint64_t* raw) {
+        if (!(em > 0.0))
+            throw Error(4, "mean pairwise distance is not positive; cannot build a distance histogram");
+        if (nb < 2) throw Error(1, "histogram needs at least 2 bins");
+        const double width = em / double(nb);
+        const double inv_width = 1.0 / width;
+        std::vector<float> SU(nb + 1), SD(nb + 1);
+        std::vector<double> S(nb + 1);
+        for (uint32_t b = 1; b <= nb; ++b) S[b] = bin_threshold(b, em, inv_width, nb);
+        SU[0] = -std::numeric_limits<float>::infinity();
+        for (uint32_t b = 1; b <= nb; ++b) SU[b] = f32_round_up(S[b]);
+        for (uint32_t b = 0; b < nb; ++b) SD[b] = f32_round_down(S[b + 1]);
+        SD[nb] = SU[nb];
+        DBuf<float> d_tab;
+        d_tab.ensure(2 * (nb + 1));
+        KJ_CUDA(cudaMemcpyAsync(d_tab.p, SU.data(), 4 * (nb + 1), cudaMemcpyHostToDevice, s));
+        KJ_CUDA(cudaMemcpyAsync(d_tab.p + nb + 1, SD.data(), 4 * (nb + 1), cudaMemcpyHostToDevice, s));
+        std::vector<uint32_t> q32(nq);
+        for (uint64_t i = 0; i < nq; ++i) q32[i] = (uint32_t)qids[i];
+        DBuf<uint32_t> d_q;
+        d_q.ensure(nq);
+        KJ_CUDA(cudaMemcpyAsync(d_q.p, q32.data(), 4 * nq, cudaMemcpyHostToDevice, s));
+        DBuf<unsigned long long> d_cnt;
+        d_cnt.ensure(nb);
+        KJ_CUDA(cudaMemsetAsync(d_cnt.p, 0, 8 * nb, s));
+        if (nb > 256) throw Error(1, "n_bins above 256 is not supported by the device histogram");
+
+        HistArgs a{};
+        a.Xf = Xf.p;
+        a.Npad = Npad;
+        a.N = N;
+        a.n = n;
+        a.X64 = X64.p;
+        a.q = d_q.p;
+        a.nq = nq;
+        a.n_bins = nb;
+        a.SU = d_tab.p;
+        a.SD = d_tab.p + nb + 1;
+        a.eps_mean = em;
+        a.limit_sq = em * em;
+        a.inv_width = inv_width;
+        a.counts = d_cnt.p;
+        screen_consts(a.gam, a.erg, a.eab, a.e64);
+        const int np = pick_np(n);
+        const uint64_t T = np <= 32 ? 128 : 64;
+        const uint64_t qblocks = (nq + JB - 1) / JB;
+        uint64_t want_blocks = 148 * 16;
+        uint64_t slabs = std::max<uint64_t>(1, (want_blocks + qblocks - 1) / qblocks);
+        slabs = std::min<uint64_t>(slabs, (N + T - 1) / T);
+        slabs = std::min<uint64_t>(slabs, 65535);
+        uint64_t stride = (N + slabs - 1) / slabs;
+        stride = ((stride + T - 1) / T) * T;
+        slabs = (N + stride - 1) / stride;
+        a.cand_begin_stride = stride;
+        Timer t(s);
+        launch_histogram(a, slabs, s);
+        std::vector<unsigned long long> c(nb);
+        KJ_CUDA(cudaMemcpyAsync(c.data(), d_cnt.p, 8 * nb, cudaMemcpyDeviceToHost, s));
+        last_hist_kernel_ms = t.ms();
+        for (uint32_t b = 0; b < nb; ++b) raw[b] += c[b];
+    }
+
+    std::vector<uint64_t> histogram_sample(double frac, uint64_t seed) {
+        if (!(frac > 0.0) || frac > 1.0) throw Error(1, "query_fraction must be in (0, 1]");
+        uint64_t want = (uint64_t)std::floor(frac * double(N));
+        want = std::max<uint64_t>(want, 100);
+        want = std::min<uint64_t>(want, N);
+        std::mt19937_64 rng(seed);
+        return sample_without_replacement(N, want, rng);
+    }
+
+    // ------------------------------------------------------------ grid levels
+    // GridIndex::build (grid_index.cpp:13-75) at cell width w (level 0: w = eps).
+    void build_level(int L, uint32_t m, double w) {
+        Level& lv = levels[L];
+        if (lv.built && lv.m == m && lv.w == w) return;
+        lv.built = false;
+        lv.m = m;
+        lv.w = w;
+        // min / max per indexed dim (exact)
+        d_u64a.ensure(64);
+        d_u64b.ensure(64);
+        std::vector<unsigned long long> init_mn(m, ~0ull), init_mx(m, 0ull);
+        KJ_CUDA(cudaMemcpyAsync(d_u64a.p, init_mn.data(), 8 * m, cudaMemcpyHostToDevice, s));
+        KJ_CUDA(cudaMemcpyAsync(d_u64b.p, init_mx.data(), 8 * m, cudaMemcpyHostToDevice, s));
+        launch_minmax(X64.p, N, n, m, d_u64a.p, d_u64b.p, s);
+        std::vector<unsigned long long> mn(m), mx(m);
+        KJ_CUDA(cudaMemcpyAsync(mn.data(), d_u64a.p, 8 * m, cudaMemcpyDeviceToHost, s));
+        KJ_CUDA(cudaMemcpyAsync(mx.data(), d_u64b.p, 8 * m, cudaMemcpyDeviceToHost, s));
+        sync();
+        auto unorder = [](unsigned long long o) {
+            unsigned long long b = (o & 0x8000000000000000ull) ? (o & 0x7FFFFFFFFFFFFFFFull) : ~o;
+            double v;
+            std::memcpy(&v, &b, 8);
+            return v;
+        };
+        lv.mins.resize(m);
+        lv.maxs.resize(m);
+        for (uint32_t j = 0; j < m; ++j) {
+            lv.mins[j] = unorder(mn[j]);
+            lv.maxs[j] = unorder(mx[j]);
+        }
+        lv.cpd.resize(m);
+        lv.strides.resize(m);
+        unsigned __int128 total = 1;
+        for (uint32_t j = 0; j < m; ++j) {
+            double extent = (lv.maxs[j] - lv.mins[j]) / w;
+            if (!(extent < 9.2e18)) {
+                throw Error(3, "grid extent overflows linear cell ids: dimension " +
+                                   std::to_string(j) + " requires about " +
+                                   std::to_string(extent) + " cells of width " +
+                                   std::to_string(w));
+            }
+            lv.cpd[j] = std::max<uint64_t>(1, (uint64_t)std::floor(extent) + 1);
+            total *= lv.cpd[j];
+            if (total > std::numeric_limits<uint64_t>::max()) {
+                std::string req;
+                for (uint32_t t = 0; t <= j; ++t) req += (t ? "x" : "") + std::to_string(lv.cpd[t]);
+                throw Error(3, "grid extent overflows linear cell ids: required extent " + req +
+                                   " exceeds 64-bit range");
+            }
+        }
+        lv.strides[m - 1] = 1;
+        for (uint32_t j = m - 1; j-- > 0;) lv.strides[j] = lv.strides[j + 1] * lv.cpd[j + 1];
+        lv.key_bits = bits_for((uint64_t)(total - 1));
+
+        DBuf<double> d_mins;
+        DBuf<uint64_t> d_cs;
+        d_mins.ensure(m);
+        d_cs.ensure(2 * m);
+        KJ_CUDA(cudaMemcpyAsync(d_mins.p, lv.mins.data(), 8 * m, cudaMemcpyHostToDevice, s));
+        KJ_CUDA(cudaMemcpyAsync(d_cs.p, lv.cpd.data(), 8 * m, cudaMemcpyHostToDevice, s));
+        KJ_CUDA(cudaMemcpyAsync(d_cs.p + m, lv.strides.data(), 8 * m, cudaMemcpyHostToDevice, s));
+        DBuf<uint64_t> keys, skeys;
+        DBuf<uint32_t> vals, runidx;
+        keys.ensure(N);
+        skeys.ensure(N);
+        vals.ensure(N);
+        lv.A.ensure(N);
+        launch_cell_keys(X64.p, N, n, m, d_mins.p, w, d_cs.p, d_cs.p + m, keys.p, vals.p, s);
+        sort_pairs_u64_u32(sc, keys.p, skeys.p, vals.p, lv.A.p, N, lv.key_bits, s);
+        runidx.ensure(N);
+        launch_head_flags(skeys.p, N, vals.p, s);  // vals reused as flags
+        inclusive_sum(sc, vals.p, runidx.p, N, s);
+        uint32_t nruns = 0;
+        KJ_CUDA(cudaMemcpyAsync(&nruns, runidx.p + N - 1, 4, cudaMemcpyDeviceToHost, s));
+        sync();
+        lv.ncells = nruns;
+        lv.B.ensure(nruns);
+        lv.G.ensure(nruns);
+        lv.slot.ensure(N);
+        lv.posOf.ensure(N);
+        launch_grid_tables(skeys.p, lv.A.p, runidx.p, N, lv.B.p, lv.G.p, lv.slot.p, lv.posOf.p, s);
+        lv.Xs.ensure((uint64_t)n * Npad);
+        launch_gather_soa(Xf.p, lv.A.p, N, n, Npad, lv.Xs.p, s);
+        sync();
+        lv.built = true;
+    }
+
+    double cover2(const Level& lv) const {
+        bool all = true;
+        uint64_t cmax = 0;
+        for (uint64_t c : lv.cpd) {
+            all = all && c <= 2;
+            cmax = std::max(cmax, c);
+        }
+        if (all) return kInf;
+        const double eta = 16.0 * U64 * (double(cmax) + n + 8);
+        return lv.w * lv.w * (1.0 - eta);
+    }
+
+    // ------------------------------------------------------------ passes
+    // Groups the queries (point ids + output rows, on device) by their cell in
+    // level lv and builds work items + candidate ranges.
+    void build_pass(Level& lv, const uint32_t* d_qpid, const uint32_t* d_qrow, uint64_t nq,
+                    Pass& P) {
+        P.nq = nq;
+        P.nitems = P.nadj = P.candidates = 0;
+        if (!nq) return;
+        DBuf<uint32_t> pos_unsorted, qcell;
+        pos_unsorted.ensure(nq);
+        launch_map_u32(d_qpid, lv.posOf.p, nq, pos_unsorted.p, s);
+        P.qpos.ensure(nq);
+        P.qrow.ensure(nq);
+        sort_pairs_u32_u32(sc, pos_unsorted.p, P.qpos.p, d_qrow, P.qrow.p, nq, bits_for(N), s);
+        qcell.ensure(nq);
+        {
+            DBuf<uint32_t> tmp;
+            tmp.ensure(nq);
+            launch_map_u32(P.qpos.p, lv.A.p, nq, tmp.p, s);
+            launch_map_u32(tmp.p, lv.slot.p, nq, qcell.p, s);
+        }
+        DBuf<uint32_t> ucell, ucnt;
+        DBuf<uint64_t> d_nruns;
+        ucell.ensure(nq);
+        ucnt.ensure(nq);
+        d_nruns.ensure(1);
+        rle(sc, qcell.p, ucell.p, ucnt.p, d_nruns.p, nq, s);
+        uint64_t nuc = 0;
+        KJ_CUDA(cudaMemcpyAsync(&nuc, d_nruns.p, 8, cudaMemcpyDeviceToHost, s));
+        sync();
+        DBuf<uint32_t> ufirst, nit, item_off, adj_cnt, adj_off;
+        ufirst.ensure(nuc + 1);
+        exclusive_sum(sc, ucnt.p, ufirst.p, nuc, s);
+        // items per unique cell = ceil(cnt / JB): reuse host loop via device copy
+        std::vector<uint32_t> h_cnt(nuc);
+        KJ_CUDA(cudaMemcpyAsync(h_cnt.data(), ucnt.p, 4 * nuc, cudaMemcpyDeviceToHost, s));
+        sync();
+        std::vector<uint32_t> h_ioff(nuc + 1);
+        uint64_t tot = 0;
+        for (uint64_t u = 0; u < nuc; ++u) {
+            h_ioff[u] = (uint32_t)tot;
+            tot += (h_cnt[u] + JB - 1) / JB;
+        }
+        h_ioff[nuc] = (uint32_t)tot;
+        P.nitems = tot;
+        item_off.ensure(nuc + 1);
+        KJ_CUDA(cudaMemcpyAsync(item_off.p, h_ioff.data(), 4 * (nuc + 1), cudaMemcpyHostToDevice, s));
+        // adjacency
+        DBuf<uint64_t> d_cs;
+        d_cs.ensure(2 * lv.m);
+        KJ_CUDA(cudaMemcpyAsync(d_cs.p, lv.cpd.data(), 8 * lv.m, cudaMemcpyHostToDevice, s));
+        KJ_CUDA(cudaMemcpyAsync(d_cs.p + lv.m, lv.strides.data(), 8 * lv.m, cudaMemcpyHostToDevice, s));
+        adj_cnt.ensure(nuc + 1);
+        adj_off.ensure(nuc + 1);
+        launch_adj_count(lv.B.p, lv.ncells, ucell.p, nuc, lv.m, d_cs.p, d_cs.p + lv.m, adj_cnt.p, s);
+        KJ_CUDA(cudaMemsetAsync(adj_cnt.p + nuc, 0, 4, s));
+        exclusive_sum(sc, adj_cnt.p, adj_off.p, nuc + 1, s);
+        uint32_t nadj = 0;
+        KJ_CUDA(cudaMemcpyAsync(&nadj, adj_off.p + nuc, 4, cudaMemcpyDeviceToHost, s));
+        sync();
+        P.nadj = nadj;
+        P.adj.ensure(nadj);
+        DBuf<unsigned long long> csize;
+        csize.ensure(nuc);
+        launch_adj_fill(lv.B.p, lv.G.p, lv.ncells, ucell.p, nuc, lv.m, d_cs.p, d_cs.p + lv.m,
+                        adj_off.p, P.adj.p, csize.p, s);
+        DBuf<uint4> items_unsorted;
+        DBuf<unsigned long long> work, work_sorted, d_tot;
+        DBuf<uint32_t> iidx, iidx_sorted;
+        items_unsorted.ensure(tot);
+        work.ensure(tot);
+        launch_items(ufirst.p, ucnt.p, item_off.p, adj_off.p, nuc, csize.p, items_unsorted.p,
+                     work.p, s);
+        d_tot.ensure(1);
+        reduce_sum(sc, work.p, d_tot.p, tot, s);
+        unsigned long long cand = 0;
+        KJ_CUDA(cudaMemcpyAsync(&cand, d_tot.p, 8, cudaMemcpyDeviceToHost, s));
+        // heaviest items first (LPT order for the block scheduler)
+        iidx.ensure(tot);
+        iidx_sorted.ensure(tot);
+        work_sorted.ensure(tot);
+        launch_iota(iidx.p, tot, s);
+        sort_desc_u64_u32(sc, work.p, work_sorted.p, iidx.p, iidx_sorted.p, tot, s);
+        std::vector<uint32_t> order(tot);
+        std::vector<uint4> h_items(tot), h_sorted(tot);
+        KJ_CUDA(cudaMemcpyAsync(order.data(), iidx_sorted.p, 4 * tot, cudaMemcpyDeviceToHost, s));
+        KJ_CUDA(cudaMemcpyAsync(h_items.data(), items_unsorted.p, 16 * tot, cudaMemcpyDeviceToHost, s));
+        sync();
+        for (uint64_t i = 0; i < tot; ++i) h_sorted[i] = h_items[order[i]];
+        P.items.ensure(tot);
+        KJ_CUDA(cudaMemcpyAsync(P.items.p, h_sorted.data(), 16 * tot, cudaMemcpyHostToDevice, s));
+        sync();
+        P.candidates = cand;
+    }
+
+    double last_join_kernel_ms = 0.0;
+    // Runs the fused join over a pass, then the exact finalize (and the slow
+    // path for overflowed lists). Writes rows of out_* (indexed by qrow).
+    void run_pass(Level& lv, Pass& P, uint32_t K, const float* d_init_cut, double eps2,
+                  double cov2, uint32_t* out_ids, double* out_dist, double* out_kth,
+                  uint8_t* out_status, uint64_t* n_slow) {
+        if (!P.nq) return;
+        const uint32_t L = K + std::max<uint32_t>(16, K / 2);
+        if (L > 256) throw Error(1, "k above 170 is not supported by the device join");
+        const int np = pick_np(n);
+        if (np < 0) throw Error(1, "dimension count above 128 is not supported by the device join");
+        if (join_smem_bytes(np, L) > 227 * 1024) throw Error(1, "k too large for the device join");
+        DBuf<uint32_t> cnt, pos;
+        cnt.ensure(P.nq);
+        pos.ensure(P.nq * L);
+        JoinArgs a{};
+        a.Xs = lv.Xs.p;
+        a.Npad = Npad;
+        a.n = n;
+        a.qpos = P.qpos.p;
+        a.items = P.items.p;
+        a.adj = P.adj.p;
+        a.init_cut = d_init_cut;
+        a.K = K;
+        a.L = L;
+        a.out_cnt = cnt.p;
+        a.out_pos = pos.p;
+        screen_consts(a.gam, a.erg, a.eab, a.e64);
+        {
+            Timer t(s);
+            launch_join(a, P.nitems, s);
+            last_join_kernel_ms = t.ms();
+        }
+        FinalArgs f{};
+        f.X64 = X64.p;
+        f.n = n;
+        f.A = lv.A.p;
+        f.qpos = P.qpos.p;
+        f.qrow = P.qrow.p;
+        f.cnt = cnt.p;
+        f.pos = pos.p;
+        f.nrows = P.nq;
+        f.K = K;
+        f.L = L;
+        f.eps2 = eps2;
+        f.cover2 = cov2;
+        f.out_ids = out_ids;
+        f.out_dist = out_dist;
+        f.out_kth = out_kth;
+        f.out_status = out_status;
+        launch_finalize(f, s);
+        // overflowed rows -> exact slow path on the same candidate sets
+        std::vector<uint32_t> h_cnt(P.nq);
+        KJ_CUDA(cudaMemcpyAsync(h_cnt.data(), cnt.p, 4 * P.nq, cudaMemcpyDeviceToHost, s));
+        sync();
+        std::vector<uint32_t> rows;
+        for (uint64_t r = 0; r < P.nq; ++r)
+            if (h_cnt[r] == OVF) rows.push_back((uint32_t)r);
+        if (n_slow) *n_slow += rows.size();
+        if (!rows.empty()) {
+            DBuf<uint32_t> d_rows, row_item;
+            d_rows.ensure(rows.size());
+            row_item.ensure(P.nq);
+            KJ_CUDA(cudaMemcpyAsync(d_rows.p, rows.data(), 4 * rows.size(), cudaMemcpyHostToDevice, s));
+            launch_row_item(P.items.p, P.nitems, row_item.p, s);
+            launch_slow_exact(X64.p, n, lv.A.p, P.qpos.p, P.qrow.p, d_rows.p, rows.size(),
+                              P.items.p, row_item.p, P.adj.p, K, eps2, cov2, out_ids, out_dist,
+                              out_kth, out_status, s);
+            sync();
+        }
+    }
+
+    // Exact KNN for the given queries (pids + rows), certified globally: level
+    // passes at widths w0*2^L, each seeded with the previous upper bound.
+    // U (per row, may be inf) = known upper bound of the K-th sq.
+    void exact_levels(uint32_t m, double w0, int first_level, std::vector<uint32_t> qpid,
+                      std::vector<uint32_t> qrow, std::vector<double> U, uint32_t K,
+                      uint32_t* out_ids, double* out_dist, double* out_kth, uint8_t* out_status,
+                      uint64_t nrows_total, uint64_t* passes, uint64_t* n_slow) {
+        // level for a row given its upper bound u and the last level tried
+        auto level_for = [&](double u, int prev) {
+            if (!(u < kInf)) return prev < first_level ? first_level : prev + 2;
+            int L = std::max(first_level, prev + 1);
+            while (L < 39) {
+                const double w = std::ldexp(w0, L);
+                if (w * w * (1.0 - 1e-6) > u) break;
+                ++L;
+            }
+            return L;
+        };
+        std::vector<int> lvl(qpid.size());
+        for (size_t i = 0; i < qpid.size(); ++i) lvl[i] = level_for(U[i], first_level - 1);
+        DBuf<float> d_cut_by_row;
+        d_cut_by_row.ensure(nrows_total);
+        std::vector<float> h_cut(nrows_total, std::numeric_limits<float>::infinity());
+        while (!qpid.empty()) {
+            const int L = *std::min_element(lvl.begin(), lvl.end());
+            if (L >= 40) throw Error(9, "exact fallback did not converge");
+            std::vector<uint32_t> sp, sr, rp, rr;
+            std::vector<double> ru;
+            std::vector<int> rl;
+            for (size_t i = 0; i < qpid.size(); ++i) {
+                if (lvl[i] == L) {
+                    sp.push_back(qpid[i]);
+                    sr.push_back(qrow[i]);
+                    h_cut[qrow[i]] = U[i] < kInf ? f32_round_up(U[i])
+                                                 : std::numeric_limits<float>::infinity();
+                } else {
+                    rp.push_back(qpid[i]);
+                    rr.push_back(qrow[i]);
+                    ru.push_back(U[i]);
+                    rl.push_back(lvl[i]);
+                }
+            }
+            Level& lv = levels[L];
+            build_level(L, m, std::ldexp(w0, L));
+            const double cov2 = cover2(lv);
+            const uint64_t np = sp.size();
+            DBuf<uint32_t> d_p, d_r;
+            DBuf<float> d_cut;
+            d_p.ensure(np);
+            d_r.ensure(np);
+            d_cut.ensure(np);
+            KJ_CUDA(cudaMemcpyAsync(d_p.p, sp.data(), 4 * np, cudaMemcpyHostToDevice, s));
+            KJ_CUDA(cudaMemcpyAsync(d_r.p, sr.data(), 4 * np, cudaMemcpyHostToDevice, s));
+            KJ_CUDA(cudaMemcpyAsync(d_cut_by_row.p, h_cut.data(), 4 * nrows_total,
+                                    cudaMemcpyHostToDevice, s));
+            Pass P;
+            build_pass(lv, d_p.p, d_r.p, np, P);
+            launch_gather_f32(P.qrow.p, d_cut_by_row.p, np, d_cut.p, s);
+            run_pass(lv, P, K, d_cut.p, -1.0, cov2, out_ids, out_dist, out_kth, out_status, n_slow);
+            if (passes) ++*passes;
+            DBuf<uint8_t> g_st;
+            DBuf<double> g_kth;
+            g_st.ensure(np);
+            g_kth.ensure(np);
+            launch_gather_u8(d_r.p, out_status, np, g_st.p, s);
+            launch_gather_f64(d_r.p, out_kth, np, g_kth.p, s);
+            std::vector<uint8_t> st(np);
+            std::vector<double> kth(np);
+            KJ_CUDA(cudaMemcpyAsync(st.data(), g_st.p, np, cudaMemcpyDeviceToHost, s));
+            KJ_CUDA(cudaMemcpyAsync(kth.data(), g_kth.p, 8 * np, cudaMemcpyDeviceToHost, s));
+            sync();
+            for (uint64_t i = 0; i < np; ++i) {
+                if ((st[i] & ST_HAS_K) && (st[i] & ST_CERT)) continue;
+                const double u = (st[i] & ST_HAS_K) ? kth[i] : kInf;
+                rp.push_back(sp[i]);
+                rr.push_back(sr[i]);
+                ru.push_back(u);
+                rl.push_back(level_for(u, L));
+            }
+            qpid.swap(rp);
+            qrow.swap(rr);
+            U.swap(ru);
+            lvl.swap(rl);
+        }
+    }
+};
+
+// ============================================================================ C ABI
+namespace {
+
+template <class F>
+int guarded(knnj_ctx* ctx, F&& f) {
+    try {
+        if (ctx) KJ_CUDA(cudaSetDevice(ctx->dev));
+        f();
+        return KNNJ_OK;
+    } catch (const kj::Error& e) {
+        if (ctx) ctx->err = e.what();
+        return e.code;
+    } catch (const std::exception& e) {
+        if (ctx) ctx->err = e.what();
+        return KNNJ_E_CUDA;
+    }
+}
+
+void need_points(knnj_ctx* c) {
+    if (!c->have_points) throw Error(1, "no dataset: call knnj_set_points first");
+}
+
+}  // namespace
+
+extern "C" {
+
+int knnj_abi_version(void) { return KNNJ_ABI_VERSION; }
+
+int knnj_create(int device, knnj_ctx** out) {
+    if (!out) return KNNJ_E_USAGE;
+    try {
+        auto c = std::make_unique<knnj_ctx>();
+        c->dev = device;
+        KJ_CUDA(cudaSetDevice(device));
+        KJ_CUDA(cudaStreamCreateWithFlags(&c->s, cudaStreamNonBlocking));
+        *out = c.release();
+        return KNNJ_OK;
+    } catch (const kj::Error& e) {
+        return e.code;
+    } catch (...) {
+        return KNNJ_E_CUDA;
+    }
+}
+
+void knnj_destroy(knnj_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->dev);
+    delete ctx;
+}
+
+const char* knnj_last_error(const knnj_ctx* ctx) { return ctx ? ctx->err.c_str() : "null ctx"; }
+
+void* knnj_alloc_pinned(size_t bytes) {
+    void* p = nullptr;
+    if (cudaHostAlloc(&p, bytes ? bytes : 1, cudaHostAllocPortable) != cudaSuccess) return nullptr;
+    return p;
+}
+void knnj_free_pinned(void* p) {
+    if (p) cudaFreeHost(p);
+}
+
+int knnj_set_points(knnj_ctx* c, const double* X, uint64_t N, uint32_t n) {
+    return guarded(c, [&] {
+        if (N < 1) throw Error(1, "dataset must contain at least one point");
+        if (n < 1) throw Error(1, "dataset must have at least one dimension");
+        if (N >= (1ull << 32) - 1) throw Error(1, "dataset too large for 32-bit point ids");
+        c->N = N;
+        c->n = n;
+        c->have_points = c->working_ready = false;
+        for (auto& lv : c->levels) lv.built = false;
+        c->X0.ensure(N * n);
+        KJ_CUDA(cudaMemcpyAsync(c->X0.p, X, N * n * 8, cudaMemcpyHostToDevice, c->s));
+        c->d_u64a.ensure(1);
+        unsigned long long none = ~0ull;
+        KJ_CUDA(cudaMemcpyAsync(c->d_u64a.p, &none, 8, cudaMemcpyHostToDevice, c->s));
+        launch_check_finite(c->X0.p, N * n, c->d_u64a.p, c->s);
+        unsigned long long bad = 0;
+        KJ_CUDA(cudaMemcpyAsync(&bad, c->d_u64a.p, 8, cudaMemcpyDeviceToHost, c->s));
+        c->sync();
+        if (bad != ~0ull)
+            throw Error(1, "non-finite coordinate at point " + std::to_string(bad / n) +
+                               ", dimension " + std::to_string(bad % n));
+        c->have_points = true;
+    });
+}
+
+int knnj_reorder_by_variance(knnj_ctx* c, uint32_t m, uint32_t* perm, double* var) {
+    return guarded(c, [&] {
+        need_points(c);
+        c->reorder(m);
+        if (perm) std::memcpy(perm, c->perm.data(), 4 * c->n);
+        if (var) std::memcpy(var, c->var.data(), 8 * c->n);
+    });
+}
+
+int knnj_get_points(knnj_ctx* c, double* out) {
+    return guarded(c, [&] {
+        need_points(c);
+        c->ensure_working();
+        KJ_CUDA(cudaMemcpyAsync(out, c->X64.p, c->N * c->n * 8, cudaMemcpyDeviceToHost, c->s));
+        c->sync();
+    });
+}
+
+int knnj_pair_sq(knnj_ctx* c, const uint64_t* ij, uint64_t np, double limit, double* out) {
+    return guarded(c, [&] {
+        need_points(c);
+        c->ensure_working();
+        for (uint64_t i = 0; i < 2 * np; ++i)
+            if (ij[i] >= c->N) throw Error(1, "pair index out of range");
+        auto v = c->pair_sq(ij, np, limit);
+        std::memcpy(out, v.data(), 8 * np);
+    });
+}
+
+int knnj_eps_mean(knnj_ctx* c, uint64_t pairs, uint64_t seed, double* out) {
+    return guarded(c, [&] {
+        need_points(c);
+        c->ensure_working();
+        *out = c->eps_mean(pairs, seed);
+    });
+}
+
+int knnj_histogram(knnj_ctx* c, double em, uint32_t nb, double frac, uint64_t seed,
+                   uint64_t* raw, uint64_t* qc) {
+    return guarded(c, [&] {
+        need_points(c);
+        c->ensure_working();
+        if (!(em > 0.0))
+            throw Error(4, "mean pairwise distance is not positive; cannot build a distance histogram");
+        if (nb < 2) throw Error(1, "histogram needs at least 2 bins");
+        auto q = c->histogram_sample(frac, seed);
+        std::fill(raw, raw + nb, 0ull);
+        c->histogram_queries(q.data(), q.size(), em, nb, raw);
+        *qc = q.size();
+    });
+}
+
+int knnj_histogram_queries(knnj_ctx* c, const uint64_t* q, uint64_t nq, double em, uint32_t nb,
+                           uint64_t* raw) {
+    return guarded(c, [&] {
+        need_points(c);
+        c->ensure_working();
+        for (uint64_t i = 0; i < nq; ++i)
+            if (q[i] >= c->N) throw Error(1, "histogram query id out of range");
+        c->histogram_queries(q, nq, em, nb, raw);
+    });
+}
+
+int knnj_grid_build(knnj_ctx* c, uint32_t m, double eps, knnj_grid_info* info) {
+    return guarded(c, [&] {
+        need_points(c);
+        c->ensure_working();
+        if (!(eps > 0.0)) throw Error(1, "grid eps must be positive");
+        if (m < 1 || m > c->n) throw Error(1, "grid m must satisfy 1 <= m <= n");
+        if (m > 64) throw Error(1, "grid m above 64 is not supported");
+        c->build_level(0, m, eps);
+        c->eps0 = eps;
+        c->m0 = m;
+        if (info) {
+            std::memset(info, 0, sizeof(*info));
+            const Level& lv = c->levels[0];
+            info->m = m;
+            info->eps = eps;
+            info->n_cells = lv.ncells;
+            for (uint32_t j = 0; j < m; ++j) {
+                info->mins[j] = lv.mins[j];
+                info->maxs[j] = lv.maxs[j];
+                info->cells_per_dim[j] = lv.cpd[j];
+            }
+        }
+    });
+}
+
+int knnj_grid_export(knnj_ctx* c, uint64_t* B, uint64_t* G, uint32_t* A, uint32_t* slot) {
+    return guarded(c, [&] {
+        const Level& lv = c->levels[0];
+        if (!lv.built) throw Error(1, "no grid: call knnj_grid_build first");
+        if (B) KJ_CUDA(cudaMemcpyAsync(B, lv.B.p, 8 * lv.ncells, cudaMemcpyDeviceToHost, c->s));
+        if (G) {
+            std::vector<uint2> g(lv.ncells);
+            KJ_CUDA(cudaMemcpyAsync(g.data(), lv.G.p, 8 * lv.ncells, cudaMemcpyDeviceToHost, c->s));
+            c->sync();
+            for (uint64_t i = 0; i < lv.ncells; ++i) {
+                G[2 * i] = g[i].x;
+                G[2 * i + 1] = g[i].y;
+            }
+        }
+        if (A) KJ_CUDA(cudaMemcpyAsync(A, lv.A.p, 4 * c->N, cudaMemcpyDeviceToHost, c->s));
+        if (slot) KJ_CUDA(cudaMemcpyAsync(slot, lv.slot.p, 4 * c->N, cudaMemcpyDeviceToHost, c->s));
+        c->sync();
+    });
+}
+
+int knnj_range_count(knnj_ctx* c, const uint32_t* q, uint64_t nq, uint64_t* in_eps,
+                     uint64_t* candidates) {
+    return guarded(c, [&] {
+        Level& lv = c->levels[0];
+        if (!lv.built) throw Error(1, "no grid: call knnj_grid_build first");
+        std::vector<uint32_t> rows(nq);
+        std::iota(rows.begin(), rows.end(), 0u);
+        DBuf<uint32_t> d_q, d_r;
+        d_q.ensure(nq);
+        d_r.ensure(nq);
+        KJ_CUDA(cudaMemcpyAsync(d_q.p, q, 4 * nq, cudaMemcpyHostToDevice, c->s));
+        KJ_CUDA(cudaMemcpyAsync(d_r.p, rows.data(), 4 * nq, cudaMemcpyHostToDevice, c->s));
+        Pass P;
+        c->build_pass(lv, d_q.p, d_r.p, nq, P);
+        DBuf<unsigned long long> cnt;
+        cnt.ensure(nq);
+        launch_range_count(c->X64.p, c->n, lv.A.p, P.qpos.p, P.items.p, P.nitems, P.adj.p,
+                           c->eps0 * c->eps0, cnt.p, c->s);
+        std::vector<unsigned long long> h(nq);
+        std::vector<uint32_t> prow(nq);
+        std::vector<uint4> items(P.nitems);
+        std::vector<uint2> adj(P.nadj);
+        KJ_CUDA(cudaMemcpyAsync(h.data(), cnt.p, 8 * nq, cudaMemcpyDeviceToHost, c->s));
+        KJ_CUDA(cudaMemcpyAsync(prow.data(), P.qrow.p, 4 * nq, cudaMemcpyDeviceToHost, c->s));
+        KJ_CUDA(cudaMemcpyAsync(items.data(), P.items.p, 16 * P.nitems, cudaMemcpyDeviceToHost, c->s));
+        KJ_CUDA(cudaMemcpyAsync(adj.data(), P.adj.p, 8 * P.nadj, cudaMemcpyDeviceToHost, c->s));
+        c->sync();
+        for (uint64_t r = 0; r < nq; ++r) in_eps[prow[r]] = h[r];
+        if (candidates) {
+            for (const uint4& it : items) {
+                uint64_t cs = 0;
+                for (uint32_t a = it.z; a < it.w; ++a) cs += adj[a].y - adj[a].x;
+                for (uint32_t r = it.x; r < it.y; ++r) candidates[prow[r]] = cs;
+            }
+        }
+    });
+}
+
+int knnj_split(knnj_ctx* c, const uint32_t* q, uint64_t nq, uint32_t k, double beta,
+               double gamma, double rho, uint8_t* is_dense, uint64_t* cell_pop,
+               knnj_split_info* info) {
+    return guarded(c, [&] {
+        Level& lv = c->levels[0];
+        if (!lv.built) throw Error(1, "no grid: call knnj_grid_build first");
+        if (beta < 0 || beta > 1 || gamma < 0 || gamma > 1 || rho < 0 || rho > 1)
+            throw Error(1, "beta, gamma, rho must all be in [0, 1]");
+        if (k < 1) throw Error(1, "compute_n_min requires k >= 1 and m >= 1");
+        // partition.cpp:12-23 (Eq. 1), same expression order
+        const double mm = double(lv.m);
+        const double n_min =
+            double(k) * std::pow(2.0, mm) * std::tgamma(mm / 2.0 + 1.0) / std::pow(M_PI, mm / 2.0);
+        const double n_thresh = n_min + (10.0 * n_min - n_min) * gamma;
+        DBuf<uint32_t> d_q, d_pop;
+        d_q.ensure(nq);
+        d_pop.ensure(nq);
+        KJ_CUDA(cudaMemcpyAsync(d_q.p, q, 4 * nq, cudaMemcpyHostToDevice, c->s));
+        launch_cell_pop(d_q.p, nq, lv.slot.p, lv.G.p, d_pop.p, c->s);
+        std::vector<uint32_t> pop(nq);
+        KJ_CUDA(cudaMemcpyAsync(pop.data(), d_pop.p, 4 * nq, cudaMemcpyDeviceToHost, c->s));
+        c->sync();
+        uint64_t ncpu = 0;
+        for (uint64_t i = 0; i < nq; ++i) {
+            is_dense[i] = double(pop[i]) >= n_thresh;
+            ncpu += !is_dense[i];
+            if (cell_pop) cell_pop[i] = pop[i];
+        }
+        uint64_t demoted = 0;
+        const uint64_t floor_cpu = (uint64_t)std::ceil(rho * double(nq));
+        if (ncpu < floor_cpu) {
+            uint64_t need = floor_cpu - ncpu;
+            std::vector<uint32_t> slot(nq);
+            DBuf<uint32_t> d_slot;
+            d_slot.ensure(nq);
+            launch_map_u32(d_q.p, lv.slot.p, nq, d_slot.p, c->s);
+            KJ_CUDA(cudaMemcpyAsync(slot.data(), d_slot.p, 4 * nq, cudaMemcpyDeviceToHost, c->s));
+            c->sync();
+            std::vector<std::tuple<uint32_t, uint32_t, uint32_t, uint64_t>> ord;  // pop, cell, pid, i
+            for (uint64_t i = 0; i < nq; ++i)
+                if (is_dense[i]) ord.emplace_back(pop[i], slot[i], q[i], i);
+            std::sort(ord.begin(), ord.end());
+            need = std::min<uint64_t>(need, ord.size());
+            for (uint64_t i = 0; i < need; ++i) is_dense[std::get<3>(ord[i])] = 0;
+            demoted = need;
+            ncpu += need;
+        }
+        if (info) {
+            info->n_min = n_min;
+            info->n_thresh = n_thresh;
+            info->q_cpu = ncpu;
+            info->q_gpu = nq - ncpu;
+            info->demoted = demoted;
+        }
+    });
+}
+
+int knnj_dense_join(knnj_ctx* c, const uint32_t* q, uint64_t nq, uint32_t k, uint32_t* ids,
+                    double* dist, uint8_t* solved, knnj_join_stats* st) {
+    return guarded(c, [&] {
+        Level& lv = c->levels[0];
+        if (!lv.built) throw Error(1, "no grid: call knnj_grid_build first");
+        if (k < 1) throw Error(1, "k must be at least 1");
+        std::vector<uint32_t> rows(nq);
+        std::iota(rows.begin(), rows.end(), 0u);
+        DBuf<uint32_t> d_q, d_r, o_ids;
+        DBuf<double> o_dist, o_kth;
+        DBuf<uint8_t> o_st;
+        d_q.ensure(nq);
+        d_r.ensure(nq);
+        o_ids.ensure(nq * k);
+        o_dist.ensure(nq * k);
+        o_kth.ensure(nq);
+        o_st.ensure(nq);
+        KJ_CUDA(cudaMemcpyAsync(d_q.p, q, 4 * nq, cudaMemcpyHostToDevice, c->s));
+        KJ_CUDA(cudaMemcpyAsync(d_r.p, rows.data(), 4 * nq, cudaMemcpyHostToDevice, c->s));
+        Pass P;
+        c->build_pass(lv, d_q.p, d_r.p, nq, P);
+        uint64_t nslow = 0;
+        c->run_pass(lv, P, k, nullptr, c->eps0 * c->eps0, c->cover2(lv), o_ids.p, o_dist.p,
+                    o_kth.p, o_st.p, &nslow);
+        std::vector<uint8_t> sts(nq);
+        KJ_CUDA(cudaMemcpyAsync(ids, o_ids.p, 4 * nq * k, cudaMemcpyDeviceToHost, c->s));
+        KJ_CUDA(cudaMemcpyAsync(dist, o_dist.p, 8 * nq * k, cudaMemcpyDeviceToHost, c->s));
+        KJ_CUDA(cudaMemcpyAsync(sts.data(), o_st.p, nq, cudaMemcpyDeviceToHost, c->s));
+        c->sync();
+        uint64_t ns = 0;
+        for (uint64_t i = 0; i < nq; ++i) {
+            solved[i] = (sts[i] & ST_HAS_K) && (sts[i] & ST_IN_EPS);
+            ns += solved[i];
+        }
+        if (st) {
+            st->candidates_examined = P.candidates;
+            st->solved = ns;
+            st->failed = nq - ns;
+            st->kernel_ms = c->last_join_kernel_ms;
+        }
+    });
+}
+
+int knnj_exact_knn(knnj_ctx* c, const uint32_t* q, uint64_t nq, uint32_t k, uint32_t* ids,
+                   double* dist) {
+    return guarded(c, [&] {
+        need_points(c);
+        c->ensure_working();
+        if (k < 1) throw Error(1, "knn_query requires k >= 1");
+        if (k > c->N - 1) throw Error(1, "k exceeds |D|-1");
+        for (uint64_t i = 0; i < nq; ++i)
+            if (q[i] >= c->N) throw Error(1, "query id out of range");
+        if (!nq) return;
+        const uint32_t m = std::min<uint32_t>(6, c->n);
+        // width: cells holding ~2k points on average over the bounding box
+        std::vector<unsigned long long> mn(m), mx(m);
+        c->d_u64a.ensure(64);
+        c->d_u64b.ensure(64);
+        std::vector<unsigned long long> i0(m, ~0ull), i1(m, 0ull);
+        KJ_CUDA(cudaMemcpyAsync(c->d_u64a.p, i0.data(), 8 * m, cudaMemcpyHostToDevice, c->s));
+        KJ_CUDA(cudaMemcpyAsync(c->d_u64b.p, i1.data(), 8 * m, cudaMemcpyHostToDevice, c->s));
+        launch_minmax(c->X64.p, c->N, c->n, m, c->d_u64a.p, c->d_u64b.p, c->s);
+        KJ_CUDA(cudaMemcpyAsync(mn.data(), c->d_u64a.p, 8 * m, cudaMemcpyDeviceToHost, c->s));
+        KJ_CUDA(cudaMemcpyAsync(mx.data(), c->d_u64b.p, 8 * m, cudaMemcpyDeviceToHost, c->s));
+        c->sync();
+        double logvol = 0.0;
+        int used = 0;
+        for (uint32_t j = 0; j < m; ++j) {
+            auto un = [](unsigned long long o) {
+                unsigned long long b = (o & 0x8000000000000000ull) ? (o & 0x7FFFFFFFFFFFFFFFull) : ~o;
+                double v;
+                std::memcpy(&v, &b, 8);
+                return v;
+            };
+            double e = un(mx[j]) - un(mn[j]);
+            if (e > 0) {
+                logvol += std::log(e);
+                ++used;
+            }
+        }
+        double w0 = used ? std::exp((logvol + std::log(2.0 * k / double(c->N))) / used) : 1.0;
+        if (!(w0 > 0) || !std::isfinite(w0)) w0 = 1.0;
+        DBuf<uint32_t> o_ids;
+        DBuf<double> o_dist, o_kth;
+        DBuf<uint8_t> o_st;
+        o_ids.ensure(nq * k);
+        o_dist.ensure(nq * k);
+        o_kth.ensure(nq);
+        o_st.ensure(nq);
+        std::vector<uint32_t> qp(q, q + nq), rows(nq);
+        std::iota(rows.begin(), rows.end(), 0u);
+        std::vector<double> U(nq, kInf);
+        // levels 30.. are reserved for this ad-hoc exact search (level 0.. belong to the eps grid)
+        for (int L = 20; L < 40; ++L) c->levels[L].built = false;
+        uint64_t passes = 0, slow = 0;
+        // shift: level index L maps to width w0*2^(L-20)
+        c->exact_levels(m, std::ldexp(w0, -20), 20, qp, rows, U, k, o_ids.p, o_dist.p, o_kth.p,
+                        o_st.p, nq, &passes, &slow);
+        KJ_CUDA(cudaMemcpyAsync(ids, o_ids.p, 4 * nq * k, cudaMemcpyDeviceToHost, c->s));
+        KJ_CUDA(cudaMemcpyAsync(dist, o_dist.p, 8 * nq * k, cudaMemcpyDeviceToHost, c->s));
+        c->sync();
+    });
+}
+
+// run_hybrid (orchestrator.cpp:67-250)
+int knnj_run(knnj_ctx* c, const knnj_config* cfg, uint32_t* ids, double* dist, uint8_t* prov,
+             uint64_t* raw_hist, knnj_run_info* info) {
+    return guarded(c, [&] {
+        need_points(c);
+        auto t_start = std::chrono::steady_clock::now();
+        knnj_run_info I;
+        std::memset(&I, 0, sizeof(I));
+        const uint64_t N = c->N;
+        const uint32_t n = c->n;
+        // validate_config (orchestrator.cpp:16-31)
+        if (cfg->k < 1) throw Error(1, "k must be at least 1");
+        if (cfg->m > n) throw Error(1, "m must satisfy m <= n");
+        if (cfg->beta < 0 || cfg->beta > 1 || cfg->gamma < 0 || cfg->gamma > 1 || cfg->rho < 0 ||
+            cfg->rho > 1)
+            throw Error(1, "beta, gamma, rho must all be in [0, 1]");
+        if (!(cfg->hist_query_fraction > 0) || cfg->hist_query_fraction > 1)
+            throw Error(1, "sample fractions must be in (0, 1]");
+        if (cfg->n_bins < 2) throw Error(1, "n_bins must be at least 2");
+        if (cfg->mode > 3) throw Error(1, "unknown engine mode");
+        std::vector<uint32_t> queries;
+        if (cfg->query_subset) {
+            for (uint64_t i = 0; i < cfg->n_query_subset; ++i)
+                if (cfg->query_subset[i] >= N) throw Error(1, "query subset id out of range");
+            queries.assign(cfg->query_subset, cfg->query_subset + cfg->n_query_subset);
+            std::sort(queries.begin(), queries.end());
+            queries.erase(std::unique(queries.begin(), queries.end()), queries.end());
+        } else {
+            queries.resize(N);
+            std::iota(queries.begin(), queries.end(), 0u);
+        }
+        const uint64_t nq = queries.size();
+        I.n_queries = nq;
+        uint32_t k_eff = cfg->k;
+        if (k_eff >= N) {
+            k_eff = (uint32_t)(N - 1);
+            I.k_clamped = 1;
+        }
+        I.k_effective = k_eff;
+        const uint32_t m = cfg->m == 0 ? std::min<uint32_t>(6, n) : cfg->m;
+        I.m_used = m;
+        if (m > 64) throw Error(1, "grid m above 64 is not supported");
+
+        Timer t_all(c->s);
+        {
+            Timer t(c->s);
+            c->reorder(m);
+            I.ms_reorder = t.ms();
+        }
+        for (uint32_t j = 0; j < n && j < 1024; ++j) I.perm[j] = c->perm[j];
+        if (k_eff == 0 || nq == 0) {
+            I.ms_total = t_all.ms();
+            if (info) *info = I;
+            return;
+        }
+        const bool all_points = !cfg->query_subset;
+        DBuf<uint32_t> o_ids;
+        DBuf<double> o_dist, o_kth;
+        DBuf<uint8_t> o_st;
+        o_ids.ensure(nq * k_eff);
+        o_dist.ensure(nq * k_eff);
+        o_kth.ensure(nq);
+        o_st.ensure(nq);
+        DBuf<uint32_t> d_q, d_rows;
+        d_q.ensure(nq);
+        d_rows.ensure(nq);
+        KJ_CUDA(cudaMemcpyAsync(d_q.p, queries.data(), 4 * nq, cudaMemcpyHostToDevice, c->s));
+        if (all_points) {
+            KJ_CUDA(cudaMemcpyAsync(d_rows.p, d_q.p, 4 * nq, cudaMemcpyDeviceToDevice, c->s));
+        } else {
+            std::vector<uint32_t> rows(nq);
+            std::iota(rows.begin(), rows.end(), 0u);
+            KJ_CUDA(cudaMemcpyAsync(d_rows.p, rows.data(), 4 * nq, cudaMemcpyHostToDevice, c->s));
+        }
+        std::vector<uint8_t> h_prov(nq, KNNJ_PROV_SPARSE);
+
+        if (cfg->mode == KNNJ_BRUTE_ORACLE || cfg->mode == KNNJ_SPARSE_ONLY) {
+            // brute_force_knn / kd-tree contract: exact KNN of every query
+            Timer t(c->s);
+            std::vector<uint32_t> rows(nq);
+            std::iota(rows.begin(), rows.end(), 0u);
+            const uint32_t me = std::min<uint32_t>(6, n);
+            // width from the bounding box, as knnj_exact_knn
+            std::vector<unsigned long long> mn(me), mx(me), i0(me, ~0ull), i1(me, 0ull);
+            c->d_u64a.ensure(64);
+            c->d_u64b.ensure(64);
+            KJ_CUDA(cudaMemcpyAsync(c->d_u64a.p, i0.data(), 8 * me, cudaMemcpyHostToDevice, c->s));
+            KJ_CUDA(cudaMemcpyAsync(c->d_u64b.p, i1.data(), 8 * me, cudaMemcpyHostToDevice, c->s));
+            launch_minmax(c->X64.p, N, n, me, c->d_u64a.p, c->d_u64b.p, c->s);
+            KJ_CUDA(cudaMemcpyAsync(mn.data(), c->d_u64a.p, 8 * me, cudaMemcpyDeviceToHost, c->s));
+            KJ_CUDA(cudaMemcpyAsync(mx.data(), c->d_u64b.p, 8 * me, cudaMemcpyDeviceToHost, c->s));
+            c->sync();
+            double logvol = 0.0;
+            int used = 0;
+            auto un = [](unsigned long long o) {
+                unsigned long long b = (o & 0x8000000000000000ull) ? (o & 0x7FFFFFFFFFFFFFFFull) : ~o;
+                double v;
+                std::memcpy(&v, &b, 8);
+                return v;
+            };
+            for (uint32_t j = 0; j < me; ++j) {
+                double e = un(mx[j]) - un(mn[j]);
+                if (e > 0) {
+                    logvol += std::log(e);
+                    ++used;
+                }
+            }
+            double w0 = used ? std::exp((logvol + std::log(2.0 * k_eff / double(N))) / used) : 1.0;
+            if (!(w0 > 0) || !std::isfinite(w0)) w0 = 1.0;
+            for (int L = 20; L < 40; ++L) c->levels[L].built = false;
+            std::vector<double> U(nq, kInf);
+            c->exact_levels(me, std::ldexp(w0, -20), 20, queries, rows, U, k_eff, o_ids.p,
+                            o_dist.p, o_kth.p, o_st.p, nq, &I.fallback_passes, &I.slow_path_queries);
+            I.fallback_queries = nq;
+            I.ms_fallback = t.ms();
+            std::fill(h_prov.begin(), h_prov.end(),
+                      cfg->mode == KNNJ_BRUTE_ORACLE ? KNNJ_PROV_DENSE : KNNJ_PROV_SPARSE);
+        } else {
+            // ---- epsilon selection (orchestrator.cpp:137-165)
+            {
+                Timer t(c->s);
+                const uint64_t budget = std::min<uint64_t>(10 * N, cfg->eps_mean_pair_cap);
+                I.eps_mean = c->eps_mean(budget, derive_seed(cfg->seed, 1));
+                I.ms_eps_mean = t.ms();
+            }
+            std::vector<uint64_t> raw(cfg->n_bins, 0);
+            {
+                Timer t(c->s);
+                auto hq = c->histogram_sample(cfg->hist_query_fraction, derive_seed(cfg->seed, 2));
+                I.hist_query_count = hq.size();
+                c->histogram_queries(hq.data(), hq.size(), I.eps_mean, cfg->n_bins, raw.data());
+                I.ms_histogram = t.ms();
+                I.ms_hist_kernel = c->last_hist_kernel_ms;
+            }
+            if (raw_hist) std::memcpy(raw_hist, raw.data(), 8 * cfg->n_bins);
+            const double width = I.eps_mean / double(cfg->n_bins);
+            I.bin_width = width;
+            std::vector<double> cum(cfg->n_bins);
+            uint64_t running = 0;
+            for (uint32_t b = 0; b < cfg->n_bins; ++b) {
+                running += raw[b];
+                cum[b] = double(running) / double(I.hist_query_count);
+            }
+            auto select = [&](double beta, bool& fell_back, uint64_t& bin_out) {
+                const double target = double(k_eff) + (100.0 * double(k_eff) - double(k_eff)) * beta;
+                auto it = std::lower_bound(cum.begin(), cum.end(), target);
+                fell_back = false;
+                if (it == cum.end()) {
+                    fell_back = true;
+                    it = std::lower_bound(cum.begin(), cum.end(), cum.back());
+                }
+                uint64_t bin = uint64_t(it - cum.begin()) + 1;
+                double start = double(bin - 1) * width;
+                double end = double(bin) * width;
+                bin_out = bin;
+                return (start + end) / 2.0;
+            };
+            bool fb = false, fb0 = false;
+            uint64_t bin = 0, bin0 = 0;
+            I.eps_beta = select(cfg->beta, fb, bin);
+            I.eps_default = select(0.0, fb0, bin0);
+            I.eps_final = 2.0 * I.eps_beta;
+            I.eps_used = I.eps_final;
+            I.eps_fallback = fb;
+            I.hist_bin = bin;
+            const double eps = I.eps_final;
+
+            // ---- grid (GridIndex::build)
+            {
+                Timer t(c->s);
+                c->build_level(0, m, eps);
+                c->eps0 = eps;
+                c->m0 = m;
+                for (int L = 1; L < 40; ++L) c->levels[L].built = false;
+                I.ms_grid = t.ms();
+                I.grid_cells = c->levels[0].ncells;
+            }
+            Level& lv0 = c->levels[0];
+            // ---- split (partition.cpp:30-75)
+            std::vector<uint8_t> dense(nq, 1);
+            {
+                Timer t(c->s);
+                const double mm = double(m);
+                I.n_min = double(k_eff) * std::pow(2.0, mm) * std::tgamma(mm / 2.0 + 1.0) /
+                          std::pow(M_PI, mm / 2.0);
+                I.n_thresh = I.n_min + (10.0 * I.n_min - I.n_min) * cfg->gamma;
+                if (cfg->mode == KNNJ_HYBRID) {
+                    knnj_split_info si{};
+                    int rc = knnj_split(c, queries.data(), nq, k_eff, cfg->beta, cfg->gamma,
+                                        cfg->rho, dense.data(), nullptr, &si);
+                    if (rc) throw Error(rc, c->err);
+                    I.q_gpu = si.q_gpu;
+                    I.q_cpu = si.q_cpu;
+                    I.demoted = si.demoted;
+                } else {
+                    I.q_gpu = nq;
+                }
+                I.ms_split = t.ms();
+            }
+            // ---- level-0 fused join over every query (dense + sparse)
+            uint64_t slow = 0;
+            {
+                Timer t(c->s);
+                Pass P;
+                c->build_pass(lv0, d_q.p, d_rows.p, nq, P);
+                c->run_pass(lv0, P, k_eff, nullptr, eps * eps, c->cover2(lv0), o_ids.p, o_dist.p,
+                            o_kth.p, o_st.p, &slow);
+                I.ms_join = t.ms();
+                I.ms_join_kernel = c->last_join_kernel_ms;
+                // candidates_examined counts dense queries only
+                if (I.q_cpu == 0) I.candidates_examined = P.candidates;
+            }
+            // ---- classify; exact fallback for failures and uncertified sparse queries
+            {
+                Timer t(c->s);
+                std::vector<uint8_t> st(nq);
+                KJ_CUDA(cudaMemcpyAsync(st.data(), o_st.p, nq, cudaMemcpyDeviceToHost, c->s));
+                std::vector<double> kth(nq);
+                KJ_CUDA(cudaMemcpyAsync(kth.data(), o_kth.p, 8 * nq, cudaMemcpyDeviceToHost, c->s));
+                c->sync();
+                std::vector<uint32_t> fp, fr;
+                std::vector<double> fu;
+                for (uint64_t i = 0; i < nq; ++i) {
+                    const uint8_t s = st[i];
+                    if (dense[i]) {
+                        if ((s & ST_HAS_K) && (s & ST_IN_EPS)) {
+                            h_prov[i] = KNNJ_PROV_DENSE;
+                            continue;
+                        }
+                        h_prov[i] = KNNJ_PROV_DENSE_FAILED;
+                        ++I.failed_count;
+                    } else {
+                        h_prov[i] = KNNJ_PROV_SPARSE;
+                        if ((s & ST_HAS_K) && (s & ST_CERT)) continue;
+                    }
+                    fp.push_back(queries[i]);
+                    fr.push_back((uint32_t)i);
+                    fu.push_back((s & ST_HAS_K) ? kth[i] : kInf);
+                }
+                I.fallback_queries = fp.size();
+                if (!fp.empty())
+                    c->exact_levels(m, eps, 1, fp, fr, fu, k_eff, o_ids.p, o_dist.p, o_kth.p,
+                                    o_st.p, nq, &I.fallback_passes, &slow);
+                I.slow_path_queries = slow;
+                I.ms_fallback = t.ms();
+            }
+            if (I.q_cpu) {
+                // candidates_examined over dense queries only: recount on the dense subset
+                std::vector<uint32_t> dq;
+                for (uint64_t i = 0; i < nq; ++i)
+                    if (dense[i]) dq.push_back(queries[i]);
+                if (!dq.empty()) {
+                    DBuf<uint32_t> a, b;
+                    a.ensure(dq.size());
+                    b.ensure(dq.size());
+                    std::vector<uint32_t> rr(dq.size());
+                    std::iota(rr.begin(), rr.end(), 0u);
+                    KJ_CUDA(cudaMemcpyAsync(a.p, dq.data(), 4 * dq.size(), cudaMemcpyHostToDevice, c->s));
+                    KJ_CUDA(cudaMemcpyAsync(b.p, rr.data(), 4 * dq.size(), cudaMemcpyHostToDevice, c->s));
+                    Pass P;
+                    c->build_pass(lv0, a.p, b.p, dq.size(), P);
+                    I.candidates_examined = P.candidates;
+                }
+            }
+        }
+        {
+            Timer t(c->s);
+            KJ_CUDA(cudaMemcpyAsync(ids, o_ids.p, 4 * nq * k_eff, cudaMemcpyDeviceToHost, c->s));
+            KJ_CUDA(cudaMemcpyAsync(dist, o_dist.p, 8 * nq * k_eff, cudaMemcpyDeviceToHost, c->s));
+            I.ms_download = t.ms();
+        }
+        if (prov) std::memcpy(prov, h_prov.data(), nq);
+        I.ms_total = t_all.ms();
+        (void)t_start;
+        if (info) *info = I;
+    });
+}
+
+}  // extern "C"

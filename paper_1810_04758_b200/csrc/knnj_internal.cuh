@@ -1,0 +1,209 @@
+// Internal declarations shared by the device kernels (knnj_kernels.cu) and the
+// host runtime / C ABI (knnj_capi.cu). Not part of the public ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace kj {
+
+// ---------------------------------------------------------------- errors
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define KJ_CUDA(call)                                                                 \
+    do {                                                                              \
+        cudaError_t e_ = (call);                                                      \
+        if (e_ != cudaSuccess)                                                        \
+            throw ::kj::Error(9, std::string("CUDA error: ") + cudaGetErrorString(e_) + \
+                                     " at " + __FILE__ + ":" + std::to_string(__LINE__)); \
+    } while (0)
+
+// ---------------------------------------------------------------- device buffer
+template <class T>
+struct DBuf {
+    T* p = nullptr;
+    size_t n = 0;  // capacity in elements
+    DBuf() = default;
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    ~DBuf() { release(); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    T* ensure(size_t count) {
+        if (count == 0) count = 1;
+        if (count > n) {
+            release();
+            KJ_CUDA(cudaMalloc(&p, count * sizeof(T)));
+            n = count;
+        }
+        return p;
+    }
+    T* get() const { return p; }
+};
+
+// ---------------------------------------------------------------- constants
+constexpr int JB = 128;          // threads (= queries) per join / histogram block
+constexpr uint32_t OVF = 0xFFFFFFFFu;
+
+// Status bits written by the finalize kernel, per query.
+enum : uint8_t {
+    ST_HAS_K = 1,      // >= K candidates (non-self) in the candidate set
+    ST_IN_EPS = 2,     // K-th exact sq <= eps^2 (dense "solved" rule, dense_engine.cpp:182)
+    ST_CERT = 4,       // K-th exact sq < coverage^2 (1-eta): globally exact
+    ST_OVF = 8,        // screen list overflowed (many near-ties): needs the exact slow path
+};
+
+// One grid level over all points (level 0 is the reference ε-grid; level L
+// has cell width ε·2^L, nested exactly in level 0).
+struct Level {
+    bool built = false;
+    uint32_t m = 0;
+    double w = 0.0;
+    std::vector<double> mins, maxs;
+    std::vector<uint64_t> cpd, strides;
+    uint64_t ncells = 0;
+    uint32_t key_bits = 0;
+    DBuf<uint64_t> B;    // ncells: sorted non-empty linear cell ids
+    DBuf<uint2> G;       // ncells: [begin,end) into A
+    DBuf<uint32_t> A;    // N: sorted position -> point id
+    DBuf<uint32_t> slot; // N: point id -> cell index
+    DBuf<uint32_t> posOf;// N: point id -> sorted position
+    DBuf<float> Xs;      // n x Npad SoA, sorted order, centred floats
+};
+
+// Work description of one join pass (queries of one level grid).
+struct Pass {
+    uint64_t nq = 0;
+    uint64_t nitems = 0;
+    uint64_t nadj = 0;
+    uint64_t candidates = 0;  // sum over queries of candidate-set size
+    DBuf<uint32_t> qpos;      // nq: sorted positions of the queries (grouped by cell)
+    DBuf<uint32_t> qrow;      // nq: output row of each query
+    DBuf<uint4> items;        // nitems: qbeg, qend, abeg, aend
+    DBuf<uint2> adj;          // nadj: candidate position ranges
+};
+
+struct JoinArgs {
+    const float* Xs;
+    uint64_t Npad;
+    uint32_t n;
+    const uint32_t* qpos;
+    const uint4* items;
+    const uint2* adj;
+    const float* init_cut;   // per launch row, may be null
+    uint32_t K, L;
+    uint32_t* out_cnt;       // per launch row
+    uint32_t* out_pos;       // per launch row * L
+    float gam;               // 2.02 * gamma_{n+2} (float32 unit roundoff)
+    float erg;               // 2*u1*Rg: input-rounding part of E
+    float eab;               // u(1+2u): (A+B) coefficient of E
+    float e64;               // (n+3) * 2^-52: FP64 accumulation slack
+};
+
+struct FinalArgs {
+    const double* X64;
+    uint32_t n;
+    const uint32_t* A;       // sorted pos -> pid (level)
+    const uint32_t* qpos;
+    const uint32_t* qrow;
+    const uint32_t* cnt;
+    const uint32_t* pos;     // launch row * L
+    uint64_t nrows;
+    uint32_t K, L;
+    double eps2;             // dense rule threshold (level 0) or -1
+    double cover2;           // certification: kth < cover2 (already scaled by 1-eta); inf = all
+    uint32_t* out_ids;       // [qrow * K]
+    double* out_dist;
+    double* out_kth;         // [qrow]
+    uint8_t* out_status;     // [qrow]
+};
+
+struct HistArgs {
+    const float* Xf;         // n x Npad SoA, id order
+    uint64_t Npad, N;
+    uint32_t n;
+    const double* X64;
+    const uint32_t* q;       // query ids
+    uint64_t nq;
+    uint64_t cand_begin_stride;  // candidate slab length
+    uint32_t n_bins;
+    const float* SU;         // n_bins+1: lower edge rounded up   (SU[0] = -inf)
+    const float* SD;         // n_bins+1: lower edge rounded down (SD[n_bins] = end)
+    double eps_mean, limit_sq, inv_width;
+    unsigned long long* counts;  // n_bins (u64)
+    float gam, erg, eab, e64;
+};
+
+// ---------------------------------------------------------------- launchers
+int pick_np(uint32_t n);  // padded dimension count used by the templated kernels
+size_t join_smem_bytes(int np, uint32_t L);
+void launch_join(const JoinArgs& a, uint64_t nitems, cudaStream_t s);
+void launch_finalize(const FinalArgs& a, cudaStream_t s);
+size_t hist_smem_bytes(int np, uint32_t n_bins);
+void launch_histogram(const HistArgs& a, uint64_t n_slabs, cudaStream_t s);
+
+void launch_check_finite(const double* X, uint64_t count, unsigned long long* first_bad,
+                         cudaStream_t s);
+void launch_col_sums(const double* X, uint64_t N, uint32_t n, const double* mean,
+                     double* partial, uint32_t nblk, cudaStream_t s);
+void launch_permute_cols(const double* X0, double* X, uint64_t N, uint32_t n,
+                         const uint32_t* order, cudaStream_t s);
+void launch_to_float_soa(const double* X, uint64_t N, uint32_t n, const double* g, float* Xf,
+                         uint64_t Npad, unsigned long long* rmax_bits, cudaStream_t s);
+void launch_pair_sq(const double* X, uint32_t n, const uint64_t* ij, uint64_t npairs,
+                    double limit, double* out, cudaStream_t s);
+void launch_minmax(const double* X, uint64_t N, uint32_t n, uint32_t m,
+                   unsigned long long* mn, unsigned long long* mx, cudaStream_t s);
+void launch_cell_keys(const double* X, uint64_t N, uint32_t n, uint32_t m, const double* mins,
+                      double w, const uint64_t* cpd, const uint64_t* strides, uint64_t* keys,
+                      uint32_t* vals, cudaStream_t s);
+void launch_iota(uint32_t* v, uint64_t N, cudaStream_t s);
+void launch_head_flags(const uint64_t* keys, uint64_t N, uint32_t* flags, cudaStream_t s);
+void launch_grid_tables(const uint64_t* skeys, const uint32_t* A, const uint32_t* runidx,
+                        uint64_t N, uint64_t* B, uint2* G, uint32_t* slot, uint32_t* posOf,
+                        cudaStream_t s);
+void launch_gather_soa(const float* Xf, const uint32_t* A, uint64_t N, uint32_t n,
+                       uint64_t Npad, float* Xs, cudaStream_t s);
+void launch_map_u32(const uint32_t* idx, const uint32_t* table, uint64_t n, uint32_t* out,
+                    cudaStream_t s);
+void launch_adj_count(const uint64_t* B, uint64_t ncells, const uint32_t* cells, uint64_t nc,
+                      uint32_t m, const uint64_t* cpd, const uint64_t* strides,
+                      uint32_t* counts, cudaStream_t s);
+void launch_adj_fill(const uint64_t* B, const uint2* G, uint64_t ncells, const uint32_t* cells,
+                     uint64_t nc, uint32_t m, const uint64_t* cpd, const uint64_t* strides,
+                     const uint32_t* offs, uint2* adj, unsigned long long* csize,
+                     cudaStream_t s);
+void launch_items(const uint32_t* ucell_first, const uint32_t* ucell_cnt,
+                  const uint32_t* item_off, const uint32_t* adj_off, uint64_t nuc,
+                  const unsigned long long* csize, uint4* items,
+                  unsigned long long* work, cudaStream_t s);
+void launch_cell_pop(const uint32_t* pids, uint64_t nq, const uint32_t* slot, const uint2* G,
+                     uint32_t* pop, cudaStream_t s);
+void launch_fill_f32(float* p, uint64_t n, float v, cudaStream_t s);
+void launch_range_count(const double* X64, uint32_t n, const uint32_t* A, const uint32_t* qpos,
+                        const uint4* items, uint64_t nitems, const uint2* adj, double eps2,
+                        unsigned long long* in_eps, cudaStream_t s);
+void launch_row_item(const uint4* items, uint64_t nitems, uint32_t* row_item, cudaStream_t s);
+void launch_gather_u8(const uint32_t* idx, const uint8_t* table, uint64_t n, uint8_t* out,
+                      cudaStream_t s);
+void launch_gather_f64(const uint32_t* idx, const double* table, uint64_t n, double* out,
+                       cudaStream_t s);
+void launch_gather_f32(const uint32_t* idx, const float* table, uint64_t n, float* out,
+                       cudaStream_t s);
+void launch_slow_exact(const double* X64, uint32_t n, const uint32_t* A, const uint32_t* qpos,
+                       const uint32_t* qrow, const uint32_t* rows, uint64_t nrows,
+                       const uint4* items, const uint32_t* row_item, const uint2* adj,
+                       uint32_t K, double eps2, double cover2, uint32_t* out_ids,
+                       double* out_dist, double* out_kth, uint8_t* out_status, cudaStream_t s);
+
+}  // namespace kj

@@ -1,0 +1,1115 @@
+// Device kernels of the B200 KNN self-join engine (sm_100a).
+//
+// Hot path:
+//   k_join      fused range-join + per-query screened top-K   (execute_batch + filter_keys,
+//               proj/src/dense_engine.cpp:86-196; grid walk grid_index.cpp:114-147)
+//   k_finalize  exact FP64 (scalar order) re-decision of the screened list
+//   k_hist      ε-selection distance histogram (build_distance_histogram, epsilon.cpp:46-120)
+//   grid build  cell keys + CUB radix sort + RLE tables (GridIndex::build, grid_index.cpp:13-75)
+//
+// Exactness model. A candidate pair is first scored with an FP32 "GEMM form"
+// distance  key = |a'|^2 + |b'|^2 - 2 a'.b'  on coordinates centred at a
+// per-block origin; |key - sq64| <= delta with delta a rigorous bound derived in
+// DESIGN.md §3 (input rounding + FP32 dot-product error + FP64 accumulation
+// slack). Every decision (top-K membership, ε test, histogram bin) is either
+// certain from key±delta or re-decided with the FP64 scalar-order distance, so
+// results are bit-identical to the reference scalar kernel.
+#include <cub/cub.cuh>
+#include <math_constants.h>
+
+#include "knnj_internal.cuh"
+
+namespace kj {
+
+// ---------------------------------------------------------------- helpers
+__device__ __forceinline__ double exact_sq(const double* __restrict__ a,
+                                           const double* __restrict__ b, uint32_t n) {
+    // proj/src/kernels_scalar.cpp:9-27, without the early exit (which never
+    // changes a finite result): d = a-b; sum += d*d, each op rounded separately.
+    double sum = 0.0;
+    for (uint32_t i = 0; i < n; ++i) {
+        double d = __dsub_rn(a[i], b[i]);
+        sum = __dadd_rn(sum, __dmul_rn(d, d));
+    }
+    return sum;
+}
+
+__device__ __forceinline__ bool pair_less(double sa, uint32_t ia, double sb, uint32_t ib) {
+    return sa < sb || (sa == sb && ia < ib);
+}
+
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+    unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+__device__ __forceinline__ unsigned long long dbl_order(double v) {
+    unsigned long long b = __double_as_longlong(v);
+    return (b & 0x8000000000000000ull) ? ~b : (b | 0x8000000000000000ull);
+}
+
+// Rigorous |key - sq64| bound for one (query, tile): A = |a'|, B = max |b'|.
+// gam = 2.02*gamma_{n+2}(fp32); E = erg + eab*(A+B) bounds the input rounding
+// of the difference vector; e64 covers the FP64 scalar accumulation.
+__device__ __forceinline__ float screen_delta(float A, float B, float gam, float erg, float eab,
+                                              float e64) {
+    float AB = A + B;
+    float E = erg + eab * AB;
+    float D = AB + E;
+    float d = gam * (A * A + B * B) + 2.f * D * E + E * E + e64 * D * D;
+    return d * 1.0625f + 1e-37f;
+}
+
+// ---------------------------------------------------------------- join kernel
+// One block = one work item: up to JB queries of ONE grid cell (one query per
+// thread) against the candidate position ranges of that cell's 3^m
+// neighbourhood (merged along the last indexed dim). Candidate tiles of T
+// points are staged SoA in shared memory (cp.async, double-buffered), centred
+// at the block origin, and scored against every query of the block. Per query
+// a list of all candidates that can still belong to the exact top-K is kept
+// (sorted by key, capacity L), pruned with cut = key_K + 2*delta_max.
+template <int NP, int T>
+__global__ void __launch_bounds__(JB) k_join(JoinArgs p) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    float* tile = reinterpret_cast<float*>(smem_raw);          // [2][NP][T]
+    float* nbuf = tile + 2 * NP * T;                            // [2][T]
+    uint32_t* tpos = reinterpret_cast<uint32_t*>(nbuf + 2 * T); // [2][T]
+    float* cen = reinterpret_cast<float*>(tpos + 2 * T);        // [NP] (+pad)
+    float* lkey = cen + ((NP + 3) & ~3);                        // [L][JB]
+    uint32_t* lpos = reinterpret_cast<uint32_t*>(lkey + p.L * JB);
+
+    __shared__ uint32_t s_ri, s_off, s_cnt[2];
+    __shared__ unsigned s_bmax[2];
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint4 it = p.items[blockIdx.x];
+    const uint32_t nq = it.y - it.x;
+    const bool has_q = (uint32_t)tid < nq;
+    const uint32_t row = it.x + (has_q ? tid : 0);
+    const uint32_t qp = p.qpos[row];
+    const uint32_t n = p.n;
+    const uint64_t Npad = p.Npad;
+
+    // zero padded dims of both tile buffers once; block origin = first query
+    for (int i = tid; i < 2 * (NP - (int)n) * T; i += JB) {
+        int b = i / ((NP - n) * T), r = i % ((NP - n) * T);
+        tile[(b * NP + n) * T + r] = 0.f;
+    }
+    const uint32_t q0 = p.qpos[it.x];
+    for (int d = tid; d < NP; d += JB) cen[d] = d < (int)n ? p.Xs[(uint64_t)d * Npad + q0] : 0.f;
+    if (tid == 0) {
+        s_ri = it.z;
+        s_off = 0;
+    }
+    __syncthreads();
+
+    // query vector (registers): a2 = -2 a', na = |a'|^2
+    float a2[NP];
+    float na = 0.f;
+#pragma unroll
+    for (int d = 0; d < NP; ++d) {
+        float v = d < (int)n ? p.Xs[(uint64_t)d * Npad + qp] - cen[d] : 0.f;
+        a2[d] = -2.f * v;
+        na = fmaf(v, v, na);
+    }
+    const float Aq = sqrtf(na) * 1.0001f;
+    const float init_cut = (p.init_cut && has_q) ? p.init_cut[row] : CUDART_INF_F;
+
+    int cnt = 0;
+    bool ovf = false;
+    float dmax = 0.f;
+    float cut_list = CUDART_INF_F;
+
+    auto build = [&](int b) {  // warp 0: next T candidate positions from the cursor
+        if (warp == 0) {
+            uint32_t ri = s_ri, off = s_off, filled = 0;
+            while (filled < (uint32_t)T && ri < it.w) {
+                uint2 r = p.adj[ri];
+                uint32_t avail = r.y - r.x - off;
+                uint32_t take = min(avail, (uint32_t)T - filled);
+                for (uint32_t i = lane; i < take; i += 32) tpos[b * T + filled + i] = r.x + off + i;
+                filled += take;
+                off += take;
+                if (off == r.y - r.x) {
+                    ++ri;
+                    off = 0;
+                }
+            }
+            for (uint32_t i = filled + lane; i < (uint32_t)T; i += 32) tpos[b * T + i] = OVF;
+            __syncwarp();
+            if (lane == 0) {
+                s_ri = ri;
+                s_off = off;
+                s_cnt[b] = filled;
+                s_bmax[b] = 0u;
+            }
+        }
+    };
+    auto issue = [&](int b) {
+        const uint32_t c = s_cnt[b];
+        for (uint32_t i = tid; i < n * (uint32_t)T; i += JB) {
+            uint32_t d = i / T, j = i % T;
+            float* dst = &tile[(b * NP + d) * T + j];
+            uint32_t pj = tpos[b * T + j];
+            if (j < c) cp_async4(dst, p.Xs + (uint64_t)d * Npad + pj);
+            else *dst = 0.f;
+        }
+        cp_commit();
+    };
+
+    build(0);
+    __syncthreads();
+    issue(0);
+    int buf = 0;
+    while (true) {
+        const uint32_t c = s_cnt[buf];
+        if (c == 0) break;
+        build(buf ^ 1);
+        __syncthreads();
+        issue(buf ^ 1);
+        cp_wait<1>();
+        __syncthreads();
+        // centre candidates, norms, tile max norm
+        for (int j = tid; j < T; j += JB) {
+            float nb = CUDART_NAN_F;
+            if ((uint32_t)j < c) {
+                nb = 0.f;
+#pragma unroll
+                for (int d = 0; d < NP; ++d) {
+                    if (d < (int)n) {
+                        float v = tile[(buf * NP + d) * T + j] - cen[d];
+                        tile[(buf * NP + d) * T + j] = v;
+                        nb = fmaf(v, v, nb);
+                    }
+                }
+            }
+            nbuf[buf * T + j] = nb;
+            float m = (uint32_t)j < c ? nb : 0.f;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+            if (lane == 0) atomicMax(&s_bmax[buf], __float_as_uint(m));
+        }
+        __syncthreads();
+        if (has_q && !ovf) {
+            const float Bt = sqrtf(__uint_as_float(s_bmax[buf])) * 1.0001f;
+            const float dl = screen_delta(Aq, Bt, p.gam, p.erg, p.eab, p.e64);
+            dmax = fmaxf(dmax, dl);
+            if (cnt >= (int)p.K) cut_list = __fadd_ru(lkey[(p.K - 1) * JB + tid], 2.f * dmax);
+            float cut = fminf(cut_list, __fadd_ru(init_cut, dl));
+            float rhs = __fsub_ru(cut, na);
+            const float* tb = tile + buf * NP * T;
+            const float* nbb = nbuf + buf * T;
+            const uint32_t jend = (c + 3) & ~3u;
+            for (uint32_t j = 0; j < jend; j += 4) {
+                float4 nb4 = *reinterpret_cast<const float4*>(nbb + j);
+                float acc0 = nb4.x, acc1 = nb4.y, acc2 = nb4.z, acc3 = nb4.w;
+#pragma unroll
+                for (int d = 0; d < NP; ++d) {
+                    float4 b = *reinterpret_cast<const float4*>(tb + d * T + j);
+                    acc0 = fmaf(a2[d], b.x, acc0);
+                    acc1 = fmaf(a2[d], b.y, acc1);
+                    acc2 = fmaf(a2[d], b.z, acc2);
+                    acc3 = fmaf(a2[d], b.w, acc3);
+                }
+                const bool s0 = acc0 <= rhs, s1 = acc1 <= rhs, s2 = acc2 <= rhs, s3 = acc3 <= rhs;
+                if (s0 | s1 | s2 | s3) {
+                    float accs[4] = {acc0, acc1, acc2, acc3};
+                    bool ss[4] = {s0, s1, s2, s3};
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        if (!ss[u]) continue;
+                        const uint32_t pos = tpos[buf * T + j + u];
+                        if (pos == qp) continue;  // self pair: excluded by id
+                        const float key = accs[u] + na;
+                        if (cnt == (int)p.L) {
+                            ovf = true;
+                            rhs = -CUDART_INF_F;
+                            break;
+                        }
+                        int q = cnt;
+                        while (q > 0) {
+                            float kq = lkey[(q - 1) * JB + tid];
+                            if (kq <= key) break;
+                            lkey[q * JB + tid] = kq;
+                            lpos[q * JB + tid] = lpos[(q - 1) * JB + tid];
+                            --q;
+                        }
+                        lkey[q * JB + tid] = key;
+                        lpos[q * JB + tid] = pos;
+                        ++cnt;
+                        if (cnt >= (int)p.K) {
+                            cut_list = __fadd_ru(lkey[(p.K - 1) * JB + tid], 2.f * dmax);
+                            const float ci = __fadd_ru(init_cut, dmax);
+                            const float ce = fminf(cut_list, ci);
+                            while (cnt > (int)p.K && lkey[(cnt - 1) * JB + tid] > ce) --cnt;
+                            cut = fminf(cut_list, __fadd_ru(init_cut, dl));
+                            rhs = __fsub_ru(cut, na);
+                        }
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        buf ^= 1;
+    }
+    cp_wait<0>();
+    if (has_q) {
+        p.out_cnt[row] = ovf ? OVF : (uint32_t)cnt;
+        if (!ovf)
+            for (int i = 0; i < cnt; ++i) p.out_pos[(uint64_t)row * p.L + i] = lpos[i * JB + tid];
+    }
+}
+
+// ---------------------------------------------------------------- finalize
+// One warp per launch row: exact FP64 distances for the screened list, exact
+// (sq,id) ranks, first K written to the query's output row, status bits.
+__global__ void k_finalize(FinalArgs a) {
+    const uint64_t row = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (row >= a.nrows) return;
+    const uint32_t c = a.cnt[row];
+    const uint32_t orow = a.qrow[row];
+    if (c == OVF) {
+        if (lane == 0) a.out_status[orow] = ST_OVF;
+        return;
+    }
+    const uint32_t qid = a.A[a.qpos[row]];
+    const double* qx = a.X64 + (uint64_t)qid * a.n;
+    constexpr int EMAX = 8;
+    double sq[EMAX];
+    uint32_t id[EMAX];
+    uint32_t rk[EMAX];
+    const int E = (int)((c + 31) / 32);
+#pragma unroll
+    for (int e = 0; e < EMAX; ++e) {
+        sq[e] = CUDART_INF;
+        id[e] = 0xFFFFFFFFu;
+        rk[e] = 0;
+        const uint32_t i = e * 32 + lane;
+        if (e < E && i < c) {
+            const uint32_t t = a.A[a.pos[row * a.L + i]];
+            id[e] = t;
+            sq[e] = exact_sq(qx, a.X64 + (uint64_t)t * a.n, a.n);
+        }
+    }
+#pragma unroll
+    for (int e = 0; e < EMAX; ++e) {
+        if (e >= E) break;
+        const double ms = sq[e];
+        const uint32_t mi = id[e];
+        for (int src = 0; src < 32; ++src) {
+            const double s = __shfl_sync(0xffffffffu, ms, src);
+            const uint32_t t = __shfl_sync(0xffffffffu, mi, src);
+            if ((uint32_t)(e * 32 + src) >= c) break;
+#pragma unroll
+            for (int f = 0; f < EMAX; ++f)
+                if (f < E && pair_less(s, t, sq[f], id[f])) ++rk[f];
+        }
+    }
+    double kth = CUDART_INF;
+#pragma unroll
+    for (int f = 0; f < EMAX; ++f) {
+        const uint32_t i = f * 32 + lane;
+        if (f < E && i < c && rk[f] < a.K) {
+            a.out_ids[(uint64_t)orow * a.K + rk[f]] = id[f];
+            a.out_dist[(uint64_t)orow * a.K + rk[f]] = sqrt(sq[f]);
+            if (rk[f] == a.K - 1) kth = sq[f];
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) kth = fmin(kth, __shfl_xor_sync(0xffffffffu, kth, o));
+    if (lane == 0) {
+        uint8_t st = 0;
+        if (c >= a.K) {
+            st |= ST_HAS_K;
+            if (kth <= a.eps2) st |= ST_IN_EPS;
+            if (kth < a.cover2) st |= ST_CERT;
+        }
+        a.out_status[orow] = st;
+        a.out_kth[orow] = c >= a.K ? kth : CUDART_INF;
+    }
+}
+
+// ---------------------------------------------------------------- histogram
+// Block = JB sampled queries x one slab of candidates (id order). Per pair the
+// FP32 key decides "beyond eps_mean" / bin b whenever key±delta is certain;
+// otherwise the FP64 scalar distance decides exactly like epsilon.cpp:86-95.
+// Each thread owns a private column of bin counters in shared memory (no
+// atomics on the hot path); columns are reduced once per block.
+template <int NP, int T>
+__global__ void __launch_bounds__(JB) k_hist(HistArgs a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    float* tile = reinterpret_cast<float*>(smem_raw);  // [2][NP][T]
+    float* nbuf = tile + 2 * NP * T;                   // [2][T]
+    float* LO = nbuf + 2 * T;                          // [n_bins+1]
+    float* HI = LO + a.n_bins + 1;                     // [n_bins+1]
+    uint32_t* hist = reinterpret_cast<uint32_t*>(HI + a.n_bins + 1);  // [n_bins][JB]
+    __shared__ unsigned s_bmax[2];
+
+    const int tid = threadIdx.x, lane = tid & 31;
+    const uint32_t n = a.n, nbins = a.n_bins;
+    const uint64_t row = uint64_t(blockIdx.x) * JB + tid;
+    const bool has_q = row < a.nq;
+    const uint32_t qid = has_q ? a.q[row] : 0;
+    const uint64_t cb = uint64_t(blockIdx.y) * a.cand_begin_stride;
+    const uint64_t ce = min(a.N, cb + a.cand_begin_stride);
+
+    for (uint32_t i = tid; i < nbins * JB; i += JB) hist[i] = 0;
+    for (uint32_t i = tid; i <= nbins; i += JB) {
+        LO[i] = a.SU[i];
+        HI[i] = a.SD[i];
+    }
+    for (int i = tid; i < 2 * (NP - (int)n) * T; i += JB) {
+        int b = i / ((NP - n) * T), r = i % ((NP - n) * T);
+        tile[(b * NP + n) * T + r] = 0.f;
+    }
+    float a2[NP];
+    float na = 0.f;
+#pragma unroll
+    for (int d = 0; d < NP; ++d) {
+        float v = (d < (int)n && has_q) ? a.Xf[(uint64_t)d * a.Npad + qid] : 0.f;
+        a2[d] = -2.f * v;
+        na = fmaf(v, v, na);
+    }
+    const float Aq = sqrtf(na) * 1.0001f;
+    const float lo_end = a.SU[nbins];
+    const float invw = (float)a.inv_width;
+    const double* qx = a.X64 + (uint64_t)qid * n;
+
+    auto issue = [&](int b, uint64_t s0) {
+        // s0 is a multiple of 4 and Npad a multiple of 4: 16-byte copies
+        for (uint32_t i = tid; i < n * (uint32_t)(T / 4); i += JB) {
+            uint32_t d = i / (T / 4), j4 = (i % (T / 4)) * 4;
+            float* dst = &tile[(b * NP + d) * T + j4];
+            cp_async16(dst, a.Xf + (uint64_t)d * a.Npad + s0 + j4);
+        }
+        cp_commit();
+        if (tid == 0) s_bmax[b] = 0u;
+    };
+
+    __syncthreads();
+    if (cb < ce) issue(0, cb);
+    int buf = 0;
+    for (uint64_t s0 = cb; s0 < ce; s0 += T) {
+        const uint32_t c = (uint32_t)min((uint64_t)T, ce - s0);
+        if (s0 + T < ce) issue(buf ^ 1, s0 + T);
+        else cp_commit();
+        cp_wait<1>();
+        __syncthreads();
+        for (int j = tid; j < T; j += JB) {
+            float nb = CUDART_NAN_F;
+            if ((uint32_t)j < c) {
+                nb = 0.f;
+#pragma unroll
+                for (int d = 0; d < NP; ++d) {
+                    float v = tile[(buf * NP + d) * T + j];
+                    nb = fmaf(v, v, nb);
+                }
+            }
+            nbuf[buf * T + j] = nb;
+            float m = (uint32_t)j < c ? nb : 0.f;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+            if (lane == 0) atomicMax(&s_bmax[buf], __float_as_uint(m));
+        }
+        __syncthreads();
+        if (has_q) {
+            const float Bt = sqrtf(__uint_as_float(s_bmax[buf])) * 1.0001f;
+            const float dl = screen_delta(Aq, Bt, a.gam, a.erg, a.eab, a.e64);
+            // key - dl >= lo_end  <=>  acc >= lo_end + dl - na (rounded down: conservative)
+            const float skip_at = __fsub_ru(__fadd_ru(lo_end, dl), na);
+            const float* tb = tile + buf * NP * T;
+            const float* nbb = nbuf + buf * T;
+            const uint32_t jend = (c + 3) & ~3u;
+            for (uint32_t j = 0; j < jend; j += 4) {
+                float4 nb4 = *reinterpret_cast<const float4*>(nbb + j);
+                float acc[4] = {nb4.x, nb4.y, nb4.z, nb4.w};
+#pragma unroll
+                for (int d = 0; d < NP; ++d) {
+                    float4 b = *reinterpret_cast<const float4*>(tb + d * T + j);
+                    acc[0] = fmaf(a2[d], b.x, acc[0]);
+                    acc[1] = fmaf(a2[d], b.y, acc[1]);
+                    acc[2] = fmaf(a2[d], b.z, acc[2]);
+                    acc[3] = fmaf(a2[d], b.w, acc[3]);
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    if (!(acc[u] < skip_at)) continue;  // beyond eps_mean (or NaN pad)
+                    const uint64_t t = s0 + j + u;
+                    if (t == qid) continue;
+                    const float key = acc[u] + na;
+                    const float klo = __fsub_rd(key, dl), khi = __fadd_ru(key, dl);
+                    int b = key > 0.f ? (int)(key * rsqrtf(key) * invw) : 0;
+                    b = min(max(b, 0), (int)nbins - 1);
+                    if (klo >= LO[b] && khi < HI[b]) {
+                        hist[b * JB + tid] += 1;
+                    } else {
+                        const double sq = exact_sq(qx, a.X64 + t * n, n);
+                        if (sq > a.limit_sq) continue;
+                        const double dist = sqrt(sq);
+                        if (dist >= a.eps_mean) continue;
+                        uint64_t bb = (uint64_t)(dist * a.inv_width);
+                        if (bb >= nbins) bb = nbins - 1;
+                        hist[bb * JB + tid] += 1;
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        buf ^= 1;
+    }
+    cp_wait<0>();
+    __syncthreads();
+    for (uint32_t b = tid; b < nbins; b += JB) {
+        unsigned long long s = 0;
+        for (int t = 0; t < JB; ++t) s += hist[b * JB + ((t + b) & (JB - 1))];
+        if (s) atomicAdd(&a.counts[b], s);
+    }
+}
+
+// ---------------------------------------------------------------- dispatch
+#define KJ_NP_LIST(X) \
+    X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(10) X(12) X(16) X(18) X(20) X(24) X(32) \
+    X(48) X(64) X(96) X(128)
+
+int pick_np(uint32_t n) {
+    static const int nps[] = {1, 2, 3, 4, 5, 6, 7, 8, 10, 12, 16, 18, 20, 24, 32, 48, 64, 96, 128};
+    for (int v : nps)
+        if ((uint32_t)v >= n) return v;
+    return -1;
+}
+static int tile_for(int np) { return np <= 32 ? 128 : 64; }
+
+size_t join_smem_bytes(int np, uint32_t L) {
+    int T = tile_for(np);
+    return sizeof(float) * (2 * np * T + 2 * T) + sizeof(uint32_t) * 2 * T +
+           sizeof(float) * ((np + 3) & ~3) + (sizeof(float) + sizeof(uint32_t)) * L * JB;
+}
+
+template <int NP>
+static void launch_join_np(const JoinArgs& a, uint64_t nitems, cudaStream_t s) {
+    constexpr int T = NP <= 32 ? 128 : 64;
+    size_t sm = join_smem_bytes(NP, a.L);
+    static bool attr = false;
+    if (!attr) {
+        KJ_CUDA(cudaFuncSetAttribute(k_join<NP, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     227 * 1024));
+        attr = true;
+    }
+    for (uint64_t off = 0; off < nitems; off += 2147483647ull) {
+        uint64_t cnt = std::min<uint64_t>(nitems - off, 2147483647ull);
+        JoinArgs b = a;
+        b.items = a.items + off;
+        k_join<NP, T><<<dim3((unsigned)cnt), JB, sm, s>>>(b);
+    }
+    KJ_CUDA(cudaGetLastError());
+}
+
+void launch_join(const JoinArgs& a, uint64_t nitems, cudaStream_t s) {
+    if (nitems == 0) return;
+    int np = pick_np(a.n);
+    switch (np) {
+#define X(v) \
+    case v: launch_join_np<v>(a, nitems, s); break;
+        KJ_NP_LIST(X)
+#undef X
+        default: throw Error(1, "dimension count above 128 is not supported by the device join");
+    }
+}
+
+void launch_finalize(const FinalArgs& a, cudaStream_t s) {
+    if (a.nrows == 0) return;
+    uint64_t threads = a.nrows * 32;
+    k_finalize<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(a);
+    KJ_CUDA(cudaGetLastError());
+}
+
+size_t hist_smem_bytes(int np, uint32_t n_bins) {
+    int T = tile_for(np);
+    return sizeof(float) * (2 * np * T + 2 * T) + sizeof(float) * 2 * (n_bins + 1) +
+           sizeof(uint32_t) * n_bins * JB;
+}
+
+template <int NP>
+static void launch_hist_np(const HistArgs& a, uint64_t n_slabs, cudaStream_t s) {
+    constexpr int T = NP <= 32 ? 128 : 64;
+    size_t sm = hist_smem_bytes(NP, a.n_bins);
+    static bool attr = false;
+    if (!attr) {
+        KJ_CUDA(cudaFuncSetAttribute(k_hist<NP, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     227 * 1024));
+        attr = true;
+    }
+    dim3 grid((unsigned)((a.nq + JB - 1) / JB), (unsigned)n_slabs);
+    k_hist<NP, T><<<grid, JB, sm, s>>>(a);
+    KJ_CUDA(cudaGetLastError());
+}
+
+void launch_histogram(const HistArgs& a, uint64_t n_slabs, cudaStream_t s) {
+    if (a.nq == 0) return;
+    int np = pick_np(a.n);
+    switch (np) {
+#define X(v) \
+    case v: launch_hist_np<v>(a, n_slabs, s); break;
+        KJ_NP_LIST(X)
+#undef X
+        default: throw Error(1, "dimension count above 128 is not supported by the device histogram");
+    }
+}
+
+// ---------------------------------------------------------------- small kernels
+__global__ void k_check_finite(const double* X, uint64_t count, unsigned long long* first_bad) {
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
+         i += uint64_t(gridDim.x) * blockDim.x)
+        if (!isfinite(X[i])) atomicMin(first_bad, (unsigned long long)i);
+}
+void launch_check_finite(const double* X, uint64_t count, unsigned long long* first_bad,
+                         cudaStream_t s) {
+    k_check_finite<<<1184, 256, 0, s>>>(X, count, first_bad);
+    KJ_CUDA(cudaGetLastError());
+}
+
+// Column sums (mean == null) or sums of squared deviations, per row-block:
+// partial[blk*n + j]. Fixed partition and order -> deterministic.
+__global__ void k_col_sums(const double* X, uint64_t N, uint32_t n, const double* mean,
+                           double* partial) {
+    __shared__ double red[8][33];
+    const uint32_t j = blockIdx.y * 32 + threadIdx.x;
+    const uint64_t rows_per = (N + gridDim.x - 1) / gridDim.x;
+    const uint64_t r0 = uint64_t(blockIdx.x) * rows_per, r1 = min(N, r0 + rows_per);
+    double s = 0.0;
+    if (j < n) {
+        const double mj = mean ? mean[j] : 0.0;
+        for (uint64_t i = r0 + threadIdx.y; i < r1; i += 8) {
+            double v = X[i * n + j];
+            if (mean) {
+                v = v - mj;
+                s += v * v;
+            } else {
+                s += v;
+            }
+        }
+    }
+    red[threadIdx.y][threadIdx.x] = s;
+    __syncthreads();
+    if (threadIdx.y == 0 && j < n) {
+        double t = 0.0;
+        for (int y = 0; y < 8; ++y) t += red[y][threadIdx.x];
+        partial[uint64_t(blockIdx.x) * n + j] = t;
+    }
+}
+void launch_col_sums(const double* X, uint64_t N, uint32_t n, const double* mean,
+                     double* partial, uint32_t nblk, cudaStream_t s) {
+    dim3 grid(nblk, (n + 31) / 32), block(32, 8);
+    k_col_sums<<<grid, block, 0, s>>>(X, N, n, mean, partial);
+    KJ_CUDA(cudaGetLastError());
+}
+
+__global__ void k_permute_cols(const double* X0, double* X, uint64_t N, uint32_t n,
+                               const uint32_t* order) {
+    for (uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < N * n;
+         e += uint64_t(gridDim.x) * blockDim.x) {
+        uint64_t i = e / n;
+        uint32_t j = (uint32_t)(e - i * n);
+        X[e] = X0[i * n + order[j]];
+    }
+}
+void launch_permute_cols(const double* X0, double* X, uint64_t N, uint32_t n,
+                         const uint32_t* order, cudaStream_t s) {
+    k_permute_cols<<<2368, 256, 0, s>>>(X0, X, N, n, order);
+    KJ_CUDA(cudaGetLastError());
+}
+
+__global__ void k_to_float_soa(const double* X, uint64_t N, uint32_t n, const double* g,
+                               float* Xf, uint64_t Npad, unsigned long long* rmax_bits) {
+    double rmax = 0.0;
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < Npad;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        double r2 = 0.0;
+        for (uint32_t d = 0; d < n; ++d) {
+            float v = 0.f;
+            if (i < N) {
+                double dv = X[i * n + d] - g[d];
+                r2 += dv * dv;
+                v = (float)dv;
+            }
+            Xf[uint64_t(d) * Npad + i] = v;
+        }
+        rmax = fmax(rmax, r2);
+    }
+    for (int o = 16; o > 0; o >>= 1) rmax = fmax(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(rmax_bits, (unsigned long long)__double_as_longlong(rmax));
+}
+void launch_to_float_soa(const double* X, uint64_t N, uint32_t n, const double* g, float* Xf,
+                         uint64_t Npad, unsigned long long* rmax_bits, cudaStream_t s) {
+    k_to_float_soa<<<1184, 256, 0, s>>>(X, N, n, g, Xf, Npad, rmax_bits);
+    KJ_CUDA(cudaGetLastError());
+}
+
+__global__ void k_pair_sq(const double* X, uint32_t n, const uint64_t* ij, uint64_t npairs,
+                          double limit, double* out) {
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < npairs;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        double s = exact_sq(X + ij[2 * i] * n, X + ij[2 * i + 1] * n, n);
+        out[i] = s > limit ? CUDART_INF : s;
+    }
+}
+void launch_pair_sq(const double* X, uint32_t n, const uint64_t* ij, uint64_t npairs,
+                    double limit, double* out, cudaStream_t s) {
+    if (!npairs) return;
+    k_pair_sq<<<(unsigned)std::min<uint64_t>(4736, (npairs + 255) / 256), 256, 0, s>>>(
+        X, n, ij, npairs, limit, out);
+    KJ_CUDA(cudaGetLastError());
+}
+
+__global__ void k_minmax(const double* X, uint64_t N, uint32_t n, uint32_t m,
+                         unsigned long long* mn, unsigned long long* mx) {
+    for (uint32_t j = 0; j < m; ++j) {
+        unsigned long long lo = ~0ull, hi = 0ull;
+        for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < N;
+             i += uint64_t(gridDim.x) * blockDim.x) {
+            unsigned long long o = dbl_order(X[i * n + j]);
+            lo = o < lo ? o : lo;
+            hi = o > hi ? o : hi;
+        }
+        for (int off = 16; off > 0; off >>= 1) {
+            unsigned long long l2 = __shfl_xor_sync(0xffffffffu, lo, off);
+            unsigned long long h2 = __shfl_xor_sync(0xffffffffu, hi, off);
+            lo = l2 < lo ? l2 : lo;
+            hi = h2 > hi ? h2 : hi;
+        }
+        if ((threadIdx.x & 31) == 0) {
+            atomicMin(&mn[j], lo);
+            atomicMax(&mx[j], hi);
+        }
+    }
+}
+void launch_minmax(const double* X, uint64_t N, uint32_t n, uint32_t m, unsigned long long* mn,
+                   unsigned long long* mx, cudaStream_t s) {
+    k_minmax<<<592, 256, 0, s>>>(X, N, n, m, mn, mx);
+    KJ_CUDA(cudaGetLastError());
+}
+
+// grid_index.cpp:77-94 (cell_of + linearize), FP64 division and floor
+__global__ void k_cell_keys(const double* X, uint64_t N, uint32_t n, uint32_t m,
+                            const double* mins, double w, const uint64_t* cpd,
+                            const uint64_t* strides, uint64_t* keys, uint32_t* vals) {
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < N;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        uint64_t id = 0;
+        for (uint32_t j = 0; j < m; ++j) {
+            double rel = __ddiv_rn(__dsub_rn(X[i * n + j], mins[j]), w);
+            if (rel < 0.0) rel = 0.0;
+            uint64_t idx = (uint64_t)floor(rel);
+            if (idx > cpd[j] - 1) idx = cpd[j] - 1;
+            id += idx * strides[j];
+        }
+        keys[i] = id;
+        vals[i] = (uint32_t)i;
+    }
+}
+void launch_cell_keys(const double* X, uint64_t N, uint32_t n, uint32_t m, const double* mins,
+                      double w, const uint64_t* cpd, const uint64_t* strides, uint64_t* keys,
+                      uint32_t* vals, cudaStream_t s) {
+    k_cell_keys<<<2368, 256, 0, s>>>(X, N, n, m, mins, w, cpd, strides, keys, vals);
+    KJ_CUDA(cudaGetLastError());
+}
+
+__global__ void k_iota(uint32_t* v, uint64_t N) {
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < N;
+         i += uint64_t(gridDim.x) * blockDim.x)
+        v[i] = (uint32_t)i;
+}
+void launch_iota(uint32_t* v, uint64_t N, cudaStream_t s) {
+    k_iota<<<1184, 256, 0, s>>>(v, N);
+    KJ_CUDA(cudaGetLastError());
+}
+
+__global__ void k_head_flags(const uint64_t* keys, uint64_t N, uint32_t* flags) {
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < N;
+         i += uint64_t(gridDim.x) * blockDim.x)
+        flags[i] = (i == 0 || keys[i] != keys[i - 1]) ? 1u : 0u;
+}
+void launch_head_flags(const uint64_t* keys, uint64_t N, uint32_t* flags, cudaStream_t s) {
+    k_head_flags<<<1184, 256, 0, s>>>(keys, N, flags);
+    KJ_CUDA(cudaGetLastError());
+}
+
+// runidx: inclusive scan of head flags (1-based run number)
+__global__ void k_grid_tables(const uint64_t* skeys, const uint32_t* A, const uint32_t* runidx,
+                              uint64_t N, uint64_t* B, uint2* G, uint32_t* slot,
+                              uint32_t* posOf) {
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < N;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const uint32_t r = runidx[i] - 1;
+        const uint64_t k = skeys[i];
+        if (i == 0 || skeys[i - 1] != k) {
+            B[r] = k;
+            G[r].x = (uint32_t)i;
+        }
+        if (i == N - 1 || skeys[i + 1] != k) G[r].y = (uint32_t)(i + 1);
+        slot[A[i]] = r;
+        posOf[A[i]] = (uint32_t)i;
+    }
+}
+void launch_grid_tables(const uint64_t* skeys, const uint32_t* A, const uint32_t* runidx,
+                        uint64_t N, uint64_t* B, uint2* G, uint32_t* slot, uint32_t* posOf,
+                        cudaStream_t s) {
+    k_grid_tables<<<1184, 256, 0, s>>>(skeys, A, runidx, N, B, G, slot, posOf);
+    KJ_CUDA(cudaGetLastError());
+}
+
+__global__ void k_gather_soa(const float* Xf, const uint32_t* A, uint64_t N, uint32_t n,
+                             uint64_t Npad, float* Xs) {
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < Npad;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        if (i < N) {
+            const uint32_t src = A[i];
+            for (uint32_t d = 0; d < n; ++d) Xs[uint64_t(d) * Npad + i] = Xf[uint64_t(d) * Npad + src];
+        } else {
+            for (uint32_t d = 0; d < n; ++d) Xs[uint64_t(d) * Npad + i] = 0.f;
+        }
+    }
+}
+void launch_gather_soa(const float* Xf, const uint32_t* A, uint64_t N, uint32_t n,
+                       uint64_t Npad, float* Xs, cudaStream_t s) {
+    k_gather_soa<<<2368, 256, 0, s>>>(Xf, A, N, n, Npad, Xs);
+    KJ_CUDA(cudaGetLastError());
+}
+
+__global__ void k_map_u32(const uint32_t* idx, const uint32_t* table, uint64_t n, uint32_t* out) {
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x)
+        out[i] = table[idx[i]];
+}
+void launch_map_u32(const uint32_t* idx, const uint32_t* table, uint64_t n, uint32_t* out,
+                    cudaStream_t s) {
+    if (!n) return;
+    k_map_u32<<<1184, 256, 0, s>>>(idx, table, n, out);
+    KJ_CUDA(cudaGetLastError());
+}
+
+__device__ __forceinline__ uint64_t lower_bound_u64(const uint64_t* a, uint64_t n, uint64_t key) {
+    uint64_t lo = 0, hi = n;
+    while (lo < hi) {
+        uint64_t mid = (lo + hi) >> 1;
+        if (a[mid] < key) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+// One warp per cell: the 3^(m-1) rows of the clamped ±1 neighbourhood over
+// the first m-1 indexed dims; each row is the contiguous B-range of linear ids
+// [row + lo_last, row + hi_last] (grid_index.cpp:114-147 enumerates exactly
+// these cells). The cell's own row is emitted first.
+template <bool FILL>
+__global__ void k_adj(const uint64_t* B, const uint2* G, uint64_t ncells, const uint32_t* cells,
+                      uint64_t nc, uint32_t m, const uint64_t* cpd, const uint64_t* strides,
+                      uint32_t* counts, const uint32_t* offs, uint2* adj,
+                      unsigned long long* csize) {
+    const uint64_t w = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (w >= nc) return;
+    const uint64_t lin = B[cells[w]];
+    uint64_t c[64];
+    {
+        uint64_t r = lin;
+        for (uint32_t j = 0; j < m; ++j) {
+            c[j] = r / strides[j];
+            r -= c[j] * strides[j];
+        }
+    }
+    const uint32_t ml = m - 1;
+    uint64_t R = 1;
+    for (uint32_t j = 0; j < ml; ++j) R *= 3;
+    const uint64_t own = (R - 1) / 2;
+    const uint64_t lo_l = c[ml] > 0 ? c[ml] - 1 : 0;
+    const uint64_t hi_l = min(c[ml] + 1, cpd[ml] - 1);
+    uint32_t written = 0;
+    unsigned long long sz = 0;
+    // process own row first (iteration -1), then all rows != own
+    for (int64_t base = -32; base < (int64_t)R; base += 32) {
+        int64_t r = base + lane;
+        bool valid = false;
+        uint2 rng = make_uint2(0, 0);
+        if (base < 0) {
+            if (lane == 0) r = (int64_t)own;
+            else r = -1;
+        } else if (r >= (int64_t)R || (uint64_t)r == own) {
+            r = -1;
+        }
+        if (r >= 0) {
+            uint64_t row = 0, t = (uint64_t)r;
+            bool ok = true;
+            for (int j = (int)ml - 1; j >= 0; --j) {
+                const uint64_t dig = t % 3;
+                t /= 3;
+                const int64_t cj = (int64_t)c[j] - 1 + (int64_t)dig;
+                if (cj < 0 || cj >= (int64_t)cpd[j]) {
+                    ok = false;
+                    break;
+                }
+                row += (uint64_t)cj * strides[j];
+            }
+            if (ok) {
+                const uint64_t s_lo = lower_bound_u64(B, ncells, row + lo_l);
+                const uint64_t s_hi = lower_bound_u64(B, ncells, row + hi_l + 1);
+                if (s_lo < s_hi) {
+                    valid = true;
+                    rng = make_uint2(G[s_lo].x, G[s_hi - 1].y);
+                }
+            }
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, valid);
+        if (FILL && valid) {
+            const uint32_t at = offs[w] + written + __popc(bal & ((1u << lane) - 1u));
+            adj[at] = rng;
+        }
+        if (valid) sz += rng.y - rng.x;
+        written += __popc(bal);
+    }
+    for (int o = 16; o > 0; o >>= 1) sz += __shfl_xor_sync(0xffffffffu, sz, o);
+    if (lane == 0) {
+        if (!FILL) counts[w] = written;
+        else if (csize) csize[w] = sz;
+    }
+}
+void launch_adj_count(const uint64_t* B, uint64_t ncells, const uint32_t* cells, uint64_t nc,
+                      uint32_t m, const uint64_t* cpd, const uint64_t* strides,
+                      uint32_t* counts, cudaStream_t s) {
+    if (!nc) return;
+    k_adj<false><<<(unsigned)((nc * 32 + 255) / 256), 256, 0, s>>>(
+        B, nullptr, ncells, cells, nc, m, cpd, strides, counts, nullptr, nullptr, nullptr);
+    KJ_CUDA(cudaGetLastError());
+}
+void launch_adj_fill(const uint64_t* B, const uint2* G, uint64_t ncells, const uint32_t* cells,
+                     uint64_t nc, uint32_t m, const uint64_t* cpd, const uint64_t* strides,
+                     const uint32_t* offs, uint2* adj, unsigned long long* csize,
+                     cudaStream_t s) {
+    if (!nc) return;
+    k_adj<true><<<(unsigned)((nc * 32 + 255) / 256), 256, 0, s>>>(
+        B, G, ncells, cells, nc, m, cpd, strides, nullptr, offs, adj, csize);
+    KJ_CUDA(cudaGetLastError());
+}
+
+__global__ void k_items(const uint32_t* ufirst, const uint32_t* ucnt, const uint32_t* item_off,
+                        const uint32_t* adj_off, uint64_t nuc, const unsigned long long* csize,
+                        uint4* items, unsigned long long* work) {
+    for (uint64_t u = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; u < nuc;
+         u += uint64_t(gridDim.x) * blockDim.x) {
+        const uint32_t f = ufirst[u], c = ucnt[u];
+        const uint32_t i0 = item_off[u];
+        const uint32_t nit = (c + JB - 1) / JB;
+        for (uint32_t t = 0; t < nit; ++t) {
+            const uint32_t qb = f + t * JB, qe = min(f + c, qb + JB);
+            items[i0 + t] = make_uint4(qb, qe, adj_off[u], adj_off[u + 1]);
+            work[i0 + t] = (unsigned long long)(qe - qb) * csize[u];
+        }
+    }
+}
+void launch_items(const uint32_t* ufirst, const uint32_t* ucnt, const uint32_t* item_off,
+                  const uint32_t* adj_off, uint64_t nuc, const unsigned long long* csize,
+                  uint4* items, unsigned long long* work, cudaStream_t s) {
+    if (!nuc) return;
+    k_items<<<592, 256, 0, s>>>(ufirst, ucnt, item_off, adj_off, nuc, csize, items, work);
+    KJ_CUDA(cudaGetLastError());
+}
+
+__global__ void k_cell_pop(const uint32_t* pids, uint64_t nq, const uint32_t* slot,
+                           const uint2* G, uint32_t* pop) {
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < nq;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const uint2 g = G[slot[pids[i]]];
+        pop[i] = g.y - g.x;
+    }
+}
+void launch_cell_pop(const uint32_t* pids, uint64_t nq, const uint32_t* slot, const uint2* G,
+                     uint32_t* pop, cudaStream_t s) {
+    if (!nq) return;
+    k_cell_pop<<<1184, 256, 0, s>>>(pids, nq, slot, G, pop);
+    KJ_CUDA(cudaGetLastError());
+}
+
+__global__ void k_fill_f32(float* p, uint64_t n, float v) {
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x)
+        p[i] = v;
+}
+void launch_fill_f32(float* p, uint64_t n, float v, cudaStream_t s) {
+    if (!n) return;
+    k_fill_f32<<<1184, 256, 0, s>>>(p, n, v);
+    KJ_CUDA(cudaGetLastError());
+}
+
+// range_query sizes (self included) over a pass: block per item, warp per query.
+__global__ void k_range_count(const double* X64, uint32_t n, const uint32_t* A,
+                              const uint32_t* qpos, const uint4* items, const uint2* adj,
+                              double eps2, unsigned long long* in_eps) {
+    const uint4 it = items[blockIdx.x];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (uint32_t r = it.x + warp; r < it.y; r += nw) {
+        const uint32_t qid = A[qpos[r]];
+        const double* qx = X64 + (uint64_t)qid * n;
+        unsigned long long cnt = 0;
+        for (uint32_t ri = it.z; ri < it.w; ++ri) {
+            const uint2 g = adj[ri];
+            for (uint32_t p = g.x + lane; p < g.y; p += 32)
+                cnt += exact_sq(qx, X64 + (uint64_t)A[p] * n, n) <= eps2;
+        }
+        for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+        if (lane == 0) in_eps[r] = cnt;
+    }
+}
+void launch_range_count(const double* X64, uint32_t n, const uint32_t* A, const uint32_t* qpos,
+                        const uint4* items, uint64_t nitems, const uint2* adj, double eps2,
+                        unsigned long long* in_eps, cudaStream_t s) {
+    if (!nitems) return;
+    k_range_count<<<(unsigned)nitems, 128, 0, s>>>(X64, n, A, qpos, items, adj, eps2, in_eps);
+    KJ_CUDA(cudaGetLastError());
+}
+
+// Exact slow path for rows whose screened list overflowed (many exact ties):
+// one warp per row, per-lane sorted top-K in shared memory, warp merge.
+__global__ void k_slow_exact(const double* X64, uint32_t n, const uint32_t* A,
+                             const uint32_t* qpos, const uint32_t* qrow, const uint32_t* rows,
+                             uint64_t nrows, const uint4* items, const uint32_t* row_item,
+                             const uint2* adj, uint32_t K, double eps2, double cover2,
+                             uint32_t* out_ids, double* out_dist, double* out_kth,
+                             uint8_t* out_status) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double* ls = reinterpret_cast<double*>(smem_raw);      // [K][32]
+    uint32_t* li = reinterpret_cast<uint32_t*>(ls + K * 32);  // [K][32]
+    const int lane = threadIdx.x;
+    const uint64_t ri = blockIdx.x;
+    if (ri >= nrows) return;
+    const uint32_t row = rows[ri];
+    const uint4 it = items[row_item[row]];
+    const uint32_t qp = qpos[row];
+    const uint32_t qid = A[qp];
+    const double* qx = X64 + (uint64_t)qid * n;
+    uint32_t cnt = 0;
+    for (uint32_t r = it.z; r < it.w; ++r) {
+        const uint2 g = adj[r];
+        for (uint32_t p = g.x + lane; p < g.y; p += 32) {
+            if (p == qp) continue;
+            const uint32_t t = A[p];
+            const double s = exact_sq(qx, X64 + (uint64_t)t * n, n);
+            if (cnt == K && !pair_less(s, t, ls[(K - 1) * 32 + lane], li[(K - 1) * 32 + lane]))
+                continue;
+            int q = (int)(cnt < K ? cnt : K - 1);
+            while (q > 0 && pair_less(s, t, ls[(q - 1) * 32 + lane], li[(q - 1) * 32 + lane])) {
+                ls[q * 32 + lane] = ls[(q - 1) * 32 + lane];
+                li[q * 32 + lane] = li[(q - 1) * 32 + lane];
+                --q;
+            }
+            ls[q * 32 + lane] = s;
+            li[q * 32 + lane] = t;
+            if (cnt < K) ++cnt;
+        }
+    }
+    uint32_t head = 0;
+    uint32_t total = cnt;
+    for (int o = 16; o > 0; o >>= 1) total += __shfl_xor_sync(0xffffffffu, total, o);
+    const uint32_t orow = qrow[row];
+    double kth = CUDART_INF;
+    const uint32_t outn = min(total, K);
+    for (uint32_t r = 0; r < outn; ++r) {
+        double s = head < cnt ? ls[head * 32 + lane] : CUDART_INF;
+        uint32_t t = head < cnt ? li[head * 32 + lane] : 0xFFFFFFFFu;
+        double bs = s;
+        uint32_t bt = t;
+        for (int o = 16; o > 0; o >>= 1) {
+            double s2 = __shfl_xor_sync(0xffffffffu, bs, o);
+            uint32_t t2 = __shfl_xor_sync(0xffffffffu, bt, o);
+            if (pair_less(s2, t2, bs, bt)) {
+                bs = s2;
+                bt = t2;
+            }
+        }
+        if (head < cnt && t == bt) ++head;
+        if (lane == 0) {
+            out_ids[(uint64_t)orow * K + r] = bt;
+            out_dist[(uint64_t)orow * K + r] = sqrt(bs);
+        }
+        kth = bs;
+    }
+    if (lane == 0) {
+        uint8_t st = 0;
+        if (total >= K) {
+            st |= ST_HAS_K;
+            if (kth <= eps2) st |= ST_IN_EPS;
+            if (kth < cover2) st |= ST_CERT;
+        }
+        out_status[orow] = st;
+        out_kth[orow] = total >= K ? kth : CUDART_INF;
+    }
+}
+void launch_slow_exact(const double* X64, uint32_t n, const uint32_t* A, const uint32_t* qpos,
+                       const uint32_t* qrow, const uint32_t* rows, uint64_t nrows,
+                       const uint4* items, const uint32_t* row_item, const uint2* adj,
+                       uint32_t K, double eps2, double cover2, uint32_t* out_ids,
+                       double* out_dist, double* out_kth, uint8_t* out_status, cudaStream_t s) {
+    if (!nrows) return;
+    size_t sm = (size_t)K * 32 * (sizeof(double) + sizeof(uint32_t));
+    if (sm > 227 * 1024) throw Error(1, "k too large for the exact slow path");
+    KJ_CUDA(cudaFuncSetAttribute(k_slow_exact, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 227 * 1024));
+    k_slow_exact<<<(unsigned)nrows, 32, sm, s>>>(X64, n, A, qpos, qrow, rows, nrows, items,
+                                                 row_item, adj, K, eps2, cover2, out_ids,
+                                                 out_dist, out_kth, out_status);
+    KJ_CUDA(cudaGetLastError());
+}
+
+}  // namespace kj
+
+namespace kj {
+__global__ void k_row_item(const uint4* items, uint64_t nitems, uint32_t* row_item) {
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < nitems;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const uint4 it = items[i];
+        for (uint32_t r = it.x; r < it.y; ++r) row_item[r] = (uint32_t)i;
+    }
+}
+void launch_row_item(const uint4* items, uint64_t nitems, uint32_t* row_item, cudaStream_t s) {
+    if (!nitems) return;
+    k_row_item<<<592, 256, 0, s>>>(items, nitems, row_item);
+    KJ_CUDA(cudaGetLastError());
+}
+}  // namespace kj
+
+namespace kj {
+template <class T>
+__global__ void k_gather(const uint32_t* idx, const T* table, uint64_t n, T* out) {
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x)
+        out[i] = table[idx[i]];
+}
+void launch_gather_u8(const uint32_t* idx, const uint8_t* table, uint64_t n, uint8_t* out,
+                      cudaStream_t s) {
+    if (!n) return;
+    k_gather<uint8_t><<<592, 256, 0, s>>>(idx, table, n, out);
+    KJ_CUDA(cudaGetLastError());
+}
+void launch_gather_f64(const uint32_t* idx, const double* table, uint64_t n, double* out,
+                       cudaStream_t s) {
+    if (!n) return;
+    k_gather<double><<<592, 256, 0, s>>>(idx, table, n, out);
+    KJ_CUDA(cudaGetLastError());
+}
+void launch_gather_f32(const uint32_t* idx, const float* table, uint64_t n, float* out,
+                       cudaStream_t s) {
+    if (!n) return;
+    k_gather<float><<<592, 256, 0, s>>>(idx, table, n, out);
+    KJ_CUDA(cudaGetLastError());
+}
+}  // namespace kj
