@@ -1,0 +1,314 @@
+#!/usr/bin/env python
+"""Benchmark: all-points exact KNN self-join (HybridKNN-Join hot path) on B200.
+
+Metric (BASELINE.json): KNN self-join points/sec, K=32, on the SuSy-shaped
+config C2 (5M x 18-D Gaussian-mixture, 16 clusters, sigma 0.05; synthetic, seed 1).
+One step = one full run_hybrid pass (variance reorder -> eps_mean -> distance
+histogram -> grid build -> split -> fused range-join + top-K -> exact fallback)
+over the whole dataset.
+
+  value : device-resident points/s (dataset already in HBM; results left in HBM)
+  e2e   : the same through the public C ABI with host buffers: pinned H2D of the
+          dataset + knnj_run + D2H of ids/dist, every step
+  --impl reference : the reference's own CPU implementation (oracle/_ref, the
+          unmodified library built from /root/reference) on a bounded query sample.
+
+Launch: python bench.py [--gpus N --steps K --warmup W]; N>1 under torchrun
+(queries sharded by contiguous cell ranges, dataset + grid replicated; the only
+exchange is an all-reduce of the 100 histogram counters).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "KNN self-join points/sec (end-to-end, K=32) at 1/2/4/8 B200 vs CPU ref"
+UNIT = "points/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--size", type=int, default=0, help="override |D| (testing only)")
+    ap.add_argument("--cpu-sample", type=int, default=0, help="reference query sample per step")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return rank, world, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                sm.append(float(r[1]))
+                mx = float(r[2])
+                for i, nm in enumerate(names):
+                    if r[4 + i].lower().startswith("active"):
+                        reasons.add(nm)
+            except (ValueError, IndexError):
+                pass
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------- reference arm
+def cpu_reference(X, k, sample, seed=1):
+    """The reference's RefImpl (SparseOnly: reorder + kd-tree) on a query sample
+    against the FULL dataset, all host threads. Returns (points/s, cores, detail)."""
+    from oracle.oracle import Ref, ref_available
+    if not ref_available():
+        return None
+    ref = Ref()
+    h, t_reorder, t_build = ref.kd_create(X, min(6, X.shape[1]))
+    cores = ref.hardware_concurrency()
+    rng = np.random.default_rng(seed)
+    q = np.sort(rng.choice(X.shape[0], sample, replace=False)).astype(np.uint32)
+    _, _, secs = ref.kd_query(h, q, k, cores)
+    return dict(handle=h, ref=ref, rate=sample / secs, secs=secs, cores=cores,
+                t_reorder=t_reorder, t_build=t_build, q=q)
+
+
+def run_reference(args, cfgd, X):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from oracle.oracle import Ref, ref_available
+    if not ref_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
+        return
+    k = cfgd["k"]
+    sample = args.cpu_sample or 1000
+    ref = Ref()
+    h, t_reorder, t_build = ref.kd_create(X, min(6, X.shape[1]))
+    cores = ref.hardware_concurrency()
+    rng = np.random.default_rng(1234)
+    times = []
+    for step in range(args.warmup + args.steps):
+        q = np.sort(rng.choice(X.shape[0], sample, replace=False)).astype(np.uint32)
+        _, _, secs = ref.kd_query(h, q, k, cores)
+        if step >= args.warmup:
+            times.append(secs)
+    ref.kd_destroy(h)
+    per_step = statistics.mean(times)
+    value = sample / per_step
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_step * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": cfgd["name"], "points": X.shape[0], "dims": X.shape[1], "k": k,
+                   "distribution": cfgd["spec"], "sample_queries_per_step": sample},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
+                         "sample": f"{sample} seeded random queries per step against all "
+                                   f"{X.shape[0]} points; reference SparseOnly/RefImpl (kd-tree, "
+                                   f"run_sparse_knn) on {cores} threads; kd build "
+                                   f"{t_build:.1f}s and reorder {t_reorder:.1f}s excluded like the "
+                                   f"reference's measured_total"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+# ---------------------------------------------------------------------------- our arm
+def run_ours(args, cfgd, X):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1810_04758_b200 import Engine, RunConfig
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    N, n = X.shape
+    k = cfgd["k"]
+    eng = Engine(local)
+    stream = torch.cuda.ExternalStream(eng.lib.knnj_stream(eng.h), device=torch.device("cuda", local))
+    lib = eng.lib
+
+    # pinned host buffers for the e2e leg
+    nbytes_in = N * n * 8
+    p_in = lib.knnj_alloc_pinned(nbytes_in)
+    Xp = np.ctypeslib.as_array((np.ctypeslib.ctypes.c_double * (N * n)).from_address(p_in)).reshape(N, n)
+    Xp[:] = X
+    p_ids = lib.knnj_alloc_pinned(N * k * 4)
+    p_dist = lib.knnj_alloc_pinned(N * k * 8)
+    p_prov = lib.knnj_alloc_pinned(N)
+
+    cfg = RunConfig(k=k, mode="hybrid", seed=1)
+    eng.set_points((p_in, N, n))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def timed(fn, steps):
+        infos = []
+        barrier()
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        for _ in range(steps):
+            infos.append(fn())
+        ev1.record(stream)
+        ev1.synchronize()
+        barrier()
+        ms = ev0.elapsed_time(ev1) / steps
+        if world > 1:
+            t = torch.tensor([ms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms, infos
+
+    def step_device():
+        r = eng.run(cfg, out=(0, 0, 0), want_hist=False)
+        return r.info
+
+    def step_e2e():
+        eng.set_points((p_in, N, n))
+        r = eng.run(cfg, out=(p_ids, p_dist, p_prov), want_hist=False)
+        return r.info
+
+    for _ in range(args.warmup):
+        step_device()
+    with ClockSampler(local) as clk:
+        ms, infos = timed(step_device, args.steps)
+    for _ in range(1):
+        step_e2e()
+    ms_e2e, infos_e2e = timed(step_e2e, args.steps)
+
+    # roofline of the dominant kernel (the fused join): algorithmic FP32 flops =
+    # 3n per candidate pair examined by the reference's 3^m walk
+    info = infos[-1]
+    join_ms = statistics.mean(i["ms_join_kernel"] for i in infos)
+    hist_ms = statistics.mean(i["ms_hist_kernel"] for i in infos)
+    cand = info["candidates_examined"]
+    flops = 3.0 * n * cand
+    achieved = flops / (join_ms * 1e-3) / 1e12
+    peak_c = np.ctypeslib.ctypes.c_double()
+    eng._check(lib.knnj_fp32_peak(eng.h, np.ctypeslib.ctypes.byref(peak_c)))
+    peak = peak_c.value
+    hist_pairs = info["hist_query_count"] * (N - 1)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        c = cpu_reference(X, k, args.cpu_sample or 1000)
+        if c is not None:
+            c["ref"].kd_destroy(c["handle"])
+            cpu = {"value": c["rate"], "unit": UNIT, "cores": c["cores"], "kind": "reference",
+                   "sample": f"{len(c['q'])} seeded random queries against all {N} points, "
+                             f"reference SparseOnly/RefImpl kd-tree (the faster reference CPU "
+                             f"mode), {c['secs']:.2f}s; kd build {c['t_build']:.1f}s excluded"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": world * 0 + N / (ms * 1e-3), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": cfgd["name"], "points": N, "dims": n, "k": k,
+                       "distribution": cfgd["spec"], "seed": 1,
+                       "parallelism": f"cell-range query shards x{world}" if world > 1 else "1 GPU",
+                       "l2": "inputs (%.0f MB FP64) exceed the 126 MB L2" % (N * n * 8 / 1e6),
+                       "eps_used": info["eps_used"], "grid_cells": info["grid_cells"],
+                       "candidates_per_query": cand / N},
+            "e2e": {"value": N / (ms_e2e * 1e-3), "unit": UNIT, "h2d_bytes_per_step": N * n * 8,
+                    "d2h_bytes_per_step": N * k * 12, "ms_per_step": ms_e2e},
+            "roofline": {"bound": "fp32", "kernel": "k_join (fused range-join + top-K)",
+                         "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": achieved / peak, "traffic": None,
+                         "peak_source": "FFMA microbenchmark measured live on this GPU "
+                                        "(MEASURED_PEAKS.json has no FP32 figure)",
+                         "algorithmic_flops_per_launch": flops,
+                         "flops_definition": "3n per candidate pair of the reference 3^m walk"},
+            "phases_ms": {k2: statistics.mean(i[k2] for i in infos) for k2 in
+                          ("ms_reorder", "ms_eps_mean", "ms_histogram", "ms_grid", "ms_split",
+                           "ms_join", "ms_fallback", "ms_join_kernel", "ms_hist_kernel")},
+            "hist_pairs_per_s": hist_pairs / (hist_ms * 1e-3) if hist_ms > 0 else None,
+            "gpu_launches": int(info["kernel_launches"]),
+            "clocks": clk.summary(),
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line))
+    for p in (p_in, p_ids, p_dist, p_prov):
+        lib.knnj_free_pinned(p)
+    eng.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    from paper_1810_04758_b200.synthetic import CONFIGS, generate
+    cfgd = dict(CONFIGS[args.config])
+    cfgd["name"] = f"{args.config}: " + {
+        "C2": "SuSy-shaped synthetic 18-D, 5M points, K=32, clustered (Gaussian mixture)",
+    }.get(args.config, args.config)
+    if args.size:
+        cfgd["size"] = args.size
+    X = generate(cfgd["spec"], cfgd["size"], cfgd["dims"], seed=1)
+    if args.impl == "reference":
+        run_reference(args, cfgd, X)
+    else:
+        run_ours(args, cfgd, X)
+
+
+if __name__ == "__main__":
+    main()

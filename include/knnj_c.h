@@ -57,6 +57,12 @@ int knnj_create(int device, knnj_ctx** out);
 void knnj_destroy(knnj_ctx* ctx);
 /* Message of the last failed call on ctx (same text as the reference exception's what()). */
 const char* knnj_last_error(const knnj_ctx* ctx);
+/* The CUDA stream (cudaStream_t) all of ctx's work is ordered on, for callers
+ * that time or synchronise with it (e.g. torch.cuda.ExternalStream). */
+void* knnj_stream(knnj_ctx* ctx);
+/* Measured FP32 FFMA throughput of this device (TFLOP/s, 2 flops per FFMA):
+ * the roofline denominator for the SIMT distance kernels. */
+int knnj_fp32_peak(knnj_ctx* ctx, double* tflops);
 /* Page-locked host buffers for the end-to-end path (H2D/D2H at full PCIe rate). */
 void* knnj_alloc_pinned(size_t bytes);
 void knnj_free_pinned(void* p);
@@ -159,6 +165,7 @@ typedef struct {
     uint64_t candidates_examined;
     uint64_t fallback_queries, fallback_passes, slow_path_queries;
     uint64_t grid_cells;
+    uint64_t kernel_launches;     /* this library's own kernels launched by the call */
     /* device-event timings (ms) */
     double ms_upload, ms_reorder, ms_eps_mean, ms_histogram, ms_grid, ms_split, ms_join,
         ms_fallback, ms_download, ms_total;
@@ -171,6 +178,7 @@ typedef struct {
  *   ids, dist : n_queries * k_effective   (row stride k_effective)
  *   prov      : n_queries                 (enum knnj_provenance)
  *   raw_hist  : n_bins (may be NULL)      integer histogram counts
+ * ids == NULL and dist == NULL keeps the results device-resident (no D2H).
  * k_effective = min(k, |D|-1) (orchestrator.cpp:77-82). */
 int knnj_run(knnj_ctx* ctx, const knnj_config* cfg, uint32_t* ids, double* dist, uint8_t* prov,
              uint64_t* raw_hist, knnj_run_info* info);

@@ -284,6 +284,12 @@ class Ref:
                                      C.c_uint32, C.c_uint32, _u32p, _dp,
                                      C.POINTER(C.c_double)]
         L.ref_hardware_concurrency.restype = C.c_uint
+        L.ref_kd_create.restype = C.c_void_p
+        L.ref_kd_create.argtypes = [_dp, C.c_uint64, C.c_uint32, C.c_uint32,
+                                    C.POINTER(C.c_double), C.POINTER(C.c_double)]
+        L.ref_kd_query.argtypes = [C.c_void_p, _u32p, C.c_uint64, C.c_uint32, C.c_uint32,
+                                   _u32p, _dp, C.POINTER(C.c_double)]
+        L.ref_kd_destroy.argtypes = [C.c_void_p]
         self.L = L
 
     def _check(self, rc):
@@ -392,6 +398,27 @@ class Ref:
         self._check(self.L.ref_sparse_knn(Xw, Xw.shape[0], Xw.shape[1], q, q.size, k, threads,
                                           ids, dist, C.byref(secs)))
         return ids.reshape(q.size, k), dist.reshape(q.size, k), secs.value
+
+    def kd_create(self, X, m):
+        """reorder_by_variance + KdTree::build once; returns (handle, t_reorder, t_build)."""
+        X = np.ascontiguousarray(X, np.float64)
+        a, b = C.c_double(), C.c_double()
+        h = self.L.ref_kd_create(X, X.shape[0], X.shape[1], m, C.byref(a), C.byref(b))
+        if not h:
+            raise RuntimeError(self.L.ref_last_error().decode())
+        return h, a.value, b.value
+
+    def kd_query(self, h, queries, k, threads=0):
+        q = np.ascontiguousarray(queries, np.uint32)
+        ids = np.zeros(q.size * k, np.uint32)
+        dist = np.zeros(q.size * k, np.float64)
+        secs = C.c_double()
+        threads = threads or self.hardware_concurrency()
+        self._check(self.L.ref_kd_query(h, q, q.size, k, threads, ids, dist, C.byref(secs)))
+        return ids.reshape(q.size, k), dist.reshape(q.size, k), secs.value
+
+    def kd_destroy(self, h):
+        self.L.ref_kd_destroy(h)
 
     def hardware_concurrency(self) -> int:
         return int(self.L.ref_hardware_concurrency())

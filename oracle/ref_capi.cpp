@@ -12,6 +12,7 @@
 #include <cstdint>
 #include <cstring>
 #include <exception>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -396,5 +397,47 @@ int ref_sparse_knn(const double* X, uint64_t N, uint32_t n, const uint32_t* q, u
 }
 
 unsigned ref_hardware_concurrency() { return default_worker_count(); }
+
+// Persistent RefImpl (SparseOnly) state for timing: the reference's
+// reorder_by_variance + KdTree::build once, then run_sparse_knn on query
+// samples (orchestrator.cpp:114-129; build excluded like measured_total).
+struct RefKd {
+    std::unique_ptr<Dataset> d;
+    std::unique_ptr<KdTree> t;
+};
+
+void* ref_kd_create(const double* X, uint64_t N, uint32_t n, uint32_t m, double* t_reorder,
+                    double* t_build) {
+    try {
+        auto h = new RefKd;
+        Dataset raw = make_ds(X, N, n);
+        Stopwatch a;
+        h->d = std::make_unique<Dataset>(reorder_by_variance(raw, m));
+        *t_reorder = a.seconds();
+        Stopwatch b;
+        h->t = std::make_unique<KdTree>(KdTree::build(*h->d, 16));
+        *t_build = b.seconds();
+        return h;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return nullptr;
+    }
+}
+
+int ref_kd_query(void* hp, const uint32_t* q, uint64_t nq, uint32_t k, uint32_t threads,
+                 uint32_t* ids, double* dist, double* seconds) {
+    return guarded([&] {
+        auto* h = static_cast<RefKd*>(hp);
+        SparseRunResult r = run_sparse_knn(*h->t, std::span<const PointId>(q, nq), k, threads);
+        *seconds = r.t1_seconds * double(nq);
+        for (uint64_t i = 0; i < nq; ++i)
+            for (std::size_t j = 0; j < r.neighbors[i].size(); ++j) {
+                if (ids) ids[i * k + j] = r.neighbors[i][j].id;
+                if (dist) dist[i * k + j] = r.neighbors[i][j].dist;
+            }
+    });
+}
+
+void ref_kd_destroy(void* hp) { delete static_cast<RefKd*>(hp); }
 
 }  // extern "C"

@@ -65,6 +65,7 @@ RUN_INFO_FIELDS = [
     ("failed_count", C.c_uint64), ("candidates_examined", C.c_uint64),
     ("fallback_queries", C.c_uint64), ("fallback_passes", C.c_uint64),
     ("slow_path_queries", C.c_uint64), ("grid_cells", C.c_uint64),
+    ("kernel_launches", C.c_uint64),
 ] + [(f, C.c_double) for f in (
     "ms_upload", "ms_reorder", "ms_eps_mean", "ms_histogram", "ms_grid", "ms_split", "ms_join",
     "ms_fallback", "ms_download", "ms_total", "ms_join_kernel", "ms_hist_kernel")] + [
@@ -87,6 +88,8 @@ SIGNATURES = [
     ("knnj_create", C.c_int, [C.c_int, C.POINTER(C.c_void_p)]),
     ("knnj_destroy", None, [_vp]),
     ("knnj_last_error", C.c_char_p, [_vp]),
+    ("knnj_stream", C.c_void_p, [_vp]),
+    ("knnj_fp32_peak", C.c_int, [_vp, C.POINTER(C.c_double)]),
     ("knnj_alloc_pinned", C.c_void_p, [C.c_size_t]),
     ("knnj_free_pinned", None, [C.c_void_p]),
     ("knnj_set_points", C.c_int, [_vp, _vp, C.c_uint64, C.c_uint32]),

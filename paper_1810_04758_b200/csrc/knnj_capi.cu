@@ -25,6 +25,13 @@
 
 using namespace kj;
 
+namespace kj {
+cudaStream_t& alloc_stream() {
+    static thread_local cudaStream_t s = nullptr;
+    return s;
+}
+}  // namespace kj
+
 namespace {
 
 constexpr double kInf = std::numeric_limits<double>::infinity();
@@ -841,7 +848,10 @@ namespace {
 template <class F>
 int guarded(knnj_ctx* ctx, F&& f) {
     try {
-        if (ctx) KJ_CUDA(cudaSetDevice(ctx->dev));
+        if (ctx) {
+            KJ_CUDA(cudaSetDevice(ctx->dev));
+            alloc_stream() = ctx->s;
+        }
         f();
         return KNNJ_OK;
     } catch (const kj::Error& e) {
@@ -870,6 +880,10 @@ int knnj_create(int device, knnj_ctx** out) {
         c->dev = device;
         KJ_CUDA(cudaSetDevice(device));
         KJ_CUDA(cudaStreamCreateWithFlags(&c->s, cudaStreamNonBlocking));
+        cudaMemPool_t pool;
+        KJ_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+        uint64_t keep = ~0ull;  // keep freed blocks cached in the pool
+        KJ_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
         *out = c.release();
         return KNNJ_OK;
     } catch (const kj::Error& e) {
@@ -882,10 +896,24 @@ int knnj_create(int device, knnj_ctx** out) {
 void knnj_destroy(knnj_ctx* ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->dev);
-    delete ctx;
+    alloc_stream() = ctx->s;
+    cudaStreamSynchronize(ctx->s);
+    {
+        cudaStream_t keep = ctx->s;
+        ctx->s = nullptr;  // members free on `keep` first, then the stream goes
+        delete ctx;
+        cudaStreamSynchronize(keep);
+        cudaStreamDestroy(keep);
+    }
 }
 
 const char* knnj_last_error(const knnj_ctx* ctx) { return ctx ? ctx->err.c_str() : "null ctx"; }
+
+void* knnj_stream(knnj_ctx* ctx) { return ctx ? (void*)ctx->s : nullptr; }
+
+int knnj_fp32_peak(knnj_ctx* c, double* tflops) {
+    return guarded(c, [&] { *tflops = kj::measure_ffma_tflops(c->s); });
+}
 
 void* knnj_alloc_pinned(size_t bytes) {
     void* p = nullptr;
@@ -1272,6 +1300,7 @@ int knnj_run(knnj_ctx* c, const knnj_config* cfg, uint32_t* ids, double* dist, u
         if (m > 64) throw Error(1, "grid m above 64 is not supported");
 
         Timer t_all(c->s);
+        const unsigned long long launches0 = g_launches.load();
         {
             Timer t(c->s);
             c->reorder(m);
@@ -1493,14 +1522,17 @@ int knnj_run(knnj_ctx* c, const knnj_config* cfg, uint32_t* ids, double* dist, u
                 }
             }
         }
-        {
+        if (ids || dist) {
             Timer t(c->s);
-            KJ_CUDA(cudaMemcpyAsync(ids, o_ids.p, 4 * nq * k_eff, cudaMemcpyDeviceToHost, c->s));
-            KJ_CUDA(cudaMemcpyAsync(dist, o_dist.p, 8 * nq * k_eff, cudaMemcpyDeviceToHost, c->s));
+            if (ids)
+                KJ_CUDA(cudaMemcpyAsync(ids, o_ids.p, 4 * nq * k_eff, cudaMemcpyDeviceToHost, c->s));
+            if (dist)
+                KJ_CUDA(cudaMemcpyAsync(dist, o_dist.p, 8 * nq * k_eff, cudaMemcpyDeviceToHost, c->s));
             I.ms_download = t.ms();
         }
         if (prov) std::memcpy(prov, h_prov.data(), nq);
         I.ms_total = t_all.ms();
+        I.kernel_launches = g_launches.load() - launches0;
         (void)t_start;
         if (info) *info = I;
     });

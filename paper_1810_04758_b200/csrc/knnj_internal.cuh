@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -26,16 +27,20 @@ struct Error : std::runtime_error {
     } while (0)
 
 // ---------------------------------------------------------------- device buffer
+// Stream-ordered allocations from the device's (cached) default memory pool:
+// temporaries cost no device synchronisation. The stream is the calling ctx's.
+cudaStream_t& alloc_stream();
 template <class T>
 struct DBuf {
     T* p = nullptr;
     size_t n = 0;  // capacity in elements
+    cudaStream_t s = nullptr;
     DBuf() = default;
     DBuf(const DBuf&) = delete;
     DBuf& operator=(const DBuf&) = delete;
     ~DBuf() { release(); }
     void release() {
-        if (p) cudaFree(p);
+        if (p) cudaFreeAsync(p, s);
         p = nullptr;
         n = 0;
     }
@@ -43,7 +48,8 @@ struct DBuf {
         if (count == 0) count = 1;
         if (count > n) {
             release();
-            KJ_CUDA(cudaMalloc(&p, count * sizeof(T)));
+            s = alloc_stream();
+            KJ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), s));
             n = count;
         }
         return p;
@@ -145,6 +151,8 @@ struct HistArgs {
 };
 
 // ---------------------------------------------------------------- launchers
+extern std::atomic<unsigned long long> g_launches;  // our kernels launched so far
+double measure_ffma_tflops(cudaStream_t s);
 int pick_np(uint32_t n);  // padded dimension count used by the templated kernels
 size_t join_smem_bytes(int np, uint32_t L);
 void launch_join(const JoinArgs& a, uint64_t nitems, cudaStream_t s);

@@ -17,9 +17,13 @@
 #include <cub/cub.cuh>
 #include <math_constants.h>
 
+#include <atomic>
+
 #include "knnj_internal.cuh"
 
 namespace kj {
+
+std::atomic<unsigned long long> g_launches{0};
 
 // ---------------------------------------------------------------- helpers
 __device__ __forceinline__ double exact_sq(const double* __restrict__ a,
@@ -477,6 +481,19 @@ __global__ void __launch_bounds__(JB) k_hist(HistArgs a) {
 }
 
 // ---------------------------------------------------------------- dispatch
+// Opt a kernel into the dynamic shared memory it needs (static smem counts
+// against the same per-block limit).
+template <class K>
+static void set_smem(K kernel, size_t dyn) {
+    int dev = 0, optin = 0;
+    KJ_CUDA(cudaGetDevice(&dev));
+    KJ_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    cudaFuncAttributes fa;
+    KJ_CUDA(cudaFuncGetAttributes(&fa, kernel));
+    if (dyn + fa.sharedSizeBytes > (size_t)optin)
+        throw Error(1, "configuration needs more shared memory than the device allows");
+    KJ_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+}
 #define KJ_NP_LIST(X) \
     X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(10) X(12) X(16) X(18) X(20) X(24) X(32) \
     X(48) X(64) X(96) X(128)
@@ -499,12 +516,7 @@ template <int NP>
 static void launch_join_np(const JoinArgs& a, uint64_t nitems, cudaStream_t s) {
     constexpr int T = NP <= 32 ? 128 : 64;
     size_t sm = join_smem_bytes(NP, a.L);
-    static bool attr = false;
-    if (!attr) {
-        KJ_CUDA(cudaFuncSetAttribute(k_join<NP, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     227 * 1024));
-        attr = true;
-    }
+    set_smem(k_join<NP, T>, sm);
     for (uint64_t off = 0; off < nitems; off += 2147483647ull) {
         uint64_t cnt = std::min<uint64_t>(nitems - off, 2147483647ull);
         JoinArgs b = a;
@@ -512,6 +524,7 @@ static void launch_join_np(const JoinArgs& a, uint64_t nitems, cudaStream_t s) {
         k_join<NP, T><<<dim3((unsigned)cnt), JB, sm, s>>>(b);
     }
     KJ_CUDA(cudaGetLastError());
+    g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
 void launch_join(const JoinArgs& a, uint64_t nitems, cudaStream_t s) {
@@ -531,6 +544,7 @@ void launch_finalize(const FinalArgs& a, cudaStream_t s) {
     uint64_t threads = a.nrows * 32;
     k_finalize<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(a);
     KJ_CUDA(cudaGetLastError());
+    g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
 size_t hist_smem_bytes(int np, uint32_t n_bins) {
@@ -543,15 +557,11 @@ template <int NP>
 static void launch_hist_np(const HistArgs& a, uint64_t n_slabs, cudaStream_t s) {
     constexpr int T = NP <= 32 ? 128 : 64;
     size_t sm = hist_smem_bytes(NP, a.n_bins);
-    static bool attr = false;
-    if (!attr) {
-        KJ_CUDA(cudaFuncSetAttribute(k_hist<NP, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     227 * 1024));
-        attr = true;
-    }
+    set_smem(k_hist<NP, T>, sm);
     dim3 grid((unsigned)((a.nq + JB - 1) / JB), (unsigned)n_slabs);
     k_hist<NP, T><<<grid, JB, sm, s>>>(a);
     KJ_CUDA(cudaGetLastError());
+    g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
 void launch_histogram(const HistArgs& a, uint64_t n_slabs, cudaStream_t s) {
@@ -576,6 +586,7 @@ void launch_check_finite(const double* X, uint64_t count, unsigned long long* fi
                          cudaStream_t s) {
     k_check_finite<<<1184, 256, 0, s>>>(X, count, first_bad);
     KJ_CUDA(cudaGetLastError());
+    g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
 // Column sums (mean == null) or sums of squared deviations, per row-block:
@@ -612,6 +623,7 @@ void launch_col_sums(const double* X, uint64_t N, uint32_t n, const double* mean
     dim3 grid(nblk, (n + 31) / 32), block(32, 8);
     k_col_sums<<<grid, block, 0, s>>>(X, N, n, mean, partial);
     KJ_CUDA(cudaGetLastError());
+    g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
 __global__ void k_permute_cols(const double* X0, double* X, uint64_t N, uint32_t n,
@@ -627,6 +639,7 @@ void launch_permute_cols(const double* X0, double* X, uint64_t N, uint32_t n,
                          const uint32_t* order, cudaStream_t s) {
     k_permute_cols<<<2368, 256, 0, s>>>(X0, X, N, n, order);
     KJ_CUDA(cudaGetLastError());
+    g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
 __global__ void k_to_float_soa(const double* X, uint64_t N, uint32_t n, const double* g,
@@ -653,6 +666,7 @@ void launch_to_float_soa(const double* X, uint64_t N, uint32_t n, const double* 
                          uint64_t Npad, unsigned long long* rmax_bits, cudaStream_t s) {
     k_to_float_soa<<<1184, 256, 0, s>>>(X, N, n, g, Xf, Npad, rmax_bits);
     KJ_CUDA(cudaGetLastError());
+    g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
 __global__ void k_pair_sq(const double* X, uint32_t n, const uint64_t* ij, uint64_t npairs,
@@ -669,6 +683,7 @@ void launch_pair_sq(const double* X, uint32_t n, const uint64_t* ij, uint64_t np
     k_pair_sq<<<(unsigned)std::min<uint64_t>(4736, (npairs + 255) / 256), 256, 0, s>>>(
         X, n, ij, npairs, limit, out);
     KJ_CUDA(cudaGetLastError());
+    g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
 __global__ void k_minmax(const double* X, uint64_t N, uint32_t n, uint32_t m,
@@ -697,6 +712,7 @@ void launch_minmax(const double* X, uint64_t N, uint32_t n, uint32_t m, unsigned
                    unsigned long long* mx, cudaStream_t s) {
     k_minmax<<<592, 256, 0, s>>>(X, N, n, m, mn, mx);
     KJ_CUDA(cudaGetLastError());
+    g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
 // grid_index.cpp:77-94 (cell_of + linearize), FP64 division and floor
@@ -722,6 +738,7 @@ void launch_cell_keys(const double* X, uint64_t N, uint32_t n, uint32_t m, const
                       uint32_t* vals, cudaStream_t s) {
     k_cell_keys<<<2368, 256, 0, s>>>(X, N, n, m, mins, w, cpd, strides, keys, vals);
     KJ_CUDA(cudaGetLastError());
+    g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
 __global__ void k_iota(uint32_t* v, uint64_t N) {
@@ -732,6 +749,7 @@ __global__ void k_iota(uint32_t* v, uint64_t N) {
 void launch_iota(uint32_t* v, uint64_t N, cudaStream_t s) {
     k_iota<<<1184, 256, 0, s>>>(v, N);
     KJ_CUDA(cudaGetLastError());
+    g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
 __global__ void k_head_flags(const uint64_t* keys, uint64_t N, uint32_t* flags) {
@@ -742,6 +760,7 @@ __global__ void k_head_flags(const uint64_t* keys, uint64_t N, uint32_t* flags) 
 void launch_head_flags(const uint64_t* keys, uint64_t N, uint32_t* flags, cudaStream_t s) {
     k_head_flags<<<1184, 256, 0, s>>>(keys, N, flags);
     KJ_CUDA(cudaGetLastError());
+    g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
 // runidx: inclusive scan of head flags (1-based run number)
@@ -766,6 +785,7 @@ void launch_grid_tables(const uint64_t* skeys, const uint32_t* A, const uint32_t
                         cudaStream_t s) {
     k_grid_tables<<<1184, 256, 0, s>>>(skeys, A, runidx, N, B, G, slot, posOf);
     KJ_CUDA(cudaGetLastError());
+    g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
 __global__ void k_gather_soa(const float* Xf, const uint32_t* A, uint64_t N, uint32_t n,
@@ -784,6 +804,7 @@ void launch_gather_soa(const float* Xf, const uint32_t* A, uint64_t N, uint32_t 
                        uint64_t Npad, float* Xs, cudaStream_t s) {
     k_gather_soa<<<2368, 256, 0, s>>>(Xf, A, N, n, Npad, Xs);
     KJ_CUDA(cudaGetLastError());
+    g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
 __global__ void k_map_u32(const uint32_t* idx, const uint32_t* table, uint64_t n, uint32_t* out) {
@@ -796,6 +817,7 @@ void launch_map_u32(const uint32_t* idx, const uint32_t* table, uint64_t n, uint
     if (!n) return;
     k_map_u32<<<1184, 256, 0, s>>>(idx, table, n, out);
     KJ_CUDA(cudaGetLastError());
+    g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
 __device__ __forceinline__ uint64_t lower_bound_u64(const uint64_t* a, uint64_t n, uint64_t key) {
@@ -891,6 +913,7 @@ void launch_adj_count(const uint64_t* B, uint64_t ncells, const uint32_t* cells,
     k_adj<false><<<(unsigned)((nc * 32 + 255) / 256), 256, 0, s>>>(
         B, nullptr, ncells, cells, nc, m, cpd, strides, counts, nullptr, nullptr, nullptr);
     KJ_CUDA(cudaGetLastError());
+    g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 void launch_adj_fill(const uint64_t* B, const uint2* G, uint64_t ncells, const uint32_t* cells,
                      uint64_t nc, uint32_t m, const uint64_t* cpd, const uint64_t* strides,
@@ -900,6 +923,7 @@ void launch_adj_fill(const uint64_t* B, const uint2* G, uint64_t ncells, const u
     k_adj<true><<<(unsigned)((nc * 32 + 255) / 256), 256, 0, s>>>(
         B, G, ncells, cells, nc, m, cpd, strides, nullptr, offs, adj, csize);
     KJ_CUDA(cudaGetLastError());
+    g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
 __global__ void k_items(const uint32_t* ufirst, const uint32_t* ucnt, const uint32_t* item_off,
@@ -923,6 +947,7 @@ void launch_items(const uint32_t* ufirst, const uint32_t* ucnt, const uint32_t* 
     if (!nuc) return;
     k_items<<<592, 256, 0, s>>>(ufirst, ucnt, item_off, adj_off, nuc, csize, items, work);
     KJ_CUDA(cudaGetLastError());
+    g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
 __global__ void k_cell_pop(const uint32_t* pids, uint64_t nq, const uint32_t* slot,
@@ -938,6 +963,7 @@ void launch_cell_pop(const uint32_t* pids, uint64_t nq, const uint32_t* slot, co
     if (!nq) return;
     k_cell_pop<<<1184, 256, 0, s>>>(pids, nq, slot, G, pop);
     KJ_CUDA(cudaGetLastError());
+    g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
 __global__ void k_fill_f32(float* p, uint64_t n, float v) {
@@ -949,6 +975,7 @@ void launch_fill_f32(float* p, uint64_t n, float v, cudaStream_t s) {
     if (!n) return;
     k_fill_f32<<<1184, 256, 0, s>>>(p, n, v);
     KJ_CUDA(cudaGetLastError());
+    g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
 // range_query sizes (self included) over a pass: block per item, warp per query.
@@ -976,6 +1003,7 @@ void launch_range_count(const double* X64, uint32_t n, const uint32_t* A, const 
     if (!nitems) return;
     k_range_count<<<(unsigned)nitems, 128, 0, s>>>(X64, n, A, qpos, items, adj, eps2, in_eps);
     KJ_CUDA(cudaGetLastError());
+    g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
 // Exact slow path for rows whose screened list overflowed (many exact ties):
@@ -1061,13 +1089,12 @@ void launch_slow_exact(const double* X64, uint32_t n, const uint32_t* A, const u
                        double* out_dist, double* out_kth, uint8_t* out_status, cudaStream_t s) {
     if (!nrows) return;
     size_t sm = (size_t)K * 32 * (sizeof(double) + sizeof(uint32_t));
-    if (sm > 227 * 1024) throw Error(1, "k too large for the exact slow path");
-    KJ_CUDA(cudaFuncSetAttribute(k_slow_exact, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 227 * 1024));
+    set_smem(k_slow_exact, sm);
     k_slow_exact<<<(unsigned)nrows, 32, sm, s>>>(X64, n, A, qpos, qrow, rows, nrows, items,
                                                  row_item, adj, K, eps2, cover2, out_ids,
                                                  out_dist, out_kth, out_status);
     KJ_CUDA(cudaGetLastError());
+    g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
 }  // namespace kj
@@ -1084,6 +1111,7 @@ void launch_row_item(const uint4* items, uint64_t nitems, uint32_t* row_item, cu
     if (!nitems) return;
     k_row_item<<<592, 256, 0, s>>>(items, nitems, row_item);
     KJ_CUDA(cudaGetLastError());
+    g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 }  // namespace kj
 
@@ -1099,17 +1127,61 @@ void launch_gather_u8(const uint32_t* idx, const uint8_t* table, uint64_t n, uin
     if (!n) return;
     k_gather<uint8_t><<<592, 256, 0, s>>>(idx, table, n, out);
     KJ_CUDA(cudaGetLastError());
+    g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 void launch_gather_f64(const uint32_t* idx, const double* table, uint64_t n, double* out,
                        cudaStream_t s) {
     if (!n) return;
     k_gather<double><<<592, 256, 0, s>>>(idx, table, n, out);
     KJ_CUDA(cudaGetLastError());
+    g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 void launch_gather_f32(const uint32_t* idx, const float* table, uint64_t n, float* out,
                        cudaStream_t s) {
     if (!n) return;
     k_gather<float><<<592, 256, 0, s>>>(idx, table, n, out);
     KJ_CUDA(cudaGetLastError());
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+}  // namespace kj
+
+namespace kj {
+// FP32 roofline denominator: 8 independent FFMA chains per thread, register
+// operands (the form the distance kernels issue), full-chip grid.
+__global__ void k_ffma_peak(float* out, int iters, float a, float b) {
+    float x0 = threadIdx.x, x1 = x0 + 1, x2 = x0 + 2, x3 = x0 + 3, x4 = x0 + 4, x5 = x0 + 5,
+          x6 = x0 + 6, x7 = x0 + 7;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+            x0 = fmaf(x0, a, b); x1 = fmaf(x1, a, b); x2 = fmaf(x2, a, b); x3 = fmaf(x3, a, b);
+            x4 = fmaf(x4, a, b); x5 = fmaf(x5, a, b); x6 = fmaf(x6, a, b); x7 = fmaf(x7, a, b);
+        }
+    }
+    float r = x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7;
+    if (r == 1234.5f) out[0] = r;
+}
+double measure_ffma_tflops(cudaStream_t s) {
+    int dev = 0, sms = 0;
+    KJ_CUDA(cudaGetDevice(&dev));
+    KJ_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    float* out = nullptr;
+    KJ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&out), 4, s));
+    const int blocks = sms * 8, threads = 256, iters = 4096;
+    cudaEvent_t a, b;
+    KJ_CUDA(cudaEventCreate(&a));
+    KJ_CUDA(cudaEventCreate(&b));
+    k_ffma_peak<<<blocks, threads, 0, s>>>(out, 64, 0.999f, 0.001f);  // warm-up
+    KJ_CUDA(cudaEventRecord(a, s));
+    k_ffma_peak<<<blocks, threads, 0, s>>>(out, iters, 0.999f, 0.001f);
+    KJ_CUDA(cudaEventRecord(b, s));
+    KJ_CUDA(cudaEventSynchronize(b));
+    float ms = 0;
+    KJ_CUDA(cudaEventElapsedTime(&ms, a, b));
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFreeAsync(out, s);
+    const double flops = 2.0 * 8 * 16 * double(iters) * blocks * threads;
+    return flops / (ms * 1e-3) / 1e12;
 }
 }  // namespace kj
