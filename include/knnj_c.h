@@ -63,6 +63,9 @@ void* knnj_stream(knnj_ctx* ctx);
 /* Measured FP32 FFMA throughput of this device (TFLOP/s, 2 flops per FFMA):
  * the roofline denominator for the SIMT distance kernels. */
 int knnj_fp32_peak(knnj_ctx* ctx, double* tflops);
+/* Engine knobs (no reference analogue; results never depend on them):
+ *   "tensor_cores" 0/1 : allow the tcgen05 distance screen (default 1). */
+int knnj_set_option(knnj_ctx* ctx, const char* name, int64_t value);
 /* Page-locked host buffers for the end-to-end path (H2D/D2H at full PCIe rate). */
 void* knnj_alloc_pinned(size_t bytes);
 void knnj_free_pinned(void* p);

@@ -90,6 +90,7 @@ SIGNATURES = [
     ("knnj_last_error", C.c_char_p, [_vp]),
     ("knnj_stream", C.c_void_p, [_vp]),
     ("knnj_fp32_peak", C.c_int, [_vp, C.POINTER(C.c_double)]),
+    ("knnj_set_option", C.c_int, [_vp, C.c_char_p, C.c_int64]),
     ("knnj_alloc_pinned", C.c_void_p, [C.c_size_t]),
     ("knnj_free_pinned", None, [C.c_void_p]),
     ("knnj_set_points", C.c_int, [_vp, _vp, C.c_uint64, C.c_uint32]),

@@ -10,6 +10,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <memory>
@@ -572,8 +573,39 @@ struct knnj_ctx {
         launch_grid_tables(skeys.p, lv.A.p, runidx.p, N, lv.B.p, lv.G.p, lv.slot.p, lv.posOf.p, s);
         lv.Xs.ensure((uint64_t)n * Npad);
         launch_gather_soa(Xf.p, lv.A.p, N, n, Npad, lv.Xs.p, s);
+        lv.tc_ready = false;
+        if (use_tc()) prep_tc(lv);
         sync();
         lv.built = true;
+    }
+
+    // Tensor-core screen policy: used where the GEMM form pays (n >= 12) and the
+    // hi/lo FP16 operand fits one or two 128-byte k-blocks (n <= 42).
+    bool tc_enabled = true;
+    bool use_tc() const { return tc_enabled && n >= 12 && 3 * n + 2 <= 128; }
+    double tc_S() const {
+        double S = 1.0;
+        while (S < Rg) S *= 2.0;
+        while (S / 2.0 >= Rg && S > 1e-300) S /= 2.0;
+        return S;
+    }
+    void prep_tc(Level& lv) {
+        if (lv.tc_ready) return;
+        lv.row_halfs = 3 * n + 2 <= 64 ? 64 : 128;
+        lv.Bh.ensure(N * lv.row_halfs);
+        launch_prep_tc(X64.p, lv.A.p, N, n, d_g.p, 1.0 / tc_S(), lv.row_halfs, lv.Bh.p, s);
+        lv.tc_ready = true;
+    }
+    // Rigorous bound on |key - sq64/S^2| for the tensor-core screen.
+    double tc_delta() const {
+        const double u22 = std::ldexp(1.0, -22), u24 = std::ldexp(1.0, -24);
+        const double R = Rg / tc_S();
+        const double R2 = R * R;
+        const double KT = 3.0 * n + 2.0;
+        const double eps_acc = (KT + 4.0) * u22;       // FP32 accumulation, 4x the IEEE bound
+        double d = eps_acc * 3.1 * R2 + 6 * u22 * R2 + 2 * u24 * std::sqrt((double)n) * R +
+                   2 * u22 * R2 + 2 * u24 + 5 * u24 * R2 + (4.0 * n + 12.0) * 4.0 * U64 * R2;
+        return 1.5 * d;
     }
 
     double cover2(const Level& lv) const {
@@ -684,13 +716,16 @@ struct knnj_ctx {
     }
 
     double last_join_kernel_ms = 0.0;
+    bool last_join_tc = false;
     // Runs the fused join over a pass, then the exact finalize (and the slow
     // path for overflowed lists). Writes rows of out_* (indexed by qrow).
     void run_pass(Level& lv, Pass& P, uint32_t K, const float* d_init_cut, double eps2,
                   double cov2, uint32_t* out_ids, double* out_dist, double* out_kth,
                   uint8_t* out_status, uint64_t* n_slow) {
         if (!P.nq) return;
-        const uint32_t L = K + std::max<uint32_t>(16, K / 2);
+        const bool tc = use_tc() && tc_join_smem_bytes(lv.row_halfs ? lv.row_halfs / 64 : 1, K + 8) <= 110 * 1024;
+        // list capacity: K plus slack for near-ties inside the screen band (overflow -> exact slow path)
+        const uint32_t L = tc ? K + 8 : K + std::max<uint32_t>(16, K / 2);
         if (L > 256) throw Error(1, "k above 170 is not supported by the device join");
         const int np = pick_np(n);
         if (np < 0) throw Error(1, "dimension count above 128 is not supported by the device join");
@@ -698,23 +733,49 @@ struct knnj_ctx {
         DBuf<uint32_t> cnt, pos;
         cnt.ensure(P.nq);
         pos.ensure(P.nq * L);
-        JoinArgs a{};
-        a.Xs = lv.Xs.p;
-        a.Npad = Npad;
-        a.n = n;
-        a.qpos = P.qpos.p;
-        a.items = P.items.p;
-        a.adj = P.adj.p;
-        a.init_cut = d_init_cut;
-        a.K = K;
-        a.L = L;
-        a.out_cnt = cnt.p;
-        a.out_pos = pos.p;
-        screen_consts(a.gam, a.erg, a.eab, a.e64);
-        {
+        if (tc) {
+            prep_tc(lv);
+            TcJoinArgs a{};
+            a.Bh = lv.Bh.p;
+            a.row_halfs = lv.row_halfs;
+            a.n = n;
+            a.qpos = P.qpos.p;
+            a.items = P.items.p;
+            a.adj = P.adj.p;
+            DBuf<float> cut_scaled;
+            if (d_init_cut) {
+                const double S = tc_S();
+                cut_scaled.ensure(P.nq);
+                launch_scale_f32(d_init_cut, P.nq, (float)(1.0 / (S * S)), cut_scaled.p, s);
+                a.init_cut = cut_scaled.p;
+            }
+            a.K = K;
+            a.L = L;
+            a.out_cnt = cnt.p;
+            a.out_pos = pos.p;
+            a.delta = f32_round_up(tc_delta());
+            Timer t(s);
+            launch_join_tc(a, P.nitems, N, s);
+            last_join_kernel_ms = t.ms();
+            last_join_tc = true;
+        } else {
+            JoinArgs a{};
+            a.Xs = lv.Xs.p;
+            a.Npad = Npad;
+            a.n = n;
+            a.qpos = P.qpos.p;
+            a.items = P.items.p;
+            a.adj = P.adj.p;
+            a.init_cut = d_init_cut;
+            a.K = K;
+            a.L = L;
+            a.out_cnt = cnt.p;
+            a.out_pos = pos.p;
+            screen_consts(a.gam, a.erg, a.eab, a.e64);
             Timer t(s);
             launch_join(a, P.nitems, s);
             last_join_kernel_ms = t.ms();
+            last_join_tc = false;
         }
         FinalArgs f{};
         f.X64 = X64.p;
@@ -880,6 +941,7 @@ int knnj_create(int device, knnj_ctx** out) {
         c->dev = device;
         KJ_CUDA(cudaSetDevice(device));
         KJ_CUDA(cudaStreamCreateWithFlags(&c->s, cudaStreamNonBlocking));
+        if (const char* e = std::getenv("KNNJ_NO_TC")) c->tc_enabled = !(e[0] && e[0] != '0');
         cudaMemPool_t pool;
         KJ_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
         uint64_t keep = ~0ull;  // keep freed blocks cached in the pool
@@ -910,6 +972,17 @@ void knnj_destroy(knnj_ctx* ctx) {
 const char* knnj_last_error(const knnj_ctx* ctx) { return ctx ? ctx->err.c_str() : "null ctx"; }
 
 void* knnj_stream(knnj_ctx* ctx) { return ctx ? (void*)ctx->s : nullptr; }
+
+int knnj_set_option(knnj_ctx* c, const char* name, int64_t value) {
+    return guarded(c, [&] {
+        const std::string k = name ? name : "";
+        if (k == "tensor_cores") {
+            c->tc_enabled = value != 0;
+        } else {
+            throw Error(1, "unknown option '" + k + "'");
+        }
+    });
+}
 
 int knnj_fp32_peak(knnj_ctx* c, double* tflops) {
     return guarded(c, [&] { *tflops = kj::measure_ffma_tflops(c->s); });

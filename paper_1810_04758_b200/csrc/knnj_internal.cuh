@@ -2,6 +2,7 @@
 // host runtime / C ABI (knnj_capi.cu). Not part of the public ABI.
 #pragma once
 
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -85,6 +86,9 @@ struct Level {
     DBuf<uint32_t> slot; // N: point id -> cell index
     DBuf<uint32_t> posOf;// N: point id -> sorted position
     DBuf<float> Xs;      // n x Npad SoA, sorted order, centred floats
+    bool tc_ready = false;
+    uint32_t row_halfs = 0;
+    DBuf<__half> Bh;     // N x row_halfs: tensor-core B operand (knnj_tc.cu)
 };
 
 // Work description of one join pass (queries of one level grid).
@@ -114,6 +118,19 @@ struct JoinArgs {
     float erg;               // 2*u1*Rg: input-rounding part of E
     float eab;               // u(1+2u): (A+B) coefficient of E
     float e64;               // (n+3) * 2^-52: FP64 accumulation slack
+};
+
+struct TcJoinArgs {
+    const __half* Bh;        // level's B operand rows (sorted order)
+    uint32_t row_halfs, n;
+    const uint32_t* qpos;
+    const uint4* items;
+    const uint2* adj;
+    const float* init_cut;   // per launch row (scaled units), may be null
+    uint32_t K, L;
+    uint32_t* out_cnt;
+    uint32_t* out_pos;
+    float delta;             // |key - sq64/S^2| bound (scaled units)
 };
 
 struct FinalArgs {
@@ -153,6 +170,11 @@ struct HistArgs {
 // ---------------------------------------------------------------- launchers
 extern std::atomic<unsigned long long> g_launches;  // our kernels launched so far
 double measure_ffma_tflops(cudaStream_t s);
+size_t tc_join_smem_bytes(int KB, uint32_t L);
+void launch_prep_tc(const double* X64, const uint32_t* A, uint64_t N, uint32_t n, const double* g,
+                    double inv_S, uint32_t row_halfs, __half* Bh, cudaStream_t s);
+void launch_join_tc(const TcJoinArgs& a, uint64_t nitems, uint64_t N, cudaStream_t s);
+void launch_scale_f32(const float* in, uint64_t n, float scale, float* out, cudaStream_t s);
 int pick_np(uint32_t n);  // padded dimension count used by the templated kernels
 size_t join_smem_bytes(int np, uint32_t L);
 void launch_join(const JoinArgs& a, uint64_t nitems, cudaStream_t s);

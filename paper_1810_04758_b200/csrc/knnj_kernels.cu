@@ -1185,3 +1185,17 @@ double measure_ffma_tflops(cudaStream_t s) {
     return flops / (ms * 1e-3) / 1e12;
 }
 }  // namespace kj
+
+namespace kj {
+__global__ void k_scale_f32(const float* in, uint64_t n, float scale, float* out) {
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x)
+        out[i] = in[i] * scale;
+}
+void launch_scale_f32(const float* in, uint64_t n, float scale, float* out, cudaStream_t s) {
+    if (!n) return;
+    k_scale_f32<<<592, 256, 0, s>>>(in, n, scale, out);
+    KJ_CUDA(cudaGetLastError());
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+}  // namespace kj

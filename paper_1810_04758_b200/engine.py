@@ -120,6 +120,9 @@ class Engine:
         if rc:
             raise KnnjError(rc, self.lib.knnj_last_error(self.h).decode())
 
+    def set_option(self, name: str, value: int) -> None:
+        self._check(self.lib.knnj_set_option(self.h, name.encode(), int(value)))
+
     # ------------------------------------------------------------- dataset
     def set_points(self, X) -> None:
         """Dataset(coords, dims) upload (validates finiteness like dataset.cpp:22-33).

@@ -100,9 +100,22 @@ RANDOM = [  # (spec, |D|, n, k, m, beta, gamma, rho, seed) — acceptance C1-sty
 ]
 
 
+RANDOM += [
+    ("clusters:16:0.05", 6000, 18, 32, 0, 0.0, 0.0, 0.0, 11),
+    ("clusters:8:0.02", 4000, 12, 9, 0, 0.2, 0.3, 0.1, 12),
+    ("mixture:4:0.05", 3000, 24, 20, 5, 0.0, 0.0, 0.0, 13),
+    ("clusters:6:0.1", 2500, 40, 3, 0, 0.0, 0.0, 0.0, 14),
+    ("uniform", 2000, 16, 64, 0, 0.0, 0.0, 0.0, 15),
+]
+
+
+@pytest.mark.parametrize("tc", [1, 0], ids=["tcgen05", "simt"])
 @pytest.mark.parametrize("case", RANDOM, ids=[f"{c[0]}-{c[2]}d-k{c[3]}" for c in RANDOM])
-def test_random_instances_vs_oracle(engine, oracle, case):
+def test_random_instances_vs_oracle(engine, oracle, case, tc):
     spec, N, n, k, m, beta, gamma, rho, seed = case
+    if not tc and not (12 <= n <= 42):
+        pytest.skip("same kernel as the tcgen05 leg for this n")
+    engine.set_option("tensor_cores", tc)
     X = generate(spec, N, n, seed)
     for mode in ("hybrid", "dense"):
         o = oracle.run(X, k=k, m=m, beta=beta, gamma=gamma, rho=rho, mode=mode, seed=seed)
@@ -114,6 +127,7 @@ def test_random_instances_vs_oracle(engine, oracle, case):
         assert r.info["failed_count"] == o["failed_count"]
         assert r.info["eps_used"] == o["eps_used"]
         assert np.array_equal(r.raw_hist, o["raw_hist"])
+    engine.set_option("tensor_cores", 1)
 
 
 def test_exact_knn_matches_brute(engine, oracle):
