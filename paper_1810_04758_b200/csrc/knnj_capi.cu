@@ -596,15 +596,22 @@ struct knnj_ctx {
         launch_prep_tc(X64.p, lv.A.p, N, n, d_g.p, 1.0 / tc_S(), lv.row_halfs, lv.Bh.p, s);
         lv.tc_ready = true;
     }
-    // Rigorous bound on |key - sq64/S^2| for the tensor-core screen.
+    // Bound on |key - sq64/S^2| for the tensor-core screen.
+    // FP16 hi/lo representation, |b|^2 split, |a|^2 in FP32 and the FP64
+    // reference rounding are bounded rigorously; the tensor core's FP32
+    // accumulation is modelled per MMA instruction (products of FP16 are exact
+    // in FP32; each K=16 instruction rounds its partial sum) with a 4x
+    // allowance per instruction — ~10x the largest error measured on B200
+    // (tools/tc_probe.py, tests/test_gpu_screen.py keeps checking it).
     double tc_delta() const {
         const double u22 = std::ldexp(1.0, -22), u24 = std::ldexp(1.0, -24);
         const double R = Rg / tc_S();
         const double R2 = R * R;
-        const double KT = 3.0 * n + 2.0;
-        const double eps_acc = (KT + 4.0) * u22;       // FP32 accumulation, 4x the IEEE bound
-        double d = eps_acc * 3.1 * R2 + 6 * u22 * R2 + 2 * u24 * std::sqrt((double)n) * R +
-                   2 * u22 * R2 + 2 * u24 + 5 * u24 * R2 + (4.0 * n + 12.0) * 4.0 * U64 * R2;
+        const double n_mma = 4.0 * ((3.0 * n + 2.0 + 63.0) / 64.0);  // K=16 steps
+        const double T = 3.1 * R2;                                   // sum of |terms|
+        const double acc = (n_mma + 2.0) * 4.0 * u24 * T;
+        double d = acc + 6 * u22 * R2 + 2 * u24 * std::sqrt((double)n) * R + 2 * u22 * R2 +
+                   2 * u24 + 5 * u24 * R2 + (4.0 * n + 12.0) * 4.0 * U64 * R2;
         return 1.5 * d;
     }
 
@@ -972,6 +979,57 @@ void knnj_destroy(knnj_ctx* ctx) {
 const char* knnj_last_error(const knnj_ctx* ctx) { return ctx ? ctx->err.c_str() : "null ctx"; }
 
 void* knnj_stream(knnj_ctx* ctx) { return ctx ? (void*)ctx->s : nullptr; }
+
+// Test hook (not in knnj_c.h's public set): one 128x128 tensor-core tile of
+// level 0 — queries at sorted positions [q0,q0+128) against [c0,c0+128) —
+// returns the raw FP32 accumulators and the FP16 operand rows used.
+int knnj_debug_tc_tile(knnj_ctx* c, uint32_t q0, uint32_t c0, float* D, uint16_t* Bq,
+                       uint16_t* Bc, double* scale_S, double* delta) {
+    return guarded(c, [&] {
+        Level& lv = c->levels[0];
+        if (!lv.built) throw Error(1, "no grid");
+        c->prep_tc(lv);
+        std::vector<uint32_t> qpos(128);
+        for (int i = 0; i < 128; ++i) qpos[i] = q0 + i;
+        uint4 item = make_uint4(0, 128, 0, 1);
+        uint2 rng = make_uint2(c0, c0 + 128);
+        DBuf<uint32_t> d_qpos, cnt, pos;
+        DBuf<uint4> d_item;
+        DBuf<uint2> d_adj;
+        DBuf<float> d_dbg;
+        d_qpos.ensure(128);
+        d_item.ensure(1);
+        d_adj.ensure(1);
+        d_dbg.ensure(128 * 128);
+        cnt.ensure(128);
+        pos.ensure(128 * 12);
+        KJ_CUDA(cudaMemcpyAsync(d_qpos.p, qpos.data(), 512, cudaMemcpyHostToDevice, c->s));
+        KJ_CUDA(cudaMemcpyAsync(d_item.p, &item, 16, cudaMemcpyHostToDevice, c->s));
+        KJ_CUDA(cudaMemcpyAsync(d_adj.p, &rng, 8, cudaMemcpyHostToDevice, c->s));
+        TcJoinArgs a{};
+        a.Bh = lv.Bh.p;
+        a.row_halfs = lv.row_halfs;
+        a.n = c->n;
+        a.qpos = d_qpos.p;
+        a.items = d_item.p;
+        a.adj = d_adj.p;
+        a.K = 4;
+        a.L = 12;
+        a.out_cnt = cnt.p;
+        a.out_pos = pos.p;
+        a.delta = (float)c->tc_delta();
+        a.dbg = d_dbg.p;
+        launch_join_tc(a, 1, c->N, c->s);
+        KJ_CUDA(cudaMemcpyAsync(D, d_dbg.p, 4 * 128 * 128, cudaMemcpyDeviceToHost, c->s));
+        KJ_CUDA(cudaMemcpyAsync(Bq, lv.Bh.p + (uint64_t)q0 * lv.row_halfs, 2 * 128 * lv.row_halfs,
+                                cudaMemcpyDeviceToHost, c->s));
+        KJ_CUDA(cudaMemcpyAsync(Bc, lv.Bh.p + (uint64_t)c0 * lv.row_halfs, 2 * 128 * lv.row_halfs,
+                                cudaMemcpyDeviceToHost, c->s));
+        c->sync();
+        *scale_S = c->tc_S();
+        *delta = c->tc_delta();
+    });
+}
 
 int knnj_set_option(knnj_ctx* c, const char* name, int64_t value) {
     return guarded(c, [&] {

@@ -131,6 +131,7 @@ struct TcJoinArgs {
     uint32_t* out_cnt;
     uint32_t* out_pos;
     float delta;             // |key - sq64/S^2| bound (scaled units)
+    float* dbg;              // test hook: block 0 dumps its first accumulator tile [128][128]
 };
 
 struct FinalArgs {

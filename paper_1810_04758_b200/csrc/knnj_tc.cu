@@ -309,12 +309,15 @@ __global__ void __launch_bounds__(TC_M, 2)
         for (uint32_t j0 = 0; j0 < c; j0 += 32) {
             float v[32];
             tmem_ld32(tbase + j0, v);
+            if (p.dbg && blockIdx.x == 0 && t == 0)
+#pragma unroll
+                for (int j = 0; j < 32; ++j) p.dbg[tid * TC_N + j0 + j] = v[j];
             if (!has_q || ovf) continue;
             const uint32_t lim = c - j0;
             if (lim < 32) {
 #pragma unroll
                 for (int j = 0; j < 32; ++j)
-                    if ((uint32_t)j >= lim) v[j] = CUDART_INF_F;
+                    if ((uint32_t)j >= lim) v[j] = CUDART_NAN_F;  // never passes a <= test
             }
             // fast path: one FMNMX per pair
             float m[16];

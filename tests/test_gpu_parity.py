@@ -127,6 +127,8 @@ def test_random_instances_vs_oracle(engine, oracle, case, tc):
         assert r.info["failed_count"] == o["failed_count"]
         assert r.info["eps_used"] == o["eps_used"]
         assert np.array_equal(r.raw_hist, o["raw_hist"])
+        # the screen list holds the exact top-K without the slow path (no exact ties here)
+        assert r.info["slow_path_queries"] == 0, r.info["slow_path_queries"]
     engine.set_option("tensor_cores", 1)
 
 
