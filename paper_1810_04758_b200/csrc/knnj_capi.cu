@@ -250,6 +250,7 @@ struct knnj_ctx {
         Rg = std::sqrt(r2) * (1.0 + 1e-12);
         perm = order;
         working_ready = true;
+        bh_id_ready = false;  // FP16 operands derive from the working coordinates
         for (auto& lv : levels) lv.built = false;
     }
 
@@ -461,6 +462,14 @@ struct knnj_ctx {
         a.inv_width = inv_width;
         a.counts = d_cnt.p;
         screen_consts(a.gam, a.erg, a.eab, a.e64);
+        if (use_tc() && tc_smem_bytes(3 * n + 2 <= 64 ? 64 : 128, 0, nb, true) <= 227 * 1024) {
+            histogram_tc(d_q.p, nq, em, nb, S, d_cnt.p);
+            std::vector<unsigned long long> c(nb);
+            KJ_CUDA(cudaMemcpyAsync(c.data(), d_cnt.p, 8 * nb, cudaMemcpyDeviceToHost, s));
+            sync();
+            for (uint32_t b = 0; b < nb; ++b) raw[b] += c[b];
+            return;
+        }
         const int np = pick_np(n);
         const uint64_t T = np <= 32 ? 128 : 64;
         const uint64_t qblocks = (nq + JB - 1) / JB;
@@ -478,6 +487,77 @@ struct knnj_ctx {
         KJ_CUDA(cudaMemcpyAsync(c.data(), d_cnt.p, 8 * nb, cudaMemcpyDeviceToHost, s));
         last_hist_kernel_ms = t.ms();
         for (uint32_t b = 0; b < nb; ++b) raw[b] += c[b];
+    }
+
+    // Tensor-core histogram: sampled queries x all points (id order) on the
+    // tcgen05 GEMM-form screen, exact-certain binning (knnj_tc.cu, HIST epilogue).
+    DBuf<__half> Bh_id;
+    bool bh_id_ready = false;
+    uint32_t bh_id_row = 0;
+    void histogram_tc(const uint32_t* d_q, uint64_t nq, double em, uint32_t nb,
+                      const std::vector<double>& S_thr, unsigned long long* d_cnt) {
+        const uint32_t row_halfs = 3 * n + 2 <= 64 ? 64 : 128;
+        if (!bh_id_ready || bh_id_row != row_halfs) {
+            DBuf<uint32_t> ident;
+            ident.ensure(N);
+            launch_iota(ident.p, N, s);
+            Bh_id.ensure(N * row_halfs);
+            launch_prep_tc(X64.p, ident.p, N, n, d_g.p, 1.0 / tc_S(), row_halfs, Bh_id.p, s);
+            bh_id_ready = true;
+            bh_id_row = row_halfs;
+        }
+        const double Ssc = tc_S(), S2 = Ssc * Ssc;
+        const double width = em / double(nb);
+        std::vector<float> tab(2 * (nb + 1));
+        tab[0] = -std::numeric_limits<float>::infinity();
+        for (uint32_t b = 1; b <= nb; ++b) tab[b] = f32_round_up(S_thr[b] / S2);
+        for (uint32_t b = 0; b < nb; ++b) tab[nb + 1 + b] = f32_round_down(S_thr[b + 1] / S2);
+        tab[nb + 1 + nb] = tab[nb];
+        DBuf<float> d_tab;
+        d_tab.ensure(tab.size());
+        KJ_CUDA(cudaMemcpyAsync(d_tab.p, tab.data(), 4 * tab.size(), cudaMemcpyHostToDevice, s));
+        const uint32_t NQ = tc_queries_per_item(row_halfs);
+        const uint64_t qblocks = (nq + NQ - 1) / NQ;
+        uint64_t slabs = std::max<uint64_t>(1, (148ull * 8 + qblocks - 1) / qblocks);
+        uint64_t stride = (N + slabs - 1) / slabs;
+        stride = ((stride + 127) / 128) * 128;
+        slabs = (N + stride - 1) / stride;
+        std::vector<uint4> items;
+        items.reserve(qblocks * slabs);
+        std::vector<uint2> adj(slabs);
+        for (uint64_t sl = 0; sl < slabs; ++sl)
+            adj[sl] = make_uint2((uint32_t)(sl * stride), (uint32_t)std::min<uint64_t>(N, (sl + 1) * stride));
+        for (uint64_t qb = 0; qb < qblocks; ++qb)
+            for (uint64_t sl = 0; sl < slabs; ++sl)
+                items.push_back(make_uint4((uint32_t)(qb * NQ), (uint32_t)std::min<uint64_t>(nq, (qb + 1) * NQ),
+                                           (uint32_t)sl, (uint32_t)sl + 1));
+        DBuf<uint4> d_items;
+        DBuf<uint2> d_adj;
+        d_items.ensure(items.size());
+        d_adj.ensure(adj.size());
+        KJ_CUDA(cudaMemcpyAsync(d_items.p, items.data(), 16 * items.size(), cudaMemcpyHostToDevice, s));
+        KJ_CUDA(cudaMemcpyAsync(d_adj.p, adj.data(), 8 * adj.size(), cudaMemcpyHostToDevice, s));
+        TcJoinArgs a{};
+        a.Bh = Bh_id.p;
+        a.row_halfs = row_halfs;
+        a.n = n;
+        a.qpos = d_q;
+        a.items = d_items.p;
+        a.adj = d_adj.p;
+        a.K = 1;
+        a.L = 1;
+        a.delta = f32_round_up(tc_delta());
+        a.n_bins = nb;
+        a.tables = d_tab.p;
+        a.inv_width_scaled = (float)(Ssc / width);
+        a.X64 = X64.p;
+        a.eps_mean = em;
+        a.limit_sq = em * em;
+        a.inv_width = 1.0 / width;
+        a.counts = d_cnt;
+        Timer t(s);
+        launch_hist_tc(a, items.size(), N, s);
+        last_hist_kernel_ms = t.ms();
     }
 
     std::vector<uint64_t> histogram_sample(double frac, uint64_t seed) {
@@ -630,9 +710,21 @@ struct knnj_ctx {
     // ------------------------------------------------------------ passes
     // Groups the queries (point ids + output rows, on device) by their cell in
     // level lv and builds work items + candidate ranges.
+    // the join kernel a pass will run on (decided before its items are built)
+    bool pass_uses_tc(const Level& lv, uint32_t K) const {
+        const uint32_t rh = 3 * n + 2 <= 64 ? 64 : 128;
+        return use_tc() && tc_smem_bytes(lv.row_halfs ? lv.row_halfs : rh, K + 8, 0, false) <=
+                               227 * 1024;
+    }
+    uint32_t pass_chunk(const Level& lv, uint32_t K) const {
+        return pass_uses_tc(lv, K) ? tc_queries_per_item(lv.row_halfs ? lv.row_halfs : 64)
+                                   : (uint32_t)JB;
+    }
     void build_pass(Level& lv, const uint32_t* d_qpid, const uint32_t* d_qrow, uint64_t nq,
-                    Pass& P) {
+                    Pass& P, uint32_t K = 0) {
         P.nq = nq;
+        const uint32_t chunk = K ? pass_chunk(lv, K) : (uint32_t)JB;
+        P.chunk = chunk;
         P.nitems = P.nadj = P.candidates = 0;
         if (!nq) return;
         DBuf<uint32_t> pos_unsorted, qcell;
@@ -668,7 +760,7 @@ struct knnj_ctx {
         uint64_t tot = 0;
         for (uint64_t u = 0; u < nuc; ++u) {
             h_ioff[u] = (uint32_t)tot;
-            tot += (h_cnt[u] + JB - 1) / JB;
+            tot += (h_cnt[u] + chunk - 1) / chunk;
         }
         h_ioff[nuc] = (uint32_t)tot;
         P.nitems = tot;
@@ -699,7 +791,7 @@ struct knnj_ctx {
         items_unsorted.ensure(tot);
         work.ensure(tot);
         launch_items(ufirst.p, ucnt.p, item_off.p, adj_off.p, nuc, csize.p, items_unsorted.p,
-                     work.p, s);
+                     work.p, chunk, s);
         d_tot.ensure(1);
         reduce_sum(sc, work.p, d_tot.p, tot, s);
         unsigned long long cand = 0;
@@ -730,7 +822,8 @@ struct knnj_ctx {
                   double cov2, uint32_t* out_ids, double* out_dist, double* out_kth,
                   uint8_t* out_status, uint64_t* n_slow) {
         if (!P.nq) return;
-        const bool tc = use_tc() && tc_join_smem_bytes(lv.row_halfs ? lv.row_halfs / 64 : 1, K + 8) <= 110 * 1024;
+        const bool tc = pass_uses_tc(lv, K) && P.chunk == tc_queries_per_item(lv.row_halfs);
+        if (!tc && P.chunk != (uint32_t)JB) throw Error(9, "pass built for a different kernel");
         // list capacity: K plus slack for near-ties inside the screen band (overflow -> exact slow path)
         const uint32_t L = tc ? K + 8 : K + std::max<uint32_t>(16, K / 2);
         if (L > 256) throw Error(1, "k above 170 is not supported by the device join");
@@ -879,7 +972,7 @@ struct knnj_ctx {
             KJ_CUDA(cudaMemcpyAsync(d_cut_by_row.p, h_cut.data(), 4 * nrows_total,
                                     cudaMemcpyHostToDevice, s));
             Pass P;
-            build_pass(lv, d_p.p, d_r.p, np, P);
+            build_pass(lv, d_p.p, d_r.p, np, P, K);
             launch_gather_f32(P.qrow.p, d_cut_by_row.p, np, d_cut.p, s);
             run_pass(lv, P, K, d_cut.p, -1.0, cov2, out_ids, out_dist, out_kth, out_status, n_slow);
             if (passes) ++*passes;
@@ -1063,6 +1156,7 @@ int knnj_set_points(knnj_ctx* c, const double* X, uint64_t N, uint32_t n) {
         c->N = N;
         c->n = n;
         c->have_points = c->working_ready = false;
+        c->bh_id_ready = false;
         for (auto& lv : c->levels) lv.built = false;
         c->X0.ensure(N * n);
         KJ_CUDA(cudaMemcpyAsync(c->X0.p, X, N * n * 8, cudaMemcpyHostToDevice, c->s));
@@ -1303,7 +1397,7 @@ int knnj_dense_join(knnj_ctx* c, const uint32_t* q, uint64_t nq, uint32_t k, uin
         KJ_CUDA(cudaMemcpyAsync(d_q.p, q, 4 * nq, cudaMemcpyHostToDevice, c->s));
         KJ_CUDA(cudaMemcpyAsync(d_r.p, rows.data(), 4 * nq, cudaMemcpyHostToDevice, c->s));
         Pass P;
-        c->build_pass(lv, d_q.p, d_r.p, nq, P);
+        c->build_pass(lv, d_q.p, d_r.p, nq, P, k);
         uint64_t nslow = 0;
         c->run_pass(lv, P, k, nullptr, c->eps0 * c->eps0, c->cover2(lv), o_ids.p, o_dist.p,
                     o_kth.p, o_st.p, &nslow);
@@ -1592,7 +1686,7 @@ int knnj_run(knnj_ctx* c, const knnj_config* cfg, uint32_t* ids, double* dist, u
             {
                 Timer t(c->s);
                 Pass P;
-                c->build_pass(lv0, d_q.p, d_rows.p, nq, P);
+                c->build_pass(lv0, d_q.p, d_rows.p, nq, P, k_eff);
                 c->run_pass(lv0, P, k_eff, nullptr, eps * eps, c->cover2(lv0), o_ids.p, o_dist.p,
                             o_kth.p, o_st.p, &slow);
                 I.ms_join = t.ms();

@@ -97,6 +97,7 @@ struct Pass {
     uint64_t nitems = 0;
     uint64_t nadj = 0;
     uint64_t candidates = 0;  // sum over queries of candidate-set size
+    uint32_t chunk = 128;     // queries per work item
     DBuf<uint32_t> qpos;      // nq: sorted positions of the queries (grouped by cell)
     DBuf<uint32_t> qrow;      // nq: output row of each query
     DBuf<uint4> items;        // nitems: qbeg, qend, abeg, aend
@@ -132,6 +133,13 @@ struct TcJoinArgs {
     uint32_t* out_pos;
     float delta;             // |key - sq64/S^2| bound (scaled units)
     float* dbg;              // test hook: block 0 dumps its first accumulator tile [128][128]
+    // histogram epilogue (HIST kernels only)
+    uint32_t n_bins;
+    const float* tables;     // LO[n_bins+1], HI[n_bins+1] in scaled units
+    float inv_width_scaled;  // S / bin_width
+    const double* X64;
+    double eps_mean, limit_sq, inv_width;
+    unsigned long long* counts;
 };
 
 struct FinalArgs {
@@ -172,6 +180,9 @@ struct HistArgs {
 extern std::atomic<unsigned long long> g_launches;  // our kernels launched so far
 double measure_ffma_tflops(cudaStream_t s);
 size_t tc_join_smem_bytes(int KB, uint32_t L);
+size_t tc_smem_bytes(uint32_t row_halfs, uint32_t L, uint32_t n_bins, bool hist);
+uint32_t tc_queries_per_item(uint32_t row_halfs);
+void launch_hist_tc(const TcJoinArgs& a, uint64_t nitems, uint64_t N, cudaStream_t s);
 void launch_prep_tc(const double* X64, const uint32_t* A, uint64_t N, uint32_t n, const double* g,
                     double inv_S, uint32_t row_halfs, __half* Bh, cudaStream_t s);
 void launch_join_tc(const TcJoinArgs& a, uint64_t nitems, uint64_t N, cudaStream_t s);
@@ -214,10 +225,9 @@ void launch_adj_fill(const uint64_t* B, const uint2* G, uint64_t ncells, const u
                      uint64_t nc, uint32_t m, const uint64_t* cpd, const uint64_t* strides,
                      const uint32_t* offs, uint2* adj, unsigned long long* csize,
                      cudaStream_t s);
-void launch_items(const uint32_t* ucell_first, const uint32_t* ucell_cnt,
-                  const uint32_t* item_off, const uint32_t* adj_off, uint64_t nuc,
-                  const unsigned long long* csize, uint4* items,
-                  unsigned long long* work, cudaStream_t s);
+void launch_items(const uint32_t* ufirst, const uint32_t* ucnt, const uint32_t* item_off,
+                  const uint32_t* adj_off, uint64_t nuc, const unsigned long long* csize,
+                  uint4* items, unsigned long long* work, uint32_t chunk, cudaStream_t s);
 void launch_cell_pop(const uint32_t* pids, uint64_t nq, const uint32_t* slot, const uint2* G,
                      uint32_t* pop, cudaStream_t s);
 void launch_fill_f32(float* p, uint64_t n, float v, cudaStream_t s);

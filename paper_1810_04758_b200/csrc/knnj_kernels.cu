@@ -928,14 +928,14 @@ void launch_adj_fill(const uint64_t* B, const uint2* G, uint64_t ncells, const u
 
 __global__ void k_items(const uint32_t* ufirst, const uint32_t* ucnt, const uint32_t* item_off,
                         const uint32_t* adj_off, uint64_t nuc, const unsigned long long* csize,
-                        uint4* items, unsigned long long* work) {
+                        uint4* items, unsigned long long* work, uint32_t chunk) {
     for (uint64_t u = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; u < nuc;
          u += uint64_t(gridDim.x) * blockDim.x) {
         const uint32_t f = ufirst[u], c = ucnt[u];
         const uint32_t i0 = item_off[u];
-        const uint32_t nit = (c + JB - 1) / JB;
+        const uint32_t nit = (c + chunk - 1) / chunk;
         for (uint32_t t = 0; t < nit; ++t) {
-            const uint32_t qb = f + t * JB, qe = min(f + c, qb + JB);
+            const uint32_t qb = f + t * chunk, qe = min(f + c, qb + chunk);
             items[i0 + t] = make_uint4(qb, qe, adj_off[u], adj_off[u + 1]);
             work[i0 + t] = (unsigned long long)(qe - qb) * csize[u];
         }
@@ -943,9 +943,9 @@ __global__ void k_items(const uint32_t* ufirst, const uint32_t* ucnt, const uint
 }
 void launch_items(const uint32_t* ufirst, const uint32_t* ucnt, const uint32_t* item_off,
                   const uint32_t* adj_off, uint64_t nuc, const unsigned long long* csize,
-                  uint4* items, unsigned long long* work, cudaStream_t s) {
+                  uint4* items, unsigned long long* work, uint32_t chunk, cudaStream_t s) {
     if (!nuc) return;
-    k_items<<<592, 256, 0, s>>>(ufirst, ucnt, item_off, adj_off, nuc, csize, items, work);
+    k_items<<<592, 256, 0, s>>>(ufirst, ucnt, item_off, adj_off, nuc, csize, items, work, chunk);
     KJ_CUDA(cudaGetLastError());
     g_launches.fetch_add(1, std::memory_order_relaxed);
 }

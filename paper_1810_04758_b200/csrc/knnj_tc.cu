@@ -140,77 +140,123 @@ __global__ void k_prep_tc(const double* X64, const uint32_t* A, uint64_t N, uint
     }
 }
 
-// One block = one work item (<=128 queries of one cell).
-template <int KB>
-__global__ void __launch_bounds__(TC_M, 2)
-    k_join_tc(const __grid_constant__ CUtensorMap tmB, TcJoinArgs p) {
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Exact bin of one histogram pair (epsilon.cpp:86-95), off the hot path.
+__device__ __noinline__ uint32_t exact_bin(const double* X64, uint32_t n, uint32_t q, uint32_t t,
+                                           double em, double limit_sq, double inv_width,
+                                           uint32_t nb) {
+    const double* a = X64 + (uint64_t)q * n;
+    const double* b = X64 + (uint64_t)t * n;
+    double sum = 0.0;
+    for (uint32_t i = 0; i < n; ++i) {
+        const double d = __dsub_rn(a[i], b[i]);
+        sum = __dadd_rn(sum, __dmul_rn(d, d));
+    }
+    if (sum > limit_sq) return nb;
+    const double dist = sqrt(sum);
+    if (dist >= em) return nb;
+    uint64_t bb = (uint64_t)(dist * inv_width);
+    return bb >= nb ? nb - 1 : (uint32_t)bb;
+}
+
+// Warp-specialised tensor-core kernel (one block = one work item):
+//   warp 0      TMA producer: candidate tiles (128 rows of the level's B operand)
+//               into a STAGES-deep smem ring (also owns the TMEM allocation)
+//   warp 1      MMA issuer: per tile and query group g, 4*KB UMMAs (M=128,N=128,K=16)
+//               into accumulator (g, t&1) of TMEM; commits free the smem stage and
+//               signal the epilogue
+//   warps 2..   epilogue, 4 warps per query group (TMEM lane quarters):
+//               JOIN: screened top-K list insertion; HIST: exact-certain binning
+// Every role walks the same deterministic tile sequence (ranges of the item,
+// <=128 positions per tile, tiles never straddle a range).
+template <int KB, int G, int STAGES, bool HIST>
+__global__ void __launch_bounds__(64 + 128 * G, 1)
+    k_tc(const __grid_constant__ CUtensorMap tmB, TcJoinArgs p) {
+    constexpr int NQ = 128 * G;                    // queries per block
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    // 1024-byte alignment for the 128B-swizzle atoms
     unsigned char* base = reinterpret_cast<unsigned char*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    unsigned char* sA = base;                         // KB x 16 KB
-    unsigned char* sB = sA + KB * KB_BYTES;           // 2 stages x KB x 16 KB
-    float* lkey = reinterpret_cast<float*>(sB + 2 * KB * KB_BYTES);  // [L][128]
-    uint32_t* lpos = reinterpret_cast<uint32_t*>(lkey + p.L * TC_M);
-    float* scr = reinterpret_cast<float*>(lpos + p.L * TC_M);        // [32][128] survivor scratch
-
-    __shared__ uint64_t bar_full[2], bar_mma[2];
+    unsigned char* sA = base;                                   // G x KB x 16 KB
+    unsigned char* sB = sA + G * KB * KB_BYTES;                 // STAGES x KB x 16 KB
+    unsigned char* tail = sB + STAGES * KB * KB_BYTES;
+    __shared__ uint64_t bar_full[STAGES], bar_empty[STAGES], bar_accf[2], bar_acce[2];
     __shared__ uint32_t s_tmem;
-    __shared__ uint32_t s_tile_s[4], s_tile_c[4];   // ring of tile descriptors
-    __shared__ uint32_t s_ri, s_off;
 
-    const int tid = threadIdx.x, warp = tid >> 5;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint4 it = p.items[blockIdx.x];
     const uint32_t nq = it.y - it.x;
-    const bool has_q = (uint32_t)tid < nq;
-    const uint32_t row = it.x + (has_q ? tid : 0);
-    const uint32_t qp = p.qpos[row];
+    constexpr uint32_t TMEM_COLS = G == 1 ? 256 : 512;
 
     if (warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(
-            smem_u32(&s_tmem)));
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(&s_tmem)),
+                     "n"(TMEM_COLS));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
-    if (tid == 0) {
-        mbar_init(&bar_full[0], 1);
-        mbar_init(&bar_full[1], 1);
-        mbar_init(&bar_mma[0], 1);
-        mbar_init(&bar_mma[1], 1);
+    if (tid == 32) {
+        for (int i = 0; i < STAGES; ++i) {
+            mbar_init(&bar_full[i], 1);
+            mbar_init(&bar_empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&bar_accf[i], 1);
+            mbar_init(&bar_acce[i], 4 * G);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
-        s_ri = it.z;
-        s_off = 0;
     }
-    // A operand: this thread's query row, written with the 128B swizzle
-    const __half* qrow_g = p.Bh + (uint64_t)qp * p.row_halfs;
+
+    // epilogue identity
+    const int e = warp - 2;                      // epilogue warp index (valid if >= 0)
+    const int g = e >= 0 ? e / 4 : 0;            // query group
+    const int quarter = warp & 3;                // TMEM lane quarter this warp may access
+    const uint32_t r = quarter * 32 + lane;      // accumulator row (= TMEM lane)
+    const uint32_t qi = g * 128 + r;             // query index inside the item
+    const bool epi = e >= 0;
+    const bool has_q = epi && qi < nq;
+    const uint32_t row = it.x + (has_q ? qi : 0);
+    const uint32_t qp = p.qpos[row];
     float na = 0.f;
-    {
+    if (epi) {
+        // A operand row r of group g: [-2hi, -2hi, -2lo, 1, 1, 0...] with the 128B swizzle
+        const __half* qrow_g = p.Bh + (uint64_t)qp * p.row_halfs;
         const uint32_t n = p.n;
         for (int kb = 0; kb < KB; ++kb) {
-            unsigned char* blk = sA + kb * KB_BYTES + (tid >> 3) * 1024 + (tid & 7) * 128;
+            unsigned char* blk =
+                sA + (g * KB + kb) * KB_BYTES + (r >> 3) * 1024 + (r & 7) * 128;
 #pragma unroll
-            for (int c = 0; c < 8; ++c) {  // 16-byte chunks of this 128-byte row
-                __half h[8];
+            for (int c = 0; c < 8; ++c) {
+                uint32_t w[4];
 #pragma unroll
-                for (int e = 0; e < 8; ++e) {
-                    const uint32_t k = kb * KBLK + c * 8 + e;
-                    __half v = __float2half(0.f);
-                    if (has_q) {
-                        if (k < 2 * n) v = __hmul(__float2half(-2.f), qrow_g[k < n ? k : k - n]);
-                        else if (k < 3 * n) v = __hmul(__float2half(-2.f), qrow_g[n + (k - 2 * n)]);
-                        else if (k < 3 * n + 2) v = __float2half(1.f);
+                for (int e2 = 0; e2 < 4; ++e2) {
+                    uint32_t pair = 0;
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const uint32_t k = kb * KBLK + c * 8 + e2 * 2 + h;
+                        __half v = __float2half(0.f);
+                        if (has_q) {
+                            if (k < 2 * n) v = __hmul(__float2half(-2.f), qrow_g[k < n ? k : k - n]);
+                            else if (k < 3 * n) v = __hmul(__float2half(-2.f), qrow_g[k - n]);
+                            else if (k < 3 * n + 2) v = __float2half(1.f);
+                        }
+                        pair |= (uint32_t)__half_as_ushort(v) << (16 * h);
                     }
-                    h[e] = v;
+                    w[e2] = pair;
                 }
-                uint4 pk;
-                pk.x = (uint32_t)__half_as_ushort(h[0]) | ((uint32_t)__half_as_ushort(h[1]) << 16);
-                pk.y = (uint32_t)__half_as_ushort(h[2]) | ((uint32_t)__half_as_ushort(h[3]) << 16);
-                pk.z = (uint32_t)__half_as_ushort(h[4]) | ((uint32_t)__half_as_ushort(h[5]) << 16);
-                pk.w = (uint32_t)__half_as_ushort(h[6]) | ((uint32_t)__half_as_ushort(h[7]) << 16);
-                *reinterpret_cast<uint4*>(blk + ((c ^ (tid & 7)) * 16)) = pk;
+                *reinterpret_cast<uint4*>(blk + ((c ^ (r & 7)) * 16)) =
+                    make_uint4(w[0], w[1], w[2], w[3]);
             }
         }
         if (has_q) na = __half2float(qrow_g[3 * n]) + __half2float(qrow_g[3 * n + 1]);
+    }
+    if (HIST) {
+        uint32_t* hist = reinterpret_cast<uint32_t*>(tail);
+        float* tab = reinterpret_cast<float*>(hist + p.n_bins * NQ);
+        for (uint32_t i = tid; i < p.n_bins * NQ; i += blockDim.x) hist[i] = 0;
+        for (uint32_t i = tid; i < 2 * (p.n_bins + 1); i += blockDim.x) tab[i] = p.tables[i];
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     fence_before();
@@ -218,174 +264,236 @@ __global__ void __launch_bounds__(TC_M, 2)
     fence_after();
     const uint32_t tmem = s_tmem;
 
-    // tile cursor (thread 0): next chunk of <=128 positions inside one range
-    auto next_tile = [&](uint32_t& s, uint32_t& c) {
-        c = 0;
-        while (s_ri < it.w) {
-            const uint2 r = p.adj[s_ri];
-            if (s_off < r.y - r.x) {
-                s = r.x + s_off;
-                c = min((uint32_t)TC_N, r.y - r.x - s_off);
-                s_off += c;
-                if (s_off == r.y - r.x) {
-                    ++s_ri;
-                    s_off = 0;
+    // deterministic tile sequence over the item's ranges
+    uint32_t cur_ri = it.z, cur_off = 0;
+    auto next_tile = [&](uint32_t& s, uint32_t& c) -> bool {
+        while (cur_ri < it.w) {
+            const uint2 rg = p.adj[cur_ri];
+            const uint32_t len = rg.y - rg.x;
+            if (cur_off < len) {
+                s = rg.x + cur_off;
+                c = min((uint32_t)TC_N, len - cur_off);
+                cur_off += c;
+                if (cur_off == len) {
+                    ++cur_ri;
+                    cur_off = 0;
                 }
-                return;
+                return true;
             }
-            ++s_ri;
-            s_off = 0;
+            ++cur_ri;
+            cur_off = 0;
         }
-    };
-    auto issue_tma = [&](int stage, uint32_t s) {
-        mbar_expect_tx(&bar_full[stage], KB * KB_BYTES);
-#pragma unroll
-        for (int kb = 0; kb < KB; ++kb)
-            tma_load_2d(sB + (stage * KB + kb) * KB_BYTES, &tmB, &bar_full[stage], kb * KBLK,
-                        (int)s);
-    };
-    auto issue_mma = [&](int stage, int acc_buf) {
-        const uint32_t a0 = smem_u32(sA), b0 = smem_u32(sB + stage * KB * KB_BYTES);
-        const uint32_t dcol = tmem + acc_buf * TC_N;
-#pragma unroll
-        for (int kb = 0; kb < KB; ++kb)
-#pragma unroll
-            for (int kk = 0; kk < KBLK / 16; ++kk) {
-                const uint64_t da = umma_desc_sw128(a0 + kb * KB_BYTES + kk * 32);
-                const uint64_t db = umma_desc_sw128(b0 + kb * KB_BYTES + kk * 32);
-                umma_f16(dcol, da, db, (kb | kk) ? 1u : 0u);
-            }
-        umma_commit(&bar_mma[acc_buf]);
+        return false;
     };
 
-    if (tid == 0) {
-        for (int t = 0; t < 2; ++t) {
+    if (warp == 0) {
+        // ------------------------------------------------ TMA producer
+        if (lane == 0) {
             uint32_t s, c;
-            next_tile(s, c);
-            s_tile_s[t] = s;
-            s_tile_c[t] = c;
-            if (c) issue_tma(t, s);
+            for (uint32_t t = 0; next_tile(s, c); ++t) {
+                const int st = t % STAGES;
+                mbar_wait(&bar_empty[st], ((t / STAGES) & 1) ^ 1);
+                mbar_expect_tx(&bar_full[st], KB * KB_BYTES);
+#pragma unroll
+                for (int kb = 0; kb < KB; ++kb)
+                    tma_load_2d(sB + (st * KB + kb) * KB_BYTES, &tmB, &bar_full[st], kb * KBLK,
+                                (int)s);
+            }
         }
-        if (s_tile_c[0]) {
-            mbar_wait(&bar_full[0], 0);
+    } else if (warp == 1) {
+        // ------------------------------------------------ MMA issuer
+        if (lane == 0) {
+            uint32_t s, c;
+            const uint32_t a0 = smem_u32(sA);
+            for (uint32_t t = 0; next_tile(s, c); ++t) {
+                const int st = t % STAGES, b = t & 1;
+                mbar_wait(&bar_full[st], (t / STAGES) & 1);
+                mbar_wait(&bar_acce[b], ((t >> 1) & 1) ^ 1);
+                fence_after();
+                const uint32_t b0 = smem_u32(sB + st * KB * KB_BYTES);
+#pragma unroll
+                for (int gg = 0; gg < G; ++gg) {
+                    const uint32_t dcol = tmem + (gg * 2 + b) * TC_N;
+#pragma unroll
+                    for (int kb = 0; kb < KB; ++kb)
+#pragma unroll
+                        for (int kk = 0; kk < KBLK / 16; ++kk)
+                            umma_f16(dcol,
+                                     umma_desc_sw128(a0 + (gg * KB + kb) * KB_BYTES + kk * 32),
+                                     umma_desc_sw128(b0 + kb * KB_BYTES + kk * 32),
+                                     (kb | kk) ? 1u : 0u);
+                }
+                umma_commit(&bar_empty[st]);
+                umma_commit(&bar_accf[b]);
+            }
+        }
+    } else if (!HIST) {
+        // ------------------------------------------------ JOIN epilogue
+        float* lkey = reinterpret_cast<float*>(tail);               // [L][NQ]
+        uint32_t* lpos = reinterpret_cast<uint32_t*>(lkey + p.L * NQ);
+        float* scr = reinterpret_cast<float*>(lpos + p.L * NQ);     // [32][NQ]
+        const uint32_t me = qi;  // column in the per-query smem arrays
+        int cnt = 0;
+        bool ovf = false;
+        const float init_cut = (p.init_cut && has_q) ? p.init_cut[row] : CUDART_INF_F;
+        const float dl = p.delta;
+        float rhs = has_q ? __fsub_ru(__fadd_ru(init_cut, dl), na) : -CUDART_INF_F;
+        uint32_t s, c;
+        for (uint32_t t = 0; next_tile(s, c); ++t) {
+            const int b = t & 1;
+            mbar_wait(&bar_accf[b], (t >> 1) & 1);
             fence_after();
-            issue_mma(0, 0);
+            const uint32_t tbase = tmem + ((uint32_t)(quarter * 32) << 16) + (g * 2 + b) * TC_N;
+            for (uint32_t j0 = 0; j0 < c; j0 += 32) {
+                float v[32];
+                tmem_ld32(tbase + j0, v);
+                if (p.dbg && blockIdx.x == 0 && t == 0 && g == 0)
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) p.dbg[r * TC_N + j0 + j] = v[j];
+                if (!has_q || ovf) continue;
+                const uint32_t lim = c - j0;
+                if (lim < 32) {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j)
+                        if ((uint32_t)j >= lim) v[j] = CUDART_NAN_F;  // never passes <=
+                }
+                float m[16];
+#pragma unroll
+                for (int j = 0; j < 16; ++j) m[j] = fminf(v[j], v[j + 16]);
+#pragma unroll
+                for (int w = 8; w > 0; w >>= 1)
+#pragma unroll
+                    for (int j = 0; j < w; ++j) m[j] = fminf(m[j], m[j + w]);
+                if (!(m[0] <= rhs)) continue;
+                uint32_t mask = 0;
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    mask |= (v[j] <= rhs ? 1u : 0u) << j;
+                    scr[j * NQ + me] = v[j];
+                }
+                while (mask) {
+                    const int j = __ffs(mask) - 1;
+                    mask &= mask - 1;
+                    const float vj = scr[j * NQ + me];
+                    if (!(vj <= rhs)) continue;
+                    const uint32_t pos = s + j0 + j;
+                    if (pos == qp) continue;  // self pair: excluded by id
+                    if (cnt == (int)p.L) {
+                        ovf = true;
+                        rhs = -CUDART_INF_F;
+                        break;
+                    }
+                    const float key = vj + na;
+                    int q = cnt;
+                    while (q > 0) {
+                        const float kq = lkey[(q - 1) * NQ + me];
+                        if (kq <= key) break;
+                        lkey[q * NQ + me] = kq;
+                        lpos[q * NQ + me] = lpos[(q - 1) * NQ + me];
+                        --q;
+                    }
+                    lkey[q * NQ + me] = key;
+                    lpos[q * NQ + me] = pos;
+                    ++cnt;
+                    if (cnt >= (int)p.K) {
+                        const float cut_list = __fadd_ru(lkey[(p.K - 1) * NQ + me], 2.f * dl);
+                        const float ce = fminf(cut_list, __fadd_ru(init_cut, dl));
+                        while (cnt > (int)p.K && lkey[(cnt - 1) * NQ + me] > ce) --cnt;
+                        rhs = __fsub_ru(ce, na);
+                    }
+                }
+            }
+            fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bar_acce[b]);
         }
-    }
-    __syncthreads();
-
-    int cnt = 0;
-    bool ovf = false;
-    float cut_list = CUDART_INF_F;
-    const float init_cut = (p.init_cut && has_q) ? p.init_cut[row] : CUDART_INF_F;
-    const float dl = p.delta;
-    float rhs = fminf(cut_list, __fadd_ru(init_cut, dl));
-    rhs = __fsub_ru(rhs, na);
-    if (!has_q) rhs = -CUDART_INF_F;
-
-    for (uint32_t t = 0;; ++t) {
-        const uint32_t c = s_tile_c[t & 3];
-        if (c == 0) break;
-        const uint32_t s = s_tile_s[t & 3];
-        const int buf = t & 1;
-        // issue MMA for tile t+1 (its accumulator was drained at the end of t-1)
-        if (tid == 0 && s_tile_c[(t + 1) & 3]) {
-            mbar_wait(&bar_full[(t + 1) & 1], ((t + 1) >> 1) & 1);
+        if (has_q) {
+            p.out_cnt[row] = ovf ? OVF : (uint32_t)cnt;
+            if (!ovf)
+                for (int i = 0; i < cnt; ++i)
+                    p.out_pos[(uint64_t)row * p.L + i] = lpos[i * NQ + me];
+        }
+    } else {
+        // ------------------------------------------------ HISTOGRAM epilogue
+        uint32_t* hist = reinterpret_cast<uint32_t*>(tail);          // [n_bins][NQ]
+        const float* LO = reinterpret_cast<const float*>(hist + p.n_bins * NQ);
+        const float* HI = LO + p.n_bins + 1;
+        const uint32_t nbins = p.n_bins;
+        const float dl = p.delta;
+        const float skip_at = has_q ? __fsub_ru(__fadd_ru(LO[nbins], dl), na) : -CUDART_INF_F;
+        const float invw = p.inv_width_scaled;
+        uint32_t s, c;
+        for (uint32_t t = 0; next_tile(s, c); ++t) {
+            const int b = t & 1;
+            mbar_wait(&bar_accf[b], (t >> 1) & 1);
             fence_after();
-            issue_mma((t + 1) & 1, (t + 1) & 1);
-        }
-        mbar_wait(&bar_mma[buf], (t >> 1) & 1);
-        fence_after();
-        // stage `buf` is free again: prefetch tile t+2 into it
-        if (tid == 0) {
-            uint32_t s2, c2;
-            next_tile(s2, c2);
-            s_tile_s[(t + 2) & 3] = s2;
-            s_tile_c[(t + 2) & 3] = c2;
-            if (c2) issue_tma(buf, s2);
-        }
-        // epilogue: this warp's 32 TMEM lanes, columns [0, c)
-        const uint32_t tbase = tmem + ((uint32_t)(warp * 32) << 16) + buf * TC_N;
-        for (uint32_t j0 = 0; j0 < c; j0 += 32) {
-            float v[32];
-            tmem_ld32(tbase + j0, v);
-            if (p.dbg && blockIdx.x == 0 && t == 0)
+            const uint32_t tbase = tmem + ((uint32_t)(quarter * 32) << 16) + (g * 2 + b) * TC_N;
+            for (uint32_t j0 = 0; j0 < c; j0 += 32) {
+                float v[32];
+                tmem_ld32(tbase + j0, v);
+                if (!has_q) continue;
+                const uint32_t lim = c - j0;
 #pragma unroll
-                for (int j = 0; j < 32; ++j) p.dbg[tid * TC_N + j0 + j] = v[j];
-            if (!has_q || ovf) continue;
-            const uint32_t lim = c - j0;
-            if (lim < 32) {
-#pragma unroll
-                for (int j = 0; j < 32; ++j)
-                    if ((uint32_t)j >= lim) v[j] = CUDART_NAN_F;  // never passes a <= test
-            }
-            // fast path: one FMNMX per pair
-            float m[16];
-#pragma unroll
-            for (int j = 0; j < 16; ++j) m[j] = fminf(v[j], v[j + 16]);
-#pragma unroll
-            for (int w = 8; w > 0; w >>= 1)
-#pragma unroll
-                for (int j = 0; j < w; ++j) m[j] = fminf(m[j], m[j + w]);
-            if (!(m[0] <= rhs)) continue;
-            // rare path: survivors through this thread's smem scratch row
-            uint32_t mask = 0;
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-                mask |= (v[j] <= rhs ? 1u : 0u) << j;
-                scr[j * TC_M + tid] = v[j];
-            }
-            while (mask) {
-                const int j = __ffs(mask) - 1;
-                mask &= mask - 1;
-                const float vj = scr[j * TC_M + tid];
-                if (!(vj <= rhs)) continue;  // rhs may have tightened
-                const uint32_t pos = s + j0 + j;
-                if (pos == qp) continue;  // self pair: excluded by id
-                if (cnt == (int)p.L) {
-                    ovf = true;
-                    rhs = -CUDART_INF_F;
-                    break;
-                }
-                const float key = vj + na;
-                int q = cnt;
-                while (q > 0) {
-                    const float kq = lkey[(q - 1) * TC_M + tid];
-                    if (kq <= key) break;
-                    lkey[q * TC_M + tid] = kq;
-                    lpos[q * TC_M + tid] = lpos[(q - 1) * TC_M + tid];
-                    --q;
-                }
-                lkey[q * TC_M + tid] = key;
-                lpos[q * TC_M + tid] = pos;
-                ++cnt;
-                if (cnt >= (int)p.K) {
-                    cut_list = __fadd_ru(lkey[(p.K - 1) * TC_M + tid], 2.f * dl);
-                    const float ce = fminf(cut_list, __fadd_ru(init_cut, dl));
-                    while (cnt > (int)p.K && lkey[(cnt - 1) * TC_M + tid] > ce) --cnt;
-                    rhs = __fsub_ru(ce, na);
+                for (int j = 0; j < 32; ++j) {
+                    if ((uint32_t)j >= lim || !(v[j] < skip_at)) continue;  // beyond eps_mean
+                    const uint32_t pos = s + j0 + j;
+                    if (pos == qp) continue;  // self
+                    const float key = v[j] + na;
+                    const float klo = __fsub_rd(key, dl), khi = __fadd_ru(key, dl);
+                    int bin = key > 0.f ? (int)(key * rsqrtf(key) * invw) : 0;
+                    bin = min(bin, (int)nbins - 1);
+                    uint32_t bb;
+                    if (klo >= LO[bin] && khi < HI[bin]) bb = (uint32_t)bin;
+                    else bb = exact_bin(p.X64, p.n, qp, pos, p.eps_mean, p.limit_sq,
+                                        p.inv_width, nbins);
+                    if (bb < nbins) hist[bb * NQ + qi] += 1;
                 }
             }
+            fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bar_acce[b]);
         }
-        fence_before();
-        __syncthreads();
-    }
-    if (has_q) {
-        p.out_cnt[row] = ovf ? OVF : (uint32_t)cnt;
-        if (!ovf)
-            for (int i = 0; i < cnt; ++i) p.out_pos[(uint64_t)row * p.L + i] = lpos[i * TC_M + tid];
     }
     fence_before();
     __syncthreads();
+    if (HIST) {
+        uint32_t* hist = reinterpret_cast<uint32_t*>(tail);
+        for (uint32_t bb = tid; bb < p.n_bins; bb += blockDim.x) {
+            unsigned long long sum = 0;
+            for (int q = 0; q < NQ; ++q) sum += hist[bb * NQ + ((q + bb) & (NQ - 1))];
+            if (sum) atomicAdd(&p.counts[bb], sum);
+        }
+    }
     if (warp == 0) {
         fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                     "n"(TMEM_COLS));
     }
 }
 
 // ---------------------------------------------------------------- host side
+namespace {
+struct TcShape {
+    int KB, G, STAGES;
+};
+TcShape tc_shape(uint32_t row_halfs) {
+    const int KB = (int)(row_halfs / KBLK);
+    return KB == 1 ? TcShape{1, 2, 4} : TcShape{2, 1, 3};
+}
+}  // namespace
+
+uint32_t tc_queries_per_item(uint32_t row_halfs) { return 128u * tc_shape(row_halfs).G; }
+
+size_t tc_smem_bytes(uint32_t row_halfs, uint32_t L, uint32_t n_bins, bool hist) {
+    const TcShape sh = tc_shape(row_halfs);
+    const size_t NQ = 128 * sh.G;
+    size_t b = 1024 + (size_t)(sh.G + sh.STAGES) * sh.KB * KB_BYTES;
+    if (hist) b += NQ * n_bins * 4 + 8 * (n_bins + 1);
+    else b += NQ * L * 8 + NQ * 32 * 4;
+    return b;
+}
 size_t tc_join_smem_bytes(int KB, uint32_t L) {
-    return 1024 + (size_t)3 * KB * KB_BYTES + (size_t)L * TC_M * 8 + 32 * TC_M * 4;
+    return tc_smem_bytes(KB * KBLK, L, 0, false);
 }
 
 void launch_prep_tc(const double* X64, const uint32_t* A, uint64_t N, uint32_t n, const double* g,
@@ -409,8 +517,8 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
     return fn;
 }
 
-template <int KB>
-static void launch_tc_kb(const TcJoinArgs& a, uint64_t nitems, uint64_t N, cudaStream_t s) {
+template <int KB, int G, int STAGES, bool HIST>
+static void launch_tc_t(const TcJoinArgs& a, uint64_t nitems, uint64_t N, cudaStream_t s) {
     CUtensorMap map;
     cuuint64_t dims[2] = {(cuuint64_t)a.row_halfs, (cuuint64_t)N};
     cuuint64_t strides[1] = {(cuuint64_t)a.row_halfs * 2};
@@ -421,13 +529,15 @@ static void launch_tc_kb(const TcJoinArgs& a, uint64_t nitems, uint64_t N, cudaS
                               CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw Error(9, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
-    const size_t sm = tc_join_smem_bytes(KB, a.L);
-    KJ_CUDA(cudaFuncSetAttribute(k_join_tc<KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    const size_t sm = tc_smem_bytes(a.row_halfs, a.L, a.n_bins, HIST);
+    if (sm > 227 * 1024) throw Error(1, "tensor-core kernel needs too much shared memory");
+    KJ_CUDA(cudaFuncSetAttribute(k_tc<KB, G, STAGES, HIST>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     for (uint64_t off = 0; off < nitems; off += 2147483647ull) {
         const uint64_t cnt = std::min<uint64_t>(nitems - off, 2147483647ull);
         TcJoinArgs b = a;
         b.items = a.items + off;
-        k_join_tc<KB><<<(unsigned)cnt, TC_M, sm, s>>>(map, b);
+        k_tc<KB, G, STAGES, HIST><<<(unsigned)cnt, 64 + 128 * G, sm, s>>>(map, b);
     }
     KJ_CUDA(cudaGetLastError());
     g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -435,10 +545,18 @@ static void launch_tc_kb(const TcJoinArgs& a, uint64_t nitems, uint64_t N, cudaS
 
 void launch_join_tc(const TcJoinArgs& a, uint64_t nitems, uint64_t N, cudaStream_t s) {
     if (!nitems) return;
-    const int KB = (int)(a.row_halfs / KBLK);
-    if (KB == 1) launch_tc_kb<1>(a, nitems, N, s);
-    else if (KB == 2) launch_tc_kb<2>(a, nitems, N, s);
+    const TcShape sh = tc_shape(a.row_halfs);
+    if (sh.KB == 1) launch_tc_t<1, 2, 4, false>(a, nitems, N, s);
+    else if (sh.KB == 2) launch_tc_t<2, 1, 3, false>(a, nitems, N, s);
     else throw Error(1, "tensor-core join supports up to 42 dimensions");
+}
+
+void launch_hist_tc(const TcJoinArgs& a, uint64_t nitems, uint64_t N, cudaStream_t s) {
+    if (!nitems) return;
+    const TcShape sh = tc_shape(a.row_halfs);
+    if (sh.KB == 1) launch_tc_t<1, 2, 4, true>(a, nitems, N, s);
+    else if (sh.KB == 2) launch_tc_t<2, 1, 3, true>(a, nitems, N, s);
+    else throw Error(1, "tensor-core histogram supports up to 42 dimensions");
 }
 
 }  // namespace kj
