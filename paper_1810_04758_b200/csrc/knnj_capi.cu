@@ -251,6 +251,7 @@ struct knnj_ctx {
         perm = order;
         working_ready = true;
         bh_id_ready = false;  // FP16 operands derive from the working coordinates
+        mm_lo.clear();
         for (auto& lv : levels) lv.built = false;
     }
 
@@ -570,6 +571,14 @@ struct knnj_ctx {
     }
 
     // ------------------------------------------------------------ grid levels
+    static double unorder(unsigned long long o) {
+        unsigned long long b = (o & 0x8000000000000000ull) ? (o & 0x7FFFFFFFFFFFFFFFull) : ~o;
+        double v;
+        std::memcpy(&v, &b, 8);
+        return v;
+    }
+    std::vector<double> mm_lo;  // Morton box of the working coords (first <=10 dims)
+    DBuf<double> d_mm;
     // GridIndex::build (grid_index.cpp:13-75) at cell width w (level 0: w = eps).
     void build_level(int L, uint32_t m, double w) {
         Level& lv = levels[L];
@@ -588,12 +597,6 @@ struct knnj_ctx {
         KJ_CUDA(cudaMemcpyAsync(mn.data(), d_u64a.p, 8 * m, cudaMemcpyDeviceToHost, s));
         KJ_CUDA(cudaMemcpyAsync(mx.data(), d_u64b.p, 8 * m, cudaMemcpyDeviceToHost, s));
         sync();
-        auto unorder = [](unsigned long long o) {
-            unsigned long long b = (o & 0x8000000000000000ull) ? (o & 0x7FFFFFFFFFFFFFFFull) : ~o;
-            double v;
-            std::memcpy(&v, &b, 8);
-            return v;
-        };
         lv.mins.resize(m);
         lv.maxs.resize(m);
         for (uint32_t j = 0; j < m; ++j) {
@@ -651,8 +654,38 @@ struct knnj_ctx {
         lv.slot.ensure(N);
         lv.posOf.ensure(N);
         launch_grid_tables(skeys.p, lv.A.p, runidx.p, N, lv.B.p, lv.G.p, lv.slot.p, lv.posOf.p, s);
+        // join order: same cell ranges, Morton order inside each cell
+        {
+            const uint32_t md = std::min<uint32_t>(n, 10);
+            if (mm_lo.size() != md) {
+                std::vector<unsigned long long> i0(md, ~0ull), i1(md, 0ull), mn(md), mx(md);
+                KJ_CUDA(cudaMemcpyAsync(d_u64a.p, i0.data(), 8 * md, cudaMemcpyHostToDevice, s));
+                KJ_CUDA(cudaMemcpyAsync(d_u64b.p, i1.data(), 8 * md, cudaMemcpyHostToDevice, s));
+                launch_minmax(X64.p, N, n, md, d_u64a.p, d_u64b.p, s);
+                KJ_CUDA(cudaMemcpyAsync(mn.data(), d_u64a.p, 8 * md, cudaMemcpyDeviceToHost, s));
+                KJ_CUDA(cudaMemcpyAsync(mx.data(), d_u64b.p, 8 * md, cudaMemcpyDeviceToHost, s));
+                sync();
+                mm_lo.resize(md);
+                std::vector<double> inv(md);
+                for (uint32_t j = 0; j < md; ++j) {
+                    mm_lo[j] = unorder(mn[j]);
+                    const double r = unorder(mx[j]) - mm_lo[j];
+                    inv[j] = r > 0 ? 1.0 / r : 0.0;
+                }
+                d_mm.ensure(2 * md);
+                KJ_CUDA(cudaMemcpyAsync(d_mm.p, mm_lo.data(), 8 * md, cudaMemcpyHostToDevice, s));
+                KJ_CUDA(cudaMemcpyAsync(d_mm.p + md, inv.data(), 8 * md, cudaMemcpyHostToDevice, s));
+            }
+            launch_morton_keys(X64.p, lv.A.p, lv.slot.p, N, n, md, d_mm.p, d_mm.p + md, keys.p,
+                               vals.p, s);
+            lv.J.ensure(N);
+            lv.posJ.ensure(N);
+            sort_pairs_u64_u32(sc, keys.p, skeys.p, vals.p, lv.J.p, N,
+                               32 + bits_for(nruns ? nruns - 1 : 0), s);
+            launch_inverse(lv.J.p, N, lv.posJ.p, s);
+        }
         lv.Xs.ensure((uint64_t)n * Npad);
-        launch_gather_soa(Xf.p, lv.A.p, N, n, Npad, lv.Xs.p, s);
+        launch_gather_soa(Xf.p, lv.J.p, N, n, Npad, lv.Xs.p, s);
         lv.tc_ready = false;
         if (use_tc()) prep_tc(lv);
         sync();
@@ -673,7 +706,7 @@ struct knnj_ctx {
         if (lv.tc_ready) return;
         lv.row_halfs = 3 * n + 2 <= 64 ? 64 : 128;
         lv.Bh.ensure(N * lv.row_halfs);
-        launch_prep_tc(X64.p, lv.A.p, N, n, d_g.p, 1.0 / tc_S(), lv.row_halfs, lv.Bh.p, s);
+        launch_prep_tc(X64.p, lv.J.p, N, n, d_g.p, 1.0 / tc_S(), lv.row_halfs, lv.Bh.p, s);
         lv.tc_ready = true;
     }
     // Bound on |key - sq64/S^2| for the tensor-core screen.
@@ -710,11 +743,14 @@ struct knnj_ctx {
     // ------------------------------------------------------------ passes
     // Groups the queries (point ids + output rows, on device) by their cell in
     // level lv and builds work items + candidate ranges.
+    // unsorted candidate buffer per query in the tcgen05 join (<= 64: warp compaction)
+    static uint32_t tc_list_len(uint32_t K) { return std::min<uint32_t>(64, K + 24); }
     // the join kernel a pass will run on (decided before its items are built)
     bool pass_uses_tc(const Level& lv, uint32_t K) const {
         const uint32_t rh = 3 * n + 2 <= 64 ? 64 : 128;
-        return use_tc() && tc_smem_bytes(lv.row_halfs ? lv.row_halfs : rh, K + 8, 0, false) <=
-                               227 * 1024;
+        return use_tc() && K + 8 <= 64 &&
+               tc_smem_bytes(lv.row_halfs ? lv.row_halfs : rh, tc_list_len(K), 0, false) <=
+                   227 * 1024;
     }
     uint32_t pass_chunk(const Level& lv, uint32_t K) const {
         return pass_uses_tc(lv, K) ? tc_queries_per_item(lv.row_halfs ? lv.row_halfs : 64)
@@ -729,7 +765,7 @@ struct knnj_ctx {
         if (!nq) return;
         DBuf<uint32_t> pos_unsorted, qcell;
         pos_unsorted.ensure(nq);
-        launch_map_u32(d_qpid, lv.posOf.p, nq, pos_unsorted.p, s);
+        launch_map_u32(d_qpid, lv.posJ.p, nq, pos_unsorted.p, s);
         P.qpos.ensure(nq);
         P.qrow.ensure(nq);
         sort_pairs_u32_u32(sc, pos_unsorted.p, P.qpos.p, d_qrow, P.qrow.p, nq, bits_for(N), s);
@@ -737,7 +773,7 @@ struct knnj_ctx {
         {
             DBuf<uint32_t> tmp;
             tmp.ensure(nq);
-            launch_map_u32(P.qpos.p, lv.A.p, nq, tmp.p, s);
+            launch_map_u32(P.qpos.p, lv.J.p, nq, tmp.p, s);
             launch_map_u32(tmp.p, lv.slot.p, nq, qcell.p, s);
         }
         DBuf<uint32_t> ucell, ucnt;
@@ -825,7 +861,7 @@ struct knnj_ctx {
         const bool tc = pass_uses_tc(lv, K) && P.chunk == tc_queries_per_item(lv.row_halfs);
         if (!tc && P.chunk != (uint32_t)JB) throw Error(9, "pass built for a different kernel");
         // list capacity: K plus slack for near-ties inside the screen band (overflow -> exact slow path)
-        const uint32_t L = tc ? K + 8 : K + std::max<uint32_t>(16, K / 2);
+        const uint32_t L = tc ? tc_list_len(K) : K + std::max<uint32_t>(16, K / 2);
         if (L > 256) throw Error(1, "k above 170 is not supported by the device join");
         const int np = pick_np(n);
         if (np < 0) throw Error(1, "dimension count above 128 is not supported by the device join");
@@ -880,7 +916,7 @@ struct knnj_ctx {
         FinalArgs f{};
         f.X64 = X64.p;
         f.n = n;
-        f.A = lv.A.p;
+        f.A = lv.J.p;
         f.qpos = P.qpos.p;
         f.qrow = P.qrow.p;
         f.cnt = cnt.p;
@@ -909,7 +945,7 @@ struct knnj_ctx {
             row_item.ensure(P.nq);
             KJ_CUDA(cudaMemcpyAsync(d_rows.p, rows.data(), 4 * rows.size(), cudaMemcpyHostToDevice, s));
             launch_row_item(P.items.p, P.nitems, row_item.p, s);
-            launch_slow_exact(X64.p, n, lv.A.p, P.qpos.p, P.qrow.p, d_rows.p, rows.size(),
+            launch_slow_exact(X64.p, n, lv.J.p, P.qpos.p, P.qrow.p, d_rows.p, rows.size(),
                               P.items.p, row_item.p, P.adj.p, K, eps2, cov2, out_ids, out_dist,
                               out_kth, out_status, s);
             sync();
@@ -1077,7 +1113,8 @@ void* knnj_stream(knnj_ctx* ctx) { return ctx ? (void*)ctx->s : nullptr; }
 // level 0 — queries at sorted positions [q0,q0+128) against [c0,c0+128) —
 // returns the raw FP32 accumulators and the FP16 operand rows used.
 int knnj_debug_tc_tile(knnj_ctx* c, uint32_t q0, uint32_t c0, float* D, uint16_t* Bq,
-                       uint16_t* Bc, double* scale_S, double* delta) {
+                       uint16_t* Bc, double* scale_S, double* delta, uint32_t* pid_q,
+                       uint32_t* pid_c) {
     return guarded(c, [&] {
         Level& lv = c->levels[0];
         if (!lv.built) throw Error(1, "no grid");
@@ -1118,6 +1155,8 @@ int knnj_debug_tc_tile(knnj_ctx* c, uint32_t q0, uint32_t c0, float* D, uint16_t
                                 cudaMemcpyDeviceToHost, c->s));
         KJ_CUDA(cudaMemcpyAsync(Bc, lv.Bh.p + (uint64_t)c0 * lv.row_halfs, 2 * 128 * lv.row_halfs,
                                 cudaMemcpyDeviceToHost, c->s));
+        KJ_CUDA(cudaMemcpyAsync(pid_q, lv.J.p + q0, 4 * 128, cudaMemcpyDeviceToHost, c->s));
+        KJ_CUDA(cudaMemcpyAsync(pid_c, lv.J.p + c0, 4 * 128, cudaMemcpyDeviceToHost, c->s));
         c->sync();
         *scale_S = c->tc_S();
         *delta = c->tc_delta();
@@ -1298,7 +1337,7 @@ int knnj_range_count(knnj_ctx* c, const uint32_t* q, uint64_t nq, uint64_t* in_e
         c->build_pass(lv, d_q.p, d_r.p, nq, P);
         DBuf<unsigned long long> cnt;
         cnt.ensure(nq);
-        launch_range_count(c->X64.p, c->n, lv.A.p, P.qpos.p, P.items.p, P.nitems, P.adj.p,
+        launch_range_count(c->X64.p, c->n, lv.J.p, P.qpos.p, P.items.p, P.nitems, P.adj.p,
                            c->eps0 * c->eps0, cnt.p, c->s);
         std::vector<unsigned long long> h(nq);
         std::vector<uint32_t> prow(nq);

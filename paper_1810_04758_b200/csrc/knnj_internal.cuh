@@ -85,6 +85,8 @@ struct Level {
     DBuf<uint32_t> A;    // N: sorted position -> point id
     DBuf<uint32_t> slot; // N: point id -> cell index
     DBuf<uint32_t> posOf;// N: point id -> sorted position
+    DBuf<uint32_t> J;    // N: join-order position -> point id (cells contiguous, Morton inside)
+    DBuf<uint32_t> posJ; // N: point id -> join-order position
     DBuf<float> Xs;      // n x Npad SoA, sorted order, centred floats
     bool tc_ready = false;
     uint32_t row_halfs = 0;
@@ -179,6 +181,10 @@ struct HistArgs {
 // ---------------------------------------------------------------- launchers
 extern std::atomic<unsigned long long> g_launches;  // our kernels launched so far
 double measure_ffma_tflops(cudaStream_t s);
+void launch_morton_keys(const double* X64, const uint32_t* A, const uint32_t* slot, uint64_t N,
+                        uint32_t n, uint32_t dims, const double* lo, const double* inv_range,
+                        uint64_t* keys, uint32_t* vals, cudaStream_t s);
+void launch_inverse(const uint32_t* J, uint64_t N, uint32_t* posJ, cudaStream_t s);
 size_t tc_join_smem_bytes(int KB, uint32_t L);
 size_t tc_smem_bytes(uint32_t row_halfs, uint32_t L, uint32_t n_bins, bool hist);
 uint32_t tc_queries_per_item(uint32_t row_halfs);

@@ -1199,3 +1199,44 @@ void launch_scale_f32(const float* in, uint64_t n, float scale, float* out, cuda
     g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 }  // namespace kj
+
+namespace kj {
+// Join-order keys: (cell slot, Morton code of the point over the first `dims`
+// working dims, 3 bits each). Points of one cell stay contiguous (same ranges
+// as the reference order) but are laid out along a space-filling curve.
+__global__ void k_morton_keys(const double* X64, const uint32_t* A, const uint32_t* slot,
+                              uint64_t N, uint32_t n, uint32_t dims, const double* lo,
+                              const double* inv_range, uint64_t* keys, uint32_t* vals) {
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < N;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const uint32_t pid = A[i];
+        const double* x = X64 + (uint64_t)pid * n;
+        uint32_t code = 0;
+        for (int bit = 2; bit >= 0; --bit)
+            for (uint32_t d = 0; d < dims; ++d) {
+                double f = (x[d] - lo[d]) * inv_range[d];
+                uint32_t q = f <= 0.0 ? 0u : (f >= 1.0 ? 7u : (uint32_t)(f * 8.0));
+                code = (code << 1) | ((q >> bit) & 1u);
+            }
+        keys[i] = ((uint64_t)slot[pid] << 32) | code;
+        vals[i] = pid;
+    }
+}
+void launch_morton_keys(const double* X64, const uint32_t* A, const uint32_t* slot, uint64_t N,
+                        uint32_t n, uint32_t dims, const double* lo, const double* inv_range,
+                        uint64_t* keys, uint32_t* vals, cudaStream_t s) {
+    k_morton_keys<<<2368, 256, 0, s>>>(X64, A, slot, N, n, dims, lo, inv_range, keys, vals);
+    KJ_CUDA(cudaGetLastError());
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+__global__ void k_inverse(const uint32_t* J, uint64_t N, uint32_t* posJ) {
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < N;
+         i += uint64_t(gridDim.x) * blockDim.x)
+        posJ[J[i]] = (uint32_t)i;
+}
+void launch_inverse(const uint32_t* J, uint64_t N, uint32_t* posJ, cudaStream_t s) {
+    k_inverse<<<1184, 256, 0, s>>>(J, N, posJ);
+    KJ_CUDA(cudaGetLastError());
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+}  // namespace kj

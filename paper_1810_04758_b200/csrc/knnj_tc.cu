@@ -96,6 +96,22 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
                  : "memory");
 }
 
+// two 32-column loads in flight, one wait (both in one asm: no use before the wait)
+__device__ __forceinline__ void tmem_ld64(uint32_t taddr, float (&v0)[32], float (&v1)[32]) {
+    uint32_t r[64];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%64];\n\t"
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%32,%33,%34,%35,%36,%37,%38,%39,%40,%41,%42,%43,%44,%45,%46,%47,%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63}, [%65];\n\t"
+        "tcgen05.wait::ld.sync.aligned;"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31]), "=r"(r[32]), "=r"(r[33]), "=r"(r[34]), "=r"(r[35]), "=r"(r[36]), "=r"(r[37]), "=r"(r[38]), "=r"(r[39]), "=r"(r[40]), "=r"(r[41]), "=r"(r[42]), "=r"(r[43]), "=r"(r[44]), "=r"(r[45]), "=r"(r[46]), "=r"(r[47]), "=r"(r[48]), "=r"(r[49]), "=r"(r[50]), "=r"(r[51]), "=r"(r[52]), "=r"(r[53]), "=r"(r[54]), "=r"(r[55]), "=r"(r[56]), "=r"(r[57]), "=r"(r[58]), "=r"(r[59]), "=r"(r[60]), "=r"(r[61]), "=r"(r[62]), "=r"(r[63])
+        : "r"(taddr), "r"(taddr + 32u)
+        : "memory");
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+        v0[i] = __uint_as_float(r[i]);
+        v1[i] = __uint_as_float(r[32 + i]);
+    }
+}
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
     uint32_t r[32];
     asm volatile(
@@ -112,6 +128,44 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
     for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ float tmem_ld1(uint32_t taddr) {
+    uint32_t r;
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(r) : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    return __uint_as_float(r);
+}
+
+// K-th smallest (1-based k) of the 64 values a0 (element lane) and a1 (element
+// 32+lane) held across a warp: bitonic sort network, ascending.
+__device__ __forceinline__ float warp_kth64(float a0, float a1, uint32_t k) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int kk = 2; kk <= 64; kk <<= 1) {
+#pragma unroll
+        for (int j = kk >> 1; j > 0; j >>= 1) {
+            if (j == 32) {
+                // pairs (lane, 32+lane): element index lane is the lower one
+                const bool up = (lane & kk) == 0;  // kk == 64 here: always ascending
+                const float lo = fminf(a0, a1), hi = fmaxf(a0, a1);
+                a0 = up ? lo : hi;
+                a1 = up ? hi : lo;
+            } else {
+                const float p0 = __shfl_xor_sync(0xffffffffu, a0, j);
+                const float p1 = __shfl_xor_sync(0xffffffffu, a1, j);
+                const uint32_t i0 = lane, i1 = 32 + lane;
+                const bool lower = (lane & j) == 0;
+                const bool up0 = (i0 & kk) == 0, up1 = (i1 & kk) == 0;
+                a0 = (lower == up0) ? fminf(a0, p0) : fmaxf(a0, p0);
+                a1 = (lower == up1) ? fminf(a1, p1) : fmaxf(a1, p1);
+            }
+        }
+    }
+    const uint32_t i = k - 1;
+    const float v0 = __shfl_sync(0xffffffffu, a0, i & 31);
+    const float v1 = __shfl_sync(0xffffffffu, a1, i & 31);
+    return i < 32 ? v0 : v1;
 }
 
 }  // namespace
@@ -177,8 +231,8 @@ __global__ void __launch_bounds__(64 + 128 * G, 1)
     k_tc(const __grid_constant__ CUtensorMap tmB, TcJoinArgs p) {
     constexpr int NQ = 128 * G;                    // queries per block
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    unsigned char* base = reinterpret_cast<unsigned char*>(
-        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // 1024-byte alignment for the 128B-swizzle atoms, staying in the shared state space
+    unsigned char* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     unsigned char* sA = base;                                   // G x KB x 16 KB
     unsigned char* sB = sA + G * KB * KB_BYTES;                 // STAGES x KB x 16 KB
     unsigned char* tail = sB + STAGES * KB * KB_BYTES;
@@ -264,9 +318,32 @@ __global__ void __launch_bounds__(64 + 128 * G, 1)
     fence_after();
     const uint32_t tmem = s_tmem;
 
-    // deterministic tile sequence over the item's ranges
-    uint32_t cur_ri = it.z, cur_off = 0;
+    // Deterministic tile sequence over the item's ranges. In the first range (the
+    // item's own cell row, where its queries live) the sweep starts at the tile
+    // holding the item's first query and wraps around: with the within-cell
+    // locality order the nearest candidates come first and the top-K cut
+    // converges after one tile.
+    uint32_t cur_ri = it.z, cur_off = 0, first_start = 0, first_done = 0;
+    if (!HIST && it.z < it.w) {
+        const uint2 rg0 = p.adj[it.z];
+        const uint32_t q0pos = p.qpos[it.x];
+        if (q0pos >= rg0.x && q0pos < rg0.y) first_start = ((q0pos - rg0.x) / TC_N) * TC_N;
+    }
     auto next_tile = [&](uint32_t& s, uint32_t& c) -> bool {
+        if (cur_ri == it.z && cur_ri < it.w) {  // first range: [first_start, len) then [0, first_start)
+            const uint2 rg = p.adj[cur_ri];
+            const uint32_t len = rg.y - rg.x;
+            while (first_done < len) {
+                const uint32_t off = (first_start + first_done) % len;
+                const uint32_t seg_end = off >= first_start ? len : first_start;
+                s = rg.x + off;
+                c = min((uint32_t)TC_N, seg_end - off);
+                first_done += c;
+                return true;
+            }
+            ++cur_ri;
+            cur_off = 0;
+        }
         while (cur_ri < it.w) {
             const uint2 rg = p.adj[cur_ri];
             const uint32_t len = rg.y - rg.x;
@@ -329,77 +406,131 @@ __global__ void __launch_bounds__(64 + 128 * G, 1)
         }
     } else if (!HIST) {
         // ------------------------------------------------ JOIN epilogue
-        float* lkey = reinterpret_cast<float*>(tail);               // [L][NQ]
+        // Per query an UNSORTED buffer (capacity p.L <= 64) of every candidate
+        // that passed the cut; the cut tightens when a full buffer is
+        // compacted warp-cooperatively (K-th key + 2 delta). Fast path: one
+        // FMNMX per pair; survivors are re-read from TMEM one warp-uniform
+        // column at a time (no per-lane dynamic indexing).
+        float* lkey = reinterpret_cast<float*>(tail);               // [NQ][L]
         uint32_t* lpos = reinterpret_cast<uint32_t*>(lkey + p.L * NQ);
-        float* scr = reinterpret_cast<float*>(lpos + p.L * NQ);     // [32][NQ]
-        const uint32_t me = qi;  // column in the per-query smem arrays
-        int cnt = 0;
+        const uint32_t LB = p.L;
+        float* mykey = lkey + (size_t)qi * LB;
+        uint32_t* mypos = lpos + (size_t)qi * LB;
+        uint32_t cnt = 0;
         bool ovf = false;
         const float init_cut = (p.init_cut && has_q) ? p.init_cut[row] : CUDART_INF_F;
         const float dl = p.delta;
-        float rhs = has_q ? __fsub_ru(__fadd_ru(init_cut, dl), na) : -CUDART_INF_F;
+        const float cap = __fadd_ru(init_cut, dl);        // U + delta
+        float cut = cap;
+        float rhs = has_q ? __fsub_ru(cut, na) : -CUDART_INF_F;
+        // compact the buffer of query column `src_lane` (all lanes cooperate)
+        auto compact = [&](int src) {
+            const uint32_t c_src = __shfl_sync(0xffffffffu, cnt, src);
+            const uint32_t col = g * 128 + quarter * 32 + src;
+            float* kb = lkey + (size_t)col * LB;
+            uint32_t* pb = lpos + (size_t)col * LB;
+            const float k0 = (uint32_t)lane < c_src ? kb[lane] : CUDART_INF_F;
+            const float k1 = (uint32_t)(lane + 32) < c_src ? kb[lane + 32] : CUDART_INF_F;
+            const uint32_t p0 = (uint32_t)lane < c_src ? pb[lane] : 0u;
+            const uint32_t p1 = (uint32_t)(lane + 32) < c_src ? pb[lane + 32] : 0u;
+            const float kth = warp_kth64(k0, k1, p.K);
+            const float cap_src = __shfl_sync(0xffffffffu, cap, src);
+            const float nc = fminf(__fadd_ru(kth, 2.f * dl), cap_src);
+            const bool keep0 = k0 <= nc, keep1 = k1 <= nc;
+            const unsigned b0 = __ballot_sync(0xffffffffu, keep0);
+            const unsigned b1 = __ballot_sync(0xffffffffu, keep1);
+            const unsigned lt = (1u << lane) - 1u;
+            __syncwarp();
+            if (keep0) {
+                const uint32_t at = __popc(b0 & lt);
+                kb[at] = k0;
+                pb[at] = p0;
+            }
+            if (keep1) {
+                const uint32_t at = __popc(b0) + __popc(b1 & lt);
+                kb[at] = k1;
+                pb[at] = p1;
+            }
+            __syncwarp();
+            if (lane == src) {
+                cnt = __popc(b0) + __popc(b1);
+                cut = nc;
+                rhs = __fsub_ru(cut, na);
+                if (cnt >= LB) {  // every entry inside the band: exact ties, slow path
+                    ovf = true;
+                    rhs = -CUDART_INF_F;
+                }
+            }
+        };
         uint32_t s, c;
         for (uint32_t t = 0; next_tile(s, c); ++t) {
             const int b = t & 1;
             mbar_wait(&bar_accf[b], (t >> 1) & 1);
             fence_after();
             const uint32_t tbase = tmem + ((uint32_t)(quarter * 32) << 16) + (g * 2 + b) * TC_N;
-            for (uint32_t j0 = 0; j0 < c; j0 += 32) {
-                float v[32];
-                tmem_ld32(tbase + j0, v);
+            for (uint32_t j0 = 0; j0 < c; j0 += 64) {
+                float v0[32], v1[32];
+                tmem_ld64(tbase + j0, v0, v1);
                 if (p.dbg && blockIdx.x == 0 && t == 0 && g == 0)
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) p.dbg[r * TC_N + j0 + j] = v[j];
-                if (!has_q || ovf) continue;
-                const uint32_t lim = c - j0;
-                if (lim < 32) {
+                    for (int j = 0; j < 32; ++j) {
+                        p.dbg[r * TC_N + j0 + j] = v0[j];
+                        p.dbg[r * TC_N + j0 + 32 + j] = v1[j];
+                    }
+                const uint32_t lim = c - j0;  // valid columns in this 64-column slab
+                if (lim < 64) {
 #pragma unroll
-                    for (int j = 0; j < 32; ++j)
-                        if ((uint32_t)j >= lim) v[j] = CUDART_NAN_F;  // never passes <=
+                    for (int j = 0; j < 32; ++j) {
+                        if ((uint32_t)j >= lim) v0[j] = CUDART_NAN_F;
+                        if ((uint32_t)(j + 32) >= lim) v1[j] = CUDART_NAN_F;
+                    }
                 }
-                float m[16];
+                float m0[16], m1[16];
 #pragma unroll
-                for (int j = 0; j < 16; ++j) m[j] = fminf(v[j], v[j + 16]);
+                for (int j = 0; j < 16; ++j) {
+                    m0[j] = fminf(v0[j], v0[j + 16]);
+                    m1[j] = fminf(v1[j], v1[j + 16]);
+                }
 #pragma unroll
                 for (int w = 8; w > 0; w >>= 1)
 #pragma unroll
-                    for (int j = 0; j < w; ++j) m[j] = fminf(m[j], m[j + w]);
-                if (!(m[0] <= rhs)) continue;
-                uint32_t mask = 0;
+                    for (int j = 0; j < w; ++j) {
+                        m0[j] = fminf(m0[j], m0[j + w]);
+                        m1[j] = fminf(m1[j], m1[j + w]);
+                    }
+                const bool hit = has_q && !ovf && fminf(m0[0], m1[0]) <= rhs;
+                if (!__any_sync(0xffffffffu, hit)) continue;
+                // rare path
+                unsigned mk[2] = {0u, 0u};
+                if (hit) {
 #pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                    mask |= (v[j] <= rhs ? 1u : 0u) << j;
-                    scr[j * NQ + me] = v[j];
+                    for (int j = 0; j < 32; ++j) {
+                        mk[0] |= (v0[j] <= rhs ? 1u : 0u) << j;
+                        mk[1] |= (v1[j] <= rhs ? 1u : 0u) << j;
+                    }
                 }
-                while (mask) {
-                    const int j = __ffs(mask) - 1;
-                    mask &= mask - 1;
-                    const float vj = scr[j * NQ + me];
-                    if (!(vj <= rhs)) continue;
-                    const uint32_t pos = s + j0 + j;
-                    if (pos == qp) continue;  // self pair: excluded by id
-                    if (cnt == (int)p.L) {
-                        ovf = true;
-                        rhs = -CUDART_INF_F;
-                        break;
-                    }
-                    const float key = vj + na;
-                    int q = cnt;
-                    while (q > 0) {
-                        const float kq = lkey[(q - 1) * NQ + me];
-                        if (kq <= key) break;
-                        lkey[q * NQ + me] = kq;
-                        lpos[q * NQ + me] = lpos[(q - 1) * NQ + me];
-                        --q;
-                    }
-                    lkey[q * NQ + me] = key;
-                    lpos[q * NQ + me] = pos;
-                    ++cnt;
-                    if (cnt >= (int)p.K) {
-                        const float cut_list = __fadd_ru(lkey[(p.K - 1) * NQ + me], 2.f * dl);
-                        const float ce = fminf(cut_list, __fadd_ru(init_cut, dl));
-                        while (cnt > (int)p.K && lkey[(cnt - 1) * NQ + me] > ce) --cnt;
-                        rhs = __fsub_ru(ce, na);
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    unsigned um = __reduce_or_sync(0xffffffffu, mk[h]);
+                    while (um) {
+                        const int j = __ffs(um) - 1;
+                        um &= um - 1;
+                        const float x = tmem_ld1(tbase + j0 + h * 32 + j);
+                        const uint32_t pos = s + j0 + h * 32 + j;
+                        bool want = ((mk[h] >> j) & 1u) && x <= rhs && pos != qp;
+                        // make room: cooperative compaction of every full buffer that needs it
+                        unsigned full = __ballot_sync(0xffffffffu, want && cnt == LB);
+                        while (full) {
+                            const int src = __ffs(full) - 1;
+                            full &= full - 1;
+                            compact(src);
+                        }
+                        want = want && !ovf && x <= rhs;  // cut may have tightened
+                        if (want) {
+                            mykey[cnt] = x + na;
+                            mypos[cnt] = pos;
+                            ++cnt;
+                        }
                     }
                 }
             }
@@ -408,51 +539,85 @@ __global__ void __launch_bounds__(64 + 128 * G, 1)
             if (lane == 0) mbar_arrive(&bar_acce[b]);
         }
         if (has_q) {
-            p.out_cnt[row] = ovf ? OVF : (uint32_t)cnt;
+            p.out_cnt[row] = ovf ? OVF : cnt;
             if (!ovf)
-                for (int i = 0; i < cnt; ++i)
-                    p.out_pos[(uint64_t)row * p.L + i] = lpos[i * NQ + me];
+                for (uint32_t i = 0; i < cnt; ++i) p.out_pos[(uint64_t)row * LB + i] = mypos[i];
         }
     } else {
         // ------------------------------------------------ HISTOGRAM epilogue
         uint32_t* hist = reinterpret_cast<uint32_t*>(tail);          // [n_bins][NQ]
         const float* LO = reinterpret_cast<const float*>(hist + p.n_bins * NQ);
         const float* HI = LO + p.n_bins + 1;
+        uint2* qbuf = reinterpret_cast<uint2*>(const_cast<float*>(HI + p.n_bins + 1)) + e * 32;
         const uint32_t nbins = p.n_bins;
         const float dl = p.delta;
         const float skip_at = has_q ? __fsub_ru(__fadd_ru(LO[nbins], dl), na) : -CUDART_INF_F;
         const float invw = p.inv_width_scaled;
+        uint32_t qn = 0;  // warp-uniform queue fill
+        // resolve queued pairs: one per lane, FP64 scalar order, exact bin
+        auto flush = [&]() {
+            if (lane < qn) {
+                const uint2 pr = qbuf[lane];  // (query column, candidate position)
+                const uint32_t qcol = pr.x & 0xFFFFu;
+                const uint32_t qid = p.qpos[it.x + qcol];
+                const uint32_t bb =
+                    exact_bin(p.X64, p.n, qid, pr.y, p.eps_mean, p.limit_sq, p.inv_width, nbins);
+                if (bb < nbins) atomicAdd(&hist[bb * NQ + qcol], 1u);
+            }
+            __syncwarp();
+            qn = 0;
+        };
         uint32_t s, c;
         for (uint32_t t = 0; next_tile(s, c); ++t) {
             const int b = t & 1;
             mbar_wait(&bar_accf[b], (t >> 1) & 1);
             fence_after();
             const uint32_t tbase = tmem + ((uint32_t)(quarter * 32) << 16) + (g * 2 + b) * TC_N;
-            for (uint32_t j0 = 0; j0 < c; j0 += 32) {
-                float v[32];
-                tmem_ld32(tbase + j0, v);
-                if (!has_q) continue;
-                const uint32_t lim = c - j0;
+            for (uint32_t j0 = 0; j0 < c; j0 += 64) {
+                float v[2][32];
+                tmem_ld64(tbase + j0, v[0], v[1]);
+                const uint32_t lim = has_q ? c - j0 : 0;
+                unsigned am[2] = {0u, 0u};
 #pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                    if ((uint32_t)j >= lim || !(v[j] < skip_at)) continue;  // beyond eps_mean
-                    const uint32_t pos = s + j0 + j;
-                    if (pos == qp) continue;  // self
-                    const float key = v[j] + na;
-                    const float klo = __fsub_rd(key, dl), khi = __fadd_ru(key, dl);
-                    int bin = key > 0.f ? (int)(key * rsqrtf(key) * invw) : 0;
-                    bin = min(bin, (int)nbins - 1);
-                    uint32_t bb;
-                    if (klo >= LO[bin] && khi < HI[bin]) bb = (uint32_t)bin;
-                    else bb = exact_bin(p.X64, p.n, qp, pos, p.eps_mean, p.limit_sq,
-                                        p.inv_width, nbins);
-                    if (bb < nbins) hist[bb * NQ + qi] += 1;
+                for (int h = 0; h < 2; ++h)
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        const uint32_t jj = h * 32 + j;
+                        const uint32_t pos = s + j0 + jj;
+                        if (jj < lim && v[h][j] < skip_at && pos != qp) {
+                            const float key = v[h][j] + na;
+                            const float klo = __fsub_rd(key, dl), khi = __fadd_ru(key, dl);
+                            int bin = key > 0.f ? (int)(key * rsqrtf(key) * invw) : 0;
+                            bin = min(bin, (int)nbins - 1);
+                            if (klo >= LO[bin] && khi < HI[bin]) hist[bin * NQ + qi] += 1;
+                            else am[h] |= 1u << j;
+                        }
+                    }
+                // queue ambiguous pairs (one per lane per round), resolve 32 at a time
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    unsigned mine = am[h];
+                    while (true) {
+                        const bool has = mine != 0u;
+                        const unsigned m = __ballot_sync(0xffffffffu, has);
+                        if (!m) break;
+                        if (qn + __popc(m) > 32) flush();
+                        if (has) {
+                            const int j = __ffs(mine) - 1;
+                            mine &= mine - 1;
+                            qbuf[qn + __popc(m & ((1u << lane) - 1u))] =
+                                make_uint2(qi, s + j0 + h * 32 + j);
+                        }
+                        __syncwarp();
+                        qn += __popc(m);
+                    }
                 }
             }
             fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&bar_acce[b]);
         }
+        flush();
     }
     fence_before();
     __syncthreads();
@@ -488,8 +653,8 @@ size_t tc_smem_bytes(uint32_t row_halfs, uint32_t L, uint32_t n_bins, bool hist)
     const TcShape sh = tc_shape(row_halfs);
     const size_t NQ = 128 * sh.G;
     size_t b = 1024 + (size_t)(sh.G + sh.STAGES) * sh.KB * KB_BYTES;
-    if (hist) b += NQ * n_bins * 4 + 8 * (n_bins + 1);
-    else b += NQ * L * 8 + NQ * 32 * 4;
+    if (hist) b += NQ * n_bins * 4 + 8 * (n_bins + 1) + 8 + (size_t)4 * sh.G * 32 * 8;
+    else b += NQ * L * 8;
     return b;
 }
 size_t tc_join_smem_bytes(int KB, uint32_t L) {

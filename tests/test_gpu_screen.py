@@ -15,15 +15,20 @@ pytestmark = pytest.mark.gpu
 def _tile(engine, q0, c0, n):
     L = engine.lib
     L.knnj_debug_tc_tile.argtypes = [C.c_void_p, C.c_uint32, C.c_uint32, C.c_void_p, C.c_void_p,
-                                     C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+                                     C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                     C.c_void_p, C.c_void_p]
     rh = 64 if 3 * n + 2 <= 64 else 128
     D = np.zeros((128, 128), np.float32)
     Bq = np.zeros((128, rh), np.uint16)
     Bc = np.zeros((128, rh), np.uint16)
     S, dl = C.c_double(), C.c_double()
+    pq = np.zeros(128, np.uint32)
+    pc = np.zeros(128, np.uint32)
     engine._check(L.knnj_debug_tc_tile(engine.h, q0, c0, D.ctypes.data, Bq.ctypes.data,
-                                       Bc.ctypes.data, C.byref(S), C.byref(dl)))
-    return D, Bq.view(np.float16).astype(np.float64), Bc.view(np.float16).astype(np.float64), S.value, dl.value
+                                       Bc.ctypes.data, C.byref(S), C.byref(dl), pq.ctypes.data,
+                                       pc.ctypes.data))
+    return (D, Bq.view(np.float16).astype(np.float64), Bc.view(np.float16).astype(np.float64),
+            S.value, dl.value, pq, pc)
 
 
 @pytest.mark.parametrize("spec,n,shift", [("clusters:16:0.05", 18, 0.0), ("uniform", 12, 0.0),
@@ -35,11 +40,9 @@ def test_tc_accumulator_error_far_below_delta(engine, spec, n, shift):
     engine.reorder_by_variance(6)
     engine.grid_build(6, 0.5)
     W = engine.working_points()
-    info = engine.grid_build(6, 0.5)
-    A = engine.grid_export(info["n_cells"])["A"]
     worst = 0.0
     for q0, c0 in ((0, 0), (1000, 3000), (5800, 17)):
-        D, bq, bc, S, delta = _tile(engine, q0, c0, n)
+        D, bq, bc, S, delta, pq, pc = _tile(engine, q0, c0, n)
         a = np.zeros_like(bq)
         a[:, :n] = -2 * bq[:, :n]
         a[:, n:2 * n] = -2 * bq[:, :n]
@@ -50,7 +53,7 @@ def test_tc_accumulator_error_far_below_delta(engine, spec, n, shift):
         # key vs the exact FP64 distance, in scaled units
         na = bq[:, 3 * n] + bq[:, 3 * n + 1]
         key = D.astype(np.float64) + na.astype(np.float32).astype(np.float64)[:, None]
-        P, Q = W[A[q0:q0 + 128]], W[A[c0:c0 + 128]]
+        P, Q = W[pq], W[pc]
         sq = ((P[:, None, :] - Q[None, :, :]) ** 2).sum(-1) / (S * S)
         assert np.abs(key - sq).max() <= delta, (np.abs(key - sq).max(), delta)
     assert worst < 0.2, worst   # accumulation error uses < 1/5 of the budget

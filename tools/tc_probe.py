@@ -8,7 +8,7 @@ from paper_1810_04758_b200.synthetic import generate
 eng = Engine(0)
 L = eng.lib
 L.knnj_debug_tc_tile.argtypes = [C.c_void_p, C.c_uint32, C.c_uint32, C.c_void_p, C.c_void_p,
-                                 C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+                                 C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_void_p, C.c_void_p]
 X = generate("clusters:16:0.05", 20000, 18, 1)
 eng.set_points(X)
 eng.reorder_by_variance(6)
@@ -19,7 +19,7 @@ rh = 64
 Bq = np.zeros((128, rh), np.uint16); Bc = np.zeros((128, rh), np.uint16)
 S, dl = C.c_double(), C.c_double()
 eng._check(L.knnj_debug_tc_tile(eng.h, 1000, 5000, D.ctypes.data, Bq.ctypes.data, Bc.ctypes.data,
-                                C.byref(S), C.byref(dl)))
+                                C.byref(S), C.byref(dl), np.zeros(128,np.uint32).ctypes.data, np.zeros(128,np.uint32).ctypes.data))
 bq = Bq.view(np.float16).astype(np.float64); bc = Bc.view(np.float16).astype(np.float64)
 A = np.zeros_like(bq)
 A[:, :n] = -2 * bq[:, :n]; A[:, n:2*n] = -2 * bq[:, :n]; A[:, 2*n:3*n] = -2 * bq[:, n:2*n]; A[:, 3*n:3*n+2] = 1
