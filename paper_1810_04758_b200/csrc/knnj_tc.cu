@@ -311,6 +311,9 @@ __global__ void __launch_bounds__(64 + 128 * G, 1)
         float* tab = reinterpret_cast<float*>(hist + p.n_bins * NQ);
         for (uint32_t i = tid; i < p.n_bins * NQ; i += blockDim.x) hist[i] = 0;
         for (uint32_t i = tid; i < 2 * (p.n_bins + 1); i += blockDim.x) tab[i] = p.tables[i];
+        float2* lh = reinterpret_cast<float2*>(tab + 2 * (p.n_bins + 1));
+        for (uint32_t i = tid; i < p.n_bins; i += blockDim.x)
+            lh[i] = make_float2(p.tables[i], p.tables[p.n_bins + 1 + i]);
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     fence_before();
@@ -548,7 +551,8 @@ __global__ void __launch_bounds__(64 + 128 * G, 1)
         uint32_t* hist = reinterpret_cast<uint32_t*>(tail);          // [n_bins][NQ]
         const float* LO = reinterpret_cast<const float*>(hist + p.n_bins * NQ);
         const float* HI = LO + p.n_bins + 1;
-        uint2* qbuf = reinterpret_cast<uint2*>(const_cast<float*>(HI + p.n_bins + 1)) + e * 32;
+        const float2* LH = reinterpret_cast<const float2*>(HI + p.n_bins + 1);  // [n_bins]
+        uint2* qbuf = reinterpret_cast<uint2*>(const_cast<float2*>(LH + p.n_bins)) + e * 32;
         const uint32_t nbins = p.n_bins;
         const float dl = p.delta;
         const float skip_at = has_q ? __fsub_ru(__fadd_ru(LO[nbins], dl), na) : -CUDART_INF_F;
@@ -578,20 +582,25 @@ __global__ void __launch_bounds__(64 + 128 * G, 1)
                 tmem_ld64(tbase + j0, v[0], v[1]);
                 const uint32_t lim = has_q ? c - j0 : 0;
                 unsigned am[2] = {0u, 0u};
+                // branch-free per pair: in range & not self -> exact-certain bin from
+                // key +- delta against the interleaved (LO,HI) edge table, else queue
+                const uint32_t selfj = qp - (s + j0);  // column of the self pair (if any)
 #pragma unroll
                 for (int h = 0; h < 2; ++h)
 #pragma unroll
                     for (int j = 0; j < 32; ++j) {
                         const uint32_t jj = h * 32 + j;
-                        const uint32_t pos = s + j0 + jj;
-                        if (jj < lim && v[h][j] < skip_at && pos != qp) {
-                            const float key = v[h][j] + na;
-                            const float klo = __fsub_rd(key, dl), khi = __fadd_ru(key, dl);
-                            int bin = key > 0.f ? (int)(key * rsqrtf(key) * invw) : 0;
-                            bin = min(bin, (int)nbins - 1);
-                            if (klo >= LO[bin] && khi < HI[bin]) hist[bin * NQ + qi] += 1;
-                            else am[h] |= 1u << j;
-                        }
+                        const float key = v[h][j] + na;
+                        const bool valid = (jj < lim) & (v[h][j] < skip_at) & (jj != selfj);
+                        const float klo = __fsub_rd(key, dl), khi = __fadd_ru(key, dl);
+                        const float rt = fmaxf(key, 1e-30f);
+                        int bin = __float2int_rz(rt * rsqrtf(rt) * invw);
+                        bin = min(bin, (int)nbins - 1);
+                        const float2 edge = LH[bin];
+                        const bool certain = valid & (klo >= edge.x) & (khi < edge.y);
+                        const uint32_t hidx = (uint32_t)bin * NQ + qi;
+                        hist[hidx] += certain ? 1u : 0u;
+                        am[h] |= ((valid & !certain) ? 1u : 0u) << j;
                     }
                 // queue ambiguous pairs (one per lane per round), resolve 32 at a time
 #pragma unroll
@@ -653,7 +662,7 @@ size_t tc_smem_bytes(uint32_t row_halfs, uint32_t L, uint32_t n_bins, bool hist)
     const TcShape sh = tc_shape(row_halfs);
     const size_t NQ = 128 * sh.G;
     size_t b = 1024 + (size_t)(sh.G + sh.STAGES) * sh.KB * KB_BYTES;
-    if (hist) b += NQ * n_bins * 4 + 8 * (n_bins + 1) + 8 + (size_t)4 * sh.G * 32 * 8;
+    if (hist) b += NQ * n_bins * 4 + 8 * (n_bins + 1) + 8 * n_bins + 8 + (size_t)4 * sh.G * 32 * 8;
     else b += NQ * L * 8;
     return b;
 }
