@@ -108,6 +108,24 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def load_peaks() -> dict:
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return {}
+
+
+def profile_traffic():
+    """dram bytes per launch of the join kernel from the committed ncu capture of this
+    workload (profiles/), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "join_traffic.json")) as f:
+            return json.load(f).get("dram_bytes_per_launch")
+    except (OSError, ValueError):
+        return None
+
+
 # ---------------------------------------------------------------------------- reference arm
 def cpu_reference(X, k, sample, seed=1):
     """The reference's RefImpl (SparseOnly: reorder + kd-tree) on a query sample
@@ -234,17 +252,35 @@ def run_ours(args, cfgd, X):
         step_e2e()
     ms_e2e, infos_e2e = timed(step_e2e, args.steps)
 
-    # roofline of the dominant kernel (the fused join): algorithmic FP32 flops =
-    # 3n per candidate pair examined by the reference's 3^m walk
+    # Roofline of the dominant kernel (the fused join), per launch:
+    #  * tcgen05 path: algorithmic tensor flops = 2*(3n+2) per candidate pair of the
+    #    reference 3^m walk (the FP16 hi/lo GEMM form: 3n products + the |b|^2 split),
+    #    against the measured dense bf16/fp16 peak (MEASURED_PEAKS.json);
+    #  * SIMT path: 3n FP32 flops per candidate pair against an
+    #    FFMA microbenchmark measured live.
     info = infos[-1]
     join_ms = statistics.mean(i["ms_join_kernel"] for i in infos)
     hist_ms = statistics.mean(i["ms_hist_kernel"] for i in infos)
     cand = info["candidates_examined"]
-    flops = 3.0 * n * cand
-    achieved = flops / (join_ms * 1e-3) / 1e12
+    flops_3n = 3.0 * n * cand
     peak_c = np.ctypeslib.ctypes.c_double()
     eng._check(lib.knnj_fp32_peak(eng.h, np.ctypeslib.ctypes.byref(peak_c)))
-    peak = peak_c.value
+    fp32_peak = peak_c.value
+    if info["join_tensor_cores"]:
+        flops = 2.0 * (3 * n + 2) * cand
+        peaks = load_peaks()
+        peak = peaks.get("bf16_tflops", 1590.0)
+        peak_src = ("MEASURED_PEAKS.json bf16_tflops (dense, burst; fp16 runs at the bf16 rate)"
+                    if "bf16_tflops" in peaks else "B200_PROFILING.md fallback 1.59 PFLOP/s")
+        bound = "tensor"
+        fdef = "2*(3n+2) tensor flops per candidate pair of the reference 3^m walk (FP16 hi/lo GEMM form)"
+    else:
+        flops = flops_3n
+        peak = fp32_peak
+        peak_src = "FFMA microbenchmark measured live on this GPU (no FP32 figure in MEASURED_PEAKS.json)"
+        bound = "fp32"
+        fdef = "3n FP32 flops per candidate pair of the reference 3^m walk"
+    achieved = flops / (join_ms * 1e-3) / 1e12
     hist_pairs = info["hist_query_count"] * (N - 1)
 
     cpu = None
@@ -271,13 +307,16 @@ def run_ours(args, cfgd, X):
                        "candidates_per_query": cand / N},
             "e2e": {"value": N / (ms_e2e * 1e-3), "unit": UNIT, "h2d_bytes_per_step": N * n * 8,
                     "d2h_bytes_per_step": N * k * 12, "ms_per_step": ms_e2e},
-            "roofline": {"bound": "fp32", "kernel": "k_join (fused range-join + top-K)",
+            "roofline": {"bound": bound,
+                         "kernel": "k_tc<JOIN> (tcgen05 fused range-join + screened top-K)"
+                                   if bound == "tensor" else "k_join (SIMT fused range-join + top-K)",
                          "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": achieved / peak, "traffic": None,
-                         "peak_source": "FFMA microbenchmark measured live on this GPU "
-                                        "(MEASURED_PEAKS.json has no FP32 figure)",
-                         "algorithmic_flops_per_launch": flops,
-                         "flops_definition": "3n per candidate pair of the reference 3^m walk"},
+                         "frac": achieved / peak, "traffic": profile_traffic(),
+                         "peak_source": peak_src,
+                         "algorithmic_flops_per_launch": flops, "flops_definition": fdef,
+                         "kernel_ms": join_ms, "candidate_pairs": cand,
+                         "fp32_3n_equivalent_tflops": flops_3n / (join_ms * 1e-3) / 1e12,
+                         "fp32_peak_measured": fp32_peak},
             "phases_ms": {k2: statistics.mean(i[k2] for i in infos) for k2 in
                           ("ms_reorder", "ms_eps_mean", "ms_histogram", "ms_grid", "ms_split",
                            "ms_join", "ms_fallback", "ms_join_kernel", "ms_hist_kernel")},

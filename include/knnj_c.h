@@ -169,6 +169,8 @@ typedef struct {
     uint64_t fallback_queries, fallback_passes, slow_path_queries;
     uint64_t grid_cells;
     uint64_t kernel_launches;     /* this library's own kernels launched by the call */
+    uint32_t join_tensor_cores;   /* 1: level-0 join ran on the tcgen05 screen, 0: SIMT FP32 */
+    uint32_t hist_tensor_cores;   /* same for the eps histogram */
     /* device-event timings (ms) */
     double ms_upload, ms_reorder, ms_eps_mean, ms_histogram, ms_grid, ms_split, ms_join,
         ms_fallback, ms_download, ms_total;

@@ -65,7 +65,8 @@ RUN_INFO_FIELDS = [
     ("failed_count", C.c_uint64), ("candidates_examined", C.c_uint64),
     ("fallback_queries", C.c_uint64), ("fallback_passes", C.c_uint64),
     ("slow_path_queries", C.c_uint64), ("grid_cells", C.c_uint64),
-    ("kernel_launches", C.c_uint64),
+    ("kernel_launches", C.c_uint64), ("join_tensor_cores", C.c_uint32),
+    ("hist_tensor_cores", C.c_uint32),
 ] + [(f, C.c_double) for f in (
     "ms_upload", "ms_reorder", "ms_eps_mean", "ms_histogram", "ms_grid", "ms_split", "ms_join",
     "ms_fallback", "ms_download", "ms_total", "ms_join_kernel", "ms_hist_kernel")] + [

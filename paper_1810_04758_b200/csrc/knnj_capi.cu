@@ -419,6 +419,7 @@ struct knnj_ctx {
     }
 
     double last_hist_kernel_ms = 0.0;
+    bool last_hist_tc = false;
     void histogram_queries(const uint64_t* qids, uint64_t nq, double em, uint32_t nb,
                            uint64_t* raw) {
         if (!(em > 0.0))
@@ -465,6 +466,7 @@ struct knnj_ctx {
         screen_consts(a.gam, a.erg, a.eab, a.e64);
         if (use_tc() && tc_smem_bytes(3 * n + 2 <= 64 ? 64 : 128, 0, nb, true) <= 227 * 1024) {
             histogram_tc(d_q.p, nq, em, nb, S, d_cnt.p);
+            last_hist_tc = true;
             std::vector<unsigned long long> c(nb);
             KJ_CUDA(cudaMemcpyAsync(c.data(), d_cnt.p, 8 * nb, cudaMemcpyDeviceToHost, s));
             sync();
@@ -483,6 +485,7 @@ struct knnj_ctx {
         slabs = (N + stride - 1) / stride;
         a.cand_begin_stride = stride;
         Timer t(s);
+        last_hist_tc = false;
         launch_histogram(a, slabs, s);
         std::vector<unsigned long long> c(nb);
         KJ_CUDA(cudaMemcpyAsync(c.data(), d_cnt.p, 8 * nb, cudaMemcpyDeviceToHost, s));
@@ -1654,6 +1657,7 @@ int knnj_run(knnj_ctx* c, const knnj_config* cfg, uint32_t* ids, double* dist, u
                 c->histogram_queries(hq.data(), hq.size(), I.eps_mean, cfg->n_bins, raw.data());
                 I.ms_histogram = t.ms();
                 I.ms_hist_kernel = c->last_hist_kernel_ms;
+                I.hist_tensor_cores = c->last_hist_tc ? 1 : 0;
             }
             if (raw_hist) std::memcpy(raw_hist, raw.data(), 8 * cfg->n_bins);
             const double width = I.eps_mean / double(cfg->n_bins);
@@ -1730,6 +1734,7 @@ int knnj_run(knnj_ctx* c, const knnj_config* cfg, uint32_t* ids, double* dist, u
                             o_kth.p, o_st.p, &slow);
                 I.ms_join = t.ms();
                 I.ms_join_kernel = c->last_join_kernel_ms;
+                I.join_tensor_cores = c->last_join_tc ? 1 : 0;
                 // candidates_examined counts dense queries only
                 if (I.q_cpu == 0) I.candidates_examined = P.candidates;
             }
