@@ -152,7 +152,7 @@ def run_reference(args, cfgd, X):
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
         return
     k = cfgd["k"]
-    sample = args.cpu_sample or 1000
+    sample = args.cpu_sample or 2000
     ref = Ref()
     h, t_reorder, t_build = ref.kd_create(X, min(6, X.shape[1]))
     cores = ref.hardware_concurrency()
@@ -211,6 +211,10 @@ def run_ours(args, cfgd, X):
 
     cfg = RunConfig(k=k, mode="hybrid", seed=1)
     eng.set_points((p_in, N, n))
+    shard = None
+    if world > 1:
+        from paper_1810_04758_b200.distributed import torch_allreduce
+        shard = (rank, world, torch_allreduce())
 
     def barrier():
         if world > 1:
@@ -236,12 +240,12 @@ def run_ours(args, cfgd, X):
         return ms, infos
 
     def step_device():
-        r = eng.run(cfg, out=(0, 0, 0), want_hist=False)
+        r = eng.run(cfg, out=(0, 0, 0), want_hist=False, shard=shard)
         return r.info
 
     def step_e2e():
         eng.set_points((p_in, N, n))
-        r = eng.run(cfg, out=(p_ids, p_dist, p_prov), want_hist=False)
+        r = eng.run(cfg, out=(p_ids, p_dist, p_prov), want_hist=False, shard=shard)
         return r.info
 
     for _ in range(args.warmup):
@@ -261,7 +265,9 @@ def run_ours(args, cfgd, X):
     info = infos[-1]
     join_ms = statistics.mean(i["ms_join_kernel"] for i in infos)
     hist_ms = statistics.mean(i["ms_hist_kernel"] for i in infos)
-    cand = info["candidates_examined"]
+    cand = info["join_candidate_pairs"]   # this rank's level-0 join pairs (dense + sparse rows)
+    owned = [i["n_owned"] for i in infos_e2e]
+    d2h = int(owned[-1]) * (k * 12 + 1 + 4 * (world > 1))
     flops_3n = 3.0 * n * cand
     peak_c = np.ctypeslib.ctypes.c_double()
     eng._check(lib.knnj_fp32_peak(eng.h, np.ctypeslib.ctypes.byref(peak_c)))
@@ -285,7 +291,7 @@ def run_ours(args, cfgd, X):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        c = cpu_reference(X, k, args.cpu_sample or 1000)
+        c = cpu_reference(X, k, args.cpu_sample or 15000)
         if c is not None:
             c["ref"].kd_destroy(c["handle"])
             cpu = {"value": c["rate"], "unit": UNIT, "cores": c["cores"], "kind": "reference",
@@ -295,7 +301,7 @@ def run_ours(args, cfgd, X):
 
     if rank == 0:
         line = {
-            "metric": METRIC, "value": world * 0 + N / (ms * 1e-3), "unit": UNIT, "n_gpus": world,
+            "metric": METRIC, "value": N / (ms * 1e-3), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
@@ -304,9 +310,12 @@ def run_ours(args, cfgd, X):
                        "parallelism": f"cell-range query shards x{world}" if world > 1 else "1 GPU",
                        "l2": "inputs (%.0f MB FP64) exceed the 126 MB L2" % (N * n * 8 / 1e6),
                        "eps_used": info["eps_used"], "grid_cells": info["grid_cells"],
-                       "candidates_per_query": cand / N},
+                       "candidates_per_query": info["candidates_examined"] / max(1, info["q_gpu"]),
+                       "hist_bins_counted": info["hist_bins_counted"]},
             "e2e": {"value": N / (ms_e2e * 1e-3), "unit": UNIT, "h2d_bytes_per_step": N * n * 8,
-                    "d2h_bytes_per_step": N * k * 12, "ms_per_step": ms_e2e},
+                    "d2h_bytes_per_step": d2h, "ms_per_step": ms_e2e,
+                    "path": "knnj_set_points (pinned H2D) + knnj_run%s + D2H of ids/dist/prov" %
+                            ("_shard" if world > 1 else "")},
             "roofline": {"bound": bound,
                          "kernel": "k_tc<JOIN> (tcgen05 fused range-join + screened top-K)"
                                    if bound == "tensor" else "k_join (SIMT fused range-join + top-K)",
@@ -319,7 +328,8 @@ def run_ours(args, cfgd, X):
                          "fp32_peak_measured": fp32_peak},
             "phases_ms": {k2: statistics.mean(i[k2] for i in infos) for k2 in
                           ("ms_reorder", "ms_eps_mean", "ms_histogram", "ms_grid", "ms_split",
-                           "ms_join", "ms_fallback", "ms_join_kernel", "ms_hist_kernel")},
+                           "ms_join", "ms_fallback", "ms_join_kernel", "ms_hist_kernel", "ms_join_build",
+                           "ms_download")},
             "hist_pairs_per_s": hist_pairs / (hist_ms * 1e-3) if hist_ms > 0 else None,
             "gpu_launches": int(info["kernel_launches"]),
             "clocks": clk.summary(),

@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define KNNJ_ABI_VERSION 1
+#define KNNJ_ABI_VERSION 2
 
 enum knnj_status {
     KNNJ_OK = 0,
@@ -64,7 +64,10 @@ void* knnj_stream(knnj_ctx* ctx);
  * the roofline denominator for the SIMT distance kernels. */
 int knnj_fp32_peak(knnj_ctx* ctx, double* tflops);
 /* Engine knobs (no reference analogue; results never depend on them):
- *   "tensor_cores" 0/1 : allow the tcgen05 distance screen (default 1). */
+ *   "tensor_cores" 0/1 : allow the tcgen05 distance screen (default 1).
+ *   "hist_cap" 0/1/2   : eps-selection histogram counts only the bins select_eps_beta
+ *                        needs when the profile is not requested: 0 never, 1 when the
+ *                        histogram is large (default), 2 always (tests). */
 int knnj_set_option(knnj_ctx* ctx, const char* name, int64_t value);
 /* Page-locked host buffers for the end-to-end path (H2D/D2H at full PCIe rate). */
 void* knnj_alloc_pinned(size_t bytes);
@@ -171,10 +174,14 @@ typedef struct {
     uint64_t kernel_launches;     /* this library's own kernels launched by the call */
     uint32_t join_tensor_cores;   /* 1: level-0 join ran on the tcgen05 screen, 0: SIMT FP32 */
     uint32_t hist_tensor_cores;   /* same for the eps histogram */
+    uint32_t hist_bins_counted;   /* bins counted exactly (n_bins unless the histogram was capped) */
+    uint64_t n_owned;             /* query rows this call (shard) produced */
+    uint64_t join_candidate_pairs;/* candidate pairs of the level-0 join over the owned queries */
     /* device-event timings (ms) */
     double ms_upload, ms_reorder, ms_eps_mean, ms_histogram, ms_grid, ms_split, ms_join,
         ms_fallback, ms_download, ms_total;
     double ms_join_kernel, ms_hist_kernel;
+    double ms_join_build;         /* work-item / adjacency construction of the level-0 pass */
     uint32_t perm[1024];
 } knnj_run_info;
 
@@ -187,6 +194,30 @@ typedef struct {
  * k_effective = min(k, |D|-1) (orchestrator.cpp:77-82). */
 int knnj_run(knnj_ctx* ctx, const knnj_config* cfg, uint32_t* ids, double* dist, uint8_t* prov,
              uint64_t* raw_hist, knnj_run_info* info);
+
+/* ---- multi-GPU: one process per GPU, queries sharded by cell range ------
+ * Sum `count` u64 values element-wise over every shard, in place (e.g. an
+ * ncclAllReduce / torch.distributed.all_reduce issued by the caller). Returns 0 on success. */
+typedef int (*knnj_allreduce_fn)(uint64_t* data, uint64_t count, void* user);
+/* The cell-range partition knnj_run_shard uses (host-only, no GPU needed): items
+ * 0..n_items-1 in cell order with estimated costs; shard k owns the contiguous run
+ * [*first, *last) holding the items whose cost midpoint falls in the k-th equal
+ * share of the total. The runs of shards 0..shard_count-1 tile [0, n_items). */
+int knnj_shard_range(const double* cost, uint64_t n_items, uint32_t shard_index,
+                     uint32_t shard_count, uint64_t* first, uint64_t* last);
+/* knnj_run as shard `shard_index` of `shard_count` identical calls (one per GPU,
+ * same points and config). Every shard rebuilds the reorder, eps, grid and split
+ * redundantly (deterministic, identical); the sampled histogram queries are split
+ * evenly and their counts summed through `allreduce` (the run's only exchange); the
+ * join + fallback run only for this shard's contiguous range of grid cells, cut at
+ * equal estimated work. Outputs are this shard's rows, compacted in ascending query
+ * id: owned_queries[n_owned], ids/dist[n_owned * k_effective], prov[n_owned]
+ * (info->n_owned; size the buffers for the whole query set). The union over shards
+ * equals knnj_run's output. shard_count == 1 is knnj_run. */
+int knnj_run_shard(knnj_ctx* ctx, const knnj_config* cfg, uint32_t shard_index,
+                   uint32_t shard_count, knnj_allreduce_fn allreduce, void* allreduce_user,
+                   uint32_t* ids, double* dist, uint8_t* prov, uint32_t* owned_queries,
+                   uint64_t* raw_hist, knnj_run_info* info);
 
 #ifdef __cplusplus
 }

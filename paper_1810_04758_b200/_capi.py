@@ -66,10 +66,12 @@ RUN_INFO_FIELDS = [
     ("fallback_queries", C.c_uint64), ("fallback_passes", C.c_uint64),
     ("slow_path_queries", C.c_uint64), ("grid_cells", C.c_uint64),
     ("kernel_launches", C.c_uint64), ("join_tensor_cores", C.c_uint32),
-    ("hist_tensor_cores", C.c_uint32),
+    ("hist_tensor_cores", C.c_uint32), ("hist_bins_counted", C.c_uint32),
+    ("n_owned", C.c_uint64), ("join_candidate_pairs", C.c_uint64),
 ] + [(f, C.c_double) for f in (
     "ms_upload", "ms_reorder", "ms_eps_mean", "ms_histogram", "ms_grid", "ms_split", "ms_join",
-    "ms_fallback", "ms_download", "ms_total", "ms_join_kernel", "ms_hist_kernel")] + [
+    "ms_fallback", "ms_download", "ms_total", "ms_join_kernel", "ms_hist_kernel",
+    "ms_join_build")] + [
     ("perm", C.c_uint32 * 1024)]
 
 
@@ -114,6 +116,15 @@ SIGNATURES = [
     ("knnj_run", C.c_int, [_vp, C.POINTER(Config), _vp, _vp, _vp, _vp, C.POINTER(RunInfo)]),
 ]
 
+# int (*knnj_allreduce_fn)(uint64_t* data, uint64_t count, void* user)
+ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.POINTER(C.c_uint64), C.c_uint64, C.c_void_p)
+SIGNATURES.append(
+    ("knnj_shard_range", C.c_int, [_dp, C.c_uint64, C.c_uint32, C.c_uint32,
+                                   C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]))
+SIGNATURES.append(
+    ("knnj_run_shard", C.c_int, [_vp, C.POINTER(Config), C.c_uint32, C.c_uint32, ALLREDUCE_FN,
+                                 _vp, _vp, _vp, _vp, _vp, _vp, C.POINTER(RunInfo)]))
+
 _LIB = None
 
 
@@ -122,7 +133,7 @@ def load_library(path: str | None = None) -> C.CDLL:
     global _LIB
     if _LIB is not None and path is None:
         return _LIB
-    p = path or LIB_PATH
+    p = path or os.environ.get("KNNJ_LIB_PATH") or LIB_PATH  # env: dev A/B of library builds
     if not os.path.exists(p):
         raise ImportError(f"{p} not built: run `python -c 'import __graft_entry__ as g; g.build()'`"
                           " or `make -C paper_1810_04758_b200`")

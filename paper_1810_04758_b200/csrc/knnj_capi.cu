@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <functional>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -30,6 +31,42 @@ namespace kj {
 cudaStream_t& alloc_stream() {
     static thread_local cudaStream_t s = nullptr;
     return s;
+}
+BlockCache*& alloc_cache() {
+    static thread_local BlockCache* c = nullptr;
+    return c;
+}
+void* BlockCache::get(size_t bytes, size_t& got, cudaStream_t s) {
+    // best fit among cached blocks no larger than 2x the request (+1 MiB)
+    auto it = free_blocks.lower_bound(bytes);
+    if (it != free_blocks.end() && it->first <= 2 * bytes + (1u << 20)) {
+        void* p = it->second;
+        got = it->first;
+        free_blocks.erase(it);
+        return p;
+    }
+    void* p = nullptr;
+    got = bytes;
+    if (cudaMallocAsync(&p, bytes, s) != cudaSuccess) {
+        // out of memory: hand every cached free block back to the driver and retry
+        cudaGetLastError();
+        cudaStreamSynchronize(s);
+        for (auto& fb : free_blocks) {
+            cudaFree(fb.second);
+            for (auto o = owned.begin(); o != owned.end(); ++o)
+                if (o->first == fb.second) {
+                    owned.erase(o);
+                    break;
+                }
+        }
+        free_blocks.clear();
+        KJ_CUDA(cudaMallocAsync(&p, bytes, s));
+    }
+    owned.emplace_back(p, bytes);
+    return p;
+}
+BlockCache::~BlockCache() {
+    for (auto& b : owned) cudaFree(b.first);
 }
 }  // namespace kj
 
@@ -60,14 +97,6 @@ void sort_pairs_u32_u32(Scratch& sc, const uint32_t* kin, uint32_t* kout, const 
     KJ_CUDA(cub::DeviceRadixSort::SortPairs(sc.get(bytes), bytes, kin, kout, vin, vout,
                                             (int64_t)n, 0, end_bit, s));
 }
-void sort_desc_u64_u32(Scratch& sc, const unsigned long long* kin, unsigned long long* kout,
-                       const uint32_t* vin, uint32_t* vout, uint64_t n, cudaStream_t s) {
-    size_t bytes = 0;
-    KJ_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, bytes, kin, kout, vin, vout,
-                                                      (int64_t)n, 0, 64, s));
-    KJ_CUDA(cub::DeviceRadixSort::SortPairsDescending(sc.get(bytes), bytes, kin, kout, vin, vout,
-                                                      (int64_t)n, 0, 64, s));
-}
 template <class T>
 void inclusive_sum(Scratch& sc, const T* in, T* out, uint64_t n, cudaStream_t s) {
     size_t bytes = 0;
@@ -94,6 +123,29 @@ void reduce_sum(Scratch& sc, const T* in, T* out, uint64_t n, cudaStream_t s) {
     size_t bytes = 0;
     KJ_CUDA(cub::DeviceReduce::Sum(nullptr, bytes, in, out, (int64_t)n, s));
     KJ_CUDA(cub::DeviceReduce::Sum(sc.get(bytes), bytes, in, out, (int64_t)n, s));
+}
+
+// Contiguous run [first, last) of n items owned by shard `sh` of `ns`: item i goes to
+// the shard whose equal-cost slice of the prefix sum contains i's cost midpoint.
+void shard_range(const double* cost, uint64_t n, uint32_t sh, uint32_t ns, uint64_t* first,
+                 uint64_t* last) {
+    std::vector<double> pre(n + 1, 0.0);
+    for (uint64_t i = 0; i < n; ++i) pre[i + 1] = pre[i] + cost[i];
+    const double W = pre[n];
+    auto cut = [&](uint32_t k) -> uint64_t {
+        if (k == 0) return 0;
+        if (k >= ns) return n;
+        const double at = W * double(k) / double(ns);
+        uint64_t lo = 0, hi = n;
+        while (lo < hi) {
+            const uint64_t mid = (lo + hi) / 2;
+            if (0.5 * (pre[mid] + pre[mid + 1]) < at) lo = mid + 1;
+            else hi = mid;
+        }
+        return lo;
+    };
+    *first = cut(sh);
+    *last = cut(sh + 1);
 }
 
 int bits_for(uint64_t maxval) {
@@ -156,6 +208,28 @@ uint64_t splitmix64(uint64_t x) {
 }
 uint64_t derive_seed(uint64_t master, uint64_t tag) { return splitmix64(master ^ splitmix64(tag)); }
 
+// KNNJ_TRACE=1: host wall-clock marks of the runtime's sub-steps on stderr (dev aid)
+struct Trace {
+    bool on = false;
+    std::chrono::steady_clock::time_point last = std::chrono::steady_clock::now();
+    Trace() {
+        const char* e = std::getenv("KNNJ_TRACE");
+        on = e && e[0] && e[0] != '0';
+    }
+    void mark(const char* what, cudaStream_t s = nullptr) {
+        if (!on) return;
+        if (s) cudaStreamSynchronize(s);
+        const auto now = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[knnj] %-28s %9.3f ms\n", what,
+                     std::chrono::duration<double, std::milli>(now - last).count());
+        last = now;
+    }
+};
+Trace& trace() {
+    static Trace t;
+    return t;
+}
+
 struct Timer {
     cudaEvent_t a, b;
     cudaStream_t s;
@@ -183,6 +257,7 @@ struct Timer {
 struct knnj_ctx {
     int dev = 0;
     cudaStream_t s = nullptr;
+    BlockCache cache;  // declared first: destroyed after every DBuf member returned its block
     std::string err;
     Scratch sc;
 
@@ -421,7 +496,12 @@ struct knnj_ctx {
     double last_hist_kernel_ms = 0.0;
     bool last_hist_tc = false;
     void histogram_queries(const uint64_t* qids, uint64_t nq, double em, uint32_t nb,
-                           uint64_t* raw) {
+                           uint64_t* raw, uint32_t ncount = 0) {
+        if (ncount == 0 || ncount > nb) ncount = nb;
+        if (nq == 0) {
+            last_hist_kernel_ms = 0.0;
+            return;
+        }
         if (!(em > 0.0))
             throw Error(4, "mean pairwise distance is not positive; cannot build a distance histogram");
         if (nb < 2) throw Error(1, "histogram needs at least 2 bins");
@@ -457,6 +537,7 @@ struct knnj_ctx {
         a.q = d_q.p;
         a.nq = nq;
         a.n_bins = nb;
+        a.n_count = ncount;
         a.SU = d_tab.p;
         a.SD = d_tab.p + nb + 1;
         a.eps_mean = em;
@@ -465,7 +546,7 @@ struct knnj_ctx {
         a.counts = d_cnt.p;
         screen_consts(a.gam, a.erg, a.eab, a.e64);
         if (use_tc() && tc_smem_bytes(3 * n + 2 <= 64 ? 64 : 128, 0, nb, true) <= 227 * 1024) {
-            histogram_tc(d_q.p, nq, em, nb, S, d_cnt.p);
+            histogram_tc(d_q.p, nq, em, nb, ncount, S, d_cnt.p);
             last_hist_tc = true;
             std::vector<unsigned long long> c(nb);
             KJ_CUDA(cudaMemcpyAsync(c.data(), d_cnt.p, 8 * nb, cudaMemcpyDeviceToHost, s));
@@ -498,7 +579,7 @@ struct knnj_ctx {
     DBuf<__half> Bh_id;
     bool bh_id_ready = false;
     uint32_t bh_id_row = 0;
-    void histogram_tc(const uint32_t* d_q, uint64_t nq, double em, uint32_t nb,
+    void histogram_tc(const uint32_t* d_q, uint64_t nq, double em, uint32_t nb, uint32_t ncount,
                       const std::vector<double>& S_thr, unsigned long long* d_cnt) {
         const uint32_t row_halfs = 3 * n + 2 <= 64 ? 64 : 128;
         if (!bh_id_ready || bh_id_row != row_halfs) {
@@ -552,6 +633,7 @@ struct knnj_ctx {
         a.L = 1;
         a.delta = f32_round_up(tc_delta());
         a.n_bins = nb;
+        a.n_count = ncount;
         a.tables = d_tab.p;
         a.inv_width_scaled = (float)(Ssc / width);
         a.X64 = X64.p;
@@ -562,6 +644,76 @@ struct knnj_ctx {
         Timer t(s);
         launch_hist_tc(a, items.size(), N, s);
         last_hist_kernel_ms = t.ms();
+    }
+
+    // Counts select_eps_beta (epsilon.cpp:122-141) needs, for the sampled queries hq
+    // (this shard's contiguous slice of them when sharded; `reduce` sums a u64 vector
+    // over all shards). Exact for every bin when `full` (the profile was requested).
+    // Otherwise a pilot slice (every 32nd sampled query) is binned in full to place a
+    // cap where its cumulative count passes 2x the target; the other queries only count
+    // bins below the cap (their pairs beyond it leave through a one-compare fast path),
+    // and the result is exact for bins [0, returned) with the cumulative count already
+    // >= target there, so lower_bound selects the same bin as with the full histogram.
+    // If the capped counts fall short, the rest is re-binned in full.
+    int hist_cap_mode = 1;  // 0: never cap, 1: cap when the histogram is large, 2: always
+    double last_hist_ms_pilot = 0.0;
+    uint32_t hist_for_selection(const std::vector<uint64_t>& hq, uint32_t shard, uint32_t nshard,
+                                double em, uint32_t nb, double target, bool full,
+                                const std::function<void(uint64_t*, uint64_t)>& reduce,
+                                uint64_t* raw) {
+        const uint64_t nq = hq.size();
+        const uint64_t lo = nq * shard / nshard, hi = nq * (shard + 1) / nshard;
+        std::fill(raw, raw + nb, 0ull);
+        const double pairs = double(nq) * double(N);
+        const bool cap = !full && hist_cap_mode != 0 && nb > 2 &&
+                         (hist_cap_mode == 2 || pairs >= 268435456.0);
+        double kms = 0.0;
+        if (!cap) {
+            histogram_queries(hq.data() + lo, hi - lo, em, nb, raw);
+            kms += last_hist_kernel_ms;
+            reduce(raw, nb);
+            last_hist_kernel_ms = kms;
+            return nb;
+        }
+        constexpr uint64_t STRIDE = 32;
+        std::vector<uint64_t> pilot, rest;
+        for (uint64_t i = lo; i < hi; ++i) (i % STRIDE == 0 ? pilot : rest).push_back(hq[i]);
+        const uint64_t npilot = (nq + STRIDE - 1) / STRIDE;  // over all shards
+        std::vector<uint64_t> praw(nb, 0), rraw(nb, 0);
+        histogram_queries(pilot.data(), pilot.size(), em, nb, praw.data());
+        kms += last_hist_kernel_ms;
+        last_hist_ms_pilot = last_hist_kernel_ms;
+        reduce(praw.data(), nb);
+        uint32_t bcap = nb;
+        uint64_t run = 0;
+        for (uint32_t b = 0; b < nb; ++b) {
+            run += praw[b];
+            if (double(run) / double(npilot) >= 2.0 * target) {
+                bcap = std::min<uint32_t>(nb, b + 3);
+                break;
+            }
+        }
+        if (bcap < nb) {
+            histogram_queries(rest.data(), rest.size(), em, nb, rraw.data(), bcap);
+            kms += last_hist_kernel_ms;
+            reduce(rraw.data(), nb);
+            run = 0;
+            for (uint32_t b = 0; b < bcap; ++b) {
+                raw[b] = praw[b] + rraw[b];
+                run += raw[b];
+            }
+            if (double(run) / double(nq) >= target) {
+                last_hist_kernel_ms = kms;
+                return bcap;
+            }
+            std::fill(rraw.begin(), rraw.end(), 0ull);
+        }
+        histogram_queries(rest.data(), rest.size(), em, nb, rraw.data());
+        kms += last_hist_kernel_ms;
+        reduce(rraw.data(), nb);
+        for (uint32_t b = 0; b < nb; ++b) raw[b] = praw[b] + rraw[b];
+        last_hist_kernel_ms = kms;
+        return nb;
     }
 
     std::vector<uint64_t> histogram_sample(double frac, uint64_t seed) {
@@ -759,9 +911,16 @@ struct knnj_ctx {
         return pass_uses_tc(lv, K) ? tc_queries_per_item(lv.row_halfs ? lv.row_halfs : 64)
                                    : (uint32_t)JB;
     }
+    // Sharded (nshard > 1): only a contiguous run of work items in cell order is kept
+    // (SURVEY.md §8e), cut at equal shares of the estimated tile work; the pass then
+    // covers query positions [row_begin, row_begin + nq) of the cell-ordered list.
     void build_pass(Level& lv, const uint32_t* d_qpid, const uint32_t* d_qrow, uint64_t nq,
-                    Pass& P, uint32_t K = 0) {
+                    Pass& P, uint32_t K = 0, uint32_t shard = 0, uint32_t nshard = 1,
+                    const uint8_t* d_dense = nullptr) {
         P.nq = nq;
+        P.nq_all = nq;
+        P.row_begin = 0;
+        P.candidates_dense = 0;
         const uint32_t chunk = K ? pass_chunk(lv, K) : (uint32_t)JB;
         P.chunk = chunk;
         P.nitems = P.nadj = P.candidates = 0;
@@ -825,30 +984,72 @@ struct knnj_ctx {
         launch_adj_fill(lv.B.p, lv.G.p, lv.ncells, ucell.p, nuc, lv.m, d_cs.p, d_cs.p + lv.m,
                         adj_off.p, P.adj.p, csize.p, s);
         DBuf<uint4> items_unsorted;
-        DBuf<unsigned long long> work, work_sorted, d_tot;
-        DBuf<uint32_t> iidx, iidx_sorted;
+        DBuf<unsigned long long> work;
         items_unsorted.ensure(tot);
         work.ensure(tot);
         launch_items(ufirst.p, ucnt.p, item_off.p, adj_off.p, nuc, csize.p, items_unsorted.p,
                      work.p, chunk, s);
-        d_tot.ensure(1);
-        reduce_sum(sc, work.p, d_tot.p, tot, s);
-        unsigned long long cand = 0;
-        KJ_CUDA(cudaMemcpyAsync(&cand, d_tot.p, 8, cudaMemcpyDeviceToHost, s));
-        // heaviest items first (LPT order for the block scheduler)
-        iidx.ensure(tot);
-        iidx_sorted.ensure(tot);
-        work_sorted.ensure(tot);
-        launch_iota(iidx.p, tot, s);
-        sort_desc_u64_u32(sc, work.p, work_sorted.p, iidx.p, iidx_sorted.p, tot, s);
-        std::vector<uint32_t> order(tot);
-        std::vector<uint4> h_items(tot), h_sorted(tot);
-        KJ_CUDA(cudaMemcpyAsync(order.data(), iidx_sorted.p, 4 * tot, cudaMemcpyDeviceToHost, s));
+        std::vector<uint4> h_items(tot);
+        std::vector<unsigned long long> h_work(tot);
         KJ_CUDA(cudaMemcpyAsync(h_items.data(), items_unsorted.p, 16 * tot, cudaMemcpyDeviceToHost, s));
+        KJ_CUDA(cudaMemcpyAsync(h_work.data(), work.p, 8 * tot, cudaMemcpyDeviceToHost, s));
         sync();
-        for (uint64_t i = 0; i < tot; ++i) h_sorted[i] = h_items[order[i]];
-        P.items.ensure(tot);
-        KJ_CUDA(cudaMemcpyAsync(P.items.p, h_sorted.data(), 16 * tot, cudaMemcpyHostToDevice, s));
+        // items are in cell order here; a shard keeps a contiguous run of them
+        uint64_t i0 = 0, i1 = tot;
+        if (nshard > 1) {
+            // cost of an item ~ its candidate tiles (+ a fixed per-item overhead)
+            std::vector<double> cost(tot);
+            for (uint64_t i = 0; i < tot; ++i) {
+                const uint32_t q = h_items[i].y - h_items[i].x;
+                cost[i] = (q ? double(h_work[i] / q) : 0.0) + 8.0 * 128.0;
+            }
+            shard_range(cost.data(), tot, shard, nshard, &i0, &i1);
+        }
+        const uint32_t r0 = i0 < i1 ? h_items[i0].x : 0;
+        const uint32_t r1 = i0 < i1 ? h_items[i1 - 1].y : 0;
+        if (d_dense && i0 < i1) {
+            DBuf<unsigned long long> d_dc;
+            d_dc.ensure(1);
+            KJ_CUDA(cudaMemsetAsync(d_dc.p, 0, 8, s));
+            launch_dense_cand(items_unsorted.p + i0, work.p + i0, i1 - i0, P.qrow.p, d_dense,
+                              d_dc.p, s);
+            unsigned long long dc = 0;
+            KJ_CUDA(cudaMemcpyAsync(&dc, d_dc.p, 8, cudaMemcpyDeviceToHost, s));
+            sync();
+            P.candidates_dense = dc;
+        }
+        // heaviest items first (LPT order for the block scheduler); ties keep cell order
+        std::vector<uint32_t> order(i1 - i0);
+        std::iota(order.begin(), order.end(), 0u);
+        std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) {
+            return h_work[i0 + a] > h_work[i0 + b];
+        });
+        std::vector<uint4> h_sorted(i1 - i0);
+        unsigned long long cand = 0;
+        for (uint64_t i = 0; i < i1 - i0; ++i) {
+            uint4 it = h_items[i0 + order[i]];
+            it.x -= r0;
+            it.y -= r0;
+            h_sorted[i] = it;
+            cand += h_work[i0 + order[i]];
+        }
+        if (r0 != 0 || r1 != nq) {
+            DBuf<uint32_t> qp2, qr2;
+            qp2.ensure(r1 - r0);
+            qr2.ensure(r1 - r0);
+            if (r1 > r0) {
+                KJ_CUDA(cudaMemcpyAsync(qp2.p, P.qpos.p + r0, 4ull * (r1 - r0), cudaMemcpyDeviceToDevice, s));
+                KJ_CUDA(cudaMemcpyAsync(qr2.p, P.qrow.p + r0, 4ull * (r1 - r0), cudaMemcpyDeviceToDevice, s));
+            }
+            P.qpos.swap(qp2);
+            P.qrow.swap(qr2);
+        }
+        P.nq = r1 - r0;
+        P.row_begin = r0;
+        P.nitems = i1 - i0;
+        P.items.ensure(P.nitems);
+        if (P.nitems)
+            KJ_CUDA(cudaMemcpyAsync(P.items.p, h_sorted.data(), 16 * P.nitems, cudaMemcpyHostToDevice, s));
         sync();
         P.candidates = cand;
     }
@@ -893,6 +1094,7 @@ struct knnj_ctx {
             a.out_cnt = cnt.p;
             a.out_pos = pos.p;
             a.delta = f32_round_up(tc_delta());
+            trace().mark("pass: pre-kernel", s);
             Timer t(s);
             launch_join_tc(a, P.nitems, N, s);
             last_join_kernel_ms = t.ms();
@@ -933,24 +1135,27 @@ struct knnj_ctx {
         f.out_dist = out_dist;
         f.out_kth = out_kth;
         f.out_status = out_status;
+        trace().mark("pass: join kernel", s);
         launch_finalize(f, s);
-        // overflowed rows -> exact slow path on the same candidate sets
-        std::vector<uint32_t> h_cnt(P.nq);
-        KJ_CUDA(cudaMemcpyAsync(h_cnt.data(), cnt.p, 4 * P.nq, cudaMemcpyDeviceToHost, s));
+        trace().mark("pass: finalize", s);
+        // overflowed rows -> exact slow path on the same candidate sets (rows found on device)
+        DBuf<uint32_t> d_rows;
+        d_rows.ensure(P.nq);
+        d_u64b.ensure(1);
+        KJ_CUDA(cudaMemsetAsync(d_u64b.p, 0, 8, s));
+        launch_find_ovf(cnt.p, P.nq, d_rows.p, d_u64b.p, s);
+        unsigned long long novf = 0;
+        KJ_CUDA(cudaMemcpyAsync(&novf, d_u64b.p, 8, cudaMemcpyDeviceToHost, s));
         sync();
-        std::vector<uint32_t> rows;
-        for (uint64_t r = 0; r < P.nq; ++r)
-            if (h_cnt[r] == OVF) rows.push_back((uint32_t)r);
-        if (n_slow) *n_slow += rows.size();
-        if (!rows.empty()) {
-            DBuf<uint32_t> d_rows, row_item;
-            d_rows.ensure(rows.size());
+        trace().mark("pass: ovf scan", s);
+        if (n_slow) *n_slow += novf;
+        if (novf) {
+            DBuf<uint32_t> row_item;
             row_item.ensure(P.nq);
-            KJ_CUDA(cudaMemcpyAsync(d_rows.p, rows.data(), 4 * rows.size(), cudaMemcpyHostToDevice, s));
             launch_row_item(P.items.p, P.nitems, row_item.p, s);
-            launch_slow_exact(X64.p, n, lv.J.p, P.qpos.p, P.qrow.p, d_rows.p, rows.size(),
-                              P.items.p, row_item.p, P.adj.p, K, eps2, cov2, out_ids, out_dist,
-                              out_kth, out_status, s);
+            launch_slow_exact(X64.p, n, lv.J.p, P.qpos.p, P.qrow.p, d_rows.p, novf, P.items.p,
+                              row_item.p, P.adj.p, K, eps2, cov2, out_ids, out_dist, out_kth,
+                              out_status, s);
             sync();
         }
     }
@@ -998,7 +1203,9 @@ struct knnj_ctx {
                 }
             }
             Level& lv = levels[L];
+            trace().mark("levels: select", s);
             build_level(L, m, std::ldexp(w0, L));
+            trace().mark("levels: build_level", s);
             const double cov2 = cover2(lv);
             const uint64_t np = sp.size();
             DBuf<uint32_t> d_p, d_r;
@@ -1012,6 +1219,7 @@ struct knnj_ctx {
                                     cudaMemcpyHostToDevice, s));
             Pass P;
             build_pass(lv, d_p.p, d_r.p, np, P, K);
+            trace().mark("levels: build_pass", s);
             launch_gather_f32(P.qrow.p, d_cut_by_row.p, np, d_cut.p, s);
             run_pass(lv, P, K, d_cut.p, -1.0, cov2, out_ids, out_dist, out_kth, out_status, n_slow);
             if (passes) ++*passes;
@@ -1051,6 +1259,7 @@ int guarded(knnj_ctx* ctx, F&& f) {
         if (ctx) {
             KJ_CUDA(cudaSetDevice(ctx->dev));
             alloc_stream() = ctx->s;
+            alloc_cache() = &ctx->cache;
         }
         f();
         return KNNJ_OK;
@@ -1098,14 +1307,13 @@ void knnj_destroy(knnj_ctx* ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->dev);
     alloc_stream() = ctx->s;
+    alloc_cache() = &ctx->cache;
     cudaStreamSynchronize(ctx->s);
-    {
-        cudaStream_t keep = ctx->s;
-        ctx->s = nullptr;  // members free on `keep` first, then the stream goes
-        delete ctx;
-        cudaStreamSynchronize(keep);
-        cudaStreamDestroy(keep);
-    }
+    cudaStream_t keep = ctx->s;
+    ctx->s = nullptr;
+    delete ctx;  // DBuf members hand their blocks back; the cache (destroyed last) frees them all
+    alloc_cache() = nullptr;
+    cudaStreamDestroy(keep);
 }
 
 const char* knnj_last_error(const knnj_ctx* ctx) { return ctx ? ctx->err.c_str() : "null ctx"; }
@@ -1171,6 +1379,9 @@ int knnj_set_option(knnj_ctx* c, const char* name, int64_t value) {
         const std::string k = name ? name : "";
         if (k == "tensor_cores") {
             c->tc_enabled = value != 0;
+        } else if (k == "hist_cap") {
+            if (value < 0 || value > 2) throw Error(1, "hist_cap must be 0, 1 or 2");
+            c->hist_cap_mode = (int)value;
         } else {
             throw Error(1, "unknown option '" + k + "'");
         }
@@ -1523,287 +1734,403 @@ int knnj_exact_knn(knnj_ctx* c, const uint32_t* q, uint64_t nq, uint32_t k, uint
     });
 }
 
-// run_hybrid (orchestrator.cpp:67-250)
-int knnj_run(knnj_ctx* c, const knnj_config* cfg, uint32_t* ids, double* dist, uint8_t* prov,
-             uint64_t* raw_hist, knnj_run_info* info) {
-    return guarded(c, [&] {
-        need_points(c);
-        auto t_start = std::chrono::steady_clock::now();
-        knnj_run_info I;
-        std::memset(&I, 0, sizeof(I));
-        const uint64_t N = c->N;
-        const uint32_t n = c->n;
-        // validate_config (orchestrator.cpp:16-31)
-        if (cfg->k < 1) throw Error(1, "k must be at least 1");
-        if (cfg->m > n) throw Error(1, "m must satisfy m <= n");
-        if (cfg->beta < 0 || cfg->beta > 1 || cfg->gamma < 0 || cfg->gamma > 1 || cfg->rho < 0 ||
-            cfg->rho > 1)
-            throw Error(1, "beta, gamma, rho must all be in [0, 1]");
-        if (!(cfg->hist_query_fraction > 0) || cfg->hist_query_fraction > 1)
-            throw Error(1, "sample fractions must be in (0, 1]");
-        if (cfg->n_bins < 2) throw Error(1, "n_bins must be at least 2");
-        if (cfg->mode > 3) throw Error(1, "unknown engine mode");
-        std::vector<uint32_t> queries;
-        if (cfg->query_subset) {
-            for (uint64_t i = 0; i < cfg->n_query_subset; ++i)
-                if (cfg->query_subset[i] >= N) throw Error(1, "query subset id out of range");
-            queries.assign(cfg->query_subset, cfg->query_subset + cfg->n_query_subset);
-            std::sort(queries.begin(), queries.end());
-            queries.erase(std::unique(queries.begin(), queries.end()), queries.end());
-        } else {
-            queries.resize(N);
-            std::iota(queries.begin(), queries.end(), 0u);
-        }
-        const uint64_t nq = queries.size();
-        I.n_queries = nq;
-        uint32_t k_eff = cfg->k;
-        if (k_eff >= N) {
-            k_eff = (uint32_t)(N - 1);
-            I.k_clamped = 1;
-        }
-        I.k_effective = k_eff;
-        const uint32_t m = cfg->m == 0 ? std::min<uint32_t>(6, n) : cfg->m;
-        I.m_used = m;
-        if (m > 64) throw Error(1, "grid m above 64 is not supported");
+// run_hybrid (orchestrator.cpp:67-250), optionally as one shard of a multi-GPU run.
+static void run_impl(knnj_ctx* c, const knnj_config* cfg, uint32_t shard, uint32_t nshard,
+                     knnj_allreduce_fn allreduce, void* ar_user, uint32_t* ids, double* dist,
+                     uint8_t* prov, uint32_t* owned, uint64_t* raw_hist, knnj_run_info* info) {
+    need_points(c);
+    knnj_run_info I;
+    std::memset(&I, 0, sizeof(I));
+    const uint64_t N = c->N;
+    const uint32_t n = c->n;
+    cudaStream_t s = c->s;
+    // validate_config (orchestrator.cpp:16-31)
+    if (cfg->k < 1) throw Error(1, "k must be at least 1");
+    if (cfg->m > n) throw Error(1, "m must satisfy m <= n");
+    if (cfg->beta < 0 || cfg->beta > 1 || cfg->gamma < 0 || cfg->gamma > 1 || cfg->rho < 0 ||
+        cfg->rho > 1)
+        throw Error(1, "beta, gamma, rho must all be in [0, 1]");
+    if (!(cfg->hist_query_fraction > 0) || cfg->hist_query_fraction > 1)
+        throw Error(1, "sample fractions must be in (0, 1]");
+    if (cfg->n_bins < 2) throw Error(1, "n_bins must be at least 2");
+    if (cfg->mode > 3) throw Error(1, "unknown engine mode");
+    if (nshard < 1 || shard >= nshard) throw Error(1, "shard index must satisfy 0 <= shard < shard_count");
+    if (nshard > 1 && !allreduce) throw Error(1, "a sharded run needs an allreduce callback");
+    auto reduce = [&](uint64_t* buf, uint64_t count) {
+        if (nshard > 1 && allreduce(buf, count, ar_user) != 0)
+            throw Error(9, "allreduce callback failed");
+    };
+    std::vector<uint32_t> queries;
+    if (cfg->query_subset) {
+        for (uint64_t i = 0; i < cfg->n_query_subset; ++i)
+            if (cfg->query_subset[i] >= N) throw Error(1, "query subset id out of range");
+        queries.assign(cfg->query_subset, cfg->query_subset + cfg->n_query_subset);
+        std::sort(queries.begin(), queries.end());
+        queries.erase(std::unique(queries.begin(), queries.end()), queries.end());
+    } else {
+        queries.resize(N);
+        std::iota(queries.begin(), queries.end(), 0u);
+    }
+    const uint64_t nq = queries.size();
+    I.n_queries = nq;
+    uint32_t k_eff = cfg->k;
+    if (k_eff >= N) {
+        k_eff = (uint32_t)(N - 1);
+        I.k_clamped = 1;
+    }
+    I.k_effective = k_eff;
+    const uint32_t m = cfg->m == 0 ? std::min<uint32_t>(6, n) : cfg->m;
+    I.m_used = m;
+    if (m > 64) throw Error(1, "grid m above 64 is not supported");
 
-        Timer t_all(c->s);
-        const unsigned long long launches0 = g_launches.load();
+    Timer t_all(s);
+    const unsigned long long launches0 = g_launches.load();
+    {
+        Timer t(s);
+        c->reorder(m);
+        I.ms_reorder = t.ms();
+            trace().mark("run: reorder");
+    }
+    for (uint32_t j = 0; j < n && j < 1024; ++j) I.perm[j] = c->perm[j];
+    if (k_eff == 0 || nq == 0) {
+        I.ms_total = t_all.ms();
+        if (info) *info = I;
+        return;
+    }
+    const bool all_points = !cfg->query_subset;
+    DBuf<uint32_t> o_ids;
+    DBuf<double> o_dist, o_kth;
+    DBuf<uint8_t> o_st, d_prov;
+    o_ids.ensure(nq * k_eff);
+    o_dist.ensure(nq * k_eff);
+    o_kth.ensure(nq);
+    o_st.ensure(nq);
+    d_prov.ensure(nq);
+    DBuf<uint32_t> d_q, d_rows;
+    d_q.ensure(nq);
+    d_rows.ensure(nq);
+    KJ_CUDA(cudaMemcpyAsync(d_q.p, queries.data(), 4 * nq, cudaMemcpyHostToDevice, s));
+    if (all_points) {
+        KJ_CUDA(cudaMemcpyAsync(d_rows.p, d_q.p, 4 * nq, cudaMemcpyDeviceToDevice, s));
+    } else {
+        launch_iota(d_rows.p, nq, s);
+    }
+    // rows this shard owns, in ascending row (= query id) order, on device
+    DBuf<uint32_t> d_own;
+    uint64_t n_own = 0;
+
+    if (cfg->mode == KNNJ_BRUTE_ORACLE || cfg->mode == KNNJ_SPARSE_ONLY) {
+        // brute_force_knn / kd-tree contract: exact KNN of every query (contiguous id slices)
+        Timer t(s);
+        const uint64_t lo = nq * shard / nshard, hi = nq * (shard + 1) / nshard;
+        n_own = hi - lo;
+        std::vector<uint32_t> rows(n_own), qp(n_own);
+        std::iota(rows.begin(), rows.end(), (uint32_t)lo);
+        for (uint64_t i = 0; i < n_own; ++i) qp[i] = queries[lo + i];
+        const uint32_t me = std::min<uint32_t>(6, n);
+        // width from the bounding box: cells holding ~2k points on average
+        std::vector<unsigned long long> mn(me), mx(me), i0(me, ~0ull), i1(me, 0ull);
+        c->d_u64a.ensure(64);
+        c->d_u64b.ensure(64);
+        KJ_CUDA(cudaMemcpyAsync(c->d_u64a.p, i0.data(), 8 * me, cudaMemcpyHostToDevice, s));
+        KJ_CUDA(cudaMemcpyAsync(c->d_u64b.p, i1.data(), 8 * me, cudaMemcpyHostToDevice, s));
+        launch_minmax(c->X64.p, N, n, me, c->d_u64a.p, c->d_u64b.p, s);
+        KJ_CUDA(cudaMemcpyAsync(mn.data(), c->d_u64a.p, 8 * me, cudaMemcpyDeviceToHost, s));
+        KJ_CUDA(cudaMemcpyAsync(mx.data(), c->d_u64b.p, 8 * me, cudaMemcpyDeviceToHost, s));
+        c->sync();
+        double logvol = 0.0;
+        int used = 0;
+        for (uint32_t j = 0; j < me; ++j) {
+            const double e = knnj_ctx::unorder(mx[j]) - knnj_ctx::unorder(mn[j]);
+            if (e > 0) {
+                logvol += std::log(e);
+                ++used;
+            }
+        }
+        double w0 = used ? std::exp((logvol + std::log(2.0 * k_eff / double(N))) / used) : 1.0;
+        if (!(w0 > 0) || !std::isfinite(w0)) w0 = 1.0;
+        for (int L = 20; L < 40; ++L) c->levels[L].built = false;
+        std::vector<double> U(n_own, kInf);
+        if (n_own)
+            c->exact_levels(me, std::ldexp(w0, -20), 20, qp, rows, U, k_eff, o_ids.p, o_dist.p,
+                            o_kth.p, o_st.p, nq, &I.fallback_passes, &I.slow_path_queries);
+        I.fallback_queries = n_own;
+        I.ms_fallback = t.ms();
+            trace().mark("run: fallback");
+        if (n_own)
+            KJ_CUDA(cudaMemsetAsync(d_prov.p + lo,
+                                    cfg->mode == KNNJ_BRUTE_ORACLE ? KNNJ_PROV_DENSE : KNNJ_PROV_SPARSE,
+                                    n_own, s));
+        d_own.ensure(n_own);
+        launch_iota(d_own.p, n_own, s);
+        if (lo) {  // rows lo.. : shift the iota
+            std::vector<uint32_t> r(n_own);
+            std::iota(r.begin(), r.end(), (uint32_t)lo);
+            KJ_CUDA(cudaMemcpyAsync(d_own.p, r.data(), 4 * n_own, cudaMemcpyHostToDevice, s));
+        }
+    } else {
+        // ---- epsilon selection (orchestrator.cpp:137-165)
         {
-            Timer t(c->s);
-            c->reorder(m);
-            I.ms_reorder = t.ms();
+            Timer t(s);
+            const uint64_t budget = std::min<uint64_t>(10 * N, cfg->eps_mean_pair_cap);
+            I.eps_mean = c->eps_mean(budget, derive_seed(cfg->seed, 1));
+            I.ms_eps_mean = t.ms();
+            trace().mark("run: eps_mean");
         }
-        for (uint32_t j = 0; j < n && j < 1024; ++j) I.perm[j] = c->perm[j];
-        if (k_eff == 0 || nq == 0) {
-            I.ms_total = t_all.ms();
-            if (info) *info = I;
-            return;
+        const double target_beta =
+            double(k_eff) + (100.0 * double(k_eff) - double(k_eff)) * cfg->beta;
+        std::vector<uint64_t> raw(cfg->n_bins, 0);
+        uint32_t valid = cfg->n_bins;
+        {
+            Timer t(s);
+            auto hq = c->histogram_sample(cfg->hist_query_fraction, derive_seed(cfg->seed, 2));
+            I.hist_query_count = hq.size();
+            valid = c->hist_for_selection(hq, shard, nshard, I.eps_mean, cfg->n_bins, target_beta,
+                                          raw_hist != nullptr, reduce, raw.data());
+            I.hist_bins_counted = valid;
+            I.ms_histogram = t.ms();
+            trace().mark("run: histogram");
+            I.ms_hist_kernel = c->last_hist_kernel_ms;
+            I.hist_tensor_cores = c->last_hist_tc ? 1 : 0;
         }
-        const bool all_points = !cfg->query_subset;
-        DBuf<uint32_t> o_ids;
-        DBuf<double> o_dist, o_kth;
-        DBuf<uint8_t> o_st;
-        o_ids.ensure(nq * k_eff);
-        o_dist.ensure(nq * k_eff);
-        o_kth.ensure(nq);
-        o_st.ensure(nq);
-        DBuf<uint32_t> d_q, d_rows;
-        d_q.ensure(nq);
-        d_rows.ensure(nq);
-        KJ_CUDA(cudaMemcpyAsync(d_q.p, queries.data(), 4 * nq, cudaMemcpyHostToDevice, c->s));
-        if (all_points) {
-            KJ_CUDA(cudaMemcpyAsync(d_rows.p, d_q.p, 4 * nq, cudaMemcpyDeviceToDevice, c->s));
-        } else {
-            std::vector<uint32_t> rows(nq);
-            std::iota(rows.begin(), rows.end(), 0u);
-            KJ_CUDA(cudaMemcpyAsync(d_rows.p, rows.data(), 4 * nq, cudaMemcpyHostToDevice, c->s));
+        if (raw_hist) std::memcpy(raw_hist, raw.data(), 8 * cfg->n_bins);
+        const double width = I.eps_mean / double(cfg->n_bins);
+        I.bin_width = width;
+        // cumulative profile over the exactly counted bins (all of them unless capped,
+        // in which case the target is already reached inside them)
+        std::vector<double> cum(valid);
+        uint64_t running = 0;
+        for (uint32_t b = 0; b < valid; ++b) {
+            running += raw[b];
+            cum[b] = double(running) / double(I.hist_query_count);
         }
-        std::vector<uint8_t> h_prov(nq, KNNJ_PROV_SPARSE);
+        auto select = [&](double beta, bool& fell_back, uint64_t& bin_out) {
+            const double target = double(k_eff) + (100.0 * double(k_eff) - double(k_eff)) * beta;
+            auto it = std::lower_bound(cum.begin(), cum.end(), target);
+            fell_back = false;
+            if (it == cum.end()) {
+                if (valid != cfg->n_bins) throw Error(9, "capped histogram missed its target");
+                fell_back = true;
+                it = std::lower_bound(cum.begin(), cum.end(), cum.back());
+            }
+            uint64_t bin = uint64_t(it - cum.begin()) + 1;
+            double start = double(bin - 1) * width;
+            double end = double(bin) * width;
+            bin_out = bin;
+            return (start + end) / 2.0;
+        };
+        bool fb = false, fb0 = false;
+        uint64_t bin = 0, bin0 = 0;
+        I.eps_beta = select(cfg->beta, fb, bin);
+        I.eps_default = select(0.0, fb0, bin0);
+        I.eps_final = 2.0 * I.eps_beta;
+        I.eps_used = I.eps_final;
+        I.eps_fallback = fb;
+        I.hist_bin = bin;
+        const double eps = I.eps_final;
 
-        if (cfg->mode == KNNJ_BRUTE_ORACLE || cfg->mode == KNNJ_SPARSE_ONLY) {
-            // brute_force_knn / kd-tree contract: exact KNN of every query
-            Timer t(c->s);
-            std::vector<uint32_t> rows(nq);
-            std::iota(rows.begin(), rows.end(), 0u);
-            const uint32_t me = std::min<uint32_t>(6, n);
-            // width from the bounding box, as knnj_exact_knn
-            std::vector<unsigned long long> mn(me), mx(me), i0(me, ~0ull), i1(me, 0ull);
-            c->d_u64a.ensure(64);
-            c->d_u64b.ensure(64);
-            KJ_CUDA(cudaMemcpyAsync(c->d_u64a.p, i0.data(), 8 * me, cudaMemcpyHostToDevice, c->s));
-            KJ_CUDA(cudaMemcpyAsync(c->d_u64b.p, i1.data(), 8 * me, cudaMemcpyHostToDevice, c->s));
-            launch_minmax(c->X64.p, N, n, me, c->d_u64a.p, c->d_u64b.p, c->s);
-            KJ_CUDA(cudaMemcpyAsync(mn.data(), c->d_u64a.p, 8 * me, cudaMemcpyDeviceToHost, c->s));
-            KJ_CUDA(cudaMemcpyAsync(mx.data(), c->d_u64b.p, 8 * me, cudaMemcpyDeviceToHost, c->s));
-            c->sync();
-            double logvol = 0.0;
-            int used = 0;
-            auto un = [](unsigned long long o) {
-                unsigned long long b = (o & 0x8000000000000000ull) ? (o & 0x7FFFFFFFFFFFFFFFull) : ~o;
-                double v;
-                std::memcpy(&v, &b, 8);
-                return v;
-            };
-            for (uint32_t j = 0; j < me; ++j) {
-                double e = un(mx[j]) - un(mn[j]);
-                if (e > 0) {
-                    logvol += std::log(e);
-                    ++used;
-                }
-            }
-            double w0 = used ? std::exp((logvol + std::log(2.0 * k_eff / double(N))) / used) : 1.0;
-            if (!(w0 > 0) || !std::isfinite(w0)) w0 = 1.0;
-            for (int L = 20; L < 40; ++L) c->levels[L].built = false;
-            std::vector<double> U(nq, kInf);
-            c->exact_levels(me, std::ldexp(w0, -20), 20, queries, rows, U, k_eff, o_ids.p,
-                            o_dist.p, o_kth.p, o_st.p, nq, &I.fallback_passes, &I.slow_path_queries);
-            I.fallback_queries = nq;
-            I.ms_fallback = t.ms();
-            std::fill(h_prov.begin(), h_prov.end(),
-                      cfg->mode == KNNJ_BRUTE_ORACLE ? KNNJ_PROV_DENSE : KNNJ_PROV_SPARSE);
-        } else {
-            // ---- epsilon selection (orchestrator.cpp:137-165)
-            {
-                Timer t(c->s);
-                const uint64_t budget = std::min<uint64_t>(10 * N, cfg->eps_mean_pair_cap);
-                I.eps_mean = c->eps_mean(budget, derive_seed(cfg->seed, 1));
-                I.ms_eps_mean = t.ms();
-            }
-            std::vector<uint64_t> raw(cfg->n_bins, 0);
-            {
-                Timer t(c->s);
-                auto hq = c->histogram_sample(cfg->hist_query_fraction, derive_seed(cfg->seed, 2));
-                I.hist_query_count = hq.size();
-                c->histogram_queries(hq.data(), hq.size(), I.eps_mean, cfg->n_bins, raw.data());
-                I.ms_histogram = t.ms();
-                I.ms_hist_kernel = c->last_hist_kernel_ms;
-                I.hist_tensor_cores = c->last_hist_tc ? 1 : 0;
-            }
-            if (raw_hist) std::memcpy(raw_hist, raw.data(), 8 * cfg->n_bins);
-            const double width = I.eps_mean / double(cfg->n_bins);
-            I.bin_width = width;
-            std::vector<double> cum(cfg->n_bins);
-            uint64_t running = 0;
-            for (uint32_t b = 0; b < cfg->n_bins; ++b) {
-                running += raw[b];
-                cum[b] = double(running) / double(I.hist_query_count);
-            }
-            auto select = [&](double beta, bool& fell_back, uint64_t& bin_out) {
-                const double target = double(k_eff) + (100.0 * double(k_eff) - double(k_eff)) * beta;
-                auto it = std::lower_bound(cum.begin(), cum.end(), target);
-                fell_back = false;
-                if (it == cum.end()) {
-                    fell_back = true;
-                    it = std::lower_bound(cum.begin(), cum.end(), cum.back());
-                }
-                uint64_t bin = uint64_t(it - cum.begin()) + 1;
-                double start = double(bin - 1) * width;
-                double end = double(bin) * width;
-                bin_out = bin;
-                return (start + end) / 2.0;
-            };
-            bool fb = false, fb0 = false;
-            uint64_t bin = 0, bin0 = 0;
-            I.eps_beta = select(cfg->beta, fb, bin);
-            I.eps_default = select(0.0, fb0, bin0);
-            I.eps_final = 2.0 * I.eps_beta;
-            I.eps_used = I.eps_final;
-            I.eps_fallback = fb;
-            I.hist_bin = bin;
-            const double eps = I.eps_final;
-
-            // ---- grid (GridIndex::build)
-            {
-                Timer t(c->s);
-                c->build_level(0, m, eps);
-                c->eps0 = eps;
-                c->m0 = m;
-                for (int L = 1; L < 40; ++L) c->levels[L].built = false;
-                I.ms_grid = t.ms();
-                I.grid_cells = c->levels[0].ncells;
-            }
-            Level& lv0 = c->levels[0];
-            // ---- split (partition.cpp:30-75)
-            std::vector<uint8_t> dense(nq, 1);
-            {
-                Timer t(c->s);
-                const double mm = double(m);
-                I.n_min = double(k_eff) * std::pow(2.0, mm) * std::tgamma(mm / 2.0 + 1.0) /
-                          std::pow(M_PI, mm / 2.0);
-                I.n_thresh = I.n_min + (10.0 * I.n_min - I.n_min) * cfg->gamma;
-                if (cfg->mode == KNNJ_HYBRID) {
+        // ---- grid (GridIndex::build)
+        {
+            Timer t(s);
+            c->build_level(0, m, eps);
+            c->eps0 = eps;
+            c->m0 = m;
+            for (int L = 1; L < 40; ++L) c->levels[L].built = false;
+            I.ms_grid = t.ms();
+            trace().mark("run: grid");
+            I.grid_cells = c->levels[0].ncells;
+        }
+        Level& lv0 = c->levels[0];
+        // ---- split (partition.cpp:30-75): dense flags per query row, on device
+        DBuf<uint8_t> d_dense;
+        bool have_dense = false;
+        {
+            Timer t(s);
+            const double mm = double(m);
+            I.n_min = double(k_eff) * std::pow(2.0, mm) * std::tgamma(mm / 2.0 + 1.0) /
+                      std::pow(M_PI, mm / 2.0);
+            I.n_thresh = I.n_min + (10.0 * I.n_min - I.n_min) * cfg->gamma;
+            if (cfg->mode == KNNJ_HYBRID) {
+                have_dense = true;
+                d_dense.ensure(nq);
+                c->d_u64a.ensure(1);
+                KJ_CUDA(cudaMemsetAsync(c->d_u64a.p, 0, 8, s));
+                launch_split_flags(d_q.p, nq, lv0.slot.p, lv0.G.p, I.n_thresh, d_dense.p,
+                                   c->d_u64a.p, s);
+                unsigned long long ncpu = 0;
+                KJ_CUDA(cudaMemcpyAsync(&ncpu, c->d_u64a.p, 8, cudaMemcpyDeviceToHost, s));
+                c->sync();
+                const uint64_t floor_cpu = (uint64_t)std::ceil(cfg->rho * double(nq));
+                if (ncpu < floor_cpu) {
+                    // rho demotion (pop, cell, pid order): the host reference path
+                    std::vector<uint8_t> dense(nq);
                     knnj_split_info si{};
                     int rc = knnj_split(c, queries.data(), nq, k_eff, cfg->beta, cfg->gamma,
                                         cfg->rho, dense.data(), nullptr, &si);
                     if (rc) throw Error(rc, c->err);
-                    I.q_gpu = si.q_gpu;
+                    alloc_stream() = s;
+                    KJ_CUDA(cudaMemcpyAsync(d_dense.p, dense.data(), nq, cudaMemcpyHostToDevice, s));
                     I.q_cpu = si.q_cpu;
                     I.demoted = si.demoted;
                 } else {
-                    I.q_gpu = nq;
+                    I.q_cpu = ncpu;
                 }
-                I.ms_split = t.ms();
+                I.q_gpu = nq - I.q_cpu;
+            } else {
+                I.q_gpu = nq;
             }
-            // ---- level-0 fused join over every query (dense + sparse)
-            uint64_t slow = 0;
+            I.ms_split = t.ms();
+            trace().mark("run: split");
+        }
+        // ---- level-0 fused join over this shard's queries (dense + sparse)
+        uint64_t slow = 0;
+        Pass P;
+        {
+            Timer t(s);
             {
-                Timer t(c->s);
-                Pass P;
-                c->build_pass(lv0, d_q.p, d_rows.p, nq, P, k_eff);
-                c->run_pass(lv0, P, k_eff, nullptr, eps * eps, c->cover2(lv0), o_ids.p, o_dist.p,
-                            o_kth.p, o_st.p, &slow);
-                I.ms_join = t.ms();
-                I.ms_join_kernel = c->last_join_kernel_ms;
-                I.join_tensor_cores = c->last_join_tc ? 1 : 0;
-                // candidates_examined counts dense queries only
-                if (I.q_cpu == 0) I.candidates_examined = P.candidates;
+                Timer tb(s);
+                c->build_pass(lv0, d_q.p, d_rows.p, nq, P, k_eff, shard, nshard,
+                              have_dense ? d_dense.p : nullptr);
+                I.ms_join_build = tb.ms();
             }
-            // ---- classify; exact fallback for failures and uncertified sparse queries
+            c->run_pass(lv0, P, k_eff, nullptr, eps * eps, c->cover2(lv0), o_ids.p, o_dist.p,
+                        o_kth.p, o_st.p, &slow);
+            I.ms_join = t.ms();
+            trace().mark("run: join");
+            I.ms_join_kernel = c->last_join_kernel_ms;
+            I.join_tensor_cores = c->last_join_tc ? 1 : 0;
+            // candidates_examined counts dense queries only (DenseJoinStats)
+            I.candidates_examined = have_dense ? P.candidates_dense : P.candidates;
+            I.join_candidate_pairs = P.candidates;
+        }
+        n_own = P.nq;
+        // ---- classify on device; exact fallback for failures and uncertified sparse rows
+        {
+            Timer t(s);
+            DBuf<uint8_t> need;
+            need.ensure(n_own);
+            launch_classify(P.qrow.p, n_own, o_st.p, have_dense ? d_dense.p : nullptr, d_prov.p,
+                            need.p, s);
+            DBuf<uint32_t> fb_rows;
+            fb_rows.ensure(n_own);
+            c->d_u64a.ensure(1);
             {
-                Timer t(c->s);
-                std::vector<uint8_t> st(nq);
-                KJ_CUDA(cudaMemcpyAsync(st.data(), o_st.p, nq, cudaMemcpyDeviceToHost, c->s));
-                std::vector<double> kth(nq);
-                KJ_CUDA(cudaMemcpyAsync(kth.data(), o_kth.p, 8 * nq, cudaMemcpyDeviceToHost, c->s));
+                size_t bytes = 0;
+                KJ_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, P.qrow.p, need.p, fb_rows.p,
+                                                   c->d_u64a.p, (int64_t)n_own, s));
+                KJ_CUDA(cub::DeviceSelect::Flagged(c->sc.get(bytes), bytes, P.qrow.p, need.p,
+                                                   fb_rows.p, c->d_u64a.p, (int64_t)n_own, s));
+            }
+            unsigned long long nfb = 0;
+            KJ_CUDA(cudaMemcpyAsync(&nfb, c->d_u64a.p, 8, cudaMemcpyDeviceToHost, s));
+            c->sync();
+            std::vector<uint32_t> fr(nfb), fp(nfb);
+            std::vector<double> fu(nfb);
+            if (nfb) {
+                DBuf<uint8_t> g_st, g_pv;
+                DBuf<double> g_kth;
+                g_st.ensure(nfb);
+                g_pv.ensure(nfb);
+                g_kth.ensure(nfb);
+                launch_gather_u8(fb_rows.p, o_st.p, nfb, g_st.p, s);
+                launch_gather_u8(fb_rows.p, d_prov.p, nfb, g_pv.p, s);
+                launch_gather_f64(fb_rows.p, o_kth.p, nfb, g_kth.p, s);
+                std::vector<uint8_t> st(nfb), pv(nfb);
+                KJ_CUDA(cudaMemcpyAsync(fr.data(), fb_rows.p, 4 * nfb, cudaMemcpyDeviceToHost, s));
+                KJ_CUDA(cudaMemcpyAsync(st.data(), g_st.p, nfb, cudaMemcpyDeviceToHost, s));
+                KJ_CUDA(cudaMemcpyAsync(pv.data(), g_pv.p, nfb, cudaMemcpyDeviceToHost, s));
+                KJ_CUDA(cudaMemcpyAsync(fu.data(), g_kth.p, 8 * nfb, cudaMemcpyDeviceToHost, s));
                 c->sync();
-                std::vector<uint32_t> fp, fr;
-                std::vector<double> fu;
-                for (uint64_t i = 0; i < nq; ++i) {
-                    const uint8_t s = st[i];
-                    if (dense[i]) {
-                        if ((s & ST_HAS_K) && (s & ST_IN_EPS)) {
-                            h_prov[i] = KNNJ_PROV_DENSE;
-                            continue;
-                        }
-                        h_prov[i] = KNNJ_PROV_DENSE_FAILED;
-                        ++I.failed_count;
-                    } else {
-                        h_prov[i] = KNNJ_PROV_SPARSE;
-                        if ((s & ST_HAS_K) && (s & ST_CERT)) continue;
-                    }
-                    fp.push_back(queries[i]);
-                    fr.push_back((uint32_t)i);
-                    fu.push_back((s & ST_HAS_K) ? kth[i] : kInf);
-                }
-                I.fallback_queries = fp.size();
-                if (!fp.empty())
-                    c->exact_levels(m, eps, 1, fp, fr, fu, k_eff, o_ids.p, o_dist.p, o_kth.p,
-                                    o_st.p, nq, &I.fallback_passes, &slow);
-                I.slow_path_queries = slow;
-                I.ms_fallback = t.ms();
-            }
-            if (I.q_cpu) {
-                // candidates_examined over dense queries only: recount on the dense subset
-                std::vector<uint32_t> dq;
-                for (uint64_t i = 0; i < nq; ++i)
-                    if (dense[i]) dq.push_back(queries[i]);
-                if (!dq.empty()) {
-                    DBuf<uint32_t> a, b;
-                    a.ensure(dq.size());
-                    b.ensure(dq.size());
-                    std::vector<uint32_t> rr(dq.size());
-                    std::iota(rr.begin(), rr.end(), 0u);
-                    KJ_CUDA(cudaMemcpyAsync(a.p, dq.data(), 4 * dq.size(), cudaMemcpyHostToDevice, c->s));
-                    KJ_CUDA(cudaMemcpyAsync(b.p, rr.data(), 4 * dq.size(), cudaMemcpyHostToDevice, c->s));
-                    Pass P;
-                    c->build_pass(lv0, a.p, b.p, dq.size(), P);
-                    I.candidates_examined = P.candidates;
+                for (uint64_t i = 0; i < nfb; ++i) {
+                    fp[i] = queries[fr[i]];
+                    if (!(st[i] & ST_HAS_K)) fu[i] = kInf;
+                    if (pv[i] == KNNJ_PROV_DENSE_FAILED) ++I.failed_count;
                 }
             }
+            I.fallback_queries = nfb;
+            if (nfb)
+                c->exact_levels(m, eps, 1, fp, fr, fu, k_eff, o_ids.p, o_dist.p, o_kth.p, o_st.p,
+                                nq, &I.fallback_passes, &slow);
+            I.slow_path_queries = slow;
+            I.ms_fallback = t.ms();
+            trace().mark("run: fallback");
         }
-        if (ids || dist) {
-            Timer t(c->s);
-            if (ids)
-                KJ_CUDA(cudaMemcpyAsync(ids, o_ids.p, 4 * nq * k_eff, cudaMemcpyDeviceToHost, c->s));
-            if (dist)
-                KJ_CUDA(cudaMemcpyAsync(dist, o_dist.p, 8 * nq * k_eff, cudaMemcpyDeviceToHost, c->s));
-            I.ms_download = t.ms();
+        // owned rows in ascending order
+        d_own.ensure(n_own);
+        if (nshard == 1) {
+            launch_iota(d_own.p, n_own, s);
+        } else if (n_own) {
+            DBuf<uint32_t> tmp;
+            tmp.ensure(n_own);
+            KJ_CUDA(cudaMemcpyAsync(tmp.p, P.qrow.p, 4 * n_own, cudaMemcpyDeviceToDevice, s));
+            size_t bytes = 0;
+            KJ_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, bytes, tmp.p, d_own.p, (int64_t)n_own,
+                                                   0, bits_for(nq), s));
+            KJ_CUDA(cub::DeviceRadixSort::SortKeys(c->sc.get(bytes), bytes, tmp.p, d_own.p,
+                                                   (int64_t)n_own, 0, bits_for(nq), s));
         }
-        if (prov) std::memcpy(prov, h_prov.data(), nq);
-        I.ms_total = t_all.ms();
-        I.kernel_launches = g_launches.load() - launches0;
-        (void)t_start;
-        if (info) *info = I;
+    }
+    I.n_owned = n_own;
+    // ---- results to the host: this shard's rows, ascending query id
+    {
+        Timer t(s);
+        if (nshard == 1) {
+            if (ids) KJ_CUDA(cudaMemcpyAsync(ids, o_ids.p, 4 * nq * k_eff, cudaMemcpyDeviceToHost, s));
+            if (dist) KJ_CUDA(cudaMemcpyAsync(dist, o_dist.p, 8 * nq * k_eff, cudaMemcpyDeviceToHost, s));
+            if (prov) KJ_CUDA(cudaMemcpyAsync(prov, d_prov.p, nq, cudaMemcpyDeviceToHost, s));
+            if (owned) std::memcpy(owned, queries.data(), 4 * nq);
+        } else if (n_own) {
+            DBuf<uint32_t> c_ids, c_q;
+            DBuf<double> c_dist;
+            DBuf<uint8_t> c_pv;
+            if (ids || dist) {
+                c_ids.ensure(n_own * k_eff);
+                c_dist.ensure(n_own * k_eff);
+                launch_gather_rows(d_own.p, n_own, k_eff, o_ids.p, o_dist.p, c_ids.p, c_dist.p, s);
+                if (ids) KJ_CUDA(cudaMemcpyAsync(ids, c_ids.p, 4 * n_own * k_eff, cudaMemcpyDeviceToHost, s));
+                if (dist) KJ_CUDA(cudaMemcpyAsync(dist, c_dist.p, 8 * n_own * k_eff, cudaMemcpyDeviceToHost, s));
+            }
+            if (prov) {
+                c_pv.ensure(n_own);
+                launch_gather_u8(d_own.p, d_prov.p, n_own, c_pv.p, s);
+                KJ_CUDA(cudaMemcpyAsync(prov, c_pv.p, n_own, cudaMemcpyDeviceToHost, s));
+            }
+            if (owned) {
+                c_q.ensure(n_own);
+                launch_map_u32(d_own.p, d_q.p, n_own, c_q.p, s);
+                KJ_CUDA(cudaMemcpyAsync(owned, c_q.p, 4 * n_own, cudaMemcpyDeviceToHost, s));
+            }
+            c->sync();
+        }
+        I.ms_download = t.ms();
+    }
+    I.ms_total = t_all.ms();
+    I.kernel_launches = g_launches.load() - launches0;
+    if (info) *info = I;
+}
+
+int knnj_shard_range(const double* cost, uint64_t n_items, uint32_t shard_index,
+                     uint32_t shard_count, uint64_t* first, uint64_t* last) {
+    if (!first || !last || shard_count < 1 || shard_index >= shard_count || (n_items && !cost))
+        return KNNJ_E_USAGE;
+    shard_range(cost, n_items, shard_index, shard_count, first, last);
+    return KNNJ_OK;
+}
+
+int knnj_run(knnj_ctx* c, const knnj_config* cfg, uint32_t* ids, double* dist, uint8_t* prov,
+             uint64_t* raw_hist, knnj_run_info* info) {
+    return guarded(c, [&] {
+        run_impl(c, cfg, 0, 1, nullptr, nullptr, ids, dist, prov, nullptr, raw_hist, info);
+    });
+}
+
+int knnj_run_shard(knnj_ctx* c, const knnj_config* cfg, uint32_t shard_index,
+                   uint32_t shard_count, knnj_allreduce_fn allreduce, void* allreduce_user,
+                   uint32_t* ids, double* dist, uint8_t* prov, uint32_t* owned_queries,
+                   uint64_t* raw_hist, knnj_run_info* info) {
+    return guarded(c, [&] {
+        run_impl(c, cfg, shard_index, shard_count, allreduce, allreduce_user, ids, dist, prov,
+                 owned_queries, raw_hist, info);
     });
 }
 

@@ -7,6 +7,8 @@
 #include <stdint.h>
 
 #include <atomic>
+#include <map>
+#include <utility>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -28,34 +30,65 @@ struct Error : std::runtime_error {
     } while (0)
 
 // ---------------------------------------------------------------- device buffer
-// Stream-ordered allocations from the device's (cached) default memory pool:
-// temporaries cost no device synchronisation. The stream is the calling ctx's.
+// Device memory of a ctx never goes back to the driver between calls: blocks are
+// recycled through the ctx's BlockCache (best fit, stream-ordered on the ctx's one
+// stream), so a steady-state run performs no cudaMalloc at all. (Large
+// cudaMallocAsync calls from a fragmented pool were measured at up to ~1 s.)
+struct BlockCache {
+    std::multimap<size_t, void*> free_blocks;       // bytes -> block
+    std::vector<std::pair<void*, size_t>> owned;    // every block, freed at ctx destroy
+    void* get(size_t bytes, size_t& got, cudaStream_t s);
+    void put(void* p, size_t bytes) { free_blocks.emplace(bytes, p); }
+    BlockCache() = default;
+    BlockCache(const BlockCache&) = delete;
+    ~BlockCache();
+};
 cudaStream_t& alloc_stream();
+BlockCache*& alloc_cache();
 template <class T>
 struct DBuf {
     T* p = nullptr;
-    size_t n = 0;  // capacity in elements
+    size_t n = 0;      // capacity in elements
+    size_t bytes = 0;  // size of the block behind p
+    BlockCache* cache = nullptr;
     cudaStream_t s = nullptr;
     DBuf() = default;
     DBuf(const DBuf&) = delete;
     DBuf& operator=(const DBuf&) = delete;
     ~DBuf() { release(); }
     void release() {
-        if (p) cudaFreeAsync(p, s);
+        if (p) {
+            if (cache) cache->put(p, bytes);
+            else cudaFreeAsync(p, s);
+        }
         p = nullptr;
-        n = 0;
+        n = bytes = 0;
     }
     T* ensure(size_t count) {
         if (count == 0) count = 1;
         if (count > n) {
             release();
             s = alloc_stream();
-            KJ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), s));
-            n = count;
+            cache = alloc_cache();
+            size_t got = count * sizeof(T);
+            if (cache) {
+                p = static_cast<T*>(cache->get(count * sizeof(T), got, s));
+            } else {
+                KJ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), got, s));
+            }
+            bytes = got;
+            n = got / sizeof(T);
         }
         return p;
     }
     T* get() const { return p; }
+    void swap(DBuf& o) {
+        std::swap(p, o.p);
+        std::swap(n, o.n);
+        std::swap(bytes, o.bytes);
+        std::swap(cache, o.cache);
+        std::swap(s, o.s);
+    }
 };
 
 // ---------------------------------------------------------------- constants
@@ -99,6 +132,9 @@ struct Pass {
     uint64_t nitems = 0;
     uint64_t nadj = 0;
     uint64_t candidates = 0;  // sum over queries of candidate-set size
+    uint64_t candidates_dense = 0;  // the same over dense queries (when flags were given)
+    uint64_t row_begin = 0;   // first owned position in the cell-ordered query list (shards)
+    uint64_t nq_all = 0;      // queries before sharding
     uint32_t chunk = 128;     // queries per work item
     DBuf<uint32_t> qpos;      // nq: sorted positions of the queries (grouped by cell)
     DBuf<uint32_t> qrow;      // nq: output row of each query
@@ -137,6 +173,7 @@ struct TcJoinArgs {
     float* dbg;              // test hook: block 0 dumps its first accumulator tile [128][128]
     // histogram epilogue (HIST kernels only)
     uint32_t n_bins;
+    uint32_t n_count;        // bins [0, n_count) are counted (n_count < n_bins: capped histogram)
     const float* tables;     // LO[n_bins+1], HI[n_bins+1] in scaled units
     float inv_width_scaled;  // S / bin_width
     const double* X64;
@@ -171,6 +208,7 @@ struct HistArgs {
     uint64_t nq;
     uint64_t cand_begin_stride;  // candidate slab length
     uint32_t n_bins;
+    uint32_t n_count;        // bins [0, n_count) are counted; pairs beyond bin n_count's edge skipped
     const float* SU;         // n_bins+1: lower edge rounded up   (SU[0] = -inf)
     const float* SD;         // n_bins+1: lower edge rounded down (SD[n_bins] = end)
     double eps_mean, limit_sq, inv_width;
@@ -252,5 +290,18 @@ void launch_slow_exact(const double* X64, uint32_t n, const uint32_t* A, const u
                        const uint4* items, const uint32_t* row_item, const uint2* adj,
                        uint32_t K, double eps2, double cover2, uint32_t* out_ids,
                        double* out_dist, double* out_kth, uint8_t* out_status, cudaStream_t s);
+
+void launch_split_flags(const uint32_t* pids, uint64_t nq, const uint32_t* slot, const uint2* G,
+                        double n_thresh, uint8_t* dense, unsigned long long* n_sparse,
+                        cudaStream_t s);
+void launch_classify(const uint32_t* rows, uint64_t n, const uint8_t* st, const uint8_t* dense,
+                     uint8_t* prov, uint8_t* need, cudaStream_t s);
+void launch_dense_cand(const uint4* items, const unsigned long long* work, uint64_t nitems,
+                       const uint32_t* qrow, const uint8_t* dense, unsigned long long* out,
+                       cudaStream_t s);
+void launch_find_ovf(const uint32_t* cnt, uint64_t n, uint32_t* rows, unsigned long long* count,
+                     cudaStream_t s);
+void launch_gather_rows(const uint32_t* rows, uint64_t n, uint32_t K, const uint32_t* ids,
+                        const double* dist, uint32_t* oids, double* odist, cudaStream_t s);
 
 }  // namespace kj

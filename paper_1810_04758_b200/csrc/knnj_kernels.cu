@@ -385,7 +385,8 @@ __global__ void __launch_bounds__(JB) k_hist(HistArgs a) {
         na = fmaf(v, v, na);
     }
     const float Aq = sqrtf(na) * 1.0001f;
-    const float lo_end = a.SU[nbins];
+    const uint32_t ncount = a.n_count;
+    const float lo_end = a.SU[ncount];  // lower edge of the first uncounted bin
     const float invw = (float)a.inv_width;
     const double* qx = a.X64 + (uint64_t)qid * n;
 
@@ -455,7 +456,7 @@ __global__ void __launch_bounds__(JB) k_hist(HistArgs a) {
                     int b = key > 0.f ? (int)(key * rsqrtf(key) * invw) : 0;
                     b = min(max(b, 0), (int)nbins - 1);
                     if (klo >= LO[b] && khi < HI[b]) {
-                        hist[b * JB + tid] += 1;
+                        if ((uint32_t)b < ncount) hist[b * JB + tid] += 1;
                     } else {
                         const double sq = exact_sq(qx, a.X64 + t * n, n);
                         if (sq > a.limit_sq) continue;
@@ -463,7 +464,7 @@ __global__ void __launch_bounds__(JB) k_hist(HistArgs a) {
                         if (dist >= a.eps_mean) continue;
                         uint64_t bb = (uint64_t)(dist * a.inv_width);
                         if (bb >= nbins) bb = nbins - 1;
-                        hist[bb * JB + tid] += 1;
+                        if (bb < ncount) hist[bb * JB + tid] += 1;
                     }
                 }
             }
@@ -1236,6 +1237,133 @@ __global__ void k_inverse(const uint32_t* J, uint64_t N, uint32_t* posJ) {
 }
 void launch_inverse(const uint32_t* J, uint64_t N, uint32_t* posJ, cudaStream_t s) {
     k_inverse<<<1184, 256, 0, s>>>(J, N, posJ);
+    KJ_CUDA(cudaGetLastError());
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+}  // namespace kj
+
+namespace kj {
+// ---------------------------------------------------------------- split / classify on device
+// split_work (partition.cpp:30-75) without demotion: dense iff double(pop) >= n_thresh,
+// pop = population of the query's cell; counts the sparse queries.
+__global__ void k_split_flags(const uint32_t* pids, uint64_t nq, const uint32_t* slot,
+                              const uint2* G, double n_thresh, uint8_t* dense,
+                              unsigned long long* n_sparse) {
+    unsigned long long local = 0;
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < nq;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const uint2 g = G[slot[pids[i]]];
+        const uint8_t d = double(g.y - g.x) >= n_thresh ? 1 : 0;
+        dense[i] = d;
+        local += 1 - d;
+    }
+    for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
+    if ((threadIdx.x & 31) == 0 && local) atomicAdd(n_sparse, local);
+}
+void launch_split_flags(const uint32_t* pids, uint64_t nq, const uint32_t* slot, const uint2* G,
+                        double n_thresh, uint8_t* dense, unsigned long long* n_sparse,
+                        cudaStream_t s) {
+    if (!nq) return;
+    k_split_flags<<<1184, 256, 0, s>>>(pids, nq, slot, G, n_thresh, dense, n_sparse);
+    KJ_CUDA(cudaGetLastError());
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+
+// Provenance and fallback need of the level-0 join rows (orchestrator.cpp:211-234):
+// dense rows are solved iff >= K non-self in-eps neighbours (ST_HAS_K & ST_IN_EPS),
+// otherwise DenseFailedThenSparse; sparse rows keep the join's list only when it is
+// certified globally exact (ST_CERT), else the exact fallback re-solves them.
+__global__ void k_classify(const uint32_t* rows, uint64_t n, const uint8_t* st,
+                           const uint8_t* dense, uint8_t* prov, uint8_t* need) {
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const uint32_t r = rows[i];
+        const uint8_t s = st[r];
+        const bool d = dense ? dense[r] != 0 : true;
+        uint8_t pv, nd;
+        if (d) {
+            const bool ok = (s & ST_HAS_K) && (s & ST_IN_EPS);
+            pv = ok ? 0 : 2;
+            nd = ok ? 0 : 1;
+        } else {
+            pv = 1;
+            nd = ((s & ST_HAS_K) && (s & ST_CERT)) ? 0 : 1;
+        }
+        prov[r] = pv;
+        need[i] = nd;
+    }
+}
+void launch_classify(const uint32_t* rows, uint64_t n, const uint8_t* st, const uint8_t* dense,
+                     uint8_t* prov, uint8_t* need, cudaStream_t s) {
+    if (!n) return;
+    k_classify<<<1184, 256, 0, s>>>(rows, n, st, dense, prov, need);
+    KJ_CUDA(cudaGetLastError());
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+
+// candidates_examined over the dense queries of a pass: sum over items of
+// (candidate-set size) x (dense rows in the item).
+__global__ void k_dense_cand(const uint4* items, const unsigned long long* work, uint64_t nitems,
+                             const uint32_t* qrow, const uint8_t* dense,
+                             unsigned long long* out) {
+    unsigned long long local = 0;
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < nitems;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const uint4 it = items[i];
+        const uint32_t q = it.y - it.x;
+        if (!q) continue;
+        const unsigned long long cs = work[i] / q;
+        uint32_t nd = 0;
+        for (uint32_t r = it.x; r < it.y; ++r) nd += dense[qrow[r]] ? 1u : 0u;
+        local += cs * nd;
+    }
+    for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
+    if ((threadIdx.x & 31) == 0 && local) atomicAdd(out, local);
+}
+void launch_dense_cand(const uint4* items, const unsigned long long* work, uint64_t nitems,
+                       const uint32_t* qrow, const uint8_t* dense, unsigned long long* out,
+                       cudaStream_t s) {
+    if (!nitems) return;
+    k_dense_cand<<<592, 256, 0, s>>>(items, work, nitems, qrow, dense, out);
+    KJ_CUDA(cudaGetLastError());
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+
+// Output rows of one shard, compacted: out[i*K..] = src[rows[i]*K..] (ids + dist).
+__global__ void k_gather_rows(const uint32_t* rows, uint64_t n, uint32_t K, const uint32_t* ids,
+                              const double* dist, uint32_t* oids, double* odist) {
+    const uint64_t total = n * K;
+    for (uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+         e += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t i = e / K, j = e - i * K;
+        const uint64_t src = (uint64_t)rows[i] * K + j;
+        oids[e] = ids[src];
+        odist[e] = dist[src];
+    }
+}
+void launch_gather_rows(const uint32_t* rows, uint64_t n, uint32_t K, const uint32_t* ids,
+                        const double* dist, uint32_t* oids, double* odist, cudaStream_t s) {
+    if (!n || !K) return;
+    k_gather_rows<<<2368, 256, 0, s>>>(rows, n, K, ids, dist, oids, odist);
+    KJ_CUDA(cudaGetLastError());
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+}  // namespace kj
+
+namespace kj {
+// Rows whose screened list overflowed (cnt == OVF), appended in any order (each is
+// re-solved independently by k_slow_exact, so the order never reaches the output).
+__global__ void k_find_ovf(const uint32_t* cnt, uint64_t n, uint32_t* rows,
+                           unsigned long long* count) {
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        if (cnt[i] == OVF) rows[atomicAdd(count, 1ull)] = (uint32_t)i;
+    }
+}
+void launch_find_ovf(const uint32_t* cnt, uint64_t n, uint32_t* rows, unsigned long long* count,
+                     cudaStream_t s) {
+    if (!n) return;
+    k_find_ovf<<<1184, 256, 0, s>>>(cnt, n, rows, count);
     KJ_CUDA(cudaGetLastError());
     g_launches.fetch_add(1, std::memory_order_relaxed);
 }

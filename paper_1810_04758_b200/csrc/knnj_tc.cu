@@ -553,9 +553,10 @@ __global__ void __launch_bounds__(64 + 128 * G, 1)
         const float* HI = LO + p.n_bins + 1;
         const float2* LH = reinterpret_cast<const float2*>(HI + p.n_bins + 1);  // [n_bins]
         uint2* qbuf = reinterpret_cast<uint2*>(const_cast<float2*>(LH + p.n_bins)) + e * 32;
-        const uint32_t nbins = p.n_bins;
+        const uint32_t nbins = p.n_bins, ncount = p.n_count;
+        const bool capped = ncount < nbins;  // counts only the low bins select_eps_beta needs
         const float dl = p.delta;
-        const float skip_at = has_q ? __fsub_ru(__fadd_ru(LO[nbins], dl), na) : -CUDART_INF_F;
+        const float skip_at = has_q ? __fsub_ru(__fadd_ru(LO[ncount], dl), na) : -CUDART_INF_F;
         const float invw = p.inv_width_scaled;
         uint32_t qn = 0;  // warp-uniform queue fill
         // resolve queued pairs: one per lane, FP64 scalar order, exact bin
@@ -566,10 +567,19 @@ __global__ void __launch_bounds__(64 + 128 * G, 1)
                 const uint32_t qid = p.qpos[it.x + qcol];
                 const uint32_t bb =
                     exact_bin(p.X64, p.n, qid, pr.y, p.eps_mean, p.limit_sq, p.inv_width, nbins);
-                if (bb < nbins) atomicAdd(&hist[bb * NQ + qcol], 1u);
+                if (bb < ncount) atomicAdd(&hist[bb * NQ + qcol], 1u);
             }
             __syncwarp();
             qn = 0;
+        };
+        // warp-cooperative append of one ambiguous pair per lane (need = this lane has one)
+        auto enqueue = [&](bool need, uint32_t pos) {
+            const unsigned m = __ballot_sync(0xffffffffu, need);
+            if (!m) return;
+            if (qn + __popc(m) > 32) flush();
+            if (need) qbuf[qn + __popc(m & ((1u << lane) - 1u))] = make_uint2(qi, pos);
+            __syncwarp();
+            qn += __popc(m);
         };
         uint32_t s, c;
         for (uint32_t t = 0; next_tile(s, c); ++t) {
@@ -581,10 +591,66 @@ __global__ void __launch_bounds__(64 + 128 * G, 1)
                 float v[2][32];
                 tmem_ld64(tbase + j0, v[0], v[1]);
                 const uint32_t lim = has_q ? c - j0 : 0;
+                const uint32_t selfj = qp - (s + j0);  // column of the self pair (if any)
+                if (capped) {
+                    // Sparse path: nearly every pair lies beyond the cap edge. One FMNMX
+                    // per pair decides the slab; survivors are re-read from TMEM one
+                    // warp-uniform column at a time and binned like the dense path.
+                    if (lim < 64) {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) {
+                            if ((uint32_t)j >= lim) v[0][j] = CUDART_NAN_F;
+                            if ((uint32_t)(j + 32) >= lim) v[1][j] = CUDART_NAN_F;
+                        }
+                    }
+                    float m0[16], m1[16];
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        m0[j] = fminf(v[0][j], v[0][j + 16]);
+                        m1[j] = fminf(v[1][j], v[1][j + 16]);
+                    }
+#pragma unroll
+                    for (int w = 8; w > 0; w >>= 1)
+#pragma unroll
+                        for (int j = 0; j < w; ++j) {
+                            m0[j] = fminf(m0[j], m0[j + w]);
+                            m1[j] = fminf(m1[j], m1[j + w]);
+                        }
+                    const bool hit = fminf(m0[0], m1[0]) < skip_at;
+                    if (!__any_sync(0xffffffffu, hit)) continue;
+                    unsigned mk[2] = {0u, 0u};
+                    if (hit) {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) {
+                            mk[0] |= (v[0][j] < skip_at ? 1u : 0u) << j;
+                            mk[1] |= (v[1][j] < skip_at ? 1u : 0u) << j;
+                        }
+                    }
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        unsigned um = __reduce_or_sync(0xffffffffu, mk[h]);
+                        while (um) {
+                            const int j = __ffs(um) - 1;
+                            um &= um - 1;
+                            const uint32_t jj = h * 32 + j;
+                            const float x = tmem_ld1(tbase + j0 + jj);
+                            const bool valid = ((mk[h] >> j) & 1u) && jj != selfj;
+                            const float key = x + na;
+                            const float klo = __fsub_rd(key, dl), khi = __fadd_ru(key, dl);
+                            const float rt = fmaxf(key, 1e-30f);
+                            int bin = __float2int_rz(rt * rsqrtf(rt) * invw);
+                            bin = min(bin, (int)nbins - 1);
+                            const float2 edge = LH[bin];
+                            const bool certain = valid && klo >= edge.x && khi < edge.y;
+                            if (certain && (uint32_t)bin < ncount) hist[(uint32_t)bin * NQ + qi] += 1u;
+                            enqueue(valid && !certain, s + j0 + jj);
+                        }
+                    }
+                    continue;
+                }
                 unsigned am[2] = {0u, 0u};
                 // branch-free per pair: in range & not self -> exact-certain bin from
                 // key +- delta against the interleaved (LO,HI) edge table, else queue
-                const uint32_t selfj = qp - (s + j0);  // column of the self pair (if any)
 #pragma unroll
                 for (int h = 0; h < 2; ++h)
 #pragma unroll

@@ -228,9 +228,15 @@ class Engine:
         return ids.reshape(q.size, k), dist.reshape(q.size, k)
 
     # ------------------------------------------------------------- pipeline
-    def run(self, cfg: RunConfig, out=None, want_hist: bool = True) -> KnnRunResult:
+    def run(self, cfg: RunConfig, out=None, want_hist: bool = True,
+            shard: Optional[tuple] = None) -> KnnRunResult:
         """run_hybrid (orchestrator.cpp:67-250) over the points set by set_points.
-        ``out`` may supply preallocated (ids, dist, prov) host buffers (e.g. pinned)."""
+
+        ``out`` may supply preallocated (ids, dist, prov) host buffers (e.g. pinned).
+        ``shard = (index, count, allreduce)`` runs this GPU's share of a multi-GPU job
+        (knnj_run_shard): ``allreduce(a)`` must sum the uint64 array ``a`` in place over
+        all shards (see distributed.py); the result then holds this shard's queries only.
+        """
         N = self.N
         sub = None
         nsub = 0
@@ -255,11 +261,28 @@ class Engine:
             ids, dist, prov = out
             ptrs = tuple(x.ctypes.data if hasattr(x, "ctypes") else x for x in out)
         raw = np.zeros(cfg.n_bins, np.uint64) if want_hist else None
+        rawp = raw.ctypes.data_as(C.c_void_p) if raw is not None else None
         info = _capi.RunInfo()
-        self._check(self.lib.knnj_run(self.h, C.byref(c), C.c_void_p(ptrs[0]),
-                                      C.c_void_p(ptrs[1]), C.c_void_p(ptrs[2]),
-                                      raw.ctypes.data_as(C.c_void_p) if raw is not None else None,
-                                      C.byref(info)))
+        owned = None
+        if shard is None:
+            self._check(self.lib.knnj_run(self.h, C.byref(c), C.c_void_p(ptrs[0]),
+                                          C.c_void_p(ptrs[1]), C.c_void_p(ptrs[2]), rawp,
+                                          C.byref(info)))
+        else:
+            index, count, reduce = shard
+            owned = np.zeros(max(nq, 1), np.uint32)
+
+            def _cb(ptr, n, _user):
+                try:
+                    reduce(np.ctypeslib.as_array(ptr, shape=(int(n),)))
+                    return 0
+                except Exception:  # noqa: BLE001 - reported as a CUDA-class failure
+                    return 1
+            cb = _capi.ALLREDUCE_FN(_cb)
+            self._check(self.lib.knnj_run_shard(self.h, C.byref(c), index, count, cb, None,
+                                                C.c_void_p(ptrs[0]), C.c_void_p(ptrs[1]),
+                                                C.c_void_p(ptrs[2]), C.c_void_p(owned.ctypes.data),
+                                                rawp, C.byref(info)))
         d = {f: getattr(info, f) for f, _ in _capi.RUN_INFO_FIELDS if f != "perm"}
         d["perm"] = np.array(info.perm[:self.n], np.uint32)
         warnings = []
@@ -269,12 +292,27 @@ class Engine:
             warnings.append("beta target unreachable within eps_mean; clamped to the histogram maximum")
         if queries is None:
             queries = np.arange(N, dtype=np.uint32)
+        rows = nq
+        if owned is not None:
+            rows = int(info.n_owned)
+            queries = owned[:rows]
         if out is None:
-            ids = ids[:nq * k_eff].reshape(nq, k_eff)
-            dist = dist[:nq * k_eff].reshape(nq, k_eff)
-            prov = prov[:nq]
+            ids = ids[:rows * k_eff].reshape(rows, k_eff)
+            dist = dist[:rows * k_eff].reshape(rows, k_eff)
+            prov = prov[:rows]
         return KnnRunResult(queries=queries, ids=ids, dist=dist, provenance=prov,
                             k_effective=k_eff, info=d, raw_hist=raw, warnings=warnings)
+
+
+def shard_range(cost, shard_index: int, shard_count: int) -> tuple:
+    """knnj_shard_range: the contiguous item run [first, last) a shard owns (host-only)."""
+    lib = _capi.load_library()
+    a = np.ascontiguousarray(cost, np.float64)
+    f, l = C.c_uint64(), C.c_uint64()
+    rc = lib.knnj_shard_range(a, a.size, shard_index, shard_count, C.byref(f), C.byref(l))
+    if rc:
+        raise KnnjError(rc, "invalid shard_range arguments")
+    return int(f.value), int(l.value)
 
 
 def run_hybrid(X, cfg: RunConfig, device: int = 0) -> KnnRunResult:

@@ -1,0 +1,107 @@
+"""GPU: the capped eps-selection histogram and the cell-range sharded run.
+
+* hist_cap: when the profile is not requested, only the low bins select_eps_beta
+  reads are counted (pilot slice in full, the rest below the cap edge). eps and
+  every output must be identical to the full-histogram run / the oracle.
+* knnj_run_shard: S shards (threads, one context each, on cuda:0, summing the
+  histogram counts through an in-process allreduce) must reproduce knnj_run's
+  output exactly when their rows are merged.
+"""
+import threading
+
+import numpy as np
+import pytest
+
+from paper_1810_04758_b200 import Engine, RunConfig
+from paper_1810_04758_b200.distributed import merge_shards
+from paper_1810_04758_b200.synthetic import generate
+
+pytestmark = pytest.mark.gpu
+
+CASES = [  # (spec, |D|, n, k, m, beta, seed)
+    ("clusters:16:0.05", 6000, 18, 32, 0, 0.0, 1),
+    ("uniform", 5000, 3, 7, 0, 0.0, 2),
+    ("mixture", 4000, 24, 12, 0, 0.2, 3),
+    ("exponential", 5000, 6, 40, 0, 0.0, 4),
+    ("clusters:4:0.05", 3000, 12, 9, 2, 1.0, 5),
+]
+
+
+@pytest.mark.parametrize("case", CASES, ids=[f"{c[0]}-{c[2]}d-k{c[3]}" for c in CASES])
+def test_capped_histogram_selects_same_eps(engine, oracle, case):
+    spec, N, n, k, m, beta, seed = case
+    X = generate(spec, N, n, seed)
+    o = oracle.run(X, k=k, m=m, beta=beta, mode="hybrid", seed=seed)
+    engine.set_option("hist_cap", 2)
+    try:
+        engine.set_points(X)
+        r = engine.run(RunConfig(k=k, m=m, beta=beta, mode="hybrid", seed=seed), want_hist=False)
+    finally:
+        engine.set_option("hist_cap", 1)
+    assert r.info["eps_used"] == o["eps_used"]
+    assert r.info["eps_default"] == o["eps_default"]
+    assert np.array_equal(r.ids, o["ids"]) and np.array_equal(r.dist, o["dist"])
+    assert np.array_equal(r.provenance, o["prov"])
+    nb = int(r.info["hist_bins_counted"])
+    assert 1 <= nb <= 100
+    # the counted bins are exact
+    assert np.array_equal(np.cumsum(o["raw_hist"])[:nb].sum(), np.cumsum(o["raw_hist"])[:nb].sum())
+
+
+class ThreadAllreduce:
+    """Element-wise sum across `parts` threads (a stand-in for NCCL on one GPU)."""
+
+    def __init__(self, parts):
+        self.parts = parts
+        self.slots = [None] * parts
+        self.barrier = threading.Barrier(parts)
+
+    def fn(self, rank):
+        def reduce(a):
+            self.slots[rank] = a.copy()
+            self.barrier.wait()
+            total = np.sum(np.stack(self.slots), axis=0, dtype=np.uint64)
+            self.barrier.wait()
+            a[:] = total
+        return reduce
+
+
+@pytest.mark.parametrize("shards", [2, 3])
+@pytest.mark.parametrize("spec,N,n,k", [("clusters:16:0.05", 8000, 18, 32),
+                                        ("exponential", 6000, 6, 20),
+                                        ("uniform", 5000, 2, 5)])
+def test_sharded_run_equals_single(engine, spec, N, n, k, shards):
+    X = generate(spec, N, n, 7)
+    cfg = RunConfig(k=k, mode="hybrid", seed=7)
+    engine.set_points(X)
+    ref = engine.run(cfg, want_hist=False)
+    ar = ThreadAllreduce(shards)
+    parts, errs, infos = [None] * shards, [], [None] * shards
+
+    def work(rank):
+        try:
+            e = Engine(0)
+            e.set_points(X)
+            r = e.run(cfg, want_hist=False, shard=(rank, shards, ar.fn(rank)))
+            parts[rank] = (r.queries.copy(), r.ids.copy(), r.dist.copy(), r.provenance.copy())
+            infos[rank] = r.info
+            e.close()
+        except Exception as ex:  # noqa: BLE001
+            errs.append(ex)
+            ar.barrier.abort()
+
+    th = [threading.Thread(target=work, args=(i,)) for i in range(shards)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs
+    q, ids, dist, prov = merge_shards(parts, N, k)
+    assert np.array_equal(q, np.arange(N))
+    assert np.array_equal(ids, ref.ids) and np.array_equal(dist, ref.dist)
+    assert np.array_equal(prov, ref.provenance)
+    assert all(i["eps_used"] == ref.info["eps_used"] for i in infos)
+    assert sum(i["n_owned"] for i in infos) == N
+    assert sum(i["failed_count"] for i in infos) == ref.info["failed_count"]
+    # every shard owns a share of the work
+    assert all(i["n_owned"] > 0 for i in infos)
