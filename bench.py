@@ -191,12 +191,21 @@ def run_ours(args, cfgd, X):
 
     from paper_1810_04758_b200 import Engine, RunConfig
     rank, world, local = dist_env()
+    # one process per GPU; KNNJ_DIST_BACKEND=gloo runs all ranks on the visible GPUs
+    # round-robin (a multi-rank smoke of the sharded path on a 1-GPU box)
+    backend = os.environ.get("KNNJ_DIST_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     N, n = X.shape
     k = cfgd["k"]
     eng = Engine(local)
+    print(f"[bench] rank {rank}/{world} on cuda:{local} backend={backend if world > 1 else '-'}",
+          file=sys.stderr)
     stream = torch.cuda.ExternalStream(eng.lib.knnj_stream(eng.h), device=torch.device("cuda", local))
     lib = eng.lib
 
@@ -234,7 +243,7 @@ def run_ours(args, cfgd, X):
         barrier()
         ms = ev0.elapsed_time(ev1) / steps
         if world > 1:
-            t = torch.tensor([ms], device="cuda")
+            t = torch.tensor([ms], device="cuda" if backend == "nccl" else "cpu")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms = float(t.item())
         return ms, infos

@@ -1,0 +1,62 @@
+// TEST INFRASTRUCTURE — drop-in check of include/knnj_knnjoin_adapter.hpp.
+//
+// Links the UNMODIFIED reference library (compiled by path, oracle/Makefile) and
+// the B200 engine, then for each case runs the reference's own
+// knnjoin::run_hybrid (kernel "scalar") and knnjoin_b200::run_hybrid on the same
+// knnjoin::Dataset (drawn by the reference's generate_synthetic) and requires
+// byte-identical io::tsv_string output, identical provenance, eps and failed
+// counts. Built only where /root/reference exists (oracle/_ref/adapter_check);
+// run on the GPU box by tests/test_gpu_adapter.py.
+#include <cstdio>
+#include <string>
+
+#include "knnj_knnjoin_adapter.hpp"
+#include "knnjoin/io.hpp"
+#include "knnjoin/kernels.hpp"
+#include "knnjoin/synthetic.hpp"
+
+int main() {
+    knnjoin::kernels::set_active_kernel("scalar");
+    struct Case {
+        const char* spec;
+        std::size_t size, dims, k, m;
+        double beta, gamma, rho;
+        knnjoin::EngineMode mode;
+    };
+    const Case cases[] = {
+        {"uniform", 4000, 2, 5, 0, 0.0, 0.0, 0.0, knnjoin::EngineMode::Hybrid},
+        {"clusters:16:0.05", 3000, 18, 32, 0, 0.0, 0.0, 0.0, knnjoin::EngineMode::Hybrid},
+        {"mixture", 2000, 6, 10, 0, 0.2, 0.5, 0.3, knnjoin::EngineMode::Hybrid},
+        {"clusters:4:0.1", 1500, 24, 16, 4, 0.0, 0.0, 0.0, knnjoin::EngineMode::DenseOnly},
+        {"mixture", 1200, 90, 8, 0, 0.0, 0.0, 0.0, knnjoin::EngineMode::SparseOnly},
+        {"uniform", 900, 3, 7, 0, 0.0, 0.0, 0.0, knnjoin::EngineMode::BruteOracle},
+    };
+    knnjoin_b200::Engine eng(0);
+    int bad = 0, n = 0;
+    for (const Case& c : cases) {
+        const knnjoin::Dataset d =
+            knnjoin::generate_synthetic(knnjoin::SyntheticSpec::parse(c.spec), c.size, c.dims, 11);
+        knnjoin::RunConfig cfg;
+        cfg.k = c.k;
+        cfg.m = c.m;
+        cfg.beta = c.beta;
+        cfg.gamma = c.gamma;
+        cfg.rho = c.rho;
+        cfg.mode = c.mode;
+        cfg.seed = 5;
+        cfg.buffer_size = 100'000'000;
+        const knnjoin::KnnRunResult ref = knnjoin::run_hybrid(d, cfg);
+        const knnjoin::KnnRunResult got = knnjoin_b200::run_hybrid(eng, d, cfg);
+        const bool tsv = knnjoin::tsv_string(ref) == knnjoin::tsv_string(got);
+        const bool prov = ref.provenance == got.provenance;
+        const bool meta = ref.eps_used == got.eps_used && ref.failed_count == got.failed_count &&
+                          ref.k_effective == got.k_effective && ref.m_used == got.m_used;
+        const bool ok = tsv && prov && meta;
+        std::printf("%s %s |D|=%zu n=%zu k=%zu mode=%s tsv=%d prov=%d meta=%d\n", ok ? "ok " : "BAD",
+                    c.spec, c.size, c.dims, c.k, knnjoin::to_string(c.mode), tsv, prov, meta);
+        bad += !ok;
+        ++n;
+    }
+    std::printf("%s %d/%d\n", bad ? "ADAPTER MISMATCH" : "ADAPTER OK", n - bad, n);
+    return bad ? 1 : 0;
+}

@@ -55,3 +55,17 @@ def test_library_is_sm100a_only():
                          capture_output=True, text=True).stdout
     assert "sm_100a" in out
     assert "sm_90" not in out and "sm_80" not in out
+
+
+def test_adapter_header_compiles_against_reference_headers():
+    """include/knnj_knnjoin_adapter.hpp is valid C++20 against the reference's own
+    knnjoin headers (the drop-in a maintainer adds)."""
+    import shutil
+    import subprocess
+    ref_inc = "/root/reference/proj/include"
+    if not os.path.isdir(ref_inc) or not shutil.which("g++"):
+        pytest.skip("reference headers / g++ not available")
+    src = '#include "knnj_knnjoin_adapter.hpp"\nint main() { return 0; }\n'
+    p = subprocess.run(["g++", "-std=c++20", "-fsyntax-only", "-I", os.path.join(ROOT, "include"),
+                        "-I", ref_inc, "-x", "c++", "-"], input=src, capture_output=True, text=True)
+    assert p.returncode == 0, p.stderr
