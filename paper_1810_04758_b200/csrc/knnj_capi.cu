@@ -283,6 +283,7 @@ struct knnj_ctx {
     DBuf<double> d_part;
 
     ~knnj_ctx() {
+        if (h_sq) cudaFreeHost(h_sq);
         if (s) cudaStreamDestroy(s);
     }
 
@@ -421,37 +422,68 @@ struct knnj_ctx {
     }
 
     // ------------------------------------------------------------ eps_mean
+    // The sampled index pairs depend only on (|D|, pair count, seed): drawn once with
+    // the reference RNG and kept on the device, so repeated runs (and every shard of
+    // a multi-GPU run after its first) skip the ~15 ms host draw.
+    struct PairSample {
+        uint64_t N = 0, pairs = 0, seed = 0, used = 0;
+        DBuf<uint64_t> d_ij;
+    } eps_pairs;
+    double* h_sq = nullptr;  // pinned staging for the per-pair distances
+    uint64_t h_sq_cap = 0;
     double eps_mean(uint64_t sample_pairs, uint64_t seed) {
         if (N < 2) throw Error(1, "eps_mean estimation needs at least two points");
         if (sample_pairs < 1) throw Error(1, "sample_pairs must be at least 1");
-        const uint64_t all = N * (N - 1);
-        std::vector<uint64_t> ij;
-        uint64_t used;
-        if (sample_pairs >= all) {
-            ij.reserve(2 * all);
-            for (uint64_t i = 0; i < N; ++i)
-                for (uint64_t j = 0; j < N; ++j)
-                    if (i != j) {
-                        ij.push_back(i);
-                        ij.push_back(j);
-                    }
-            used = all;
-        } else {
-            ij.resize(2 * sample_pairs);
-            std::mt19937_64 rng(seed);
-            std::uniform_int_distribution<uint64_t> pick(0, N - 1);
-            for (uint64_t p = 0; p < sample_pairs; ++p) {
-                uint64_t i = pick(rng);
-                uint64_t j = pick(rng);
-                while (j == i) j = pick(rng);
-                ij[2 * p] = i;
-                ij[2 * p + 1] = j;
+        PairSample& ps = eps_pairs;
+        if (!(ps.N == N && ps.pairs == sample_pairs && ps.seed == seed && ps.used)) {
+            const uint64_t all = N * (N - 1);
+            std::vector<uint64_t> ij;
+            uint64_t used;
+            if (sample_pairs >= all) {  // exhaustive sweep (epsilon.cpp:14-44)
+                ij.reserve(2 * all);
+                for (uint64_t i = 0; i < N; ++i)
+                    for (uint64_t j = 0; j < N; ++j)
+                        if (i != j) {
+                            ij.push_back(i);
+                            ij.push_back(j);
+                        }
+                used = all;
+            } else {
+                ij.resize(2 * sample_pairs);
+                std::mt19937_64 rng(seed);
+                std::uniform_int_distribution<uint64_t> pick(0, N - 1);
+                for (uint64_t p = 0; p < sample_pairs; ++p) {
+                    uint64_t i = pick(rng);
+                    uint64_t j = pick(rng);
+                    while (j == i) j = pick(rng);
+                    ij[2 * p] = i;
+                    ij[2 * p + 1] = j;
+                }
+                used = sample_pairs;
             }
-            used = sample_pairs;
+            ps.d_ij.ensure(2 * used);
+            KJ_CUDA(cudaMemcpyAsync(ps.d_ij.p, ij.data(), 16 * used, cudaMemcpyHostToDevice, s));
+            sync();
+            ps.N = N;
+            ps.pairs = sample_pairs;
+            ps.seed = seed;
+            ps.used = used;
         }
-        std::vector<double> sq = pair_sq(ij.data(), used, kInf);
+        const uint64_t used = ps.used;
+        if (h_sq_cap < used) {
+            if (h_sq) cudaFreeHost(h_sq);
+            h_sq = nullptr;
+            KJ_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&h_sq), 8 * used, cudaHostAllocDefault));
+            h_sq_cap = used;
+        }
+        DBuf<double> d_out;
+        d_out.ensure(used);
+        launch_pair_sq(X64.p, n, ps.d_ij.p, used, kInf, d_out.p, s);
+        KJ_CUDA(cudaMemcpyAsync(h_sq, d_out.p, 8 * used, cudaMemcpyDeviceToHost, s));
+        sync();
+        // sequential FP64 sum in sample order, as the reference (bit-identical)
         double sum = 0.0;
-        for (uint64_t p = 0; p < used; ++p) sum += std::sqrt(sq[p]);
+        for (uint64_t p = 0; p < used; ++p) sum += std::sqrt(h_sq[p]);
         return sum / double(used);
     }
 
@@ -716,13 +748,27 @@ struct knnj_ctx {
         return nb;
     }
 
+    // sample_without_replacement depends only on (|D|, count, seed): cached like eps_pairs
+    struct QuerySample {
+        uint64_t N = 0, want = 0, seed = 0;
+        bool valid = false;
+        std::vector<uint64_t> ids;
+    } hist_sample;
     std::vector<uint64_t> histogram_sample(double frac, uint64_t seed) {
         if (!(frac > 0.0) || frac > 1.0) throw Error(1, "query_fraction must be in (0, 1]");
         uint64_t want = (uint64_t)std::floor(frac * double(N));
         want = std::max<uint64_t>(want, 100);
         want = std::min<uint64_t>(want, N);
-        std::mt19937_64 rng(seed);
-        return sample_without_replacement(N, want, rng);
+        QuerySample& qs = hist_sample;
+        if (!(qs.valid && qs.N == N && qs.want == want && qs.seed == seed)) {
+            std::mt19937_64 rng(seed);
+            qs.ids = sample_without_replacement(N, want, rng);
+            qs.N = N;
+            qs.want = want;
+            qs.seed = seed;
+            qs.valid = true;
+        }
+        return qs.ids;
     }
 
     // ------------------------------------------------------------ grid levels
