@@ -577,7 +577,7 @@ struct knnj_ctx {
         a.inv_width = inv_width;
         a.counts = d_cnt.p;
         screen_consts(a.gam, a.erg, a.eab, a.e64);
-        if (use_tc() && tc_smem_bytes(3 * n + 2 <= 64 ? 64 : 128, 0, nb, true) <= 227 * 1024) {
+        if (use_tc() && tc_smem_bytes(tc_hist_shape(), 0, nb, true) <= 227 * 1024) {
             histogram_tc(d_q.p, nq, em, nb, ncount, S, d_cnt.p);
             last_hist_tc = true;
             std::vector<unsigned long long> c(nb);
@@ -613,13 +613,14 @@ struct knnj_ctx {
     uint32_t bh_id_row = 0;
     void histogram_tc(const uint32_t* d_q, uint64_t nq, double em, uint32_t nb, uint32_t ncount,
                       const std::vector<double>& S_thr, unsigned long long* d_cnt) {
-        const uint32_t row_halfs = 3 * n + 2 <= 64 ? 64 : 128;
+        const uint32_t row_halfs = tc_row_halfs();
         if (!bh_id_ready || bh_id_row != row_halfs) {
             DBuf<uint32_t> ident;
             ident.ensure(N);
             launch_iota(ident.p, N, s);
             Bh_id.ensure(N * row_halfs);
-            launch_prep_tc(X64.p, ident.p, N, n, d_g.p, 1.0 / tc_S(), row_halfs, Bh_id.p, s);
+            launch_prep_tc(X64.p, ident.p, N, n, d_g.p, 1.0 / tc_S(), row_halfs, tc_split(),
+                           Bh_id.p, s);
             bh_id_ready = true;
             bh_id_row = row_halfs;
         }
@@ -633,7 +634,8 @@ struct knnj_ctx {
         DBuf<float> d_tab;
         d_tab.ensure(tab.size());
         KJ_CUDA(cudaMemcpyAsync(d_tab.p, tab.data(), 4 * tab.size(), cudaMemcpyHostToDevice, s));
-        const uint32_t NQ = tc_queries_per_item(row_halfs);
+        const TcShape hsh = tc_hist_shape();
+        const uint32_t NQ = 128u * hsh.G;
         const uint64_t qblocks = (nq + NQ - 1) / NQ;
         uint64_t slabs = std::max<uint64_t>(1, (148ull * 8 + qblocks - 1) / qblocks);
         uint64_t stride = (N + slabs - 1) / slabs;
@@ -657,6 +659,7 @@ struct knnj_ctx {
         TcJoinArgs a{};
         a.Bh = Bh_id.p;
         a.row_halfs = row_halfs;
+        a.split = tc_split();
         a.n = n;
         a.qpos = d_q;
         a.items = d_items.p;
@@ -674,7 +677,7 @@ struct knnj_ctx {
         a.inv_width = 1.0 / width;
         a.counts = d_cnt;
         Timer t(s);
-        launch_hist_tc(a, items.size(), N, s);
+        launch_hist_tc(a, hsh, items.size(), N, s);
         last_hist_kernel_ms = t.ms();
     }
 
@@ -893,10 +896,15 @@ struct knnj_ctx {
         lv.built = true;
     }
 
-    // Tensor-core screen policy: used where the GEMM form pays (n >= 12) and the
-    // hi/lo FP16 operand fits one or two 128-byte k-blocks (n <= 42).
+    // Tensor-core screen policy. Operand rows: split 3 (hi|lo|hi, K = 3n+2, ~22-bit
+    // products) when 3n+2 <= 128, padded to 64 or 128 halfs (1 or 2 128-byte
+    // k-blocks). The kernels also implement split 1 (hi only, K = n+2), but its
+    // 2^-11 |a||b| product error overflowed the near-tie lists on 90-D data (C3:
+    // 350k slow-path rows), so wider dims use the SIMT kernels.
     bool tc_enabled = true;
-    bool use_tc() const { return tc_enabled && n >= 12 && 3 * n + 2 <= 128; }
+    uint32_t tc_split() const { return 3 * n + 2 <= 128 ? 3 : 0; }
+    uint32_t tc_row_halfs() const { return tc_split() * n + 2 <= 64 ? 64 : 128; }
+    bool use_tc() const { return tc_enabled && tc_split() != 0; }
     double tc_S() const {
         double S = 1.0;
         while (S < Rg) S *= 2.0;
@@ -905,9 +913,10 @@ struct knnj_ctx {
     }
     void prep_tc(Level& lv) {
         if (lv.tc_ready) return;
-        lv.row_halfs = 3 * n + 2 <= 64 ? 64 : 128;
+        lv.row_halfs = tc_row_halfs();
+        lv.split = tc_split();
         lv.Bh.ensure(N * lv.row_halfs);
-        launch_prep_tc(X64.p, lv.J.p, N, n, d_g.p, 1.0 / tc_S(), lv.row_halfs, lv.Bh.p, s);
+        launch_prep_tc(X64.p, lv.J.p, N, n, d_g.p, 1.0 / tc_S(), lv.row_halfs, lv.split, lv.Bh.p, s);
         lv.tc_ready = true;
     }
     // Bound on |key - sq64/S^2| for the tensor-core screen.
@@ -917,16 +926,55 @@ struct knnj_ctx {
     // in FP32; each K=16 instruction rounds its partial sum) with a 4x
     // allowance per instruction — ~10x the largest error measured on B200
     // (tools/tc_probe.py, tests/test_gpu_screen.py keeps checking it).
+    // Split 1 (hi only) adds the dropped lo parts: |2a.b - 2a_hi.b_hi| <=
+    // 2(|a_lo||b| + |a_hi||b_lo|), |x_lo| <= 2^-11 |x| + sqrt(n) 2^-25 (FP16 subnormals).
     double tc_delta() const {
         const double u22 = std::ldexp(1.0, -22), u24 = std::ldexp(1.0, -24);
         const double R = Rg / tc_S();
         const double R2 = R * R;
-        const double n_mma = 4.0 * ((3.0 * n + 2.0 + 63.0) / 64.0);  // K=16 steps
-        const double T = 3.1 * R2;                                   // sum of |terms|
+        const double kdim = double(tc_split()) * n + 2.0;
+        const double n_mma = 4.0 * std::ceil(kdim / 64.0);  // K=16 steps
+        const double T = 3.1 * R2;                          // sum of |terms|
         const double acc = (n_mma + 2.0) * 4.0 * u24 * T;
         double d = acc + 6 * u22 * R2 + 2 * u24 * std::sqrt((double)n) * R + 2 * u22 * R2 +
                    2 * u24 + 5 * u24 * R2 + (4.0 * n + 12.0) * 4.0 * U64 * R2;
+        if (tc_split() == 1) {
+            const double lo = std::ldexp(1.0, -11) * R + std::sqrt((double)n) * std::ldexp(1.0, -25);
+            d += 4.0 * lo * R * (1.0 + std::ldexp(1.0, -10)) + 2.0 * lo * lo;
+        }
         return 1.5 * d;
+    }
+    // join kernel configuration for list capacity L (K + slack for near-ties in the band)
+    struct TcJoinCfg {
+        bool ok = false;
+        TcShape sh{1, 2, 4};
+        uint32_t L = 0;
+    };
+    // The GEMM-form key errs by ~u*R^2 (R = radius about the global centre) however
+    // close the pair is, so the tensor-core screen only pays when that band is small
+    // next to the pass's cell width w (skewed or very dense data: SIMT, whose tiles
+    // are centred per block).
+    bool tc_precise_for(double w) const {
+        const double S = tc_S();
+        return 2.0 * tc_delta() * S * S <= 0.02 * w * w;
+    }
+    TcJoinCfg tc_join_cfg(uint32_t K, double w) const {
+        TcJoinCfg c;
+        if (!use_tc() || K < 1 || !tc_precise_for(w)) return c;
+        const uint32_t KB = tc_row_halfs() / 64;
+        const uint32_t L0 = K + (tc_split() == 3 ? 24u : 48u);
+        if (L0 <= 64) {
+            c.sh = KB == 1 ? TcShape{1, 2, 4} : TcShape{2, 1, 3};
+            c.L = L0;
+        } else {
+            c.sh = KB == 1 ? TcShape{1, 1, 4} : TcShape{2, 1, 2};
+            c.L = std::min<uint32_t>(L0, 128);
+        }
+        c.ok = K + 8 <= c.L && tc_smem_bytes(c.sh, c.L, 0, false) <= 227 * 1024;
+        return c;
+    }
+    TcShape tc_hist_shape() const {
+        return tc_row_halfs() == 64 ? TcShape{1, 2, 4} : TcShape{2, 1, 3};
     }
 
     double cover2(const Level& lv) const {
@@ -944,18 +992,11 @@ struct knnj_ctx {
     // ------------------------------------------------------------ passes
     // Groups the queries (point ids + output rows, on device) by their cell in
     // level lv and builds work items + candidate ranges.
-    // unsorted candidate buffer per query in the tcgen05 join (<= 64: warp compaction)
-    static uint32_t tc_list_len(uint32_t K) { return std::min<uint32_t>(64, K + 24); }
     // the join kernel a pass will run on (decided before its items are built)
-    bool pass_uses_tc(const Level& lv, uint32_t K) const {
-        const uint32_t rh = 3 * n + 2 <= 64 ? 64 : 128;
-        return use_tc() && K + 8 <= 64 &&
-               tc_smem_bytes(lv.row_halfs ? lv.row_halfs : rh, tc_list_len(K), 0, false) <=
-                   227 * 1024;
-    }
+    bool pass_uses_tc(const Level& lv, uint32_t K) const { return tc_join_cfg(K, lv.w).ok; }
     uint32_t pass_chunk(const Level& lv, uint32_t K) const {
-        return pass_uses_tc(lv, K) ? tc_queries_per_item(lv.row_halfs ? lv.row_halfs : 64)
-                                   : (uint32_t)JB;
+        const TcJoinCfg c = tc_join_cfg(K, lv.w);
+        return c.ok ? 128u * c.sh.G : (uint32_t)JB;
     }
     // Sharded (nshard > 1): only a contiguous run of work items in cell order is kept
     // (SURVEY.md §8e), cut at equal shares of the estimated tile work; the pass then
@@ -1108,10 +1149,11 @@ struct knnj_ctx {
                   double cov2, uint32_t* out_ids, double* out_dist, double* out_kth,
                   uint8_t* out_status, uint64_t* n_slow) {
         if (!P.nq) return;
-        const bool tc = pass_uses_tc(lv, K) && P.chunk == tc_queries_per_item(lv.row_halfs);
+        const TcJoinCfg tcc = tc_join_cfg(K, lv.w);
+        const bool tc = tcc.ok && P.chunk == 128u * tcc.sh.G;
         if (!tc && P.chunk != (uint32_t)JB) throw Error(9, "pass built for a different kernel");
         // list capacity: K plus slack for near-ties inside the screen band (overflow -> exact slow path)
-        const uint32_t L = tc ? tc_list_len(K) : K + std::max<uint32_t>(16, K / 2);
+        const uint32_t L = tc ? tcc.L : K + std::max<uint32_t>(16, K / 2);
         if (L > 256) throw Error(1, "k above 170 is not supported by the device join");
         const int np = pick_np(n);
         if (np < 0) throw Error(1, "dimension count above 128 is not supported by the device join");
@@ -1124,6 +1166,7 @@ struct knnj_ctx {
             TcJoinArgs a{};
             a.Bh = lv.Bh.p;
             a.row_halfs = lv.row_halfs;
+            a.split = lv.split;
             a.n = n;
             a.qpos = P.qpos.p;
             a.items = P.items.p;
@@ -1142,7 +1185,7 @@ struct knnj_ctx {
             a.delta = f32_round_up(tc_delta());
             trace().mark("pass: pre-kernel", s);
             Timer t(s);
-            launch_join_tc(a, P.nitems, N, s);
+            launch_join_tc(a, tcc.sh, P.nitems, N, s);
             last_join_kernel_ms = t.ms();
             last_join_tc = true;
         } else {
@@ -1396,6 +1439,7 @@ int knnj_debug_tc_tile(knnj_ctx* c, uint32_t q0, uint32_t c0, float* D, uint16_t
         TcJoinArgs a{};
         a.Bh = lv.Bh.p;
         a.row_halfs = lv.row_halfs;
+        a.split = lv.split;
         a.n = c->n;
         a.qpos = d_qpos.p;
         a.items = d_item.p;
@@ -1406,7 +1450,7 @@ int knnj_debug_tc_tile(knnj_ctx* c, uint32_t q0, uint32_t c0, float* D, uint16_t
         a.out_pos = pos.p;
         a.delta = (float)c->tc_delta();
         a.dbg = d_dbg.p;
-        launch_join_tc(a, 1, c->N, c->s);
+        launch_join_tc(a, lv.row_halfs == 64 ? TcShape{1, 2, 4} : TcShape{2, 1, 3}, 1, c->N, c->s);
         KJ_CUDA(cudaMemcpyAsync(D, d_dbg.p, 4 * 128 * 128, cudaMemcpyDeviceToHost, c->s));
         KJ_CUDA(cudaMemcpyAsync(Bq, lv.Bh.p + (uint64_t)q0 * lv.row_halfs, 2 * 128 * lv.row_halfs,
                                 cudaMemcpyDeviceToHost, c->s));

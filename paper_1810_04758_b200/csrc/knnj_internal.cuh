@@ -122,7 +122,7 @@ struct Level {
     DBuf<uint32_t> posJ; // N: point id -> join-order position
     DBuf<float> Xs;      // n x Npad SoA, sorted order, centred floats
     bool tc_ready = false;
-    uint32_t row_halfs = 0;
+    uint32_t row_halfs = 0, split = 0;
     DBuf<__half> Bh;     // N x row_halfs: tensor-core B operand (knnj_tc.cu)
 };
 
@@ -162,6 +162,7 @@ struct JoinArgs {
 struct TcJoinArgs {
     const __half* Bh;        // level's B operand rows (sorted order)
     uint32_t row_halfs, n;
+    uint32_t split;          // 3: hi|lo|hi operand (K = 3n+2); 1: hi only (K = n+2)
     const uint32_t* qpos;
     const uint4* items;
     const uint2* adj;
@@ -223,13 +224,18 @@ void launch_morton_keys(const double* X64, const uint32_t* A, const uint32_t* sl
                         uint32_t n, uint32_t dims, const double* lo, const double* inv_range,
                         uint64_t* keys, uint32_t* vals, cudaStream_t s);
 void launch_inverse(const uint32_t* J, uint64_t N, uint32_t* posJ, cudaStream_t s);
-size_t tc_join_smem_bytes(int KB, uint32_t L);
-size_t tc_smem_bytes(uint32_t row_halfs, uint32_t L, uint32_t n_bins, bool hist);
-uint32_t tc_queries_per_item(uint32_t row_halfs);
-void launch_hist_tc(const TcJoinArgs& a, uint64_t nitems, uint64_t N, cudaStream_t s);
+// tensor-core kernel shape: KB 128-byte k-blocks per operand row (row_halfs = 64*KB),
+// G groups of 128 queries per CTA, STAGES candidate tiles in flight
+struct TcShape {
+    int KB, G, STAGES;
+};
+size_t tc_smem_bytes(const TcShape& sh, uint32_t L, uint32_t n_bins, bool hist);
+void launch_hist_tc(const TcJoinArgs& a, const TcShape& sh, uint64_t nitems, uint64_t N,
+                    cudaStream_t s);
 void launch_prep_tc(const double* X64, const uint32_t* A, uint64_t N, uint32_t n, const double* g,
-                    double inv_S, uint32_t row_halfs, __half* Bh, cudaStream_t s);
-void launch_join_tc(const TcJoinArgs& a, uint64_t nitems, uint64_t N, cudaStream_t s);
+                    double inv_S, uint32_t row_halfs, uint32_t split, __half* Bh, cudaStream_t s);
+void launch_join_tc(const TcJoinArgs& a, const TcShape& sh, uint64_t nitems, uint64_t N,
+                    cudaStream_t s);
 void launch_scale_f32(const float* in, uint64_t n, float scale, float* out, cudaStream_t s);
 int pick_np(uint32_t n);  // padded dimension count used by the templated kernels
 size_t join_smem_bytes(int np, uint32_t L);

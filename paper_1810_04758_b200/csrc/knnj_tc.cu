@@ -137,42 +137,57 @@ __device__ __forceinline__ float tmem_ld1(uint32_t taddr) {
     return __uint_as_float(r);
 }
 
-// K-th smallest (1-based k) of the 64 values a0 (element lane) and a1 (element
-// 32+lane) held across a warp: bitonic sort network, ascending.
-__device__ __forceinline__ float warp_kth64(float a0, float a1, uint32_t k) {
+// K-th smallest (1-based k) of the 32*R values a[r] (element index r*32 + lane)
+// held across a warp: bitonic sort network, ascending.
+template <int R>
+__device__ __forceinline__ float warp_kth(float (&a)[R], uint32_t k) {
     const int lane = threadIdx.x & 31;
 #pragma unroll
-    for (int kk = 2; kk <= 64; kk <<= 1) {
+    for (int kk = 2; kk <= 32 * R; kk <<= 1) {
 #pragma unroll
         for (int j = kk >> 1; j > 0; j >>= 1) {
-            if (j == 32) {
-                // pairs (lane, 32+lane): element index lane is the lower one
-                const bool up = (lane & kk) == 0;  // kk == 64 here: always ascending
-                const float lo = fminf(a0, a1), hi = fmaxf(a0, a1);
-                a0 = up ? lo : hi;
-                a1 = up ? hi : lo;
+            if (j >= 32) {
+                // partner in register r ^ (j/32) of the same lane
+                const int rj = j >> 5;
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    if (r & rj) continue;
+                    const int e = r * 32 + lane;
+                    const bool up = (e & kk) == 0;
+                    const float lo = fminf(a[r], a[r | rj]), hi = fmaxf(a[r], a[r | rj]);
+                    a[r] = up ? lo : hi;
+                    a[r | rj] = up ? hi : lo;
+                }
             } else {
-                const float p0 = __shfl_xor_sync(0xffffffffu, a0, j);
-                const float p1 = __shfl_xor_sync(0xffffffffu, a1, j);
-                const uint32_t i0 = lane, i1 = 32 + lane;
                 const bool lower = (lane & j) == 0;
-                const bool up0 = (i0 & kk) == 0, up1 = (i1 & kk) == 0;
-                a0 = (lower == up0) ? fminf(a0, p0) : fmaxf(a0, p0);
-                a1 = (lower == up1) ? fminf(a1, p1) : fmaxf(a1, p1);
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const float pv = __shfl_xor_sync(0xffffffffu, a[r], j);
+                    const int e = r * 32 + lane;
+                    const bool up = (e & kk) == 0;
+                    a[r] = (lower == up) ? fminf(a[r], pv) : fmaxf(a[r], pv);
+                }
             }
         }
     }
     const uint32_t i = k - 1;
-    const float v0 = __shfl_sync(0xffffffffu, a0, i & 31);
-    const float v1 = __shfl_sync(0xffffffffu, a1, i & 31);
-    return i < 32 ? v0 : v1;
+    float v = 0.f;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const float t = __shfl_sync(0xffffffffu, a[r], i & 31);
+        if ((i >> 5) == (uint32_t)r) v = t;
+    }
+    return v;
 }
 
 }  // namespace
 
-// B-operand rows for one grid level, sorted order: [hi | lo | hi | nb_hi nb_lo | 0]
+// B-operand rows for one grid level, sorted order. split 3: [hi | lo | hi | nb_hi nb_lo | 0]
+// (K = 3n+2, ~22-bit products); split 1: [hi | nb_hi nb_lo | 0] (K = n+2, for n > 42;
+// the dropped lo parts are part of the screen bound tc_delta).
 __global__ void k_prep_tc(const double* X64, const uint32_t* A, uint64_t N, uint32_t n,
-                          const double* g, double inv_S, uint32_t row_halfs, __half* Bh) {
+                          const double* g, double inv_S, uint32_t row_halfs, uint32_t split,
+                          __half* Bh) {
     for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < N;
          i += uint64_t(gridDim.x) * blockDim.x) {
         const double* x = X64 + (uint64_t)A[i] * n;
@@ -181,16 +196,18 @@ __global__ void k_prep_tc(const double* X64, const uint32_t* A, uint64_t N, uint
         for (uint32_t d = 0; d < n; ++d) {
             const double v = (x[d] - g[d]) * inv_S;
             const __half hi = __double2half(v);
-            const __half lo = __double2half(v - (double)__half2float(hi));
             row[d] = hi;
-            row[n + d] = lo;
-            row[2 * n + d] = hi;
+            if (split == 3) {
+                row[n + d] = __double2half(v - (double)__half2float(hi));
+                row[2 * n + d] = hi;
+            }
             nb += v * v;
         }
+        const uint32_t o = split * n;
         const __half nh = __double2half(nb);
-        row[3 * n] = nh;
-        row[3 * n + 1] = __double2half(nb - (double)__half2float(nh));
-        for (uint32_t c = 3 * n + 2; c < row_halfs; ++c) row[c] = __float2half(0.f);
+        row[o] = nh;
+        row[o + 1] = __double2half(nb - (double)__half2float(nh));
+        for (uint32_t c = o + 2; c < row_halfs; ++c) row[c] = __float2half(0.f);
     }
 }
 
@@ -226,7 +243,7 @@ __device__ __noinline__ uint32_t exact_bin(const double* X64, uint32_t n, uint32
 //               JOIN: screened top-K list insertion; HIST: exact-certain binning
 // Every role walks the same deterministic tile sequence (ranges of the item,
 // <=128 positions per tile, tiles never straddle a range).
-template <int KB, int G, int STAGES, bool HIST>
+template <int KB, int G, int STAGES, bool HIST, int LR>
 __global__ void __launch_bounds__(64 + 128 * G, 1)
     k_tc(const __grid_constant__ CUtensorMap tmB, TcJoinArgs p) {
     constexpr int NQ = 128 * G;                    // queries per block
@@ -292,9 +309,14 @@ __global__ void __launch_bounds__(64 + 128 * G, 1)
                         const uint32_t k = kb * KBLK + c * 8 + e2 * 2 + h;
                         __half v = __float2half(0.f);
                         if (has_q) {
-                            if (k < 2 * n) v = __hmul(__float2half(-2.f), qrow_g[k < n ? k : k - n]);
-                            else if (k < 3 * n) v = __hmul(__float2half(-2.f), qrow_g[k - n]);
-                            else if (k < 3 * n + 2) v = __float2half(1.f);
+                            if (p.split == 3) {  // [-2hi, -2hi, -2lo, 1, 1]
+                                if (k < 2 * n) v = __hmul(__float2half(-2.f), qrow_g[k < n ? k : k - n]);
+                                else if (k < 3 * n) v = __hmul(__float2half(-2.f), qrow_g[k - n]);
+                                else if (k < 3 * n + 2) v = __float2half(1.f);
+                            } else {             // [-2hi, 1, 1]
+                                if (k < n) v = __hmul(__float2half(-2.f), qrow_g[k]);
+                                else if (k < n + 2) v = __float2half(1.f);
+                            }
                         }
                         pair |= (uint32_t)__half_as_ushort(v) << (16 * h);
                     }
@@ -304,7 +326,7 @@ __global__ void __launch_bounds__(64 + 128 * G, 1)
                     make_uint4(w[0], w[1], w[2], w[3]);
             }
         }
-        if (has_q) na = __half2float(qrow_g[3 * n]) + __half2float(qrow_g[3 * n + 1]);
+        if (has_q) na = __half2float(qrow_g[p.split * n]) + __half2float(qrow_g[p.split * n + 1]);
     }
     if (HIST) {
         uint32_t* hist = reinterpret_cast<uint32_t*>(tail);
@@ -432,31 +454,37 @@ __global__ void __launch_bounds__(64 + 128 * G, 1)
             const uint32_t col = g * 128 + quarter * 32 + src;
             float* kb = lkey + (size_t)col * LB;
             uint32_t* pb = lpos + (size_t)col * LB;
-            const float k0 = (uint32_t)lane < c_src ? kb[lane] : CUDART_INF_F;
-            const float k1 = (uint32_t)(lane + 32) < c_src ? kb[lane + 32] : CUDART_INF_F;
-            const uint32_t p0 = (uint32_t)lane < c_src ? pb[lane] : 0u;
-            const uint32_t p1 = (uint32_t)(lane + 32) < c_src ? pb[lane + 32] : 0u;
-            const float kth = warp_kth64(k0, k1, p.K);
+            float kv[LR];
+            uint32_t pv[LR];
+#pragma unroll
+            for (int r = 0; r < LR; ++r) {
+                const uint32_t i = r * 32 + lane;
+                kv[r] = i < c_src ? kb[i] : CUDART_INF_F;
+                pv[r] = i < c_src ? pb[i] : 0u;
+            }
+            float srt[LR];
+#pragma unroll
+            for (int r = 0; r < LR; ++r) srt[r] = kv[r];
+            const float kth = warp_kth<LR>(srt, p.K);
             const float cap_src = __shfl_sync(0xffffffffu, cap, src);
             const float nc = fminf(__fadd_ru(kth, 2.f * dl), cap_src);
-            const bool keep0 = k0 <= nc, keep1 = k1 <= nc;
-            const unsigned b0 = __ballot_sync(0xffffffffu, keep0);
-            const unsigned b1 = __ballot_sync(0xffffffffu, keep1);
+            unsigned bal[LR];
+#pragma unroll
+            for (int r = 0; r < LR; ++r) bal[r] = __ballot_sync(0xffffffffu, kv[r] <= nc);
             const unsigned lt = (1u << lane) - 1u;
             __syncwarp();
-            if (keep0) {
-                const uint32_t at = __popc(b0 & lt);
-                kb[at] = k0;
-                pb[at] = p0;
-            }
-            if (keep1) {
-                const uint32_t at = __popc(b0) + __popc(b1 & lt);
-                kb[at] = k1;
-                pb[at] = p1;
+            uint32_t at = 0;
+#pragma unroll
+            for (int r = 0; r < LR; ++r) {
+                if (kv[r] <= nc) {
+                    kb[at + __popc(bal[r] & lt)] = kv[r];
+                    pb[at + __popc(bal[r] & lt)] = pv[r];
+                }
+                at += __popc(bal[r]);
             }
             __syncwarp();
             if (lane == src) {
-                cnt = __popc(b0) + __popc(b1);
+                cnt = at;
                 cut = nc;
                 rhs = __fsub_ru(cut, na);
                 if (cnt >= LB) {  // every entry inside the band: exact ties, slow path
@@ -712,33 +740,17 @@ __global__ void __launch_bounds__(64 + 128 * G, 1)
 }
 
 // ---------------------------------------------------------------- host side
-namespace {
-struct TcShape {
-    int KB, G, STAGES;
-};
-TcShape tc_shape(uint32_t row_halfs) {
-    const int KB = (int)(row_halfs / KBLK);
-    return KB == 1 ? TcShape{1, 2, 4} : TcShape{2, 1, 3};
-}
-}  // namespace
-
-uint32_t tc_queries_per_item(uint32_t row_halfs) { return 128u * tc_shape(row_halfs).G; }
-
-size_t tc_smem_bytes(uint32_t row_halfs, uint32_t L, uint32_t n_bins, bool hist) {
-    const TcShape sh = tc_shape(row_halfs);
+size_t tc_smem_bytes(const TcShape& sh, uint32_t L, uint32_t n_bins, bool hist) {
     const size_t NQ = 128 * sh.G;
     size_t b = 1024 + (size_t)(sh.G + sh.STAGES) * sh.KB * KB_BYTES;
     if (hist) b += NQ * n_bins * 4 + 8 * (n_bins + 1) + 8 * n_bins + 8 + (size_t)4 * sh.G * 32 * 8;
     else b += NQ * L * 8;
     return b;
 }
-size_t tc_join_smem_bytes(int KB, uint32_t L) {
-    return tc_smem_bytes(KB * KBLK, L, 0, false);
-}
 
 void launch_prep_tc(const double* X64, const uint32_t* A, uint64_t N, uint32_t n, const double* g,
-                    double inv_S, uint32_t row_halfs, __half* Bh, cudaStream_t s) {
-    k_prep_tc<<<2368, 256, 0, s>>>(X64, A, N, n, g, inv_S, row_halfs, Bh);
+                    double inv_S, uint32_t row_halfs, uint32_t split, __half* Bh, cudaStream_t s) {
+    k_prep_tc<<<2368, 256, 0, s>>>(X64, A, N, n, g, inv_S, row_halfs, split, Bh);
     KJ_CUDA(cudaGetLastError());
     g_launches.fetch_add(1, std::memory_order_relaxed);
 }
@@ -757,7 +769,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
     return fn;
 }
 
-template <int KB, int G, int STAGES, bool HIST>
+template <int KB, int G, int STAGES, bool HIST, int LR>
 static void launch_tc_t(const TcJoinArgs& a, uint64_t nitems, uint64_t N, cudaStream_t s) {
     CUtensorMap map;
     cuuint64_t dims[2] = {(cuuint64_t)a.row_halfs, (cuuint64_t)N};
@@ -769,34 +781,37 @@ static void launch_tc_t(const TcJoinArgs& a, uint64_t nitems, uint64_t N, cudaSt
                               CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw Error(9, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
-    const size_t sm = tc_smem_bytes(a.row_halfs, a.L, a.n_bins, HIST);
+    const size_t sm = tc_smem_bytes(TcShape{KB, G, STAGES}, a.L, a.n_bins, HIST);
     if (sm > 227 * 1024) throw Error(1, "tensor-core kernel needs too much shared memory");
-    KJ_CUDA(cudaFuncSetAttribute(k_tc<KB, G, STAGES, HIST>,
+    KJ_CUDA(cudaFuncSetAttribute(k_tc<KB, G, STAGES, HIST, LR>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     for (uint64_t off = 0; off < nitems; off += 2147483647ull) {
         const uint64_t cnt = std::min<uint64_t>(nitems - off, 2147483647ull);
         TcJoinArgs b = a;
         b.items = a.items + off;
-        k_tc<KB, G, STAGES, HIST><<<(unsigned)cnt, 64 + 128 * G, sm, s>>>(map, b);
+        k_tc<KB, G, STAGES, HIST, LR><<<(unsigned)cnt, 64 + 128 * G, sm, s>>>(map, b);
     }
     KJ_CUDA(cudaGetLastError());
     g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
-void launch_join_tc(const TcJoinArgs& a, uint64_t nitems, uint64_t N, cudaStream_t s) {
+void launch_join_tc(const TcJoinArgs& a, const TcShape& sh, uint64_t nitems, uint64_t N,
+                    cudaStream_t s) {
     if (!nitems) return;
-    const TcShape sh = tc_shape(a.row_halfs);
-    if (sh.KB == 1) launch_tc_t<1, 2, 4, false>(a, nitems, N, s);
-    else if (sh.KB == 2) launch_tc_t<2, 1, 3, false>(a, nitems, N, s);
-    else throw Error(1, "tensor-core join supports up to 42 dimensions");
+    const bool wide = a.L > 64;  // list compaction over 128 entries
+    if (sh.KB == 1 && sh.G == 2 && sh.STAGES == 4 && !wide) launch_tc_t<1, 2, 4, false, 2>(a, nitems, N, s);
+    else if (sh.KB == 1 && sh.G == 1 && sh.STAGES == 4 && wide) launch_tc_t<1, 1, 4, false, 4>(a, nitems, N, s);
+    else if (sh.KB == 2 && sh.G == 1 && sh.STAGES == 3 && !wide) launch_tc_t<2, 1, 3, false, 2>(a, nitems, N, s);
+    else if (sh.KB == 2 && sh.G == 1 && sh.STAGES == 2 && wide) launch_tc_t<2, 1, 2, false, 4>(a, nitems, N, s);
+    else throw Error(1, "no tensor-core join instance for this shape");
 }
 
-void launch_hist_tc(const TcJoinArgs& a, uint64_t nitems, uint64_t N, cudaStream_t s) {
+void launch_hist_tc(const TcJoinArgs& a, const TcShape& sh, uint64_t nitems, uint64_t N,
+                    cudaStream_t s) {
     if (!nitems) return;
-    const TcShape sh = tc_shape(a.row_halfs);
-    if (sh.KB == 1) launch_tc_t<1, 2, 4, true>(a, nitems, N, s);
-    else if (sh.KB == 2) launch_tc_t<2, 1, 3, true>(a, nitems, N, s);
-    else throw Error(1, "tensor-core histogram supports up to 42 dimensions");
+    if (sh.KB == 1 && sh.G == 2 && sh.STAGES == 4) launch_tc_t<1, 2, 4, true, 2>(a, nitems, N, s);
+    else if (sh.KB == 2 && sh.G == 1 && sh.STAGES == 3) launch_tc_t<2, 1, 3, true, 2>(a, nitems, N, s);
+    else throw Error(1, "no tensor-core histogram instance for this shape");
 }
 
 }  // namespace kj

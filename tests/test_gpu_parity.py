@@ -113,8 +113,6 @@ RANDOM += [
 @pytest.mark.parametrize("case", RANDOM, ids=[f"{c[0]}-{c[2]}d-k{c[3]}" for c in RANDOM])
 def test_random_instances_vs_oracle(engine, oracle, case, tc):
     spec, N, n, k, m, beta, gamma, rho, seed = case
-    if not tc and not (12 <= n <= 42):
-        pytest.skip("same kernel as the tcgen05 leg for this n")
     engine.set_option("tensor_cores", tc)
     X = generate(spec, N, n, seed)
     for mode in ("hybrid", "dense"):

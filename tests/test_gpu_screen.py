@@ -17,7 +17,8 @@ def _tile(engine, q0, c0, n):
     L.knnj_debug_tc_tile.argtypes = [C.c_void_p, C.c_uint32, C.c_uint32, C.c_void_p, C.c_void_p,
                                      C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double),
                                      C.c_void_p, C.c_void_p]
-    rh = 64 if 3 * n + 2 <= 64 else 128
+    split = 3 if 3 * n + 2 <= 128 else 1
+    rh = 64 if split * n + 2 <= 64 else 128
     D = np.zeros((128, 128), np.float32)
     Bq = np.zeros((128, rh), np.uint16)
     Bc = np.zeros((128, rh), np.uint16)
@@ -33,25 +34,29 @@ def _tile(engine, q0, c0, n):
 
 @pytest.mark.parametrize("spec,n,shift", [("clusters:16:0.05", 18, 0.0), ("uniform", 12, 0.0),
                                           ("clusters:4:0.01", 24, 1e3), ("mixture", 40, -7.5),
-                                          ("clusters:16:0.05", 18, 1e5)])
+                                          ("clusters:16:0.05", 18, 1e5), ("uniform", 2, 0.0),
+                                          ("exponential", 6, 0.0)])
 def test_tc_accumulator_error_far_below_delta(engine, spec, n, shift):
     X = generate(spec, 6000, n, 3) + shift
     engine.set_points(X)
-    engine.reorder_by_variance(6)
-    engine.grid_build(6, 0.5)
+    m = min(6, n)
+    engine.reorder_by_variance(m)
+    engine.grid_build(m, 0.5)
     W = engine.working_points()
     worst = 0.0
     for q0, c0 in ((0, 0), (1000, 3000), (5800, 17)):
         D, bq, bc, S, delta, pq, pc = _tile(engine, q0, c0, n)
+        split = 3 if 3 * n + 2 <= 128 else 1   # hi|lo|hi operand, or hi only (n > 42)
         a = np.zeros_like(bq)
         a[:, :n] = -2 * bq[:, :n]
-        a[:, n:2 * n] = -2 * bq[:, :n]
-        a[:, 2 * n:3 * n] = -2 * bq[:, n:2 * n]
-        a[:, 3 * n:3 * n + 2] = 1
+        if split == 3:
+            a[:, n:2 * n] = -2 * bq[:, :n]
+            a[:, 2 * n:3 * n] = -2 * bq[:, n:2 * n]
+        a[:, split * n:split * n + 2] = 1
         gemm = a @ bc.T
         worst = max(worst, float(np.abs(D - gemm).max()) / delta)
         # key vs the exact FP64 distance, in scaled units
-        na = bq[:, 3 * n] + bq[:, 3 * n + 1]
+        na = bq[:, split * n] + bq[:, split * n + 1]
         key = D.astype(np.float64) + na.astype(np.float32).astype(np.float64)[:, None]
         P, Q = W[pq], W[pc]
         sq = ((P[:, None, :] - Q[None, :, :]) ** 2).sum(-1) / (S * S)
