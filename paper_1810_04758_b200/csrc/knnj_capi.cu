@@ -278,6 +278,13 @@ struct knnj_ctx {
     double eps0 = 0.0;
     uint32_t m0 = 0;
 
+    // large per-run buffers kept across calls (grow only): no allocator churn in steady state
+    DBuf<uint32_t> pass_cnt, pass_pos;                   // join lists (run_pass)
+    DBuf<uint64_t> gk_keys, gk_skeys;                    // grid build sort scratch
+    DBuf<uint32_t> gk_vals, gk_runidx;
+    DBuf<uint32_t> r_ids, r_q, r_rows;                   // run outputs / query lists (run_impl)
+    DBuf<double> r_dist, r_kth;
+    DBuf<uint8_t> r_st, r_prov;
     // small device scratch
     DBuf<unsigned long long> d_u64a, d_u64b;
     DBuf<double> d_part;
@@ -838,8 +845,10 @@ struct knnj_ctx {
         KJ_CUDA(cudaMemcpyAsync(d_mins.p, lv.mins.data(), 8 * m, cudaMemcpyHostToDevice, s));
         KJ_CUDA(cudaMemcpyAsync(d_cs.p, lv.cpd.data(), 8 * m, cudaMemcpyHostToDevice, s));
         KJ_CUDA(cudaMemcpyAsync(d_cs.p + m, lv.strides.data(), 8 * m, cudaMemcpyHostToDevice, s));
-        DBuf<uint64_t> keys, skeys;
-        DBuf<uint32_t> vals, runidx;
+        DBuf<uint64_t>& keys = gk_keys;
+        DBuf<uint64_t>& skeys = gk_skeys;
+        DBuf<uint32_t>& vals = gk_vals;
+        DBuf<uint32_t>& runidx = gk_runidx;
         keys.ensure(N);
         skeys.ensure(N);
         vals.ensure(N);
@@ -902,6 +911,7 @@ struct knnj_ctx {
     // 2^-11 |a||b| product error overflowed the near-tie lists on 90-D data (C3:
     // 350k slow-path rows), so wider dims use the SIMT kernels.
     bool tc_enabled = true;
+    bool split_items = true;  // split oversized work items into candidate-range parts
     uint32_t tc_split() const { return 3 * n + 2 <= 128 ? 3 : 0; }
     uint32_t tc_row_halfs() const { return tc_split() * n + 2 <= 64 ? 64 : 128; }
     bool use_tc() const { return tc_enabled && tc_split() != 0; }
@@ -1006,6 +1016,8 @@ struct knnj_ctx {
                     const uint8_t* d_dense = nullptr) {
         P.nq = nq;
         P.nq_all = nq;
+        P.nv = nq;
+        P.nsplits = 0;
         P.row_begin = 0;
         P.candidates_dense = 0;
         const uint32_t chunk = K ? pass_chunk(lv, K) : (uint32_t)JB;
@@ -1105,35 +1117,128 @@ struct knnj_ctx {
             sync();
             P.candidates_dense = dc;
         }
-        // heaviest items first (LPT order for the block scheduler); ties keep cell order
-        std::vector<uint32_t> order(i1 - i0);
-        std::iota(order.begin(), order.end(), 0u);
-        std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) {
-            return h_work[i0 + a] > h_work[i0 + b];
-        });
-        std::vector<uint4> h_sorted(i1 - i0);
+        // rebase the owned items to the shard's row range
+        std::vector<uint4> own(h_items.begin() + i0, h_items.begin() + i1);
+        std::vector<unsigned long long> own_w(h_work.begin() + i0, h_work.begin() + i1);
         unsigned long long cand = 0;
-        for (uint64_t i = 0; i < i1 - i0; ++i) {
-            uint4 it = h_items[i0 + order[i]];
-            it.x -= r0;
-            it.y -= r0;
-            h_sorted[i] = it;
-            cand += h_work[i0 + order[i]];
+        for (uint64_t i = 0; i < own.size(); ++i) {
+            own[i].x -= r0;
+            own[i].y -= r0;
+            cand += own_w[i];
         }
-        if (r0 != 0 || r1 != nq) {
+        const uint64_t nq_own = r1 - r0;
+        // Split items whose candidate set is a large slice of the pass (few queries
+        // against huge neighbourhoods: fallback passes, skewed cells) into parts over
+        // candidate sub-ranges, so the tail of the schedule is not one CTA's scan.
+        P.nv = nq_own;
+        P.nsplits = 0;
+        std::vector<uint2> extra_adj;
+        std::vector<uint32_t> vsrc;
+        std::vector<uint4> splits;
+        {
+            std::vector<uint64_t> csz(own.size());
+            double W = 0.0;
+            uint64_t cmax = 0;
+            for (uint64_t i = 0; i < own.size(); ++i) {
+                const uint32_t q = own[i].y - own[i].x;
+                csz[i] = q ? own_w[i] / q : 0;
+                W += double(csz[i]) / 128.0 + 8.0;  // candidate tiles + per-item overhead
+                cmax = std::max(cmax, csz[i]);
+            }
+            const double part_tiles = std::max(64.0, W / (148.0 * 4.0));
+            if (split_items && K > 0 && double(cmax) / 128.0 > 2.0 * part_tiles) {
+                std::vector<uint2> h_adj(P.nadj);
+                KJ_CUDA(cudaMemcpyAsync(h_adj.data(), P.adj.p, 8 * P.nadj, cudaMemcpyDeviceToHost, s));
+                sync();
+                std::vector<uint4> kept;
+                std::vector<unsigned long long> kept_w;
+                for (uint64_t i = 0; i < own.size(); ++i) {
+                    const uint4 it = own[i];
+                    const uint32_t q = it.y - it.x;
+                    const double tiles = double(csz[i]) / 128.0;
+                    if (!(tiles > 2.0 * part_tiles) || q == 0) {
+                        kept.push_back(it);
+                        kept_w.push_back(own_w[i]);
+                        continue;
+                    }
+                    const uint32_t parts = (uint32_t)std::min<double>(32.0, std::ceil(tiles / part_tiles));
+                    const uint64_t per = (csz[i] + parts - 1) / parts;
+                    const uint32_t vbase = (uint32_t)P.nv;
+                    uint32_t made = 0;
+                    uint64_t filled = 0;
+                    uint32_t a_begin = (uint32_t)(P.nadj + extra_adj.size());
+                    for (uint32_t r = it.z; r < it.w; ++r) {
+                        uint32_t lo = h_adj[r].x;
+                        const uint32_t hi = h_adj[r].y;
+                        while (lo < hi) {
+                            const uint64_t take = std::min<uint64_t>(hi - lo, per - filled);
+                            extra_adj.push_back(make_uint2(lo, lo + (uint32_t)take));
+                            lo += (uint32_t)take;
+                            filled += take;
+                            if (filled == per) {  // close this part
+                                const uint32_t a_end = (uint32_t)(P.nadj + extra_adj.size());
+                                const uint32_t v0 = vbase + made * q;
+                                kept.push_back(make_uint4(v0, v0 + q, a_begin, a_end));
+                                kept_w.push_back((unsigned long long)q * filled);
+                                ++made;
+                                filled = 0;
+                                a_begin = a_end;
+                            }
+                        }
+                    }
+                    if (filled) {
+                        const uint32_t a_end = (uint32_t)(P.nadj + extra_adj.size());
+                        const uint32_t v0 = vbase + made * q;
+                        kept.push_back(make_uint4(v0, v0 + q, a_begin, a_end));
+                        kept_w.push_back((unsigned long long)q * filled);
+                        ++made;
+                    }
+                    for (uint32_t pidx = 0; pidx < made; ++pidx)
+                        for (uint32_t j = 0; j < q; ++j) vsrc.push_back(it.x + j);
+                    splits.push_back(make_uint4(it.x, q, made, vbase - (uint32_t)nq_own));
+                    P.nv += (uint64_t)made * q;
+                }
+                own.swap(kept);
+                own_w.swap(kept_w);
+                P.nsplits = splits.size();
+            }
+        }
+        // heaviest items first (LPT order for the block scheduler); ties keep cell order
+        std::vector<uint32_t> order(own.size());
+        std::iota(order.begin(), order.end(), 0u);
+        std::stable_sort(order.begin(), order.end(),
+                         [&](uint32_t a, uint32_t b) { return own_w[a] > own_w[b]; });
+        std::vector<uint4> h_sorted(own.size());
+        for (uint64_t i = 0; i < own.size(); ++i) h_sorted[i] = own[order[i]];
+        if (r0 != 0 || r1 != nq || P.nv > nq_own) {
             DBuf<uint32_t> qp2, qr2;
-            qp2.ensure(r1 - r0);
-            qr2.ensure(r1 - r0);
+            qp2.ensure(P.nv);
+            qr2.ensure(nq_own);
             if (r1 > r0) {
-                KJ_CUDA(cudaMemcpyAsync(qp2.p, P.qpos.p + r0, 4ull * (r1 - r0), cudaMemcpyDeviceToDevice, s));
-                KJ_CUDA(cudaMemcpyAsync(qr2.p, P.qrow.p + r0, 4ull * (r1 - r0), cudaMemcpyDeviceToDevice, s));
+                KJ_CUDA(cudaMemcpyAsync(qp2.p, P.qpos.p + r0, 4ull * nq_own, cudaMemcpyDeviceToDevice, s));
+                KJ_CUDA(cudaMemcpyAsync(qr2.p, P.qrow.p + r0, 4ull * nq_own, cudaMemcpyDeviceToDevice, s));
+            }
+            if (P.nv > nq_own) {  // virtual rows mirror their real row's query
+                P.vsrc.ensure(vsrc.size());
+                KJ_CUDA(cudaMemcpyAsync(P.vsrc.p, vsrc.data(), 4 * vsrc.size(), cudaMemcpyHostToDevice, s));
+                launch_map_u32(P.vsrc.p, qp2.p, vsrc.size(), qp2.p + nq_own, s);
+                P.splits.ensure(splits.size());
+                KJ_CUDA(cudaMemcpyAsync(P.splits.p, splits.data(), 16 * splits.size(), cudaMemcpyHostToDevice, s));
+                DBuf<uint2> adj2;
+                adj2.ensure(P.nadj + extra_adj.size());
+                if (P.nadj)
+                    KJ_CUDA(cudaMemcpyAsync(adj2.p, P.adj.p, 8 * P.nadj, cudaMemcpyDeviceToDevice, s));
+                KJ_CUDA(cudaMemcpyAsync(adj2.p + P.nadj, extra_adj.data(), 8 * extra_adj.size(),
+                                        cudaMemcpyHostToDevice, s));
+                P.adj.swap(adj2);
+                P.nadj += extra_adj.size();
             }
             P.qpos.swap(qp2);
             P.qrow.swap(qr2);
         }
-        P.nq = r1 - r0;
+        P.nq = nq_own;
         P.row_begin = r0;
-        P.nitems = i1 - i0;
+        P.nitems = h_sorted.size();
         P.items.ensure(P.nitems);
         if (P.nitems)
             KJ_CUDA(cudaMemcpyAsync(P.items.p, h_sorted.data(), 16 * P.nitems, cudaMemcpyHostToDevice, s));
@@ -1158,9 +1263,19 @@ struct knnj_ctx {
         const int np = pick_np(n);
         if (np < 0) throw Error(1, "dimension count above 128 is not supported by the device join");
         if (join_smem_bytes(np, L) > 227 * 1024) throw Error(1, "k too large for the device join");
-        DBuf<uint32_t> cnt, pos;
-        cnt.ensure(P.nq);
-        pos.ensure(P.nq * L);
+        const uint64_t nv = P.nv, nvv = P.nv - P.nq;  // launch rows; virtual (split-part) rows
+        DBuf<uint32_t>& cnt = pass_cnt;
+        DBuf<uint32_t>& pos = pass_pos;
+        cnt.ensure(nv);
+        pos.ensure(nv * L);
+        if (P.nsplits) launch_fill_u32(cnt.p, P.nq, SKIP, s);  // split real rows are merged later
+        DBuf<float> cut_ext;
+        if (d_init_cut && nvv) {  // virtual rows start from their real row's bound
+            cut_ext.ensure(nv);
+            KJ_CUDA(cudaMemcpyAsync(cut_ext.p, d_init_cut, 4 * P.nq, cudaMemcpyDeviceToDevice, s));
+            launch_gather_f32(P.vsrc.p, d_init_cut, nvv, cut_ext.p + P.nq, s);
+            d_init_cut = cut_ext.p;
+        }
         if (tc) {
             prep_tc(lv);
             TcJoinArgs a{};
@@ -1174,8 +1289,8 @@ struct knnj_ctx {
             DBuf<float> cut_scaled;
             if (d_init_cut) {
                 const double S = tc_S();
-                cut_scaled.ensure(P.nq);
-                launch_scale_f32(d_init_cut, P.nq, (float)(1.0 / (S * S)), cut_scaled.p, s);
+                cut_scaled.ensure(nv);
+                launch_scale_f32(d_init_cut, nv, (float)(1.0 / (S * S)), cut_scaled.p, s);
                 a.init_cut = cut_scaled.p;
             }
             a.K = K;
@@ -1226,27 +1341,68 @@ struct knnj_ctx {
         f.out_status = out_status;
         trace().mark("pass: join kernel", s);
         launch_finalize(f, s);
+        // split-part rows: finalized into their own exact top-K (with sq), merged below
+        DBuf<uint32_t> t_ids, t_cnt, v_iota;
+        DBuf<double> t_dist, t_sq, t_kth;
+        DBuf<uint8_t> t_st;
+        if (nvv) {
+            t_ids.ensure(nvv * K);
+            t_dist.ensure(nvv * K);
+            t_sq.ensure(nvv * K);
+            t_kth.ensure(nvv);
+            t_st.ensure(nvv);
+            t_cnt.ensure(nvv);
+            v_iota.ensure(nvv);
+            launch_iota(v_iota.p, nvv, s);
+            FinalArgs fv = f;
+            fv.qpos = P.qpos.p + P.nq;
+            fv.qrow = v_iota.p;
+            fv.cnt = cnt.p + P.nq;
+            fv.pos = pos.p + P.nq * L;
+            fv.nrows = nvv;
+            fv.out_ids = t_ids.p;
+            fv.out_dist = t_dist.p;
+            fv.out_kth = t_kth.p;
+            fv.out_status = t_st.p;
+            fv.out_sq = t_sq.p;
+            fv.out_count = t_cnt.p;
+            launch_finalize(fv, s);
+        }
         trace().mark("pass: finalize", s);
         // overflowed rows -> exact slow path on the same candidate sets (rows found on device)
-        DBuf<uint32_t> d_rows;
-        d_rows.ensure(P.nq);
-        d_u64b.ensure(1);
-        KJ_CUDA(cudaMemsetAsync(d_u64b.p, 0, 8, s));
-        launch_find_ovf(cnt.p, P.nq, d_rows.p, d_u64b.p, s);
-        unsigned long long novf = 0;
-        KJ_CUDA(cudaMemcpyAsync(&novf, d_u64b.p, 8, cudaMemcpyDeviceToHost, s));
-        sync();
-        trace().mark("pass: ovf scan", s);
-        if (n_slow) *n_slow += novf;
-        if (novf) {
-            DBuf<uint32_t> row_item;
-            row_item.ensure(P.nq);
-            launch_row_item(P.items.p, P.nitems, row_item.p, s);
-            launch_slow_exact(X64.p, n, lv.J.p, P.qpos.p, P.qrow.p, d_rows.p, novf, P.items.p,
-                              row_item.p, P.adj.p, K, eps2, cov2, out_ids, out_dist, out_kth,
-                              out_status, s);
+        DBuf<uint32_t> row_item;
+        bool have_row_item = false;
+        auto slow_range = [&](uint64_t r0, uint64_t nr, const uint32_t* qrow, uint32_t* o_ids,
+                              double* o_dist, double* o_kth, uint8_t* o_st, double* o_sq,
+                              uint32_t* o_cnt) {
+            if (!nr) return;
+            DBuf<uint32_t> d_rows;
+            d_rows.ensure(nr);
+            d_u64b.ensure(1);
+            KJ_CUDA(cudaMemsetAsync(d_u64b.p, 0, 8, s));
+            launch_find_ovf(cnt.p + r0, nr, d_rows.p, d_u64b.p, s);
+            unsigned long long novf = 0;
+            KJ_CUDA(cudaMemcpyAsync(&novf, d_u64b.p, 8, cudaMemcpyDeviceToHost, s));
             sync();
+            if (n_slow) *n_slow += novf;
+            if (!novf) return;
+            if (!have_row_item) {
+                row_item.ensure(nv);
+                launch_row_item(P.items.p, P.nitems, row_item.p, s);
+                have_row_item = true;
+            }
+            launch_slow_exact(X64.p, n, lv.J.p, P.qpos.p + r0, qrow, d_rows.p, novf, P.items.p,
+                              row_item.p + r0, P.adj.p, K, eps2, cov2, o_ids, o_dist, o_kth,
+                              o_st, o_sq, o_cnt, s);
+            sync();
+        };
+        slow_range(0, P.nq, P.qrow.p, out_ids, out_dist, out_kth, out_status, nullptr, nullptr);
+        if (nvv) {
+            slow_range(P.nq, nvv, v_iota.p, t_ids.p, t_dist.p, t_kth.p, t_st.p, t_sq.p, t_cnt.p);
+            launch_merge_parts(P.splits.p, P.nsplits, K, t_ids.p, t_sq.p, t_cnt.p, P.qrow.p, eps2,
+                               cov2, out_ids, out_dist, out_kth, out_status, s);
         }
+        trace().mark("pass: ovf + merge", s);
     }
 
     // Exact KNN for the given queries (pids + rows), certified globally: level
@@ -1269,21 +1425,21 @@ struct knnj_ctx {
         };
         std::vector<int> lvl(qpid.size());
         for (size_t i = 0; i < qpid.size(); ++i) lvl[i] = level_for(U[i], first_level - 1);
-        DBuf<float> d_cut_by_row;
+        DBuf<float> d_cut_by_row;  // only the current pass's rows are ever written / read
         d_cut_by_row.ensure(nrows_total);
-        std::vector<float> h_cut(nrows_total, std::numeric_limits<float>::infinity());
         while (!qpid.empty()) {
             const int L = *std::min_element(lvl.begin(), lvl.end());
             if (L >= 40) throw Error(9, "exact fallback did not converge");
             std::vector<uint32_t> sp, sr, rp, rr;
+            std::vector<float> scut;
             std::vector<double> ru;
             std::vector<int> rl;
             for (size_t i = 0; i < qpid.size(); ++i) {
                 if (lvl[i] == L) {
                     sp.push_back(qpid[i]);
                     sr.push_back(qrow[i]);
-                    h_cut[qrow[i]] = U[i] < kInf ? f32_round_up(U[i])
-                                                 : std::numeric_limits<float>::infinity();
+                    scut.push_back(U[i] < kInf ? f32_round_up(U[i])
+                                               : std::numeric_limits<float>::infinity());
                 } else {
                     rp.push_back(qpid[i]);
                     rr.push_back(qrow[i]);
@@ -1304,8 +1460,9 @@ struct knnj_ctx {
             d_cut.ensure(np);
             KJ_CUDA(cudaMemcpyAsync(d_p.p, sp.data(), 4 * np, cudaMemcpyHostToDevice, s));
             KJ_CUDA(cudaMemcpyAsync(d_r.p, sr.data(), 4 * np, cudaMemcpyHostToDevice, s));
-            KJ_CUDA(cudaMemcpyAsync(d_cut_by_row.p, h_cut.data(), 4 * nrows_total,
-                                    cudaMemcpyHostToDevice, s));
+            d_cut.ensure(np);
+            KJ_CUDA(cudaMemcpyAsync(d_cut.p, scut.data(), 4 * np, cudaMemcpyHostToDevice, s));
+            launch_scatter_f32(d_r.p, d_cut.p, np, d_cut_by_row.p, s);
             Pass P;
             build_pass(lv, d_p.p, d_r.p, np, P, K);
             trace().mark("levels: build_pass", s);
@@ -1469,6 +1626,8 @@ int knnj_set_option(knnj_ctx* c, const char* name, int64_t value) {
         const std::string k = name ? name : "";
         if (k == "tensor_cores") {
             c->tc_enabled = value != 0;
+        } else if (k == "split_items") {
+            c->split_items = value != 0;
         } else if (k == "hist_cap") {
             if (value < 0 || value > 2) throw Error(1, "hist_cap must be 0, 1 or 2");
             c->hist_cap_mode = (int)value;
@@ -1850,6 +2009,7 @@ static void run_impl(knnj_ctx* c, const knnj_config* cfg, uint32_t shard, uint32
         if (nshard > 1 && allreduce(buf, count, ar_user) != 0)
             throw Error(9, "allreduce callback failed");
     };
+    // query ids ascending (make_query_list, orchestrator.cpp:33-44); all points: implicit iota
     std::vector<uint32_t> queries;
     if (cfg->query_subset) {
         for (uint64_t i = 0; i < cfg->n_query_subset; ++i)
@@ -1857,11 +2017,16 @@ static void run_impl(knnj_ctx* c, const knnj_config* cfg, uint32_t shard, uint32
         queries.assign(cfg->query_subset, cfg->query_subset + cfg->n_query_subset);
         std::sort(queries.begin(), queries.end());
         queries.erase(std::unique(queries.begin(), queries.end()), queries.end());
-    } else {
-        queries.resize(N);
-        std::iota(queries.begin(), queries.end(), 0u);
     }
-    const uint64_t nq = queries.size();
+    const uint64_t nq = cfg->query_subset ? queries.size() : N;
+    auto qid = [&](uint64_t i) -> uint32_t { return cfg->query_subset ? queries[i] : (uint32_t)i; };
+    auto host_queries = [&]() -> const std::vector<uint32_t>& {
+        if (queries.size() != nq) {
+            queries.resize(nq);
+            std::iota(queries.begin(), queries.end(), 0u);
+        }
+        return queries;
+    };
     I.n_queries = nq;
     uint32_t k_eff = cfg->k;
     if (k_eff >= N) {
@@ -1888,18 +2053,22 @@ static void run_impl(knnj_ctx* c, const knnj_config* cfg, uint32_t shard, uint32
         return;
     }
     const bool all_points = !cfg->query_subset;
-    DBuf<uint32_t> o_ids;
-    DBuf<double> o_dist, o_kth;
-    DBuf<uint8_t> o_st, d_prov;
+    DBuf<uint32_t>& o_ids = c->r_ids;
+    DBuf<double>& o_dist = c->r_dist;
+    DBuf<double>& o_kth = c->r_kth;
+    DBuf<uint8_t>& o_st = c->r_st;
+    DBuf<uint8_t>& d_prov = c->r_prov;
     o_ids.ensure(nq * k_eff);
     o_dist.ensure(nq * k_eff);
     o_kth.ensure(nq);
     o_st.ensure(nq);
     d_prov.ensure(nq);
-    DBuf<uint32_t> d_q, d_rows;
+    DBuf<uint32_t>& d_q = c->r_q;
+    DBuf<uint32_t>& d_rows = c->r_rows;
     d_q.ensure(nq);
     d_rows.ensure(nq);
-    KJ_CUDA(cudaMemcpyAsync(d_q.p, queries.data(), 4 * nq, cudaMemcpyHostToDevice, s));
+    if (all_points) launch_iota(d_q.p, nq, s);
+    else KJ_CUDA(cudaMemcpyAsync(d_q.p, queries.data(), 4 * nq, cudaMemcpyHostToDevice, s));
     if (all_points) {
         KJ_CUDA(cudaMemcpyAsync(d_rows.p, d_q.p, 4 * nq, cudaMemcpyDeviceToDevice, s));
     } else {
@@ -1916,7 +2085,7 @@ static void run_impl(knnj_ctx* c, const knnj_config* cfg, uint32_t shard, uint32
         n_own = hi - lo;
         std::vector<uint32_t> rows(n_own), qp(n_own);
         std::iota(rows.begin(), rows.end(), (uint32_t)lo);
-        for (uint64_t i = 0; i < n_own; ++i) qp[i] = queries[lo + i];
+        for (uint64_t i = 0; i < n_own; ++i) qp[i] = qid(lo + i);
         const uint32_t me = std::min<uint32_t>(6, n);
         // width from the bounding box: cells holding ~2k points on average
         std::vector<unsigned long long> mn(me), mx(me), i0(me, ~0ull), i1(me, 0ull);
@@ -2055,7 +2224,7 @@ static void run_impl(knnj_ctx* c, const knnj_config* cfg, uint32_t shard, uint32
                     // rho demotion (pop, cell, pid order): the host reference path
                     std::vector<uint8_t> dense(nq);
                     knnj_split_info si{};
-                    int rc = knnj_split(c, queries.data(), nq, k_eff, cfg->beta, cfg->gamma,
+                    int rc = knnj_split(c, host_queries().data(), nq, k_eff, cfg->beta, cfg->gamma,
                                         cfg->rho, dense.data(), nullptr, &si);
                     if (rc) throw Error(rc, c->err);
                     alloc_stream() = s;
@@ -2132,7 +2301,7 @@ static void run_impl(knnj_ctx* c, const knnj_config* cfg, uint32_t shard, uint32
                 KJ_CUDA(cudaMemcpyAsync(fu.data(), g_kth.p, 8 * nfb, cudaMemcpyDeviceToHost, s));
                 c->sync();
                 for (uint64_t i = 0; i < nfb; ++i) {
-                    fp[i] = queries[fr[i]];
+                    fp[i] = qid(fr[i]);
                     if (!(st[i] & ST_HAS_K)) fu[i] = kInf;
                     if (pv[i] == KNNJ_PROV_DENSE_FAILED) ++I.failed_count;
                 }
@@ -2168,7 +2337,7 @@ static void run_impl(knnj_ctx* c, const knnj_config* cfg, uint32_t shard, uint32
             if (ids) KJ_CUDA(cudaMemcpyAsync(ids, o_ids.p, 4 * nq * k_eff, cudaMemcpyDeviceToHost, s));
             if (dist) KJ_CUDA(cudaMemcpyAsync(dist, o_dist.p, 8 * nq * k_eff, cudaMemcpyDeviceToHost, s));
             if (prov) KJ_CUDA(cudaMemcpyAsync(prov, d_prov.p, nq, cudaMemcpyDeviceToHost, s));
-            if (owned) std::memcpy(owned, queries.data(), 4 * nq);
+            if (owned) std::memcpy(owned, host_queries().data(), 4 * nq);
         } else if (n_own) {
             DBuf<uint32_t> c_ids, c_q;
             DBuf<double> c_dist;

@@ -94,6 +94,7 @@ struct DBuf {
 // ---------------------------------------------------------------- constants
 constexpr int JB = 128;          // threads (= queries) per join / histogram block
 constexpr uint32_t OVF = 0xFFFFFFFFu;
+constexpr uint32_t SKIP = 0xFFFFFFFEu;  // list count of a row whose item was split into parts
 
 // Status bits written by the finalize kernel, per query.
 enum : uint8_t {
@@ -140,6 +141,12 @@ struct Pass {
     DBuf<uint32_t> qrow;      // nq: output row of each query
     DBuf<uint4> items;        // nitems: qbeg, qend, abeg, aend
     DBuf<uint2> adj;          // nadj: candidate position ranges
+    // Items too large for the schedule are split into candidate-range parts. Parts run
+    // on virtual launch rows [nq, nv) (qpos copied from their real row, vsrc[v - nq]);
+    // splits[i] = (first real row, queries, parts, first virtual row - nq).
+    uint64_t nv = 0, nsplits = 0;
+    DBuf<uint32_t> vsrc;
+    DBuf<uint4> splits;
 };
 
 struct JoinArgs {
@@ -198,6 +205,8 @@ struct FinalArgs {
     double* out_dist;
     double* out_kth;         // [qrow]
     uint8_t* out_status;     // [qrow]
+    double* out_sq;          // optional [qrow * K]: exact sq (split-part rows, for the merge)
+    uint32_t* out_count;     // optional [qrow]: entries written (min(candidates, K))
 };
 
 struct HistArgs {
@@ -295,7 +304,15 @@ void launch_slow_exact(const double* X64, uint32_t n, const uint32_t* A, const u
                        const uint32_t* qrow, const uint32_t* rows, uint64_t nrows,
                        const uint4* items, const uint32_t* row_item, const uint2* adj,
                        uint32_t K, double eps2, double cover2, uint32_t* out_ids,
-                       double* out_dist, double* out_kth, uint8_t* out_status, cudaStream_t s);
+                       double* out_dist, double* out_kth, uint8_t* out_status, double* out_sq,
+                       uint32_t* out_count, cudaStream_t s);
+void launch_scatter_f32(const uint32_t* idx, const float* vals, uint64_t n, float* out,
+                        cudaStream_t s);
+void launch_fill_u32(uint32_t* p, uint64_t n, uint32_t v, cudaStream_t s);
+void launch_merge_parts(const uint4* splits, uint64_t nsplits, uint32_t K, const uint32_t* t_ids,
+                        const double* t_sq, const uint32_t* t_count, const uint32_t* qrow,
+                        double eps2, double cover2, uint32_t* out_ids, double* out_dist,
+                        double* out_kth, uint8_t* out_status, cudaStream_t s);
 
 void launch_split_flags(const uint32_t* pids, uint64_t nq, const uint32_t* slot, const uint2* G,
                         double n_thresh, uint8_t* dense, unsigned long long* n_sparse,

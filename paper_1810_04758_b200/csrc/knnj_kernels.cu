@@ -281,6 +281,7 @@ __global__ void k_finalize(FinalArgs a) {
     const int lane = threadIdx.x & 31;
     if (row >= a.nrows) return;
     const uint32_t c = a.cnt[row];
+    if (c == SKIP) return;  // a split row: its parts are finalized and merged separately
     const uint32_t orow = a.qrow[row];
     if (c == OVF) {
         if (lane == 0) a.out_status[orow] = ST_OVF;
@@ -326,6 +327,7 @@ __global__ void k_finalize(FinalArgs a) {
         if (f < E && i < c && rk[f] < a.K) {
             a.out_ids[(uint64_t)orow * a.K + rk[f]] = id[f];
             a.out_dist[(uint64_t)orow * a.K + rk[f]] = sqrt(sq[f]);
+            if (a.out_sq) a.out_sq[(uint64_t)orow * a.K + rk[f]] = sq[f];
             if (rk[f] == a.K - 1) kth = sq[f];
         }
     }
@@ -340,6 +342,7 @@ __global__ void k_finalize(FinalArgs a) {
         }
         a.out_status[orow] = st;
         a.out_kth[orow] = c >= a.K ? kth : CUDART_INF;
+        if (a.out_count) a.out_count[orow] = min(c, a.K);
     }
 }
 
@@ -1014,7 +1017,7 @@ __global__ void k_slow_exact(const double* X64, uint32_t n, const uint32_t* A,
                              uint64_t nrows, const uint4* items, const uint32_t* row_item,
                              const uint2* adj, uint32_t K, double eps2, double cover2,
                              uint32_t* out_ids, double* out_dist, double* out_kth,
-                             uint8_t* out_status) {
+                             uint8_t* out_status, double* out_sq, uint32_t* out_count) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     double* ls = reinterpret_cast<double*>(smem_raw);      // [K][32]
     uint32_t* li = reinterpret_cast<uint32_t*>(ls + K * 32);  // [K][32]
@@ -1069,6 +1072,7 @@ __global__ void k_slow_exact(const double* X64, uint32_t n, const uint32_t* A,
         if (lane == 0) {
             out_ids[(uint64_t)orow * K + r] = bt;
             out_dist[(uint64_t)orow * K + r] = sqrt(bs);
+            if (out_sq) out_sq[(uint64_t)orow * K + r] = bs;
         }
         kth = bs;
     }
@@ -1081,19 +1085,21 @@ __global__ void k_slow_exact(const double* X64, uint32_t n, const uint32_t* A,
         }
         out_status[orow] = st;
         out_kth[orow] = total >= K ? kth : CUDART_INF;
+        if (out_count) out_count[orow] = outn;
     }
 }
 void launch_slow_exact(const double* X64, uint32_t n, const uint32_t* A, const uint32_t* qpos,
                        const uint32_t* qrow, const uint32_t* rows, uint64_t nrows,
                        const uint4* items, const uint32_t* row_item, const uint2* adj,
                        uint32_t K, double eps2, double cover2, uint32_t* out_ids,
-                       double* out_dist, double* out_kth, uint8_t* out_status, cudaStream_t s) {
+                       double* out_dist, double* out_kth, uint8_t* out_status, double* out_sq,
+                       uint32_t* out_count, cudaStream_t s) {
     if (!nrows) return;
     size_t sm = (size_t)K * 32 * (sizeof(double) + sizeof(uint32_t));
     set_smem(k_slow_exact, sm);
     k_slow_exact<<<(unsigned)nrows, 32, sm, s>>>(X64, n, A, qpos, qrow, rows, nrows, items,
                                                  row_item, adj, K, eps2, cover2, out_ids,
-                                                 out_dist, out_kth, out_status);
+                                                 out_dist, out_kth, out_status, out_sq, out_count);
     KJ_CUDA(cudaGetLastError());
     g_launches.fetch_add(1, std::memory_order_relaxed);
 }
@@ -1364,6 +1370,108 @@ void launch_find_ovf(const uint32_t* cnt, uint64_t n, uint32_t* rows, unsigned l
                      cudaStream_t s) {
     if (!n) return;
     k_find_ovf<<<1184, 256, 0, s>>>(cnt, n, rows, count);
+    KJ_CUDA(cudaGetLastError());
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+}  // namespace kj
+
+namespace kj {
+// Rows whose work item was split into candidate-range parts (pass build): each part
+// was finalized exactly into its own sorted (sq, id) top-K; this merges the parts'
+// lists per query (warp argmin over the part heads, K steps) into the real row.
+// splits[i] = (first real row, queries, parts, first virtual row - nq).
+__global__ void k_merge_parts(const uint4* splits, uint64_t nsplits, uint32_t K,
+                              const uint32_t* t_ids, const double* t_sq, const uint32_t* t_count,
+                              const uint32_t* qrow, double eps2, double cover2,
+                              uint32_t* out_ids, double* out_dist, double* out_kth,
+                              uint8_t* out_status) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (uint64_t si = blockIdx.x; si < nsplits; si += gridDim.x) {
+        const uint4 sp = splits[si];
+        for (uint32_t qi = w; qi < sp.y; qi += nw) {
+            // lane p < parts follows part p's list
+            const bool act = (uint32_t)lane < sp.z;
+            const uint64_t v = act ? (uint64_t)sp.w + (uint64_t)lane * sp.y + qi : 0;
+            const uint32_t cnt = act ? t_count[v] : 0u;
+            uint32_t head = 0;
+            uint32_t total = cnt;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) total += __shfl_xor_sync(0xffffffffu, total, o);
+            const uint32_t orow = qrow[sp.x + qi];
+            const uint32_t outn = min(total, K);
+            double kth = CUDART_INF;
+            for (uint32_t r = 0; r < outn; ++r) {
+                const double s0 = head < cnt ? t_sq[v * K + head] : CUDART_INF;
+                const uint32_t i0 = head < cnt ? t_ids[v * K + head] : 0xFFFFFFFFu;
+                double bs = s0;
+                uint32_t bt = i0;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    const double s2 = __shfl_xor_sync(0xffffffffu, bs, o);
+                    const uint32_t t2 = __shfl_xor_sync(0xffffffffu, bt, o);
+                    if (pair_less(s2, t2, bs, bt)) {
+                        bs = s2;
+                        bt = t2;
+                    }
+                }
+                // parts hold disjoint candidates, so exactly one head carries (bs, bt)
+                if (head < cnt && i0 == bt && s0 == bs) ++head;
+                if (lane == 0) {
+                    out_ids[(uint64_t)orow * K + r] = bt;
+                    out_dist[(uint64_t)orow * K + r] = sqrt(bs);
+                }
+                kth = bs;
+            }
+            if (lane == 0) {
+                uint8_t st = 0;
+                if (total >= K) {
+                    st |= ST_HAS_K;
+                    if (kth <= eps2) st |= ST_IN_EPS;
+                    if (kth < cover2) st |= ST_CERT;
+                }
+                out_status[orow] = st;
+                out_kth[orow] = total >= K ? kth : CUDART_INF;
+            }
+        }
+    }
+}
+void launch_merge_parts(const uint4* splits, uint64_t nsplits, uint32_t K, const uint32_t* t_ids,
+                        const double* t_sq, const uint32_t* t_count, const uint32_t* qrow,
+                        double eps2, double cover2, uint32_t* out_ids, double* out_dist,
+                        double* out_kth, uint8_t* out_status, cudaStream_t s) {
+    if (!nsplits) return;
+    k_merge_parts<<<(unsigned)std::min<uint64_t>(nsplits, 4096), 256, 0, s>>>(
+        splits, nsplits, K, t_ids, t_sq, t_count, qrow, eps2, cover2, out_ids, out_dist, out_kth,
+        out_status);
+    KJ_CUDA(cudaGetLastError());
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+}  // namespace kj
+
+namespace kj {
+__global__ void k_fill_u32(uint32_t* p, uint64_t n, uint32_t v) {
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x)
+        p[i] = v;
+}
+void launch_fill_u32(uint32_t* p, uint64_t n, uint32_t v, cudaStream_t s) {
+    if (!n) return;
+    k_fill_u32<<<1184, 256, 0, s>>>(p, n, v);
+    KJ_CUDA(cudaGetLastError());
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+}  // namespace kj
+
+namespace kj {
+__global__ void k_scatter_f32(const uint32_t* idx, const float* vals, uint64_t n, float* out) {
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x)
+        out[idx[i]] = vals[i];
+}
+void launch_scatter_f32(const uint32_t* idx, const float* vals, uint64_t n, float* out,
+                        cudaStream_t s) {
+    if (!n) return;
+    k_scatter_f32<<<592, 256, 0, s>>>(idx, vals, n, out);
     KJ_CUDA(cudaGetLastError());
     g_launches.fetch_add(1, std::memory_order_relaxed);
 }

@@ -105,3 +105,25 @@ def test_sharded_run_equals_single(engine, spec, N, n, k, shards):
     assert sum(i["failed_count"] for i in infos) == ref.info["failed_count"]
     # every shard owns a share of the work
     assert all(i["n_owned"] > 0 for i in infos)
+
+
+@pytest.mark.parametrize("spec,N,n,k,m", [("mixture", 60000, 5, 8, 0), ("uniform", 80000, 2, 20, 0),
+                                          ("mixture:4:0.02", 40000, 18, 32, 6)])
+def test_split_items_identical(engine, oracle, spec, N, n, k, m):
+    """Oversized work items are split into candidate-range parts and merged; the
+    output must not depend on it, and must equal brute force on sampled queries."""
+    X = generate(spec, N, n, 17)
+    cfg = RunConfig(k=k, m=m, mode="hybrid", seed=17)
+    out = []
+    for split in (0, 1):
+        engine.set_option("split_items", split)
+        engine.set_points(X)
+        out.append(engine.run(cfg, want_hist=False))
+    engine.set_option("split_items", 1)
+    a, b = out
+    assert np.array_equal(a.ids, b.ids) and np.array_equal(a.dist, b.dist)
+    assert np.array_equal(a.provenance, b.provenance)
+    W = X[:, b.info["perm"]]
+    q = np.random.default_rng(3).choice(N, 64, replace=False).astype(np.uint32)
+    oi, od = oracle.brute_knn(W, q, k)
+    assert np.array_equal(b.ids[q], oi) and np.array_equal(b.dist[q], od)
