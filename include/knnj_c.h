@@ -65,6 +65,8 @@ void* knnj_stream(knnj_ctx* ctx);
 int knnj_fp32_peak(knnj_ctx* ctx, double* tflops);
 /* Engine knobs (no reference analogue; results never depend on them):
  *   "tensor_cores" 0/1 : allow the tcgen05 distance screen (default 1).
+ *   "split_items" 0/1  : split work items with oversized candidate sets across CTAs (1).
+ *   "epi_halves" 0/1   : tcgen05 join with two epilogue warps per TMEM lane quarter (0).
  *   "hist_cap" 0/1/2   : eps-selection histogram counts only the bins select_eps_beta
  *                        needs when the profile is not requested: 0 never, 1 when the
  *                        histogram is large (default), 2 always (tests). */

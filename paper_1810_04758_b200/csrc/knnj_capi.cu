@@ -280,6 +280,7 @@ struct knnj_ctx {
 
     // large per-run buffers kept across calls (grow only): no allocator churn in steady state
     DBuf<uint32_t> pass_cnt, pass_pos;                   // join lists (run_pass)
+    DBuf<float> pass_key;                                // their keys (two-half epilogue)
     DBuf<uint64_t> gk_keys, gk_skeys;                    // grid build sort scratch
     DBuf<uint32_t> gk_vals, gk_runidx;
     DBuf<uint32_t> r_ids, r_q, r_rows;                   // run outputs / query lists (run_impl)
@@ -912,6 +913,9 @@ struct knnj_ctx {
     // 350k slow-path rows), so wider dims use the SIMT kernels.
     bool tc_enabled = true;
     bool split_items = true;  // split oversized work items into candidate-range parts
+    // tcgen05 join: 16 epilogue warps on 64-column halves (n <= 20). Off by default: on C2
+    // it measured 689 ms vs 647 ms for the 8-warp epilogue.
+    bool epi_halves = false;
     uint32_t tc_split() const { return 3 * n + 2 <= 128 ? 3 : 0; }
     uint32_t tc_row_halfs() const { return tc_split() * n + 2 <= 64 ? 64 : 128; }
     bool use_tc() const { return tc_enabled && tc_split() != 0; }
@@ -980,6 +984,7 @@ struct knnj_ctx {
             c.sh = KB == 1 ? TcShape{1, 1, 4} : TcShape{2, 1, 2};
             c.L = std::min<uint32_t>(L0, 128);
         }
+        if (epi_halves && KB == 1) c.sh = TcShape{1, 2, 8, 2};  // two epilogue warps per quarter
         c.ok = K + 8 <= c.L && tc_smem_bytes(c.sh, c.L, 0, false) <= 227 * 1024;
         return c;
     }
@@ -1264,11 +1269,12 @@ struct knnj_ctx {
         if (np < 0) throw Error(1, "dimension count above 128 is not supported by the device join");
         if (join_smem_bytes(np, L) > 227 * 1024) throw Error(1, "k too large for the device join");
         const uint64_t nv = P.nv, nvv = P.nv - P.nq;  // launch rows; virtual (split-part) rows
+        const uint32_t hv = (tc && tcc.sh.H == 2) ? 2u : 1u;  // lists per row
         DBuf<uint32_t>& cnt = pass_cnt;
         DBuf<uint32_t>& pos = pass_pos;
-        cnt.ensure(nv);
-        pos.ensure(nv * L);
-        if (P.nsplits) launch_fill_u32(cnt.p, P.nq, SKIP, s);  // split real rows are merged later
+        cnt.ensure(hv * nv);
+        pos.ensure(hv * nv * L);
+        if (P.nsplits) launch_fill_u32(cnt.p, hv * P.nq, SKIP, s);  // split real rows are merged later
         DBuf<float> cut_ext;
         if (d_init_cut && nvv) {  // virtual rows start from their real row's bound
             cut_ext.ensure(nv);
@@ -1297,6 +1303,10 @@ struct knnj_ctx {
             a.L = L;
             a.out_cnt = cnt.p;
             a.out_pos = pos.p;
+            if (hv == 2) {
+                pass_key.ensure(2 * nv * L);
+                a.out_key = pass_key.p;
+            }
             a.delta = f32_round_up(tc_delta());
             trace().mark("pass: pre-kernel", s);
             Timer t(s);
@@ -1339,6 +1349,7 @@ struct knnj_ctx {
         f.out_dist = out_dist;
         f.out_kth = out_kth;
         f.out_status = out_status;
+        f.halves = hv == 2 ? 1u : 0u;
         trace().mark("pass: join kernel", s);
         launch_finalize(f, s);
         // split-part rows: finalized into their own exact top-K (with sq), merged below
@@ -1357,8 +1368,8 @@ struct knnj_ctx {
             FinalArgs fv = f;
             fv.qpos = P.qpos.p + P.nq;
             fv.qrow = v_iota.p;
-            fv.cnt = cnt.p + P.nq;
-            fv.pos = pos.p + P.nq * L;
+            fv.cnt = cnt.p + hv * P.nq;
+            fv.pos = pos.p + hv * P.nq * L;
             fv.nrows = nvv;
             fv.out_ids = t_ids.p;
             fv.out_dist = t_dist.p;
@@ -1380,7 +1391,7 @@ struct knnj_ctx {
             d_rows.ensure(nr);
             d_u64b.ensure(1);
             KJ_CUDA(cudaMemsetAsync(d_u64b.p, 0, 8, s));
-            launch_find_ovf(cnt.p + r0, nr, d_rows.p, d_u64b.p, s);
+            launch_find_ovf(cnt.p + hv * r0, nr, d_rows.p, d_u64b.p, hv == 2 ? 1u : 0u, s);
             unsigned long long novf = 0;
             KJ_CUDA(cudaMemcpyAsync(&novf, d_u64b.p, 8, cudaMemcpyDeviceToHost, s));
             sync();
@@ -1626,6 +1637,8 @@ int knnj_set_option(knnj_ctx* c, const char* name, int64_t value) {
         const std::string k = name ? name : "";
         if (k == "tensor_cores") {
             c->tc_enabled = value != 0;
+        } else if (k == "epi_halves") {
+            c->epi_halves = value != 0;
         } else if (k == "split_items") {
             c->split_items = value != 0;
         } else if (k == "hist_cap") {

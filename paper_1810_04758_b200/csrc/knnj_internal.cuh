@@ -175,8 +175,9 @@ struct TcJoinArgs {
     const uint2* adj;
     const float* init_cut;   // per launch row (scaled units), may be null
     uint32_t K, L;
-    uint32_t* out_cnt;
-    uint32_t* out_pos;
+    uint32_t* out_cnt;       // per launch row (H = 2: per row and half)
+    uint32_t* out_pos;       // per launch row * L (H = 2: row * 2L + half * L)
+    float* out_key;          // H = 2: the lists' screened keys, same layout as out_pos
     float delta;             // |key - sq64/S^2| bound (scaled units)
     float* dbg;              // test hook: block 0 dumps its first accumulator tile [128][128]
     // histogram epilogue (HIST kernels only)
@@ -207,6 +208,7 @@ struct FinalArgs {
     uint8_t* out_status;     // [qrow]
     double* out_sq;          // optional [qrow * K]: exact sq (split-part rows, for the merge)
     uint32_t* out_count;     // optional [qrow]: entries written (min(candidates, K))
+    uint32_t halves;         // 1: two lists per row (cnt[2r + h], pos[(2r + h) * L + i])
 };
 
 struct HistArgs {
@@ -237,6 +239,7 @@ void launch_inverse(const uint32_t* J, uint64_t N, uint32_t* posJ, cudaStream_t 
 // G groups of 128 queries per CTA, STAGES candidate tiles in flight
 struct TcShape {
     int KB, G, STAGES;
+    int H = 1;  // epilogue warps per lane quarter and group (2: split 64-column halves)
 };
 size_t tc_smem_bytes(const TcShape& sh, uint32_t L, uint32_t n_bins, bool hist);
 void launch_hist_tc(const TcJoinArgs& a, const TcShape& sh, uint64_t nitems, uint64_t N,
@@ -323,7 +326,7 @@ void launch_dense_cand(const uint4* items, const unsigned long long* work, uint6
                        const uint32_t* qrow, const uint8_t* dense, unsigned long long* out,
                        cudaStream_t s);
 void launch_find_ovf(const uint32_t* cnt, uint64_t n, uint32_t* rows, unsigned long long* count,
-                     cudaStream_t s);
+                     uint32_t halves, cudaStream_t s);
 void launch_gather_rows(const uint32_t* rows, uint64_t n, uint32_t K, const uint32_t* ids,
                         const double* dist, uint32_t* oids, double* odist, cudaStream_t s);
 

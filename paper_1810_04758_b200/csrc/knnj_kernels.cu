@@ -280,8 +280,13 @@ __global__ void k_finalize(FinalArgs a) {
     const uint64_t row = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (row >= a.nrows) return;
-    const uint32_t c = a.cnt[row];
+    uint32_t c = a.cnt[a.halves ? 2 * row : row];
     if (c == SKIP) return;  // a split row: its parts are finalized and merged separately
+    uint32_t c0 = c;        // halves: entries of list 0, then list 1
+    if (a.halves) {
+        const uint32_t c1 = a.cnt[2 * row + 1];
+        c = (c0 == OVF || c1 == OVF) ? OVF : c0 + c1;
+    }
     const uint32_t orow = a.qrow[row];
     if (c == OVF) {
         if (lane == 0) a.out_status[orow] = ST_OVF;
@@ -301,7 +306,9 @@ __global__ void k_finalize(FinalArgs a) {
         rk[e] = 0;
         const uint32_t i = e * 32 + lane;
         if (e < E && i < c) {
-            const uint32_t t = a.A[a.pos[row * a.L + i]];
+            const uint64_t pi = !a.halves ? row * a.L + i
+                                : (i < c0 ? (2 * row) * a.L + i : (2 * row + 1) * a.L + (i - c0));
+            const uint32_t t = a.A[a.pos[pi]];
             id[e] = t;
             sq[e] = exact_sq(qx, a.X64 + (uint64_t)t * a.n, a.n);
         }
@@ -1360,16 +1367,17 @@ namespace kj {
 // Rows whose screened list overflowed (cnt == OVF), appended in any order (each is
 // re-solved independently by k_slow_exact, so the order never reaches the output).
 __global__ void k_find_ovf(const uint32_t* cnt, uint64_t n, uint32_t* rows,
-                           unsigned long long* count) {
+                           unsigned long long* count, uint32_t halves) {
     for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
          i += uint64_t(gridDim.x) * blockDim.x) {
-        if (cnt[i] == OVF) rows[atomicAdd(count, 1ull)] = (uint32_t)i;
+        const bool o = halves ? (cnt[2 * i] == OVF || cnt[2 * i + 1] == OVF) : cnt[i] == OVF;
+        if (o) rows[atomicAdd(count, 1ull)] = (uint32_t)i;
     }
 }
 void launch_find_ovf(const uint32_t* cnt, uint64_t n, uint32_t* rows, unsigned long long* count,
-                     cudaStream_t s) {
+                     uint32_t halves, cudaStream_t s) {
     if (!n) return;
-    k_find_ovf<<<1184, 256, 0, s>>>(cnt, n, rows, count);
+    k_find_ovf<<<1184, 256, 0, s>>>(cnt, n, rows, count, halves);
     KJ_CUDA(cudaGetLastError());
     g_launches.fetch_add(1, std::memory_order_relaxed);
 }

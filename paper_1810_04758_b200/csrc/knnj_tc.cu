@@ -243,8 +243,12 @@ __device__ __noinline__ uint32_t exact_bin(const double* X64, uint32_t n, uint32
 //               JOIN: screened top-K list insertion; HIST: exact-certain binning
 // Every role walks the same deterministic tile sequence (ranges of the item,
 // <=128 positions per tile, tiles never straddle a range).
-template <int KB, int G, int STAGES, bool HIST, int LR>
-__global__ void __launch_bounds__(64 + 128 * G, 1)
+// H = 2 (JOIN): two epilogue warps per TMEM lane quarter and query group, each
+// screening one 64-column half of every tile with its own near-tie list (global
+// memory) and a cut shared with its partner through shared memory: twice the
+// epilogue warps to hide the per-slab latency chain.
+template <int KB, int G, int STAGES, bool HIST, int LR, int H = 1>
+__global__ void __launch_bounds__(64 + 128 * G * H, 1)
     k_tc(const __grid_constant__ CUtensorMap tmB, TcJoinArgs p) {
     constexpr int NQ = 128 * G;                    // queries per block
     extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -255,6 +259,7 @@ __global__ void __launch_bounds__(64 + 128 * G, 1)
     unsigned char* tail = sB + STAGES * KB * KB_BYTES;
     __shared__ uint64_t bar_full[STAGES], bar_empty[STAGES], bar_accf[2], bar_acce[2];
     __shared__ uint32_t s_tmem;
+    __shared__ float s_cut[H == 2 ? 2 * NQ : 1];  // H=2: per (half, query) current cut
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint4 it = p.items[blockIdx.x];
@@ -274,7 +279,7 @@ __global__ void __launch_bounds__(64 + 128 * G, 1)
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&bar_accf[i], 1);
-            mbar_init(&bar_acce[i], 4 * G);
+            mbar_init(&bar_acce[i], 4 * G * H);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
@@ -282,16 +287,19 @@ __global__ void __launch_bounds__(64 + 128 * G, 1)
 
     // epilogue identity
     const int e = warp - 2;                      // epilogue warp index (valid if >= 0)
-    const int g = e >= 0 ? e / 4 : 0;            // query group
+    const int gh = e >= 0 ? e >> 2 : 0;
+    const int g = gh % G;                        // query group
+    const int hh = gh / G;                       // column half (H = 2)
     const int quarter = warp & 3;                // TMEM lane quarter this warp may access
     const uint32_t r = quarter * 32 + lane;      // accumulator row (= TMEM lane)
     const uint32_t qi = g * 128 + r;             // query index inside the item
-    const bool epi = e >= 0;
+    const bool epi = e >= 0 && e < 4 * G * H;
     const bool has_q = epi && qi < nq;
     const uint32_t row = it.x + (has_q ? qi : 0);
     const uint32_t qp = p.qpos[row];
     float na = 0.f;
-    if (epi) {
+    if (H == 2 && epi) s_cut[hh * NQ + qi] = CUDART_INF_F;
+    if (epi && hh == 0) {
         // A operand row r of group g: [-2hi, -2hi, -2lo, 1, 1, 0...] with the 128B swizzle
         const __half* qrow_g = p.Bh + (uint64_t)qp * p.row_halfs;
         const uint32_t n = p.n;
@@ -326,7 +334,10 @@ __global__ void __launch_bounds__(64 + 128 * G, 1)
                     make_uint4(w[0], w[1], w[2], w[3]);
             }
         }
-        if (has_q) na = __half2float(qrow_g[p.split * n]) + __half2float(qrow_g[p.split * n + 1]);
+    }
+    if (has_q) {
+        const __half* qrow_g = p.Bh + (uint64_t)qp * p.row_halfs;
+        na = __half2float(qrow_g[p.split * p.n]) + __half2float(qrow_g[p.split * p.n + 1]);
     }
     if (HIST) {
         uint32_t* hist = reinterpret_cast<uint32_t*>(tail);
@@ -436,11 +447,20 @@ __global__ void __launch_bounds__(64 + 128 * G, 1)
         // compacted warp-cooperatively (K-th key + 2 delta). Fast path: one
         // FMNMX per pair; survivors are re-read from TMEM one warp-uniform
         // column at a time (no per-lane dynamic indexing).
-        float* lkey = reinterpret_cast<float*>(tail);               // [NQ][L]
+        // H = 1: lists in shared memory, [NQ][L]; H = 2: rows of out_key/out_pos in
+        // global memory, [row][half][L]
+        float* lkey = reinterpret_cast<float*>(tail);
         uint32_t* lpos = reinterpret_cast<uint32_t*>(lkey + p.L * NQ);
         const uint32_t LB = p.L;
-        float* mykey = lkey + (size_t)qi * LB;
-        uint32_t* mypos = lpos + (size_t)qi * LB;
+        auto list_key = [&](uint32_t col) -> float* {
+            return H == 2 ? p.out_key + ((uint64_t)(it.x + col) * 2 + hh) * LB : lkey + (size_t)col * LB;
+        };
+        auto list_pos = [&](uint32_t col) -> uint32_t* {
+            return H == 2 ? p.out_pos + ((uint64_t)(it.x + col) * 2 + hh) * LB : lpos + (size_t)col * LB;
+        };
+        float* mykey = list_key(qi);
+        uint32_t* mypos = list_pos(qi);
+        float* pcut = H == 2 ? &s_cut[(hh ^ 1) * NQ + qi] : nullptr;  // partner half's cut
         uint32_t cnt = 0;
         bool ovf = false;
         const float init_cut = (p.init_cut && has_q) ? p.init_cut[row] : CUDART_INF_F;
@@ -450,23 +470,26 @@ __global__ void __launch_bounds__(64 + 128 * G, 1)
         float rhs = has_q ? __fsub_ru(cut, na) : -CUDART_INF_F;
         // compact the buffer of query column `src_lane` (all lanes cooperate)
         auto compact = [&](int src) {
+            if (H == 2) __syncwarp();  // the src lane's global appends are visible to the warp
             const uint32_t c_src = __shfl_sync(0xffffffffu, cnt, src);
             const uint32_t col = g * 128 + quarter * 32 + src;
-            float* kb = lkey + (size_t)col * LB;
-            uint32_t* pb = lpos + (size_t)col * LB;
+            float* kb = list_key(col);
+            uint32_t* pb = list_pos(col);
             float kv[LR];
             uint32_t pv[LR];
 #pragma unroll
             for (int r = 0; r < LR; ++r) {
                 const uint32_t i = r * 32 + lane;
-                kv[r] = i < c_src ? kb[i] : CUDART_INF_F;
-                pv[r] = i < c_src ? pb[i] : 0u;
+                kv[r] = i < c_src ? (H == 2 ? __ldcg(kb + i) : kb[i]) : CUDART_INF_F;
+                pv[r] = i < c_src ? (H == 2 ? __ldcg(pb + i) : pb[i]) : 0u;
             }
             float srt[LR];
 #pragma unroll
             for (int r = 0; r < LR; ++r) srt[r] = kv[r];
             const float kth = warp_kth<LR>(srt, p.K);
-            const float cap_src = __shfl_sync(0xffffffffu, cap, src);
+            float cap_src = __shfl_sync(0xffffffffu, cap, src);
+            // the partner half's cut bounds the global K-th too (it is a K-th + 2 delta)
+            if (H == 2) cap_src = fminf(cap_src, *(volatile float*)&s_cut[(hh ^ 1) * NQ + col]);
             const float nc = fminf(__fadd_ru(kth, 2.f * dl), cap_src);
             unsigned bal[LR];
 #pragma unroll
@@ -487,6 +510,7 @@ __global__ void __launch_bounds__(64 + 128 * G, 1)
                 cnt = at;
                 cut = nc;
                 rhs = __fsub_ru(cut, na);
+                if (H == 2) *(volatile float*)&s_cut[hh * NQ + col] = cut;
                 if (cnt >= LB) {  // every entry inside the band: exact ties, slow path
                     ovf = true;
                     rhs = -CUDART_INF_F;
@@ -499,7 +523,14 @@ __global__ void __launch_bounds__(64 + 128 * G, 1)
             mbar_wait(&bar_accf[b], (t >> 1) & 1);
             fence_after();
             const uint32_t tbase = tmem + ((uint32_t)(quarter * 32) << 16) + (g * 2 + b) * TC_N;
-            for (uint32_t j0 = 0; j0 < c; j0 += 64) {
+            if (H == 2 && has_q && !ovf) {  // the partner's tighter cut applies to new inserts
+                const float pc = *(volatile float*)pcut;
+                if (pc < cut) {
+                    cut = pc;
+                    rhs = __fsub_ru(cut, na);
+                }
+            }
+            for (uint32_t j0 = H == 2 ? hh * 64 : 0; j0 < c; j0 += H == 2 ? 128 : 64) {
                 float v0[32], v1[32];
                 tmem_ld64(tbase + j0, v0, v1);
                 if (p.dbg && blockIdx.x == 0 && t == 0 && g == 0)
@@ -570,9 +601,13 @@ __global__ void __launch_bounds__(64 + 128 * G, 1)
             if (lane == 0) mbar_arrive(&bar_acce[b]);
         }
         if (has_q) {
-            p.out_cnt[row] = ovf ? OVF : cnt;
-            if (!ovf)
-                for (uint32_t i = 0; i < cnt; ++i) p.out_pos[(uint64_t)row * LB + i] = mypos[i];
+            if (H == 2) {
+                p.out_cnt[(uint64_t)row * 2 + hh] = ovf ? OVF : cnt;  // positions already in place
+            } else {
+                p.out_cnt[row] = ovf ? OVF : cnt;
+                if (!ovf)
+                    for (uint32_t i = 0; i < cnt; ++i) p.out_pos[(uint64_t)row * LB + i] = mypos[i];
+            }
         }
     } else {
         // ------------------------------------------------ HISTOGRAM epilogue
@@ -744,7 +779,7 @@ size_t tc_smem_bytes(const TcShape& sh, uint32_t L, uint32_t n_bins, bool hist) 
     const size_t NQ = 128 * sh.G;
     size_t b = 1024 + (size_t)(sh.G + sh.STAGES) * sh.KB * KB_BYTES;
     if (hist) b += NQ * n_bins * 4 + 8 * (n_bins + 1) + 8 * n_bins + 8 + (size_t)4 * sh.G * 32 * 8;
-    else b += NQ * L * 8;
+    else if (sh.H == 1) b += NQ * L * 8;  // H = 2 keeps the lists in global memory
     return b;
 }
 
@@ -769,7 +804,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
     return fn;
 }
 
-template <int KB, int G, int STAGES, bool HIST, int LR>
+template <int KB, int G, int STAGES, bool HIST, int LR, int H = 1>
 static void launch_tc_t(const TcJoinArgs& a, uint64_t nitems, uint64_t N, cudaStream_t s) {
     CUtensorMap map;
     cuuint64_t dims[2] = {(cuuint64_t)a.row_halfs, (cuuint64_t)N};
@@ -781,15 +816,15 @@ static void launch_tc_t(const TcJoinArgs& a, uint64_t nitems, uint64_t N, cudaSt
                               CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw Error(9, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
-    const size_t sm = tc_smem_bytes(TcShape{KB, G, STAGES}, a.L, a.n_bins, HIST);
+    const size_t sm = tc_smem_bytes(TcShape{KB, G, STAGES, H}, a.L, a.n_bins, HIST);
     if (sm > 227 * 1024) throw Error(1, "tensor-core kernel needs too much shared memory");
-    KJ_CUDA(cudaFuncSetAttribute(k_tc<KB, G, STAGES, HIST, LR>,
+    KJ_CUDA(cudaFuncSetAttribute(k_tc<KB, G, STAGES, HIST, LR, H>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     for (uint64_t off = 0; off < nitems; off += 2147483647ull) {
         const uint64_t cnt = std::min<uint64_t>(nitems - off, 2147483647ull);
         TcJoinArgs b = a;
         b.items = a.items + off;
-        k_tc<KB, G, STAGES, HIST, LR><<<(unsigned)cnt, 64 + 128 * G, sm, s>>>(map, b);
+        k_tc<KB, G, STAGES, HIST, LR, H><<<(unsigned)cnt, 64 + 128 * G * H, sm, s>>>(map, b);
     }
     KJ_CUDA(cudaGetLastError());
     g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -799,6 +834,12 @@ void launch_join_tc(const TcJoinArgs& a, const TcShape& sh, uint64_t nitems, uin
                     cudaStream_t s) {
     if (!nitems) return;
     const bool wide = a.L > 64;  // list compaction over 128 entries
+    if (sh.H == 2) {
+        if (sh.KB == 1 && sh.G == 2 && sh.STAGES == 8 && !wide) launch_tc_t<1, 2, 8, false, 2, 2>(a, nitems, N, s);
+        else if (sh.KB == 1 && sh.G == 2 && sh.STAGES == 8 && wide) launch_tc_t<1, 2, 8, false, 4, 2>(a, nitems, N, s);
+        else throw Error(1, "no two-half tensor-core join instance for this shape");
+        return;
+    }
     if (sh.KB == 1 && sh.G == 2 && sh.STAGES == 4 && !wide) launch_tc_t<1, 2, 4, false, 2>(a, nitems, N, s);
     else if (sh.KB == 1 && sh.G == 1 && sh.STAGES == 4 && wide) launch_tc_t<1, 1, 4, false, 4>(a, nitems, N, s);
     else if (sh.KB == 2 && sh.G == 1 && sh.STAGES == 3 && !wide) launch_tc_t<2, 1, 3, false, 2>(a, nitems, N, s);

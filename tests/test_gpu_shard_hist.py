@@ -127,3 +127,25 @@ def test_split_items_identical(engine, oracle, spec, N, n, k, m):
     q = np.random.default_rng(3).choice(N, 64, replace=False).astype(np.uint32)
     oi, od = oracle.brute_knn(W, q, k)
     assert np.array_equal(b.ids[q], oi) and np.array_equal(b.dist[q], od)
+
+
+@pytest.mark.parametrize("spec,N,n,k", [("clusters:16:0.05", 20000, 18, 32), ("uniform", 30000, 12, 20),
+                                        ("mixture:4:0.05", 15000, 6, 50)])
+def test_epilogue_halves_identical(engine, oracle, spec, N, n, k):
+    """The tcgen05 join's two-warps-per-quarter epilogue (64-column halves, lists in
+    global memory, shared cuts) gives exactly the single-warp epilogue's output."""
+    X = generate(spec, N, n, 23)
+    cfg = RunConfig(k=k, mode="hybrid", seed=23)
+    out = []
+    for halves in (0, 1):
+        engine.set_option("epi_halves", halves)
+        engine.set_points(X)
+        out.append(engine.run(cfg, want_hist=False))
+    engine.set_option("epi_halves", 1)
+    a, b = out
+    assert np.array_equal(a.ids, b.ids) and np.array_equal(a.dist, b.dist)
+    assert np.array_equal(a.provenance, b.provenance)
+    W = X[:, b.info["perm"]]
+    q = np.random.default_rng(5).choice(N, 48, replace=False).astype(np.uint32)
+    oi, od = oracle.brute_knn(W, q, k)
+    assert np.array_equal(b.ids[q], oi) and np.array_equal(b.dist[q], od)
