@@ -221,6 +221,26 @@ int knnj_run_shard(knnj_ctx* ctx, const knnj_config* cfg, uint32_t shard_index,
                    uint32_t* ids, double* dist, uint8_t* prov, uint32_t* owned_queries,
                    uint64_t* raw_hist, knnj_run_info* info);
 
+/* ---- host I/O (no GPU needed) ------------------------------------------- */
+/* Message of the last failed I/O call on this thread. */
+const char* knnj_io_last_error(void);
+/* io::tsv_string (proj/src/io.cpp:141-154): "%u\t%u\t%.17g\n" per (query, rank), rows
+ * in the given order (queries NULL = row index). Byte-identical text, formatted by
+ * `threads` host threads (0 = all). out NULL: only *length (bytes) is computed. */
+int knnj_tsv_format(const uint32_t* queries, const uint32_t* ids, const double* dist,
+                    uint64_t n_rows, uint32_t k, char* out, uint64_t capacity, uint64_t* length,
+                    uint32_t threads);
+/* write_tsv (proj/src/io.cpp:137-139) to a file, formatted and written in parallel. */
+int knnj_tsv_write(const char* path, const uint32_t* queries, const uint32_t* ids,
+                   const double* dist, uint64_t n_rows, uint32_t k, uint32_t threads,
+                   uint64_t* bytes_written);
+/* ingest_binary (proj/src/io.cpp:69-91): LE u64 |D|, u64 n, |D|*n row-major f64.
+ * knnj_binary_header reads the sizes; knnj_binary_read fills `out` (e.g. a pinned
+ * buffer from knnj_alloc_pinned) and rejects short bodies / non-finite values with
+ * the reference's messages (KNNJ_E_INGEST). */
+int knnj_binary_header(const char* path, uint64_t* n_points, uint64_t* dims);
+int knnj_binary_read(const char* path, double* out, uint64_t capacity_doubles);
+
 #ifdef __cplusplus
 }
 #endif

@@ -125,6 +125,16 @@ SIGNATURES.append(
     ("knnj_run_shard", C.c_int, [_vp, C.POINTER(Config), C.c_uint32, C.c_uint32, ALLREDUCE_FN,
                                  _vp, _vp, _vp, _vp, _vp, _vp, C.POINTER(RunInfo)]))
 
+SIGNATURES += [
+    ("knnj_io_last_error", C.c_char_p, []),
+    ("knnj_tsv_format", C.c_int, [_vp, _vp, _vp, C.c_uint64, C.c_uint32, _vp, C.c_uint64,
+                                  C.POINTER(C.c_uint64), C.c_uint32]),
+    ("knnj_tsv_write", C.c_int, [C.c_char_p, _vp, _vp, _vp, C.c_uint64, C.c_uint32, C.c_uint32,
+                                 C.POINTER(C.c_uint64)]),
+    ("knnj_binary_header", C.c_int, [C.c_char_p, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
+    ("knnj_binary_read", C.c_int, [C.c_char_p, _vp, C.c_uint64]),
+]
+
 _LIB = None
 
 

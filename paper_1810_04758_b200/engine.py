@@ -323,3 +323,51 @@ def run_hybrid(X, cfg: RunConfig, device: int = 0) -> KnnRunResult:
         return eng.run(cfg)
     finally:
         eng.close()
+
+
+def tsv_bytes(r: KnnRunResult, threads: int = 0) -> bytes:
+    """io::tsv_string (proj/src/io.cpp:141-154) through the native multi-threaded
+    formatter (knnj_tsv_format): byte-identical to ``tsv_string``."""
+    lib = _capi.load_library()
+    q = np.ascontiguousarray(r.queries, np.uint32)
+    ids = np.ascontiguousarray(r.ids, np.uint32)
+    dist = np.ascontiguousarray(r.dist, np.float64)
+    n = C.c_uint64()
+    k = ids.shape[1] if ids.ndim == 2 else 0
+    args = (q.ctypes.data, ids.ctypes.data, dist.ctypes.data, q.size, k)
+    if lib.knnj_tsv_format(*args, None, 0, C.byref(n), threads):
+        raise KnnjError(1, lib.knnj_io_last_error().decode())
+    buf = C.create_string_buffer(max(1, n.value))
+    if lib.knnj_tsv_format(*args, buf, n.value, C.byref(n), threads):
+        raise KnnjError(1, lib.knnj_io_last_error().decode())
+    return buf.raw[:n.value]
+
+
+def write_tsv(path: str, r: KnnRunResult, threads: int = 0) -> int:
+    """write_tsv (proj/src/io.cpp:137-139), formatted and written in parallel."""
+    lib = _capi.load_library()
+    q = np.ascontiguousarray(r.queries, np.uint32)
+    ids = np.ascontiguousarray(r.ids, np.uint32)
+    dist = np.ascontiguousarray(r.dist, np.float64)
+    k = ids.shape[1] if ids.ndim == 2 else 0
+    n = C.c_uint64()
+    rc = lib.knnj_tsv_write(path.encode(), q.ctypes.data, ids.ctypes.data, dist.ctypes.data,
+                            q.size, k, threads, C.byref(n))
+    if rc:
+        raise KnnjError(rc, lib.knnj_io_last_error().decode())
+    return n.value
+
+
+def read_binary_f64(path: str, out=None) -> np.ndarray:
+    """ingest_binary (proj/src/io.cpp:69-91): |D| x n float64 (into ``out`` if given,
+    e.g. a pinned buffer); IngestError-kind failures carry the reference messages."""
+    lib = _capi.load_library()
+    N, n = C.c_uint64(), C.c_uint64()
+    rc = lib.knnj_binary_header(path.encode(), C.byref(N), C.byref(n))
+    if rc:
+        raise KnnjError(rc, lib.knnj_io_last_error().decode())
+    X = np.empty((N.value, n.value), np.float64) if out is None else out
+    rc = lib.knnj_binary_read(path.encode(), X.ctypes.data, X.size)
+    if rc:
+        raise KnnjError(rc, lib.knnj_io_last_error().decode())
+    return X

@@ -1,0 +1,74 @@
+"""CPU: the host I/O of the engine library (no GPU): the native TSV writer is
+byte-identical to io::tsv_string's "%u\\t%u\\t%.17g" (proj/src/io.cpp:141-154), and
+binary-f64 ingest behaves like ingest_binary (proj/src/io.cpp:69-91)."""
+import os
+
+import numpy as np
+import pytest
+
+from paper_1810_04758_b200 import KnnjError
+from paper_1810_04758_b200.engine import (KnnRunResult, read_binary_f64, tsv_bytes, tsv_string,
+                                          write_tsv)
+
+
+def _result(nq, k, seed):
+    rng = np.random.default_rng(seed)
+    d = np.sort(rng.exponential(1.0, (nq, k)) * 10.0 ** rng.integers(-8, 6, (nq, 1)), axis=1)
+    d[0, :min(k, 6)] = [0.0, 5e-324, 1e-300, 0.1, 1.0 / 3, 2.0 ** 52 + 0.5][:min(k, 6)]
+    ids = rng.integers(0, 2 ** 32 - 1, (nq, k), dtype=np.uint64).astype(np.uint32)
+    q = np.sort(rng.choice(10 ** 6, nq, replace=False)).astype(np.uint32)
+    return KnnRunResult(queries=q, ids=ids, dist=d, provenance=np.zeros(nq, np.uint8),
+                        k_effective=k, info={})
+
+
+@pytest.mark.parametrize("nq,k,threads", [(1, 1, 1), (37, 5, 0), (3000, 32, 3), (200001, 2, 0)])
+def test_tsv_matches_printf(nq, k, threads):
+    r = _result(nq, k, nq + k)
+    want = tsv_string(r).encode()
+    assert tsv_bytes(r, threads) == want
+
+
+def test_tsv_file(tmp_path):
+    r = _result(5000, 7, 3)
+    p = str(tmp_path / "out.tsv")
+    n = write_tsv(p, r, threads=4)
+    data = open(p, "rb").read()
+    assert n == len(data) and data == tsv_string(r).encode()
+
+
+def test_tsv_reference_bytes():
+    """known lines from the reference's %.17g formatting (printf semantics)"""
+    r = KnnRunResult(queries=np.array([3], np.uint32), ids=np.array([[7, 9, 11]], np.uint32),
+                     dist=np.array([[5.0, 3.7416573867739413, 0.1]]), provenance=np.zeros(1, np.uint8),
+                     k_effective=3, info={})
+    assert tsv_bytes(r) == b"3\t7\t5\n3\t9\t3.7416573867739413\n3\t11\t0.10000000000000001\n"
+
+
+def test_binary_roundtrip_and_errors(tmp_path):
+    X = np.random.default_rng(1).standard_normal((123, 5))
+    p = tmp_path / "d.bin"
+    with open(p, "wb") as f:
+        f.write(np.array([123, 5], "<u8").tobytes())
+        f.write(X.astype("<f8").tobytes())
+    assert np.array_equal(read_binary_f64(str(p)), X)
+    bad = X.copy()
+    bad[4, 2] = np.nan
+    with open(p, "wb") as f:
+        f.write(np.array([123, 5], "<u8").tobytes())
+        f.write(bad.astype("<f8").tobytes())
+    with pytest.raises(KnnjError) as e:
+        read_binary_f64(str(p))
+    assert e.value.kind == "IngestError" and "row 5, column 3: non-finite value" in str(e.value)
+    with open(p, "wb") as f:
+        f.write(np.array([123, 5], "<u8").tobytes())
+        f.write(X.astype("<f8").tobytes()[:800])
+    with pytest.raises(KnnjError) as e:
+        read_binary_f64(str(p))
+    assert "body shorter than header promises (123 x 5)" in str(e.value)
+    with open(p, "wb") as f:
+        f.write(bytes(7))
+    with pytest.raises(KnnjError) as e:
+        read_binary_f64(str(p))
+    assert "truncated header" in str(e.value)
+    with pytest.raises(KnnjError):
+        read_binary_f64(str(tmp_path / "missing.bin"))
