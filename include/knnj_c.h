@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define KNNJ_ABI_VERSION 2
+#define KNNJ_ABI_VERSION 3
 
 enum knnj_status {
     KNNJ_OK = 0,
@@ -66,6 +66,7 @@ int knnj_fp32_peak(knnj_ctx* ctx, double* tflops);
 /* Engine knobs (no reference analogue; results never depend on them):
  *   "tensor_cores" 0/1 : allow the tcgen05 distance screen (default 1).
  *   "split_items" 0/1  : split work items with oversized candidate sets across CTAs (1).
+ *   "box_filter" 0/1   : drop candidate blocks provably out of the pass radius (1).
  *   "epi_halves" 0/1   : tcgen05 join with two epilogue warps per TMEM lane quarter (0).
  *   "hist_cap" 0/1/2   : eps-selection histogram counts only the bins select_eps_beta
  *                        needs when the profile is not requested: 0 never, 1 when the
@@ -179,6 +180,7 @@ typedef struct {
     uint32_t hist_bins_counted;   /* bins counted exactly (n_bins unless the histogram was capped) */
     uint64_t n_owned;             /* query rows this call (shard) produced */
     uint64_t join_candidate_pairs;/* candidate pairs of the level-0 join over the owned queries */
+    uint64_t join_screened_pairs; /* of which left after the exact box filter (the work done) */
     /* device-event timings (ms) */
     double ms_upload, ms_reorder, ms_eps_mean, ms_histogram, ms_grid, ms_split, ms_join,
         ms_fallback, ms_download, ms_total;

@@ -68,6 +68,7 @@ RUN_INFO_FIELDS = [
     ("kernel_launches", C.c_uint64), ("join_tensor_cores", C.c_uint32),
     ("hist_tensor_cores", C.c_uint32), ("hist_bins_counted", C.c_uint32),
     ("n_owned", C.c_uint64), ("join_candidate_pairs", C.c_uint64),
+    ("join_screened_pairs", C.c_uint64),
 ] + [(f, C.c_double) for f in (
     "ms_upload", "ms_reorder", "ms_eps_mean", "ms_histogram", "ms_grid", "ms_split", "ms_join",
     "ms_fallback", "ms_download", "ms_total", "ms_join_kernel", "ms_hist_kernel",

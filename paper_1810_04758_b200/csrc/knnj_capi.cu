@@ -898,6 +898,7 @@ struct knnj_ctx {
                                32 + bits_for(nruns ? nruns - 1 : 0), s);
             launch_inverse(lv.J.p, N, lv.posJ.p, s);
         }
+        lv.bbox_ready = false;
         lv.Xs.ensure((uint64_t)n * Npad);
         launch_gather_soa(Xf.p, lv.J.p, N, n, Npad, lv.Xs.p, s);
         lv.tc_ready = false;
@@ -1016,9 +1017,11 @@ struct knnj_ctx {
     // Sharded (nshard > 1): only a contiguous run of work items in cell order is kept
     // (SURVEY.md §8e), cut at equal shares of the estimated tile work; the pass then
     // covers query positions [row_begin, row_begin + nq) of the cell-ordered list.
+    // filter_r2 > 0: candidate blocks provably farther than sqrt(filter_r2) from every
+    // query of their item are dropped (filter_ranges).
     void build_pass(Level& lv, const uint32_t* d_qpid, const uint32_t* d_qrow, uint64_t nq,
                     Pass& P, uint32_t K = 0, uint32_t shard = 0, uint32_t nshard = 1,
-                    const uint8_t* d_dense = nullptr) {
+                    const uint8_t* d_dense = nullptr, double filter_r2 = 0.0) {
         P.nq = nq;
         P.nq_all = nq;
         P.nv = nq;
@@ -1249,6 +1252,51 @@ struct knnj_ctx {
             KJ_CUDA(cudaMemcpyAsync(P.items.p, h_sorted.data(), 16 * P.nitems, cudaMemcpyHostToDevice, s));
         sync();
         P.candidates = cand;
+        P.screened = cand;
+        if (filter_r2 > 0.0 && box_filter && P.nitems) filter_ranges(lv, P, filter_r2);
+    }
+
+    // Box filter of a join pass (after build_pass): a candidate can matter to a query
+    // only within radius r of it (level 0: eps, the dense rule; level L: the cell width
+    // w_L, the coverage certificate), so 128-position blocks whose FP64 bounding box is
+    // farther than r from the item's query box (all n dims, rounded down) are dropped.
+    // Leaves every outcome unchanged; removes e.g. the other Gaussian clusters that
+    // share a cell's 3^m neighbourhood in the first m dims.
+    bool box_filter = true;
+    // The radius a pass may filter to: every decision taken from its lists (in-eps at
+    // level 0, the coverage certificate kth < cover2) concerns pairs within the cell
+    // width w. When the grid is at most 2 cells wide in every dim the certificate is
+    // unconditional (cover2 = inf) and nothing may be dropped.
+    double filter_radius2(const Level& lv) const { return cover2(lv) < kInf ? lv.w * lv.w : 0.0; }
+    void filter_ranges(Level& lv, Pass& P, double r2) {
+        if (!lv.bbox_ready) {
+            lv.bbox.ensure(((N + FB - 1) / FB) * 2 * n);
+            launch_block_boxes(X64.p, lv.J.p, N, n, lv.bbox.p, s);
+            lv.bbox_ready = true;
+        }
+        const double r2c = r2 * (1.0 + 1e-9);  // FP64 scalar sums can fall below the true sq
+        DBuf<uint32_t> cnt, off;
+        cnt.ensure(P.nitems + 1);
+        off.ensure(P.nitems + 1);
+        KJ_CUDA(cudaMemsetAsync(cnt.p + P.nitems, 0, 4, s));
+        launch_filter_ranges(P.items.p, P.nitems, P.qpos.p, lv.J.p, X64.p, n, P.adj.p, lv.bbox.p,
+                             r2c, cnt.p, nullptr, nullptr, nullptr, false, s);
+        exclusive_sum(sc, cnt.p, off.p, P.nitems + 1, s);
+        uint32_t total = 0;
+        KJ_CUDA(cudaMemcpyAsync(&total, off.p + P.nitems, 4, cudaMemcpyDeviceToHost, s));
+        sync();
+        DBuf<uint2> adj2;
+        adj2.ensure(total);
+        d_u64a.ensure(1);
+        KJ_CUDA(cudaMemsetAsync(d_u64a.p, 0, 8, s));
+        launch_filter_ranges(P.items.p, P.nitems, P.qpos.p, lv.J.p, X64.p, n, P.adj.p, lv.bbox.p,
+                             r2c, nullptr, off.p, adj2.p, d_u64a.p, true, s);
+        unsigned long long scr = 0;
+        KJ_CUDA(cudaMemcpyAsync(&scr, d_u64a.p, 8, cudaMemcpyDeviceToHost, s));
+        sync();
+        P.adj.swap(adj2);
+        P.nadj = total;
+        P.screened = scr;
     }
 
     double last_join_kernel_ms = 0.0;
@@ -1475,7 +1523,7 @@ struct knnj_ctx {
             KJ_CUDA(cudaMemcpyAsync(d_cut.p, scut.data(), 4 * np, cudaMemcpyHostToDevice, s));
             launch_scatter_f32(d_r.p, d_cut.p, np, d_cut_by_row.p, s);
             Pass P;
-            build_pass(lv, d_p.p, d_r.p, np, P, K);
+            build_pass(lv, d_p.p, d_r.p, np, P, K, 0, 1, nullptr, filter_radius2(lv));
             trace().mark("levels: build_pass", s);
             launch_gather_f32(P.qrow.p, d_cut_by_row.p, np, d_cut.p, s);
             run_pass(lv, P, K, d_cut.p, -1.0, cov2, out_ids, out_dist, out_kth, out_status, n_slow);
@@ -1637,6 +1685,8 @@ int knnj_set_option(knnj_ctx* c, const char* name, int64_t value) {
         const std::string k = name ? name : "";
         if (k == "tensor_cores") {
             c->tc_enabled = value != 0;
+        } else if (k == "box_filter") {
+            c->box_filter = value != 0;
         } else if (k == "epi_halves") {
             c->epi_halves = value != 0;
         } else if (k == "split_items") {
@@ -2262,7 +2312,7 @@ static void run_impl(knnj_ctx* c, const knnj_config* cfg, uint32_t shard, uint32
             {
                 Timer tb(s);
                 c->build_pass(lv0, d_q.p, d_rows.p, nq, P, k_eff, shard, nshard,
-                              have_dense ? d_dense.p : nullptr);
+                              have_dense ? d_dense.p : nullptr, c->filter_radius2(lv0));
                 I.ms_join_build = tb.ms();
             }
             c->run_pass(lv0, P, k_eff, nullptr, eps * eps, c->cover2(lv0), o_ids.p, o_dist.p,
@@ -2274,6 +2324,7 @@ static void run_impl(knnj_ctx* c, const knnj_config* cfg, uint32_t shard, uint32
             // candidates_examined counts dense queries only (DenseJoinStats)
             I.candidates_examined = have_dense ? P.candidates_dense : P.candidates;
             I.join_candidate_pairs = P.candidates;
+            I.join_screened_pairs = P.screened;
         }
         n_own = P.nq;
         // ---- classify on device; exact fallback for failures and uncertified sparse rows

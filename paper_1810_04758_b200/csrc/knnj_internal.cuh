@@ -94,7 +94,8 @@ struct DBuf {
 // ---------------------------------------------------------------- constants
 constexpr int JB = 128;          // threads (= queries) per join / histogram block
 constexpr uint32_t OVF = 0xFFFFFFFFu;
-constexpr uint32_t SKIP = 0xFFFFFFFEu;  // list count of a row whose item was split into parts
+constexpr uint32_t SKIP = 0xFFFFFFFEu;
+constexpr uint32_t FB = 128;     // positions per candidate block of the box filter  // list count of a row whose item was split into parts
 
 // Status bits written by the finalize kernel, per query.
 enum : uint8_t {
@@ -125,6 +126,8 @@ struct Level {
     bool tc_ready = false;
     uint32_t row_halfs = 0, split = 0;
     DBuf<__half> Bh;     // N x row_halfs: tensor-core B operand (knnj_tc.cu)
+    DBuf<double> bbox;   // ceil(N/FB) x 2n: FP64 boxes of FB-position blocks (J order)
+    bool bbox_ready = false;
 };
 
 // Work description of one join pass (queries of one level grid).
@@ -134,6 +137,7 @@ struct Pass {
     uint64_t nadj = 0;
     uint64_t candidates = 0;  // sum over queries of candidate-set size
     uint64_t candidates_dense = 0;  // the same over dense queries (when flags were given)
+    uint64_t screened = 0;    // candidate pairs left after the box filter (join work)
     uint64_t row_begin = 0;   // first owned position in the cell-ordered query list (shards)
     uint64_t nq_all = 0;      // queries before sharding
     uint32_t chunk = 128;     // queries per work item
@@ -311,6 +315,12 @@ void launch_slow_exact(const double* X64, uint32_t n, const uint32_t* A, const u
                        uint32_t* out_count, cudaStream_t s);
 void launch_scatter_f32(const uint32_t* idx, const float* vals, uint64_t n, float* out,
                         cudaStream_t s);
+void launch_block_boxes(const double* X64, const uint32_t* J, uint64_t N, uint32_t n, double* box,
+                        cudaStream_t s);
+void launch_filter_ranges(uint4* items, uint64_t nitems, const uint32_t* qpos, const uint32_t* J,
+                          const double* X64, uint32_t n, const uint2* adj, const double* box,
+                          double r2, uint32_t* out_cnt, const uint32_t* out_off, uint2* out_adj,
+                          unsigned long long* screened, bool fill, cudaStream_t s);
 void launch_fill_u32(uint32_t* p, uint64_t n, uint32_t v, cudaStream_t s);
 void launch_merge_parts(const uint4* splits, uint64_t nsplits, uint32_t K, const uint32_t* t_ids,
                         const double* t_sq, const uint32_t* t_count, const uint32_t* qrow,

@@ -1484,3 +1484,144 @@ void launch_scatter_f32(const uint32_t* idx, const float* vals, uint64_t n, floa
     g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 }  // namespace kj
+
+namespace kj {
+// ---------------------------------------------------------------- candidate box filter
+// Per 128-position block of a level's join order (J), the FP64 bounding box of its
+// points over all n working dims: lo[n] then hi[n]. One warp per block.
+__global__ void k_block_boxes(const double* X64, const uint32_t* J, uint64_t N, uint32_t n,
+                              double* box) {
+    const uint64_t nblk = (N + FB - 1) / FB;
+    const uint64_t w = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (w >= nblk) return;
+    double* out = box + w * 2 * n;
+    for (uint32_t d = 0; d < n; ++d) {
+        double lo = CUDART_INF, hi = -CUDART_INF;
+        for (uint64_t p = w * FB + lane; p < min(N, (w + 1) * FB); p += 32) {
+            const double v = X64[(uint64_t)J[p] * n + d];
+            lo = fmin(lo, v);
+            hi = fmax(hi, v);
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+            hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+        }
+        if (lane == 0) {
+            out[d] = lo;
+            out[n + d] = hi;
+        }
+    }
+}
+void launch_block_boxes(const double* X64, const uint32_t* J, uint64_t N, uint32_t n, double* box,
+                        cudaStream_t s) {
+    const uint64_t nblk = (N + FB - 1) / FB;
+    if (!nblk) return;
+    k_block_boxes<<<(unsigned)((nblk * 32 + 255) / 256), 256, 0, s>>>(X64, J, N, n, box);
+    KJ_CUDA(cudaGetLastError());
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+
+// Lower bound (rounded down, real arithmetic) of the squared distance between a
+// point of box a and a point of box b.
+__device__ __forceinline__ double box_gap2(const double* alo, const double* ahi, const double* blo,
+                                           const double* bhi, uint32_t n) {
+    double acc = 0.0;
+    for (uint32_t d = 0; d < n; ++d) {
+        const double g = fmax(0.0, fmax(__dsub_rd(blo[d], ahi[d]), __dsub_rd(alo[d], bhi[d])));
+        acc = __dadd_rd(acc, __dmul_rd(g, g));
+    }
+    return acc;
+}
+
+// One warp per work item: the item's query box, then every 128-block of its
+// candidate ranges tested against it; blocks farther than the pass radius from
+// every query are dropped and the survivors re-emitted as merged ranges.
+// COUNT: out_cnt[item] = ranges kept. FILL: ranges written at out_off[item] and the
+// item's (abeg, aend) rewritten.
+template <bool FILL>
+__global__ void k_filter_ranges(uint4* items, uint64_t nitems, const uint32_t* qpos,
+                                const uint32_t* J, const double* X64, uint32_t n, const uint2* adj,
+                                const double* box, double r2, uint32_t* out_cnt,
+                                const uint32_t* out_off, uint2* out_adj,
+                                unsigned long long* screened) {
+    extern __shared__ double s_qbox[];  // per warp: lo[n], hi[n]
+    const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+    const uint64_t item = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    if (item >= nitems) return;
+    double* qlo = s_qbox + (size_t)wl * 2 * n;
+    double* qhi = qlo + n;
+    const uint4 it = items[item];
+    for (uint32_t d = 0; d < n; ++d) {
+        double lo = CUDART_INF, hi = -CUDART_INF;
+        for (uint32_t q = it.x + lane; q < it.y; q += 32) {
+            const double v = X64[(uint64_t)J[qpos[q]] * n + d];
+            lo = fmin(lo, v);
+            hi = fmax(hi, v);
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+            hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+        }
+        if (lane == 0) {
+            qlo[d] = lo;
+            qhi[d] = hi;
+        }
+    }
+    __syncwarp();
+    uint32_t kept = 0;
+    unsigned long long span = 0;  // FILL: candidate positions kept (this lane's ranges)
+    const uint32_t base = FILL ? out_off[item] : 0;
+    for (uint32_t ri = it.z; ri < it.w; ++ri) {
+        const uint2 rg = adj[ri];
+        if (rg.x >= rg.y) continue;
+        const uint32_t b0 = rg.x / FB, b1 = (rg.y - 1) / FB;
+        // 32-block chunks are handled independently: a kept run crossing a chunk
+        // boundary becomes two ranges (both block-aligned, so no extra partial tiles)
+        for (uint32_t c0 = b0; c0 <= b1; c0 += 32) {
+            const uint32_t blk = c0 + lane;
+            bool keep = false;
+            if (blk <= b1) {
+                const double* bb = box + (uint64_t)blk * 2 * n;
+                keep = box_gap2(qlo, qhi, bb, bb + n, n) <= r2;
+            }
+            const unsigned m = __ballot_sync(0xffffffffu, keep);
+            const unsigned starts = m & ~(m << 1);  // first block of each kept run
+            if (FILL && ((starts >> lane) & 1u)) {
+                const unsigned above = lane == 31 ? 0u : ~m & ~((2u << lane) - 1u);
+                const uint32_t e = above ? c0 + (uint32_t)(__ffs(above) - 2) : min(c0 + 31, b1);
+                const uint32_t rank = kept + __popc(starts & ((1u << lane) - 1u));
+                const uint2 o = make_uint2(max(rg.x, blk * FB), min(rg.y, (e + 1) * FB));
+                out_adj[base + rank] = o;
+                span += o.y - o.x;
+            }
+            kept += __popc(starts);
+        }
+    }
+    if (FILL && screened) {
+        for (int o = 16; o > 0; o >>= 1) span += __shfl_xor_sync(0xffffffffu, span, o);
+        if (lane == 0 && span) atomicAdd(screened, span * (unsigned long long)(it.y - it.x));
+    }
+    if (lane == 0) {
+        if (FILL) items[item] = make_uint4(it.x, it.y, base, base + kept);
+        else out_cnt[item] = kept;
+    }
+}
+void launch_filter_ranges(uint4* items, uint64_t nitems, const uint32_t* qpos, const uint32_t* J,
+                          const double* X64, uint32_t n, const uint2* adj, const double* box,
+                          double r2, uint32_t* out_cnt, const uint32_t* out_off, uint2* out_adj,
+                          unsigned long long* screened, bool fill, cudaStream_t s) {
+    if (!nitems) return;
+    const unsigned threads = 128;
+    const size_t sm = (size_t)(threads / 32) * 2 * n * sizeof(double);
+    const unsigned grid = (unsigned)((nitems * 32 + threads - 1) / threads);
+    if (fill)
+        k_filter_ranges<true><<<grid, threads, sm, s>>>(items, nitems, qpos, J, X64, n, adj, box, r2,
+                                                       out_cnt, out_off, out_adj, screened);
+    else
+        k_filter_ranges<false><<<grid, threads, sm, s>>>(items, nitems, qpos, J, X64, n, adj, box,
+                                                        r2, out_cnt, out_off, out_adj, screened);
+    KJ_CUDA(cudaGetLastError());
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+}  // namespace kj

@@ -149,3 +149,27 @@ def test_epilogue_halves_identical(engine, oracle, spec, N, n, k):
     q = np.random.default_rng(5).choice(N, 48, replace=False).astype(np.uint32)
     oi, od = oracle.brute_knn(W, q, k)
     assert np.array_equal(b.ids[q], oi) and np.array_equal(b.dist[q], od)
+
+
+@pytest.mark.parametrize("spec,N,n,k", [("clusters:16:0.05", 30000, 18, 32), ("mixture", 40000, 5, 8),
+                                        ("exponential", 30000, 6, 40), ("mixture:8:0.05", 6000, 90, 16)])
+def test_box_filter_identical(engine, oracle, spec, N, n, k):
+    """Dropping candidate blocks outside the pass radius (eps at level 0, the cell
+    width in the fallback) leaves every output bit unchanged."""
+    X = generate(spec, N, n, 29)
+    cfg = RunConfig(k=k, mode="hybrid", seed=29)
+    out = []
+    for f in (0, 1):
+        engine.set_option("box_filter", f)
+        engine.set_points(X)
+        out.append(engine.run(cfg, want_hist=False))
+    engine.set_option("box_filter", 1)
+    a, b = out
+    assert np.array_equal(a.ids, b.ids) and np.array_equal(a.dist, b.dist)
+    assert np.array_equal(a.provenance, b.provenance)
+    assert a.info["failed_count"] == b.info["failed_count"]
+    assert b.info["join_screened_pairs"] <= b.info["join_candidate_pairs"]
+    W = X[:, b.info["perm"]]
+    q = np.random.default_rng(9).choice(N, 48, replace=False).astype(np.uint32)
+    oi, od = oracle.brute_knn(W, q, k)
+    assert np.array_equal(b.ids[q], oi) and np.array_equal(b.dist[q], od)
