@@ -1269,18 +1269,23 @@ struct knnj_ctx {
     // unconditional (cover2 = inf) and nothing may be dropped.
     double filter_radius2(const Level& lv) const { return cover2(lv) < kInf ? lv.w * lv.w : 0.0; }
     void filter_ranges(Level& lv, Pass& P, double r2) {
+        const uint64_t nblk = (N + FB - 1) / FB;
         if (!lv.bbox_ready) {
-            lv.bbox.ensure(((N + FB - 1) / FB) * 2 * n);
+            lv.bbox.ensure(nblk * 2 * n);
             launch_block_boxes(X64.p, lv.J.p, N, n, lv.bbox.p, s);
             lv.bbox_ready = true;
         }
-        const double r2c = r2 * (1.0 + 1e-9);  // FP64 scalar sums can fall below the true sq
+        // FP64 scalar sums can fall below the true sq: widen, then round up to FP32
+        const float r2c = f32_round_up(r2 * (1.0 + 1e-9));
+        DBuf<float> qbox;
         DBuf<uint32_t> cnt, off;
+        qbox.ensure(P.nitems * 2 * n);
         cnt.ensure(P.nitems + 1);
         off.ensure(P.nitems + 1);
+        launch_item_boxes(P.items.p, P.nitems, P.qpos.p, lv.J.p, X64.p, n, qbox.p, s);
         KJ_CUDA(cudaMemsetAsync(cnt.p + P.nitems, 0, 4, s));
-        launch_filter_ranges(P.items.p, P.nitems, P.qpos.p, lv.J.p, X64.p, n, P.adj.p, lv.bbox.p,
-                             r2c, cnt.p, nullptr, nullptr, nullptr, false, s);
+        launch_filter_ranges(P.items.p, P.nitems, qbox.p, n, P.adj.p, lv.bbox.p, nblk, r2c, cnt.p,
+                             nullptr, nullptr, nullptr, false, s);
         exclusive_sum(sc, cnt.p, off.p, P.nitems + 1, s);
         uint32_t total = 0;
         KJ_CUDA(cudaMemcpyAsync(&total, off.p + P.nitems, 4, cudaMemcpyDeviceToHost, s));
@@ -1289,8 +1294,8 @@ struct knnj_ctx {
         adj2.ensure(total);
         d_u64a.ensure(1);
         KJ_CUDA(cudaMemsetAsync(d_u64a.p, 0, 8, s));
-        launch_filter_ranges(P.items.p, P.nitems, P.qpos.p, lv.J.p, X64.p, n, P.adj.p, lv.bbox.p,
-                             r2c, nullptr, off.p, adj2.p, d_u64a.p, true, s);
+        launch_filter_ranges(P.items.p, P.nitems, qbox.p, n, P.adj.p, lv.bbox.p, nblk, r2c, nullptr,
+                             off.p, adj2.p, d_u64a.p, true, s);
         unsigned long long scr = 0;
         KJ_CUDA(cudaMemcpyAsync(&scr, d_u64a.p, 8, cudaMemcpyDeviceToHost, s));
         sync();

@@ -126,7 +126,7 @@ struct Level {
     bool tc_ready = false;
     uint32_t row_halfs = 0, split = 0;
     DBuf<__half> Bh;     // N x row_halfs: tensor-core B operand (knnj_tc.cu)
-    DBuf<double> bbox;   // ceil(N/FB) x 2n: FP64 boxes of FB-position blocks (J order)
+    DBuf<float> bbox;    // 2n x ceil(N/FB): FP32 boxes (outward) of FB-position blocks (J order)
     bool bbox_ready = false;
 };
 
@@ -315,11 +315,13 @@ void launch_slow_exact(const double* X64, uint32_t n, const uint32_t* A, const u
                        uint32_t* out_count, cudaStream_t s);
 void launch_scatter_f32(const uint32_t* idx, const float* vals, uint64_t n, float* out,
                         cudaStream_t s);
-void launch_block_boxes(const double* X64, const uint32_t* J, uint64_t N, uint32_t n, double* box,
+void launch_block_boxes(const double* X64, const uint32_t* J, uint64_t N, uint32_t n, float* box,
                         cudaStream_t s);
-void launch_filter_ranges(uint4* items, uint64_t nitems, const uint32_t* qpos, const uint32_t* J,
-                          const double* X64, uint32_t n, const uint2* adj, const double* box,
-                          double r2, uint32_t* out_cnt, const uint32_t* out_off, uint2* out_adj,
+void launch_item_boxes(const uint4* items, uint64_t nitems, const uint32_t* qpos, const uint32_t* J,
+                       const double* X64, uint32_t n, float* qbox, cudaStream_t s);
+void launch_filter_ranges(uint4* items, uint64_t nitems, const float* qbox, uint32_t n,
+                          const uint2* adj, const float* box, uint64_t nblk, float r2,
+                          uint32_t* out_cnt, const uint32_t* out_off, uint2* out_adj,
                           unsigned long long* screened, bool fill, cudaStream_t s);
 void launch_fill_u32(uint32_t* p, uint64_t n, uint32_t v, cudaStream_t s);
 void launch_merge_parts(const uint4* splits, uint64_t nsplits, uint32_t K, const uint32_t* t_ids,

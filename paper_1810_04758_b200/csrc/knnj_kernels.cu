@@ -1487,33 +1487,44 @@ void launch_scatter_f32(const uint32_t* idx, const float* vals, uint64_t n, floa
 
 namespace kj {
 // ---------------------------------------------------------------- candidate box filter
-// Per 128-position block of a level's join order (J), the FP64 bounding box of its
-// points over all n working dims: lo[n] then hi[n]. One warp per block.
+// Boxes are FP32, rounded outward from the FP64 coordinates (lo down, hi up), stored
+// dimension-major so a warp testing 32 consecutive blocks reads coalesced rows.
+__device__ __forceinline__ void box_of(const double* X64, const uint32_t* ids_pos, const uint32_t* J,
+                                       uint64_t p0, uint64_t p1, uint32_t n, uint32_t d, int lane,
+                                       float& lo, float& hi) {
+    double l = CUDART_INF, h = -CUDART_INF;
+    for (uint64_t p = p0 + lane; p < p1; p += 32) {
+        const uint32_t pos = ids_pos ? ids_pos[p] : (uint32_t)p;
+        const double v = X64[(uint64_t)J[pos] * n + d];
+        l = fmin(l, v);
+        h = fmax(h, v);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        l = fmin(l, __shfl_xor_sync(0xffffffffu, l, o));
+        h = fmax(h, __shfl_xor_sync(0xffffffffu, h, o));
+    }
+    lo = __double2float_rd(l);
+    hi = __double2float_ru(h);
+}
+
+// Per FB-position block of a level's join order (J): box[d * nblk + b] (lo), then
+// box[(n + d) * nblk + b] (hi). One warp per block.
 __global__ void k_block_boxes(const double* X64, const uint32_t* J, uint64_t N, uint32_t n,
-                              double* box) {
+                              float* box) {
     const uint64_t nblk = (N + FB - 1) / FB;
     const uint64_t w = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (w >= nblk) return;
-    double* out = box + w * 2 * n;
     for (uint32_t d = 0; d < n; ++d) {
-        double lo = CUDART_INF, hi = -CUDART_INF;
-        for (uint64_t p = w * FB + lane; p < min(N, (w + 1) * FB); p += 32) {
-            const double v = X64[(uint64_t)J[p] * n + d];
-            lo = fmin(lo, v);
-            hi = fmax(hi, v);
-        }
-        for (int o = 16; o > 0; o >>= 1) {
-            lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-            hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
-        }
+        float lo, hi;
+        box_of(X64, nullptr, J, w * FB, min(N, (w + 1) * FB), n, d, lane, lo, hi);
         if (lane == 0) {
-            out[d] = lo;
-            out[n + d] = hi;
+            box[(uint64_t)d * nblk + w] = lo;
+            box[(uint64_t)(n + d) * nblk + w] = hi;
         }
     }
 }
-void launch_block_boxes(const double* X64, const uint32_t* J, uint64_t N, uint32_t n, double* box,
+void launch_block_boxes(const double* X64, const uint32_t* J, uint64_t N, uint32_t n, float* box,
                         cudaStream_t s) {
     const uint64_t nblk = (N + FB - 1) / FB;
     if (!nblk) return;
@@ -1522,68 +1533,60 @@ void launch_block_boxes(const double* X64, const uint32_t* J, uint64_t N, uint32
     g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
-// Lower bound (rounded down, real arithmetic) of the squared distance between a
-// point of box a and a point of box b.
-__device__ __forceinline__ double box_gap2(const double* alo, const double* ahi, const double* blo,
-                                           const double* bhi, uint32_t n) {
-    double acc = 0.0;
-    for (uint32_t d = 0; d < n; ++d) {
-        const double g = fmax(0.0, fmax(__dsub_rd(blo[d], ahi[d]), __dsub_rd(alo[d], bhi[d])));
-        acc = __dadd_rd(acc, __dmul_rd(g, g));
-    }
-    return acc;
-}
-
-// One warp per work item: the item's query box, then every 128-block of its
-// candidate ranges tested against it; blocks farther than the pass radius from
-// every query are dropped and the survivors re-emitted as merged ranges.
-// COUNT: out_cnt[item] = ranges kept. FILL: ranges written at out_off[item] and the
-// item's (abeg, aend) rewritten.
-template <bool FILL>
-__global__ void k_filter_ranges(uint4* items, uint64_t nitems, const uint32_t* qpos,
-                                const uint32_t* J, const double* X64, uint32_t n, const uint2* adj,
-                                const double* box, double r2, uint32_t* out_cnt,
-                                const uint32_t* out_off, uint2* out_adj,
-                                unsigned long long* screened) {
-    extern __shared__ double s_qbox[];  // per warp: lo[n], hi[n]
-    const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+// Per work item, the box of its queries (qpos rows [x, y)): qbox[item * 2n + d] lo, [+ n] hi.
+__global__ void k_item_boxes(const uint4* items, uint64_t nitems, const uint32_t* qpos,
+                             const uint32_t* J, const double* X64, uint32_t n, float* qbox) {
     const uint64_t item = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
     if (item >= nitems) return;
-    double* qlo = s_qbox + (size_t)wl * 2 * n;
-    double* qhi = qlo + n;
     const uint4 it = items[item];
     for (uint32_t d = 0; d < n; ++d) {
-        double lo = CUDART_INF, hi = -CUDART_INF;
-        for (uint32_t q = it.x + lane; q < it.y; q += 32) {
-            const double v = X64[(uint64_t)J[qpos[q]] * n + d];
-            lo = fmin(lo, v);
-            hi = fmax(hi, v);
-        }
-        for (int o = 16; o > 0; o >>= 1) {
-            lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-            hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
-        }
+        float lo, hi;
+        box_of(X64, qpos, J, it.x, it.y, n, d, lane, lo, hi);
         if (lane == 0) {
-            qlo[d] = lo;
-            qhi[d] = hi;
+            qbox[item * 2 * n + d] = lo;
+            qbox[item * 2 * n + n + d] = hi;
         }
     }
-    __syncwarp();
+}
+
+// One warp per work item: every FB-block of its candidate ranges is tested against
+// the item's query box (lanes = 32 consecutive blocks); blocks whose squared box gap
+// (rounded down, early exit) exceeds r2 are dropped, the survivors re-emitted as
+// merged ranges. COUNT: out_cnt[item] = ranges kept. FILL: ranges written at
+// out_off[item], (abeg, aend) of the item rewritten, kept pairs summed into screened.
+template <bool FILL>
+__global__ void k_filter_ranges(uint4* items, uint64_t nitems, const float* qbox, uint32_t n,
+                                const uint2* adj, const float* box, uint64_t nblk, float r2,
+                                uint32_t* out_cnt, const uint32_t* out_off, uint2* out_adj,
+                                unsigned long long* screened) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t item = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    if (item >= nitems) return;
+    const uint4 it = items[item];
+    const float* ql = qbox + item * 2 * n;
+    const float* qh = ql + n;
     uint32_t kept = 0;
-    unsigned long long span = 0;  // FILL: candidate positions kept (this lane's ranges)
+    unsigned long long span = 0;
     const uint32_t base = FILL ? out_off[item] : 0;
     for (uint32_t ri = it.z; ri < it.w; ++ri) {
         const uint2 rg = adj[ri];
         if (rg.x >= rg.y) continue;
         const uint32_t b0 = rg.x / FB, b1 = (rg.y - 1) / FB;
-        // 32-block chunks are handled independently: a kept run crossing a chunk
-        // boundary becomes two ranges (both block-aligned, so no extra partial tiles)
+        // 32-block chunks independently: a kept run crossing a chunk boundary becomes two
+        // ranges (block-aligned, so no extra partial tiles in the join)
         for (uint32_t c0 = b0; c0 <= b1; c0 += 32) {
             const uint32_t blk = c0 + lane;
             bool keep = false;
             if (blk <= b1) {
-                const double* bb = box + (uint64_t)blk * 2 * n;
-                keep = box_gap2(qlo, qhi, bb, bb + n, n) <= r2;
+                float acc = 0.f;
+                for (uint32_t d = 0; d < n && acc <= r2; ++d) {
+                    const float lo = __ldg(box + (uint64_t)d * nblk + blk);
+                    const float hi = __ldg(box + (uint64_t)(n + d) * nblk + blk);
+                    const float g = fmaxf(0.f, fmaxf(__fsub_rd(lo, qh[d]), __fsub_rd(ql[d], hi)));
+                    acc = __fadd_rd(acc, __fmul_rd(g, g));
+                }
+                keep = acc <= r2;
             }
             const unsigned m = __ballot_sync(0xffffffffu, keep);
             const unsigned starts = m & ~(m << 1);  // first block of each kept run
@@ -1607,20 +1610,26 @@ __global__ void k_filter_ranges(uint4* items, uint64_t nitems, const uint32_t* q
         else out_cnt[item] = kept;
     }
 }
-void launch_filter_ranges(uint4* items, uint64_t nitems, const uint32_t* qpos, const uint32_t* J,
-                          const double* X64, uint32_t n, const uint2* adj, const double* box,
-                          double r2, uint32_t* out_cnt, const uint32_t* out_off, uint2* out_adj,
+void launch_item_boxes(const uint4* items, uint64_t nitems, const uint32_t* qpos, const uint32_t* J,
+                       const double* X64, uint32_t n, float* qbox, cudaStream_t s) {
+    if (!nitems) return;
+    k_item_boxes<<<(unsigned)((nitems * 32 + 255) / 256), 256, 0, s>>>(items, nitems, qpos, J, X64, n,
+                                                                       qbox);
+    KJ_CUDA(cudaGetLastError());
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+void launch_filter_ranges(uint4* items, uint64_t nitems, const float* qbox, uint32_t n,
+                          const uint2* adj, const float* box, uint64_t nblk, float r2,
+                          uint32_t* out_cnt, const uint32_t* out_off, uint2* out_adj,
                           unsigned long long* screened, bool fill, cudaStream_t s) {
     if (!nitems) return;
-    const unsigned threads = 128;
-    const size_t sm = (size_t)(threads / 32) * 2 * n * sizeof(double);
-    const unsigned grid = (unsigned)((nitems * 32 + threads - 1) / threads);
+    const unsigned grid = (unsigned)((nitems * 32 + 255) / 256);
     if (fill)
-        k_filter_ranges<true><<<grid, threads, sm, s>>>(items, nitems, qpos, J, X64, n, adj, box, r2,
-                                                       out_cnt, out_off, out_adj, screened);
+        k_filter_ranges<true><<<grid, 256, 0, s>>>(items, nitems, qbox, n, adj, box, nblk, r2,
+                                                   out_cnt, out_off, out_adj, screened);
     else
-        k_filter_ranges<false><<<grid, threads, sm, s>>>(items, nitems, qpos, J, X64, n, adj, box,
-                                                        r2, out_cnt, out_off, out_adj, screened);
+        k_filter_ranges<false><<<grid, 256, 0, s>>>(items, nitems, qbox, n, adj, box, nblk, r2,
+                                                    out_cnt, out_off, out_adj, screened);
     KJ_CUDA(cudaGetLastError());
     g_launches.fetch_add(1, std::memory_order_relaxed);
 }
