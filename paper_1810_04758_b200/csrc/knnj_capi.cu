@@ -335,6 +335,7 @@ struct knnj_ctx {
         perm = order;
         working_ready = true;
         bh_id_ready = false;  // FP16 operands derive from the working coordinates
+        hist_order_ready = false;
         mm_lo.clear();
         for (auto& lv : levels) lv.built = false;
     }
@@ -619,18 +620,56 @@ struct knnj_ctx {
     DBuf<__half> Bh_id;
     bool bh_id_ready = false;
     uint32_t bh_id_row = 0;
+    // The histogram's candidate order: all points in Morton order over the first
+    // <= 10 working dims (no grid exists yet), with the tensor-core operand rows and the
+    // FP32 block boxes of that order. Sampled queries are sorted into it, so a work item
+    // (256 queries) is spatially compact and the box filter can drop candidate blocks
+    // beyond the counted radius (eps_mean, or the cap edge when capped).
+    DBuf<uint32_t> hJ, hposJ;
+    DBuf<float> hbox;
+    bool hist_order_ready = false;
+    void ensure_hist_order(uint32_t row_halfs) {
+        if (hist_order_ready && bh_id_ready && bh_id_row == row_halfs) return;
+        const uint32_t md = ensure_morton_box();
+        DBuf<uint32_t> ident, zero, vals;
+        DBuf<uint64_t> keys, skeys;
+        ident.ensure(N);
+        zero.ensure(N);
+        vals.ensure(N);
+        keys.ensure(N);
+        skeys.ensure(N);
+        launch_iota(ident.p, N, s);
+        KJ_CUDA(cudaMemsetAsync(zero.p, 0, 4 * N, s));
+        launch_morton_keys(X64.p, ident.p, zero.p, N, n, md, d_mm.p, d_mm.p + md, keys.p, vals.p, s);
+        hJ.ensure(N);
+        hposJ.ensure(N);
+        sort_pairs_u64_u32(sc, keys.p, skeys.p, vals.p, hJ.p, N, 3 * (int)md, s);
+        launch_inverse(hJ.p, N, hposJ.p, s);
+        Bh_id.ensure(N * row_halfs);
+        launch_prep_tc(X64.p, hJ.p, N, n, d_g.p, 1.0 / tc_S(), row_halfs, tc_split(), Bh_id.p, s);
+        const uint64_t nblk = (N + FB - 1) / FB;
+        hbox.ensure(nblk * 2 * n);
+        launch_block_boxes(X64.p, hJ.p, N, n, hbox.p, s);
+        bh_id_ready = true;
+        bh_id_row = row_halfs;
+        hist_order_ready = true;
+    }
+    uint64_t last_hist_screened = 0, last_hist_pairs = 0;
     void histogram_tc(const uint32_t* d_q, uint64_t nq, double em, uint32_t nb, uint32_t ncount,
                       const std::vector<double>& S_thr, unsigned long long* d_cnt) {
         const uint32_t row_halfs = tc_row_halfs();
-        if (!bh_id_ready || bh_id_row != row_halfs) {
-            DBuf<uint32_t> ident;
-            ident.ensure(N);
-            launch_iota(ident.p, N, s);
-            Bh_id.ensure(N * row_halfs);
-            launch_prep_tc(X64.p, ident.p, N, n, d_g.p, 1.0 / tc_S(), row_halfs, tc_split(),
-                           Bh_id.p, s);
-            bh_id_ready = true;
-            bh_id_row = row_halfs;
+        ensure_hist_order(row_halfs);
+        // sampled queries -> sorted positions in the histogram order
+        DBuf<uint32_t> qp_u, qp;
+        qp_u.ensure(nq);
+        qp.ensure(nq);
+        launch_map_u32(d_q, hposJ.p, nq, qp_u.p, s);
+        {
+            size_t bytes = 0;
+            KJ_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, bytes, qp_u.p, qp.p, (int64_t)nq, 0,
+                                                   bits_for(N), s));
+            KJ_CUDA(cub::DeviceRadixSort::SortKeys(sc.get(bytes), bytes, qp_u.p, qp.p, (int64_t)nq, 0,
+                                                   bits_for(N), s));
         }
         const double Ssc = tc_S(), S2 = Ssc * Ssc;
         const double width = em / double(nb);
@@ -664,12 +703,21 @@ struct knnj_ctx {
         d_adj.ensure(adj.size());
         KJ_CUDA(cudaMemcpyAsync(d_items.p, items.data(), 16 * items.size(), cudaMemcpyHostToDevice, s));
         KJ_CUDA(cudaMemcpyAsync(d_adj.p, adj.data(), 8 * adj.size(), cudaMemcpyHostToDevice, s));
+        // pairs at or beyond the counted radius are never counted: drop their blocks
+        last_hist_pairs = nq * N;
+        last_hist_screened = last_hist_pairs;
+        if (box_filter) {
+            const double r2 = ncount < nb ? S_thr[ncount] : em * em;
+            uint64_t nadj = adj.size();
+            last_hist_screened = filter_items(d_items.p, items.size(), qp.p, hJ.p, hbox.p, d_adj, nadj, r2);
+        }
         TcJoinArgs a{};
         a.Bh = Bh_id.p;
         a.row_halfs = row_halfs;
         a.split = tc_split();
         a.n = n;
-        a.qpos = d_q;
+        a.qpos = qp.p;
+        a.A = hJ.p;
         a.items = d_items.p;
         a.adj = d_adj.p;
         a.K = 1;
@@ -791,6 +839,31 @@ struct knnj_ctx {
     }
     std::vector<double> mm_lo;  // Morton box of the working coords (first <=10 dims)
     DBuf<double> d_mm;
+    uint32_t ensure_morton_box() {
+        const uint32_t md = std::min<uint32_t>(n, 10);
+        if (mm_lo.size() != md) {
+            d_u64a.ensure(64);
+            d_u64b.ensure(64);
+            std::vector<unsigned long long> i0(md, ~0ull), i1(md, 0ull), mn(md), mx(md);
+            KJ_CUDA(cudaMemcpyAsync(d_u64a.p, i0.data(), 8 * md, cudaMemcpyHostToDevice, s));
+            KJ_CUDA(cudaMemcpyAsync(d_u64b.p, i1.data(), 8 * md, cudaMemcpyHostToDevice, s));
+            launch_minmax(X64.p, N, n, md, d_u64a.p, d_u64b.p, s);
+            KJ_CUDA(cudaMemcpyAsync(mn.data(), d_u64a.p, 8 * md, cudaMemcpyDeviceToHost, s));
+            KJ_CUDA(cudaMemcpyAsync(mx.data(), d_u64b.p, 8 * md, cudaMemcpyDeviceToHost, s));
+            sync();
+            mm_lo.resize(md);
+            std::vector<double> inv(md);
+            for (uint32_t j = 0; j < md; ++j) {
+                mm_lo[j] = unorder(mn[j]);
+                const double r = unorder(mx[j]) - mm_lo[j];
+                inv[j] = r > 0 ? 1.0 / r : 0.0;
+            }
+            d_mm.ensure(2 * md);
+            KJ_CUDA(cudaMemcpyAsync(d_mm.p, mm_lo.data(), 8 * md, cudaMemcpyHostToDevice, s));
+            KJ_CUDA(cudaMemcpyAsync(d_mm.p + md, inv.data(), 8 * md, cudaMemcpyHostToDevice, s));
+        }
+        return md;
+    }
     // GridIndex::build (grid_index.cpp:13-75) at cell width w (level 0: w = eps).
     void build_level(int L, uint32_t m, double w) {
         Level& lv = levels[L];
@@ -870,26 +943,7 @@ struct knnj_ctx {
         launch_grid_tables(skeys.p, lv.A.p, runidx.p, N, lv.B.p, lv.G.p, lv.slot.p, lv.posOf.p, s);
         // join order: same cell ranges, Morton order inside each cell
         {
-            const uint32_t md = std::min<uint32_t>(n, 10);
-            if (mm_lo.size() != md) {
-                std::vector<unsigned long long> i0(md, ~0ull), i1(md, 0ull), mn(md), mx(md);
-                KJ_CUDA(cudaMemcpyAsync(d_u64a.p, i0.data(), 8 * md, cudaMemcpyHostToDevice, s));
-                KJ_CUDA(cudaMemcpyAsync(d_u64b.p, i1.data(), 8 * md, cudaMemcpyHostToDevice, s));
-                launch_minmax(X64.p, N, n, md, d_u64a.p, d_u64b.p, s);
-                KJ_CUDA(cudaMemcpyAsync(mn.data(), d_u64a.p, 8 * md, cudaMemcpyDeviceToHost, s));
-                KJ_CUDA(cudaMemcpyAsync(mx.data(), d_u64b.p, 8 * md, cudaMemcpyDeviceToHost, s));
-                sync();
-                mm_lo.resize(md);
-                std::vector<double> inv(md);
-                for (uint32_t j = 0; j < md; ++j) {
-                    mm_lo[j] = unorder(mn[j]);
-                    const double r = unorder(mx[j]) - mm_lo[j];
-                    inv[j] = r > 0 ? 1.0 / r : 0.0;
-                }
-                d_mm.ensure(2 * md);
-                KJ_CUDA(cudaMemcpyAsync(d_mm.p, mm_lo.data(), 8 * md, cudaMemcpyHostToDevice, s));
-                KJ_CUDA(cudaMemcpyAsync(d_mm.p + md, inv.data(), 8 * md, cudaMemcpyHostToDevice, s));
-            }
+            const uint32_t md = ensure_morton_box();
             launch_morton_keys(X64.p, lv.A.p, lv.slot.p, N, n, md, d_mm.p, d_mm.p + md, keys.p,
                                vals.p, s);
             lv.J.ensure(N);
@@ -1269,39 +1323,45 @@ struct knnj_ctx {
     // unconditional (cover2 = inf) and nothing may be dropped.
     double filter_radius2(const Level& lv) const { return cover2(lv) < kInf ? lv.w * lv.w : 0.0; }
     void filter_ranges(Level& lv, Pass& P, double r2) {
-        const uint64_t nblk = (N + FB - 1) / FB;
         if (!lv.bbox_ready) {
-            lv.bbox.ensure(nblk * 2 * n);
+            lv.bbox.ensure(((N + FB - 1) / FB) * 2 * n);
             launch_block_boxes(X64.p, lv.J.p, N, n, lv.bbox.p, s);
             lv.bbox_ready = true;
         }
+        P.screened = filter_items(P.items.p, P.nitems, P.qpos.p, lv.J.p, lv.bbox.p, P.adj, P.nadj, r2);
+    }
+    // items (qbeg, qend, abeg, aend) over adjacency ranges adj: keep only the blocks within
+    // sqrt(r2) of the item's query box; adj is replaced. Returns the kept candidate pairs.
+    uint64_t filter_items(uint4* items, uint64_t nitems, const uint32_t* qpos, const uint32_t* J,
+                          const float* bbox, DBuf<uint2>& adj, uint64_t& nadj, double r2) {
+        const uint64_t nblk = (N + FB - 1) / FB;
         // FP64 scalar sums can fall below the true sq: widen, then round up to FP32
         const float r2c = f32_round_up(r2 * (1.0 + 1e-9));
         DBuf<float> qbox;
         DBuf<uint32_t> cnt, off;
-        qbox.ensure(P.nitems * 2 * n);
-        cnt.ensure(P.nitems + 1);
-        off.ensure(P.nitems + 1);
-        launch_item_boxes(P.items.p, P.nitems, P.qpos.p, lv.J.p, X64.p, n, qbox.p, s);
-        KJ_CUDA(cudaMemsetAsync(cnt.p + P.nitems, 0, 4, s));
-        launch_filter_ranges(P.items.p, P.nitems, qbox.p, n, P.adj.p, lv.bbox.p, nblk, r2c, cnt.p,
-                             nullptr, nullptr, nullptr, false, s);
-        exclusive_sum(sc, cnt.p, off.p, P.nitems + 1, s);
+        qbox.ensure(nitems * 2 * n);
+        cnt.ensure(nitems + 1);
+        off.ensure(nitems + 1);
+        launch_item_boxes(items, nitems, qpos, J, X64.p, n, qbox.p, s);
+        KJ_CUDA(cudaMemsetAsync(cnt.p + nitems, 0, 4, s));
+        launch_filter_ranges(items, nitems, qbox.p, n, adj.p, bbox, nblk, r2c, cnt.p, nullptr,
+                             nullptr, nullptr, false, s);
+        exclusive_sum(sc, cnt.p, off.p, nitems + 1, s);
         uint32_t total = 0;
-        KJ_CUDA(cudaMemcpyAsync(&total, off.p + P.nitems, 4, cudaMemcpyDeviceToHost, s));
+        KJ_CUDA(cudaMemcpyAsync(&total, off.p + nitems, 4, cudaMemcpyDeviceToHost, s));
         sync();
         DBuf<uint2> adj2;
         adj2.ensure(total);
         d_u64a.ensure(1);
         KJ_CUDA(cudaMemsetAsync(d_u64a.p, 0, 8, s));
-        launch_filter_ranges(P.items.p, P.nitems, qbox.p, n, P.adj.p, lv.bbox.p, nblk, r2c, nullptr,
-                             off.p, adj2.p, d_u64a.p, true, s);
+        launch_filter_ranges(items, nitems, qbox.p, n, adj.p, bbox, nblk, r2c, nullptr, off.p,
+                             adj2.p, d_u64a.p, true, s);
         unsigned long long scr = 0;
         KJ_CUDA(cudaMemcpyAsync(&scr, d_u64a.p, 8, cudaMemcpyDeviceToHost, s));
         sync();
-        P.adj.swap(adj2);
-        P.nadj = total;
-        P.screened = scr;
+        adj.swap(adj2);
+        nadj = total;
+        return scr;
     }
 
     double last_join_kernel_ms = 0.0;
@@ -1727,6 +1787,7 @@ int knnj_set_points(knnj_ctx* c, const double* X, uint64_t N, uint32_t n) {
         c->n = n;
         c->have_points = c->working_ready = false;
         c->bh_id_ready = false;
+        c->hist_order_ready = false;
         for (auto& lv : c->levels) lv.built = false;
         c->X0.ensure(N * n);
         KJ_CUDA(cudaMemcpyAsync(c->X0.p, X, N * n * 8, cudaMemcpyHostToDevice, c->s));

@@ -190,6 +190,7 @@ struct TcJoinArgs {
     const float* tables;     // LO[n_bins+1], HI[n_bins+1] in scaled units
     float inv_width_scaled;  // S / bin_width
     const double* X64;
+    const uint32_t* A;       // HIST: candidate/query position -> point id (null: identity)
     double eps_mean, limit_sq, inv_width;
     unsigned long long* counts;
 };

@@ -627,9 +627,11 @@ __global__ void __launch_bounds__(64 + 128 * G * H, 1)
             if (lane < qn) {
                 const uint2 pr = qbuf[lane];  // (query column, candidate position)
                 const uint32_t qcol = pr.x & 0xFFFFu;
-                const uint32_t qid = p.qpos[it.x + qcol];
+                const uint32_t qps = p.qpos[it.x + qcol];
+                const uint32_t qid = p.A ? p.A[qps] : qps;   // positions -> point ids
+                const uint32_t cid = p.A ? p.A[pr.y] : pr.y;
                 const uint32_t bb =
-                    exact_bin(p.X64, p.n, qid, pr.y, p.eps_mean, p.limit_sq, p.inv_width, nbins);
+                    exact_bin(p.X64, p.n, qid, cid, p.eps_mean, p.limit_sq, p.inv_width, nbins);
                 if (bb < ncount) atomicAdd(&hist[bb * NQ + qcol], 1u);
             }
             __syncwarp();
