@@ -971,6 +971,9 @@ struct knnj_ctx {
     // tcgen05 join: 16 epilogue warps on 64-column halves (n <= 20). Off by default: on C2
     // it measured 689 ms vs 647 ms for the 8-warp epilogue.
     bool epi_halves = false;
+    // tcgen05 join (n <= 20): 64-candidate tiles, 4 early-released buffers. Off: 646 ms vs
+    // 540 ms for 128-candidate tiles on C2.
+    bool tile64 = false;
     uint32_t tc_split() const { return 3 * n + 2 <= 128 ? 3 : 0; }
     uint32_t tc_row_halfs() const { return tc_split() * n + 2 <= 64 ? 64 : 128; }
     bool use_tc() const { return tc_enabled && tc_split() != 0; }
@@ -1040,6 +1043,7 @@ struct knnj_ctx {
             c.L = std::min<uint32_t>(L0, 128);
         }
         if (epi_halves && KB == 1) c.sh = TcShape{1, 2, 8, 2};  // two epilogue warps per quarter
+        else if (tile64 && KB == 1) c.sh = TcShape{1, 2, 8, 1, 64};  // 64-col tiles, early release
         c.ok = K + 8 <= c.L && tc_smem_bytes(c.sh, c.L, 0, false) <= 227 * 1024;
         return c;
     }
@@ -1752,6 +1756,8 @@ int knnj_set_option(knnj_ctx* c, const char* name, int64_t value) {
             c->tc_enabled = value != 0;
         } else if (k == "box_filter") {
             c->box_filter = value != 0;
+        } else if (k == "tile64") {
+            c->tile64 = value != 0;
         } else if (k == "epi_halves") {
             c->epi_halves = value != 0;
         } else if (k == "split_items") {

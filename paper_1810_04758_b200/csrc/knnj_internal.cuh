@@ -244,7 +244,8 @@ void launch_inverse(const uint32_t* J, uint64_t N, uint32_t* posJ, cudaStream_t 
 // G groups of 128 queries per CTA, STAGES candidate tiles in flight
 struct TcShape {
     int KB, G, STAGES;
-    int H = 1;  // epilogue warps per lane quarter and group (2: split 64-column halves)
+    int H = 1;    // epilogue warps per lane quarter and group (2: split 64-column halves)
+    int TN = 128; // candidates per tile (64: four early-released accumulator buffers)
 };
 size_t tc_smem_bytes(const TcShape& sh, uint32_t L, uint32_t n_bins, bool hist);
 void launch_hist_tc(const TcJoinArgs& a, const TcShape& sh, uint64_t nitems, uint64_t N,

@@ -80,15 +80,19 @@ __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
 }
 
 // kind::f16: A=F16, B=F16, D=F32, both K-major, M=128, N=128
-constexpr uint32_t IDESC = (1u << 4) | (0u << 7) | (0u << 10) | ((uint32_t)(TC_N >> 3) << 17) |
-                           ((uint32_t)(TC_M >> 4) << 24);
+template <int TN>
+constexpr uint32_t idesc_f16() {
+    return (1u << 4) | (0u << 7) | (0u << 10) | ((uint32_t)(TN >> 3) << 17) |
+           ((uint32_t)(TC_M >> 4) << 24);
+}
 
+template <int TN>
 __device__ __forceinline__ void umma_f16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t acc) {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "setp.ne.b32 p, %4, 0;\n\t"
         "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-        "l"(da), "l"(db), "r"(IDESC), "r"(acc));
+        "l"(da), "l"(db), "r"(idesc_f16<TN>()), "r"(acc));
 }
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -128,6 +132,21 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
     for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// v[j] for a warp-uniform runtime j without local memory (5-level select tree):
+// the early-release epilogue's rare path, which can no longer re-read TMEM.
+__device__ __forceinline__ float sel32(const float (&v)[32], uint32_t j) {
+    float a[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) a[i] = (j & 16u) ? v[i + 16] : v[i];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) a[i] = (j & 8u) ? a[i + 8] : a[i];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) a[i] = (j & 4u) ? a[i + 4] : a[i];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) a[i] = (j & 2u) ? a[i + 2] : a[i];
+    return (j & 1u) ? a[1] : a[0];
 }
 
 __device__ __forceinline__ float tmem_ld1(uint32_t taddr) {
@@ -247,24 +266,30 @@ __device__ __noinline__ uint32_t exact_bin(const double* X64, uint32_t n, uint32
 // screening one 64-column half of every tile with its own near-tie list (global
 // memory) and a cut shared with its partner through shared memory: twice the
 // epilogue warps to hide the per-slab latency chain.
-template <int KB, int G, int STAGES, bool HIST, int LR, int H = 1>
+// TN = 64 with ER (JOIN, G = 2): 64-candidate tiles in NB = 4 accumulator buffers,
+// each released right after tcgen05.ld, so the MMAs of later tiles overlap the
+// screening of this one (the buffer is no longer held for the screening time).
+template <int KB, int G, int STAGES, bool HIST, int LR, int H = 1, int TN = 128, bool ER = false>
 __global__ void __launch_bounds__(64 + 128 * G * H, 1)
     k_tc(const __grid_constant__ CUtensorMap tmB, TcJoinArgs p) {
+    static_assert(!ER || (TN == 64 && H == 1 && !HIST), "early release: 64-column JOIN tiles");
     constexpr int NQ = 128 * G;                    // queries per block
+    constexpr int BK = TN * 128;                   // bytes of one k-block of a candidate tile
+    constexpr int NB = (G == 2 ? 512 : 256) / (G * TN);  // accumulator buffers per group
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     // 1024-byte alignment for the 128B-swizzle atoms, staying in the shared state space
     unsigned char* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     unsigned char* sA = base;                                   // G x KB x 16 KB
-    unsigned char* sB = sA + G * KB * KB_BYTES;                 // STAGES x KB x 16 KB
-    unsigned char* tail = sB + STAGES * KB * KB_BYTES;
-    __shared__ uint64_t bar_full[STAGES], bar_empty[STAGES], bar_accf[2], bar_acce[2];
+    unsigned char* sB = sA + G * KB * KB_BYTES;                 // STAGES x KB x BK
+    unsigned char* tail = sB + STAGES * KB * BK;
+    __shared__ uint64_t bar_full[STAGES], bar_empty[STAGES], bar_accf[NB], bar_acce[NB];
     __shared__ uint32_t s_tmem;
     __shared__ float s_cut[H == 2 ? 2 * NQ : 1];  // H=2: per (half, query) current cut
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint4 it = p.items[blockIdx.x];
     const uint32_t nq = it.y - it.x;
-    constexpr uint32_t TMEM_COLS = G == 1 ? 256 : 512;
+    constexpr uint32_t TMEM_COLS = G * NB * TN;
 
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -277,7 +302,7 @@ __global__ void __launch_bounds__(64 + 128 * G * H, 1)
             mbar_init(&bar_full[i], 1);
             mbar_init(&bar_empty[i], 1);
         }
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < NB; ++i) {
             mbar_init(&bar_accf[i], 1);
             mbar_init(&bar_acce[i], 4 * G * H);
         }
@@ -363,7 +388,7 @@ __global__ void __launch_bounds__(64 + 128 * G * H, 1)
     if (!HIST && it.z < it.w) {
         const uint2 rg0 = p.adj[it.z];
         const uint32_t q0pos = p.qpos[it.x];
-        if (q0pos >= rg0.x && q0pos < rg0.y) first_start = ((q0pos - rg0.x) / TC_N) * TC_N;
+        if (q0pos >= rg0.x && q0pos < rg0.y) first_start = ((q0pos - rg0.x) / TN) * TN;
     }
     auto next_tile = [&](uint32_t& s, uint32_t& c) -> bool {
         if (cur_ri == it.z && cur_ri < it.w) {  // first range: [first_start, len) then [0, first_start)
@@ -373,7 +398,7 @@ __global__ void __launch_bounds__(64 + 128 * G * H, 1)
                 const uint32_t off = (first_start + first_done) % len;
                 const uint32_t seg_end = off >= first_start ? len : first_start;
                 s = rg.x + off;
-                c = min((uint32_t)TC_N, seg_end - off);
+                c = min((uint32_t)TN, seg_end - off);
                 first_done += c;
                 return true;
             }
@@ -385,7 +410,7 @@ __global__ void __launch_bounds__(64 + 128 * G * H, 1)
             const uint32_t len = rg.y - rg.x;
             if (cur_off < len) {
                 s = rg.x + cur_off;
-                c = min((uint32_t)TC_N, len - cur_off);
+                c = min((uint32_t)TN, len - cur_off);
                 cur_off += c;
                 if (cur_off == len) {
                     ++cur_ri;
@@ -406,11 +431,10 @@ __global__ void __launch_bounds__(64 + 128 * G * H, 1)
             for (uint32_t t = 0; next_tile(s, c); ++t) {
                 const int st = t % STAGES;
                 mbar_wait(&bar_empty[st], ((t / STAGES) & 1) ^ 1);
-                mbar_expect_tx(&bar_full[st], KB * KB_BYTES);
+                mbar_expect_tx(&bar_full[st], KB * BK);
 #pragma unroll
                 for (int kb = 0; kb < KB; ++kb)
-                    tma_load_2d(sB + (st * KB + kb) * KB_BYTES, &tmB, &bar_full[st], kb * KBLK,
-                                (int)s);
+                    tma_load_2d(sB + (st * KB + kb) * BK, &tmB, &bar_full[st], kb * KBLK, (int)s);
             }
         }
     } else if (warp == 1) {
@@ -419,22 +443,22 @@ __global__ void __launch_bounds__(64 + 128 * G * H, 1)
             uint32_t s, c;
             const uint32_t a0 = smem_u32(sA);
             for (uint32_t t = 0; next_tile(s, c); ++t) {
-                const int st = t % STAGES, b = t & 1;
+                const int st = t % STAGES, b = t % NB;
                 mbar_wait(&bar_full[st], (t / STAGES) & 1);
-                mbar_wait(&bar_acce[b], ((t >> 1) & 1) ^ 1);
+                mbar_wait(&bar_acce[b], ((t / NB) & 1) ^ 1);
                 fence_after();
-                const uint32_t b0 = smem_u32(sB + st * KB * KB_BYTES);
+                const uint32_t b0 = smem_u32(sB + st * KB * BK);
 #pragma unroll
                 for (int gg = 0; gg < G; ++gg) {
-                    const uint32_t dcol = tmem + (gg * 2 + b) * TC_N;
+                    const uint32_t dcol = tmem + (gg * NB + b) * TN;
 #pragma unroll
                     for (int kb = 0; kb < KB; ++kb)
 #pragma unroll
                         for (int kk = 0; kk < KBLK / 16; ++kk)
-                            umma_f16(dcol,
-                                     umma_desc_sw128(a0 + (gg * KB + kb) * KB_BYTES + kk * 32),
-                                     umma_desc_sw128(b0 + kb * KB_BYTES + kk * 32),
-                                     (kb | kk) ? 1u : 0u);
+                            umma_f16<TN>(dcol,
+                                         umma_desc_sw128(a0 + (gg * KB + kb) * KB_BYTES + kk * 32),
+                                         umma_desc_sw128(b0 + kb * BK + kk * 32),
+                                         (kb | kk) ? 1u : 0u);
                 }
                 umma_commit(&bar_empty[st]);
                 umma_commit(&bar_accf[b]);
@@ -519,10 +543,10 @@ __global__ void __launch_bounds__(64 + 128 * G * H, 1)
         };
         uint32_t s, c;
         for (uint32_t t = 0; next_tile(s, c); ++t) {
-            const int b = t & 1;
-            mbar_wait(&bar_accf[b], (t >> 1) & 1);
+            const int b = t % NB;
+            mbar_wait(&bar_accf[b], (t / NB) & 1);
             fence_after();
-            const uint32_t tbase = tmem + ((uint32_t)(quarter * 32) << 16) + (g * 2 + b) * TC_N;
+            const uint32_t tbase = tmem + ((uint32_t)(quarter * 32) << 16) + (g * NB + b) * TN;
             if (H == 2 && has_q && !ovf) {  // the partner's tighter cut applies to new inserts
                 const float pc = *(volatile float*)pcut;
                 if (pc < cut) {
@@ -533,6 +557,11 @@ __global__ void __launch_bounds__(64 + 128 * G * H, 1)
             for (uint32_t j0 = H == 2 ? hh * 64 : 0; j0 < c; j0 += H == 2 ? 128 : 64) {
                 float v0[32], v1[32];
                 tmem_ld64(tbase + j0, v0, v1);
+                if (ER) {  // the whole (64-column) tile is in registers: free the buffer
+                    fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&bar_acce[b]);
+                }
                 if (p.dbg && blockIdx.x == 0 && t == 0 && g == 0)
 #pragma unroll
                     for (int j = 0; j < 32; ++j) {
@@ -577,7 +606,8 @@ __global__ void __launch_bounds__(64 + 128 * G * H, 1)
                     while (um) {
                         const int j = __ffs(um) - 1;
                         um &= um - 1;
-                        const float x = tmem_ld1(tbase + j0 + h * 32 + j);
+                        const float x = ER ? (h == 0 ? sel32(v0, (uint32_t)j) : sel32(v1, (uint32_t)j))
+                                           : tmem_ld1(tbase + j0 + h * 32 + j);
                         const uint32_t pos = s + j0 + h * 32 + j;
                         bool want = ((mk[h] >> j) & 1u) && x <= rhs && pos != qp;
                         // make room: cooperative compaction of every full buffer that needs it
@@ -596,9 +626,11 @@ __global__ void __launch_bounds__(64 + 128 * G * H, 1)
                     }
                 }
             }
-            fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&bar_acce[b]);
+            if (!ER) {
+                fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&bar_acce[b]);
+            }
         }
         if (has_q) {
             if (H == 2) {
@@ -648,10 +680,10 @@ __global__ void __launch_bounds__(64 + 128 * G * H, 1)
         };
         uint32_t s, c;
         for (uint32_t t = 0; next_tile(s, c); ++t) {
-            const int b = t & 1;
-            mbar_wait(&bar_accf[b], (t >> 1) & 1);
+            const int b = t % NB;
+            mbar_wait(&bar_accf[b], (t / NB) & 1);
             fence_after();
-            const uint32_t tbase = tmem + ((uint32_t)(quarter * 32) << 16) + (g * 2 + b) * TC_N;
+            const uint32_t tbase = tmem + ((uint32_t)(quarter * 32) << 16) + (g * NB + b) * TN;
             for (uint32_t j0 = 0; j0 < c; j0 += 64) {
                 float v[2][32];
                 tmem_ld64(tbase + j0, v[0], v[1]);
@@ -779,7 +811,7 @@ __global__ void __launch_bounds__(64 + 128 * G * H, 1)
 // ---------------------------------------------------------------- host side
 size_t tc_smem_bytes(const TcShape& sh, uint32_t L, uint32_t n_bins, bool hist) {
     const size_t NQ = 128 * sh.G;
-    size_t b = 1024 + (size_t)(sh.G + sh.STAGES) * sh.KB * KB_BYTES;
+    size_t b = 1024 + (size_t)sh.G * sh.KB * KB_BYTES + (size_t)sh.STAGES * sh.KB * sh.TN * 128;
     if (hist) b += NQ * n_bins * 4 + 8 * (n_bins + 1) + 8 * n_bins + 8 + (size_t)4 * sh.G * 32 * 8;
     else if (sh.H == 1) b += NQ * L * 8;  // H = 2 keeps the lists in global memory
     return b;
@@ -806,27 +838,27 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
     return fn;
 }
 
-template <int KB, int G, int STAGES, bool HIST, int LR, int H = 1>
+template <int KB, int G, int STAGES, bool HIST, int LR, int H = 1, int TN = 128, bool ER = false>
 static void launch_tc_t(const TcJoinArgs& a, uint64_t nitems, uint64_t N, cudaStream_t s) {
     CUtensorMap map;
     cuuint64_t dims[2] = {(cuuint64_t)a.row_halfs, (cuuint64_t)N};
     cuuint64_t strides[1] = {(cuuint64_t)a.row_halfs * 2};
-    cuuint32_t box[2] = {KBLK, TC_N};
+    cuuint32_t box[2] = {KBLK, (cuuint32_t)TN};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = get_encode()(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, (void*)a.Bh, dims, strides,
                               box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                               CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw Error(9, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
-    const size_t sm = tc_smem_bytes(TcShape{KB, G, STAGES, H}, a.L, a.n_bins, HIST);
+    const size_t sm = tc_smem_bytes(TcShape{KB, G, STAGES, H, TN}, a.L, a.n_bins, HIST);
     if (sm > 227 * 1024) throw Error(1, "tensor-core kernel needs too much shared memory");
-    KJ_CUDA(cudaFuncSetAttribute(k_tc<KB, G, STAGES, HIST, LR, H>,
+    KJ_CUDA(cudaFuncSetAttribute(k_tc<KB, G, STAGES, HIST, LR, H, TN, ER>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     for (uint64_t off = 0; off < nitems; off += 2147483647ull) {
         const uint64_t cnt = std::min<uint64_t>(nitems - off, 2147483647ull);
         TcJoinArgs b = a;
         b.items = a.items + off;
-        k_tc<KB, G, STAGES, HIST, LR, H><<<(unsigned)cnt, 64 + 128 * G * H, sm, s>>>(map, b);
+        k_tc<KB, G, STAGES, HIST, LR, H, TN, ER><<<(unsigned)cnt, 64 + 128 * G * H, sm, s>>>(map, b);
     }
     KJ_CUDA(cudaGetLastError());
     g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -836,6 +868,12 @@ void launch_join_tc(const TcJoinArgs& a, const TcShape& sh, uint64_t nitems, uin
                     cudaStream_t s) {
     if (!nitems) return;
     const bool wide = a.L > 64;  // list compaction over 128 entries
+    if (sh.TN == 64) {
+        if (sh.KB == 1 && sh.G == 2 && sh.STAGES == 8 && !wide) launch_tc_t<1, 2, 8, false, 2, 1, 64, true>(a, nitems, N, s);
+        else if (sh.KB == 1 && sh.G == 2 && sh.STAGES == 8 && wide) launch_tc_t<1, 2, 8, false, 4, 1, 64, true>(a, nitems, N, s);
+        else throw Error(1, "no 64-column tensor-core join instance for this shape");
+        return;
+    }
     if (sh.H == 2) {
         if (sh.KB == 1 && sh.G == 2 && sh.STAGES == 8 && !wide) launch_tc_t<1, 2, 8, false, 2, 2>(a, nitems, N, s);
         else if (sh.KB == 1 && sh.G == 2 && sh.STAGES == 8 && wide) launch_tc_t<1, 2, 8, false, 4, 2>(a, nitems, N, s);

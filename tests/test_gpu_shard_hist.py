@@ -173,3 +173,25 @@ def test_box_filter_identical(engine, oracle, spec, N, n, k):
     q = np.random.default_rng(9).choice(N, 48, replace=False).astype(np.uint32)
     oi, od = oracle.brute_knn(W, q, k)
     assert np.array_equal(b.ids[q], oi) and np.array_equal(b.dist[q], od)
+
+
+@pytest.mark.parametrize("spec,N,n,k", [("clusters:16:0.05", 20000, 18, 32), ("uniform", 30000, 12, 20),
+                                        ("mixture:4:0.05", 15000, 16, 50)])
+def test_tile64_identical(engine, oracle, spec, N, n, k):
+    """64-candidate tiles with early-released accumulators (sel32 rare path) give
+    exactly the 128-candidate kernel's output."""
+    X = generate(spec, N, n, 31)
+    cfg = RunConfig(k=k, mode="hybrid", seed=31)
+    out = []
+    for t64 in (0, 1):
+        engine.set_option("tile64", t64)
+        engine.set_points(X)
+        out.append(engine.run(cfg, want_hist=False))
+    engine.set_option("tile64", 1)
+    a, b = out
+    assert np.array_equal(a.ids, b.ids) and np.array_equal(a.dist, b.dist)
+    assert np.array_equal(a.provenance, b.provenance)
+    W = X[:, b.info["perm"]]
+    q = np.random.default_rng(8).choice(N, 48, replace=False).astype(np.uint32)
+    oi, od = oracle.brute_knn(W, q, k)
+    assert np.array_equal(b.ids[q], oi) and np.array_equal(b.dist[q], od)
