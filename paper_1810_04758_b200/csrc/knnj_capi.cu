@@ -1086,7 +1086,7 @@ struct knnj_ctx {
         P.nsplits = 0;
         P.row_begin = 0;
         P.candidates_dense = 0;
-        const uint32_t chunk = K ? pass_chunk(lv, K) : (uint32_t)JB;
+        uint32_t chunk = K ? pass_chunk(lv, K) : (uint32_t)JB;
         P.chunk = chunk;
         P.nitems = P.nadj = P.candidates = 0;
         if (!nq) return;
@@ -1119,6 +1119,15 @@ struct knnj_ctx {
         std::vector<uint32_t> h_cnt(nuc);
         KJ_CUDA(cudaMemcpyAsync(h_cnt.data(), ucnt.p, 4 * nuc, cudaMemcpyDeviceToHost, s));
         sync();
+        // SIMT level-0 join over sparse cells (few queries per cell): 32-query items on
+        // 32-thread blocks instead of mostly idle 128-thread ones. (Not in the fallback
+        // levels: few queries against huge neighbourhoods are tile-load bound there, and
+        // 128 threads load a tile 4x faster; measured on C4.)
+        if (chunk == (uint32_t)JB && K && &lv == &levels[0] &&
+            double(nq) / double(std::max<uint64_t>(nuc, 1)) < 48.0) {
+            chunk = 32;
+            P.chunk = 32;
+        }
         std::vector<uint32_t> h_ioff(nuc + 1);
         uint64_t tot = 0;
         for (uint64_t u = 0; u < nuc; ++u) {
@@ -1378,13 +1387,15 @@ struct knnj_ctx {
         if (!P.nq) return;
         const TcJoinCfg tcc = tc_join_cfg(K, lv.w);
         const bool tc = tcc.ok && P.chunk == 128u * tcc.sh.G;
-        if (!tc && P.chunk != (uint32_t)JB) throw Error(9, "pass built for a different kernel");
+        if (!tc && P.chunk != (uint32_t)JB && P.chunk != 32u)
+            throw Error(9, "pass built for a different kernel");
         // list capacity: K plus slack for near-ties inside the screen band (overflow -> exact slow path)
         const uint32_t L = tc ? tcc.L : K + std::max<uint32_t>(16, K / 2);
         if (L > 256) throw Error(1, "k above 170 is not supported by the device join");
         const int np = pick_np(n);
         if (np < 0) throw Error(1, "dimension count above 128 is not supported by the device join");
-        if (join_smem_bytes(np, L) > 227 * 1024) throw Error(1, "k too large for the device join");
+        if (!tc && join_smem_bytes(np, L, P.chunk) > 227 * 1024)
+            throw Error(1, "k too large for the device join");
         const uint64_t nv = P.nv, nvv = P.nv - P.nq;  // launch rows; virtual (split-part) rows
         const uint32_t hv = (tc && tcc.sh.H == 2) ? 2u : 1u;  // lists per row
         DBuf<uint32_t>& cnt = pass_cnt;
@@ -1445,7 +1456,7 @@ struct knnj_ctx {
             a.out_pos = pos.p;
             screen_consts(a.gam, a.erg, a.eab, a.e64);
             Timer t(s);
-            launch_join(a, P.nitems, s);
+            launch_join(a, P.nitems, P.chunk, s);
             last_join_kernel_ms = t.ms();
             last_join_tc = false;
         }

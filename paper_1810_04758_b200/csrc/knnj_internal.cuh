@@ -256,8 +256,8 @@ void launch_join_tc(const TcJoinArgs& a, const TcShape& sh, uint64_t nitems, uin
                     cudaStream_t s);
 void launch_scale_f32(const float* in, uint64_t n, float scale, float* out, cudaStream_t s);
 int pick_np(uint32_t n);  // padded dimension count used by the templated kernels
-size_t join_smem_bytes(int np, uint32_t L);
-void launch_join(const JoinArgs& a, uint64_t nitems, cudaStream_t s);
+size_t join_smem_bytes(int np, uint32_t L, uint32_t qb);
+void launch_join(const JoinArgs& a, uint64_t nitems, uint32_t qb, cudaStream_t s);
 void launch_finalize(const FinalArgs& a, cudaStream_t s);
 size_t hist_smem_bytes(int np, uint32_t n_bins);
 void launch_histogram(const HistArgs& a, uint64_t n_slabs, cudaStream_t s);

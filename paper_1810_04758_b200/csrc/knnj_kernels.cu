@@ -74,22 +74,22 @@ __device__ __forceinline__ float screen_delta(float A, float B, float gam, float
 }
 
 // ---------------------------------------------------------------- join kernel
-// One block = one work item: up to JB queries of ONE grid cell (one query per
+// One block = one work item: up to QB (128, or 32 for sparse cells) queries of ONE grid cell (one query per
 // thread) against the candidate position ranges of that cell's 3^m
 // neighbourhood (merged along the last indexed dim). Candidate tiles of T
 // points are staged SoA in shared memory (cp.async, double-buffered), centred
 // at the block origin, and scored against every query of the block. Per query
 // a list of all candidates that can still belong to the exact top-K is kept
 // (sorted by key, capacity L), pruned with cut = key_K + 2*delta_max.
-template <int NP, int T>
-__global__ void __launch_bounds__(JB) k_join(JoinArgs p) {
+template <int NP, int T, int QB>
+__global__ void __launch_bounds__(QB) k_join(JoinArgs p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     float* tile = reinterpret_cast<float*>(smem_raw);          // [2][NP][T]
     float* nbuf = tile + 2 * NP * T;                            // [2][T]
     uint32_t* tpos = reinterpret_cast<uint32_t*>(nbuf + 2 * T); // [2][T]
     float* cen = reinterpret_cast<float*>(tpos + 2 * T);        // [NP] (+pad)
-    float* lkey = cen + ((NP + 3) & ~3);                        // [L][JB]
-    uint32_t* lpos = reinterpret_cast<uint32_t*>(lkey + p.L * JB);
+    float* lkey = cen + ((NP + 3) & ~3);                        // [L][QB]
+    uint32_t* lpos = reinterpret_cast<uint32_t*>(lkey + p.L * QB);
 
     __shared__ uint32_t s_ri, s_off, s_cnt[2];
     __shared__ unsigned s_bmax[2];
@@ -104,12 +104,12 @@ __global__ void __launch_bounds__(JB) k_join(JoinArgs p) {
     const uint64_t Npad = p.Npad;
 
     // zero padded dims of both tile buffers once; block origin = first query
-    for (int i = tid; i < 2 * (NP - (int)n) * T; i += JB) {
+    for (int i = tid; i < 2 * (NP - (int)n) * T; i += QB) {
         int b = i / ((NP - n) * T), r = i % ((NP - n) * T);
         tile[(b * NP + n) * T + r] = 0.f;
     }
     const uint32_t q0 = p.qpos[it.x];
-    for (int d = tid; d < NP; d += JB) cen[d] = d < (int)n ? p.Xs[(uint64_t)d * Npad + q0] : 0.f;
+    for (int d = tid; d < NP; d += QB) cen[d] = d < (int)n ? p.Xs[(uint64_t)d * Npad + q0] : 0.f;
     if (tid == 0) {
         s_ri = it.z;
         s_off = 0;
@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(JB) k_join(JoinArgs p) {
     };
     auto issue = [&](int b) {
         const uint32_t c = s_cnt[b];
-        for (uint32_t i = tid; i < n * (uint32_t)T; i += JB) {
+        for (uint32_t i = tid; i < n * (uint32_t)T; i += QB) {
             uint32_t d = i / T, j = i % T;
             float* dst = &tile[(b * NP + d) * T + j];
             uint32_t pj = tpos[b * T + j];
@@ -183,7 +183,7 @@ __global__ void __launch_bounds__(JB) k_join(JoinArgs p) {
         cp_wait<1>();
         __syncthreads();
         // centre candidates, norms, tile max norm
-        for (int j = tid; j < T; j += JB) {
+        for (int j = tid; j < T; j += QB) {
             float nb = CUDART_NAN_F;
             if ((uint32_t)j < c) {
                 nb = 0.f;
@@ -207,7 +207,7 @@ __global__ void __launch_bounds__(JB) k_join(JoinArgs p) {
             const float Bt = sqrtf(__uint_as_float(s_bmax[buf])) * 1.0001f;
             const float dl = screen_delta(Aq, Bt, p.gam, p.erg, p.eab, p.e64);
             dmax = fmaxf(dmax, dl);
-            if (cnt >= (int)p.K) cut_list = __fadd_ru(lkey[(p.K - 1) * JB + tid], 2.f * dmax);
+            if (cnt >= (int)p.K) cut_list = __fadd_ru(lkey[(p.K - 1) * QB + tid], 2.f * dmax);
             float cut = fminf(cut_list, __fadd_ru(init_cut, dl));
             float rhs = __fsub_ru(cut, na);
             const float* tb = tile + buf * NP * T;
@@ -241,20 +241,20 @@ __global__ void __launch_bounds__(JB) k_join(JoinArgs p) {
                         }
                         int q = cnt;
                         while (q > 0) {
-                            float kq = lkey[(q - 1) * JB + tid];
+                            float kq = lkey[(q - 1) * QB + tid];
                             if (kq <= key) break;
-                            lkey[q * JB + tid] = kq;
-                            lpos[q * JB + tid] = lpos[(q - 1) * JB + tid];
+                            lkey[q * QB + tid] = kq;
+                            lpos[q * QB + tid] = lpos[(q - 1) * QB + tid];
                             --q;
                         }
-                        lkey[q * JB + tid] = key;
-                        lpos[q * JB + tid] = pos;
+                        lkey[q * QB + tid] = key;
+                        lpos[q * QB + tid] = pos;
                         ++cnt;
                         if (cnt >= (int)p.K) {
-                            cut_list = __fadd_ru(lkey[(p.K - 1) * JB + tid], 2.f * dmax);
+                            cut_list = __fadd_ru(lkey[(p.K - 1) * QB + tid], 2.f * dmax);
                             const float ci = __fadd_ru(init_cut, dmax);
                             const float ce = fminf(cut_list, ci);
-                            while (cnt > (int)p.K && lkey[(cnt - 1) * JB + tid] > ce) --cnt;
+                            while (cnt > (int)p.K && lkey[(cnt - 1) * QB + tid] > ce) --cnt;
                             cut = fminf(cut_list, __fadd_ru(init_cut, dl));
                             rhs = __fsub_ru(cut, na);
                         }
@@ -269,7 +269,7 @@ __global__ void __launch_bounds__(JB) k_join(JoinArgs p) {
     if (has_q) {
         p.out_cnt[row] = ovf ? OVF : (uint32_t)cnt;
         if (!ovf)
-            for (int i = 0; i < cnt; ++i) p.out_pos[(uint64_t)row * p.L + i] = lpos[i * JB + tid];
+            for (int i = 0; i < cnt; ++i) p.out_pos[(uint64_t)row * p.L + i] = lpos[i * QB + tid];
     }
 }
 
@@ -517,33 +517,36 @@ int pick_np(uint32_t n) {
 }
 static int tile_for(int np) { return np <= 32 ? 128 : 64; }
 
-size_t join_smem_bytes(int np, uint32_t L) {
+size_t join_smem_bytes(int np, uint32_t L, uint32_t qb) {
     int T = tile_for(np);
     return sizeof(float) * (2 * np * T + 2 * T) + sizeof(uint32_t) * 2 * T +
-           sizeof(float) * ((np + 3) & ~3) + (sizeof(float) + sizeof(uint32_t)) * L * JB;
+           sizeof(float) * ((np + 3) & ~3) + (sizeof(float) + sizeof(uint32_t)) * L * qb;
 }
 
-template <int NP>
+template <int NP, int QB>
 static void launch_join_np(const JoinArgs& a, uint64_t nitems, cudaStream_t s) {
     constexpr int T = NP <= 32 ? 128 : 64;
-    size_t sm = join_smem_bytes(NP, a.L);
-    set_smem(k_join<NP, T>, sm);
+    size_t sm = join_smem_bytes(NP, a.L, QB);
+    set_smem(k_join<NP, T, QB>, sm);
     for (uint64_t off = 0; off < nitems; off += 2147483647ull) {
         uint64_t cnt = std::min<uint64_t>(nitems - off, 2147483647ull);
         JoinArgs b = a;
         b.items = a.items + off;
-        k_join<NP, T><<<dim3((unsigned)cnt), JB, sm, s>>>(b);
+        k_join<NP, T, QB><<<dim3((unsigned)cnt), QB, sm, s>>>(b);
     }
     KJ_CUDA(cudaGetLastError());
     g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
-void launch_join(const JoinArgs& a, uint64_t nitems, cudaStream_t s) {
+void launch_join(const JoinArgs& a, uint64_t nitems, uint32_t qb, cudaStream_t s) {
     if (nitems == 0) return;
     int np = pick_np(a.n);
     switch (np) {
 #define X(v) \
-    case v: launch_join_np<v>(a, nitems, s); break;
+    case v:                                                         \
+        if (qb == 32) launch_join_np<v, 32>(a, nitems, s);          \
+        else launch_join_np<v, JB>(a, nitems, s);                   \
+        break;
         KJ_NP_LIST(X)
 #undef X
         default: throw Error(1, "dimension count above 128 is not supported by the device join");
