@@ -34,6 +34,7 @@
 #include "knnjoin/dataset.hpp"
 #include "knnjoin/errors.hpp"
 #include "knnjoin/orchestrator.hpp"
+#include "knnjoin/util.hpp"
 
 namespace knnjoin_b200 {
 
@@ -151,7 +152,7 @@ inline knnjoin::KnnRunResult run_hybrid(Engine& eng, const knnjoin::Dataset& d,
         p.bin_width = info->bin_width;
         p.sample_fraction = cfg.hist_query_fraction;
         p.query_count = info->hist_query_count;
-        p.seed = cfg.seed;
+        p.seed = knnjoin::derive_seed(cfg.seed, knnjoin::kSeedHistogram);  // the histogram sub-stream
         p.counts.resize(cfg.n_bins);
         p.cumulative.resize(cfg.n_bins);
         uint64_t run = 0;

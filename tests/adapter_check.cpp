@@ -12,6 +12,7 @@
 
 #include "knnj_knnjoin_adapter.hpp"
 #include "knnjoin/io.hpp"
+#include "knnjoin/report.hpp"
 #include "knnjoin/kernels.hpp"
 #include "knnjoin/synthetic.hpp"
 
@@ -51,9 +52,30 @@ int main() {
         const bool prov = ref.provenance == got.provenance;
         const bool meta = ref.eps_used == got.eps_used && ref.failed_count == got.failed_count &&
                           ref.k_effective == got.k_effective && ref.m_used == got.m_used;
-        const bool ok = tsv && prov && meta;
-        std::printf("%s %s |D|=%zu n=%zu k=%zu mode=%s tsv=%d prov=%d meta=%d\n", ok ? "ok " : "BAD",
-                    c.spec, c.size, c.dims, c.k, knnjoin::to_string(c.mode), tsv, prov, meta);
+        // ε-profile text (epsilon.cpp:149-164) and the run report's deterministic view
+        // (report.cpp:18-134). The reference's batch plan and worker round-robin are
+        // CPU-engine artefacts with no device analogue: dropped before comparing.
+        const bool prof = (!ref.profile && !got.profile) ||
+                          (ref.profile && got.profile && ref.profile->to_text() == got.profile->to_text());
+        auto view = [&](const knnjoin::KnnRunResult& r) {
+            auto j = knnjoin::deterministic_view(knnjoin::make_run_report(d, cfg, r));
+            if (j.contains("dense")) {
+                j["dense"].erase("n_batches");
+                j["dense"].erase("estimate_e");
+                j["dense"].erase("batch_pair_counts");
+            }
+            j.erase("sparse");
+            return j.dump();
+        };
+        const bool rep = view(ref) == view(got);
+        const bool ok = tsv && prov && meta && prof && rep;
+        std::printf("%s %s |D|=%zu n=%zu k=%zu mode=%s tsv=%d prov=%d meta=%d profile=%d report=%d\n",
+                    ok ? "ok " : "BAD", c.spec, c.size, c.dims, c.k, knnjoin::to_string(c.mode), tsv,
+                    prov, meta, prof, rep);
+        if (!rep) std::printf("  ref: %s\n  got: %s\n", view(ref).c_str(), view(got).c_str());
+        if (!prof && ref.profile && got.profile)
+            std::printf("  ref profile:\n%.400s\n  got profile:\n%.400s\n", ref.profile->to_text().c_str(),
+                        got.profile->to_text().c_str());
         bad += !ok;
         ++n;
     }
