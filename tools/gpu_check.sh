@@ -18,7 +18,7 @@ if [ -z "$SKIP_NCU" ]; then
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
    python bench.py --steps 1 --warmup 0 --no-cpu-baseline ${NCU_BENCH_ARGS:-} > gpurun_out/ncu_launch_run.log 2>&1
 timeout 1200 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
-   -k "regex:${NCU_KERNEL:-k_tc.*bool.0}" -c 1 \
+   -k "regex:${NCU_KERNEL:-k_tc<.int.1, .int.2, .int.4, .bool.0}" -c 1 \
    -o gpurun_out/prof -f python bench.py --steps 1 --warmup 0 --no-cpu-baseline ${NCU_BENCH_ARGS:-} > gpurun_out/ncu_full.log 2>&1
 fi
 echo done
