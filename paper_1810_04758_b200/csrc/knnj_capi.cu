@@ -586,7 +586,7 @@ struct knnj_ctx {
         a.inv_width = inv_width;
         a.counts = d_cnt.p;
         screen_consts(a.gam, a.erg, a.eab, a.e64);
-        if (use_tc() && tc_smem_bytes(tc_hist_shape(), 0, nb, true) <= 227 * 1024) {
+        if (use_tc_hist() && tc_smem_bytes(tc_hist_shape(), 0, nb, true) <= 227 * 1024) {
             histogram_tc(d_q.p, nq, em, nb, ncount, S, d_cnt.p);
             last_hist_tc = true;
             std::vector<unsigned long long> c(nb);
@@ -974,9 +974,12 @@ struct knnj_ctx {
     // tcgen05 join (n <= 20): 64-candidate tiles, 4 early-released buffers. Off: 646 ms vs
     // 540 ms for 128-candidate tiles on C2.
     bool tile64 = false;
-    uint32_t tc_split() const { return 3 * n + 2 <= 128 ? 3 : 0; }
-    uint32_t tc_row_halfs() const { return tc_split() * n + 2 <= 64 ? 64 : 128; }
+    uint32_t tc_split() const { return 3 * n + 2 <= 320 ? 3 : 0; }
+    // operand row = KB 128-byte k-blocks of 64 halfs (KB <= 5: n <= 106)
+    uint32_t tc_row_halfs() const { return 64u * ((tc_split() * n + 2 + 63) / 64); }
     bool use_tc() const { return tc_enabled && tc_split() != 0; }
+    // the histogram's tensor-core instances cover one or two k-blocks (n <= 42)
+    bool use_tc_hist() const { return use_tc() && tc_row_halfs() <= 128; }
     double tc_S() const {
         double S = 1.0;
         while (S < Rg) S *= 2.0;
@@ -1035,7 +1038,11 @@ struct knnj_ctx {
         if (!use_tc() || K < 1 || !tc_precise_for(w)) return c;
         const uint32_t KB = tc_row_halfs() / 64;
         const uint32_t L0 = K + (tc_split() == 3 ? 24u : 48u);
-        if (L0 <= 64) {
+        if (KB >= 3) {
+            // wide operands (43 <= n <= 106): 64-candidate tiles keep A + B stages in smem
+            c.sh = TcShape{(int)KB, 1, KB == 5 ? 2 : 3, 1, 64};
+            c.L = std::min<uint32_t>(L0, 64);
+        } else if (L0 <= 64) {
             c.sh = KB == 1 ? TcShape{1, 2, 4} : TcShape{2, 1, 3};
             c.L = L0;
         } else {

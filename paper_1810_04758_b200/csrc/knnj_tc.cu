@@ -868,6 +868,13 @@ void launch_join_tc(const TcJoinArgs& a, const TcShape& sh, uint64_t nitems, uin
                     cudaStream_t s) {
     if (!nitems) return;
     const bool wide = a.L > 64;  // list compaction over 128 entries
+    if (sh.TN == 64 && sh.KB >= 3) {  // wide operands, 64-candidate tiles (no early release)
+        if (sh.KB == 3 && sh.G == 1 && sh.STAGES == 3 && !wide) launch_tc_t<3, 1, 3, false, 2, 1, 64, false>(a, nitems, N, s);
+        else if (sh.KB == 4 && sh.G == 1 && sh.STAGES == 3 && !wide) launch_tc_t<4, 1, 3, false, 2, 1, 64, false>(a, nitems, N, s);
+        else if (sh.KB == 5 && sh.G == 1 && sh.STAGES == 2 && !wide) launch_tc_t<5, 1, 2, false, 2, 1, 64, false>(a, nitems, N, s);
+        else throw Error(1, "no wide-operand tensor-core join instance for this shape");
+        return;
+    }
     if (sh.TN == 64) {
         if (sh.KB == 1 && sh.G == 2 && sh.STAGES == 8 && !wide) launch_tc_t<1, 2, 8, false, 2, 1, 64, true>(a, nitems, N, s);
         else if (sh.KB == 1 && sh.G == 2 && sh.STAGES == 8 && wide) launch_tc_t<1, 2, 8, false, 4, 1, 64, true>(a, nitems, N, s);
