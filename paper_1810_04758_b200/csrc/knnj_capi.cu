@@ -18,6 +18,7 @@
 #include <numeric>
 #include <random>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include <cub/cub.cuh>
@@ -431,69 +432,63 @@ struct knnj_ctx {
     }
 
     // ------------------------------------------------------------ eps_mean
-    // The sampled index pairs depend only on (|D|, pair count, seed): drawn once with
-    // the reference RNG and kept on the device, so repeated runs (and every shard of
-    // a multi-GPU run after its first) skip the ~15 ms host draw.
-    struct PairSample {
-        uint64_t N = 0, pairs = 0, seed = 0, used = 0;
-        DBuf<uint64_t> d_ij;
-    } eps_pairs;
+    // estimate_eps_mean (epsilon.cpp:14-44) in two halves: the index pairs are drawn on
+    // the host with the reference RNG (draw_pairs, a pure function of |D|, the pair
+    // count and the seed, so knnj_run draws them on a host thread while the GPU does the
+    // reorder and the histogram's candidate order), then evaluated on the device and
+    // summed sequentially in sample order (bit-identical to the reference).
+    static std::vector<uint64_t> draw_pairs(uint64_t N, uint64_t sample_pairs, uint64_t seed) {
+        const uint64_t all = N * (N - 1);
+        std::vector<uint64_t> ij;
+        if (sample_pairs >= all) {  // exhaustive sweep
+            ij.reserve(2 * all);
+            for (uint64_t i = 0; i < N; ++i)
+                for (uint64_t j = 0; j < N; ++j)
+                    if (i != j) {
+                        ij.push_back(i);
+                        ij.push_back(j);
+                    }
+            return ij;
+        }
+        ij.resize(2 * sample_pairs);
+        std::mt19937_64 rng(seed);
+        std::uniform_int_distribution<uint64_t> pick(0, N - 1);
+        for (uint64_t p = 0; p < sample_pairs; ++p) {
+            uint64_t i = pick(rng);
+            uint64_t j = pick(rng);
+            while (j == i) j = pick(rng);
+            ij[2 * p] = i;
+            ij[2 * p + 1] = j;
+        }
+        return ij;
+    }
     double* h_sq = nullptr;  // pinned staging for the per-pair distances
     uint64_t h_sq_cap = 0;
-    double eps_mean(uint64_t sample_pairs, uint64_t seed) {
-        if (N < 2) throw Error(1, "eps_mean estimation needs at least two points");
-        if (sample_pairs < 1) throw Error(1, "sample_pairs must be at least 1");
-        PairSample& ps = eps_pairs;
-        if (!(ps.N == N && ps.pairs == sample_pairs && ps.seed == seed && ps.used)) {
-            const uint64_t all = N * (N - 1);
-            std::vector<uint64_t> ij;
-            uint64_t used;
-            if (sample_pairs >= all) {  // exhaustive sweep (epsilon.cpp:14-44)
-                ij.reserve(2 * all);
-                for (uint64_t i = 0; i < N; ++i)
-                    for (uint64_t j = 0; j < N; ++j)
-                        if (i != j) {
-                            ij.push_back(i);
-                            ij.push_back(j);
-                        }
-                used = all;
-            } else {
-                ij.resize(2 * sample_pairs);
-                std::mt19937_64 rng(seed);
-                std::uniform_int_distribution<uint64_t> pick(0, N - 1);
-                for (uint64_t p = 0; p < sample_pairs; ++p) {
-                    uint64_t i = pick(rng);
-                    uint64_t j = pick(rng);
-                    while (j == i) j = pick(rng);
-                    ij[2 * p] = i;
-                    ij[2 * p + 1] = j;
-                }
-                used = sample_pairs;
-            }
-            ps.d_ij.ensure(2 * used);
-            KJ_CUDA(cudaMemcpyAsync(ps.d_ij.p, ij.data(), 16 * used, cudaMemcpyHostToDevice, s));
-            sync();
-            ps.N = N;
-            ps.pairs = sample_pairs;
-            ps.seed = seed;
-            ps.used = used;
-        }
-        const uint64_t used = ps.used;
+    double eps_mean_of(const std::vector<uint64_t>& ij) {
+        const uint64_t used = ij.size() / 2;
+        if (!used) throw Error(1, "sample_pairs must be at least 1");
         if (h_sq_cap < used) {
             if (h_sq) cudaFreeHost(h_sq);
             h_sq = nullptr;
             KJ_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&h_sq), 8 * used, cudaHostAllocDefault));
             h_sq_cap = used;
         }
+        DBuf<uint64_t> d_ij;
         DBuf<double> d_out;
+        d_ij.ensure(2 * used);
         d_out.ensure(used);
-        launch_pair_sq(X64.p, n, ps.d_ij.p, used, kInf, d_out.p, s);
+        KJ_CUDA(cudaMemcpyAsync(d_ij.p, ij.data(), 16 * used, cudaMemcpyHostToDevice, s));
+        launch_pair_sq(X64.p, n, d_ij.p, used, kInf, d_out.p, s);
         KJ_CUDA(cudaMemcpyAsync(h_sq, d_out.p, 8 * used, cudaMemcpyDeviceToHost, s));
         sync();
-        // sequential FP64 sum in sample order, as the reference (bit-identical)
         double sum = 0.0;
         for (uint64_t p = 0; p < used; ++p) sum += std::sqrt(h_sq[p]);
         return sum / double(used);
+    }
+    double eps_mean(uint64_t sample_pairs, uint64_t seed) {
+        if (N < 2) throw Error(1, "eps_mean estimation needs at least two points");
+        if (sample_pairs < 1) throw Error(1, "sample_pairs must be at least 1");
+        return eps_mean_of(draw_pairs(N, sample_pairs, seed));
     }
 
     std::vector<double> pair_sq(const uint64_t* ij, uint64_t np, double limit) {
@@ -807,27 +802,20 @@ struct knnj_ctx {
         return nb;
     }
 
-    // sample_without_replacement depends only on (|D|, count, seed): cached like eps_pairs
-    struct QuerySample {
-        uint64_t N = 0, want = 0, seed = 0;
-        bool valid = false;
-        std::vector<uint64_t> ids;
-    } hist_sample;
-    std::vector<uint64_t> histogram_sample(double frac, uint64_t seed) {
+    // build_distance_histogram's query sample (epsilon.cpp:46-60, util.hpp:70-92)
+    static uint64_t histogram_sample_size(uint64_t N, double frac) {
         if (!(frac > 0.0) || frac > 1.0) throw Error(1, "query_fraction must be in (0, 1]");
         uint64_t want = (uint64_t)std::floor(frac * double(N));
         want = std::max<uint64_t>(want, 100);
-        want = std::min<uint64_t>(want, N);
-        QuerySample& qs = hist_sample;
-        if (!(qs.valid && qs.N == N && qs.want == want && qs.seed == seed)) {
-            std::mt19937_64 rng(seed);
-            qs.ids = sample_without_replacement(N, want, rng);
-            qs.N = N;
-            qs.want = want;
-            qs.seed = seed;
-            qs.valid = true;
-        }
-        return qs.ids;
+        return std::min<uint64_t>(want, N);
+    }
+    static std::vector<uint64_t> draw_histogram_sample(uint64_t N, double frac, uint64_t seed) {
+        const uint64_t want = histogram_sample_size(N, frac);
+        std::mt19937_64 rng(seed);
+        return sample_without_replacement(N, want, rng);
+    }
+    std::vector<uint64_t> histogram_sample(double frac, uint64_t seed) {
+        return draw_histogram_sample(N, frac, seed);
     }
 
     // ------------------------------------------------------------ grid levels
@@ -953,8 +941,7 @@ struct knnj_ctx {
             launch_inverse(lv.J.p, N, lv.posJ.p, s);
         }
         lv.bbox_ready = false;
-        lv.Xs.ensure((uint64_t)n * Npad);
-        launch_gather_soa(Xf.p, lv.J.p, N, n, Npad, lv.Xs.p, s);
+        lv.xs_ready = false;  // the SIMT join's FP32 SoA copy is built on first use
         lv.tc_ready = false;
         if (use_tc()) prep_tc(lv);
         sync();
@@ -1450,6 +1437,11 @@ struct knnj_ctx {
             last_join_tc = true;
         } else {
             JoinArgs a{};
+            if (!lv.xs_ready) {
+                lv.Xs.ensure((uint64_t)n * Npad);
+                launch_gather_soa(Xf.p, lv.J.p, N, n, Npad, lv.Xs.p, s);
+                lv.xs_ready = true;
+            }
             a.Xs = lv.Xs.p;
             a.Npad = Npad;
             a.n = n;
@@ -2193,6 +2185,26 @@ static void run_impl(knnj_ctx* c, const knnj_config* cfg, uint32_t shard, uint32
 
     Timer t_all(s);
     const unsigned long long launches0 = g_launches.load();
+    // host-side reference RNG streams (pairs for eps_mean, the histogram's query sample)
+    // drawn on a helper thread while the GPU reorders and orders the candidates
+    const bool sampling = cfg->mode == KNNJ_HYBRID || cfg->mode == KNNJ_DENSE_ONLY;
+    std::vector<uint64_t> eps_ij, hist_q;
+    std::thread drawer;
+    if (sampling && N >= 2) {
+        knnj_ctx::histogram_sample_size(N, cfg->hist_query_fraction);  // validates the fraction here
+        drawer = std::thread([&] {
+            eps_ij = knnj_ctx::draw_pairs(N, std::min<uint64_t>(10 * N, cfg->eps_mean_pair_cap),
+                                          derive_seed(cfg->seed, 1));
+            hist_q = knnj_ctx::draw_histogram_sample(N, cfg->hist_query_fraction,
+                                                     derive_seed(cfg->seed, 2));
+        });
+    }
+    struct Joiner {
+        std::thread& t;
+        ~Joiner() {
+            if (t.joinable()) t.join();
+        }
+    } joiner{drawer};
     {
         Timer t(s);
         c->reorder(m);
@@ -2284,8 +2296,10 @@ static void run_impl(knnj_ctx* c, const knnj_config* cfg, uint32_t shard, uint32
         // ---- epsilon selection (orchestrator.cpp:137-165)
         {
             Timer t(s);
-            const uint64_t budget = std::min<uint64_t>(10 * N, cfg->eps_mean_pair_cap);
-            I.eps_mean = c->eps_mean(budget, derive_seed(cfg->seed, 1));
+            if (N < 2) throw Error(1, "eps_mean estimation needs at least two points");
+            if (c->use_tc_hist()) c->ensure_hist_order(c->tc_row_halfs());  // overlaps the draw
+            if (drawer.joinable()) drawer.join();
+            I.eps_mean = c->eps_mean_of(eps_ij);
             I.ms_eps_mean = t.ms();
             trace().mark("run: eps_mean");
         }
@@ -2295,7 +2309,7 @@ static void run_impl(knnj_ctx* c, const knnj_config* cfg, uint32_t shard, uint32
         uint32_t valid = cfg->n_bins;
         {
             Timer t(s);
-            auto hq = c->histogram_sample(cfg->hist_query_fraction, derive_seed(cfg->seed, 2));
+            auto& hq = hist_q;
             I.hist_query_count = hq.size();
             valid = c->hist_for_selection(hq, shard, nshard, I.eps_mean, cfg->n_bins, target_beta,
                                           raw_hist != nullptr, reduce, raw.data());

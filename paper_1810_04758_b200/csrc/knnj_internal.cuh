@@ -122,7 +122,8 @@ struct Level {
     DBuf<uint32_t> posOf;// N: point id -> sorted position
     DBuf<uint32_t> J;    // N: join-order position -> point id (cells contiguous, Morton inside)
     DBuf<uint32_t> posJ; // N: point id -> join-order position
-    DBuf<float> Xs;      // n x Npad SoA, sorted order, centred floats
+    DBuf<float> Xs;      // n x Npad SoA, sorted order, centred floats (SIMT join; lazy)
+    bool xs_ready = false;
     bool tc_ready = false;
     uint32_t row_halfs = 0, split = 0;
     DBuf<__half> Bh;     // N x row_halfs: tensor-core B operand (knnj_tc.cu)
