@@ -275,7 +275,7 @@ struct knnj_ctx {
     DBuf<float> Xf;           // SoA id order
     DBuf<double> d_g;
 
-    Level levels[40];
+    Level levels[44];  // 0..39: eps * 2^L; 40..43: the fine cascade (eps * fine_f[i])
     double eps0 = 0.0;
     uint32_t m0 = 0;
 
@@ -625,7 +625,7 @@ struct knnj_ctx {
     bool hist_order_ready = false;
     void ensure_hist_order(uint32_t row_halfs) {
         if (hist_order_ready && bh_id_ready && bh_id_row == row_halfs) return;
-        const uint32_t md = ensure_morton_box();
+        const uint32_t md = std::min<uint32_t>(ensure_morton_box(), 21);  // 3 bits per dim in 64
         DBuf<uint32_t> ident, zero, vals;
         DBuf<uint64_t> keys, skeys;
         ident.ensure(N);
@@ -828,7 +828,7 @@ struct knnj_ctx {
     std::vector<double> mm_lo;  // Morton box of the working coords (first <=10 dims)
     DBuf<double> d_mm;
     uint32_t ensure_morton_box() {
-        const uint32_t md = std::min<uint32_t>(n, 10);
+        const uint32_t md = std::min<uint32_t>(n, morton_dims);
         if (mm_lo.size() != md) {
             d_u64a.ensure(64);
             d_u64b.ensure(64);
@@ -932,12 +932,14 @@ struct knnj_ctx {
         // join order: same cell ranges, Morton order inside each cell
         {
             const uint32_t md = ensure_morton_box();
+            const uint32_t sb = bits_for(nruns ? nruns - 1 : 0);
+            // code bits per dim: as many as the 64-bit key leaves next to the cell slot
+            const uint32_t mb = std::max<uint32_t>(1, std::min<uint32_t>(morton_bits, (64 - sb) / md));
             launch_morton_keys(X64.p, lv.A.p, lv.slot.p, N, n, md, d_mm.p, d_mm.p + md, keys.p,
-                               vals.p, s);
+                               vals.p, s, mb);
             lv.J.ensure(N);
             lv.posJ.ensure(N);
-            sort_pairs_u64_u32(sc, keys.p, skeys.p, vals.p, lv.J.p, N,
-                               32 + bits_for(nruns ? nruns - 1 : 0), s);
+            sort_pairs_u64_u32(sc, keys.p, skeys.p, vals.p, lv.J.p, N, (int)std::min<uint32_t>(64, md * mb + sb), s);
             launch_inverse(lv.J.p, N, lv.posJ.p, s);
         }
         lv.bbox_ready = false;
@@ -961,6 +963,9 @@ struct knnj_ctx {
     // tcgen05 join (n <= 20): 64-candidate tiles, 4 early-released buffers. Off: 646 ms vs
     // 540 ms for 128-candidate tiles on C2.
     bool tile64 = false;
+    // Fine cascade ahead of level 0 (widths eps * f / 1000, coarsest first is NOT
+    // required: each is tried on the rows still uncertified). 0 = off.
+    uint32_t fine_f[2] = {0, 0};
     uint32_t tc_split() const { return 3 * n + 2 <= 320 ? 3 : 0; }
     // operand row = KB 128-byte k-blocks of 64 halfs (KB <= 5: n <= 106)
     uint32_t tc_row_halfs() const { return 64u * ((tc_split() * n + 2 + 63) / 64); }
@@ -1117,7 +1122,7 @@ struct knnj_ctx {
         // 32-thread blocks instead of mostly idle 128-thread ones. (Not in the fallback
         // levels: few queries against huge neighbourhoods are tile-load bound there, and
         // 128 threads load a tile 4x faster; measured on C4.)
-        if (chunk == (uint32_t)JB && K && &lv == &levels[0] &&
+        if (chunk == (uint32_t)JB && K && (&lv == &levels[0] || &lv >= &levels[40]) &&
             double(nq) / double(std::max<uint64_t>(nuc, 1)) < 48.0) {
             chunk = 32;
             P.chunk = 32;
@@ -1324,6 +1329,11 @@ struct knnj_ctx {
     // Leaves every outcome unchanged; removes e.g. the other Gaussian clusters that
     // share a cell's 3^m neighbourhood in the first m dims.
     bool box_filter = true;
+    // join passes sweep each item's kept blocks nearest-first (box centres)
+    bool sweep_order = true;
+    // join order inside a cell: Morton code over the first morton_dims working dims,
+    // morton_bits per dim (global range)
+    uint32_t morton_dims = 10, morton_bits = 3;
     // The radius a pass may filter to: every decision taken from its lists (in-eps at
     // level 0, the coverage certificate kth < cover2) concerns pairs within the cell
     // width w. When the grid is at most 2 cells wide in every dim the certificate is
@@ -1335,12 +1345,14 @@ struct knnj_ctx {
             launch_block_boxes(X64.p, lv.J.p, N, n, lv.bbox.p, s);
             lv.bbox_ready = true;
         }
-        P.screened = filter_items(P.items.p, P.nitems, P.qpos.p, lv.J.p, lv.bbox.p, P.adj, P.nadj, r2);
+        P.screened = filter_items(P.items.p, P.nitems, P.qpos.p, lv.J.p, lv.bbox.p, P.adj, P.nadj, r2,
+                                  sweep_order);
     }
     // items (qbeg, qend, abeg, aend) over adjacency ranges adj: keep only the blocks within
     // sqrt(r2) of the item's query box; adj is replaced. Returns the kept candidate pairs.
     uint64_t filter_items(uint4* items, uint64_t nitems, const uint32_t* qpos, const uint32_t* J,
-                          const float* bbox, DBuf<uint2>& adj, uint64_t& nadj, double r2) {
+                          const float* bbox, DBuf<uint2>& adj, uint64_t& nadj, double r2,
+                          bool order = false) {
         const uint64_t nblk = (N + FB - 1) / FB;
         // FP64 scalar sums can fall below the true sq: widen, then round up to FP32
         const float r2c = f32_round_up(r2 * (1.0 + 1e-9));
@@ -1351,18 +1363,44 @@ struct knnj_ctx {
         off.ensure(nitems + 1);
         launch_item_boxes(items, nitems, qpos, J, X64.p, n, qbox.p, s);
         KJ_CUDA(cudaMemsetAsync(cnt.p + nitems, 0, 4, s));
+        DBuf<float> okey, okey2;
+        float* kp = nullptr;
+        if (order) {
+            okey.ensure(1);
+            kp = okey.p;  // non-null selects the per-block (ordered) variant
+        }
         launch_filter_ranges(items, nitems, qbox.p, n, adj.p, bbox, nblk, r2c, cnt.p, nullptr,
-                             nullptr, nullptr, false, s);
+                             nullptr, nullptr, false, s, kp);
         exclusive_sum(sc, cnt.p, off.p, nitems + 1, s);
         uint32_t total = 0;
         KJ_CUDA(cudaMemcpyAsync(&total, off.p + nitems, 4, cudaMemcpyDeviceToHost, s));
         sync();
         DBuf<uint2> adj2;
         adj2.ensure(total);
+        if (order) {
+            okey.ensure(total);
+            kp = okey.p;
+        }
         d_u64a.ensure(1);
         KJ_CUDA(cudaMemsetAsync(d_u64a.p, 0, 8, s));
         launch_filter_ranges(items, nitems, qbox.p, n, adj.p, bbox, nblk, r2c, nullptr, off.p,
-                             adj2.p, d_u64a.p, true, s);
+                             adj2.p, d_u64a.p, true, s, kp);
+        if (order && total) {
+            // nearest blocks first inside every item: the top-K cut converges early
+            DBuf<uint2> adj3;
+            adj3.ensure(total);
+            okey2.ensure(total);
+            size_t bytes = 0;
+            auto* v_in = reinterpret_cast<uint64_t*>(adj2.p);
+            auto* v_out = reinterpret_cast<uint64_t*>(adj3.p);
+            KJ_CUDA(cub::DeviceSegmentedSort::SortPairs(nullptr, bytes, okey.p, okey2.p, v_in, v_out,
+                                                        (int64_t)total, (int64_t)nitems, off.p,
+                                                        off.p + 1, s));
+            KJ_CUDA(cub::DeviceSegmentedSort::SortPairs(sc.get(bytes), bytes, okey.p, okey2.p, v_in,
+                                                        v_out, (int64_t)total, (int64_t)nitems,
+                                                        off.p, off.p + 1, s));
+            adj2.swap(adj3);
+        }
         unsigned long long scr = 0;
         KJ_CUDA(cudaMemcpyAsync(&scr, d_u64a.p, 8, cudaMemcpyDeviceToHost, s));
         sync();
@@ -1430,10 +1468,25 @@ struct knnj_ctx {
                 a.out_key = pass_key.p;
             }
             a.delta = f32_round_up(tc_delta());
+            static const bool want_stats = getenv("KNNJ_JOIN_STATS") != nullptr;
+            if (const char* dm = getenv("KNNJ_JOIN_DBG")) a.dbg_mode = (uint32_t)atoi(dm);
+            DBuf<unsigned long long> st;
+            if (want_stats) {
+                st.ensure(8);
+                KJ_CUDA(cudaMemsetAsync(st.p, 0, 64, s));
+                a.stats = st.p;
+            }
             trace().mark("pass: pre-kernel", s);
             Timer t(s);
             launch_join_tc(a, tcc.sh, P.nitems, N, s);
             last_join_kernel_ms = t.ms();
+            if (want_stats) {
+                unsigned long long h[8];
+                KJ_CUDA(cudaMemcpyAsync(h, st.p, 64, cudaMemcpyDeviceToHost, s));
+                KJ_CUDA(cudaStreamSynchronize(s));
+                fprintf(stderr, "join stats: items %llu rows %llu slabs %llu rare %llu bits %llu inserts %llu compactions %llu ms %.1f\n",
+                        (unsigned long long)P.nitems, (unsigned long long)nv, h[0], h[1], h[2], h[3], h[4], last_join_kernel_ms);
+            }
             last_join_tc = true;
         } else {
             JoinArgs a{};
@@ -1459,6 +1512,11 @@ struct knnj_ctx {
             last_join_kernel_ms = t.ms();
             last_join_tc = false;
         }
+        if (getenv("KNNJ_JOIN_STATS"))
+            fprintf(stderr, "pass: tc %d chunk %u items %llu rows %llu cand %llu screened %llu w %.6g cover2 %.6g K %u L %u ms %.1f\n",
+                    (int)tc, P.chunk, (unsigned long long)P.nitems, (unsigned long long)nv,
+                    (unsigned long long)P.candidates, (unsigned long long)P.screened, lv.w, cov2, K, L,
+                    last_join_kernel_ms);
         FinalArgs f{};
         f.X64 = X64.p;
         f.n = n;
@@ -1546,6 +1604,71 @@ struct knnj_ctx {
     // Exact KNN for the given queries (pids + rows), certified globally: level
     // passes at widths w0*2^L, each seeded with the previous upper bound.
     // U (per row, may be inf) = known upper bound of the K-th sq.
+    // Level-0 join through the fine cascade: the pass's rows are first joined on grids of
+    // width eps * f (f < 1). A row whose K-th exact distance there is below the fine cell
+    // width (ST_CERT) already has its exact top-K, and that K-th is below eps, so it is a
+    // dense success too (ST_IN_EPS): the outcome level 0 would give, over a neighbourhood
+    // (3f)^m times the size. Only the remaining rows run the level-0 pass.
+    void fine_cascade(uint32_t m, double eps, const Pass& P, uint32_t K, const uint8_t* d_dense,
+                      uint32_t* out_ids, double* out_dist, double* out_kth, uint8_t* out_status,
+                      uint64_t* n_slow, knnj_run_info& I) {
+        uint64_t nrem = P.nq;
+        DBuf<uint32_t> rows, pids, rows2, pids2;
+        rows.ensure(nrem);
+        pids.ensure(nrem);
+        if (nrem) {
+            KJ_CUDA(cudaMemcpyAsync(rows.p, P.qrow.p, 4 * nrem, cudaMemcpyDeviceToDevice, s));
+            launch_map_u32(P.qpos.p, levels[0].J.p, nrem, pids.p, s);
+        }
+        double kernel_ms = 0.0;
+        uint64_t screened = 0;
+        for (int i = 0; i < 2 && nrem; ++i) {
+            if (!fine_f[i]) continue;
+            const int L = 40 + i;
+            build_level(L, m, eps * double(fine_f[i]) / 1000.0);
+            Level& lf = levels[L];
+            Pass Pf;
+            build_pass(lf, pids.p, rows.p, nrem, Pf, K, 0, 1, nullptr, filter_radius2(lf));
+            run_pass(lf, Pf, K, nullptr, eps * eps, cover2(lf), out_ids, out_dist, out_kth,
+                     out_status, n_slow);
+            kernel_ms += last_join_kernel_ms;
+            screened += Pf.screened;
+            DBuf<uint8_t> flags;
+            flags.ensure(nrem);
+            launch_uncert_flags(rows.p, nrem, out_status, flags.p, s);
+            rows2.ensure(nrem);
+            pids2.ensure(nrem);
+            d_u64a.ensure(1);
+            size_t bytes = 0;
+            KJ_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, rows.p, flags.p, rows2.p, d_u64a.p,
+                                               (int64_t)nrem, s));
+            KJ_CUDA(cub::DeviceSelect::Flagged(sc.get(bytes), bytes, rows.p, flags.p, rows2.p,
+                                               d_u64a.p, (int64_t)nrem, s));
+            KJ_CUDA(cub::DeviceSelect::Flagged(sc.get(bytes), bytes, pids.p, flags.p, pids2.p,
+                                               d_u64a.p, (int64_t)nrem, s));
+            unsigned long long left = 0;
+            KJ_CUDA(cudaMemcpyAsync(&left, d_u64a.p, 8, cudaMemcpyDeviceToHost, s));
+            sync();
+            if (getenv("KNNJ_JOIN_STATS"))
+                fprintf(stderr, "fine %u: %llu of %llu rows left\n", fine_f[i], left,
+                        (unsigned long long)nrem);
+            nrem = left;
+            rows.swap(rows2);
+            pids.swap(pids2);
+        }
+        if (nrem) {
+            Level& lv0 = levels[0];
+            Pass P0;
+            build_pass(lv0, pids.p, rows.p, nrem, P0, K, 0, 1, d_dense, filter_radius2(lv0));
+            run_pass(lv0, P0, K, nullptr, eps * eps, cover2(lv0), out_ids, out_dist, out_kth,
+                     out_status, n_slow);
+            kernel_ms += last_join_kernel_ms;
+            screened += P0.screened;
+        }
+        I.ms_join_kernel = kernel_ms;
+        I.join_screened_pairs = screened;
+    }
+
     void exact_levels(uint32_t m, double w0, int first_level, std::vector<uint32_t> qpid,
                       std::vector<uint32_t> qrow, std::vector<double> U, uint32_t K,
                       uint32_t* out_ids, double* out_dist, double* out_kth, uint8_t* out_status,
@@ -1766,10 +1889,21 @@ int knnj_set_option(knnj_ctx* c, const char* name, int64_t value) {
             c->tc_enabled = value != 0;
         } else if (k == "box_filter") {
             c->box_filter = value != 0;
+        } else if (k == "morton_dims" || k == "morton_bits") {
+            if (value < 1 || value > 32) throw Error(1, k + " must be in [1, 32]");
+            (k == "morton_dims" ? c->morton_dims : c->morton_bits) = (uint32_t)value;
+            for (auto& lv : c->levels) lv.built = false;
+            c->mm_lo.clear();
+            c->hist_order_ready = false;
+        } else if (k == "sweep_order") {
+            c->sweep_order = value != 0;
         } else if (k == "tile64") {
             c->tile64 = value != 0;
         } else if (k == "epi_halves") {
             c->epi_halves = value != 0;
+        } else if (k == "fine" || k == "fine2") {
+            if (value < 0 || value >= 1000) throw Error(1, "fine width must be in [0, 1000) permille of eps");
+            c->fine_f[k == "fine" ? 0 : 1] = (uint32_t)value;
         } else if (k == "split_items") {
             c->split_items = value != 0;
         } else if (k == "hist_cap") {
@@ -2413,22 +2547,28 @@ static void run_impl(knnj_ctx* c, const knnj_config* cfg, uint32_t shard, uint32
         Pass P;
         {
             Timer t(s);
+            const bool fine = c->fine_f[0] > 0 || c->fine_f[1] > 0;
             {
                 Timer tb(s);
                 c->build_pass(lv0, d_q.p, d_rows.p, nq, P, k_eff, shard, nshard,
-                              have_dense ? d_dense.p : nullptr, c->filter_radius2(lv0));
+                              have_dense ? d_dense.p : nullptr, fine ? 0.0 : c->filter_radius2(lv0));
                 I.ms_join_build = tb.ms();
             }
-            c->run_pass(lv0, P, k_eff, nullptr, eps * eps, c->cover2(lv0), o_ids.p, o_dist.p,
-                        o_kth.p, o_st.p, &slow);
+            if (!fine) {
+                c->run_pass(lv0, P, k_eff, nullptr, eps * eps, c->cover2(lv0), o_ids.p, o_dist.p,
+                            o_kth.p, o_st.p, &slow);
+                I.ms_join_kernel = c->last_join_kernel_ms;
+                I.join_screened_pairs = P.screened;
+            } else {
+                c->fine_cascade(m, eps, P, k_eff, have_dense ? d_dense.p : nullptr, o_ids.p,
+                                o_dist.p, o_kth.p, o_st.p, &slow, I);
+            }
             I.ms_join = t.ms();
             trace().mark("run: join");
-            I.ms_join_kernel = c->last_join_kernel_ms;
             I.join_tensor_cores = c->last_join_tc ? 1 : 0;
             // candidates_examined counts dense queries only (DenseJoinStats)
             I.candidates_examined = have_dense ? P.candidates_dense : P.candidates;
             I.join_candidate_pairs = P.candidates;
-            I.join_screened_pairs = P.screened;
         }
         n_own = P.nq;
         // ---- classify on device; exact fallback for failures and uncertified sparse rows

@@ -185,6 +185,8 @@ struct TcJoinArgs {
     float* out_key;          // H = 2: the lists' screened keys, same layout as out_pos
     float delta;             // |key - sq64/S^2| bound (scaled units)
     float* dbg;              // test hook: block 0 dumps its first accumulator tile [128][128]
+    uint32_t dbg_mode;       // dev hook (KNNJ_JOIN_DBG, timing only): 1 fast path only, 2 loads only, 3 no loads
+    unsigned long long* stats;  // dev hook (KNNJ_JOIN_STATS): slabs, rare slabs, bits, inserts, compactions
     // histogram epilogue (HIST kernels only)
     uint32_t n_bins;
     uint32_t n_count;        // bins [0, n_count) are counted (n_count < n_bins: capped histogram)
@@ -239,7 +241,8 @@ extern std::atomic<unsigned long long> g_launches;  // our kernels launched so f
 double measure_ffma_tflops(cudaStream_t s);
 void launch_morton_keys(const double* X64, const uint32_t* A, const uint32_t* slot, uint64_t N,
                         uint32_t n, uint32_t dims, const double* lo, const double* inv_range,
-                        uint64_t* keys, uint32_t* vals, cudaStream_t s);
+                        uint64_t* keys, uint32_t* vals, cudaStream_t s,
+                        uint32_t bits = 3);
 void launch_inverse(const uint32_t* J, uint64_t N, uint32_t* posJ, cudaStream_t s);
 // tensor-core kernel shape: KB 128-byte k-blocks per operand row (row_halfs = 64*KB),
 // G groups of 128 queries per CTA, STAGES candidate tiles in flight
@@ -325,7 +328,8 @@ void launch_item_boxes(const uint4* items, uint64_t nitems, const uint32_t* qpos
 void launch_filter_ranges(uint4* items, uint64_t nitems, const float* qbox, uint32_t n,
                           const uint2* adj, const float* box, uint64_t nblk, float r2,
                           uint32_t* out_cnt, const uint32_t* out_off, uint2* out_adj,
-                          unsigned long long* screened, bool fill, cudaStream_t s);
+                          unsigned long long* screened, bool fill, cudaStream_t s,
+                          float* out_key = nullptr);
 void launch_fill_u32(uint32_t* p, uint64_t n, uint32_t v, cudaStream_t s);
 void launch_merge_parts(const uint4* splits, uint64_t nsplits, uint32_t K, const uint32_t* t_ids,
                         const double* t_sq, const uint32_t* t_count, const uint32_t* qrow,
@@ -335,6 +339,8 @@ void launch_merge_parts(const uint4* splits, uint64_t nsplits, uint32_t K, const
 void launch_split_flags(const uint32_t* pids, uint64_t nq, const uint32_t* slot, const uint2* G,
                         double n_thresh, uint8_t* dense, unsigned long long* n_sparse,
                         cudaStream_t s);
+void launch_uncert_flags(const uint32_t* rows, uint64_t n, const uint8_t* st, uint8_t* flags,
+                         cudaStream_t s);
 void launch_classify(const uint32_t* rows, uint64_t n, const uint8_t* st, const uint8_t* dense,
                      uint8_t* prov, uint8_t* need, cudaStream_t s);
 void launch_dense_cand(const uint4* items, const unsigned long long* work, uint64_t nitems,

@@ -1223,26 +1223,30 @@ namespace kj {
 // as the reference order) but are laid out along a space-filling curve.
 __global__ void k_morton_keys(const double* X64, const uint32_t* A, const uint32_t* slot,
                               uint64_t N, uint32_t n, uint32_t dims, const double* lo,
-                              const double* inv_range, uint64_t* keys, uint32_t* vals) {
+                              const double* inv_range, uint64_t* keys, uint32_t* vals,
+                              uint32_t bits) {
+    const uint32_t cb = dims * bits;
+    const double lv = double(1u << bits);
+    const uint32_t qmax = (1u << bits) - 1u;
     for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < N;
          i += uint64_t(gridDim.x) * blockDim.x) {
         const uint32_t pid = A[i];
         const double* x = X64 + (uint64_t)pid * n;
-        uint32_t code = 0;
-        for (int bit = 2; bit >= 0; --bit)
+        uint64_t code = 0;
+        for (int bit = (int)bits - 1; bit >= 0; --bit)
             for (uint32_t d = 0; d < dims; ++d) {
                 double f = (x[d] - lo[d]) * inv_range[d];
-                uint32_t q = f <= 0.0 ? 0u : (f >= 1.0 ? 7u : (uint32_t)(f * 8.0));
+                uint32_t q = f <= 0.0 ? 0u : (f >= 1.0 ? qmax : min(qmax, (uint32_t)(f * lv)));
                 code = (code << 1) | ((q >> bit) & 1u);
             }
-        keys[i] = ((uint64_t)slot[pid] << 32) | code;
+        keys[i] = (cb >= 64 ? 0ull : ((uint64_t)slot[pid] << cb)) | code;
         vals[i] = pid;
     }
 }
 void launch_morton_keys(const double* X64, const uint32_t* A, const uint32_t* slot, uint64_t N,
                         uint32_t n, uint32_t dims, const double* lo, const double* inv_range,
-                        uint64_t* keys, uint32_t* vals, cudaStream_t s) {
-    k_morton_keys<<<2368, 256, 0, s>>>(X64, A, slot, N, n, dims, lo, inv_range, keys, vals);
+                        uint64_t* keys, uint32_t* vals, cudaStream_t s, uint32_t bits) {
+    k_morton_keys<<<2368, 256, 0, s>>>(X64, A, slot, N, n, dims, lo, inv_range, keys, vals, bits);
     KJ_CUDA(cudaGetLastError());
     g_launches.fetch_add(1, std::memory_order_relaxed);
 }
@@ -1313,6 +1317,22 @@ void launch_classify(const uint32_t* rows, uint64_t n, const uint8_t* st, const 
                      uint8_t* prov, uint8_t* need, cudaStream_t s) {
     if (!n) return;
     k_classify<<<1184, 256, 0, s>>>(rows, n, st, dense, prov, need);
+    KJ_CUDA(cudaGetLastError());
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+
+// rows whose list is not yet globally exact (fine cascade: they go on to level 0)
+__global__ void k_uncert_flags(const uint32_t* rows, uint64_t n, const uint8_t* st, uint8_t* flags) {
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const uint8_t v = st[rows[i]];
+        flags[i] = ((v & ST_HAS_K) && (v & ST_CERT)) ? 0 : 1;
+    }
+}
+void launch_uncert_flags(const uint32_t* rows, uint64_t n, const uint8_t* st, uint8_t* flags,
+                         cudaStream_t s) {
+    if (!n) return;
+    k_uncert_flags<<<1184, 256, 0, s>>>(rows, n, st, flags);
     KJ_CUDA(cudaGetLastError());
     g_launches.fetch_add(1, std::memory_order_relaxed);
 }
@@ -1558,11 +1578,13 @@ __global__ void k_item_boxes(const uint4* items, uint64_t nitems, const uint32_t
 // (rounded down, early exit) exceeds r2 are dropped, the survivors re-emitted as
 // merged ranges. COUNT: out_cnt[item] = ranges kept. FILL: ranges written at
 // out_off[item], (abeg, aend) of the item rewritten, kept pairs summed into screened.
-template <bool FILL>
+// ORDER: one range per kept block plus a sweep-order key (squared distance between the
+// item box centre and the block box centre), for a per-item sort nearest-first.
+template <bool FILL, bool ORDER>
 __global__ void k_filter_ranges(uint4* items, uint64_t nitems, const float* qbox, uint32_t n,
                                 const uint2* adj, const float* box, uint64_t nblk, float r2,
                                 uint32_t* out_cnt, const uint32_t* out_off, uint2* out_adj,
-                                unsigned long long* screened) {
+                                unsigned long long* screened, float* out_key) {
     const int lane = threadIdx.x & 31;
     const uint64_t item = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     if (item >= nitems) return;
@@ -1581,6 +1603,7 @@ __global__ void k_filter_ranges(uint4* items, uint64_t nitems, const float* qbox
         for (uint32_t c0 = b0; c0 <= b1; c0 += 32) {
             const uint32_t blk = c0 + lane;
             bool keep = false;
+            float ck = 0.f;
             if (blk <= b1) {
                 float acc = 0.f;
                 for (uint32_t d = 0; d < n && acc <= r2; ++d) {
@@ -1590,8 +1613,26 @@ __global__ void k_filter_ranges(uint4* items, uint64_t nitems, const float* qbox
                     acc = __fadd_rd(acc, __fmul_rd(g, g));
                 }
                 keep = acc <= r2;
+                if (ORDER && FILL && keep)
+                    for (uint32_t d = 0; d < n; ++d) {
+                        const float lo = __ldg(box + (uint64_t)d * nblk + blk);
+                        const float hi = __ldg(box + (uint64_t)(n + d) * nblk + blk);
+                        const float dc = 0.5f * ((lo + hi) - (ql[d] + qh[d]));
+                        ck = fmaf(dc, dc, ck);
+                    }
             }
             const unsigned m = __ballot_sync(0xffffffffu, keep);
+            if (ORDER) {
+                if (FILL && keep) {
+                    const uint32_t rank = kept + __popc(m & ((1u << lane) - 1u));
+                    const uint2 o = make_uint2(max(rg.x, blk * FB), min(rg.y, (blk + 1) * FB));
+                    out_adj[base + rank] = o;
+                    out_key[base + rank] = ck;
+                    span += o.y - o.x;
+                }
+                kept += __popc(m);
+                continue;
+            }
             const unsigned starts = m & ~(m << 1);  // first block of each kept run
             if (FILL && ((starts >> lane) & 1u)) {
                 const unsigned above = lane == 31 ? 0u : ~m & ~((2u << lane) - 1u);
@@ -1624,15 +1665,21 @@ void launch_item_boxes(const uint4* items, uint64_t nitems, const uint32_t* qpos
 void launch_filter_ranges(uint4* items, uint64_t nitems, const float* qbox, uint32_t n,
                           const uint2* adj, const float* box, uint64_t nblk, float r2,
                           uint32_t* out_cnt, const uint32_t* out_off, uint2* out_adj,
-                          unsigned long long* screened, bool fill, cudaStream_t s) {
+                          unsigned long long* screened, bool fill, cudaStream_t s,
+                          float* out_key) {
     if (!nitems) return;
     const unsigned grid = (unsigned)((nitems * 32 + 255) / 256);
-    if (fill)
-        k_filter_ranges<true><<<grid, 256, 0, s>>>(items, nitems, qbox, n, adj, box, nblk, r2,
-                                                   out_cnt, out_off, out_adj, screened);
-    else
-        k_filter_ranges<false><<<grid, 256, 0, s>>>(items, nitems, qbox, n, adj, box, nblk, r2,
-                                                    out_cnt, out_off, out_adj, screened);
+#define KJ_FR(F, O)                                                                       \
+    k_filter_ranges<F, O><<<grid, 256, 0, s>>>(items, nitems, qbox, n, adj, box, nblk, r2, \
+                                               out_cnt, out_off, out_adj, screened, out_key)
+    if (out_key) {
+        if (fill) KJ_FR(true, true);
+        else KJ_FR(false, true);
+    } else {
+        if (fill) KJ_FR(true, false);
+        else KJ_FR(false, false);
+    }
+#undef KJ_FR
     KJ_CUDA(cudaGetLastError());
     g_launches.fetch_add(1, std::memory_order_relaxed);
 }

@@ -44,6 +44,15 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
                  : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#ifdef KNNJ_MBAR_SUSPEND
+    asm volatile(
+        "{\n\t.reg .pred P;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1, %2;\n\t"
+        "@!P bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity), "r"(KNNJ_MBAR_SUSPEND)
+        : "memory");
+#else
     asm volatile(
         "{\n\t.reg .pred P;\n\t"
         "WAIT_%=:\n\t"
@@ -51,6 +60,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "@!P bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
         "r"(parity)
         : "memory");
+#endif
 }
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar,
                                             int c0, int c1) {
@@ -494,7 +504,7 @@ __global__ void __launch_bounds__(64 + 128 * G * H, 1)
         float rhs = has_q ? __fsub_ru(cut, na) : -CUDART_INF_F;
         // compact the buffer of query column `src_lane` (all lanes cooperate)
         auto compact = [&](int src) {
-            if (H == 2) __syncwarp();  // the src lane's global appends are visible to the warp
+            __syncwarp();  // the src lane's appends are visible to the warp
             const uint32_t c_src = __shfl_sync(0xffffffffu, cnt, src);
             const uint32_t col = g * 128 + quarter * 32 + src;
             float* kb = list_key(col);
@@ -542,6 +552,7 @@ __global__ void __launch_bounds__(64 + 128 * G * H, 1)
             }
         };
         uint32_t s, c;
+        unsigned long long st_slab = 0, st_rare = 0, st_bits = 0, st_ins = 0, st_cmp = 0;
         for (uint32_t t = 0; next_tile(s, c); ++t) {
             const int b = t % NB;
             mbar_wait(&bar_accf[b], (t / NB) & 1);
@@ -553,6 +564,21 @@ __global__ void __launch_bounds__(64 + 128 * G * H, 1)
                     cut = pc;
                     rhs = __fsub_ru(cut, na);
                 }
+            }
+            if (p.dbg_mode) {  // timing decomposition (output is meaningless)
+                for (uint32_t j0 = 0; j0 < c && p.dbg_mode < 3; j0 += 64) {
+                    float v0[32], v1[32];
+                    tmem_ld64(tbase + j0, v0, v1);
+                    float mn = fminf(v0[0], v1[0]);
+                    if (p.dbg_mode == 1)
+#pragma unroll
+                        for (int j = 1; j < 32; ++j) mn = fminf(mn, fminf(v0[j], v1[j]));
+                    if (__any_sync(0xffffffffu, mn < -1e30f)) ++cnt;
+                }
+                fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&bar_acce[b]);
+                continue;
             }
             for (uint32_t j0 = H == 2 ? hh * 64 : 0; j0 < c; j0 += H == 2 ? 128 : 64) {
                 float v0[32], v1[32];
@@ -590,8 +616,10 @@ __global__ void __launch_bounds__(64 + 128 * G * H, 1)
                         m1[j] = fminf(m1[j], m1[j + w]);
                     }
                 const bool hit = has_q && !ovf && fminf(m0[0], m1[0]) <= rhs;
+                ++st_slab;
                 if (!__any_sync(0xffffffffu, hit)) continue;
-                // rare path
+                ++st_rare;
+                // rare path: warp-uniform loop over the columns any lane hit
                 unsigned mk[2] = {0u, 0u};
                 if (hit) {
 #pragma unroll
@@ -606,6 +634,7 @@ __global__ void __launch_bounds__(64 + 128 * G * H, 1)
                     while (um) {
                         const int j = __ffs(um) - 1;
                         um &= um - 1;
+                        ++st_bits;
                         const float x = ER ? (h == 0 ? sel32(v0, (uint32_t)j) : sel32(v1, (uint32_t)j))
                                            : tmem_ld1(tbase + j0 + h * 32 + j);
                         const uint32_t pos = s + j0 + h * 32 + j;
@@ -615,9 +644,11 @@ __global__ void __launch_bounds__(64 + 128 * G * H, 1)
                         while (full) {
                             const int src = __ffs(full) - 1;
                             full &= full - 1;
+                            ++st_cmp;
                             compact(src);
                         }
                         want = want && !ovf && x <= rhs;  // cut may have tightened
+                        if (p.stats) st_ins += __popc(__ballot_sync(0xffffffffu, want));
                         if (want) {
                             mykey[cnt] = x + na;
                             mypos[cnt] = pos;
@@ -631,6 +662,13 @@ __global__ void __launch_bounds__(64 + 128 * G * H, 1)
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&bar_acce[b]);
             }
+        }
+        if (p.stats && lane == 0) {
+            atomicAdd(p.stats + 0, st_slab);
+            atomicAdd(p.stats + 1, st_rare);
+            atomicAdd(p.stats + 2, st_bits);
+            atomicAdd(p.stats + 3, st_ins);
+            atomicAdd(p.stats + 4, st_cmp);
         }
         if (has_q) {
             if (H == 2) {

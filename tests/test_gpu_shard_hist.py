@@ -141,7 +141,7 @@ def test_epilogue_halves_identical(engine, oracle, spec, N, n, k):
         engine.set_option("epi_halves", halves)
         engine.set_points(X)
         out.append(engine.run(cfg, want_hist=False))
-    engine.set_option("epi_halves", 1)
+    engine.set_option("epi_halves", 0)
     a, b = out
     assert np.array_equal(a.ids, b.ids) and np.array_equal(a.dist, b.dist)
     assert np.array_equal(a.provenance, b.provenance)
@@ -187,11 +187,62 @@ def test_tile64_identical(engine, oracle, spec, N, n, k):
         engine.set_option("tile64", t64)
         engine.set_points(X)
         out.append(engine.run(cfg, want_hist=False))
-    engine.set_option("tile64", 1)
+    engine.set_option("tile64", 0)
     a, b = out
     assert np.array_equal(a.ids, b.ids) and np.array_equal(a.dist, b.dist)
     assert np.array_equal(a.provenance, b.provenance)
     W = X[:, b.info["perm"]]
     q = np.random.default_rng(8).choice(N, 48, replace=False).astype(np.uint32)
+    oi, od = oracle.brute_knn(W, q, k)
+    assert np.array_equal(b.ids[q], oi) and np.array_equal(b.dist[q], od)
+
+
+@pytest.mark.parametrize("spec,N,n,k", [("clusters:16:0.05", 30000, 18, 32), ("exponential", 40000, 6, 40),
+                                        ("uniform", 50000, 2, 10), ("mixture:8:0.05", 6000, 90, 16)])
+def test_fine_cascade_identical(engine, oracle, spec, N, n, k):
+    """Rows certified on the fine grids (width f*eps) skip level 0; every output bit,
+    the provenance and the failure count equal the plain level-0 run."""
+    X = generate(spec, N, n, 37)
+    cfg = RunConfig(k=k, mode="hybrid", seed=37)
+    out = []
+    for f1, f2 in ((0, 0), (700, 0), (500, 700)):
+        engine.set_option("fine", f1)
+        engine.set_option("fine2", f2)
+        engine.set_points(X)
+        out.append(engine.run(cfg, want_hist=False))
+    engine.set_option("fine", 0)
+    engine.set_option("fine2", 0)
+    a = out[0]
+    for b in out[1:]:
+        assert np.array_equal(a.ids, b.ids) and np.array_equal(a.dist, b.dist)
+        assert np.array_equal(a.provenance, b.provenance)
+        assert a.info["failed_count"] == b.info["failed_count"]
+        assert a.info["candidates_examined"] == b.info["candidates_examined"]
+    W = X[:, a.info["perm"]]
+    q = np.random.default_rng(4).choice(N, 48, replace=False).astype(np.uint32)
+    oi, od = oracle.brute_knn(W, q, k)
+    assert np.array_equal(out[2].ids[q], oi) and np.array_equal(out[2].dist[q], od)
+
+
+@pytest.mark.parametrize("spec,N,n,k", [("clusters:16:0.05", 30000, 18, 32), ("exponential", 40000, 6, 40),
+                                        ("mixture", 40000, 5, 8), ("mixture:8:0.05", 6000, 90, 16)])
+def test_sweep_order_identical(engine, oracle, spec, N, n, k):
+    """Sweeping each item's kept blocks nearest-first (per-block ranges, segmented
+    sort) changes only the order candidates are screened in, never the output."""
+    X = generate(spec, N, n, 41)
+    cfg = RunConfig(k=k, mode="hybrid", seed=41)
+    out = []
+    for o in (0, 1):
+        engine.set_option("sweep_order", o)
+        engine.set_points(X)
+        out.append(engine.run(cfg, want_hist=False))
+    engine.set_option("sweep_order", 0)
+    a, b = out
+    assert np.array_equal(a.ids, b.ids) and np.array_equal(a.dist, b.dist)
+    assert np.array_equal(a.provenance, b.provenance)
+    assert a.info["failed_count"] == b.info["failed_count"]
+    assert a.info["join_screened_pairs"] == b.info["join_screened_pairs"]
+    W = X[:, b.info["perm"]]
+    q = np.random.default_rng(6).choice(N, 48, replace=False).astype(np.uint32)
     oi, od = oracle.brute_knn(W, q, k)
     assert np.array_equal(b.ids[q], oi) and np.array_equal(b.dist[q], od)
