@@ -963,6 +963,7 @@ struct knnj_ctx {
     // tcgen05 join (n <= 20): 64-candidate tiles, 4 early-released buffers. Off: 646 ms vs
     // 540 ms for 128-candidate tiles on C2.
     bool tile64 = false;
+    uint32_t tc_slack = 24;  // tcgen05 join list capacity K + slack (compaction when full)
     // Fine cascade ahead of level 0 (widths eps * f / 1000, coarsest first is NOT
     // required: each is tried on the rows still uncertified). 0 = off.
     uint32_t fine_f[2] = {0, 0};
@@ -1029,7 +1030,7 @@ struct knnj_ctx {
         TcJoinCfg c;
         if (!use_tc() || K < 1 || !tc_precise_for(w)) return c;
         const uint32_t KB = tc_row_halfs() / 64;
-        const uint32_t L0 = K + (tc_split() == 3 ? 24u : 48u);
+        const uint32_t L0 = K + (tc_split() == 3 ? tc_slack : 48u);
         if (KB >= 3) {
             // wide operands (43 <= n <= 106): 64-candidate tiles keep A + B stages in smem
             c.sh = TcShape{(int)KB, 1, KB == 5 ? 2 : 3, 1, 64};
@@ -1897,6 +1898,9 @@ int knnj_set_option(knnj_ctx* c, const char* name, int64_t value) {
             c->hist_order_ready = false;
         } else if (k == "sweep_order") {
             c->sweep_order = value != 0;
+        } else if (k == "tc_slack") {
+            if (value < 8 || value > 96) throw Error(1, "tc_slack must be in [8, 96]");
+            c->tc_slack = (uint32_t)value;
         } else if (k == "tile64") {
             c->tile64 = value != 0;
         } else if (k == "epi_halves") {
