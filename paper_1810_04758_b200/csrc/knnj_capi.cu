@@ -943,6 +943,7 @@ struct knnj_ctx {
             launch_inverse(lv.J.p, N, lv.posJ.p, s);
         }
         lv.bbox_ready = false;
+        lv.xj_ready = false;
         lv.xs_ready = false;  // the SIMT join's FP32 SoA copy is built on first use
         lv.tc_ready = false;
         if (use_tc()) prep_tc(lv);
@@ -963,7 +964,8 @@ struct knnj_ctx {
     // tcgen05 join (n <= 20): 64-candidate tiles, 4 early-released buffers. Off: 646 ms vs
     // 540 ms for 128-candidate tiles on C2.
     bool tile64 = false;
-    uint32_t tc_slack = 24;  // tcgen05 join list capacity K + slack (compaction when full)
+    uint32_t tc_slack = 24;
+    bool finalize_xj = true;  // finalize reads FP64 rows from a join-ordered copy  // tcgen05 join list capacity K + slack (compaction when full)
     // Fine cascade ahead of level 0 (widths eps * f / 1000, coarsest first is NOT
     // required: each is tried on the rows still uncertified). 0 = off.
     uint32_t fine_f[2] = {0, 0};
@@ -1536,6 +1538,14 @@ struct knnj_ctx {
         f.out_kth = out_kth;
         f.out_status = out_status;
         f.halves = hv == 2 ? 1u : 0u;
+        if (finalize_xj && P.nq >= (1u << 16)) {  // big passes: gather rows in join order once
+            if (!lv.xj_ready) {
+                lv.XJ.ensure((uint64_t)N * n);
+                launch_rows_by(X64.p, lv.J.p, N, n, lv.XJ.p, s);
+                lv.xj_ready = true;
+            }
+            f.XJ = lv.XJ.p;
+        }
         trace().mark("pass: join kernel", s);
         launch_finalize(f, s);
         // split-part rows: finalized into their own exact top-K (with sq), merged below
@@ -1898,6 +1908,8 @@ int knnj_set_option(knnj_ctx* c, const char* name, int64_t value) {
             c->hist_order_ready = false;
         } else if (k == "sweep_order") {
             c->sweep_order = value != 0;
+        } else if (k == "finalize_xj") {
+            c->finalize_xj = value != 0;
         } else if (k == "tc_slack") {
             if (value < 8 || value > 96) throw Error(1, "tc_slack must be in [8, 96]");
             c->tc_slack = (uint32_t)value;

@@ -129,6 +129,8 @@ struct Level {
     DBuf<__half> Bh;     // N x row_halfs: tensor-core B operand (knnj_tc.cu)
     DBuf<float> bbox;    // 2n x ceil(N/FB): FP32 boxes (outward) of FB-position blocks (J order)
     bool bbox_ready = false;
+    DBuf<double> XJ;     // N x n: FP64 rows in join order (finalize gathers; lazy)
+    bool xj_ready = false;
 };
 
 // Work description of one join pass (queries of one level grid).
@@ -217,6 +219,7 @@ struct FinalArgs {
     double* out_sq;          // optional [qrow * K]: exact sq (split-part rows, for the merge)
     uint32_t* out_count;     // optional [qrow]: entries written (min(candidates, K))
     uint32_t halves;         // 1: two lists per row (cnt[2r + h], pos[(2r + h) * L + i])
+    const double* XJ;        // optional: X64 rows in A order (row p = point A[p]); locality
 };
 
 struct HistArgs {
@@ -339,6 +342,8 @@ void launch_merge_parts(const uint4* splits, uint64_t nsplits, uint32_t K, const
 void launch_split_flags(const uint32_t* pids, uint64_t nq, const uint32_t* slot, const uint2* G,
                         double n_thresh, uint8_t* dense, unsigned long long* n_sparse,
                         cudaStream_t s);
+void launch_rows_by(const double* X64, const uint32_t* A, uint64_t N, uint32_t n, double* out,
+                    cudaStream_t s);
 void launch_uncert_flags(const uint32_t* rows, uint64_t n, const uint8_t* st, uint8_t* flags,
                          cudaStream_t s);
 void launch_classify(const uint32_t* rows, uint64_t n, const uint8_t* st, const uint8_t* dense,

@@ -292,8 +292,8 @@ __global__ void k_finalize(FinalArgs a) {
         if (lane == 0) a.out_status[orow] = ST_OVF;
         return;
     }
-    const uint32_t qid = a.A[a.qpos[row]];
-    const double* qx = a.X64 + (uint64_t)qid * a.n;
+    const uint32_t qp = a.qpos[row];
+    const double* qx = a.XJ ? a.XJ + (uint64_t)qp * a.n : a.X64 + (uint64_t)a.A[qp] * a.n;
     constexpr int EMAX = 8;
     double sq[EMAX];
     uint32_t id[EMAX];
@@ -308,9 +308,10 @@ __global__ void k_finalize(FinalArgs a) {
         if (e < E && i < c) {
             const uint64_t pi = !a.halves ? row * a.L + i
                                 : (i < c0 ? (2 * row) * a.L + i : (2 * row + 1) * a.L + (i - c0));
-            const uint32_t t = a.A[a.pos[pi]];
+            const uint32_t ps = a.pos[pi];
+            const uint32_t t = a.A[ps];
             id[e] = t;
-            sq[e] = exact_sq(qx, a.X64 + (uint64_t)t * a.n, a.n);
+            sq[e] = exact_sq(qx, a.XJ ? a.XJ + (uint64_t)ps * a.n : a.X64 + (uint64_t)t * a.n, a.n);
         }
     }
 #pragma unroll
@@ -1317,6 +1318,23 @@ void launch_classify(const uint32_t* rows, uint64_t n, const uint8_t* st, const 
                      uint8_t* prov, uint8_t* need, cudaStream_t s) {
     if (!n) return;
     k_classify<<<1184, 256, 0, s>>>(rows, n, st, dense, prov, need);
+    KJ_CUDA(cudaGetLastError());
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+
+// FP64 rows in a level's position order (same values, contiguous per cell)
+__global__ void k_rows_by(const double* X64, const uint32_t* A, uint64_t N, uint32_t n, double* out) {
+    const uint64_t total = N * n;
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t r = i / n;
+        out[i] = X64[(uint64_t)A[r] * n + (i - r * n)];
+    }
+}
+void launch_rows_by(const double* X64, const uint32_t* A, uint64_t N, uint32_t n, double* out,
+                    cudaStream_t s) {
+    if (!N) return;
+    k_rows_by<<<2368, 256, 0, s>>>(X64, A, N, n, out);
     KJ_CUDA(cudaGetLastError());
     g_launches.fetch_add(1, std::memory_order_relaxed);
 }
