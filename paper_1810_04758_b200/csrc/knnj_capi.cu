@@ -965,7 +965,8 @@ struct knnj_ctx {
     // 540 ms for 128-candidate tiles on C2.
     bool tile64 = false;
     uint32_t tc_slack = 24;
-    bool finalize_xj = true;  // finalize reads FP64 rows from a join-ordered copy  // tcgen05 join list capacity K + slack (compaction when full)
+    bool finalize_xj = true;
+    bool brute_fallback = false;  // <= 64 fallback rows: brute force over all points (off: 16.6 vs 8.3 ms on C2)  // finalize reads FP64 rows from a join-ordered copy  // tcgen05 join list capacity K + slack (compaction when full)
     // Fine cascade ahead of level 0 (widths eps * f / 1000, coarsest first is NOT
     // required: each is tried on the rows still uncertified). 0 = off.
     uint32_t fine_f[2] = {0, 0};
@@ -1695,6 +1696,33 @@ struct knnj_ctx {
             }
             return L;
         };
+        // A handful of rows on a big dataset: brute force over all points (32 warps per
+        // row, merged) instead of building a grid level for them.
+        if (brute_fallback && !qpid.empty() && qpid.size() <= 64 && N >= 65536 && K <= 128) {
+            const uint64_t nq = qpid.size();
+            const uint32_t P = 32;
+            DBuf<uint32_t> d_p, d_r, t_ids, t_cnt;
+            DBuf<double> t_sq;
+            DBuf<uint4> sp;
+            d_p.ensure(nq);
+            d_r.ensure(nq);
+            t_ids.ensure(nq * P * K);
+            t_sq.ensure(nq * P * K);
+            t_cnt.ensure(nq * P);
+            sp.ensure(nq);
+            std::vector<uint4> hs(nq);
+            for (uint64_t i = 0; i < nq; ++i)
+                hs[i] = make_uint4((uint32_t)i, 1u, P, (uint32_t)(i * P));
+            KJ_CUDA(cudaMemcpyAsync(d_p.p, qpid.data(), 4 * nq, cudaMemcpyHostToDevice, s));
+            KJ_CUDA(cudaMemcpyAsync(d_r.p, qrow.data(), 4 * nq, cudaMemcpyHostToDevice, s));
+            KJ_CUDA(cudaMemcpyAsync(sp.p, hs.data(), 16 * nq, cudaMemcpyHostToDevice, s));
+            launch_brute_parts(X64.p, N, n, d_p.p, nq, P, K, t_ids.p, t_sq.p, t_cnt.p, s);
+            launch_merge_parts(sp.p, nq, K, t_ids.p, t_sq.p, t_cnt.p, d_r.p, -1.0, kInf, out_ids,
+                               out_dist, out_kth, out_status, s);
+            if (passes) ++*passes;
+            sync();
+            return;
+        }
         std::vector<int> lvl(qpid.size());
         for (size_t i = 0; i < qpid.size(); ++i) lvl[i] = level_for(U[i], first_level - 1);
         DBuf<float> d_cut_by_row;  // only the current pass's rows are ever written / read
@@ -1908,6 +1936,8 @@ int knnj_set_option(knnj_ctx* c, const char* name, int64_t value) {
             c->hist_order_ready = false;
         } else if (k == "sweep_order") {
             c->sweep_order = value != 0;
+        } else if (k == "brute_fallback") {
+            c->brute_fallback = value != 0;
         } else if (k == "finalize_xj") {
             c->finalize_xj = value != 0;
         } else if (k == "tc_slack") {

@@ -342,6 +342,9 @@ void launch_merge_parts(const uint4* splits, uint64_t nsplits, uint32_t K, const
 void launch_split_flags(const uint32_t* pids, uint64_t nq, const uint32_t* slot, const uint2* G,
                         double n_thresh, uint8_t* dense, unsigned long long* n_sparse,
                         cudaStream_t s);
+void launch_brute_parts(const double* X64, uint64_t N, uint32_t n, const uint32_t* qpid,
+                        uint64_t nq, uint32_t P, uint32_t K, uint32_t* t_ids, double* t_sq,
+                        uint32_t* t_count, cudaStream_t s);
 void launch_rows_by(const double* X64, const uint32_t* A, uint64_t N, uint32_t n, double* out,
                     cudaStream_t s);
 void launch_uncert_flags(const uint32_t* rows, uint64_t n, const uint8_t* st, uint8_t* flags,

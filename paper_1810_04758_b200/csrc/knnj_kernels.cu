@@ -1322,6 +1322,74 @@ void launch_classify(const uint32_t* rows, uint64_t n, const uint8_t* st, const 
     g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
+// Brute-force exact top-K of a few query points over all points, cut into P parts of the
+// point-id range (one warp per (query, part)); parts are merged by k_merge_parts. For
+// fallback sets too small to pay for a grid level.
+__global__ void k_brute_parts(const double* X64, uint64_t N, uint32_t n, const uint32_t* qpid,
+                              uint32_t P, uint32_t K, uint32_t* t_ids, double* t_sq,
+                              uint32_t* t_count) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double* ls = reinterpret_cast<double*>(smem_raw);          // [K][32]
+    uint32_t* li = reinterpret_cast<uint32_t*>(ls + K * 32);   // [K][32]
+    const int lane = threadIdx.x;
+    const uint32_t q = blockIdx.x / P, part = blockIdx.x % P;
+    const uint32_t qid = qpid[q];
+    const double* qx = X64 + (uint64_t)qid * n;
+    const uint64_t b = N * part / P, e = N * (part + 1) / P;
+    uint32_t cnt = 0;
+    for (uint64_t t = b + lane; t < e; t += 32) {
+        if (t == qid) continue;
+        const double s = exact_sq(qx, X64 + t * n, n);
+        const uint32_t ti = (uint32_t)t;
+        if (cnt == K && !pair_less(s, ti, ls[(K - 1) * 32 + lane], li[(K - 1) * 32 + lane]))
+            continue;
+        int r = (int)(cnt < K ? cnt : K - 1);
+        while (r > 0 && pair_less(s, ti, ls[(r - 1) * 32 + lane], li[(r - 1) * 32 + lane])) {
+            ls[r * 32 + lane] = ls[(r - 1) * 32 + lane];
+            li[r * 32 + lane] = li[(r - 1) * 32 + lane];
+            --r;
+        }
+        ls[r * 32 + lane] = s;
+        li[r * 32 + lane] = ti;
+        if (cnt < K) ++cnt;
+    }
+    uint32_t total = cnt;
+    for (int o = 16; o > 0; o >>= 1) total += __shfl_xor_sync(0xffffffffu, total, o);
+    const uint32_t outn = min(total, K);
+    const uint64_t v = blockIdx.x;  // = q * P + part
+    uint32_t head = 0;
+    for (uint32_t r = 0; r < outn; ++r) {
+        const double s = head < cnt ? ls[head * 32 + lane] : CUDART_INF;
+        const uint32_t t = head < cnt ? li[head * 32 + lane] : 0xFFFFFFFFu;
+        double bs = s;
+        uint32_t bt = t;
+        for (int o = 16; o > 0; o >>= 1) {
+            const double s2 = __shfl_xor_sync(0xffffffffu, bs, o);
+            const uint32_t t2 = __shfl_xor_sync(0xffffffffu, bt, o);
+            if (pair_less(s2, t2, bs, bt)) {
+                bs = s2;
+                bt = t2;
+            }
+        }
+        if (head < cnt && t == bt) ++head;
+        if (lane == 0) {
+            t_ids[v * K + r] = bt;
+            t_sq[v * K + r] = bs;
+        }
+    }
+    if (lane == 0) t_count[v] = outn;
+}
+void launch_brute_parts(const double* X64, uint64_t N, uint32_t n, const uint32_t* qpid,
+                        uint64_t nq, uint32_t P, uint32_t K, uint32_t* t_ids, double* t_sq,
+                        uint32_t* t_count, cudaStream_t s) {
+    if (!nq) return;
+    const size_t sm = (size_t)K * 32 * (sizeof(double) + sizeof(uint32_t));
+    set_smem(k_brute_parts, sm);
+    k_brute_parts<<<(unsigned)(nq * P), 32, sm, s>>>(X64, N, n, qpid, P, K, t_ids, t_sq, t_count);
+    KJ_CUDA(cudaGetLastError());
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+
 // FP64 rows in a level's position order (same values, contiguous per cell)
 __global__ void k_rows_by(const double* X64, const uint32_t* A, uint64_t N, uint32_t n, double* out) {
     const uint64_t total = N * n;

@@ -246,3 +246,27 @@ def test_sweep_order_identical(engine, oracle, spec, N, n, k):
     q = np.random.default_rng(6).choice(N, 48, replace=False).astype(np.uint32)
     oi, od = oracle.brute_knn(W, q, k)
     assert np.array_equal(b.ids[q], oi) and np.array_equal(b.dist[q], od)
+
+
+@pytest.mark.parametrize("spec,N,n,k", [("clusters:16:0.05", 70000, 18, 32), ("mixture", 80000, 5, 8),
+                                        ("uniform", 70000, 3, 20)])
+def test_brute_fallback_identical(engine, oracle, spec, N, n, k):
+    """A small fallback set (<= 64 rows) is solved by brute force over all points
+    instead of a grid level; rows, distances and provenance are unchanged."""
+    X = generate(spec, N, n, 43)
+    cfg = RunConfig(k=k, mode="hybrid", seed=43)
+    out = []
+    for o in (0, 1):
+        engine.set_option("brute_fallback", o)
+        engine.set_points(X)
+        out.append(engine.run(cfg, want_hist=False))
+    engine.set_option("brute_fallback", 0)
+    a, b = out
+    assert np.array_equal(a.ids, b.ids) and np.array_equal(a.dist, b.dist)
+    assert np.array_equal(a.provenance, b.provenance)
+    assert a.info["failed_count"] == b.info["failed_count"]
+    W = X[:, b.info["perm"]]
+    fb = np.flatnonzero(b.provenance != 0)[:16].astype(np.uint32)
+    q = np.concatenate([fb, np.random.default_rng(2).choice(N, 16, replace=False).astype(np.uint32)])
+    oi, od = oracle.brute_knn(W, q, k)
+    assert np.array_equal(b.ids[q], oi) and np.array_equal(b.dist[q], od)
