@@ -964,9 +964,11 @@ struct knnj_ctx {
     // tcgen05 join (n <= 20): 64-candidate tiles, 4 early-released buffers. Off: 646 ms vs
     // 540 ms for 128-candidate tiles on C2.
     bool tile64 = false;
-    uint32_t tc_slack = 24;
-    bool finalize_xj = true;
-    bool brute_fallback = false;  // <= 64 fallback rows: brute force over all points (off: 16.6 vs 8.3 ms on C2)  // finalize reads FP64 rows from a join-ordered copy  // tcgen05 join list capacity K + slack (compaction when full)
+    uint32_t tc_slack = 24;       // tcgen05 join list capacity K + slack (compaction when full)
+    bool finalize_xj = true;      // finalize reads FP64 rows from a join-ordered copy
+    // <= 64 fallback rows: brute force over all points. Off: 16.6 ms vs 8.3 ms through a
+    // grid level on C2 (64 warps cannot hide the FP64 row loads)
+    bool brute_fallback = false;
     // Fine cascade ahead of level 0 (widths eps * f / 1000, coarsest first is NOT
     // required: each is tried on the rows still uncertified). 0 = off.
     uint32_t fine_f[2] = {0, 0};
