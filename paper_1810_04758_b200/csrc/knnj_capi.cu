@@ -29,6 +29,7 @@
 using namespace kj;
 
 namespace kj {
+void draw_pairs_fast(uint64_t N, uint64_t pairs, uint64_t seed, uint64_t* ij);  // knnj_rng.cpp
 cudaStream_t& alloc_stream() {
     static thread_local cudaStream_t s = nullptr;
     return s;
@@ -293,6 +294,7 @@ struct knnj_ctx {
 
     ~knnj_ctx() {
         if (h_sq) cudaFreeHost(h_sq);
+        if (h_ij) cudaFreeHost(h_ij);
         if (s) cudaStreamDestroy(s);
     }
 
@@ -451,21 +453,30 @@ struct knnj_ctx {
             return ij;
         }
         ij.resize(2 * sample_pairs);
-        std::mt19937_64 rng(seed);
-        std::uniform_int_distribution<uint64_t> pick(0, N - 1);
-        for (uint64_t p = 0; p < sample_pairs; ++p) {
-            uint64_t i = pick(rng);
-            uint64_t j = pick(rng);
-            while (j == i) j = pick(rng);
-            ij[2 * p] = i;
-            ij[2 * p + 1] = j;
-        }
+        draw_pairs_into(N, sample_pairs, seed, ij.data());
         return ij;
+    }
+    // the sampled (non-exhaustive) stream straight into caller memory (e.g. pinned)
+    // (block-generated engine: knnj_rng.hpp, the same stream as std::mt19937_64 +
+    // std::uniform_int_distribution, 3-5x faster; tests/test_rng.py)
+    static void draw_pairs_into(uint64_t N, uint64_t sample_pairs, uint64_t seed, uint64_t* ij) {
+        draw_pairs_fast(N, sample_pairs, seed, ij);
+    }
+    uint64_t* h_ij = nullptr;  // pinned pair indices (knnj_run's eps_mean draw)
+    uint64_t h_ij_cap = 0;
+    uint64_t* pinned_pairs(uint64_t pairs) {
+        if (h_ij_cap < pairs) {
+            if (h_ij) cudaFreeHost(h_ij);
+            h_ij = nullptr;
+            KJ_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&h_ij), 16 * pairs, cudaHostAllocDefault));
+            h_ij_cap = pairs;
+        }
+        return h_ij;
     }
     double* h_sq = nullptr;  // pinned staging for the per-pair distances
     uint64_t h_sq_cap = 0;
-    double eps_mean_of(const std::vector<uint64_t>& ij) {
-        const uint64_t used = ij.size() / 2;
+    double eps_mean_of(const std::vector<uint64_t>& ij) { return eps_mean_of(ij.data(), ij.size() / 2); }
+    double eps_mean_of(const uint64_t* ij, uint64_t used) {
         if (!used) throw Error(1, "sample_pairs must be at least 1");
         if (h_sq_cap < used) {
             if (h_sq) cudaFreeHost(h_sq);
@@ -477,7 +488,7 @@ struct knnj_ctx {
         DBuf<double> d_out;
         d_ij.ensure(2 * used);
         d_out.ensure(used);
-        KJ_CUDA(cudaMemcpyAsync(d_ij.p, ij.data(), 16 * used, cudaMemcpyHostToDevice, s));
+        KJ_CUDA(cudaMemcpyAsync(d_ij.p, ij, 16 * used, cudaMemcpyHostToDevice, s));
         launch_pair_sq(X64.p, n, d_ij.p, used, kInf, d_out.p, s);
         KJ_CUDA(cudaMemcpyAsync(h_sq, d_out.p, 8 * used, cudaMemcpyDeviceToHost, s));
         sync();
@@ -2370,13 +2381,22 @@ static void run_impl(knnj_ctx* c, const knnj_config* cfg, uint32_t shard, uint32
     // host-side reference RNG streams (pairs for eps_mean, the histogram's query sample)
     // drawn on a helper thread while the GPU reorders and orders the candidates
     const bool sampling = cfg->mode == KNNJ_HYBRID || cfg->mode == KNNJ_DENSE_ONLY;
+    // (two independent streams: one thread each, so eps_mean waits only for its pairs)
     std::vector<uint64_t> eps_ij, hist_q;
-    std::thread drawer;
+    uint64_t* eps_pin = nullptr;  // pinned pairs (sampled case)
+    uint64_t eps_pin_n = 0;
+    std::thread drawer, hdrawer;
     if (sampling && N >= 2) {
         knnj_ctx::histogram_sample_size(N, cfg->hist_query_fraction);  // validates the fraction here
-        drawer = std::thread([&] {
-            eps_ij = knnj_ctx::draw_pairs(N, std::min<uint64_t>(10 * N, cfg->eps_mean_pair_cap),
-                                          derive_seed(cfg->seed, 1));
+        const uint64_t pairs = std::min<uint64_t>(10 * N, cfg->eps_mean_pair_cap);
+        uint64_t* pin = pairs < N * (N - 1) ? c->pinned_pairs(pairs) : nullptr;
+        drawer = std::thread([&, pairs, pin] {
+            if (pin) knnj_ctx::draw_pairs_into(N, pairs, derive_seed(cfg->seed, 1), pin);
+            else eps_ij = knnj_ctx::draw_pairs(N, pairs, derive_seed(cfg->seed, 1));
+        });
+        eps_pin = pin;
+        eps_pin_n = pin ? pairs : 0;
+        hdrawer = std::thread([&] {
             hist_q = knnj_ctx::draw_histogram_sample(N, cfg->hist_query_fraction,
                                                      derive_seed(cfg->seed, 2));
         });
@@ -2386,7 +2406,7 @@ static void run_impl(knnj_ctx* c, const knnj_config* cfg, uint32_t shard, uint32
         ~Joiner() {
             if (t.joinable()) t.join();
         }
-    } joiner{drawer};
+    } joiner{drawer}, hjoiner{hdrawer};
     {
         Timer t(s);
         c->reorder(m);
@@ -2481,7 +2501,7 @@ static void run_impl(knnj_ctx* c, const knnj_config* cfg, uint32_t shard, uint32
             if (N < 2) throw Error(1, "eps_mean estimation needs at least two points");
             if (c->use_tc_hist()) c->ensure_hist_order(c->tc_row_halfs());  // overlaps the draw
             if (drawer.joinable()) drawer.join();
-            I.eps_mean = c->eps_mean_of(eps_ij);
+            I.eps_mean = eps_pin ? c->eps_mean_of(eps_pin, eps_pin_n) : c->eps_mean_of(eps_ij);
             I.ms_eps_mean = t.ms();
             trace().mark("run: eps_mean");
         }
@@ -2491,6 +2511,7 @@ static void run_impl(knnj_ctx* c, const knnj_config* cfg, uint32_t shard, uint32
         uint32_t valid = cfg->n_bins;
         {
             Timer t(s);
+            if (hdrawer.joinable()) hdrawer.join();
             auto& hq = hist_q;
             I.hist_query_count = hq.size();
             valid = c->hist_for_selection(hq, shard, nshard, I.eps_mean, cfg->n_bins, target_beta,

@@ -217,26 +217,45 @@ __device__ __forceinline__ float warp_kth(float (&a)[R], uint32_t k) {
 __global__ void k_prep_tc(const double* X64, const uint32_t* A, uint64_t N, uint32_t n,
                           const double* g, double inv_S, uint32_t row_halfs, uint32_t split,
                           __half* Bh) {
+    // one thread per row; the row is emitted as 16-byte chunks of 8 halfs, so a warp
+    // writes whole 128-byte rows instead of scattered 2-byte stores
     for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < N;
          i += uint64_t(gridDim.x) * blockDim.x) {
         const double* x = X64 + (uint64_t)A[i] * n;
-        __half* row = Bh + i * row_halfs;
         double nb = 0.0;
         for (uint32_t d = 0; d < n; ++d) {
             const double v = (x[d] - g[d]) * inv_S;
-            const __half hi = __double2half(v);
-            row[d] = hi;
-            if (split == 3) {
-                row[n + d] = __double2half(v - (double)__half2float(hi));
-                row[2 * n + d] = hi;
-            }
             nb += v * v;
         }
-        const uint32_t o = split * n;
         const __half nh = __double2half(nb);
-        row[o] = nh;
-        row[o + 1] = __double2half(nb - (double)__half2float(nh));
-        for (uint32_t c = o + 2; c < row_halfs; ++c) row[c] = __float2half(0.f);
+        const __half nl = __double2half(nb - (double)__half2float(nh));
+        const uint32_t o = split * n;
+        uint4* row = reinterpret_cast<uint4*>(Bh + i * row_halfs);
+        for (uint32_t c0 = 0; c0 < row_halfs; c0 += 8) {
+            uint32_t w[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                uint32_t pair = 0;
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const uint32_t k = c0 + 2 * e + h;
+                    __half hv = __float2half(0.f);
+                    if (k < o) {
+                        const uint32_t d = k % n, part = k / n;  // split 3: hi | lo | hi
+                        const double v = (x[d] - g[d]) * inv_S;
+                        const __half hi = __double2half(v);
+                        hv = part == 1 ? __double2half(v - (double)__half2float(hi)) : hi;
+                    } else if (k == o) {
+                        hv = nh;
+                    } else if (k == o + 1) {
+                        hv = nl;
+                    }
+                    pair |= (uint32_t)__half_as_ushort(hv) << (16 * h);
+                }
+                w[e] = pair;
+            }
+            row[c0 / 8] = make_uint4(w[0], w[1], w[2], w[3]);
+        }
     }
 }
 
