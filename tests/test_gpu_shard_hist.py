@@ -27,17 +27,21 @@ CASES = [  # (spec, |D|, n, k, m, beta, seed)
 ]
 
 
+@pytest.mark.parametrize("pilot_cap", [1, 0])
 @pytest.mark.parametrize("case", CASES, ids=[f"{c[0]}-{c[2]}d-k{c[3]}" for c in CASES])
-def test_capped_histogram_selects_same_eps(engine, oracle, case):
+def test_capped_histogram_selects_same_eps(engine, oracle, case, pilot_cap):
+    """pilot_cap: the pilot slice itself first bins only the lowest third of the bins."""
     spec, N, n, k, m, beta, seed = case
     X = generate(spec, N, n, seed)
     o = oracle.run(X, k=k, m=m, beta=beta, mode="hybrid", seed=seed)
     engine.set_option("hist_cap", 2)
+    engine.set_option("pilot_cap", pilot_cap)
     try:
         engine.set_points(X)
         r = engine.run(RunConfig(k=k, m=m, beta=beta, mode="hybrid", seed=seed), want_hist=False)
     finally:
         engine.set_option("hist_cap", 1)
+        engine.set_option("pilot_cap", 0)
     assert r.info["eps_used"] == o["eps_used"]
     assert r.info["eps_default"] == o["eps_default"]
     assert np.array_equal(r.ids, o["ids"]) and np.array_equal(r.dist, o["dist"])
