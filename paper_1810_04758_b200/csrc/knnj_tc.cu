@@ -311,7 +311,8 @@ __global__ void __launch_bounds__(64 + 128 * G * H, 1)
     unsigned char* sA = base;                                   // G x KB x 16 KB
     unsigned char* sB = sA + G * KB * KB_BYTES;                 // STAGES x KB x BK
     unsigned char* tail = sB + STAGES * KB * BK;
-    __shared__ uint64_t bar_full[STAGES], bar_empty[STAGES], bar_accf[NB], bar_acce[NB];
+    // accumulator barriers per (query group, buffer): the groups' pipelines are decoupled
+    __shared__ uint64_t bar_full[STAGES], bar_empty[STAGES], bar_accf[G * NB], bar_acce[G * NB];
     __shared__ uint32_t s_tmem;
     __shared__ float s_cut[H == 2 ? 2 * NQ : 1];  // H=2: per (half, query) current cut
 
@@ -329,11 +330,11 @@ __global__ void __launch_bounds__(64 + 128 * G * H, 1)
     if (tid == 32) {
         for (int i = 0; i < STAGES; ++i) {
             mbar_init(&bar_full[i], 1);
-            mbar_init(&bar_empty[i], 1);
+            mbar_init(&bar_empty[i], G);  // one MMA commit per query group
         }
-        for (int i = 0; i < NB; ++i) {
+        for (int i = 0; i < G * NB; ++i) {
             mbar_init(&bar_accf[i], 1);
-            mbar_init(&bar_acce[i], 4 * G * H);
+            mbar_init(&bar_acce[i], 4 * H);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
@@ -468,29 +469,27 @@ __global__ void __launch_bounds__(64 + 128 * G * H, 1)
         }
     } else if (warp == 1) {
         // ------------------------------------------------ MMA issuer
-        if (lane == 0) {
+        // one issuing lane per query group: a group whose epilogue is in its rare path
+        // holds only its own accumulators; the other runs ahead within the stage ring
+        if (lane < G) {
+            const int gg = lane;
             uint32_t s, c;
             const uint32_t a0 = smem_u32(sA);
             for (uint32_t t = 0; next_tile(s, c); ++t) {
                 const int st = t % STAGES, b = t % NB;
                 mbar_wait(&bar_full[st], (t / STAGES) & 1);
-                mbar_wait(&bar_acce[b], ((t / NB) & 1) ^ 1);
+                mbar_wait(&bar_acce[gg * NB + b], ((t / NB) & 1) ^ 1);
                 fence_after();
                 const uint32_t b0 = smem_u32(sB + st * KB * BK);
+                const uint32_t dcol = tmem + (gg * NB + b) * TN;
 #pragma unroll
-                for (int gg = 0; gg < G; ++gg) {
-                    const uint32_t dcol = tmem + (gg * NB + b) * TN;
+                for (int kb = 0; kb < KB; ++kb)
 #pragma unroll
-                    for (int kb = 0; kb < KB; ++kb)
-#pragma unroll
-                        for (int kk = 0; kk < KBLK / 16; ++kk)
-                            umma_f16<TN>(dcol,
-                                         umma_desc_sw128(a0 + (gg * KB + kb) * KB_BYTES + kk * 32),
-                                         umma_desc_sw128(b0 + kb * BK + kk * 32),
-                                         (kb | kk) ? 1u : 0u);
-                }
+                    for (int kk = 0; kk < KBLK / 16; ++kk)
+                        umma_f16<TN>(dcol, umma_desc_sw128(a0 + (gg * KB + kb) * KB_BYTES + kk * 32),
+                                     umma_desc_sw128(b0 + kb * BK + kk * 32), (kb | kk) ? 1u : 0u);
                 umma_commit(&bar_empty[st]);
-                umma_commit(&bar_accf[b]);
+                umma_commit(&bar_accf[gg * NB + b]);
             }
         }
     } else if (!HIST) {
@@ -574,7 +573,7 @@ __global__ void __launch_bounds__(64 + 128 * G * H, 1)
         unsigned long long st_slab = 0, st_rare = 0, st_bits = 0, st_ins = 0, st_cmp = 0;
         for (uint32_t t = 0; next_tile(s, c); ++t) {
             const int b = t % NB;
-            mbar_wait(&bar_accf[b], (t / NB) & 1);
+            mbar_wait(&bar_accf[g * NB + b], (t / NB) & 1);
             fence_after();
             const uint32_t tbase = tmem + ((uint32_t)(quarter * 32) << 16) + (g * NB + b) * TN;
             if (H == 2 && has_q && !ovf) {  // the partner's tighter cut applies to new inserts
@@ -596,7 +595,7 @@ __global__ void __launch_bounds__(64 + 128 * G * H, 1)
                 }
                 fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&bar_acce[b]);
+                if (lane == 0) mbar_arrive(&bar_acce[g * NB + b]);
                 continue;
             }
             for (uint32_t j0 = H == 2 ? hh * 64 : 0; j0 < c; j0 += H == 2 ? 128 : 64) {
@@ -605,7 +604,7 @@ __global__ void __launch_bounds__(64 + 128 * G * H, 1)
                 if (ER) {  // the whole (64-column) tile is in registers: free the buffer
                     fence_before();
                     __syncwarp();
-                    if (lane == 0) mbar_arrive(&bar_acce[b]);
+                    if (lane == 0) mbar_arrive(&bar_acce[g * NB + b]);
                 }
                 if (p.dbg && blockIdx.x == 0 && t == 0 && g == 0)
 #pragma unroll
@@ -679,7 +678,7 @@ __global__ void __launch_bounds__(64 + 128 * G * H, 1)
             if (!ER) {
                 fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&bar_acce[b]);
+                if (lane == 0) mbar_arrive(&bar_acce[g * NB + b]);
             }
         }
         if (p.stats && lane == 0) {
@@ -738,7 +737,7 @@ __global__ void __launch_bounds__(64 + 128 * G * H, 1)
         uint32_t s, c;
         for (uint32_t t = 0; next_tile(s, c); ++t) {
             const int b = t % NB;
-            mbar_wait(&bar_accf[b], (t / NB) & 1);
+            mbar_wait(&bar_accf[g * NB + b], (t / NB) & 1);
             fence_after();
             const uint32_t tbase = tmem + ((uint32_t)(quarter * 32) << 16) + (g * NB + b) * TN;
             for (uint32_t j0 = 0; j0 < c; j0 += 64) {
@@ -844,7 +843,7 @@ __global__ void __launch_bounds__(64 + 128 * G * H, 1)
             }
             fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&bar_acce[b]);
+            if (lane == 0) mbar_arrive(&bar_acce[g * NB + b]);
         }
         flush();
     }
