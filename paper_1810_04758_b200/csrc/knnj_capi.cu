@@ -758,9 +758,11 @@ struct knnj_ctx {
     // >= target there, so lower_bound selects the same bin as with the full histogram.
     // If the capped counts fall short, the rest is re-binned in full.
     int hist_cap_mode = 1;  // 0: never cap, 1: cap when the histogram is large, 2: always
-    // the pilot first bins only the lowest third of the bins. Off: on C2 the capped pilot
-    // screens 6.5e9 of 7.8e9 pairs and its per-column path runs 19.7 ms vs 15.8 ms
-    bool pilot_cap = false;
+    // The pilot first bins only the lowest quarter of the bins (0 never, 1 always, 2 when
+    // n <= 8). Low-dim data is where the box filter at that radius drops most pairs: C5
+    // pilot 7.1 s over 3.1e12 pairs in full. In 18-D (C2) the capped pilot still screens
+    // 6.5e9 of 7.8e9 pairs and its per-column path is slower (19.7 vs 15.8 ms).
+    int pilot_cap = 2;
     double last_hist_ms_pilot = 0.0;
     uint32_t hist_for_selection(const std::vector<uint64_t>& hq, uint32_t shard, uint32_t nshard,
                                 double em, uint32_t nb, double target, bool full,
@@ -780,7 +782,8 @@ struct knnj_ctx {
             last_hist_kernel_ms = kms;
             return nb;
         }
-        constexpr uint64_t STRIDE = 32;
+        // pilot: every STRIDE-th sampled query, at most ~8k of them (enough to place the cap)
+        const uint64_t STRIDE = std::max<uint64_t>(32, nq / 8192);
         std::vector<uint64_t> pilot, rest;
         for (uint64_t i = lo; i < hi; ++i) (i % STRIDE == 0 ? pilot : rest).push_back(hq[i]);
         const uint64_t npilot = (nq + STRIDE - 1) / STRIDE;  // over all shards
@@ -796,7 +799,8 @@ struct knnj_ctx {
             }
             return nb + 1;  // not found inside the counted bins
         };
-        const uint32_t pcap = pilot_cap ? std::max<uint32_t>(8, nb / 3) : nb;
+        const bool pc = pilot_cap == 1 || (pilot_cap == 2 && n <= 8);
+        const uint32_t pcap = pc ? std::max<uint32_t>(8, nb / 4) : nb;
         uint32_t bcap = nb + 1;
         bool pilot_partial = false;
         if (pcap < nb) {
@@ -1983,7 +1987,8 @@ int knnj_set_option(knnj_ctx* c, const char* name, int64_t value) {
         } else if (k == "sweep_order") {
             c->sweep_order = value != 0;
         } else if (k == "pilot_cap") {
-            c->pilot_cap = value != 0;
+            if (value < 0 || value > 2) throw Error(1, "pilot_cap must be 0, 1 or 2");
+            c->pilot_cap = (int)value;
         } else if (k == "brute_fallback") {
             c->brute_fallback = value != 0;
         } else if (k == "finalize_xj") {

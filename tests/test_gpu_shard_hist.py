@@ -41,7 +41,7 @@ def test_capped_histogram_selects_same_eps(engine, oracle, case, pilot_cap):
         r = engine.run(RunConfig(k=k, m=m, beta=beta, mode="hybrid", seed=seed), want_hist=False)
     finally:
         engine.set_option("hist_cap", 1)
-        engine.set_option("pilot_cap", 0)
+        engine.set_option("pilot_cap", 2)
     assert r.info["eps_used"] == o["eps_used"]
     assert r.info["eps_default"] == o["eps_default"]
     assert np.array_equal(r.ids, o["ids"]) and np.array_equal(r.dist, o["dist"])
