@@ -1224,11 +1224,18 @@ struct knnj_ctx {
         // items are in cell order here; a shard keeps a contiguous run of them
         uint64_t i0 = 0, i1 = tot;
         if (nshard > 1) {
-            // cost of an item ~ its candidate tiles (+ a fixed per-item overhead)
+            // cost of an item ~ its candidate tiles (+ a fixed per-item overhead); with the
+            // box filter on, the tiles that survive it (every rank counts all items: the
+            // unfiltered count misjudges cells whose neighbourhood holds far clusters)
             std::vector<double> cost(tot);
+            std::vector<uint32_t> kept;
+            if (filter_r2 > 0.0 && box_filter && tot)
+                kept = filtered_blocks(lv, items_unsorted.p, tot, P.qpos.p, P.adj.p, filter_r2);
             for (uint64_t i = 0; i < tot; ++i) {
                 const uint32_t q = h_items[i].y - h_items[i].x;
-                cost[i] = (q ? double(h_work[i] / q) : 0.0) + 8.0 * 128.0;
+                const double cand = kept.empty() ? (q ? double(h_work[i] / q) : 0.0)
+                                                 : double(kept[i]) * double(FB);
+                cost[i] = cand + 8.0 * 128.0;
             }
             shard_range(cost.data(), tot, shard, nshard, &i0, &i1);
         }
@@ -1401,6 +1408,30 @@ struct knnj_ctx {
         }
         P.screened = filter_items(P.items.p, P.nitems, P.qpos.p, lv.J.p, lv.bbox.p, P.adj, P.nadj, r2,
                                   sweep_order);
+    }
+    // kept FB-blocks per item under the box filter (the filter's count pass only; items and
+    // adj are left unchanged)
+    std::vector<uint32_t> filtered_blocks(Level& lv, uint4* items, uint64_t nitems,
+                                          const uint32_t* qpos, const uint2* adj, double r2) {
+        if (!lv.bbox_ready) {
+            lv.bbox.ensure(((N + FB - 1) / FB) * 2 * n);
+            launch_block_boxes(X64.p, lv.J.p, N, n, lv.bbox.p, s);
+            lv.bbox_ready = true;
+        }
+        const uint64_t nblk = (N + FB - 1) / FB;
+        const float r2c = f32_round_up(r2 * (1.0 + 1e-9));
+        DBuf<float> qbox, okey;
+        DBuf<uint32_t> cnt;
+        qbox.ensure(nitems * 2 * n);
+        cnt.ensure(nitems);
+        okey.ensure(1);
+        launch_item_boxes(items, nitems, qpos, lv.J.p, X64.p, n, qbox.p, s);
+        launch_filter_ranges(items, nitems, qbox.p, n, adj, lv.bbox.p, nblk, r2c, cnt.p, nullptr,
+                             nullptr, nullptr, false, s, okey.p);  // ORDER count: kept blocks
+        std::vector<uint32_t> h(nitems);
+        KJ_CUDA(cudaMemcpyAsync(h.data(), cnt.p, 4 * nitems, cudaMemcpyDeviceToHost, s));
+        sync();
+        return h;
     }
     // items (qbeg, qend, abeg, aend) over adjacency ranges adj: keep only the blocks within
     // sqrt(r2) of the item's query box; adj is replaced. Returns the kept candidate pairs.
