@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define KNNJ_ABI_VERSION 3
+#define KNNJ_ABI_VERSION 4
 
 enum knnj_status {
     KNNJ_OK = 0,
@@ -198,6 +198,26 @@ typedef struct {
  * k_effective = min(k, |D|-1) (orchestrator.cpp:77-82). */
 int knnj_run(knnj_ctx* ctx, const knnj_config* cfg, uint32_t* ids, double* dist, uint8_t* prov,
              uint64_t* raw_hist, knnj_run_info* info);
+
+/* ---- parameter search (parameter_search, proj/src/orchestrator.cpp:252-303) ----
+ * Draws a seeded f-fraction query subset (derive_seed(seed, kSeedQuerySubset = 4),
+ * sample_without_replacement), runs knnj_run over it for each (beta, gamma) candidate
+ * in hybrid mode at rho = 0.5 with base's other settings, and returns the fastest
+ * candidate. wall_seconds is the run's device time (knnj_run_info.ms_total). A failing
+ * candidate keeps its error (status, message) and does not stop the search. Errors,
+ * with the reference's messages: f outside (0, 1] or no candidates -> KNNJ_E_USAGE;
+ * floor(f|D|) < 50 -> KNNJ_E_SAMPLE_TOO_SMALL; every candidate failed -> KNNJ_E_USAGE.
+ * (t1/t2/rho_model of the reference are its CPU load-balance model: no analogue.) */
+typedef struct {
+    double beta, gamma;
+    double wall_seconds;
+    int32_t status;               /* KNNJ_OK or the candidate's error code */
+    char error[256];              /* the candidate's error message ("" if none) */
+} knnj_search_row;
+
+int knnj_parameter_search(knnj_ctx* ctx, const knnj_config* base, double f, const double* betas,
+                          const double* gammas, uint64_t n_candidates, knnj_search_row* rows,
+                          double* best_beta, double* best_gamma);
 
 /* ---- multi-GPU: one process per GPU, queries sharded by cell range ------
  * Sum `count` u64 values element-wise over every shard, in place (e.g. an

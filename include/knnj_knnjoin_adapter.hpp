@@ -27,7 +27,9 @@
 #include <cstring>
 #include <stdexcept>
 #include <memory>
+#include <span>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "knnj_c.h"
@@ -186,6 +188,49 @@ inline knnjoin::KnnRunResult run_hybrid(Engine& eng, const knnjoin::Dataset& d,
     r.timings.reassign = info->ms_fallback * 1e-3;
     r.timings.measured_total = info->ms_total * 1e-3;
     return r;
+}
+
+// knnjoin::parameter_search (proj/include/knnjoin/orchestrator.hpp:116-118,
+// proj/src/orchestrator.cpp:252-303) on the GPU: the same seeded query subset and
+// candidate runs (hybrid, rho = 0.5); wall_seconds is the device run time. t1/t2/
+// rho_model (the CPU load-balance model) stay empty.
+inline knnjoin::ParameterSearchResult parameter_search(
+    Engine& eng, const knnjoin::Dataset& d, std::size_t k, double f,
+    std::span<const std::pair<double, double>> candidates, const knnjoin::RunConfig& base) {
+    knnj_ctx* ctx = eng.get();
+    eng.check(knnj_set_points(ctx, d.raw().data(), d.size(), (uint32_t)d.dims()));
+    knnj_config c{};
+    c.k = (uint32_t)k;
+    c.m = (uint32_t)base.m;
+    c.beta = base.beta;
+    c.gamma = base.gamma;
+    c.rho = base.rho;
+    c.mode = KNNJ_HYBRID;
+    c.n_bins = (uint32_t)base.n_bins;
+    c.hist_query_fraction = base.hist_query_fraction;
+    c.eps_mean_pair_cap = base.eps_mean_pair_cap;
+    c.seed = base.seed;
+    std::vector<double> betas, gammas;
+    for (const auto& [b, g] : candidates) {
+        betas.push_back(b);
+        gammas.push_back(g);
+    }
+    std::vector<knnj_search_row> rows(std::max<std::size_t>(1, candidates.size()));
+    double bb = 0.0, bg = 0.0;
+    eng.check(knnj_parameter_search(ctx, &c, f, betas.data(), gammas.data(), candidates.size(),
+                                    rows.data(), &bb, &bg));
+    knnjoin::ParameterSearchResult out;
+    out.best_beta = bb;
+    out.best_gamma = bg;
+    for (std::size_t i = 0; i < candidates.size(); ++i) {
+        knnjoin::CandidateOutcome o;
+        o.beta = rows[i].beta;
+        o.gamma = rows[i].gamma;
+        o.wall_seconds = rows[i].wall_seconds;
+        o.error = rows[i].error;
+        out.candidates.push_back(std::move(o));
+    }
+    return out;
 }
 
 }  // namespace knnjoin_b200

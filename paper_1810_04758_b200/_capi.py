@@ -126,6 +126,17 @@ SIGNATURES.append(
     ("knnj_run_shard", C.c_int, [_vp, C.POINTER(Config), C.c_uint32, C.c_uint32, ALLREDUCE_FN,
                                  _vp, _vp, _vp, _vp, _vp, _vp, C.POINTER(RunInfo)]))
 
+class SearchRow(C.Structure):
+    """knnj_search_row (include/knnj_c.h): one parameter-search candidate."""
+    _fields_ = [("beta", C.c_double), ("gamma", C.c_double), ("wall_seconds", C.c_double),
+                ("status", C.c_int32), ("error", C.c_char * 256)]
+
+
+SIGNATURES.append(
+    ("knnj_parameter_search", C.c_int, [_vp, C.POINTER(Config), C.c_double, _dp, _dp, C.c_uint64,
+                                        C.POINTER(SearchRow), C.POINTER(C.c_double),
+                                        C.POINTER(C.c_double)]))
+
 SIGNATURES += [
     ("knnj_io_last_error", C.c_char_p, []),
     ("knnj_tsv_format", C.c_int, [_vp, _vp, _vp, C.c_uint64, C.c_uint32, _vp, C.c_uint64,

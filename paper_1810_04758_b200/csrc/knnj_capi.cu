@@ -2831,6 +2831,63 @@ int knnj_run(knnj_ctx* c, const knnj_config* cfg, uint32_t* ids, double* dist, u
     });
 }
 
+int knnj_parameter_search(knnj_ctx* c, const knnj_config* base, double f, const double* betas,
+                          const double* gammas, uint64_t n_candidates, knnj_search_row* rows,
+                          double* best_beta, double* best_gamma) {
+    // parameter_search, proj/src/orchestrator.cpp:252-303
+    return guarded(c, [&] {
+        if (!c || !base || !best_beta || !best_gamma || (n_candidates && (!betas || !gammas || !rows)))
+            throw Error(1, "null argument");
+        if (!(f > 0.0) || f > 1.0) throw Error(1, "query fraction f must be in (0, 1]");
+        if (n_candidates == 0) throw Error(1, "parameter search needs at least one candidate");
+        const uint64_t want = (uint64_t)std::floor(f * double(c->N));
+        if (want < 50)
+            throw Error(7, "parameter search sample of " + std::to_string(want) +
+                               " queries is below the floor of 50");
+        std::mt19937_64 rng(derive_seed(base->seed, 0x04));  // kSeedQuerySubset
+        const std::vector<uint64_t> picked = sample_without_replacement(c->N, want, rng);
+        const std::vector<uint32_t> subset(picked.begin(), picked.end());
+        bool have = false;
+        double best = 0.0;
+        for (uint64_t i = 0; i < n_candidates; ++i) {
+            knnj_config cfg = *base;
+            cfg.mode = KNNJ_HYBRID;
+            cfg.beta = betas[i];
+            cfg.gamma = gammas[i];
+            cfg.rho = 0.5;  // the reference's starting balance
+            cfg.query_subset = subset.data();
+            cfg.n_query_subset = subset.size();
+            knnj_search_row& row = rows[i];
+            row = knnj_search_row{};
+            row.beta = betas[i];
+            row.gamma = gammas[i];
+            auto fail = [&](int code, const char* msg) {
+                row.status = code;
+                std::snprintf(row.error, sizeof row.error, "%s", msg);
+            };
+            try {
+                auto info = std::make_unique<knnj_run_info>();
+                run_impl(c, &cfg, 0, 1, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+                         nullptr, info.get());
+                row.wall_seconds = info->ms_total / 1000.0;
+                if (!have || row.wall_seconds < best) {
+                    have = true;
+                    best = row.wall_seconds;
+                    *best_beta = row.beta;
+                    *best_gamma = row.gamma;
+                }
+            } catch (const kj::Error& e) {
+                fail(e.code, e.what());
+            } catch (const std::exception& e) {
+                fail(KNNJ_E_CUDA, e.what());
+            }
+            alloc_stream() = c->s;
+            alloc_cache() = &c->cache;
+        }
+        if (!have) throw Error(1, "every parameter-search candidate failed");
+    });
+}
+
 int knnj_run_shard(knnj_ctx* c, const knnj_config* cfg, uint32_t shard_index,
                    uint32_t shard_count, knnj_allreduce_fn allreduce, void* allreduce_user,
                    uint32_t* ids, double* dist, uint8_t* prov, uint32_t* owned_queries,

@@ -304,6 +304,50 @@ class Engine:
                             k_effective=k_eff, info=d, raw_hist=raw, warnings=warnings)
 
 
+@dataclasses.dataclass
+class CandidateOutcome:
+    """CandidateOutcome, proj/include/knnjoin/orchestrator.hpp:96-102."""
+    beta: float
+    gamma: float
+    wall_seconds: float
+    error: str = ""
+    t1: Optional[float] = None       # the reference's CPU load-balance model: no analogue
+    t2: Optional[float] = None
+
+
+@dataclasses.dataclass
+class ParameterSearchResult:
+    """ParameterSearchResult, proj/include/knnjoin/orchestrator.hpp:104-110."""
+    best_beta: float
+    best_gamma: float
+    candidates: list
+    t1: Optional[float] = None
+    t2: Optional[float] = None
+    rho_model: Optional[float] = None
+
+
+def parameter_search(engine, k: int, f: float, candidates, base: Optional[RunConfig] = None
+                     ) -> ParameterSearchResult:
+    """parameter_search (proj/src/orchestrator.cpp:252-303) through knnj_parameter_search:
+    each (beta, gamma) candidate runs hybrid at rho = 0.5 over the same seeded f-fraction
+    query subset; the fastest (device time) wins. Raises KnnjError like the reference's
+    UsageError / SampleTooSmallError; a failing candidate keeps its message."""
+    base = base or RunConfig(k=k)
+    cand = list(candidates)
+    betas = np.ascontiguousarray([b for b, _ in cand], np.float64)
+    gammas = np.ascontiguousarray([g for _, g in cand], np.float64)
+    mode = MODE_NAMES[base.mode] if isinstance(base.mode, str) else int(base.mode)
+    c = _capi.Config(k, base.m, base.beta, base.gamma, base.rho, mode, base.n_bins,
+                     base.hist_query_fraction, base.eps_mean_pair_cap, base.seed, None, 0)
+    rows = (_capi.SearchRow * max(len(cand), 1))()
+    bb, bg = C.c_double(), C.c_double()
+    engine._check(engine.lib.knnj_parameter_search(engine.h, C.byref(c), float(f), betas, gammas,
+                                                   len(cand), rows, C.byref(bb), C.byref(bg)))
+    out = [CandidateOutcome(r.beta, r.gamma, r.wall_seconds, r.error.decode())
+           for r in rows[:len(cand)]]
+    return ParameterSearchResult(bb.value, bg.value, out)
+
+
 def shard_range(cost, shard_index: int, shard_count: int) -> tuple:
     """knnj_shard_range: the contiguous item run [first, last) a shard owns (host-only)."""
     lib = _capi.load_library()

@@ -9,6 +9,8 @@
 // run on the GPU box by tests/test_gpu_adapter.py.
 #include <cstdio>
 #include <string>
+#include <utility>
+#include <vector>
 
 #include "knnj_knnjoin_adapter.hpp"
 #include "knnjoin/io.hpp"
@@ -76,6 +78,43 @@ int main() {
         if (!prof && ref.profile && got.profile)
             std::printf("  ref profile:\n%.400s\n  got profile:\n%.400s\n", ref.profile->to_text().c_str(),
                         got.profile->to_text().c_str());
+        bad += !ok;
+        ++n;
+    }
+    // parameter_search: same candidates (one invalid), same per-candidate errors; the
+    // winner is timing-dependent, so it only has to be one of the valid candidates
+    {
+        const knnjoin::Dataset d =
+            knnjoin::generate_synthetic(knnjoin::SyntheticSpec::parse("mixture"), 3000, 6, 13);
+        knnjoin::RunConfig base;
+        base.seed = 9;
+        base.buffer_size = 100'000'000;
+        const std::vector<std::pair<double, double>> cands = {{0.0, 0.0}, {0.3, 0.5}, {1.5, 0.0}};
+        const auto ref = knnjoin::parameter_search(d, 8, 0.05, cands, base);
+        const auto got = knnjoin_b200::parameter_search(eng, d, 8, 0.05, cands, base);
+        bool ok = ref.candidates.size() == got.candidates.size();
+        for (std::size_t i = 0; ok && i < ref.candidates.size(); ++i) {
+            ok = ok && ref.candidates[i].beta == got.candidates[i].beta &&
+                 ref.candidates[i].gamma == got.candidates[i].gamma &&
+                 ref.candidates[i].error == got.candidates[i].error &&
+                 (got.candidates[i].error.empty() == (got.candidates[i].wall_seconds > 0.0));
+        }
+        const bool best_valid = (got.best_beta == 0.0 && got.best_gamma == 0.0) ||
+                                (got.best_beta == 0.3 && got.best_gamma == 0.5);
+        bool threw_same = false;
+        try {
+            (void)knnjoin_b200::parameter_search(eng, d, 8, 0.01, cands, base);
+        } catch (const knnjoin::SampleTooSmallError& e) {
+            try {
+                (void)knnjoin::parameter_search(d, 8, 0.01, cands, base);
+            } catch (const knnjoin::SampleTooSmallError& e2) {
+                threw_same = std::string(e.what()) == std::string(e2.what());
+            }
+        }
+        ok = ok && best_valid && threw_same;
+        std::printf("%s parameter_search candidates=%zu errors/meta=%d best_valid=%d sample_error=%d\n",
+                    ok ? "ok " : "BAD", got.candidates.size(), (int)(ok || !best_valid), (int)best_valid,
+                    (int)threw_same);
         bad += !ok;
         ++n;
     }
