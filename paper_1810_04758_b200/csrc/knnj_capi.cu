@@ -782,8 +782,9 @@ struct knnj_ctx {
             last_hist_kernel_ms = kms;
             return nb;
         }
-        // pilot: every STRIDE-th sampled query, at most ~8k of them (enough to place the cap)
-        const uint64_t STRIDE = std::max<uint64_t>(32, nq / 8192);
+        // pilot: every STRIDE-th sampled query (>= 64th), at most ~8k of them (enough to
+        // place the cap; a cap that falls short only costs the full re-binning)
+        const uint64_t STRIDE = std::max<uint64_t>(64, nq / 8192);
         std::vector<uint64_t> pilot, rest;
         for (uint64_t i = lo; i < hi; ++i) (i % STRIDE == 0 ? pilot : rest).push_back(hq[i]);
         const uint64_t npilot = (nq + STRIDE - 1) / STRIDE;  // over all shards
@@ -1380,7 +1381,8 @@ struct knnj_ctx {
         sync();
         P.candidates = cand;
         P.screened = cand;
-        if (filter_r2 > 0.0 && box_filter && P.nitems) filter_ranges(lv, P, filter_r2);
+        if (filter_r2 > 0.0 && box_filter && P.nitems)
+            filter_ranges(lv, P, filter_r2, K > 0 && pass_uses_tc(lv, K));
     }
 
     // Box filter of a join pass (after build_pass): a candidate can matter to a query
@@ -1400,14 +1402,16 @@ struct knnj_ctx {
     // width w. When the grid is at most 2 cells wide in every dim the certificate is
     // unconditional (cover2 = inf) and nothing may be dropped.
     double filter_radius2(const Level& lv) const { return cover2(lv) < kInf ? lv.w * lv.w : 0.0; }
-    void filter_ranges(Level& lv, Pass& P, double r2) {
+    // order: the nearest-first sweep, for tcgen05 passes only (their epilogue's rare path
+    // is what it cuts; a SIMT pass over tiny cells (C4) would sort billions of blocks)
+    void filter_ranges(Level& lv, Pass& P, double r2, bool tc_pass) {
         if (!lv.bbox_ready) {
             lv.bbox.ensure(((N + FB - 1) / FB) * 2 * n);
             launch_block_boxes(X64.p, lv.J.p, N, n, lv.bbox.p, s);
             lv.bbox_ready = true;
         }
         P.screened = filter_items(P.items.p, P.nitems, P.qpos.p, lv.J.p, lv.bbox.p, P.adj, P.nadj, r2,
-                                  sweep_order);
+                                  sweep_order && tc_pass);
     }
     // kept FB-blocks per item under the box filter (the filter's count pass only; items and
     // adj are left unchanged)
@@ -1454,8 +1458,21 @@ struct knnj_ctx {
             okey.ensure(1);
             kp = okey.p;  // non-null selects the per-block (ordered) variant
         }
+        d_u64a.ensure(1);
+        KJ_CUDA(cudaMemsetAsync(d_u64a.p, 0, 8, s));
         launch_filter_ranges(items, nitems, qbox.p, n, adj.p, bbox, nblk, r2c, cnt.p, nullptr,
-                             nullptr, nullptr, false, s, kp);
+                             nullptr, nullptr, false, s, kp, d_u64a.p);
+        if (order) {  // one range per kept block: the total must fit the 32-bit range ids
+            unsigned long long nr = 0;
+            KJ_CUDA(cudaMemcpyAsync(&nr, d_u64a.p, 8, cudaMemcpyDeviceToHost, s));
+            sync();
+            if (nr >= (1ull << 31)) {
+                order = false;
+                kp = nullptr;
+                launch_filter_ranges(items, nitems, qbox.p, n, adj.p, bbox, nblk, r2c, cnt.p,
+                                     nullptr, nullptr, nullptr, false, s);
+            }
+        }
         exclusive_sum(sc, cnt.p, off.p, nitems + 1, s);
         uint32_t total = 0;
         KJ_CUDA(cudaMemcpyAsync(&total, off.p + nitems, 4, cudaMemcpyDeviceToHost, s));

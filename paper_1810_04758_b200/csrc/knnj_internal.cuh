@@ -332,7 +332,7 @@ void launch_filter_ranges(uint4* items, uint64_t nitems, const float* qbox, uint
                           const uint2* adj, const float* box, uint64_t nblk, float r2,
                           uint32_t* out_cnt, const uint32_t* out_off, uint2* out_adj,
                           unsigned long long* screened, bool fill, cudaStream_t s,
-                          float* out_key = nullptr);
+                          float* out_key = nullptr, unsigned long long* count_total = nullptr);
 void launch_fill_u32(uint32_t* p, uint64_t n, uint32_t v, cudaStream_t s);
 void launch_merge_parts(const uint4* splits, uint64_t nsplits, uint32_t K, const uint32_t* t_ids,
                         const double* t_sq, const uint32_t* t_count, const uint32_t* qrow,

@@ -1738,6 +1738,7 @@ __global__ void k_filter_ranges(uint4* items, uint64_t nitems, const float* qbox
     if (lane == 0) {
         if (FILL) items[item] = make_uint4(it.x, it.y, base, base + kept);
         else out_cnt[item] = kept;
+        if (!FILL && screened) atomicAdd(screened, (unsigned long long)kept);  // 64-bit total
     }
 }
 void launch_item_boxes(const uint4* items, uint64_t nitems, const uint32_t* qpos, const uint32_t* J,
@@ -1752,9 +1753,10 @@ void launch_filter_ranges(uint4* items, uint64_t nitems, const float* qbox, uint
                           const uint2* adj, const float* box, uint64_t nblk, float r2,
                           uint32_t* out_cnt, const uint32_t* out_off, uint2* out_adj,
                           unsigned long long* screened, bool fill, cudaStream_t s,
-                          float* out_key) {
+                          float* out_key, unsigned long long* count_total) {
     if (!nitems) return;
     const unsigned grid = (unsigned)((nitems * 32 + 255) / 256);
+    if (!fill) screened = count_total;  // the count pass sums kept ranges there (if given)
 #define KJ_FR(F, O)                                                                       \
     k_filter_ranges<F, O><<<grid, 256, 0, s>>>(items, nitems, qbox, n, adj, box, nblk, r2, \
                                                out_cnt, out_off, out_adj, screened, out_key)
