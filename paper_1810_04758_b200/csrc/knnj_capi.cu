@@ -796,7 +796,7 @@ struct knnj_ctx {
             uint64_t run = 0;
             for (uint32_t b = 0; b < counted; ++b) {
                 run += praw[b];
-                if (double(run) / double(npilot) >= 2.0 * target) return b + 3;
+                if (double(run) / double(npilot) >= 2.0 * target) return b + 1;
             }
             return nb + 1;  // not found inside the counted bins
         };
