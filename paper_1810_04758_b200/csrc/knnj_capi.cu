@@ -801,23 +801,24 @@ struct knnj_ctx {
             return nb + 1;  // not found inside the counted bins
         };
         const bool pc = pilot_cap == 1 || (pilot_cap == 2 && n <= 8);
-        const uint32_t pcap = pc ? std::max<uint32_t>(8, nb / 4) : nb;
+        // capped pilot rounds at a tenth, then a quarter of the bins, then in full
+        std::vector<uint32_t> rounds;
+        if (pc) {
+            for (uint32_t c : {std::max<uint32_t>(8, nb / 10), std::max<uint32_t>(8, nb / 4)})
+                if (c < nb && (rounds.empty() || c > rounds.back())) rounds.push_back(c);
+        }
+        rounds.push_back(nb);
         uint32_t bcap = nb + 1;
         bool pilot_partial = false;
-        if (pcap < nb) {
-            pilot_partial = true;
-            histogram_queries(pilot.data(), pilot.size(), em, nb, praw.data(), pcap);
+        for (uint32_t rc : rounds) {
+            std::fill(praw.begin(), praw.end(), 0ull);
+            if (rc < nb) histogram_queries(pilot.data(), pilot.size(), em, nb, praw.data(), rc);
+            else histogram_queries(pilot.data(), pilot.size(), em, nb, praw.data());
             kms += last_hist_kernel_ms;
             reduce(praw.data(), nb);
-            bcap = place_cap(pcap);
-            if (bcap > pcap) std::fill(praw.begin(), praw.end(), 0ull);  // cap beyond the pilot's
-        }
-        if (bcap > pcap) {
-            histogram_queries(pilot.data(), pilot.size(), em, nb, praw.data());
-            kms += last_hist_kernel_ms;
-            reduce(praw.data(), nb);
-            pilot_partial = false;
-            bcap = place_cap(nb);
+            pilot_partial = rc < nb;
+            bcap = place_cap(rc);
+            if (bcap <= rc) break;  // the cap lies inside the bins this round counted
         }
         last_hist_ms_pilot = kms;
         bcap = std::min<uint32_t>(bcap, nb);
@@ -837,7 +838,7 @@ struct knnj_ctx {
             }
             std::fill(rraw.begin(), rraw.end(), 0ull);
         }
-        if (pilot_partial) {  // the pilot's counts stop at pcap
+        if (pilot_partial) {  // the pilot's counts stop at its cap
             std::fill(praw.begin(), praw.end(), 0ull);
             histogram_queries(pilot.data(), pilot.size(), em, nb, praw.data());
             kms += last_hist_kernel_ms;
