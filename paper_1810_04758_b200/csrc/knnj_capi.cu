@@ -758,10 +758,10 @@ struct knnj_ctx {
     // >= target there, so lower_bound selects the same bin as with the full histogram.
     // If the capped counts fall short, the rest is re-binned in full.
     int hist_cap_mode = 1;  // 0: never cap, 1: cap when the histogram is large, 2: always
-    // The pilot first bins only the lowest quarter of the bins (0 never, 1 always, 2 when
-    // n <= 8). Low-dim data is where the box filter at that radius drops most pairs: C5
-    // pilot 7.1 s over 3.1e12 pairs in full. In 18-D (C2) the capped pilot still screens
-    // 6.5e9 of 7.8e9 pairs and its per-column path is slower (19.7 vs 15.8 ms).
+    // The pilot first bins only the lowest tenth of the bins, then a quarter, then all
+    // (0: always in full; 1: all rounds; 2: the quarter round only for n <= 8). In 18-D
+    // the pair count below the radius grows ~8x per bin, so a quarter of the bins is
+    // already slower than binning in full; a tenth is not (C2's cap sits at bin 9).
     int pilot_cap = 2;
     double last_hist_ms_pilot = 0.0;
     uint32_t hist_for_selection(const std::vector<uint64_t>& hq, uint32_t shard, uint32_t nshard,
@@ -800,11 +800,13 @@ struct knnj_ctx {
             }
             return nb + 1;  // not found inside the counted bins
         };
-        const bool pc = pilot_cap == 1 || (pilot_cap == 2 && n <= 8);
-        // capped pilot rounds at a tenth, then a quarter of the bins, then in full
+        // capped pilot rounds at a tenth of the bins, then (n <= 8, where the counts grow
+        // slowly with the radius) a quarter, then in full
         std::vector<uint32_t> rounds;
-        if (pc) {
-            for (uint32_t c : {std::max<uint32_t>(8, nb / 10), std::max<uint32_t>(8, nb / 4)})
+        if (pilot_cap != 0) {
+            std::vector<uint32_t> want{std::max<uint32_t>(8, nb / 10)};
+            if (pilot_cap == 1 || n <= 8) want.push_back(std::max<uint32_t>(8, nb / 4));
+            for (uint32_t c : want)
                 if (c < nb && (rounds.empty() || c > rounds.back())) rounds.push_back(c);
         }
         rounds.push_back(nb);
