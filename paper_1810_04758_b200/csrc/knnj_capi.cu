@@ -1640,7 +1640,9 @@ struct knnj_ctx {
         f.out_kth = out_kth;
         f.out_status = out_status;
         f.halves = hv == 2 ? 1u : 0u;
-        if (finalize_xj && P.nq >= (1u << 16)) {  // big passes: gather rows in join order once
+        // big passes (at least a quarter of the points: the copy is N rows) gather rows in
+        // join order once
+        if (finalize_xj && P.nq >= (1u << 16) && 4 * P.nq >= N) {
             if (!lv.xj_ready) {
                 lv.XJ.ensure((uint64_t)N * n);
                 launch_rows_by(X64.p, lv.J.p, N, n, lv.XJ.p, s);
