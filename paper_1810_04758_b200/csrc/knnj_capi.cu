@@ -292,7 +292,11 @@ struct knnj_ctx {
     DBuf<unsigned long long> d_u64a, d_u64b;
     DBuf<double> d_part;
 
+    cudaStream_t s_out = nullptr;  // result D2H overlapping the fallback (knnj_run)
+    cudaEvent_t ev_out = nullptr;
     ~knnj_ctx() {
+        if (ev_out) cudaEventDestroy(ev_out);
+        if (s_out) cudaStreamDestroy(s_out);
         if (h_sq) cudaFreeHost(h_sq);
         if (h_ij) cudaFreeHost(h_ij);
         if (s) cudaStreamDestroy(s);
@@ -1018,6 +1022,7 @@ struct knnj_ctx {
     bool tile64 = false;
     uint32_t tc_slack = 24;       // tcgen05 join list capacity K + slack (compaction when full)
     bool finalize_xj = true;      // finalize reads FP64 rows from a join-ordered copy
+    bool early_d2h = true;        // knnj_run: result D2H overlaps classification + fallback
     // <= 64 fallback rows: brute force over all points. Off: 16.6 ms vs 8.3 ms through a
     // grid level on C2 (64 warps cannot hide the FP64 row loads)
     bool brute_fallback = false;
@@ -2044,6 +2049,8 @@ int knnj_set_option(knnj_ctx* c, const char* name, int64_t value) {
             c->pilot_cap = (int)value;
         } else if (k == "brute_fallback") {
             c->brute_fallback = value != 0;
+        } else if (k == "early_d2h") {
+            c->early_d2h = value != 0;
         } else if (k == "finalize_xj") {
             c->finalize_xj = value != 0;
         } else if (k == "tc_slack") {
@@ -2471,6 +2478,16 @@ static void run_impl(knnj_ctx* c, const knnj_config* cfg, uint32_t shard, uint32
 
     Timer t_all(s);
     const unsigned long long launches0 = g_launches.load();
+    const bool early_d2h = c->early_d2h;
+    bool early_started = false;
+    std::vector<uint32_t> fb_rows_host;  // rows the fallback rewrote (host ids)
+    struct OutSync {  // an early result copy never outlives the call (errors included)
+        knnj_ctx* c;
+        const bool& on;
+        ~OutSync() {
+            if (on && c->s_out) cudaStreamSynchronize(c->s_out);
+        }
+    } out_sync{c, early_started};
     // host-side reference RNG streams (pairs for eps_mean, the histogram's query sample)
     // drawn on a helper thread while the GPU reorders and orders the candidates
     const bool sampling = cfg->mode == KNNJ_HYBRID || cfg->mode == KNNJ_DENSE_ONLY;
@@ -2733,6 +2750,20 @@ static void run_impl(knnj_ctx* c, const knnj_config* cfg, uint32_t shard, uint32
             I.join_candidate_pairs = P.candidates;
         }
         n_own = P.nq;
+        // single-GPU runs with host outputs: copy every row now, on a second stream, while
+        // classification and the fallback run; the few rows the fallback rewrites are
+        // patched afterwards
+        if (nshard == 1 && ids && dist && early_d2h) {
+            if (!c->s_out) {
+                KJ_CUDA(cudaStreamCreateWithFlags(&c->s_out, cudaStreamNonBlocking));
+                KJ_CUDA(cudaEventCreateWithFlags(&c->ev_out, cudaEventDisableTiming));
+            }
+            KJ_CUDA(cudaEventRecord(c->ev_out, s));
+            KJ_CUDA(cudaStreamWaitEvent(c->s_out, c->ev_out, 0));
+            KJ_CUDA(cudaMemcpyAsync(ids, o_ids.p, 4 * nq * k_eff, cudaMemcpyDeviceToHost, c->s_out));
+            KJ_CUDA(cudaMemcpyAsync(dist, o_dist.p, 8 * nq * k_eff, cudaMemcpyDeviceToHost, c->s_out));
+            early_started = true;
+        }
         // ---- classify on device; exact fallback for failures and uncertified sparse rows
         {
             Timer t(s);
@@ -2753,7 +2784,9 @@ static void run_impl(knnj_ctx* c, const knnj_config* cfg, uint32_t shard, uint32
             unsigned long long nfb = 0;
             KJ_CUDA(cudaMemcpyAsync(&nfb, c->d_u64a.p, 8, cudaMemcpyDeviceToHost, s));
             c->sync();
-            std::vector<uint32_t> fr(nfb), fp(nfb);
+            std::vector<uint32_t>& fr = fb_rows_host;
+            fr.assign(nfb, 0u);
+            std::vector<uint32_t> fp(nfb);
             std::vector<double> fu(nfb);
             if (nfb) {
                 DBuf<uint8_t> g_st, g_pv;
@@ -2803,7 +2836,36 @@ static void run_impl(knnj_ctx* c, const knnj_config* cfg, uint32_t shard, uint32
     // ---- results to the host: this shard's rows, ascending query id
     {
         Timer t(s);
-        if (nshard == 1) {
+        if (nshard == 1 && early_started) {
+            const uint64_t nfb = fb_rows_host.size();
+            if (nfb > 65536) {  // many rewritten rows: copy everything again (after the early copy)
+                KJ_CUDA(cudaStreamSynchronize(c->s_out));
+                KJ_CUDA(cudaMemcpyAsync(ids, o_ids.p, 4 * nq * k_eff, cudaMemcpyDeviceToHost, s));
+                KJ_CUDA(cudaMemcpyAsync(dist, o_dist.p, 8 * nq * k_eff, cudaMemcpyDeviceToHost, s));
+            } else if (nfb) {
+                DBuf<uint32_t> d_fr, c_ids;
+                DBuf<double> c_dist;
+                d_fr.ensure(nfb);
+                c_ids.ensure(nfb * k_eff);
+                c_dist.ensure(nfb * k_eff);
+                KJ_CUDA(cudaMemcpyAsync(d_fr.p, fb_rows_host.data(), 4 * nfb, cudaMemcpyHostToDevice, s));
+                launch_gather_rows(d_fr.p, nfb, k_eff, o_ids.p, o_dist.p, c_ids.p, c_dist.p, s);
+                std::vector<uint32_t> h_ids(nfb * k_eff);
+                std::vector<double> h_dist(nfb * k_eff);
+                KJ_CUDA(cudaMemcpyAsync(h_ids.data(), c_ids.p, 4 * nfb * k_eff, cudaMemcpyDeviceToHost, s));
+                KJ_CUDA(cudaMemcpyAsync(h_dist.data(), c_dist.p, 8 * nfb * k_eff, cudaMemcpyDeviceToHost, s));
+                c->sync();
+                KJ_CUDA(cudaStreamSynchronize(c->s_out));  // the bulk copy must land first
+                for (uint64_t i = 0; i < nfb; ++i) {
+                    const uint64_t r = fb_rows_host[i];
+                    std::memcpy(ids + r * k_eff, h_ids.data() + i * k_eff, 4 * k_eff);
+                    std::memcpy(dist + r * k_eff, h_dist.data() + i * k_eff, 8 * k_eff);
+                }
+            }
+            KJ_CUDA(cudaStreamSynchronize(c->s_out));
+            if (prov) KJ_CUDA(cudaMemcpyAsync(prov, d_prov.p, nq, cudaMemcpyDeviceToHost, s));
+            if (owned) std::memcpy(owned, host_queries().data(), 4 * nq);
+        } else if (nshard == 1) {
             if (ids) KJ_CUDA(cudaMemcpyAsync(ids, o_ids.p, 4 * nq * k_eff, cudaMemcpyDeviceToHost, s));
             if (dist) KJ_CUDA(cudaMemcpyAsync(dist, o_dist.p, 8 * nq * k_eff, cudaMemcpyDeviceToHost, s));
             if (prov) KJ_CUDA(cudaMemcpyAsync(prov, d_prov.p, nq, cudaMemcpyDeviceToHost, s));

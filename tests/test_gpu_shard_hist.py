@@ -274,3 +274,22 @@ def test_brute_fallback_identical(engine, oracle, spec, N, n, k):
     q = np.concatenate([fb, np.random.default_rng(2).choice(N, 16, replace=False).astype(np.uint32)])
     oi, od = oracle.brute_knn(W, q, k)
     assert np.array_equal(b.ids[q], oi) and np.array_equal(b.dist[q], od)
+
+
+@pytest.mark.parametrize("spec,N,n,k", [("clusters:16:0.05", 30000, 18, 32), ("exponential", 40000, 6, 40),
+                                        ("uniform", 50000, 2, 10)])
+def test_early_d2h_identical(engine, spec, N, n, k):
+    """Host results copied during classification + fallback (rows the fallback rewrites
+    patched afterwards) equal the copy taken after the whole run."""
+    X = generate(spec, N, n, 47)
+    cfg = RunConfig(k=k, mode="hybrid", seed=47)
+    out = []
+    for o in (0, 1):
+        engine.set_option("early_d2h", o)
+        engine.set_points(X)
+        out.append(engine.run(cfg, want_hist=False))
+    engine.set_option("early_d2h", 1)
+    a, b = out
+    assert b.info["fallback_queries"] > 0 or spec == "clusters:16:0.05"
+    assert np.array_equal(a.ids, b.ids) and np.array_equal(a.dist, b.dist)
+    assert np.array_equal(a.provenance, b.provenance)
