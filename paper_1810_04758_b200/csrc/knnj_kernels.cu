@@ -1697,15 +1697,12 @@ __global__ void k_filter_ranges(uint4* items, uint64_t nitems, const float* qbox
                     const float hi = __ldg(box + (uint64_t)(n + d) * nblk + blk);
                     const float g = fmaxf(0.f, fmaxf(__fsub_rd(lo, qh[d]), __fsub_rd(ql[d], hi)));
                     acc = __fadd_rd(acc, __fmul_rd(g, g));
-                }
-                keep = acc <= r2;
-                if (ORDER && FILL && keep)
-                    for (uint32_t d = 0; d < n; ++d) {
-                        const float lo = __ldg(box + (uint64_t)d * nblk + blk);
-                        const float hi = __ldg(box + (uint64_t)(n + d) * nblk + blk);
+                    if (ORDER && FILL) {  // sweep key from the same loads (complete for kept blocks)
                         const float dc = 0.5f * ((lo + hi) - (ql[d] + qh[d]));
                         ck = fmaf(dc, dc, ck);
                     }
+                }
+                keep = acc <= r2;
             }
             const unsigned m = __ballot_sync(0xffffffffu, keep);
             if (ORDER) {
