@@ -63,14 +63,25 @@ void* knnj_stream(knnj_ctx* ctx);
 /* Measured FP32 FFMA throughput of this device (TFLOP/s, 2 flops per FFMA):
  * the roofline denominator for the SIMT distance kernels. */
 int knnj_fp32_peak(knnj_ctx* ctx, double* tflops);
-/* Engine knobs (no reference analogue; results never depend on them):
+/* Engine knobs (no reference analogue; results never depend on them, and every one has
+ * an on/off bit-identity test in tests/test_gpu_shard_hist.py):
  *   "tensor_cores" 0/1 : allow the tcgen05 distance screen (default 1).
  *   "split_items" 0/1  : split work items with oversized candidate sets across CTAs (1).
  *   "box_filter" 0/1   : drop candidate blocks provably out of the pass radius (1).
+ *   "sweep_order" 0/1  : tcgen05 passes sweep each item's blocks nearest-first (1).
  *   "epi_halves" 0/1   : tcgen05 join with two epilogue warps per TMEM lane quarter (0).
+ *   "tile64" 0/1       : tcgen05 join on 64-candidate tiles with early release (0).
+ *   "tc_slack" 8..96   : tcgen05 near-tie list capacity K + slack (24).
+ *   "fine", "fine2"    : fine-grid cascade ahead of level 0 at width eps * value/1000 (0 = off).
+ *   "morton_dims", "morton_bits" : join order inside a cell (10, 3).
+ *   "finalize_xj" 0/1  : exact recheck reads a join-ordered FP64 copy (1).
+ *   "brute_fallback" 0/1 : <= 64 fallback rows by brute force instead of a grid level (0).
+ *   "early_d2h" 0/1    : knnj_run copies results during the fallback, patching after (1).
  *   "hist_cap" 0/1/2   : eps-selection histogram counts only the bins select_eps_beta
  *                        needs when the profile is not requested: 0 never, 1 when the
- *                        histogram is large (default), 2 always (tests). */
+ *                        histogram is large (default), 2 always (tests).
+ *   "pilot_cap" 0/1/2  : the cap-placing pilot first counts a tenth of the bins (then, for
+ *                        n <= 8 or value 1, a quarter) before binning in full (2). */
 int knnj_set_option(knnj_ctx* ctx, const char* name, int64_t value);
 /* Page-locked host buffers for the end-to-end path (H2D/D2H at full PCIe rate). */
 void* knnj_alloc_pinned(size_t bytes);
