@@ -293,3 +293,27 @@ def test_early_d2h_identical(engine, spec, N, n, k):
     assert b.info["fallback_queries"] > 0 or spec == "clusters:16:0.05"
     assert np.array_equal(a.ids, b.ids) and np.array_equal(a.dist, b.dist)
     assert np.array_equal(a.provenance, b.provenance)
+
+
+@pytest.mark.parametrize("opt,val,default", [("morton_dims", 6, 10), ("morton_bits", 5, 3),
+                                             ("finalize_xj", 0, 1), ("tc_slack", 12, 24),
+                                             ("sweep_order", 0, 1)])
+def test_engine_knobs_identical(engine, oracle, opt, val, default):
+    """The remaining engine knobs change only work order and layout, never an output bit
+    (70k points so the finalize's join-ordered copy is in play)."""
+    N, n, k = 70000, 18, 32
+    X = generate("clusters:16:0.05", N, n, 53)
+    cfg = RunConfig(k=k, mode="hybrid", seed=53)
+    out = []
+    for v in (default, val):
+        engine.set_option(opt, v)
+        engine.set_points(X)
+        out.append(engine.run(cfg, want_hist=False))
+    engine.set_option(opt, default)
+    a, b = out
+    assert np.array_equal(a.ids, b.ids) and np.array_equal(a.dist, b.dist)
+    assert np.array_equal(a.provenance, b.provenance)
+    W = X[:, b.info["perm"]]
+    q = np.random.default_rng(11).choice(N, 32, replace=False).astype(np.uint32)
+    oi, od = oracle.brute_knn(W, q, k)
+    assert np.array_equal(b.ids[q], oi) and np.array_equal(b.dist[q], od)
