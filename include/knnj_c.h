@@ -72,6 +72,7 @@ int knnj_fp32_peak(knnj_ctx* ctx, double* tflops);
  *   "epi_halves" 0/1   : tcgen05 join with two epilogue warps per TMEM lane quarter (0).
  *   "tile64" 0/1       : tcgen05 join on 64-candidate tiles with early release (0).
  *   "tc_slack" 8..96   : tcgen05 near-tie list capacity K + slack (24).
+ *   "simt_slack" 0..128: SIMT near-tie list capacity K + slack (0 = max(8, K/8)).
  *   "fine", "fine2"    : fine-grid cascade ahead of level 0 at width eps * value/1000 (0 = off).
  *   "morton_dims", "morton_bits" : join order inside a cell (10, 3).
  *   "finalize_xj" 0/1  : exact recheck reads a join-ordered FP64 copy (1).

@@ -1023,6 +1023,7 @@ struct knnj_ctx {
     uint32_t tc_slack = 24;       // tcgen05 join list capacity K + slack (compaction when full)
     bool finalize_xj = true;      // finalize reads FP64 rows from a join-ordered copy
     bool early_d2h = true;        // knnj_run: result D2H overlaps classification + fallback
+    uint32_t simt_slack = 0;      // SIMT join list capacity K + slack (0: max(8, K/8))
     // <= 64 fallback rows: brute force over all points. Off: 16.6 ms vs 8.3 ms through a
     // grid level on C2 (64 warps cannot hide the FP64 row loads)
     bool brute_fallback = false;
@@ -1532,7 +1533,9 @@ struct knnj_ctx {
         if (!tc && P.chunk != (uint32_t)JB && P.chunk != 32u)
             throw Error(9, "pass built for a different kernel");
         // list capacity: K plus slack for near-ties inside the screen band (overflow -> exact slow path)
-        const uint32_t L = tc ? tcc.L : K + std::max<uint32_t>(16, K / 2);
+        // SIMT list slack: every extra slot costs shared memory (occupancy) and insertion
+        // shifts; C4 (K=64) runs 11.8 s at K+32, 9.1 s at K+8 with no overflow rows
+        const uint32_t L = tc ? tcc.L : K + (simt_slack ? simt_slack : std::max<uint32_t>(8, K / 8));
         if (L > 256) throw Error(1, "k above 170 is not supported by the device join");
         const int np = pick_np(n);
         if (np < 0) throw Error(1, "dimension count above 128 is not supported by the device join");
@@ -2049,6 +2052,9 @@ int knnj_set_option(knnj_ctx* c, const char* name, int64_t value) {
             c->pilot_cap = (int)value;
         } else if (k == "brute_fallback") {
             c->brute_fallback = value != 0;
+        } else if (k == "simt_slack") {
+            if (value < 0 || value > 128) throw Error(1, "simt_slack must be in [0, 128]");
+            c->simt_slack = (uint32_t)value;
         } else if (k == "early_d2h") {
             c->early_d2h = value != 0;
         } else if (k == "finalize_xj") {
