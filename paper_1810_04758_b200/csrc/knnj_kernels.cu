@@ -518,15 +518,18 @@ int pick_np(uint32_t n) {
 }
 static int tile_for(int np) { return np <= 32 ? 128 : 64; }
 
+// 32-query blocks over small dims stage 64-candidate tiles: their smem (and with it the
+// blocks per SM) is bounded by the per-query lists, so a smaller tile buys occupancy
+static int join_tile_for(int np, uint32_t qb) { return (qb == 32 && np <= 16) ? 64 : tile_for(np); }
 size_t join_smem_bytes(int np, uint32_t L, uint32_t qb) {
-    int T = tile_for(np);
+    int T = join_tile_for(np, qb);
     return sizeof(float) * (2 * np * T + 2 * T) + sizeof(uint32_t) * 2 * T +
            sizeof(float) * ((np + 3) & ~3) + (sizeof(float) + sizeof(uint32_t)) * L * qb;
 }
 
 template <int NP, int QB>
 static void launch_join_np(const JoinArgs& a, uint64_t nitems, cudaStream_t s) {
-    constexpr int T = NP <= 32 ? 128 : 64;
+    constexpr int T = (QB == 32 && NP <= 16) ? 64 : (NP <= 32 ? 128 : 64);
     size_t sm = join_smem_bytes(NP, a.L, QB);
     set_smem(k_join<NP, T, QB>, sm);
     for (uint64_t off = 0; off < nitems; off += 2147483647ull) {
