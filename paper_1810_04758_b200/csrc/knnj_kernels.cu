@@ -212,54 +212,66 @@ __global__ void __launch_bounds__(QB) k_join(JoinArgs p) {
             float rhs = __fsub_ru(cut, na);
             const float* tb = tile + buf * NP * T;
             const float* nbb = nbuf + buf * T;
-            const uint32_t jend = (c + 3) & ~3u;
-            for (uint32_t j = 0; j < jend; j += 4) {
-                float4 nb4 = *reinterpret_cast<const float4*>(nbb + j);
-                float acc0 = nb4.x, acc1 = nb4.y, acc2 = nb4.z, acc3 = nb4.w;
-#pragma unroll
-                for (int d = 0; d < NP; ++d) {
-                    float4 b = *reinterpret_cast<const float4*>(tb + d * T + j);
-                    acc0 = fmaf(a2[d], b.x, acc0);
-                    acc1 = fmaf(a2[d], b.y, acc1);
-                    acc2 = fmaf(a2[d], b.z, acc2);
-                    acc3 = fmaf(a2[d], b.w, acc3);
-                }
+            // hits of 4 candidates (j .. j+3), screened against the current rhs
+            auto proc4 = [&](uint32_t j, float acc0, float acc1, float acc2, float acc3) {
                 const bool s0 = acc0 <= rhs, s1 = acc1 <= rhs, s2 = acc2 <= rhs, s3 = acc3 <= rhs;
-                if (s0 | s1 | s2 | s3) {
-                    float accs[4] = {acc0, acc1, acc2, acc3};
-                    bool ss[4] = {s0, s1, s2, s3};
+                if (!(s0 | s1 | s2 | s3)) return;
+                float accs[4] = {acc0, acc1, acc2, acc3};
+                bool ss[4] = {s0, s1, s2, s3};
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        if (!ss[u]) continue;
-                        const uint32_t pos = tpos[buf * T + j + u];
-                        if (pos == qp) continue;  // self pair: excluded by id
-                        const float key = accs[u] + na;
-                        if (cnt == (int)p.L) {
-                            ovf = true;
-                            rhs = -CUDART_INF_F;
-                            break;
-                        }
-                        int q = cnt;
-                        while (q > 0) {
-                            float kq = lkey[(q - 1) * QB + tid];
-                            if (kq <= key) break;
-                            lkey[q * QB + tid] = kq;
-                            lpos[q * QB + tid] = lpos[(q - 1) * QB + tid];
-                            --q;
-                        }
-                        lkey[q * QB + tid] = key;
-                        lpos[q * QB + tid] = pos;
-                        ++cnt;
-                        if (cnt >= (int)p.K) {
-                            cut_list = __fadd_ru(lkey[(p.K - 1) * QB + tid], 2.f * dmax);
-                            const float ci = __fadd_ru(init_cut, dmax);
-                            const float ce = fminf(cut_list, ci);
-                            while (cnt > (int)p.K && lkey[(cnt - 1) * QB + tid] > ce) --cnt;
-                            cut = fminf(cut_list, __fadd_ru(init_cut, dl));
-                            rhs = __fsub_ru(cut, na);
-                        }
+                for (int u = 0; u < 4; ++u) {
+                    if (!ss[u]) continue;
+                    const uint32_t pos = tpos[buf * T + j + u];
+                    if (pos == qp) continue;  // self pair: excluded by id
+                    const float key = accs[u] + na;
+                    if (cnt == (int)p.L) {
+                        ovf = true;
+                        rhs = -CUDART_INF_F;
+                        return;
+                    }
+                    int q = cnt;
+                    while (q > 0) {
+                        float kq = lkey[(q - 1) * QB + tid];
+                        if (kq <= key) break;
+                        lkey[q * QB + tid] = kq;
+                        lpos[q * QB + tid] = lpos[(q - 1) * QB + tid];
+                        --q;
+                    }
+                    lkey[q * QB + tid] = key;
+                    lpos[q * QB + tid] = pos;
+                    ++cnt;
+                    if (cnt >= (int)p.K) {
+                        cut_list = __fadd_ru(lkey[(p.K - 1) * QB + tid], 2.f * dmax);
+                        const float ci = __fadd_ru(init_cut, dmax);
+                        const float ce = fminf(cut_list, ci);
+                        while (cnt > (int)p.K && lkey[(cnt - 1) * QB + tid] > ce) --cnt;
+                        cut = fminf(cut_list, __fadd_ru(init_cut, dl));
+                        rhs = __fsub_ru(cut, na);
                     }
                 }
+            };
+            // 8 candidates per step: two independent groups of FMA chains (ILP)
+            const uint32_t jend = (c + 7) & ~7u;
+            for (uint32_t j = 0; j < jend; j += 8) {
+                const float4 na4 = *reinterpret_cast<const float4*>(nbb + j);
+                const float4 nb4 = *reinterpret_cast<const float4*>(nbb + j + 4);
+                float a0 = na4.x, a1 = na4.y, a2v = na4.z, a3 = na4.w;
+                float b0 = nb4.x, b1 = nb4.y, b2 = nb4.z, b3 = nb4.w;
+#pragma unroll
+                for (int d = 0; d < NP; ++d) {
+                    const float4 x = *reinterpret_cast<const float4*>(tb + d * T + j);
+                    const float4 y = *reinterpret_cast<const float4*>(tb + d * T + j + 4);
+                    a0 = fmaf(a2[d], x.x, a0);
+                    a1 = fmaf(a2[d], x.y, a1);
+                    a2v = fmaf(a2[d], x.z, a2v);
+                    a3 = fmaf(a2[d], x.w, a3);
+                    b0 = fmaf(a2[d], y.x, b0);
+                    b1 = fmaf(a2[d], y.y, b1);
+                    b2 = fmaf(a2[d], y.z, b2);
+                    b3 = fmaf(a2[d], y.w, b3);
+                }
+                proc4(j, a0, a1, a2v, a3);
+                if (!ovf) proc4(j + 4, b0, b1, b2, b3);
             }
         }
         __syncthreads();
