@@ -285,6 +285,25 @@ __global__ void __launch_bounds__(QB) k_join(JoinArgs p) {
     }
 }
 
+// rank of each of this lane's E entries among all c entries of the warp's list
+template <int E, int EMAX>
+__device__ __forceinline__ void rank_entries(const double (&sq)[EMAX], const uint32_t (&id)[EMAX],
+                                             uint32_t (&rk)[EMAX], uint32_t c) {
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        const double ms = sq[e];
+        const uint32_t mi = id[e];
+        for (int src = 0; src < 32; ++src) {
+            const double s = __shfl_sync(0xffffffffu, ms, src);
+            const uint32_t t = __shfl_sync(0xffffffffu, mi, src);
+            if ((uint32_t)(e * 32 + src) >= c) break;
+#pragma unroll
+            for (int f = 0; f < E; ++f)
+                if (pair_less(s, t, sq[f], id[f])) ++rk[f];
+        }
+    }
+}
+
 // ---------------------------------------------------------------- finalize
 // One warp per launch row: exact FP64 distances for the screened list, exact
 // (sq,id) ranks, first K written to the query's output row, status bits.
@@ -326,19 +345,16 @@ __global__ void k_finalize(FinalArgs a) {
             sq[e] = exact_sq(qx, a.XJ ? a.XJ + (uint64_t)ps * a.n : a.X64 + (uint64_t)t * a.n, a.n);
         }
     }
-#pragma unroll
-    for (int e = 0; e < EMAX; ++e) {
-        if (e >= E) break;
-        const double ms = sq[e];
-        const uint32_t mi = id[e];
-        for (int src = 0; src < 32; ++src) {
-            const double s = __shfl_sync(0xffffffffu, ms, src);
-            const uint32_t t = __shfl_sync(0xffffffffu, mi, src);
-            if ((uint32_t)(e * 32 + src) >= c) break;
-#pragma unroll
-            for (int f = 0; f < EMAX; ++f)
-                if (f < E && pair_less(s, t, sq[f], id[f])) ++rk[f];
-        }
+    // exact (sq, id) rank of every entry: compile-time entry count per lane, so the
+    // inner comparisons are not issued for empty register slots
+    switch (E) {
+#define KJ_RANK(EE)                                        \
+        case EE:                                           \
+            rank_entries<EE, EMAX>(sq, id, rk, c);         \
+            break;
+        KJ_RANK(1) KJ_RANK(2) KJ_RANK(3) KJ_RANK(4) KJ_RANK(5) KJ_RANK(6) KJ_RANK(7) KJ_RANK(8)
+#undef KJ_RANK
+        default: break;
     }
     double kth = CUDART_INF;
 #pragma unroll
