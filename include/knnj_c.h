@@ -81,8 +81,9 @@ int knnj_fp32_peak(knnj_ctx* ctx, double* tflops);
  *   "hist_cap" 0/1/2   : eps-selection histogram counts only the bins select_eps_beta
  *                        needs when the profile is not requested: 0 never, 1 when the
  *                        histogram is large (default), 2 always (tests).
- *   "pilot_cap" 0/1/2  : the cap-placing pilot first counts a tenth of the bins (then, for
- *                        n <= 8 or value 1, a quarter) before binning in full (2). */
+ *   "pilot_cap" 0/1/2  : the cap-placing pilot counts growing prefixes of the bins (4% and
+ *                        a quarter only for n <= 8 or value 1; a tenth always) before
+ *                        binning in full (2). */
 int knnj_set_option(knnj_ctx* ctx, const char* name, int64_t value);
 /* Page-locked host buffers for the end-to-end path (H2D/D2H at full PCIe rate). */
 void* knnj_alloc_pinned(size_t bytes);

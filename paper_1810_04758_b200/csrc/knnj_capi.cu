@@ -808,7 +808,9 @@ struct knnj_ctx {
         // slowly with the radius) a quarter, then in full
         std::vector<uint32_t> rounds;
         if (pilot_cap != 0) {
-            std::vector<uint32_t> want{std::max<uint32_t>(8, nb / 10)};
+            std::vector<uint32_t> want;
+            if (pilot_cap == 1 || n <= 8) want.push_back(std::max<uint32_t>(4, nb / 25));
+            want.push_back(std::max<uint32_t>(8, nb / 10));
             if (pilot_cap == 1 || n <= 8) want.push_back(std::max<uint32_t>(8, nb / 4));
             for (uint32_t c : want)
                 if (c < nb && (rounds.empty() || c > rounds.back())) rounds.push_back(c);
