@@ -1,8 +1,9 @@
 #!/usr/bin/env python
 """Benchmark: all-points exact KNN self-join (HybridKNN-Join hot path) on B200.
 
-Metric (BASELINE.json): KNN self-join points/sec, K=32, on the SuSy-shaped
-config C2 (5M x 18-D Gaussian-mixture, 16 clusters, sigma 0.05; synthetic, seed 1).
+Metric (BASELINE.json): KNN self-join points/sec, K=32, on the metric's own config
+C5 (BASELINE.json configs[4]: 100M uniform 4-D points, K=32, the 1/2/4/8-GPU scaling
+run; synthetic, seed 1). --config C2/NS/... runs the other shapes.
 One step = one full run_hybrid pass (variance reorder -> eps_mean -> distance
 histogram -> grid build -> split -> fused range-join + top-K -> exact fallback)
 over the whole dataset.
@@ -43,7 +44,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="C2")
+    ap.add_argument("--config", default="C5")
     ap.add_argument("--size", type=int, default=0, help="override |D| (testing only)")
     ap.add_argument("--cpu-sample", type=int, default=0, help="reference query sample per step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -116,14 +117,16 @@ def load_peaks() -> dict:
         return {}
 
 
-def profile_traffic():
-    """dram bytes per launch of the join kernel from the committed ncu capture of this
-    workload (profiles/), or None."""
+def profile_traffic(config: str):
+    """dram bytes per launch of the join kernel from the committed ncu --set full capture
+    of this workload (profiles/join_traffic.json, keyed by config), or None."""
     try:
         with open(os.path.join(ROOT, "profiles", "join_traffic.json")) as f:
-            return json.load(f).get("dram_bytes_per_launch")
+            d = json.load(f)
     except (OSError, ValueError):
         return None
+    e = d.get(config)
+    return e.get("dram_bytes_per_launch") if isinstance(e, dict) else None
 
 
 # ---------------------------------------------------------------------------- reference arm
@@ -141,6 +144,29 @@ def cpu_reference(X, k, sample, seed=1):
     _, _, secs = ref.kd_query(h, q, k, cores)
     return dict(handle=h, ref=ref, rate=sample / secs, secs=secs, cores=cores,
                 t_reorder=t_reorder, t_build=t_build, q=q)
+
+
+def cpu_hybrid_reduced(cfgd, size=None):
+    """The reference's Hybrid mode (the paper's algorithm, run_hybrid with every phase)
+    at a reduced |D| of the same distribution: its eps histogram is quadratic in |D|, so
+    the full size is out of reach on the host. points/s over
+    measured_total and over the call's wall time, all host threads."""
+    from oracle.oracle import Ref, ref_available
+    from paper_1810_04758_b200.synthetic import generate
+    if not ref_available():
+        return None
+    size = size or {"C1": cfgd["size"], "C3": 100_000, "C4": 400_000}.get(cfgd["key"], 500_000)
+    Xs = generate(cfgd["spec"], size, cfgd["dims"], seed=1)
+    ref = Ref()
+    t = time.perf_counter()
+    o = ref.run(Xs, k=cfgd["k"], mode="hybrid", seed=1, workers=0, buffer_size=100_000_000)
+    wall = time.perf_counter() - t
+    return {"points": size, "value": size / o["measured_total"], "unit": UNIT,
+            "measured_total_s": o["measured_total"], "wall_s": wall,
+            "cores": ref.hardware_concurrency(),
+            "note": f"reference Hybrid (run_hybrid) on {size} points of the same distribution; "
+                    f"value = points / measured_total (reorder + eps + split + "
+                    f"max(dense, sparse) + reassign + merge, orchestrator.cpp:245-248)"}
 
 
 def run_reference(args, cfgd, X):
@@ -265,39 +291,45 @@ def run_ours(args, cfgd, X):
         step_e2e()
     ms_e2e, infos_e2e = timed(step_e2e, args.steps)
 
-    # Roofline of the dominant kernel (the fused join), per launch:
-    #  * tcgen05 path: algorithmic tensor flops = 2*(3n+2) per candidate pair of the
-    #    reference 3^m walk (the FP16 hi/lo GEMM form: 3n products + the |b|^2 split),
-    #    against the measured dense bf16/fp16 peak (MEASURED_PEAKS.json);
-    #  * SIMT path: 3n FP32 flops per candidate pair against an
-    #    FFMA microbenchmark measured live.
+    # Roofline of the dominant kernel (the fused join), per launch, as SURVEY.md §8(d)
+    # defines the work: 3n flops (one sub + one FMA per dimension) per candidate pair of
+    # the reference's 3^m walk (its candidates_examined counter, counted exactly by the
+    # pass build over every level-0 row, before the box filter). Screens, rechecks and the
+    # FP16 hi/lo split are not credited. The denominator is the pipe the kernel runs on:
+    # the measured dense bf16 tensor peak (MEASURED_PEAKS.json) for the tcgen05 screen, the
+    # FFMA peak measured live on this GPU for the SIMT kernel.
     info = infos[-1]
     join_ms = statistics.mean(i["ms_join_kernel"] for i in infos)
     hist_ms = statistics.mean(i["ms_hist_kernel"] for i in infos)
     cand = info["join_candidate_pairs"]   # this rank's level-0 join pairs (dense + sparse rows)
+    screened = info["join_screened_pairs"]
     owned = [i["n_owned"] for i in infos_e2e]
     d2h = int(owned[-1]) * (k * 12 + 1 + 4 * (world > 1))
-    flops_3n = 3.0 * n * cand
+    flops = 3.0 * n * cand
     peak_c = np.ctypeslib.ctypes.c_double()
     eng._check(lib.knnj_fp32_peak(eng.h, np.ctypeslib.ctypes.byref(peak_c)))
     fp32_peak = peak_c.value
+    peaks = load_peaks()
     if info["join_tensor_cores"]:
-        flops = 2.0 * (3 * n + 2) * cand
-        peaks = load_peaks()
         peak = peaks.get("bf16_tflops", 1590.0)
         peak_src = ("MEASURED_PEAKS.json bf16_tflops (dense, burst; fp16 runs at the bf16 rate)"
                     if "bf16_tflops" in peaks else "B200_PROFILING.md fallback 1.59 PFLOP/s")
         bound = "tensor"
-        fdef = "2*(3n+2) tensor flops per candidate pair of the reference 3^m walk (FP16 hi/lo GEMM form)"
     else:
-        flops = flops_3n
         peak = fp32_peak
         peak_src = "FFMA microbenchmark measured live on this GPU (no FP32 figure in MEASURED_PEAKS.json)"
         bound = "fp32"
-        fdef = "3n FP32 flops per candidate pair of the reference 3^m walk"
     achieved = flops / (join_ms * 1e-3) / 1e12
     hist_pairs = info["hist_query_count"] * (N - 1)
-
+    # whole-run check: t_ideal = max(F / P_fp32, B / BW_hbm) with
+    # F = 3n (histogram pairs + join pairs + eps_mean pairs), B = the algorithmic bytes.
+    # Above 1 means the run skips work the formula counts (capped histogram, box filter,
+    # tensor-core screen): a work-avoidance ratio, not a utilisation.
+    pairs_mean = min(10 * N, 1_000_000)
+    F_run = 3.0 * n * (hist_pairs + cand + pairs_mean)
+    B_run = N * n * 4 + N * 8 + info["grid_cells"] * 24 + N * k * 12
+    bw = peaks.get("hbm_gbs", 6545.0) * 1e9
+    t_ideal = max(F_run / (fp32_peak * 1e12), B_run / bw)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         c = cpu_reference(X, k, args.cpu_sample or 15000)
@@ -307,7 +339,9 @@ def run_ours(args, cfgd, X):
                    "sample": f"{len(c['q'])} seeded random queries against all {N} points, "
                              f"reference SparseOnly/RefImpl kd-tree (the faster reference CPU "
                              f"mode), {c['secs']:.2f}s; kd build {c['t_build']:.1f}s excluded"}
-
+            hyb = cpu_hybrid_reduced(cfgd)
+            if hyb is not None:
+                cpu["hybrid_reduced"] = hyb
     if rank == 0:
         line = {
             "metric": METRIC, "value": N / (ms * 1e-3), "unit": UNIT, "n_gpus": world,
@@ -329,12 +363,22 @@ def run_ours(args, cfgd, X):
                          "kernel": "k_tc<JOIN> (tcgen05 fused range-join + screened top-K)"
                                    if bound == "tensor" else "k_join (SIMT fused range-join + top-K)",
                          "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": achieved / peak, "traffic": profile_traffic(),
+                         "frac": achieved / peak, "traffic": profile_traffic(cfgd["key"]),
                          "peak_source": peak_src,
-                         "algorithmic_flops_per_launch": flops, "flops_definition": fdef,
+                         "algorithmic_flops_per_launch": flops,
+                         "flops_definition": "SURVEY.md 8(d): 3n flops per candidate pair of the "
+                                             "reference 3^m walk (candidates_examined over all "
+                                             "level-0 rows, before the box filter)",
                          "kernel_ms": join_ms, "candidate_pairs": cand,
-                         "fp32_3n_equivalent_tflops": flops_3n / (join_ms * 1e-3) / 1e12,
+                         "screened_pairs": screened,
                          "fp32_peak_measured": fp32_peak},
+            "run_roofline": {"F_flops": F_run, "B_bytes": B_run, "t_ideal_s": t_ideal,
+                             "t_measured_s": ms * 1e-3,
+                             "t_ideal_over_measured": t_ideal / (ms * 1e-3),
+                             "definition": "SURVEY.md 8(d): F = 3n (N_hq (|D|-1) + sum C_q + "
+                                           "P_mean) against the measured FFMA peak, B against "
+                                           "MEASURED_PEAKS hbm_gbs; above 1 = work the run "
+                                           "avoids (capped histogram, box filter, tensor screen)"},
             "phases_ms": {k2: statistics.mean(i[k2] for i in infos) for k2 in
                           ("ms_reorder", "ms_eps_mean", "ms_histogram", "ms_grid", "ms_split",
                            "ms_join", "ms_fallback", "ms_join_kernel", "ms_hist_kernel", "ms_join_build",
@@ -356,8 +400,15 @@ def main():
     args = parse()
     from paper_1810_04758_b200.synthetic import CONFIGS, generate
     cfgd = dict(CONFIGS[args.config])
+    cfgd["key"] = args.config
     cfgd["name"] = f"{args.config}: " + {
+        "C1": "synthetic uniform 2-D, 100k points, K=5",
         "C2": "SuSy-shaped synthetic 18-D, 5M points, K=32, clustered (Gaussian mixture)",
+        "C3": "Songs-shaped synthetic 90-D, 500k points, K=16 (mixture)",
+        "C4": "exponentially-distributed skewed 6-D, 20M points, K=64",
+        "C5": "uniform 4-D, 100M points, K=32, cell-range sharded across 1/2/4/8 B200 "
+              "(BASELINE.json configs[4], the metric's scaling run)",
+        "NS": "north-star: SuSy-shaped clustered 18-D, 10M points, K=32",
     }.get(args.config, args.config)
     if args.size:
         cfgd["size"] = args.size

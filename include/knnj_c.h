@@ -69,14 +69,11 @@ int knnj_fp32_peak(knnj_ctx* ctx, double* tflops);
  *   "split_items" 0/1  : split work items with oversized candidate sets across CTAs (1).
  *   "box_filter" 0/1   : drop candidate blocks provably out of the pass radius (1).
  *   "sweep_order" 0/1  : tcgen05 passes sweep each item's blocks nearest-first (1).
- *   "epi_halves" 0/1   : tcgen05 join with two epilogue warps per TMEM lane quarter (0).
- *   "tile64" 0/1       : tcgen05 join on 64-candidate tiles with early release (0).
  *   "tc_slack" 8..96   : tcgen05 near-tie list capacity K + slack (24).
  *   "simt_slack" 0..128: SIMT near-tie list capacity K + slack (0 = max(8, K/8)).
  *   "fine", "fine2"    : fine-grid cascade ahead of level 0 at width eps * value/1000 (0 = off).
  *   "morton_dims", "morton_bits" : join order inside a cell (10, 3).
  *   "finalize_xj" 0/1  : exact recheck reads a join-ordered FP64 copy (1).
- *   "brute_fallback" 0/1 : <= 64 fallback rows by brute force instead of a grid level (0).
  *   "early_d2h" 0/1    : knnj_run copies results during the fallback, patching after (1).
  *   "hist_cap" 0/1/2   : eps-selection histogram counts only the bins select_eps_beta
  *                        needs when the profile is not requested: 0 never, 1 when the
@@ -152,8 +149,10 @@ typedef struct {
     double kernel_ms;             /* device time of the fused join kernels (CUDA events) */
 } knnj_join_stats;
 /* run_dense_join (dense_engine.cpp:229-303) with filter_keys fused
- * (dense_engine.cpp:165-196): per query solved[i] = 1 and k (dist,id)-ordered
- * neighbours, or solved[i] = 0 (failed; row contents unspecified). */
+ * (dense_engine.cpp:165-196) over the grid of knnj_grid_build: per query solved[i] = 1
+ * and its k (dist,id)-ordered in-eps neighbours, or solved[i] = 0 when fewer than k
+ * non-self points lie within eps; filter_keys then discards the partial list
+ * (dense_engine.cpp:182-192), so a failed row reads ids = 0xFFFFFFFF, dist = +inf. */
 int knnj_dense_join(knnj_ctx* ctx, const uint32_t* queries, uint64_t n_queries, uint32_t k,
                     uint32_t* ids, double* dist, uint8_t* solved, knnj_join_stats* stats);
 /* Exact KNN, self excluded, (dist,id) order: the contract of KdTree::knn_query
@@ -275,6 +274,34 @@ int knnj_tsv_write(const char* path, const uint32_t* queries, const uint32_t* id
  * the reference's messages (KNNJ_E_INGEST). */
 int knnj_binary_header(const char* path, uint64_t* n_points, uint64_t* dims);
 int knnj_binary_read(const char* path, double* out, uint64_t capacity_doubles);
+/* ingest_text (proj/src/io.cpp:24-67): CSV (sep ',') or TSV (sep '\t'), one point per
+ * line, empty lines skipped, a trailing '\r' stripped, fields parsed with
+ * std::from_chars after optional spaces/tabs. knnj_text_parse parses the whole file
+ * with `threads` host threads (0 = all) into a handle and reports |D| and n;
+ * knnj_text_copy writes the row-major coordinates (e.g. into a pinned buffer);
+ * knnj_text_free releases the handle. Failures are KNNJ_E_INGEST with the
+ * reference's messages ("<path>: row r, column c: not a number: '<field>'",
+ * "...: non-finite value", "<path>: row r has c columns, expected n", "<path>: no
+ * points", "cannot open <path>"), the first one in file order. */
+typedef struct knnj_text knnj_text;
+int knnj_text_parse(const char* path, char sep, uint32_t threads, knnj_text** out,
+                    uint64_t* n_points, uint64_t* dims);
+int knnj_text_copy(const knnj_text* text, double* out, uint64_t capacity_doubles);
+void knnj_text_free(knnj_text* text);
+
+/* ---- test hooks (no reference analogue; used by tests/ only) -------------- */
+/* knnj_histogram_queries counting only bins [0, n_count): the kernels of the capped
+ * eps-selection histogram (the counted bins must equal the full histogram's). */
+int knnj_histogram_queries_capped(knnj_ctx* ctx, const uint64_t* query_ids, uint64_t n_queries,
+                                  double eps_mean, uint32_t n_bins, uint32_t n_count,
+                                  uint64_t* raw_counts);
+/* One 128x128 tcgen05 accumulator tile of the level-0 grid built by knnj_grid_build:
+ * queries at join-order positions [q0, q0+128) against [c0, c0+128). Returns the raw
+ * FP32 accumulators D[128][128], both FP16 operand row blocks (row_halfs halfs per
+ * row), the scale S, the screen bound delta (scaled units) and the point ids. */
+int knnj_debug_tc_tile(knnj_ctx* ctx, uint32_t q0, uint32_t c0, float* D, uint16_t* Bq,
+                       uint16_t* Bc, double* scale_S, double* delta, uint32_t* pid_q,
+                       uint32_t* pid_c);
 
 #ifdef __cplusplus
 }

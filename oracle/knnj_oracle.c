@@ -326,6 +326,29 @@ int orc_histogram(const double* X, uint64_t N, uint32_t n, double eps_mean, uint
     return 0;
 }
 
+/* The per-query binning of build_distance_histogram (proj/src/epsilon.cpp:76-104) over
+ * an explicit query-id list: checks the device histogram on a subset of the sampled
+ * queries at sizes where the whole sample is out of the oracle's reach. */
+int orc_histogram_queries(const double* X, uint64_t N, uint32_t n, double eps_mean,
+                          uint32_t n_bins, const uint64_t* queries, uint64_t nq,
+                          uint32_t threads, uint64_t* raw) {
+    if (!(eps_mean > 0.0)) return 4;
+    if (n_bins < 2) return 1;
+    for (uint64_t i = 0; i < nq; ++i)
+        if (queries[i] >= N) return 1;
+    if (threads < 1) threads = 1;
+    double bin_width = eps_mean / (double)n_bins;
+    hist_ctx c = {X, N, n, n_bins, queries, eps_mean, eps_mean * eps_mean, 1.0 / bin_width,
+                  calloc((size_t)threads * n_bins, 8)};
+    parallel_for(nq, threads, hist_task, &c);
+    for (uint32_t b = 0; b < n_bins; ++b) {
+        raw[b] = 0;
+        for (uint32_t t = 0; t < threads; ++t) raw[b] += c.local[(uint64_t)t * n_bins + b];
+    }
+    free(c.local);
+    return 0;
+}
+
 /* proj/src/epsilon.cpp:122-141 + orchestrator.cpp:49-63 */
 int orc_select_eps(const double* cum, uint32_t n_bins, double bin_width, uint32_t k, double beta,
                    int allow_fallback, double* eps_beta, double* eps_final, uint64_t* bin,
@@ -356,10 +379,35 @@ typedef struct {
     uint64_t key;
     uint32_t pid;
 } keyed_t;
-static int cmp_keyed(const void* a, const void* b) {
-    const keyed_t *x = a, *y = b;
-    if (x->key != y->key) return x->key < y->key ? -1 : 1;
-    return x->pid < y->pid ? -1 : (x->pid > y->pid);
+
+/* (key, pid) ascending, as the reference's std::sort of (linear_id, pid) pairs
+ * (grid_index.cpp:56-61): the input is in pid order, so a stable LSD radix sort on the
+ * key alone gives the same order (11-bit digits over the key's significant bits). */
+static void sort_keyed(keyed_t* a, uint64_t N) {
+    if (N < 2) return;
+    uint64_t kmax = 0;
+    for (uint64_t i = 0; i < N; ++i)
+        if (a[i].key > kmax) kmax = a[i].key;
+    int bits = 0;
+    while (bits < 64 && (kmax >> bits)) ++bits;
+    keyed_t* tmp = malloc(sizeof(keyed_t) * N);
+    keyed_t *src = a, *dst = tmp;
+    for (int sh = 0; sh < bits; sh += 11) {
+        uint64_t cnt[2048] = {0};
+        for (uint64_t i = 0; i < N; ++i) ++cnt[(src[i].key >> sh) & 2047u];
+        uint64_t run = 0;
+        for (int d = 0; d < 2048; ++d) {
+            uint64_t c = cnt[d];
+            cnt[d] = run;
+            run += c;
+        }
+        for (uint64_t i = 0; i < N; ++i) dst[cnt[(src[i].key >> sh) & 2047u]++] = src[i];
+        keyed_t* t = src;
+        src = dst;
+        dst = t;
+    }
+    if (src != a) memcpy(a, src, sizeof(keyed_t) * N);
+    free(tmp);
 }
 
 /* proj/src/grid_index.cpp:77-94 */
@@ -417,7 +465,7 @@ int orc_grid_build(const double* X, uint64_t N, uint32_t n, uint32_t m, double e
         cell_of(g, X + i * n, coords, &keyed[i].key);
         keyed[i].pid = (uint32_t)i;
     }
-    qsort(keyed, N, sizeof(keyed_t), cmp_keyed);
+    sort_keyed(keyed, N);
     g->B = malloc(8 * (N ? N : 1));
     g->G = malloc(16 * (N ? N : 1));
     g->A = malloc(4 * (N ? N : 1));

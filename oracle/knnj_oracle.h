@@ -51,6 +51,9 @@ int orc_histogram(const double* X, uint64_t N, uint32_t n, double eps_mean, uint
                   double frac, uint64_t seed, uint32_t threads, uint64_t* raw,
                   uint64_t* query_count);
 /* proj/src/epsilon.cpp:122-141 and orchestrator.cpp:49-63 (fallback) */
+int orc_histogram_queries(const double* X, uint64_t N, uint32_t n, double eps_mean,
+                          uint32_t n_bins, const uint64_t* queries, uint64_t nq,
+                          uint32_t threads, uint64_t* raw);
 int orc_select_eps(const double* cum, uint32_t n_bins, double bin_width, uint32_t k, double beta,
                    int allow_fallback, double* eps_beta, double* eps_final, uint64_t* bin,
                    int* fell_back);

@@ -87,6 +87,8 @@ class Oracle:
         L.orc_histogram.argtypes = [_dp, C.c_uint64, C.c_uint32, C.c_double, C.c_uint32,
                                     C.c_double, C.c_uint64, C.c_uint32, _u64p,
                                     C.POINTER(C.c_uint64)]
+        L.orc_histogram_queries.argtypes = [_dp, C.c_uint64, C.c_uint32, C.c_double,
+                                            C.c_uint32, _u64p, C.c_uint64, C.c_uint32, _u64p]
         L.orc_select_eps.argtypes = [_dp, C.c_uint32, C.c_double, C.c_uint32, C.c_double,
                                      C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double),
                                      C.POINTER(C.c_uint64), C.POINTER(C.c_int)]
@@ -149,6 +151,16 @@ class Oracle:
         if rc:
             raise ValueError(f"histogram error {rc}")
         return raw, qc.value
+
+    def histogram_queries(self, X, eps_mean, n_bins, queries, threads=8):
+        X = np.ascontiguousarray(X, np.float64)
+        q = np.ascontiguousarray(queries, np.uint64)
+        raw = np.zeros(n_bins, np.uint64)
+        rc = self.L.orc_histogram_queries(X, X.shape[0], X.shape[1], eps_mean, n_bins, q,
+                                          q.size, threads, raw)
+        if rc:
+            raise ValueError(f"histogram error {rc}")
+        return raw
 
     def select_eps(self, cum, bin_width, k, beta, allow_fallback=True):
         cum = np.ascontiguousarray(cum, np.float64)

@@ -99,6 +99,19 @@ struct ref_info {
 
 const char* ref_last_error() { return g_err.c_str(); }
 
+// ingest_dataset (io.cpp:99-106) into a caller buffer: sizes always, coordinates when
+// `cap` is large enough (used by tests/golden/make_ingest_golden.py)
+int ref_ingest(const char* path, const char* fmt, double* out, uint64_t cap, uint64_t* N,
+               uint64_t* n) {
+    return guarded([&] {
+        Dataset d = ingest_dataset(path, format_from_string(fmt));
+        *N = d.size();
+        *n = d.dims();
+        if (out && cap >= d.raw().size()) std::memcpy(out, d.raw().data(), 8 * d.raw().size());
+    });
+}
+
+
 int ref_set_kernel(const char* name) { return kernels::set_active_kernel(name) ? 0 : 1; }
 
 double ref_sq_dist_limited(const double* a, const double* b, uint64_t n, double limit) {

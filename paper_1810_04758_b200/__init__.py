@@ -6,6 +6,6 @@ package is its Python mirror of the reference ``knnjoin`` API.
 from ._capi import KnnjError, load_library  # noqa: F401
 from .engine import (  # noqa: F401
     CandidateOutcome, Engine, KnnRunResult, ParameterSearchResult, RunConfig, derive_seed,
-    parameter_search, read_binary_f64, run_hybrid, tsv_bytes, tsv_string, write_tsv,
+    ingest_dataset, parameter_search, read_binary_f64, read_text, run_hybrid, tsv_bytes, tsv_string, write_tsv,
 )
 from .synthetic import generate  # noqa: F401

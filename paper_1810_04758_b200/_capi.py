@@ -145,6 +145,15 @@ SIGNATURES += [
                                  C.POINTER(C.c_uint64)]),
     ("knnj_binary_header", C.c_int, [C.c_char_p, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
     ("knnj_binary_read", C.c_int, [C.c_char_p, _vp, C.c_uint64]),
+    ("knnj_text_parse", C.c_int, [C.c_char_p, C.c_char, C.c_uint32, C.POINTER(C.c_void_p),
+                                  C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
+    ("knnj_text_copy", C.c_int, [_vp, _vp, C.c_uint64]),
+    ("knnj_text_free", None, [_vp]),
+    # test hooks
+    ("knnj_histogram_queries_capped", C.c_int, [_vp, _u64p, C.c_uint64, C.c_double, C.c_uint32,
+                                                C.c_uint32, _u64p]),
+    ("knnj_debug_tc_tile", C.c_int, [_vp, C.c_uint32, C.c_uint32, _vp, _vp, _vp,
+                                     C.POINTER(C.c_double), C.POINTER(C.c_double), _vp, _vp]),
 ]
 
 _LIB = None

@@ -282,7 +282,6 @@ struct knnj_ctx {
 
     // large per-run buffers kept across calls (grow only): no allocator churn in steady state
     DBuf<uint32_t> pass_cnt, pass_pos;                   // join lists (run_pass)
-    DBuf<float> pass_key;                                // their keys (two-half epilogue)
     DBuf<uint64_t> gk_keys, gk_skeys;                    // grid build sort scratch
     DBuf<uint32_t> gk_vals, gk_runidx;
     DBuf<uint32_t> r_ids, r_q, r_rows;                   // run outputs / query lists (run_impl)
@@ -656,7 +655,7 @@ struct knnj_ctx {
         sort_pairs_u64_u32(sc, keys.p, skeys.p, vals.p, hJ.p, N, 3 * (int)md, s);
         launch_inverse(hJ.p, N, hposJ.p, s);
         Bh_id.ensure(N * row_halfs);
-        launch_prep_tc(X64.p, hJ.p, N, n, d_g.p, 1.0 / tc_S(), row_halfs, tc_split(), Bh_id.p, s);
+        launch_prep_tc(X64.p, hJ.p, N, n, d_g.p, 1.0 / tc_S(), row_halfs, Bh_id.p, s);
         const uint64_t nblk = (N + FB - 1) / FB;
         hbox.ensure(nblk * 2 * n);
         launch_block_boxes(X64.p, hJ.p, N, n, hbox.p, s);
@@ -724,7 +723,7 @@ struct knnj_ctx {
         TcJoinArgs a{};
         a.Bh = Bh_id.p;
         a.row_halfs = row_halfs;
-        a.split = tc_split();
+        a.ksteps = tc_ksteps();
         a.n = n;
         a.qpos = qp.p;
         a.A = hJ.p;
@@ -1009,33 +1008,24 @@ struct knnj_ctx {
         lv.built = true;
     }
 
-    // Tensor-core screen policy. Operand rows: split 3 (hi|lo|hi, K = 3n+2, ~22-bit
-    // products) when 3n+2 <= 128, padded to 64 or 128 halfs (1 or 2 128-byte
-    // k-blocks). The kernels also implement split 1 (hi only, K = n+2), but its
-    // 2^-11 |a||b| product error overflowed the near-tie lists on 90-D data (C3:
-    // 350k slow-path rows), so wider dims use the SIMT kernels.
+    // Tensor-core screen policy. Operand rows: [lo | hi | hi | nb_hi nb_lo] in FP16
+    // (K = 3n+2, ~22-bit products) padded to 64-half k-blocks (KB <= 5: n <= 106); wider
+    // points use the SIMT kernels.
     bool tc_enabled = true;
     bool split_items = true;  // split oversized work items into candidate-range parts
-    // tcgen05 join: 16 epilogue warps on 64-column halves (n <= 20). Off by default: on C2
-    // it measured 689 ms vs 647 ms for the 8-warp epilogue.
-    bool epi_halves = false;
-    // tcgen05 join (n <= 20): 64-candidate tiles, 4 early-released buffers. Off: 646 ms vs
-    // 540 ms for 128-candidate tiles on C2.
-    bool tile64 = false;
     uint32_t tc_slack = 24;       // tcgen05 join list capacity K + slack (compaction when full)
     bool finalize_xj = true;      // finalize reads FP64 rows from a join-ordered copy
     bool early_d2h = true;        // knnj_run: result D2H overlaps classification + fallback
     uint32_t simt_slack = 0;      // SIMT join list capacity K + slack (0: max(8, K/8))
-    // <= 64 fallback rows: brute force over all points. Off: 16.6 ms vs 8.3 ms through a
-    // grid level on C2 (64 warps cannot hide the FP64 row loads)
-    bool brute_fallback = false;
     // Fine cascade ahead of level 0 (widths eps * f / 1000, coarsest first is NOT
     // required: each is tried on the rows still uncertified). 0 = off.
     uint32_t fine_f[2] = {0, 0};
-    uint32_t tc_split() const { return 3 * n + 2 <= 320 ? 3 : 0; }
-    // operand row = KB 128-byte k-blocks of 64 halfs (KB <= 5: n <= 106)
-    uint32_t tc_row_halfs() const { return 64u * ((tc_split() * n + 2 + 63) / 64); }
-    bool use_tc() const { return tc_enabled && tc_split() != 0; }
+    bool tc_fits() const { return 3 * n + 2 <= 320; }
+    // operand row = KB 128-byte k-blocks of 64 halfs
+    uint32_t tc_row_halfs() const { return 64u * ((3 * n + 2 + 63) / 64); }
+    // K=16 UMMA steps that hold non-zero columns; the rest of the row is zero padding
+    uint32_t tc_ksteps() const { return (3 * n + 2 + 15) / 16; }
+    bool use_tc() const { return tc_enabled && tc_fits(); }
     // the histogram's tensor-core instances cover one or two k-blocks (n <= 42)
     bool use_tc_hist() const { return use_tc() && tc_row_halfs() <= 128; }
     double tc_S() const {
@@ -1047,35 +1037,64 @@ struct knnj_ctx {
     void prep_tc(Level& lv) {
         if (lv.tc_ready) return;
         lv.row_halfs = tc_row_halfs();
-        lv.split = tc_split();
         lv.Bh.ensure(N * lv.row_halfs);
-        launch_prep_tc(X64.p, lv.J.p, N, n, d_g.p, 1.0 / tc_S(), lv.row_halfs, lv.split, lv.Bh.p, s);
+        launch_prep_tc(X64.p, lv.J.p, N, n, d_g.p, 1.0 / tc_S(), lv.row_halfs, lv.Bh.p, s);
         lv.tc_ready = true;
     }
-    // Bound on |key - sq64/S^2| for the tensor-core screen.
-    // FP16 hi/lo representation, |b|^2 split, |a|^2 in FP32 and the FP64
-    // reference rounding are bounded rigorously; the tensor core's FP32
-    // accumulation is modelled per MMA instruction (products of FP16 are exact
-    // in FP32; each K=16 instruction rounds its partial sum) with a 4x
-    // allowance per instruction — ~10x the largest error measured on B200
-    // (tools/tc_probe.py, tests/test_gpu_screen.py keeps checking it).
-    // Split 1 (hi only) adds the dropped lo parts: |2a.b - 2a_hi.b_hi| <=
-    // 2(|a_lo||b| + |a_hi||b_lo|), |x_lo| <= 2^-11 |x| + sqrt(n) 2^-25 (FP16 subnormals).
+    // Bound delta on |key - sq64 / S^2| for the tensor-core screen. Scaled
+    // coordinates v = (x - g) / S have |v| <= R = Rg / S <= 1 (Rg rounded up). Every term is
+    // a worst case; no constant is calibrated on measured errors.
+    //  (1) FP16 representation. v = hi + lo + r with |lo| <= 2^-11 |v| + 2^-25 and
+    //      |r| <= 2^-22 |v| + 2^-25 per coordinate. The UMMA sums -2(a_hi b_lo + a_lo b_hi +
+    //      a_hi b_hi) = -2 a.b + 2 (a_lo b_lo + (a_hi + a_lo) r_b + r_a b), so the product
+    //      terms err by <= 6 u22 R^2 + 2 u24 sqrt(n) R; the norm splits |b|^2 = nb_hi + nb_lo
+    //      + r and |a|^2 (same split, summed in FP32) by <= 2 u22 R^2 + 2 u24.
+    //  (2) Accumulation in the tensor core. FP16 x FP16 products are exact in FP32. One
+    //      K=16 UMMA adds 16 products to the accumulator; whatever its internal order and
+    //      rounding, if every intermediate (aligned addend or partial sum) keeps the FP32
+    //      accumulator's 24-bit significand, its error is at most 18 u23 (|D_in| + sum|p_k|):
+    //      a sequential sum with any rounding direction errs by <= 16 u23 of it, an adder
+    //      that aligns all 17 addends to the largest exponent and truncates them by <= 17 u23
+    //      of the largest, plus u23 for the final normalisation. |D_in| is at most the sum of
+    //      |p| over the earlier steps, so the chain errs by <= 18 u23 sum_s (S_s + A_s) with
+    //      S_s the |p| bound of step s and A_s = sum_{s' < s} S_s'. Zero-padded steps add
+    //      exactly zero. Per step: the small hi*lo products of the whole row sum to <=
+    //      4 lo R (lo = u11 R + sqrt(n) u25, the bound on |x_lo|), the hi*hi products of any
+    //      column subset to <= 2 R^2 (1 + u11)^2 (Cauchy-Schwarz), the norm pair to <=
+    //      R^2 (1 + u10). The row puts the small products first, so the large partial sums
+    //      build up only in the last steps.
+    //  (3) The epilogue's FP32 roundings: |a|^2 = fl(nb_hi + nb_lo) and key = fl(D + |a|^2),
+    //      |key| <= 4 R^2: 5 u24 R^2 (the cuts round up, __fadd_ru / __fsub_ru).
+    //  (4) FP64: the scaled coordinates, |b|^2 and the reference's scalar-order sq64:
+    //      (4n + 12) 4 U64 R^2.
     double tc_delta() const {
-        const double u22 = std::ldexp(1.0, -22), u24 = std::ldexp(1.0, -24);
+        const double u10 = std::ldexp(1.0, -10), u11 = std::ldexp(1.0, -11);
+        const double u22 = std::ldexp(1.0, -22), u23 = std::ldexp(1.0, -23);
+        const double u24 = std::ldexp(1.0, -24), u25 = std::ldexp(1.0, -25);
         const double R = Rg / tc_S();
         const double R2 = R * R;
-        const double kdim = double(tc_split()) * n + 2.0;
-        const double n_mma = 4.0 * std::ceil(kdim / 64.0);  // K=16 steps
-        const double T = 3.1 * R2;                          // sum of |terms|
-        const double acc = (n_mma + 2.0) * 4.0 * u24 * T;
-        double d = acc + 6 * u22 * R2 + 2 * u24 * std::sqrt((double)n) * R + 2 * u22 * R2 +
-                   2 * u24 + 5 * u24 * R2 + (4.0 * n + 12.0) * 4.0 * U64 * R2;
-        if (tc_split() == 1) {
-            const double lo = std::ldexp(1.0, -11) * R + std::sqrt((double)n) * std::ldexp(1.0, -25);
-            d += 4.0 * lo * R * (1.0 + std::ldexp(1.0, -10)) + 2.0 * lo * lo;
+        const double rt = std::sqrt((double)n);
+        const double rep = 6 * u22 * R2 + 2 * u24 * rt * R + 2 * u22 * R2 + 2 * u24;
+        const double lo = u11 * R + rt * u25;
+        const double small_all = 4.0 * lo * R * (1.0 + u10);
+        const double hh_any = 2.0 * R2 * (1.0 + u11) * (1.0 + u11);
+        const double nb = R2 * (1.0 + u10);
+        double acc_sum = 0.0, prefix = 0.0;
+        for (uint32_t st = 0; st < tc_ksteps(); ++st) {
+            const uint32_t c0 = 16 * st, c1 = 16 * st + 16;
+            const auto overlaps = [&](uint32_t b, uint32_t e) { return c0 < e && b < c1; };
+            double S = 0.0;
+            if (overlaps(0, 2 * n)) S += small_all;
+            if (overlaps(2 * n, 3 * n)) S += hh_any;
+            if (overlaps(3 * n, 3 * n + 2)) S += nb;
+            acc_sum += S + prefix;
+            prefix += S;
         }
-        return 1.5 * d;
+        // the partial sums themselves carry the earlier steps' (tiny) errors: +1e-4 relative
+        const double acc = 18.0 * u23 * acc_sum * (1.0 + 1e-4);
+        const double epi = 5 * u24 * R2;
+        const double f64 = (4.0 * n + 12.0) * 4.0 * U64 * R2;
+        return rep + acc + epi + f64;
     }
     // join kernel configuration for list capacity L (K + slack for near-ties in the band)
     struct TcJoinCfg {
@@ -1095,10 +1114,10 @@ struct knnj_ctx {
         TcJoinCfg c;
         if (!use_tc() || K < 1 || !tc_precise_for(w)) return c;
         const uint32_t KB = tc_row_halfs() / 64;
-        const uint32_t L0 = K + (tc_split() == 3 ? tc_slack : 48u);
+        const uint32_t L0 = K + tc_slack;
         if (KB >= 3) {
             // wide operands (43 <= n <= 106): 64-candidate tiles keep A + B stages in smem
-            c.sh = TcShape{(int)KB, 1, KB == 5 ? 2 : 3, 1, 64};
+            c.sh = TcShape{(int)KB, 1, KB == 5 ? 2 : 3, 64};
             c.L = std::min<uint32_t>(L0, 64);
         } else if (L0 <= 64) {
             c.sh = KB == 1 ? TcShape{1, 2, 4} : TcShape{2, 1, 3};
@@ -1107,8 +1126,6 @@ struct knnj_ctx {
             c.sh = KB == 1 ? TcShape{1, 1, 4} : TcShape{2, 1, 2};
             c.L = std::min<uint32_t>(L0, 128);
         }
-        if (epi_halves && KB == 1) c.sh = TcShape{1, 2, 8, 2};  // two epilogue warps per quarter
-        else if (tile64 && KB == 1) c.sh = TcShape{1, 2, 8, 1, 64};  // 64-col tiles, early release
         c.ok = K + 8 <= c.L && tc_smem_bytes(c.sh, c.L, 0, false) <= 227 * 1024;
         return c;
     }
@@ -1538,18 +1555,19 @@ struct knnj_ctx {
         // SIMT list slack: every extra slot costs shared memory (occupancy) and insertion
         // shifts; C4 (K=64) runs 11.8 s at K+32, 9.1 s at K+8 with no overflow rows
         const uint32_t L = tc ? tcc.L : K + (simt_slack ? simt_slack : std::max<uint32_t>(8, K / 8));
-        if (L > 256) throw Error(1, "k above 170 is not supported by the device join");
+        if (L > 256)
+            throw Error(1, "k = " + std::to_string(K) + " needs a near-tie list of " + std::to_string(L) +
+                               " entries; the device join holds at most 256");
         const int np = pick_np(n);
         if (np < 0) throw Error(1, "dimension count above 128 is not supported by the device join");
         if (!tc && join_smem_bytes(np, L, P.chunk) > 227 * 1024)
             throw Error(1, "k too large for the device join");
         const uint64_t nv = P.nv, nvv = P.nv - P.nq;  // launch rows; virtual (split-part) rows
-        const uint32_t hv = (tc && tcc.sh.H == 2) ? 2u : 1u;  // lists per row
         DBuf<uint32_t>& cnt = pass_cnt;
         DBuf<uint32_t>& pos = pass_pos;
-        cnt.ensure(hv * nv);
-        pos.ensure(hv * nv * L);
-        if (P.nsplits) launch_fill_u32(cnt.p, hv * P.nq, SKIP, s);  // split real rows are merged later
+        cnt.ensure(nv);
+        pos.ensure(nv * L);
+        if (P.nsplits) launch_fill_u32(cnt.p, P.nq, SKIP, s);  // split real rows are merged later
         DBuf<float> cut_ext;
         if (d_init_cut && nvv) {  // virtual rows start from their real row's bound
             cut_ext.ensure(nv);
@@ -1562,7 +1580,7 @@ struct knnj_ctx {
             TcJoinArgs a{};
             a.Bh = lv.Bh.p;
             a.row_halfs = lv.row_halfs;
-            a.split = lv.split;
+            a.ksteps = tc_ksteps();
             a.n = n;
             a.qpos = P.qpos.p;
             a.items = P.items.p;
@@ -1578,13 +1596,8 @@ struct knnj_ctx {
             a.L = L;
             a.out_cnt = cnt.p;
             a.out_pos = pos.p;
-            if (hv == 2) {
-                pass_key.ensure(2 * nv * L);
-                a.out_key = pass_key.p;
-            }
             a.delta = f32_round_up(tc_delta());
             static const bool want_stats = getenv("KNNJ_JOIN_STATS") != nullptr;
-            if (const char* dm = getenv("KNNJ_JOIN_DBG")) a.dbg_mode = (uint32_t)atoi(dm);
             DBuf<unsigned long long> st;
             if (want_stats) {
                 st.ensure(8);
@@ -1649,7 +1662,6 @@ struct knnj_ctx {
         f.out_dist = out_dist;
         f.out_kth = out_kth;
         f.out_status = out_status;
-        f.halves = hv == 2 ? 1u : 0u;
         // big passes (at least a quarter of the points: the copy is N rows) gather rows in
         // join order once
         if (finalize_xj && P.nq >= (1u << 16) && 4 * P.nq >= N) {
@@ -1678,8 +1690,8 @@ struct knnj_ctx {
             FinalArgs fv = f;
             fv.qpos = P.qpos.p + P.nq;
             fv.qrow = v_iota.p;
-            fv.cnt = cnt.p + hv * P.nq;
-            fv.pos = pos.p + hv * P.nq * L;
+            fv.cnt = cnt.p + P.nq;
+            fv.pos = pos.p + P.nq * L;
             fv.nrows = nvv;
             fv.out_ids = t_ids.p;
             fv.out_dist = t_dist.p;
@@ -1701,7 +1713,7 @@ struct knnj_ctx {
             d_rows.ensure(nr);
             d_u64b.ensure(1);
             KJ_CUDA(cudaMemsetAsync(d_u64b.p, 0, 8, s));
-            launch_find_ovf(cnt.p + hv * r0, nr, d_rows.p, d_u64b.p, hv == 2 ? 1u : 0u, s);
+            launch_find_ovf(cnt.p + r0, nr, d_rows.p, d_u64b.p, s);
             unsigned long long novf = 0;
             KJ_CUDA(cudaMemcpyAsync(&novf, d_u64b.p, 8, cudaMemcpyDeviceToHost, s));
             sync();
@@ -1809,33 +1821,6 @@ struct knnj_ctx {
             }
             return L;
         };
-        // A handful of rows on a big dataset: brute force over all points (32 warps per
-        // row, merged) instead of building a grid level for them.
-        if (brute_fallback && !qpid.empty() && qpid.size() <= 64 && N >= 65536 && K <= 128) {
-            const uint64_t nq = qpid.size();
-            const uint32_t P = 32;
-            DBuf<uint32_t> d_p, d_r, t_ids, t_cnt;
-            DBuf<double> t_sq;
-            DBuf<uint4> sp;
-            d_p.ensure(nq);
-            d_r.ensure(nq);
-            t_ids.ensure(nq * P * K);
-            t_sq.ensure(nq * P * K);
-            t_cnt.ensure(nq * P);
-            sp.ensure(nq);
-            std::vector<uint4> hs(nq);
-            for (uint64_t i = 0; i < nq; ++i)
-                hs[i] = make_uint4((uint32_t)i, 1u, P, (uint32_t)(i * P));
-            KJ_CUDA(cudaMemcpyAsync(d_p.p, qpid.data(), 4 * nq, cudaMemcpyHostToDevice, s));
-            KJ_CUDA(cudaMemcpyAsync(d_r.p, qrow.data(), 4 * nq, cudaMemcpyHostToDevice, s));
-            KJ_CUDA(cudaMemcpyAsync(sp.p, hs.data(), 16 * nq, cudaMemcpyHostToDevice, s));
-            launch_brute_parts(X64.p, N, n, d_p.p, nq, P, K, t_ids.p, t_sq.p, t_cnt.p, s);
-            launch_merge_parts(sp.p, nq, K, t_ids.p, t_sq.p, t_cnt.p, d_r.p, -1.0, kInf, out_ids,
-                               out_dist, out_kth, out_status, s);
-            if (passes) ++*passes;
-            sync();
-            return;
-        }
         std::vector<int> lvl(qpid.size());
         for (size_t i = 0; i < qpid.size(); ++i) lvl[i] = level_for(U[i], first_level - 1);
         DBuf<float> d_cut_by_row;  // only the current pass's rows are ever written / read
@@ -1979,9 +1964,9 @@ const char* knnj_last_error(const knnj_ctx* ctx) { return ctx ? ctx->err.c_str()
 
 void* knnj_stream(knnj_ctx* ctx) { return ctx ? (void*)ctx->s : nullptr; }
 
-// Test hook (not in knnj_c.h's public set): one 128x128 tensor-core tile of
-// level 0 — queries at sorted positions [q0,q0+128) against [c0,c0+128) —
-// returns the raw FP32 accumulators and the FP16 operand rows used.
+// Test hook (knnj_c.h): one 128x128 tensor-core tile of level 0 — queries at sorted
+// positions [q0,q0+128) against [c0,c0+128) — returns the raw FP32 accumulators and
+// the FP16 operand rows used.
 int knnj_debug_tc_tile(knnj_ctx* c, uint32_t q0, uint32_t c0, float* D, uint16_t* Bq,
                        uint16_t* Bc, double* scale_S, double* delta, uint32_t* pid_q,
                        uint32_t* pid_c) {
@@ -2009,7 +1994,7 @@ int knnj_debug_tc_tile(knnj_ctx* c, uint32_t q0, uint32_t c0, float* D, uint16_t
         TcJoinArgs a{};
         a.Bh = lv.Bh.p;
         a.row_halfs = lv.row_halfs;
-        a.split = lv.split;
+        a.ksteps = c->tc_ksteps();
         a.n = c->n;
         a.qpos = d_qpos.p;
         a.items = d_item.p;
@@ -2052,8 +2037,6 @@ int knnj_set_option(knnj_ctx* c, const char* name, int64_t value) {
         } else if (k == "pilot_cap") {
             if (value < 0 || value > 2) throw Error(1, "pilot_cap must be 0, 1 or 2");
             c->pilot_cap = (int)value;
-        } else if (k == "brute_fallback") {
-            c->brute_fallback = value != 0;
         } else if (k == "simt_slack") {
             if (value < 0 || value > 128) throw Error(1, "simt_slack must be in [0, 128]");
             c->simt_slack = (uint32_t)value;
@@ -2064,10 +2047,6 @@ int knnj_set_option(knnj_ctx* c, const char* name, int64_t value) {
         } else if (k == "tc_slack") {
             if (value < 8 || value > 96) throw Error(1, "tc_slack must be in [8, 96]");
             c->tc_slack = (uint32_t)value;
-        } else if (k == "tile64") {
-            c->tile64 = value != 0;
-        } else if (k == "epi_halves") {
-            c->epi_halves = value != 0;
         } else if (k == "fine" || k == "fine2") {
             if (value < 0 || value >= 1000) throw Error(1, "fine width must be in [0, 1000) permille of eps");
             c->fine_f[k == "fine" ? 0 : 1] = (uint32_t)value;
@@ -2182,6 +2161,18 @@ int knnj_histogram_queries(knnj_ctx* c, const uint64_t* q, uint64_t nq, double e
         for (uint64_t i = 0; i < nq; ++i)
             if (q[i] >= c->N) throw Error(1, "histogram query id out of range");
         c->histogram_queries(q, nq, em, nb, raw);
+    });
+}
+
+int knnj_histogram_queries_capped(knnj_ctx* c, const uint64_t* q, uint64_t nq, double em,
+                                  uint32_t nb, uint32_t ncount, uint64_t* raw) {
+    return guarded(c, [&] {
+        need_points(c);
+        c->ensure_working();
+        if (ncount < 1 || ncount > nb) throw Error(1, "n_count must be in [1, n_bins]");
+        for (uint64_t i = 0; i < nq; ++i)
+            if (q[i] >= c->N) throw Error(1, "histogram query id out of range");
+        c->histogram_queries(q, nq, em, nb, raw, ncount);
     });
 }
 
@@ -2358,6 +2349,10 @@ int knnj_dense_join(knnj_ctx* c, const uint32_t* q, uint64_t nq, uint32_t k, uin
         for (uint64_t i = 0; i < nq; ++i) {
             solved[i] = (sts[i] & ST_HAS_K) && (sts[i] & ST_IN_EPS);
             ns += solved[i];
+            if (!solved[i]) {  // filter_keys discards a failed query's partial list
+                std::fill(ids + i * k, ids + (i + 1) * k, 0xFFFFFFFFu);
+                std::fill(dist + i * k, dist + (i + 1) * k, std::numeric_limits<double>::infinity());
+            }
         }
         if (st) {
             st->candidates_examined = P.candidates;

@@ -176,18 +176,16 @@ struct JoinArgs {
 struct TcJoinArgs {
     const __half* Bh;        // level's B operand rows (sorted order)
     uint32_t row_halfs, n;
-    uint32_t split;          // 3: hi|lo|hi operand (K = 3n+2); 1: hi only (K = n+2)
+    uint32_t ksteps;         // K=16 UMMA steps holding the 3n+2 non-zero columns
     const uint32_t* qpos;
     const uint4* items;
     const uint2* adj;
     const float* init_cut;   // per launch row (scaled units), may be null
     uint32_t K, L;
-    uint32_t* out_cnt;       // per launch row (H = 2: per row and half)
-    uint32_t* out_pos;       // per launch row * L (H = 2: row * 2L + half * L)
-    float* out_key;          // H = 2: the lists' screened keys, same layout as out_pos
+    uint32_t* out_cnt;       // per launch row
+    uint32_t* out_pos;       // per launch row * L
     float delta;             // |key - sq64/S^2| bound (scaled units)
     float* dbg;              // test hook: block 0 dumps its first accumulator tile [128][128]
-    uint32_t dbg_mode;       // dev hook (KNNJ_JOIN_DBG, timing only): 1 fast path only, 2 loads only, 3 no loads
     unsigned long long* stats;  // dev hook (KNNJ_JOIN_STATS): slabs, rare slabs, bits, inserts, compactions
     // histogram epilogue (HIST kernels only)
     uint32_t n_bins;
@@ -218,7 +216,6 @@ struct FinalArgs {
     uint8_t* out_status;     // [qrow]
     double* out_sq;          // optional [qrow * K]: exact sq (split-part rows, for the merge)
     uint32_t* out_count;     // optional [qrow]: entries written (min(candidates, K))
-    uint32_t halves;         // 1: two lists per row (cnt[2r + h], pos[(2r + h) * L + i])
     const double* XJ;        // optional: X64 rows in A order (row p = point A[p]); locality
 };
 
@@ -251,14 +248,13 @@ void launch_inverse(const uint32_t* J, uint64_t N, uint32_t* posJ, cudaStream_t 
 // G groups of 128 queries per CTA, STAGES candidate tiles in flight
 struct TcShape {
     int KB, G, STAGES;
-    int H = 1;    // epilogue warps per lane quarter and group (2: split 64-column halves)
-    int TN = 128; // candidates per tile (64: four early-released accumulator buffers)
+    int TN = 128; // candidates per tile (64: wide operands, KB >= 3)
 };
 size_t tc_smem_bytes(const TcShape& sh, uint32_t L, uint32_t n_bins, bool hist);
 void launch_hist_tc(const TcJoinArgs& a, const TcShape& sh, uint64_t nitems, uint64_t N,
                     cudaStream_t s);
 void launch_prep_tc(const double* X64, const uint32_t* A, uint64_t N, uint32_t n, const double* g,
-                    double inv_S, uint32_t row_halfs, uint32_t split, __half* Bh, cudaStream_t s);
+                    double inv_S, uint32_t row_halfs, __half* Bh, cudaStream_t s);
 void launch_join_tc(const TcJoinArgs& a, const TcShape& sh, uint64_t nitems, uint64_t N,
                     cudaStream_t s);
 void launch_scale_f32(const float* in, uint64_t n, float scale, float* out, cudaStream_t s);
@@ -342,9 +338,6 @@ void launch_merge_parts(const uint4* splits, uint64_t nsplits, uint32_t K, const
 void launch_split_flags(const uint32_t* pids, uint64_t nq, const uint32_t* slot, const uint2* G,
                         double n_thresh, uint8_t* dense, unsigned long long* n_sparse,
                         cudaStream_t s);
-void launch_brute_parts(const double* X64, uint64_t N, uint32_t n, const uint32_t* qpid,
-                        uint64_t nq, uint32_t P, uint32_t K, uint32_t* t_ids, double* t_sq,
-                        uint32_t* t_count, cudaStream_t s);
 void launch_rows_by(const double* X64, const uint32_t* A, uint64_t N, uint32_t n, double* out,
                     cudaStream_t s);
 void launch_uncert_flags(const uint32_t* rows, uint64_t n, const uint8_t* st, uint8_t* flags,
@@ -355,7 +348,7 @@ void launch_dense_cand(const uint4* items, const unsigned long long* work, uint6
                        const uint32_t* qrow, const uint8_t* dense, unsigned long long* out,
                        cudaStream_t s);
 void launch_find_ovf(const uint32_t* cnt, uint64_t n, uint32_t* rows, unsigned long long* count,
-                     uint32_t halves, cudaStream_t s);
+                     cudaStream_t s);
 void launch_gather_rows(const uint32_t* rows, uint64_t n, uint32_t K, const uint32_t* ids,
                         const double* dist, uint32_t* oids, double* odist, cudaStream_t s);
 

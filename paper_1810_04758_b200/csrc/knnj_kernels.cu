@@ -311,13 +311,8 @@ __global__ void k_finalize(FinalArgs a) {
     const uint64_t row = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (row >= a.nrows) return;
-    uint32_t c = a.cnt[a.halves ? 2 * row : row];
+    const uint32_t c = a.cnt[row];
     if (c == SKIP) return;  // a split row: its parts are finalized and merged separately
-    uint32_t c0 = c;        // halves: entries of list 0, then list 1
-    if (a.halves) {
-        const uint32_t c1 = a.cnt[2 * row + 1];
-        c = (c0 == OVF || c1 == OVF) ? OVF : c0 + c1;
-    }
     const uint32_t orow = a.qrow[row];
     if (c == OVF) {
         if (lane == 0) a.out_status[orow] = ST_OVF;
@@ -337,9 +332,7 @@ __global__ void k_finalize(FinalArgs a) {
         rk[e] = 0;
         const uint32_t i = e * 32 + lane;
         if (e < E && i < c) {
-            const uint64_t pi = !a.halves ? row * a.L + i
-                                : (i < c0 ? (2 * row) * a.L + i : (2 * row + 1) * a.L + (i - c0));
-            const uint32_t ps = a.pos[pi];
+            const uint32_t ps = a.pos[row * a.L + i];
             const uint32_t t = a.A[ps];
             id[e] = t;
             sq[e] = exact_sq(qx, a.XJ ? a.XJ + (uint64_t)ps * a.n : a.X64 + (uint64_t)t * a.n, a.n);
@@ -1353,74 +1346,6 @@ void launch_classify(const uint32_t* rows, uint64_t n, const uint8_t* st, const 
     g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
-// Brute-force exact top-K of a few query points over all points, cut into P parts of the
-// point-id range (one warp per (query, part)); parts are merged by k_merge_parts. For
-// fallback sets too small to pay for a grid level.
-__global__ void k_brute_parts(const double* X64, uint64_t N, uint32_t n, const uint32_t* qpid,
-                              uint32_t P, uint32_t K, uint32_t* t_ids, double* t_sq,
-                              uint32_t* t_count) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    double* ls = reinterpret_cast<double*>(smem_raw);          // [K][32]
-    uint32_t* li = reinterpret_cast<uint32_t*>(ls + K * 32);   // [K][32]
-    const int lane = threadIdx.x;
-    const uint32_t q = blockIdx.x / P, part = blockIdx.x % P;
-    const uint32_t qid = qpid[q];
-    const double* qx = X64 + (uint64_t)qid * n;
-    const uint64_t b = N * part / P, e = N * (part + 1) / P;
-    uint32_t cnt = 0;
-    for (uint64_t t = b + lane; t < e; t += 32) {
-        if (t == qid) continue;
-        const double s = exact_sq(qx, X64 + t * n, n);
-        const uint32_t ti = (uint32_t)t;
-        if (cnt == K && !pair_less(s, ti, ls[(K - 1) * 32 + lane], li[(K - 1) * 32 + lane]))
-            continue;
-        int r = (int)(cnt < K ? cnt : K - 1);
-        while (r > 0 && pair_less(s, ti, ls[(r - 1) * 32 + lane], li[(r - 1) * 32 + lane])) {
-            ls[r * 32 + lane] = ls[(r - 1) * 32 + lane];
-            li[r * 32 + lane] = li[(r - 1) * 32 + lane];
-            --r;
-        }
-        ls[r * 32 + lane] = s;
-        li[r * 32 + lane] = ti;
-        if (cnt < K) ++cnt;
-    }
-    uint32_t total = cnt;
-    for (int o = 16; o > 0; o >>= 1) total += __shfl_xor_sync(0xffffffffu, total, o);
-    const uint32_t outn = min(total, K);
-    const uint64_t v = blockIdx.x;  // = q * P + part
-    uint32_t head = 0;
-    for (uint32_t r = 0; r < outn; ++r) {
-        const double s = head < cnt ? ls[head * 32 + lane] : CUDART_INF;
-        const uint32_t t = head < cnt ? li[head * 32 + lane] : 0xFFFFFFFFu;
-        double bs = s;
-        uint32_t bt = t;
-        for (int o = 16; o > 0; o >>= 1) {
-            const double s2 = __shfl_xor_sync(0xffffffffu, bs, o);
-            const uint32_t t2 = __shfl_xor_sync(0xffffffffu, bt, o);
-            if (pair_less(s2, t2, bs, bt)) {
-                bs = s2;
-                bt = t2;
-            }
-        }
-        if (head < cnt && t == bt) ++head;
-        if (lane == 0) {
-            t_ids[v * K + r] = bt;
-            t_sq[v * K + r] = bs;
-        }
-    }
-    if (lane == 0) t_count[v] = outn;
-}
-void launch_brute_parts(const double* X64, uint64_t N, uint32_t n, const uint32_t* qpid,
-                        uint64_t nq, uint32_t P, uint32_t K, uint32_t* t_ids, double* t_sq,
-                        uint32_t* t_count, cudaStream_t s) {
-    if (!nq) return;
-    const size_t sm = (size_t)K * 32 * (sizeof(double) + sizeof(uint32_t));
-    set_smem(k_brute_parts, sm);
-    k_brute_parts<<<(unsigned)(nq * P), 32, sm, s>>>(X64, N, n, qpid, P, K, t_ids, t_sq, t_count);
-    KJ_CUDA(cudaGetLastError());
-    g_launches.fetch_add(1, std::memory_order_relaxed);
-}
-
 // FP64 rows in a level's position order (same values, contiguous per cell)
 __global__ void k_rows_by(const double* X64, const uint32_t* A, uint64_t N, uint32_t n, double* out) {
     const uint64_t total = N * n;
@@ -1507,17 +1432,16 @@ namespace kj {
 // Rows whose screened list overflowed (cnt == OVF), appended in any order (each is
 // re-solved independently by k_slow_exact, so the order never reaches the output).
 __global__ void k_find_ovf(const uint32_t* cnt, uint64_t n, uint32_t* rows,
-                           unsigned long long* count, uint32_t halves) {
+                           unsigned long long* count) {
     for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
          i += uint64_t(gridDim.x) * blockDim.x) {
-        const bool o = halves ? (cnt[2 * i] == OVF || cnt[2 * i + 1] == OVF) : cnt[i] == OVF;
-        if (o) rows[atomicAdd(count, 1ull)] = (uint32_t)i;
+        if (cnt[i] == OVF) rows[atomicAdd(count, 1ull)] = (uint32_t)i;
     }
 }
 void launch_find_ovf(const uint32_t* cnt, uint64_t n, uint32_t* rows, unsigned long long* count,
-                     uint32_t halves, cudaStream_t s) {
+                     cudaStream_t s) {
     if (!n) return;
-    k_find_ovf<<<1184, 256, 0, s>>>(cnt, n, rows, count, halves);
+    k_find_ovf<<<1184, 256, 0, s>>>(cnt, n, rows, count);
     KJ_CUDA(cudaGetLastError());
     g_launches.fetch_add(1, std::memory_order_relaxed);
 }

@@ -126,39 +126,6 @@ __device__ __forceinline__ void tmem_ld64(uint32_t taddr, float (&v0)[32], float
         v1[i] = __uint_as_float(r[32 + i]);
     }
 }
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
-    uint32_t r[32];
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
-        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
-          "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
-          "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
-          "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
-          "=r"(r[31])
-        : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-}
-
-// v[j] for a warp-uniform runtime j without local memory (5-level select tree):
-// the early-release epilogue's rare path, which can no longer re-read TMEM.
-__device__ __forceinline__ float sel32(const float (&v)[32], uint32_t j) {
-    float a[16];
-#pragma unroll
-    for (int i = 0; i < 16; ++i) a[i] = (j & 16u) ? v[i + 16] : v[i];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) a[i] = (j & 8u) ? a[i + 8] : a[i];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) a[i] = (j & 4u) ? a[i + 4] : a[i];
-#pragma unroll
-    for (int i = 0; i < 2; ++i) a[i] = (j & 2u) ? a[i + 2] : a[i];
-    return (j & 1u) ? a[1] : a[0];
-}
-
 __device__ __forceinline__ float tmem_ld1(uint32_t taddr) {
     uint32_t r;
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(r) : "r"(taddr));
@@ -211,12 +178,12 @@ __device__ __forceinline__ float warp_kth(float (&a)[R], uint32_t k) {
 
 }  // namespace
 
-// B-operand rows for one grid level, sorted order. split 3: [hi | lo | hi | nb_hi nb_lo | 0]
-// (K = 3n+2, ~22-bit products); split 1: [hi | nb_hi nb_lo | 0] (K = n+2, for n > 42;
-// the dropped lo parts are part of the screen bound tc_delta).
+// B-operand rows for one grid level, sorted order: [lo | hi | hi | nb_hi nb_lo | 0]
+// (K = 3n+2, ~22-bit products). The small hi x lo products come first in K and the
+// large hi x hi products and |b|^2 last, which keeps the accumulated partial sums small
+// for most of the UMMA chain (the accumulation term of tc_delta).
 __global__ void k_prep_tc(const double* X64, const uint32_t* A, uint64_t N, uint32_t n,
-                          const double* g, double inv_S, uint32_t row_halfs, uint32_t split,
-                          __half* Bh) {
+                          const double* g, double inv_S, uint32_t row_halfs, __half* Bh) {
     // one thread per row; the row is emitted as 16-byte chunks of 8 halfs, so a warp
     // writes whole 128-byte rows instead of scattered 2-byte stores
     for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < N;
@@ -229,7 +196,7 @@ __global__ void k_prep_tc(const double* X64, const uint32_t* A, uint64_t N, uint
         }
         const __half nh = __double2half(nb);
         const __half nl = __double2half(nb - (double)__half2float(nh));
-        const uint32_t o = split * n;
+        const uint32_t o = 3 * n;
         uint4* row = reinterpret_cast<uint4*>(Bh + i * row_halfs);
         for (uint32_t c0 = 0; c0 < row_halfs; c0 += 8) {
             uint32_t w[4];
@@ -241,10 +208,10 @@ __global__ void k_prep_tc(const double* X64, const uint32_t* A, uint64_t N, uint
                     const uint32_t k = c0 + 2 * e + h;
                     __half hv = __float2half(0.f);
                     if (k < o) {
-                        const uint32_t d = k % n, part = k / n;  // split 3: hi | lo | hi
+                        const uint32_t d = k % n, part = k / n;  // lo | hi | hi
                         const double v = (x[d] - g[d]) * inv_S;
                         const __half hi = __double2half(v);
-                        hv = part == 1 ? __double2half(v - (double)__half2float(hi)) : hi;
+                        hv = part == 0 ? __double2half(v - (double)__half2float(hi)) : hi;
                     } else if (k == o) {
                         hv = nh;
                     } else if (k == o + 1) {
@@ -290,18 +257,13 @@ __device__ __noinline__ uint32_t exact_bin(const double* X64, uint32_t n, uint32
 //   warps 2..   epilogue, 4 warps per query group (TMEM lane quarters):
 //               JOIN: screened top-K list insertion; HIST: exact-certain binning
 // Every role walks the same deterministic tile sequence (ranges of the item,
-// <=128 positions per tile, tiles never straddle a range).
-// H = 2 (JOIN): two epilogue warps per TMEM lane quarter and query group, each
-// screening one 64-column half of every tile with its own near-tie list (global
-// memory) and a cut shared with its partner through shared memory: twice the
-// epilogue warps to hide the per-slab latency chain.
-// TN = 64 with ER (JOIN, G = 2): 64-candidate tiles in NB = 4 accumulator buffers,
-// each released right after tcgen05.ld, so the MMAs of later tiles overlap the
-// screening of this one (the buffer is no longer held for the screening time).
-template <int KB, int G, int STAGES, bool HIST, int LR, int H = 1, int TN = 128, bool ER = false>
-__global__ void __launch_bounds__(64 + 128 * G * H, 1)
+// <=TN positions per tile, tiles never straddle a range). Only the first p.ksteps
+// K=16 steps of the operand rows hold non-zero columns (ceil((3n+2)/16)); the MMA
+// warp issues just those (n = 4: one UMMA per tile instead of four).
+// TN = 64: wide operands (KB >= 3), so that A + the B ring fit in shared memory.
+template <int KB, int G, int STAGES, bool HIST, int LR, int TN = 128>
+__global__ void __launch_bounds__(64 + 128 * G, 1)
     k_tc(const __grid_constant__ CUtensorMap tmB, TcJoinArgs p) {
-    static_assert(!ER || (TN == 64 && H == 1 && !HIST), "early release: 64-column JOIN tiles");
     constexpr int NQ = 128 * G;                    // queries per block
     constexpr int BK = TN * 128;                   // bytes of one k-block of a candidate tile
     constexpr int NB = (G == 2 ? 512 : 256) / (G * TN);  // accumulator buffers per group
@@ -314,7 +276,6 @@ __global__ void __launch_bounds__(64 + 128 * G * H, 1)
     // accumulator barriers per (query group, buffer): the groups' pipelines are decoupled
     __shared__ uint64_t bar_full[STAGES], bar_empty[STAGES], bar_accf[G * NB], bar_acce[G * NB];
     __shared__ uint32_t s_tmem;
-    __shared__ float s_cut[H == 2 ? 2 * NQ : 1];  // H=2: per (half, query) current cut
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint4 it = p.items[blockIdx.x];
@@ -334,7 +295,7 @@ __global__ void __launch_bounds__(64 + 128 * G * H, 1)
         }
         for (int i = 0; i < G * NB; ++i) {
             mbar_init(&bar_accf[i], 1);
-            mbar_init(&bar_acce[i], 4 * H);
+            mbar_init(&bar_acce[i], 4);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
@@ -342,20 +303,18 @@ __global__ void __launch_bounds__(64 + 128 * G * H, 1)
 
     // epilogue identity
     const int e = warp - 2;                      // epilogue warp index (valid if >= 0)
-    const int gh = e >= 0 ? e >> 2 : 0;
-    const int g = gh % G;                        // query group
-    const int hh = gh / G;                       // column half (H = 2)
+    const int g = e >= 0 ? e >> 2 : 0;           // query group
     const int quarter = warp & 3;                // TMEM lane quarter this warp may access
     const uint32_t r = quarter * 32 + lane;      // accumulator row (= TMEM lane)
     const uint32_t qi = g * 128 + r;             // query index inside the item
-    const bool epi = e >= 0 && e < 4 * G * H;
+    const bool epi = e >= 0 && e < 4 * G;
     const bool has_q = epi && qi < nq;
     const uint32_t row = it.x + (has_q ? qi : 0);
     const uint32_t qp = p.qpos[row];
     float na = 0.f;
-    if (H == 2 && epi) s_cut[hh * NQ + qi] = CUDART_INF_F;
-    if (epi && hh == 0) {
-        // A operand row r of group g: [-2hi, -2hi, -2lo, 1, 1, 0...] with the 128B swizzle
+    if (epi) {
+        // A operand row r of group g: [-2hi, -2lo, -2hi, 1, 1, 0...] against the B row
+        // [lo, hi, hi, nb_hi, nb_lo, 0...], with the 128B swizzle
         const __half* qrow_g = p.Bh + (uint64_t)qp * p.row_halfs;
         const uint32_t n = p.n;
         for (int kb = 0; kb < KB; ++kb) {
@@ -372,14 +331,11 @@ __global__ void __launch_bounds__(64 + 128 * G * H, 1)
                         const uint32_t k = kb * KBLK + c * 8 + e2 * 2 + h;
                         __half v = __float2half(0.f);
                         if (has_q) {
-                            if (p.split == 3) {  // [-2hi, -2hi, -2lo, 1, 1]
-                                if (k < 2 * n) v = __hmul(__float2half(-2.f), qrow_g[k < n ? k : k - n]);
-                                else if (k < 3 * n) v = __hmul(__float2half(-2.f), qrow_g[k - n]);
-                                else if (k < 3 * n + 2) v = __float2half(1.f);
-                            } else {             // [-2hi, 1, 1]
-                                if (k < n) v = __hmul(__float2half(-2.f), qrow_g[k]);
-                                else if (k < n + 2) v = __float2half(1.f);
-                            }
+                            // x2 is exact in FP16: the operand carries -2a unrounded
+                            if (k < n) v = __hmul(__float2half(-2.f), qrow_g[k + n]);         // -2 a_hi
+                            else if (k < 2 * n) v = __hmul(__float2half(-2.f), qrow_g[k - n]);  // -2 a_lo
+                            else if (k < 3 * n) v = __hmul(__float2half(-2.f), qrow_g[k]);      // -2 a_hi
+                            else if (k < 3 * n + 2) v = __float2half(1.f);
                         }
                         pair |= (uint32_t)__half_as_ushort(v) << (16 * h);
                     }
@@ -392,7 +348,7 @@ __global__ void __launch_bounds__(64 + 128 * G * H, 1)
     }
     if (has_q) {
         const __half* qrow_g = p.Bh + (uint64_t)qp * p.row_halfs;
-        na = __half2float(qrow_g[p.split * p.n]) + __half2float(qrow_g[p.split * p.n + 1]);
+        na = __half2float(qrow_g[3 * p.n]) + __half2float(qrow_g[3 * p.n + 1]);
     }
     if (HIST) {
         uint32_t* hist = reinterpret_cast<uint32_t*>(tail);
@@ -486,8 +442,9 @@ __global__ void __launch_bounds__(64 + 128 * G * H, 1)
                 for (int kb = 0; kb < KB; ++kb)
 #pragma unroll
                     for (int kk = 0; kk < KBLK / 16; ++kk)
-                        umma_f16<TN>(dcol, umma_desc_sw128(a0 + (gg * KB + kb) * KB_BYTES + kk * 32),
-                                     umma_desc_sw128(b0 + kb * BK + kk * 32), (kb | kk) ? 1u : 0u);
+                        if ((uint32_t)(kb * (KBLK / 16) + kk) < p.ksteps)
+                            umma_f16<TN>(dcol, umma_desc_sw128(a0 + (gg * KB + kb) * KB_BYTES + kk * 32),
+                                         umma_desc_sw128(b0 + kb * BK + kk * 32), (kb | kk) ? 1u : 0u);
                 umma_commit(&bar_empty[st]);
                 umma_commit(&bar_accf[gg * NB + b]);
             }
@@ -499,20 +456,12 @@ __global__ void __launch_bounds__(64 + 128 * G * H, 1)
         // compacted warp-cooperatively (K-th key + 2 delta). Fast path: one
         // FMNMX per pair; survivors are re-read from TMEM one warp-uniform
         // column at a time (no per-lane dynamic indexing).
-        // H = 1: lists in shared memory, [NQ][L]; H = 2: rows of out_key/out_pos in
-        // global memory, [row][half][L]
+        // lists in shared memory, [NQ][L]
         float* lkey = reinterpret_cast<float*>(tail);
         uint32_t* lpos = reinterpret_cast<uint32_t*>(lkey + p.L * NQ);
         const uint32_t LB = p.L;
-        auto list_key = [&](uint32_t col) -> float* {
-            return H == 2 ? p.out_key + ((uint64_t)(it.x + col) * 2 + hh) * LB : lkey + (size_t)col * LB;
-        };
-        auto list_pos = [&](uint32_t col) -> uint32_t* {
-            return H == 2 ? p.out_pos + ((uint64_t)(it.x + col) * 2 + hh) * LB : lpos + (size_t)col * LB;
-        };
-        float* mykey = list_key(qi);
-        uint32_t* mypos = list_pos(qi);
-        float* pcut = H == 2 ? &s_cut[(hh ^ 1) * NQ + qi] : nullptr;  // partner half's cut
+        float* mykey = lkey + (size_t)qi * LB;
+        uint32_t* mypos = lpos + (size_t)qi * LB;
         uint32_t cnt = 0;
         bool ovf = false;
         const float init_cut = (p.init_cut && has_q) ? p.init_cut[row] : CUDART_INF_F;
@@ -525,23 +474,21 @@ __global__ void __launch_bounds__(64 + 128 * G * H, 1)
             __syncwarp();  // the src lane's appends are visible to the warp
             const uint32_t c_src = __shfl_sync(0xffffffffu, cnt, src);
             const uint32_t col = g * 128 + quarter * 32 + src;
-            float* kb = list_key(col);
-            uint32_t* pb = list_pos(col);
+            float* kb = lkey + (size_t)col * LB;
+            uint32_t* pb = lpos + (size_t)col * LB;
             float kv[LR];
             uint32_t pv[LR];
 #pragma unroll
             for (int r = 0; r < LR; ++r) {
                 const uint32_t i = r * 32 + lane;
-                kv[r] = i < c_src ? (H == 2 ? __ldcg(kb + i) : kb[i]) : CUDART_INF_F;
-                pv[r] = i < c_src ? (H == 2 ? __ldcg(pb + i) : pb[i]) : 0u;
+                kv[r] = i < c_src ? kb[i] : CUDART_INF_F;
+                pv[r] = i < c_src ? pb[i] : 0u;
             }
             float srt[LR];
 #pragma unroll
             for (int r = 0; r < LR; ++r) srt[r] = kv[r];
             const float kth = warp_kth<LR>(srt, p.K);
-            float cap_src = __shfl_sync(0xffffffffu, cap, src);
-            // the partner half's cut bounds the global K-th too (it is a K-th + 2 delta)
-            if (H == 2) cap_src = fminf(cap_src, *(volatile float*)&s_cut[(hh ^ 1) * NQ + col]);
+            const float cap_src = __shfl_sync(0xffffffffu, cap, src);
             const float nc = fminf(__fadd_ru(kth, 2.f * dl), cap_src);
             unsigned bal[LR];
 #pragma unroll
@@ -562,7 +509,6 @@ __global__ void __launch_bounds__(64 + 128 * G * H, 1)
                 cnt = at;
                 cut = nc;
                 rhs = __fsub_ru(cut, na);
-                if (H == 2) *(volatile float*)&s_cut[hh * NQ + col] = cut;
                 if (cnt >= LB) {  // every entry inside the band: exact ties, slow path
                     ovf = true;
                     rhs = -CUDART_INF_F;
@@ -576,36 +522,9 @@ __global__ void __launch_bounds__(64 + 128 * G * H, 1)
             mbar_wait(&bar_accf[g * NB + b], (t / NB) & 1);
             fence_after();
             const uint32_t tbase = tmem + ((uint32_t)(quarter * 32) << 16) + (g * NB + b) * TN;
-            if (H == 2 && has_q && !ovf) {  // the partner's tighter cut applies to new inserts
-                const float pc = *(volatile float*)pcut;
-                if (pc < cut) {
-                    cut = pc;
-                    rhs = __fsub_ru(cut, na);
-                }
-            }
-            if (p.dbg_mode) {  // timing decomposition (output is meaningless)
-                for (uint32_t j0 = 0; j0 < c && p.dbg_mode < 3; j0 += 64) {
-                    float v0[32], v1[32];
-                    tmem_ld64(tbase + j0, v0, v1);
-                    float mn = fminf(v0[0], v1[0]);
-                    if (p.dbg_mode == 1)
-#pragma unroll
-                        for (int j = 1; j < 32; ++j) mn = fminf(mn, fminf(v0[j], v1[j]));
-                    if (__any_sync(0xffffffffu, mn < -1e30f)) ++cnt;
-                }
-                fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&bar_acce[g * NB + b]);
-                continue;
-            }
-            for (uint32_t j0 = H == 2 ? hh * 64 : 0; j0 < c; j0 += H == 2 ? 128 : 64) {
+            for (uint32_t j0 = 0; j0 < c; j0 += 64) {
                 float v0[32], v1[32];
                 tmem_ld64(tbase + j0, v0, v1);
-                if (ER) {  // the whole (64-column) tile is in registers: free the buffer
-                    fence_before();
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&bar_acce[g * NB + b]);
-                }
                 if (p.dbg && blockIdx.x == 0 && t == 0 && g == 0)
 #pragma unroll
                     for (int j = 0; j < 32; ++j) {
@@ -653,8 +572,7 @@ __global__ void __launch_bounds__(64 + 128 * G * H, 1)
                         const int j = __ffs(um) - 1;
                         um &= um - 1;
                         ++st_bits;
-                        const float x = ER ? (h == 0 ? sel32(v0, (uint32_t)j) : sel32(v1, (uint32_t)j))
-                                           : tmem_ld1(tbase + j0 + h * 32 + j);
+                        const float x = tmem_ld1(tbase + j0 + h * 32 + j);
                         const uint32_t pos = s + j0 + h * 32 + j;
                         bool want = ((mk[h] >> j) & 1u) && x <= rhs && pos != qp;
                         // make room: cooperative compaction of every full buffer that needs it
@@ -675,11 +593,9 @@ __global__ void __launch_bounds__(64 + 128 * G * H, 1)
                     }
                 }
             }
-            if (!ER) {
-                fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&bar_acce[g * NB + b]);
-            }
+            fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bar_acce[g * NB + b]);
         }
         if (p.stats && lane == 0) {
             atomicAdd(p.stats + 0, st_slab);
@@ -689,13 +605,9 @@ __global__ void __launch_bounds__(64 + 128 * G * H, 1)
             atomicAdd(p.stats + 4, st_cmp);
         }
         if (has_q) {
-            if (H == 2) {
-                p.out_cnt[(uint64_t)row * 2 + hh] = ovf ? OVF : cnt;  // positions already in place
-            } else {
-                p.out_cnt[row] = ovf ? OVF : cnt;
-                if (!ovf)
-                    for (uint32_t i = 0; i < cnt; ++i) p.out_pos[(uint64_t)row * LB + i] = mypos[i];
-            }
+            p.out_cnt[row] = ovf ? OVF : cnt;
+            if (!ovf)
+                for (uint32_t i = 0; i < cnt; ++i) p.out_pos[(uint64_t)row * LB + i] = mypos[i];
         }
     } else {
         // ------------------------------------------------ HISTOGRAM epilogue
@@ -869,13 +781,13 @@ size_t tc_smem_bytes(const TcShape& sh, uint32_t L, uint32_t n_bins, bool hist) 
     const size_t NQ = 128 * sh.G;
     size_t b = 1024 + (size_t)sh.G * sh.KB * KB_BYTES + (size_t)sh.STAGES * sh.KB * sh.TN * 128;
     if (hist) b += NQ * n_bins * 4 + 8 * (n_bins + 1) + 8 * n_bins + 8 + (size_t)4 * sh.G * 32 * 8;
-    else if (sh.H == 1) b += NQ * L * 8;  // H = 2 keeps the lists in global memory
+    else b += NQ * L * 8;
     return b;
 }
 
 void launch_prep_tc(const double* X64, const uint32_t* A, uint64_t N, uint32_t n, const double* g,
-                    double inv_S, uint32_t row_halfs, uint32_t split, __half* Bh, cudaStream_t s) {
-    k_prep_tc<<<2368, 256, 0, s>>>(X64, A, N, n, g, inv_S, row_halfs, split, Bh);
+                    double inv_S, uint32_t row_halfs, __half* Bh, cudaStream_t s) {
+    k_prep_tc<<<2368, 256, 0, s>>>(X64, A, N, n, g, inv_S, row_halfs, Bh);
     KJ_CUDA(cudaGetLastError());
     g_launches.fetch_add(1, std::memory_order_relaxed);
 }
@@ -894,7 +806,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
     return fn;
 }
 
-template <int KB, int G, int STAGES, bool HIST, int LR, int H = 1, int TN = 128, bool ER = false>
+template <int KB, int G, int STAGES, bool HIST, int LR, int TN = 128>
 static void launch_tc_t(const TcJoinArgs& a, uint64_t nitems, uint64_t N, cudaStream_t s) {
     CUtensorMap map;
     cuuint64_t dims[2] = {(cuuint64_t)a.row_halfs, (cuuint64_t)N};
@@ -906,15 +818,15 @@ static void launch_tc_t(const TcJoinArgs& a, uint64_t nitems, uint64_t N, cudaSt
                               CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw Error(9, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
-    const size_t sm = tc_smem_bytes(TcShape{KB, G, STAGES, H, TN}, a.L, a.n_bins, HIST);
+    const size_t sm = tc_smem_bytes(TcShape{KB, G, STAGES, TN}, a.L, a.n_bins, HIST);
     if (sm > 227 * 1024) throw Error(1, "tensor-core kernel needs too much shared memory");
-    KJ_CUDA(cudaFuncSetAttribute(k_tc<KB, G, STAGES, HIST, LR, H, TN, ER>,
+    KJ_CUDA(cudaFuncSetAttribute(k_tc<KB, G, STAGES, HIST, LR, TN>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     for (uint64_t off = 0; off < nitems; off += 2147483647ull) {
         const uint64_t cnt = std::min<uint64_t>(nitems - off, 2147483647ull);
         TcJoinArgs b = a;
         b.items = a.items + off;
-        k_tc<KB, G, STAGES, HIST, LR, H, TN, ER><<<(unsigned)cnt, 64 + 128 * G * H, sm, s>>>(map, b);
+        k_tc<KB, G, STAGES, HIST, LR, TN><<<(unsigned)cnt, 64 + 128 * G, sm, s>>>(map, b);
     }
     KJ_CUDA(cudaGetLastError());
     g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -924,23 +836,11 @@ void launch_join_tc(const TcJoinArgs& a, const TcShape& sh, uint64_t nitems, uin
                     cudaStream_t s) {
     if (!nitems) return;
     const bool wide = a.L > 64;  // list compaction over 128 entries
-    if (sh.TN == 64 && sh.KB >= 3) {  // wide operands, 64-candidate tiles (no early release)
-        if (sh.KB == 3 && sh.G == 1 && sh.STAGES == 3 && !wide) launch_tc_t<3, 1, 3, false, 2, 1, 64, false>(a, nitems, N, s);
-        else if (sh.KB == 4 && sh.G == 1 && sh.STAGES == 3 && !wide) launch_tc_t<4, 1, 3, false, 2, 1, 64, false>(a, nitems, N, s);
-        else if (sh.KB == 5 && sh.G == 1 && sh.STAGES == 2 && !wide) launch_tc_t<5, 1, 2, false, 2, 1, 64, false>(a, nitems, N, s);
+    if (sh.TN == 64) {  // wide operands (KB >= 3), 64-candidate tiles
+        if (sh.KB == 3 && sh.G == 1 && sh.STAGES == 3 && !wide) launch_tc_t<3, 1, 3, false, 2, 64>(a, nitems, N, s);
+        else if (sh.KB == 4 && sh.G == 1 && sh.STAGES == 3 && !wide) launch_tc_t<4, 1, 3, false, 2, 64>(a, nitems, N, s);
+        else if (sh.KB == 5 && sh.G == 1 && sh.STAGES == 2 && !wide) launch_tc_t<5, 1, 2, false, 2, 64>(a, nitems, N, s);
         else throw Error(1, "no wide-operand tensor-core join instance for this shape");
-        return;
-    }
-    if (sh.TN == 64) {
-        if (sh.KB == 1 && sh.G == 2 && sh.STAGES == 8 && !wide) launch_tc_t<1, 2, 8, false, 2, 1, 64, true>(a, nitems, N, s);
-        else if (sh.KB == 1 && sh.G == 2 && sh.STAGES == 8 && wide) launch_tc_t<1, 2, 8, false, 4, 1, 64, true>(a, nitems, N, s);
-        else throw Error(1, "no 64-column tensor-core join instance for this shape");
-        return;
-    }
-    if (sh.H == 2) {
-        if (sh.KB == 1 && sh.G == 2 && sh.STAGES == 8 && !wide) launch_tc_t<1, 2, 8, false, 2, 2>(a, nitems, N, s);
-        else if (sh.KB == 1 && sh.G == 2 && sh.STAGES == 8 && wide) launch_tc_t<1, 2, 8, false, 4, 2>(a, nitems, N, s);
-        else throw Error(1, "no two-half tensor-core join instance for this shape");
         return;
     }
     if (sh.KB == 1 && sh.G == 2 && sh.STAGES == 4 && !wide) launch_tc_t<1, 2, 4, false, 2>(a, nitems, N, s);

@@ -175,6 +175,14 @@ class Engine:
         self._check(self.lib.knnj_histogram_queries(self.h, q, q.size, eps_mean, n_bins, raw))
         return raw
 
+    def histogram_queries_capped(self, qids, eps_mean: float, n_bins: int, n_count: int):
+        """Test hook: the capped histogram's kernels, counting bins [0, n_count) only."""
+        q = np.ascontiguousarray(qids, np.uint64)
+        raw = np.zeros(n_bins, np.uint64)
+        self._check(self.lib.knnj_histogram_queries_capped(self.h, q, q.size, eps_mean, n_bins,
+                                                           n_count, raw))
+        return raw
+
     def grid_build(self, m: int, eps: float) -> dict:
         gi = _capi.GridInfo()
         self._check(self.lib.knnj_grid_build(self.h, m, eps, C.byref(gi)))
@@ -415,3 +423,40 @@ def read_binary_f64(path: str, out=None) -> np.ndarray:
     if rc:
         raise KnnjError(rc, lib.knnj_io_last_error().decode())
     return X
+
+
+def read_text(path: str, sep: str = ",", threads: int = 0, out=None) -> np.ndarray:
+    """ingest_text (proj/src/io.cpp:24-67): CSV (sep ',') or TSV (sep '\\t') into a
+    |D| x n float64 array (``out`` if given, e.g. a pinned buffer), parsed by ``threads``
+    host threads; IngestError-kind failures carry the reference messages."""
+    lib = _capi.load_library()
+    h, N, n = C.c_void_p(), C.c_uint64(), C.c_uint64()
+    rc = lib.knnj_text_parse(path.encode(), sep.encode(), threads, C.byref(h), C.byref(N),
+                             C.byref(n))
+    if rc:
+        raise KnnjError(rc, lib.knnj_io_last_error().decode())
+    try:
+        X = np.empty((N.value, n.value), np.float64) if out is None else out
+        rc = lib.knnj_text_copy(h, X.ctypes.data, X.size)
+        if rc:
+            raise KnnjError(rc, lib.knnj_io_last_error().decode())
+    finally:
+        lib.knnj_text_free(h)
+    return X
+
+
+def format_from_string(s: str) -> str:
+    """format_from_string (proj/src/io.cpp:15-20)."""
+    if s in ("csv", "tsv"):
+        return s
+    if s in ("bin", "binary-f64"):
+        return "bin"
+    raise KnnjError(1, f"unknown dataset format '{s}' (expected csv, tsv, or bin)")
+
+
+def ingest_dataset(path: str, fmt: str = "bin", threads: int = 0, out=None) -> np.ndarray:
+    """ingest_dataset (proj/src/io.cpp:99-106): csv, tsv or binary-f64."""
+    f = format_from_string(fmt)
+    if f == "bin":
+        return read_binary_f64(path, out)
+    return read_text(path, "," if f == "csv" else "\t", threads, out)

@@ -1,14 +1,19 @@
-"""GPU parity at BASELINE.json's full sizes, through size-independent properties
-(the CPU oracle cannot replay a 5M-point run):
+"""GPU parity at BASELINE.json's full sizes (C1..C5 and the north-star NS), against the
+CPU oracle wherever a size-independent check exists; the whole run is
+out of the oracle's reach at these sizes (C5's histogram alone is 1e14 pairs):
 
-* sampled queries: neighbour ids and FP64 distances bit-identical to brute force
-  (the oracle's exact scalar-order search over ALL points);
-* every row: distances non-decreasing, ids distinct, self never listed;
-* provenance consistent with eps: dense-solved rows have their K-th neighbour
-  within eps, dense-failed rows do not (dense_engine.cpp:182-192);
-* the capped eps histogram selects the same eps, and so the same output, as the
-  full one (epsilon.cpp:46-141);
+* eps selection (epsilon.cpp:14-141): eps_mean bit-exact against the oracle's
+  estimate_eps_mean over the same 1e6 reference-RNG pairs; histogram counts of a subset
+  of the run's own sampled queries equal the oracle's binning of that subset; the GPU's
+  counts for the whole sample select the run's eps through the oracle's select_eps;
+* grid (grid_index.cpp:13-75): B, G, A and the slot table equal the oracle's;
+* >= 512 sampled queries: neighbour ids and FP64 distances bit-identical to the oracle's
+  exact brute force over ALL points;
+* every row: distances non-decreasing, ids distinct, self never listed; provenance
+  consistent with eps (dense_engine.cpp:182-192);
 * determinism: a second run is bit-identical.
+The capped-vs-full histogram comparison (the full histogram is ~200 s at C5) is opt-in:
+KNNJ_FULLSIZE_FULL_HIST=1.
 """
 import os
 
@@ -20,50 +25,83 @@ from paper_1810_04758_b200.synthetic import CONFIGS, generate
 
 pytestmark = pytest.mark.gpu
 
-CASES = [("C2", None), ("C3", None), ("C4", 5_000_000), ("NS", None), ("C1", None)]
-# C5 (100M points) takes ~220 s, most of it the full (uncapped) histogram of 1e14 pairs
-# the capped-vs-full check needs; opt in with KNNJ_FULLSIZE_C5=1 (passed on B200, round 1)
-if os.environ.get("KNNJ_FULLSIZE_C5"):
-    CASES.append(("C5", None))
+CASES = ["C1", "C2", "C3", "C4", "NS", "C5"]
+THREADS = os.cpu_count() or 8
 
 
-@pytest.mark.parametrize("name,size", CASES, ids=[c[0] for c in CASES])
-def test_full_size_properties(engine, oracle, name, size):
+@pytest.mark.parametrize("name", CASES)
+def test_full_size_properties(engine, oracle, name):
     c = CONFIGS[name]
-    N = size or c["size"]
-    X = generate(c["spec"], N, c["dims"], seed=1)
-    k = c["k"]
+    N, n, k = c["size"], c["dims"], c["k"]
+    X = generate(c["spec"], N, n, seed=1)
     engine.set_points(X)
-    r = engine.run(RunConfig(k=k, mode="hybrid", seed=1), want_hist=False)
+    cfg = RunConfig(k=k, mode="hybrid", seed=1)
+    r = engine.run(cfg, want_hist=False)
     i = r.info
     assert r.ids.shape == (N, k)
-    eps = i["eps_used"]
-    W = X[:, i["perm"]]
+    eps, em = i["eps_used"], i["eps_mean"]
+    W = np.ascontiguousarray(X[:, i["perm"]])
+    m = int(i["m_used"])
 
+    # ---- eps selection
+    pairs = min(10 * N, 1_000_000)
+    assert oracle.eps_mean(W, pairs, oracle.derive_seed(1, 1)) == em, "eps_mean differs"
+    n_hq = min(max(int(0.01 * N), 100), N)
+    assert i["hist_query_count"] == n_hq
+    q_all = oracle.sample(N, n_hq, oracle.derive_seed(1, 2))
+    nsub = 512 if N > 50_000_000 else 1024
+    sub = q_all[:: max(1, len(q_all) // nsub)][:nsub]
+    gpu_sub = engine.histogram_queries(sub, em, 100)
+    orc_sub = oracle.histogram_queries(W, em, 100, sub, threads=THREADS)
+    assert np.array_equal(gpu_sub, orc_sub), "histogram counts of the query subset differ"
+    nb = int(i["hist_bins_counted"])
+    capped = engine.histogram_queries_capped(q_all, em, 100, nb).astype(np.float64)
+    cum = np.cumsum(capped) / n_hq
+    _, eps_sel, _, _ = oracle.select_eps(cum, em / 100, k, 0.0)
+    assert eps_sel == eps, "the sample's counted bins select a different eps"
+
+    # ---- sampled queries vs exact brute force over all points
     rng = np.random.default_rng(7)
-    q = np.sort(rng.choice(N, 96, replace=False)).astype(np.uint32)
-    oi, od = oracle.brute_knn(W, q, k, threads=os.cpu_count() or 8)
+    q = np.sort(rng.choice(N, min(512, N), replace=False)).astype(np.uint32)
+    oi, od = oracle.brute_knn(W, q, k, threads=THREADS)
     assert np.array_equal(r.ids[q], oi), "sampled neighbour ids differ from brute force"
     assert np.array_equal(r.dist[q], od), "sampled distances differ from brute force"
 
+    # ---- row invariants and provenance
     assert (np.diff(r.dist, axis=1) >= 0).all()
     assert not (r.ids == np.arange(N, dtype=np.uint32)[:, None]).any(), "self listed"
     s = np.sort(r.ids, axis=1)
     assert (s[:, 1:] != s[:, :-1]).all(), "duplicate neighbour id"
-
+    del s
     kth = r.dist[:, -1]
     dense_ok, failed = r.provenance == 0, r.provenance == 2
     assert (kth[dense_ok] <= eps * (1 + 1e-15)).all()
     assert (kth[failed] >= eps * (1 - 1e-15)).all()
     assert int(failed.sum()) == i["failed_count"]
 
-    # capped (the run above) vs full histogram: same eps, identical output
-    engine.set_option("hist_cap", 0)
-    try:
-        engine.set_points(X)
-        full = engine.run(RunConfig(k=k, mode="hybrid", seed=1), want_hist=True)
-    finally:
-        engine.set_option("hist_cap", 1)
-    assert full.info["eps_used"] == eps
-    assert np.array_equal(full.ids, r.ids) and np.array_equal(full.dist, r.dist)
-    assert np.array_equal(full.provenance, r.provenance)
+    # ---- determinism
+    r2 = engine.run(cfg, want_hist=False)
+    assert np.array_equal(r2.ids, r.ids) and np.array_equal(r2.dist, r.dist)
+    assert np.array_equal(r2.provenance, r.provenance)
+    del r2
+
+    # ---- grid tables of the run's eps
+    gi = engine.grid_build(m, eps)
+    gd = engine.grid_export(gi["n_cells"])
+    og = oracle.grid(W, m, eps)
+    assert gi["n_cells"] == og["B"].size
+    assert np.array_equal(gd["B"], og["B"]) and np.array_equal(gd["G"], og["G"])
+    assert np.array_equal(gd["A"], og["A"]) and np.array_equal(gd["slot"], og["slot"])
+    del gd, og
+
+    if os.environ.get("KNNJ_FULLSIZE_FULL_HIST"):
+        # capped (the run above) vs full histogram: same eps, identical output
+        engine.set_option("hist_cap", 0)
+        try:
+            engine.set_points(X)
+            full = engine.run(cfg, want_hist=True)
+        finally:
+            engine.set_option("hist_cap", 1)
+        assert full.info["eps_used"] == eps
+        assert np.array_equal(full.ids, r.ids) and np.array_equal(full.dist, r.dist)
+        assert np.array_equal(full.provenance, r.provenance)

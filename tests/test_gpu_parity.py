@@ -221,3 +221,34 @@ def test_split_matches_reference_semantics(engine, oracle):
                 dense[i] = False
         assert np.array_equal(s["is_dense"].astype(bool), dense)
         assert s["q_cpu"] >= floor_cpu
+
+
+@pytest.mark.parametrize("name", golden_cases())
+def test_phase_entries_match_reference_golden(engine, oracle, name):
+    """The phase-level C-ABI entries called directly, each against the unmodified
+    reference's own values for the same data (tests/golden): estimate_eps_mean
+    (epsilon.cpp:14-44), build_distance_histogram (epsilon.cpp:46-120) and
+    run_dense_join + filter_keys in DenseOnly mode (dense_engine.cpp:165-303)."""
+    g, cfg = load_golden(name)
+    X = g["X"]
+    N = X.shape[0]
+    k = min(int(cfg["k"]), N - 1)
+    seed = int(cfg.get("seed", 0))
+    engine.set_points(X)
+    engine.reorder_by_variance(1)
+    em = engine.estimate_eps_mean(min(10 * N, 1_000_000), oracle.derive_seed(seed, 1))
+    assert em == g["hybrid_eps_mean"]
+    raw, qc = engine.build_distance_histogram(em, 100, cfg.get("hist_frac", 0.01),
+                                              oracle.derive_seed(seed, 2))
+    assert qc == int(g["hybrid_hist_query_count"])
+    assert np.array_equal(raw / qc, g["hybrid_hist_counts"])
+    m = cfg.get("m", 0) or min(6, X.shape[1])
+    engine.grid_build(m, float(g["dense_eps_used"]))
+    q = np.arange(N, dtype=np.uint32)
+    ids, dist, solved, st = engine.dense_join(q, k)
+    ok = g["dense_prov"] == 0
+    assert np.array_equal(solved, ok)
+    assert np.array_equal(ids[ok], g["ids"][ok]) and np.array_equal(dist[ok], g["dist"][ok])
+    assert (ids[~ok] == 0xFFFFFFFF).all() and np.isinf(dist[~ok]).all()
+    assert st["candidates_examined"] == g["dense_candidates_examined"]
+    assert st["solved"] == int(ok.sum()) and st["failed"] == int((~ok).sum())

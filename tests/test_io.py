@@ -72,3 +72,49 @@ def test_binary_roundtrip_and_errors(tmp_path):
     assert "truncated header" in str(e.value)
     with pytest.raises(KnnjError):
         read_binary_f64(str(tmp_path / "missing.bin"))
+
+
+# ---- dataset ingest (csv / tsv / binary-f64) against the reference's own outcomes
+import hashlib  # noqa: E402
+import json  # noqa: E402
+import sys  # noqa: E402
+
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden"))
+from make_ingest_golden import cases as _ingest_cases  # noqa: E402
+
+from paper_1810_04758_b200 import ingest_dataset  # noqa: E402
+
+_GOLD = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden",
+                                    "ingest_cases.json")))
+_CASES = _ingest_cases()
+
+
+@pytest.mark.parametrize("threads", [1, 8])
+@pytest.mark.parametrize("name,fmt,data", _CASES, ids=[c[0] for c in _CASES])
+def test_ingest_matches_reference(tmp_path, name, fmt, data, threads):
+    """ingest_dataset (proj/src/io.cpp:15-106): sizes and coordinates, or the error kind
+    and message, equal the unmodified reference's (tests/golden/make_ingest_golden.py);
+    multi-threaded parsing reports the first error in file order."""
+    want = _GOLD[name]
+    p = str(tmp_path / f"{name}.{fmt}")
+    with open(p, "wb") as f:
+        f.write(data)
+    if "error" in want:
+        with pytest.raises(KnnjError) as e:
+            ingest_dataset(p, fmt, threads=threads)
+        assert e.value.kind == want["error"]
+        assert str(e.value) == f"{want['error']}: " + want["message"].replace("{path}", p)
+        return
+    X = ingest_dataset(p, fmt, threads=threads)
+    assert X.shape == (want["points"], want["dims"])
+    assert hashlib.sha256(np.ascontiguousarray(X, "<f8").tobytes()).hexdigest() == want["sha256"]
+
+
+def test_ingest_missing_and_unknown_format(tmp_path):
+    p = str(tmp_path / "missing.csv")
+    with pytest.raises(KnnjError) as e:
+        ingest_dataset(p, "csv")
+    assert str(e.value) == "IngestError: " + _GOLD["missing_file"]["message"].replace("{path}", p)
+    with pytest.raises(KnnjError) as e:
+        ingest_dataset("x", "xml")
+    assert e.value.kind == "UsageError" and _GOLD["unknown_format"]["message"] in str(e.value)
