@@ -78,6 +78,8 @@ int knnj_fp32_peak(knnj_ctx* ctx, double* tflops);
  *   "hist_cap" 0/1/2   : eps-selection histogram counts only the bins select_eps_beta
  *                        needs when the profile is not requested: 0 never, 1 when the
  *                        histogram is large (default), 2 always (tests).
+ *   "hist_grid" 0/1/2  : capped histogram bins of n <= 8 data on a grid of the cap radius
+ *                        (k_hist_grid): 0 never, 1 for >= 65536 queries (default), 2 always.
  *   "pilot_cap" 0/1/2  : the cap-placing pilot counts growing prefixes of the bins (4% and
  *                        a quarter only for n <= 8 or value 1; a tenth always) before
  *                        binning in full (2). */

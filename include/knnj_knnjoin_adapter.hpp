@@ -144,10 +144,13 @@ inline knnjoin::KnnRunResult run_hybrid(Engine& eng, const knnjoin::Dataset& d,
     r.eps_used = info->eps_used;
     r.failed_count = info->failed_count;
     r.eps_fallback = info->eps_fallback != 0;
-    if (info->k_clamped) r.warnings.push_back("k clamped to |D|-1");
+    if (info->k_clamped)
+        r.warnings.push_back("k clamped to |D|-1 = " + std::to_string(info->k_effective));
     if (info->eps_fallback)
         r.warnings.push_back("beta target unreachable within eps_mean; clamped to the histogram maximum");
-    if (profiled) {
+    // k_eff == 0 (|D| == 1): the reference returns before eps selection and the split
+    // (orchestrator.cpp:94-97), so there is no profile, partition or dense stats
+    if (profiled && info->k_effective > 0) {
         knnjoin::EpsilonProfile p;
         p.eps_mean = info->eps_mean;
         p.n_bins = cfg.n_bins;

@@ -344,6 +344,7 @@ struct knnj_ctx {
         hist_order_ready = false;
         mm_lo.clear();
         for (auto& lv : levels) lv.built = false;
+        hist_lv.built = false;
     }
 
     // column means (and variances when want_var) of X0, deterministic on device
@@ -595,6 +596,15 @@ struct knnj_ctx {
         a.inv_width = inv_width;
         a.counts = d_cnt.p;
         screen_consts(a.gam, a.erg, a.eab, a.e64);
+        if (grid_hist_applies(nq, ncount, nb)) {
+            histogram_grid(d_q.p, nq, a, S[ncount]);
+            last_hist_tc = false;
+            std::vector<unsigned long long> c(nb);
+            KJ_CUDA(cudaMemcpyAsync(c.data(), d_cnt.p, 8 * nb, cudaMemcpyDeviceToHost, s));
+            sync();
+            for (uint32_t b = 0; b < nb; ++b) raw[b] += c[b];
+            return;
+        }
         if (use_tc_hist() && tc_smem_bytes(tc_hist_shape(), 0, nb, true) <= 227 * 1024) {
             histogram_tc(d_q.p, nq, em, nb, ncount, S, d_cnt.p);
             last_hist_tc = true;
@@ -622,6 +632,88 @@ struct knnj_ctx {
         KJ_CUDA(cudaMemcpyAsync(c.data(), d_cnt.p, 8 * nb, cudaMemcpyDeviceToHost, s));
         last_hist_kernel_ms = t.ms();
         for (uint32_t b = 0; b < nb; ++b) raw[b] += c[b];
+    }
+
+    // Capped histogram on a grid (k_hist_grid): when only bins [0, n_count) are counted,
+    // every counted pair lies within r = sqrt(S[n_count]) in all n dims, so a grid of
+    // cell width >= r over the first min(n, 6) dims holds each of them in the query's
+    // 3^m neighbourhood. For small n that neighbourhood is a tight superset of the
+    // counted ball: C5's capped phase screens ~7e3 candidates per sampled query instead
+    // of the ~2.5e6 the box-filtered all-points sweep leaves. The grid (cells sorted by
+    // linear id, points by id inside a cell) is rebuilt per call: its width depends on
+    // the cap the pilot placed.
+    int hist_grid = 1;  // 0 never, 1 when it pays (below), 2 always (tests)
+    uint64_t hist_grid_min_queries = 65536;  // ... for this many queries
+    uint64_t hist_grid_min_points = 1u << 20;  // ... or this many points
+    bool grid_hist_applies(uint64_t nq, uint32_t ncount, uint32_t nb) const {
+        return ncount < nb && hist_grid && n <= 8 &&
+               (hist_grid == 2 || nq >= hist_grid_min_queries || N >= hist_grid_min_points);
+    }
+    Level hist_lv;  // built = its tables match the current working points
+    DBuf<float> hist_Xs;
+    double last_hist_grid_build_ms = 0.0;
+    void histogram_grid(const uint32_t* d_q, uint64_t nq, const HistArgs& h, double r2) {
+        const uint32_t m = std::min<uint32_t>(n, 6);
+        const double w = std::sqrt(r2) * (1.0 + 1e-9);
+        Timer tb(s);
+        // a grid built for a slightly larger radius (the pilot's) serves this one too
+        if (!(hist_lv.built && hist_lv.m == m && hist_lv.w >= w && hist_lv.w <= 1.2 * w)) {
+            grid_tables_into(hist_lv, m, w);
+            hist_Xs.ensure((uint64_t)n * Npad);
+            launch_gather_soa(Xf.p, hist_lv.A.p, N, n, Npad, hist_Xs.p, s);
+            hist_lv.built = true;
+        }
+        // queries in the grid's sorted order (neighbouring warps share candidate rows)
+        DBuf<uint32_t> qp_u, qp;
+        qp_u.ensure(nq);
+        qp.ensure(nq);
+        launch_map_u32(d_q, hist_lv.posOf.p, nq, qp_u.p, s);
+        {
+            size_t bytes = 0;
+            KJ_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, bytes, qp_u.p, qp.p, (int64_t)nq, 0,
+                                                   bits_for(N), s));
+            KJ_CUDA(cub::DeviceRadixSort::SortKeys(sc.get(bytes), bytes, qp_u.p, qp.p, (int64_t)nq, 0,
+                                                   bits_for(N), s));
+        }
+        DBuf<uint64_t> d_cs;
+        d_cs.ensure(2 * m);
+        KJ_CUDA(cudaMemcpyAsync(d_cs.p, hist_lv.cpd.data(), 8 * m, cudaMemcpyHostToDevice, s));
+        KJ_CUDA(cudaMemcpyAsync(d_cs.p + m, hist_lv.strides.data(), 8 * m, cudaMemcpyHostToDevice, s));
+        last_hist_grid_build_ms = tb.ms();
+        HistGridArgs a{};
+        a.Xs = hist_Xs.p;
+        a.Npad = Npad;
+        a.X64 = X64.p;
+        a.A = hist_lv.A.p;
+        a.slot = hist_lv.slot.p;
+        a.B = hist_lv.B.p;
+        a.G = hist_lv.G.p;
+        a.ncells = hist_lv.ncells;
+        a.cpd = d_cs.p;
+        a.strides = d_cs.p + m;
+        a.n = n;
+        a.m = m;
+        a.qpos = qp.p;
+        a.nq = nq;
+        a.n_bins = h.n_bins;
+        a.n_count = h.n_count;
+        a.SU = h.SU;
+        a.SD = h.SD;
+        a.eps_mean = h.eps_mean;
+        a.limit_sq = h.limit_sq;
+        a.inv_width = h.inv_width;
+        a.counts = h.counts;
+        a.gam = h.gam;
+        a.erg = h.erg;
+        a.eab = h.eab;
+        a.e64 = h.e64;
+        Timer t(s);
+        launch_hist_grid(a, s);
+        last_hist_kernel_ms = t.ms();
+        if (getenv("KNNJ_JOIN_STATS"))
+            fprintf(stderr, "hist grid: queries %llu bins %u/%u cells %llu w %.6g build %.1f ms kernel %.1f ms\n",
+                    (unsigned long long)nq, h.n_count, h.n_bins, (unsigned long long)hist_lv.ncells, hist_lv.w,
+                    last_hist_grid_build_ms, last_hist_kernel_ms);
     }
 
     // Tensor-core histogram: sampled queries x all points (id order) on the
@@ -913,6 +1005,11 @@ struct knnj_ctx {
     void build_level(int L, uint32_t m, double w) {
         Level& lv = levels[L];
         if (lv.built && lv.m == m && lv.w == w) return;
+        grid_tables_into(lv, m, w);
+        finish_level(lv);
+    }
+    // GridIndex::build's tables (grid_index.cpp:13-75) for lv: B, G, A, slot, posOf
+    void grid_tables_into(Level& lv, uint32_t m, double w) {
         lv.built = false;
         lv.m = m;
         lv.w = w;
@@ -986,6 +1083,14 @@ struct knnj_ctx {
         lv.slot.ensure(N);
         lv.posOf.ensure(N);
         launch_grid_tables(skeys.p, lv.A.p, runidx.p, N, lv.B.p, lv.G.p, lv.slot.p, lv.posOf.p, s);
+        lv.bbox_ready = lv.xj_ready = lv.xs_ready = lv.tc_ready = false;
+    }
+    // the join's order and operands on top of the tables
+    void finish_level(Level& lv) {
+        DBuf<uint64_t>& keys = gk_keys;
+        DBuf<uint64_t>& skeys = gk_skeys;
+        DBuf<uint32_t>& vals = gk_vals;
+        const uint32_t nruns = (uint32_t)lv.ncells;
         // join order: same cell ranges, Morton order inside each cell
         {
             const uint32_t md = ensure_morton_box();
@@ -2050,6 +2155,9 @@ int knnj_set_option(knnj_ctx* c, const char* name, int64_t value) {
         } else if (k == "fine" || k == "fine2") {
             if (value < 0 || value >= 1000) throw Error(1, "fine width must be in [0, 1000) permille of eps");
             c->fine_f[k == "fine" ? 0 : 1] = (uint32_t)value;
+        } else if (k == "hist_grid") {
+            if (value < 0 || value > 2) throw Error(1, "hist_grid must be 0, 1 or 2");
+            c->hist_grid = (int)value;
         } else if (k == "split_items") {
             c->split_items = value != 0;
         } else if (k == "hist_cap") {
@@ -2528,6 +2636,13 @@ static void run_impl(knnj_ctx* c, const knnj_config* cfg, uint32_t shard, uint32
     }
     for (uint32_t j = 0; j < n && j < 1024; ++j) I.perm[j] = c->perm[j];
     if (k_eff == 0 || nq == 0) {
+        // |D| == 1: every neighbour list is empty and every query keeps the reference's
+        // initial Provenance::Sparse (orchestrator.cpp:72-97); shard 0 owns the rows
+        const bool mine = shard == 0;
+        I.n_owned = mine ? nq : 0;
+        if (mine && prov) std::memset(prov, KNNJ_PROV_SPARSE, nq);
+        if (mine && owned)
+            for (uint64_t i = 0; i < nq; ++i) owned[i] = qid(i);
         I.ms_total = t_all.ms();
         if (info) *info = I;
         return;
@@ -2612,7 +2727,10 @@ static void run_impl(knnj_ctx* c, const knnj_config* cfg, uint32_t shard, uint32
         {
             Timer t(s);
             if (N < 2) throw Error(1, "eps_mean estimation needs at least two points");
-            if (c->use_tc_hist()) c->ensure_hist_order(c->tc_row_halfs());  // overlaps the draw
+            // the tensor-core histogram's candidate order, built while the host draws the
+            // pairs; not needed when the grid histogram will bin the capped rounds
+            const bool grid_only = !raw_hist && c->grid_hist_applies(0, 1, cfg->n_bins);
+            if (c->use_tc_hist() && !grid_only) c->ensure_hist_order(c->tc_row_halfs());
             if (drawer.joinable()) drawer.join();
             I.eps_mean = eps_pin ? c->eps_mean_of(eps_pin, eps_pin_n) : c->eps_mean_of(eps_ij);
             I.ms_eps_mean = t.ms();

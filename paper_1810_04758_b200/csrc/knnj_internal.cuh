@@ -236,6 +236,31 @@ struct HistArgs {
     float gam, erg, eab, e64;
 };
 
+// Capped histogram over a grid whose cell width covers the counted radius
+// (k_hist_grid, knnj_kernels.cu): queries by their sorted position in that grid.
+struct HistGridArgs {
+    const float* Xs;         // n x Npad SoA, the grid's sorted order, centred
+    uint64_t Npad;
+    const double* X64;       // working FP64 rows, id order
+    const uint32_t* A;       // sorted position -> point id
+    const uint32_t* slot;    // point id -> cell index
+    const uint64_t* B;       // ncells sorted linear ids
+    const uint2* G;          // ncells position ranges
+    uint64_t ncells;
+    const uint64_t* cpd;     // m
+    const uint64_t* strides; // m
+    uint32_t n, m;
+    const uint32_t* qpos;    // nq sorted query positions
+    uint64_t nq;
+    uint32_t n_bins, n_count;
+    const float* SU;
+    const float* SD;
+    double eps_mean, limit_sq, inv_width;
+    unsigned long long* counts;
+    float gam, erg, eab, e64;
+};
+void launch_hist_grid(const HistGridArgs& a, cudaStream_t s);
+
 // ---------------------------------------------------------------- launchers
 extern std::atomic<unsigned long long> g_launches;  // our kernels launched so far
 double measure_ffma_tflops(cudaStream_t s);

@@ -615,6 +615,150 @@ void launch_histogram(const HistArgs& a, uint64_t n_slabs, cudaStream_t s) {
     }
 }
 
+// ---------------------------------------------------------------- grid histogram
+__device__ __forceinline__ uint64_t lower_bound_u64(const uint64_t* a, uint64_t n, uint64_t key) {
+    uint64_t lo = 0, hi = n;
+    while (lo < hi) {
+        uint64_t mid = (lo + hi) >> 1;
+        if (a[mid] < key) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+// Capped eps-selection histogram over a grid of cell width >= the counted radius r
+// (every counted pair, dist < r in all n dims, lies in the query's 3^m cell
+// neighbourhood): one warp per sampled query. The warp's lanes first resolve the
+// 3^(m-1) rows of the neighbourhood (each row one contiguous position range of the
+// grid's sorted order: cells sorted by linear id, the last dim fastest), then stride
+// over the candidates. Same screen and exact-bin rule as k_hist (FP32 key +- delta
+// certain, else the FP64 scalar distance bins it like epsilon.cpp:86-95); only bins
+// [0, n_count) are counted. Used for small n, where the grid neighbourhood is a tight
+// superset of the counted ball.
+template <int NP>
+__global__ void __launch_bounds__(256) k_hist_grid(HistGridArgs a) {
+    constexpr int WARPS = 8, MAXR = 243;  // 3^5 rows for m <= 6
+    __shared__ uint2 s_rng[WARPS][MAXR];
+    __shared__ uint32_t s_hist[WARPS][256];
+    __shared__ float s_lo[257], s_hi[257];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t n = a.n, m = a.m, nbins = a.n_bins, ncount = a.n_count;
+    for (uint32_t i = threadIdx.x; i < WARPS * 256; i += blockDim.x) (&s_hist[0][0])[i] = 0;
+    for (uint32_t i = threadIdx.x; i <= nbins; i += blockDim.x) {
+        s_lo[i] = a.SU[i];
+        s_hi[i] = a.SD[i];
+    }
+    __syncthreads();
+    const float lo_end = a.SU[ncount];
+    const float invw = (float)a.inv_width;
+    const uint32_t ml = m - 1;
+    uint32_t R = 1;
+    for (uint32_t j = 0; j < ml; ++j) R *= 3;
+    for (uint64_t row = uint64_t(blockIdx.x) * WARPS + warp; row < a.nq;
+         row += uint64_t(gridDim.x) * WARPS) {
+        const uint32_t qp = a.qpos[row];
+        const uint32_t qid = a.A[qp];
+        const uint64_t lin = a.B[a.slot[qid]];
+        uint64_t c[8];
+        {
+            uint64_t r = lin;
+            for (uint32_t j = 0; j < m; ++j) {
+                c[j] = r / a.strides[j];
+                r -= c[j] * a.strides[j];
+            }
+        }
+        const uint64_t lo_l = c[ml] > 0 ? c[ml] - 1 : 0;
+        const uint64_t hi_l = min(c[ml] + 1, a.cpd[ml] - 1);
+        __syncwarp();
+        for (uint32_t r = lane; r < R; r += 32) {
+            uint64_t base = 0, t = r;
+            bool ok = true;
+            for (int j = (int)ml - 1; j >= 0; --j) {
+                const uint64_t dig = t % 3;
+                t /= 3;
+                const int64_t cj = (int64_t)c[j] - 1 + (int64_t)dig;
+                if (cj < 0 || cj >= (int64_t)a.cpd[j]) {
+                    ok = false;
+                    break;
+                }
+                base += (uint64_t)cj * a.strides[j];
+            }
+            uint2 rg = make_uint2(0, 0);
+            if (ok) {
+                const uint64_t i0 = lower_bound_u64(a.B, a.ncells, base + lo_l);
+                const uint64_t i1 = lower_bound_u64(a.B, a.ncells, base + hi_l + 1);
+                if (i0 < i1) rg = make_uint2(a.G[i0].x, a.G[i1 - 1].y);
+            }
+            s_rng[warp][r] = rg;
+        }
+        __syncwarp();
+        float a2[NP];
+        float na = 0.f;
+#pragma unroll
+        for (int d = 0; d < NP; ++d) {
+            const float v = d < (int)n ? a.Xs[(uint64_t)d * a.Npad + qp] : 0.f;
+            a2[d] = -2.f * v;
+            na = fmaf(v, v, na);
+        }
+        const float Aq = sqrtf(na) * 1.0001f;
+        const double* qx = a.X64 + (uint64_t)qid * n;
+        for (uint32_t r = 0; r < R; ++r) {
+            const uint2 rg = s_rng[warp][r];
+            for (uint32_t t = rg.x + lane; t < rg.y; t += 32) {
+                float nb = 0.f, acc = 0.f;
+#pragma unroll
+                for (int d = 0; d < NP; ++d) {
+                    const float b = d < (int)n ? a.Xs[(uint64_t)d * a.Npad + t] : 0.f;
+                    nb = fmaf(b, b, nb);
+                    acc = fmaf(a2[d], b, acc);
+                }
+                acc += nb;
+                const float dl = screen_delta(Aq, sqrtf(nb) * 1.0001f, a.gam, a.erg, a.eab, a.e64);
+                if (!(acc < __fsub_ru(__fadd_ru(lo_end, dl), na)) || t == qp) continue;
+                const float key = acc + na;
+                const float klo = __fsub_rd(key, dl), khi = __fadd_ru(key, dl);
+                int b = key > 0.f ? (int)(key * rsqrtf(key) * invw) : 0;
+                b = min(max(b, 0), (int)nbins - 1);
+                uint32_t bb = nbins;
+                if (klo >= s_lo[b] && khi < s_hi[b]) {
+                    bb = (uint32_t)b;
+                } else {
+                    const double sq = exact_sq(qx, a.X64 + (uint64_t)a.A[t] * n, n);
+                    if (!(sq > a.limit_sq)) {
+                        const double dist = sqrt(sq);
+                        if (dist < a.eps_mean) {
+                            uint64_t e = (uint64_t)(dist * a.inv_width);
+                            bb = e >= nbins ? nbins - 1 : (uint32_t)e;
+                        }
+                    }
+                }
+                if (bb < ncount) atomicAdd(&s_hist[warp][bb], 1u);
+            }
+        }
+    }
+    __syncthreads();
+    for (uint32_t b = threadIdx.x; b < ncount; b += blockDim.x) {
+        unsigned long long sum = 0;
+        for (int w = 0; w < WARPS; ++w) sum += s_hist[w][b];
+        if (sum) atomicAdd(&a.counts[b], sum);
+    }
+}
+
+void launch_hist_grid(const HistGridArgs& a, cudaStream_t s) {
+    if (a.nq == 0) return;
+    if (a.m < 1 || a.m > 6 || a.n > 8 || a.n_bins > 256 || a.n_count > a.n_bins)
+        throw Error(1, "grid histogram: unsupported shape");
+    const unsigned blocks = (unsigned)std::min<uint64_t>((a.nq + 7) / 8, 148ull * 16);
+    switch (a.n) {
+#define X(v) \
+    case v: k_hist_grid<v><<<blocks, 256, 0, s>>>(a); break;
+        X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8)
+#undef X
+    }
+    KJ_CUDA(cudaGetLastError());
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+
 // ---------------------------------------------------------------- small kernels
 __global__ void k_check_finite(const double* X, uint64_t count, unsigned long long* first_bad) {
     for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
@@ -859,15 +1003,6 @@ void launch_map_u32(const uint32_t* idx, const uint32_t* table, uint64_t n, uint
     g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
-__device__ __forceinline__ uint64_t lower_bound_u64(const uint64_t* a, uint64_t n, uint64_t key) {
-    uint64_t lo = 0, hi = n;
-    while (lo < hi) {
-        uint64_t mid = (lo + hi) >> 1;
-        if (a[mid] < key) lo = mid + 1;
-        else hi = mid;
-    }
-    return lo;
-}
 
 // One warp per cell: the 3^(m-1) rows of the clamped ±1 neighbourhood over
 // the first m-1 indexed dims; each row is the contiguous B-range of linear ids

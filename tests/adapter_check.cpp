@@ -33,12 +33,20 @@ int main() {
         {"clusters:4:0.1", 1500, 24, 16, 4, 0.0, 0.0, 0.0, knnjoin::EngineMode::DenseOnly},
         {"mixture", 1200, 90, 8, 0, 0.0, 0.0, 0.0, knnjoin::EngineMode::SparseOnly},
         {"uniform", 900, 3, 7, 0, 0.0, 0.0, 0.0, knnjoin::EngineMode::BruteOracle},
+        // k >= |D|: k clamped to |D|-1 with the reference's warning text (orchestrator.cpp:77-82)
+        {"uniform", 24, 3, 40, 0, 0.0, 0.0, 0.0, knnjoin::EngineMode::Hybrid},
+        {"clusters:2:0.1", 30, 5, 30, 0, 0.0, 0.0, 0.0, knnjoin::EngineMode::DenseOnly},
+        // |D| == 1: k_eff = 0, empty lists, Sparse provenance, no profile (orchestrator.cpp:94-97)
+        {"uniform", 1, 4, 3, 0, 0.0, 0.0, 0.0, knnjoin::EngineMode::Hybrid},
     };
     knnjoin_b200::Engine eng(0);
     int bad = 0, n = 0;
     for (const Case& c : cases) {
+        // (the reference generator needs two points; a one-point dataset is built directly)
         const knnjoin::Dataset d =
-            knnjoin::generate_synthetic(knnjoin::SyntheticSpec::parse(c.spec), c.size, c.dims, 11);
+            c.size == 1 ? knnjoin::Dataset(std::vector<double>(c.dims, 0.25), c.dims)
+                        : knnjoin::generate_synthetic(knnjoin::SyntheticSpec::parse(c.spec), c.size,
+                                                      c.dims, 11);
         knnjoin::RunConfig cfg;
         cfg.k = c.k;
         cfg.m = c.m;

@@ -256,3 +256,34 @@ def test_engine_knobs_identical(engine, oracle, opt, val, default):
     q = np.random.default_rng(11).choice(N, 32, replace=False).astype(np.uint32)
     oi, od = oracle.brute_knn(W, q, k)
     assert np.array_equal(b.ids[q], oi) and np.array_equal(b.dist[q], od)
+
+
+@pytest.mark.parametrize("spec,N,n,k", [("uniform", 40000, 4, 32), ("exponential", 30000, 6, 20),
+                                        ("uniform", 50000, 2, 5), ("mixture", 30000, 3, 8),
+                                        ("clusters:4:0.05", 20000, 8, 16)])
+def test_grid_histogram_counts_exact(engine, oracle, spec, N, n, k):
+    """The capped histogram on a grid of the cap radius (k_hist_grid, n <= 8) counts
+    bins [0, n_count) exactly like the reference's binning (epsilon.cpp:76-104), and a
+    run through it is bit-identical to one through the tensor-core histogram."""
+    X = generate(spec, N, n, 13)
+    o = oracle.run(X, k=k, mode="hybrid", seed=13)
+    engine.set_option("hist_cap", 2)
+    engine.set_option("hist_grid", 2)
+    try:
+        engine.set_points(X)
+        r = engine.run(RunConfig(k=k, mode="hybrid", seed=13), want_hist=False)
+        want = min(max(int(0.01 * N), 100), N)
+        q = oracle.sample(N, want, oracle.derive_seed(13, 2))
+        for ncount in (1, 3, 7, 20):
+            raw = engine.histogram_queries_capped(q, r.info["eps_mean"], 100, ncount)
+            assert np.array_equal(raw[:ncount], o["raw_hist"][:ncount]), ncount
+            assert not raw[ncount:].any()
+        engine.set_option("hist_grid", 0)
+        engine.set_points(X)
+        t = engine.run(RunConfig(k=k, mode="hybrid", seed=13), want_hist=False)
+    finally:
+        engine.set_option("hist_cap", 1)
+        engine.set_option("hist_grid", 1)
+    assert r.info["eps_used"] == o["eps_used"] == t.info["eps_used"]
+    assert np.array_equal(r.ids, o["ids"]) and np.array_equal(r.dist, o["dist"])
+    assert np.array_equal(t.ids, r.ids) and np.array_equal(t.provenance, r.provenance)
