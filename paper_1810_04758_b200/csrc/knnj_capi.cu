@@ -29,7 +29,12 @@
 using namespace kj;
 
 namespace kj {
-void draw_pairs_fast(uint64_t N, uint64_t pairs, uint64_t seed, uint64_t* ij);  // knnj_rng.cpp
+// knnj_rng.cpp (host-compiled: its AVX2 clones stay out of nvcc's host pass)
+void draw_pairs_fast(uint64_t N, uint64_t pairs, uint64_t seed, uint64_t* ij);
+struct SampleWork;
+void sample_fast(uint64_t n, uint64_t k, uint64_t seed, uint64_t* out, bool sorted, SampleWork* w);
+SampleWork* sample_work_new();
+void sample_work_free(SampleWork* w);
 cudaStream_t& alloc_stream() {
     static thread_local cudaStream_t s = nullptr;
     return s;
@@ -167,38 +172,12 @@ float f32_round_down(double v) {
     return f;
 }
 
-// Sampler with the reference's exact output (proj/include/knnjoin/util.hpp:70-92):
-// partial Fisher-Yates over an index map, same libstdc++ distribution calls.
-std::vector<uint64_t> sample_without_replacement(uint64_t n, uint64_t k, std::mt19937_64& rng) {
-    std::vector<uint64_t> out;
-    if (k >= n) {
-        out.resize(n);
-        std::iota(out.begin(), out.end(), 0ull);
-        return out;
-    }
-    out.reserve(k);
-    uint64_t cap = 16;
-    while (cap < 2 * k + 16) cap <<= 1;
-    std::vector<uint64_t> keys(cap, ~0ull), vals(cap);
-    auto slot = [&](uint64_t key) {
-        uint64_t h = (key * 0x9E3779B97F4A7C15ull) >> 17;
-        h &= cap - 1;
-        while (keys[h] != ~0ull && keys[h] != key) h = (h + 1) & (cap - 1);
-        return h;
-    };
-    for (uint64_t i = 0; i < k; ++i) {
-        std::uniform_int_distribution<uint64_t> dist(i, n - 1);
-        uint64_t j = dist(rng);
-        uint64_t sj = slot(j);
-        uint64_t jv = keys[sj] == j ? vals[sj] : j;
-        uint64_t si = slot(i);
-        uint64_t iv = keys[si] == i ? vals[si] : i;
-        out.push_back(jv);
-        sj = slot(j);
-        keys[sj] = j;
-        vals[sj] = iv;
-    }
-    std::sort(out.begin(), out.end());
+// sample_without_replacement(n, k, std::mt19937_64(seed)) with the reference's exact
+// output (proj/include/knnjoin/util.hpp:70-92): knnj_rng.cpp (tests/test_rng.py).
+std::vector<uint64_t> sample_seeded(uint64_t n, uint64_t k, uint64_t seed, bool sorted = true,
+                                    SampleWork* w = nullptr) {
+    std::vector<uint64_t> out(std::min(n, k));
+    sample_fast(n, k, seed, out.data(), sorted, w);
     return out;
 }
 
@@ -294,6 +273,7 @@ struct knnj_ctx {
     cudaStream_t s_out = nullptr;  // result D2H overlapping the fallback (knnj_run)
     cudaEvent_t ev_out = nullptr;
     ~knnj_ctx() {
+        if (sample_work) sample_work_free(sample_work);
         if (ev_out) cudaEventDestroy(ev_out);
         if (s_out) cudaStreamDestroy(s_out);
         if (h_sq) cudaFreeHost(h_sq);
@@ -958,13 +938,16 @@ struct knnj_ctx {
         want = std::max<uint64_t>(want, 100);
         return std::min<uint64_t>(want, N);
     }
-    static std::vector<uint64_t> draw_histogram_sample(uint64_t N, double frac, uint64_t seed) {
+    // The sample comes back unsorted (the reference sorts it): the counts do not depend
+    // on the order of the queries, and the device sorts them into its candidate order.
+    SampleWork* sample_work = nullptr;  // the sampler's buffers, kept across runs
+    std::vector<uint64_t> draw_histogram_sample(double frac, uint64_t seed) {
         const uint64_t want = histogram_sample_size(N, frac);
-        std::mt19937_64 rng(seed);
-        return sample_without_replacement(N, want, rng);
+        if (!sample_work) sample_work = sample_work_new();
+        return sample_seeded(N, want, seed, false, sample_work);
     }
     std::vector<uint64_t> histogram_sample(double frac, uint64_t seed) {
-        return draw_histogram_sample(N, frac, seed);
+        return draw_histogram_sample(frac, seed);
     }
 
     // ------------------------------------------------------------ grid levels
@@ -2618,8 +2601,7 @@ static void run_impl(knnj_ctx* c, const knnj_config* cfg, uint32_t shard, uint32
         eps_pin = pin;
         eps_pin_n = pin ? pairs : 0;
         hdrawer = std::thread([&] {
-            hist_q = knnj_ctx::draw_histogram_sample(N, cfg->hist_query_fraction,
-                                                     derive_seed(cfg->seed, 2));
+            hist_q = c->draw_histogram_sample(cfg->hist_query_fraction, derive_seed(cfg->seed, 2));
         });
     }
     struct Joiner {
@@ -3049,8 +3031,8 @@ int knnj_parameter_search(knnj_ctx* c, const knnj_config* base, double f, const 
         if (want < 50)
             throw Error(7, "parameter search sample of " + std::to_string(want) +
                                " queries is below the floor of 50");
-        std::mt19937_64 rng(derive_seed(base->seed, 0x04));  // kSeedQuerySubset
-        const std::vector<uint64_t> picked = sample_without_replacement(c->N, want, rng);
+        // kSeedQuerySubset
+        const std::vector<uint64_t> picked = sample_seeded(c->N, want, derive_seed(base->seed, 0x04));
         const std::vector<uint32_t> subset(picked.begin(), picked.end());
         bool have = false;
         double best = 0.0;

@@ -10,6 +10,7 @@
 // pair stream against the std types for small, large and near-2^63 ranges.
 #pragma once
 #include <cstdint>
+#include <vector>
 
 namespace kj {
 
@@ -91,5 +92,20 @@ inline void draw_pairs_stream(uint64_t N, uint64_t pairs, uint64_t seed, uint64_
     }
     delete st;
 }
+
+// buffers of sample_fast (knnj_rng.cpp), kept across calls by the caller
+struct SampleWork {
+    struct Slot {
+        uint64_t key, val;
+    };
+    std::vector<uint64_t> J, D;
+    std::vector<Slot> T;
+};
+// sample_without_replacement(n, k, std::mt19937_64(seed)) (util.hpp:70-92); ascending
+// when `sorted`, else in an order that depends only on (n, k, seed)
+void sample_fast(uint64_t n, uint64_t k, uint64_t seed, uint64_t* out, bool sorted = true,
+                 SampleWork* w = nullptr);
+SampleWork* sample_work_new();
+void sample_work_free(SampleWork* w);
 
 }  // namespace kj
