@@ -130,15 +130,28 @@ def profile_traffic(config: str):
 
 
 # ---------------------------------------------------------------------------- reference arm
-def cpu_reference(X, k, sample, seed=1):
+def calibrated_sample(ref, h, N, k, cores, seconds, seed):
+    """Query-sample size that keeps the reference's kd-tree queries busy for about
+    `seconds` on `cores` threads (a 20k-query probe sets the rate)."""
+    rng = np.random.default_rng(seed + 99)
+    probe = np.sort(rng.choice(N, min(N, 20000), replace=False)).astype(np.uint32)
+    _, _, secs = ref.kd_query(h, probe, k, cores)
+    rate = probe.size / max(secs, 1e-6)
+    return int(min(N, max(20000, rate * seconds)))
+
+
+def cpu_reference(X, k, sample, seed=1, seconds=15.0):
     """The reference's RefImpl (SparseOnly: reorder + kd-tree) on a query sample
-    against the FULL dataset, all host threads. Returns (points/s, cores, detail)."""
+    against the FULL dataset, all host threads; the sample is sized to ~`seconds` of
+    query time unless given. Returns (points/s, cores, detail)."""
     from oracle.oracle import Ref, ref_available
     if not ref_available():
         return None
     ref = Ref()
     h, t_reorder, t_build = ref.kd_create(X, min(6, X.shape[1]))
     cores = ref.hardware_concurrency()
+    if not sample:
+        sample = calibrated_sample(ref, h, X.shape[0], k, cores, seconds, seed)
     rng = np.random.default_rng(seed)
     q = np.sort(rng.choice(X.shape[0], sample, replace=False)).astype(np.uint32)
     _, _, secs = ref.kd_query(h, q, k, cores)
@@ -178,10 +191,11 @@ def run_reference(args, cfgd, X):
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
         return
     k = cfgd["k"]
-    sample = args.cpu_sample or 2000
     ref = Ref()
     h, t_reorder, t_build = ref.kd_create(X, min(6, X.shape[1]))
     cores = ref.hardware_concurrency()
+    # each step a bounded sample: ~3 s of kd-tree queries on all host threads
+    sample = args.cpu_sample or calibrated_sample(ref, h, X.shape[0], k, cores, 3.0, 1234)
     rng = np.random.default_rng(1234)
     times = []
     for step in range(args.warmup + args.steps):
@@ -332,13 +346,15 @@ def run_ours(args, cfgd, X):
     t_ideal = max(F_run / (fp32_peak * 1e12), B_run / bw)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        c = cpu_reference(X, k, args.cpu_sample or 15000)
+        c = cpu_reference(X, k, args.cpu_sample)
         if c is not None:
             c["ref"].kd_destroy(c["handle"])
             cpu = {"value": c["rate"], "unit": UNIT, "cores": c["cores"], "kind": "reference",
                    "sample": f"{len(c['q'])} seeded random queries against all {N} points, "
                              f"reference SparseOnly/RefImpl kd-tree (the faster reference CPU "
-                             f"mode), {c['secs']:.2f}s; kd build {c['t_build']:.1f}s excluded"}
+                             f"mode), {c['secs']:.2f}s of queries on {c['cores']} threads; kd build "
+                             f"{c['t_build']:.1f}s and reorder {c['t_reorder']:.1f}s excluded like the "
+                             f"reference's measured_total"}
             hyb = cpu_hybrid_reduced(cfgd)
             if hyb is not None:
                 cpu["hybrid_reduced"] = hyb

@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define KNNJ_ABI_VERSION 4
+#define KNNJ_ABI_VERSION 5
 
 enum knnj_status {
     KNNJ_OK = 0,
@@ -200,6 +200,8 @@ typedef struct {
         ms_fallback, ms_download, ms_total;
     double ms_join_kernel, ms_hist_kernel;
     double ms_join_build;         /* work-item / adjacency construction of the level-0 pass */
+    double kth_bound2;            /* radius bound (squared) of the level-0 pass; 0 = unbounded */
+    uint64_t bound_retried;       /* level-0 rows re-run without the bound */
     uint32_t perm[1024];
 } knnj_run_info;
 

@@ -73,6 +73,7 @@ RUN_INFO_FIELDS = [
     "ms_upload", "ms_reorder", "ms_eps_mean", "ms_histogram", "ms_grid", "ms_split", "ms_join",
     "ms_fallback", "ms_download", "ms_total", "ms_join_kernel", "ms_hist_kernel",
     "ms_join_build")] + [
+    ("kth_bound2", C.c_double), ("bound_retried", C.c_uint64),
     ("perm", C.c_uint32 * 1024)]
 
 

@@ -22,6 +22,7 @@
 #include <vector>
 
 #include <cub/cub.cuh>
+#include <nvtx3/nvToolsExt.h>
 
 #include "knnj_c.h"
 #include "knnj_internal.cuh"
@@ -189,6 +190,14 @@ uint64_t splitmix64(uint64_t x) {
 }
 uint64_t derive_seed(uint64_t master, uint64_t tag) { return splitmix64(master ^ splitmix64(tag)); }
 
+// NVTX range over one phase of a run (visible in nsys / ncu --nvtx timelines)
+struct Nvtx {
+    explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+    ~Nvtx() { nvtxRangePop(); }
+    Nvtx(const Nvtx&) = delete;
+    Nvtx& operator=(const Nvtx&) = delete;
+};
+
 // KNNJ_TRACE=1: host wall-clock marks of the runtime's sub-steps on stderr (dev aid)
 struct Trace {
     bool on = false;
@@ -209,6 +218,22 @@ struct Trace {
 Trace& trace() {
     static Trace t;
     return t;
+}
+
+// Device address of a host range in pinned (page-locked, mapped) memory, else null:
+// kernels may then store straight into it over PCIe.
+void* mapped_host(void* p, size_t bytes) {
+    if (!p || !bytes) return nullptr;
+    cudaPointerAttributes a{}, b{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess ||
+        cudaPointerGetAttributes(&b, static_cast<char*>(p) + bytes - 1) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    if (a.type != cudaMemoryTypeHost || b.type != cudaMemoryTypeHost || !a.devicePointer ||
+        static_cast<char*>(b.devicePointer) - static_cast<char*>(a.devicePointer) != (ptrdiff_t)(bytes - 1))
+        return nullptr;
+    return a.devicePointer;
 }
 
 struct Timer {
@@ -282,6 +307,12 @@ struct knnj_ctx {
     }
 
     void sync() { KJ_CUDA(cudaStreamSynchronize(s)); }
+    void ensure_out_stream() {
+        if (!s_out) {
+            KJ_CUDA(cudaStreamCreateWithFlags(&s_out, cudaStreamNonBlocking));
+            KJ_CUDA(cudaEventCreateWithFlags(&ev_out, cudaEventDisableTiming));
+        }
+    }
 
     // ------------------------------------------------------------ screen constants
     void screen_consts(float& gam, float& erg, float& eab, float& e64) const {
@@ -1104,6 +1135,49 @@ struct knnj_ctx {
     uint32_t tc_slack = 24;       // tcgen05 join list capacity K + slack (compaction when full)
     bool finalize_xj = true;      // finalize reads FP64 rows from a join-ordered copy
     bool early_d2h = true;        // knnj_run: result D2H overlaps classification + fallback
+    bool stream_host = true;      // knnj_run into pinned outputs: rows written by the finalize
+    uint32_t join_chunks = 8;     // level-0 launches (finalize of one overlaps the next join)
+    uint32_t chunk_min_rows = 65536;  // ... each of at least this many query rows
+    // level-0 radius bound (run_impl): sample size, quantile (per mille) of the sample's
+    // K-th sq, the largest bound worth using (fraction of the filter radius^2), and the
+    // smallest pass it is tried on
+    bool kth_bound = true;
+    uint32_t bound_sample = 4096;
+    uint32_t kth_bound_q = 990;
+    double bound_max_frac = 0.8;
+    uint64_t bound_min_rows = 200000;
+
+    // The kth_bound_q-quantile of the exact K-th sq over the sample rows sq_ids (a
+    // level-0 pass of their own; rows without K candidates count as infinite).
+    double sample_kth_bound(Level& lv, const std::vector<uint32_t>& q_ids, uint32_t K, double eps2,
+                            uint32_t q_permille) {
+        const uint64_t S = q_ids.size();
+        if (!S) return 0.0;
+        DBuf<uint32_t> d_sq, d_sr, t_ids;
+        DBuf<double> t_dist, t_kth;
+        DBuf<uint8_t> t_st;
+        d_sq.ensure(S);
+        d_sr.ensure(S);
+        t_ids.ensure(S * K);
+        t_dist.ensure(S * K);
+        t_kth.ensure(S);
+        t_st.ensure(S);
+        KJ_CUDA(cudaMemcpyAsync(d_sq.p, q_ids.data(), 4 * S, cudaMemcpyHostToDevice, s));
+        launch_iota(d_sr.p, S, s);
+        Pass Ps;
+        build_pass(lv, d_sq.p, d_sr.p, S, Ps, K, 0, 1, nullptr, filter_radius2(lv));
+        run_pass(lv, Ps, K, nullptr, eps2, cover2(lv), t_ids.p, t_dist.p, t_kth.p, t_st.p, nullptr);
+        std::vector<double> kth(S);
+        std::vector<uint8_t> st(S);
+        KJ_CUDA(cudaMemcpyAsync(kth.data(), t_kth.p, 8 * S, cudaMemcpyDeviceToHost, s));
+        KJ_CUDA(cudaMemcpyAsync(st.data(), t_st.p, S, cudaMemcpyDeviceToHost, s));
+        sync();
+        for (uint64_t i = 0; i < S; ++i)
+            if (!(st[i] & ST_HAS_K)) kth[i] = kInf;
+        const uint64_t at = std::min<uint64_t>(S - 1, (S * q_permille + 999) / 1000);
+        std::nth_element(kth.begin(), kth.begin() + at, kth.end());
+        return kth[at];
+    }
     uint32_t simt_slack = 0;      // SIMT join list capacity K + slack (0: max(8, K/8))
     // Fine cascade ahead of level 0 (widths eps * f / 1000, coarsest first is NOT
     // required: each is tried on the rows still uncertified). 0 = off.
@@ -1249,7 +1323,7 @@ struct knnj_ctx {
     // query of their item are dropped (filter_ranges).
     void build_pass(Level& lv, const uint32_t* d_qpid, const uint32_t* d_qrow, uint64_t nq,
                     Pass& P, uint32_t K = 0, uint32_t shard = 0, uint32_t nshard = 1,
-                    const uint8_t* d_dense = nullptr, double filter_r2 = 0.0) {
+                    const uint8_t* d_dense = nullptr, double filter_r2 = 0.0, bool allow_split = true) {
         P.nq = nq;
         P.nq_all = nq;
         P.nv = nq;
@@ -1398,7 +1472,7 @@ struct knnj_ctx {
                 cmax = std::max(cmax, csz[i]);
             }
             const double part_tiles = std::max(64.0, W / (148.0 * 4.0));
-            if (split_items && K > 0 && double(cmax) / 128.0 > 2.0 * part_tiles) {
+            if (split_items && allow_split && K > 0 && double(cmax) / 128.0 > 2.0 * part_tiles) {
                 std::vector<uint2> h_adj(P.nadj);
                 KJ_CUDA(cudaMemcpyAsync(h_adj.data(), P.adj.p, 8 * P.nadj, cudaMemcpyDeviceToHost, s));
                 sync();
@@ -1455,13 +1529,39 @@ struct knnj_ctx {
                 P.nsplits = splits.size();
             }
         }
-        // heaviest items first (LPT order for the block scheduler); ties keep cell order
+        // heaviest items first (LPT order for the block scheduler); ties keep cell order.
+        // A streamed pass is cut into stream_chunks launches over contiguous row ranges
+        // (items grouped by the chunk their first row falls in, LPT inside each), so one
+        // chunk's finalize and result copy overlap the next chunk's join.
+        const uint32_t nch = (stream_chunks > 1 && P.nv == nq_own &&
+                              nq_own >= (uint64_t)chunk_min_rows * stream_chunks)
+                                 ? stream_chunks : 1;
+        auto chunk_of = [&](const uint4& it) { return (uint32_t)((uint64_t)it.x * nch / nq_own); };
         std::vector<uint32_t> order(own.size());
         std::iota(order.begin(), order.end(), 0u);
-        std::stable_sort(order.begin(), order.end(),
-                         [&](uint32_t a, uint32_t b) { return own_w[a] > own_w[b]; });
+        std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) {
+            const uint32_t ca = chunk_of(own[a]), cb = chunk_of(own[b]);
+            return ca != cb ? ca < cb : own_w[a] > own_w[b];
+        });
         std::vector<uint4> h_sorted(own.size());
         for (uint64_t i = 0; i < own.size(); ++i) h_sorted[i] = own[order[i]];
+        P.chunk_item.clear();
+        P.chunk_row.clear();
+        if (nch > 1) {
+            P.chunk_item.assign(nch + 1, own.size());
+            P.chunk_row.assign(nch + 1, nq_own);
+            for (uint64_t i = own.size(); i-- > 0;) {
+                const uint32_t c = chunk_of(h_sorted[i]);
+                P.chunk_item[c] = i;
+                P.chunk_row[c] = std::min<uint64_t>(P.chunk_row[c], h_sorted[i].x);
+            }
+            for (uint32_t c = nch; c-- > 0;) {  // empty chunks start where the next does
+                P.chunk_item[c] = std::min(P.chunk_item[c], P.chunk_item[c + 1]);
+                P.chunk_row[c] = std::min(P.chunk_row[c], P.chunk_row[c + 1]);
+            }
+            P.chunk_row[0] = 0;
+            P.chunk_item[0] = 0;
+        }
         if (r0 != 0 || r1 != nq || P.nv > nq_own) {
             DBuf<uint32_t> qp2, qr2;
             qp2.ensure(P.nv);
@@ -1500,6 +1600,9 @@ struct knnj_ctx {
         if (filter_r2 > 0.0 && box_filter && P.nitems)
             filter_ranges(lv, P, filter_r2, K > 0 && pass_uses_tc(lv, K));
     }
+
+    // launches a big level-0 pass is cut into (build_pass; 1 = one launch)
+    uint32_t stream_chunks = 1;
 
     // Box filter of a join pass (after build_pass): a candidate can matter to a query
     // only within radius r of it (level 0: eps, the dense rule; level L: the cell width
@@ -1631,10 +1734,17 @@ struct knnj_ctx {
     bool last_join_tc = false;
     // Runs the fused join over a pass, then the exact finalize (and the slow
     // path for overflowed lists). Writes rows of out_* (indexed by qrow).
-    void run_pass(Level& lv, Pass& P, uint32_t K, const float* d_init_cut, double eps2,
+    // With host_ids/host_dist (mapped pinned host memory) and a pass built in chunks, the
+    // finalize of chunk c runs on s_out while chunk c+1 joins on s, and writes its rows to
+    // the host too: the result copy streams under the join. Returns whether it did; the
+    // rows the exact slow path rewrites afterwards are appended to *host_patch.
+    bool run_pass(Level& lv, Pass& P, uint32_t K, const float* d_init_cut, double eps2,
                   double cov2, uint32_t* out_ids, double* out_dist, double* out_kth,
-                  uint8_t* out_status, uint64_t* n_slow) {
-        if (!P.nq) return;
+                  uint8_t* out_status, uint64_t* n_slow, uint32_t* host_ids = nullptr,
+                  double* host_dist = nullptr, std::vector<uint32_t>* host_patch = nullptr,
+                  double bound2 = 0.0) {
+        if (!P.nq) return false;
+        if (bound2 > 0.0 && P.nv != P.nq) throw Error(9, "a radius-bounded pass cannot hold split items");
         const TcJoinCfg tcc = tc_join_cfg(K, lv.w);
         const bool tc = tcc.ok && P.chunk == 128u * tcc.sh.G;
         if (!tc && P.chunk != (uint32_t)JB && P.chunk != 32u)
@@ -1651,6 +1761,31 @@ struct knnj_ctx {
         if (!tc && join_smem_bytes(np, L, P.chunk) > 227 * 1024)
             throw Error(1, "k too large for the device join");
         const uint64_t nv = P.nv, nvv = P.nv - P.nq;  // launch rows; virtual (split-part) rows
+        // chunk boundaries (one launch unless the pass was built in chunks)
+        std::vector<uint64_t> ci = P.chunk_item, cr = P.chunk_row;
+        if (ci.size() < 2 || nvv) {
+            ci = {0, P.nitems};
+            cr = {0, P.nq};
+        }
+        const size_t nch = ci.size() - 1;
+        const bool to_host = host_ids && host_dist && !nvv;
+        const bool overlap = nch > 1;
+        if (overlap) ensure_out_stream();
+        std::vector<cudaEvent_t> ev_join(nch, nullptr);
+        cudaEvent_t ev_fin = nullptr;
+        struct EvFree {
+            std::vector<cudaEvent_t>& v;
+            cudaEvent_t& f;
+            ~EvFree() {
+                for (auto e : v)
+                    if (e) cudaEventDestroy(e);
+                if (f) cudaEventDestroy(f);
+            }
+        } ev_free{ev_join, ev_fin};
+        if (overlap) {
+            for (auto& e : ev_join) KJ_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            KJ_CUDA(cudaEventCreateWithFlags(&ev_fin, cudaEventDisableTiming));
+        }
         DBuf<uint32_t>& cnt = pass_cnt;
         DBuf<uint32_t>& pos = pass_pos;
         cnt.ensure(nv);
@@ -1663,6 +1798,49 @@ struct knnj_ctx {
             launch_gather_f32(P.vsrc.p, d_init_cut, nvv, cut_ext.p + P.nq, s);
             d_init_cut = cut_ext.p;
         }
+        FinalArgs f{};
+        f.X64 = X64.p;
+        f.n = n;
+        f.A = lv.J.p;
+        f.qpos = P.qpos.p;
+        f.qrow = P.qrow.p;
+        f.cnt = cnt.p;
+        f.pos = pos.p;
+        f.nrows = P.nq;
+        f.K = K;
+        f.L = L;
+        f.eps2 = eps2;
+        f.cover2 = cov2;
+        f.out_ids = out_ids;
+        f.out_dist = out_dist;
+        f.out_kth = out_kth;
+        f.out_status = out_status;
+        f.bound2 = bound2;
+        if (to_host) {
+            f.host_ids = host_ids;
+            f.host_dist = host_dist;
+        }
+        // big passes (at least a quarter of the points: the copy is N rows) gather rows in
+        // join order once
+        if (finalize_xj && P.nq >= (1u << 16) && 4 * P.nq >= N) {
+            if (!lv.xj_ready) {
+                lv.XJ.ensure((uint64_t)N * n);
+                launch_rows_by(X64.p, lv.J.p, N, n, lv.XJ.p, s);
+                lv.xj_ready = true;
+            }
+            f.XJ = lv.XJ.p;
+        }
+        // the finalize of launch rows [cr[c], cr[c+1]) (on s_out behind chunk c's join)
+        auto finalize_chunk = [&](size_t c) {
+            FinalArgs fc = f;
+            fc.qpos = P.qpos.p + cr[c];
+            fc.qrow = P.qrow.p + cr[c];
+            fc.cnt = cnt.p + cr[c];
+            fc.pos = pos.p + cr[c] * L;
+            fc.nrows = cr[c + 1] - cr[c];
+            KJ_CUDA(cudaStreamWaitEvent(s_out, ev_join[c], 0));
+            launch_finalize(fc, s_out);
+        };
         if (tc) {
             prep_tc(lv);
             TcJoinArgs a{};
@@ -1694,7 +1872,15 @@ struct knnj_ctx {
             }
             trace().mark("pass: pre-kernel", s);
             Timer t(s);
-            launch_join_tc(a, tcc.sh, P.nitems, N, s);
+            for (size_t c = 0; c < nch; ++c) {
+                TcJoinArgs ac = a;
+                ac.items = P.items.p + ci[c];
+                launch_join_tc(ac, tcc.sh, ci[c + 1] - ci[c], N, s);
+                if (overlap) {
+                    KJ_CUDA(cudaEventRecord(ev_join[c], s));
+                    finalize_chunk(c);
+                }
+            }
             last_join_kernel_ms = t.ms();
             if (want_stats) {
                 unsigned long long h[8];
@@ -1724,7 +1910,15 @@ struct knnj_ctx {
             a.out_pos = pos.p;
             screen_consts(a.gam, a.erg, a.eab, a.e64);
             Timer t(s);
-            launch_join(a, P.nitems, P.chunk, s);
+            for (size_t c = 0; c < nch; ++c) {
+                JoinArgs ac = a;
+                ac.items = P.items.p + ci[c];
+                launch_join(ac, ci[c + 1] - ci[c], P.chunk, s);
+                if (overlap) {
+                    KJ_CUDA(cudaEventRecord(ev_join[c], s));
+                    finalize_chunk(c);
+                }
+            }
             last_join_kernel_ms = t.ms();
             last_join_tc = false;
         }
@@ -1733,35 +1927,13 @@ struct knnj_ctx {
                     (int)tc, P.chunk, (unsigned long long)P.nitems, (unsigned long long)nv,
                     (unsigned long long)P.candidates, (unsigned long long)P.screened, lv.w, cov2, K, L,
                     last_join_kernel_ms);
-        FinalArgs f{};
-        f.X64 = X64.p;
-        f.n = n;
-        f.A = lv.J.p;
-        f.qpos = P.qpos.p;
-        f.qrow = P.qrow.p;
-        f.cnt = cnt.p;
-        f.pos = pos.p;
-        f.nrows = P.nq;
-        f.K = K;
-        f.L = L;
-        f.eps2 = eps2;
-        f.cover2 = cov2;
-        f.out_ids = out_ids;
-        f.out_dist = out_dist;
-        f.out_kth = out_kth;
-        f.out_status = out_status;
-        // big passes (at least a quarter of the points: the copy is N rows) gather rows in
-        // join order once
-        if (finalize_xj && P.nq >= (1u << 16) && 4 * P.nq >= N) {
-            if (!lv.xj_ready) {
-                lv.XJ.ensure((uint64_t)N * n);
-                launch_rows_by(X64.p, lv.J.p, N, n, lv.XJ.p, s);
-                lv.xj_ready = true;
-            }
-            f.XJ = lv.XJ.p;
-        }
         trace().mark("pass: join kernel", s);
-        launch_finalize(f, s);
+        if (overlap) {  // the chunks' finalizes ran on s_out; s continues after the last one
+            KJ_CUDA(cudaEventRecord(ev_fin, s_out));
+            KJ_CUDA(cudaStreamWaitEvent(s, ev_fin, 0));
+        } else {
+            launch_finalize(f, s);
+        }
         // split-part rows: finalized into their own exact top-K (with sq), merged below
         DBuf<uint32_t> t_ids, t_cnt, v_iota;
         DBuf<double> t_dist, t_sq, t_kth;
@@ -1815,15 +1987,26 @@ struct knnj_ctx {
             launch_slow_exact(X64.p, n, lv.J.p, P.qpos.p + r0, qrow, d_rows.p, novf, P.items.p,
                               row_item.p + r0, P.adj.p, K, eps2, cov2, o_ids, o_dist, o_kth,
                               o_st, o_sq, o_cnt, s);
+            if (to_host && host_patch && r0 == 0) {  // these rows reach the host by the patch
+                DBuf<uint32_t> orow;
+                orow.ensure(novf);
+                launch_map_u32(d_rows.p, qrow, novf, orow.p, s);
+                const size_t at = host_patch->size();
+                host_patch->resize(at + novf);
+                KJ_CUDA(cudaMemcpyAsync(host_patch->data() + at, orow.p, 4 * novf, cudaMemcpyDeviceToHost, s));
+            }
             sync();
         };
-        slow_range(0, P.nq, P.qrow.p, out_ids, out_dist, out_kth, out_status, nullptr, nullptr);
+        // (a bounded pass marks overflowed rows ST_MISS: they are re-run unbounded)
+        if (bound2 <= 0.0)
+            slow_range(0, P.nq, P.qrow.p, out_ids, out_dist, out_kth, out_status, nullptr, nullptr);
         if (nvv) {
             slow_range(P.nq, nvv, v_iota.p, t_ids.p, t_dist.p, t_kth.p, t_st.p, t_sq.p, t_cnt.p);
             launch_merge_parts(P.splits.p, P.nsplits, K, t_ids.p, t_sq.p, t_cnt.p, P.qrow.p, eps2,
                                cov2, out_ids, out_dist, out_kth, out_status, s);
         }
         trace().mark("pass: ovf + merge", s);
+        return to_host;
     }
 
     // Exact KNN for the given queries (pids + rows), certified globally: level
@@ -2130,6 +2313,25 @@ int knnj_set_option(knnj_ctx* c, const char* name, int64_t value) {
             c->simt_slack = (uint32_t)value;
         } else if (k == "early_d2h") {
             c->early_d2h = value != 0;
+        } else if (k == "stream_host") {
+            c->stream_host = value != 0;
+        } else if (k == "chunk_min_rows") {
+            if (value < 1 || value > (1 << 30)) throw Error(1, "chunk_min_rows must be in [1, 2^30]");
+            c->chunk_min_rows = (uint32_t)value;
+        } else if (k == "kth_bound") {
+            c->kth_bound = value != 0;
+        } else if (k == "kth_bound_q") {
+            if (value < 1 || value > 1000) throw Error(1, "kth_bound_q must be in [1, 1000] per mille");
+            c->kth_bound_q = (uint32_t)value;
+        } else if (k == "bound_min_rows") {
+            if (value < 0) throw Error(1, "bound_min_rows must be >= 0");
+            c->bound_min_rows = (uint64_t)value;
+        } else if (k == "bound_sample") {
+            if (value < 16 || value > (1 << 20)) throw Error(1, "bound_sample must be in [16, 2^20]");
+            c->bound_sample = (uint32_t)value;
+        } else if (k == "join_chunks") {
+            if (value < 1 || value > 64) throw Error(1, "join_chunks must be in [1, 64]");
+            c->join_chunks = (uint32_t)value;
         } else if (k == "finalize_xj") {
             c->finalize_xj = value != 0;
         } else if (k == "tc_slack") {
@@ -2575,6 +2777,10 @@ static void run_impl(knnj_ctx* c, const knnj_config* cfg, uint32_t shard, uint32
     const bool early_d2h = c->early_d2h;
     bool early_started = false;
     std::vector<uint32_t> fb_rows_host;  // rows the fallback rewrote (host ids)
+    bool streamed = false;               // level-0 rows went to the host from the finalize
+    uint32_t* h_ids_dev = nullptr;       // device views of the mapped host outputs
+    double* h_dist_dev = nullptr;
+    std::vector<uint32_t> patch_rows;    // rows rewritten after the streamed finalize
     struct OutSync {  // an early result copy never outlives the call (errors included)
         knnj_ctx* c;
         const bool& on;
@@ -2611,6 +2817,7 @@ static void run_impl(knnj_ctx* c, const knnj_config* cfg, uint32_t shard, uint32
         }
     } joiner{drawer}, hjoiner{hdrawer};
     {
+        Nvtx nv("knnj: reorder_by_variance");
         Timer t(s);
         c->reorder(m);
         I.ms_reorder = t.ms();
@@ -2707,6 +2914,7 @@ static void run_impl(knnj_ctx* c, const knnj_config* cfg, uint32_t shard, uint32
     } else {
         // ---- epsilon selection (orchestrator.cpp:137-165)
         {
+            Nvtx nv("knnj: estimate_eps_mean");
             Timer t(s);
             if (N < 2) throw Error(1, "eps_mean estimation needs at least two points");
             // the tensor-core histogram's candidate order, built while the host draws the
@@ -2723,6 +2931,7 @@ static void run_impl(knnj_ctx* c, const knnj_config* cfg, uint32_t shard, uint32
         std::vector<uint64_t> raw(cfg->n_bins, 0);
         uint32_t valid = cfg->n_bins;
         {
+            Nvtx nv("knnj: build_distance_histogram");
             Timer t(s);
             if (hdrawer.joinable()) hdrawer.join();
             auto& hq = hist_q;
@@ -2773,6 +2982,7 @@ static void run_impl(knnj_ctx* c, const knnj_config* cfg, uint32_t shard, uint32
 
         // ---- grid (GridIndex::build)
         {
+            Nvtx nv("knnj: grid build");
             Timer t(s);
             c->build_level(0, m, eps);
             c->eps0 = eps;
@@ -2787,6 +2997,7 @@ static void run_impl(knnj_ctx* c, const knnj_config* cfg, uint32_t shard, uint32
         DBuf<uint8_t> d_dense;
         bool have_dense = false;
         {
+            Nvtx nv("knnj: split_work");
             Timer t(s);
             const double mm = double(m);
             I.n_min = double(k_eff) * std::pow(2.0, mm) * std::tgamma(mm / 2.0 + 1.0) /
@@ -2828,19 +3039,88 @@ static void run_impl(knnj_ctx* c, const knnj_config* cfg, uint32_t shard, uint32
         uint64_t slow = 0;
         Pass P;
         {
+            Nvtx nv("knnj: level-0 join + top-K");
             Timer t(s);
             const bool fine = c->fine_f[0] > 0 || c->fine_f[1] > 0;
+            // Streamed results: host outputs in pinned memory are written by the finalize of
+            // each launch chunk while the next chunk joins (rows the slow path or the
+            // fallback rewrite later are patched at the end); otherwise one bulk copy.
+            if (nshard == 1 && ids && dist && !fine && c->stream_host) {
+                h_ids_dev = static_cast<uint32_t*>(mapped_host(ids, 4 * nq * k_eff));
+                h_dist_dev = static_cast<double*>(mapped_host(dist, 8 * nq * k_eff));
+                if (!h_ids_dev || !h_dist_dev) h_ids_dev = nullptr, h_dist_dev = nullptr;
+            }
+            // Radius bound (kth_bound): the K-th distance of a strided sample of the queries,
+            // taken at the kth_bound_q quantile, bounds most rows' K-th. The pass then
+            // screens only candidates within it (box filter and list cut); a row whose K-th
+            // is not within it (ST_MISS) is re-run without the bound, so every row ends with
+            // exactly the unbounded pass's result.
+            const double filt0 = fine ? 0.0 : c->filter_radius2(lv0);
+            double B2 = 0.0;
+            if (!fine && filt0 > 0.0 && c->kth_bound && nq >= c->bound_min_rows) {
+                std::vector<uint32_t> sq(c->bound_sample);
+                for (uint32_t i = 0; i < c->bound_sample; ++i)
+                    sq[i] = qid((uint64_t)i * nq / c->bound_sample);
+                B2 = c->sample_kth_bound(lv0, sq, k_eff, eps * eps, c->kth_bound_q);
+                if (!(B2 < c->bound_max_frac * filt0)) B2 = 0.0;
+                else B2 = (double)f32_round_up(B2);
+            }
+            I.kth_bound2 = B2;
             {
                 Timer tb(s);
+                c->stream_chunks = (nshard == 1 && !fine) ? c->join_chunks : 1;
                 c->build_pass(lv0, d_q.p, d_rows.p, nq, P, k_eff, shard, nshard,
-                              have_dense ? d_dense.p : nullptr, fine ? 0.0 : c->filter_radius2(lv0));
+                              have_dense ? d_dense.p : nullptr, B2 > 0.0 ? B2 : filt0, B2 <= 0.0);
+                c->stream_chunks = 1;
                 I.ms_join_build = tb.ms();
             }
             if (!fine) {
-                c->run_pass(lv0, P, k_eff, nullptr, eps * eps, c->cover2(lv0), o_ids.p, o_dist.p,
-                            o_kth.p, o_st.p, &slow);
+                DBuf<float> d_cut;
+                if (B2 > 0.0) {
+                    d_cut.ensure(P.nq);
+                    launch_fill_f32(d_cut.p, P.nq, (float)B2, s);
+                }
+                streamed = c->run_pass(lv0, P, k_eff, B2 > 0.0 ? d_cut.p : nullptr, eps * eps,
+                                       c->cover2(lv0), o_ids.p, o_dist.p, o_kth.p, o_st.p, &slow,
+                                       h_ids_dev, h_dist_dev, &patch_rows, B2);
                 I.ms_join_kernel = c->last_join_kernel_ms;
                 I.join_screened_pairs = P.screened;
+                if (B2 > 0.0) {
+                    // rows the bound missed: the unbounded level-0 pass over just those
+                    DBuf<uint8_t> fl;
+                    DBuf<uint32_t> mrows, mq;
+                    fl.ensure(P.nq);
+                    mrows.ensure(P.nq);
+                    launch_miss_flags(P.qrow.p, P.nq, o_st.p, fl.p, s);
+                    c->d_u64a.ensure(1);
+                    size_t bytes = 0;
+                    KJ_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, P.qrow.p, fl.p, mrows.p,
+                                                       c->d_u64a.p, (int64_t)P.nq, s));
+                    KJ_CUDA(cub::DeviceSelect::Flagged(c->sc.get(bytes), bytes, P.qrow.p, fl.p,
+                                                       mrows.p, c->d_u64a.p, (int64_t)P.nq, s));
+                    unsigned long long nmiss = 0;
+                    KJ_CUDA(cudaMemcpyAsync(&nmiss, c->d_u64a.p, 8, cudaMemcpyDeviceToHost, s));
+                    c->sync();
+                    I.bound_retried = nmiss;
+                    if (nmiss) {
+                        mq.ensure(nmiss);
+                        launch_map_u32(mrows.p, d_q.p, nmiss, mq.p, s);
+                        Pass P2;
+                        c->build_pass(lv0, mq.p, mrows.p, nmiss, P2, k_eff, 0, 1,
+                                      have_dense ? d_dense.p : nullptr, filt0);
+                        c->run_pass(lv0, P2, k_eff, nullptr, eps * eps, c->cover2(lv0), o_ids.p,
+                                    o_dist.p, o_kth.p, o_st.p, &slow);
+                        I.ms_join_kernel += c->last_join_kernel_ms;
+                        I.join_screened_pairs += P2.screened;
+                        if (streamed) {  // these host rows are patched at the end
+                            const size_t at = patch_rows.size();
+                            patch_rows.resize(at + nmiss);
+                            KJ_CUDA(cudaMemcpyAsync(patch_rows.data() + at, mrows.p, 4 * nmiss,
+                                                    cudaMemcpyDeviceToHost, s));
+                            c->sync();
+                        }
+                    }
+                }
             } else {
                 c->fine_cascade(m, eps, P, k_eff, have_dense ? d_dense.p : nullptr, o_ids.p,
                                 o_dist.p, o_kth.p, o_st.p, &slow, I);
@@ -2856,11 +3136,8 @@ static void run_impl(knnj_ctx* c, const knnj_config* cfg, uint32_t shard, uint32
         // single-GPU runs with host outputs: copy every row now, on a second stream, while
         // classification and the fallback run; the few rows the fallback rewrites are
         // patched afterwards
-        if (nshard == 1 && ids && dist && early_d2h) {
-            if (!c->s_out) {
-                KJ_CUDA(cudaStreamCreateWithFlags(&c->s_out, cudaStreamNonBlocking));
-                KJ_CUDA(cudaEventCreateWithFlags(&c->ev_out, cudaEventDisableTiming));
-            }
+        if (nshard == 1 && ids && dist && early_d2h && !streamed) {
+            c->ensure_out_stream();
             KJ_CUDA(cudaEventRecord(c->ev_out, s));
             KJ_CUDA(cudaStreamWaitEvent(c->s_out, c->ev_out, 0));
             KJ_CUDA(cudaMemcpyAsync(ids, o_ids.p, 4 * nq * k_eff, cudaMemcpyDeviceToHost, c->s_out));
@@ -2869,6 +3146,7 @@ static void run_impl(knnj_ctx* c, const knnj_config* cfg, uint32_t shard, uint32
         }
         // ---- classify on device; exact fallback for failures and uncertified sparse rows
         {
+            Nvtx nv("knnj: classify + exact fallback");
             Timer t(s);
             DBuf<uint8_t> need;
             need.ensure(n_own);
@@ -2939,7 +3217,23 @@ static void run_impl(knnj_ctx* c, const knnj_config* cfg, uint32_t shard, uint32
     // ---- results to the host: this shard's rows, ascending query id
     {
         Timer t(s);
-        if (nshard == 1 && early_started) {
+        if (nshard == 1 && streamed) {
+            // the level-0 rows are on the host already; patch what was rewritten after
+            std::vector<uint32_t>& pr = patch_rows;
+            pr.insert(pr.end(), fb_rows_host.begin(), fb_rows_host.end());
+            std::sort(pr.begin(), pr.end());
+            pr.erase(std::unique(pr.begin(), pr.end()), pr.end());
+            const uint64_t np = pr.size();
+            if (np) {
+                DBuf<uint32_t> d_pr;
+                d_pr.ensure(np);
+                KJ_CUDA(cudaMemcpyAsync(d_pr.p, pr.data(), 4 * np, cudaMemcpyHostToDevice, s));
+                launch_scatter_rows(d_pr.p, np, k_eff, o_ids.p, o_dist.p, h_ids_dev, h_dist_dev, s);
+            }
+            if (prov) KJ_CUDA(cudaMemcpyAsync(prov, d_prov.p, nq, cudaMemcpyDeviceToHost, s));
+            if (owned) std::memcpy(owned, host_queries().data(), 4 * nq);
+            c->sync();
+        } else if (nshard == 1 && early_started) {
             const uint64_t nfb = fb_rows_host.size();
             if (nfb > 65536) {  // many rewritten rows: copy everything again (after the early copy)
                 KJ_CUDA(cudaStreamSynchronize(c->s_out));

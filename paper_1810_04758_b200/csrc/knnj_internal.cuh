@@ -103,6 +103,8 @@ enum : uint8_t {
     ST_IN_EPS = 2,     // K-th exact sq <= eps^2 (dense "solved" rule, dense_engine.cpp:182)
     ST_CERT = 4,       // K-th exact sq < coverage^2 (1-eta): globally exact
     ST_OVF = 8,        // screen list overflowed (many near-ties): needs the exact slow path
+    ST_MISS = 16,      // radius-bounded pass: fewer than K candidates within the bound, or
+                       // the list overflowed; the row is re-run without the bound
 };
 
 // One grid level over all points (level 0 is the reference ε-grid; level L
@@ -154,6 +156,11 @@ struct Pass {
     uint64_t nv = 0, nsplits = 0;
     DBuf<uint32_t> vsrc;
     DBuf<uint4> splits;
+    // Launch chunks (passes built with stream_chunks > 1 and no split items): chunk c is
+    // items [chunk_item[c], chunk_item[c+1]) over the contiguous launch rows
+    // [chunk_row[c], chunk_row[c+1]); items are LPT-ordered inside each chunk. Empty: one
+    // launch over everything.
+    std::vector<uint64_t> chunk_item, chunk_row;
 };
 
 struct JoinArgs {
@@ -217,6 +224,10 @@ struct FinalArgs {
     double* out_sq;          // optional [qrow * K]: exact sq (split-part rows, for the merge)
     uint32_t* out_count;     // optional [qrow]: entries written (min(candidates, K))
     const double* XJ;        // optional: X64 rows in A order (row p = point A[p]); locality
+    double bound2;           // > 0: radius-bounded pass (every candidate with sq <= bound2 was
+                             // screened); rows whose K-th is not within it get ST_MISS only
+    uint32_t* host_ids;      // optional: the same rows also written straight to mapped host
+    double* host_dist;       //   memory (pinned), one coalesced store per row
 };
 
 struct HistArgs {
@@ -365,6 +376,8 @@ void launch_split_flags(const uint32_t* pids, uint64_t nq, const uint32_t* slot,
                         cudaStream_t s);
 void launch_rows_by(const double* X64, const uint32_t* A, uint64_t N, uint32_t n, double* out,
                     cudaStream_t s);
+void launch_miss_flags(const uint32_t* rows, uint64_t n, const uint8_t* st, uint8_t* flags,
+                       cudaStream_t s);
 void launch_uncert_flags(const uint32_t* rows, uint64_t n, const uint8_t* st, uint8_t* flags,
                          cudaStream_t s);
 void launch_classify(const uint32_t* rows, uint64_t n, const uint8_t* st, const uint8_t* dense,
@@ -376,5 +389,7 @@ void launch_find_ovf(const uint32_t* cnt, uint64_t n, uint32_t* rows, unsigned l
                      cudaStream_t s);
 void launch_gather_rows(const uint32_t* rows, uint64_t n, uint32_t K, const uint32_t* ids,
                         const double* dist, uint32_t* oids, double* odist, cudaStream_t s);
+void launch_scatter_rows(const uint32_t* rows, uint64_t n, uint32_t K, const uint32_t* ids,
+                         const double* dist, uint32_t* oids, double* odist, cudaStream_t s);
 
 }  // namespace kj

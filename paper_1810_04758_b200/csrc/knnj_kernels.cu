@@ -305,6 +305,9 @@ __device__ __forceinline__ void rank_entries(const double (&sq)[EMAX], const uin
 }
 
 // ---------------------------------------------------------------- finalize
+// per-warp staging of one output row (K ids, pad, K doubles), 16-byte multiples
+__host__ __device__ __forceinline__ uint32_t fin_stage_words(uint32_t K) { return 4 * ((3 * K + 7) / 4); }
+
 // One warp per launch row: exact FP64 distances for the screened list, exact
 // (sq,id) ranks, first K written to the query's output row, status bits.
 __global__ void k_finalize(FinalArgs a) {
@@ -315,7 +318,7 @@ __global__ void k_finalize(FinalArgs a) {
     if (c == SKIP) return;  // a split row: its parts are finalized and merged separately
     const uint32_t orow = a.qrow[row];
     if (c == OVF) {
-        if (lane == 0) a.out_status[orow] = ST_OVF;
+        if (lane == 0) a.out_status[orow] = a.bound2 > 0.0 ? ST_MISS : ST_OVF;
         return;
     }
     const uint32_t qp = a.qpos[row];
@@ -350,15 +353,31 @@ __global__ void k_finalize(FinalArgs a) {
         default: break;
     }
     double kth = CUDART_INF;
+    // mapped host rows: staged per warp, then one coalesced store per row (full PCIe lines)
+    extern __shared__ __align__(16) unsigned char fin_smem[];
+    const int wib = threadIdx.x >> 5;
+    uint32_t* s_ids = reinterpret_cast<uint32_t*>(fin_smem) + (size_t)wib * fin_stage_words(a.K);
+    double* s_dist = reinterpret_cast<double*>(s_ids + a.K + (a.K & 1));
 #pragma unroll
     for (int f = 0; f < EMAX; ++f) {
         const uint32_t i = f * 32 + lane;
         if (f < E && i < c && rk[f] < a.K) {
+            const double d = sqrt(sq[f]);
             a.out_ids[(uint64_t)orow * a.K + rk[f]] = id[f];
-            a.out_dist[(uint64_t)orow * a.K + rk[f]] = sqrt(sq[f]);
+            a.out_dist[(uint64_t)orow * a.K + rk[f]] = d;
             if (a.out_sq) a.out_sq[(uint64_t)orow * a.K + rk[f]] = sq[f];
+            if (a.host_ids) {
+                s_ids[rk[f]] = id[f];
+                s_dist[rk[f]] = d;
+            }
             if (rk[f] == a.K - 1) kth = sq[f];
         }
+    }
+    if (a.host_ids) {
+        __syncwarp();
+        const uint32_t w = min(c, a.K);
+        for (uint32_t i = lane; i < w; i += 32) a.host_ids[(uint64_t)orow * a.K + i] = s_ids[i];
+        for (uint32_t i = lane; i < w; i += 32) a.host_dist[(uint64_t)orow * a.K + i] = s_dist[i];
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) kth = fmin(kth, __shfl_xor_sync(0xffffffffu, kth, o));
@@ -369,6 +388,9 @@ __global__ void k_finalize(FinalArgs a) {
             if (kth <= a.eps2) st |= ST_IN_EPS;
             if (kth < a.cover2) st |= ST_CERT;
         }
+        // bounded pass: the listed top-K is the exact one only if its K-th lies within the
+        // bound (every candidate up to it was screened); otherwise re-run unbounded
+        if (a.bound2 > 0.0 && !(c >= a.K && kth <= a.bound2)) st = ST_MISS;
         a.out_status[orow] = st;
         a.out_kth[orow] = c >= a.K ? kth : CUDART_INF;
         if (a.out_count) a.out_count[orow] = min(c, a.K);
@@ -581,7 +603,12 @@ void launch_join(const JoinArgs& a, uint64_t nitems, uint32_t qb, cudaStream_t s
 void launch_finalize(const FinalArgs& a, cudaStream_t s) {
     if (a.nrows == 0) return;
     uint64_t threads = a.nrows * 32;
-    k_finalize<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(a);
+    if (a.host_ids) {  // 2 warps per block, K x 12 B staging each (fits next to a join CTA)
+        const size_t sm = 2 * 4 * (size_t)fin_stage_words(a.K);
+        k_finalize<<<(unsigned)((threads + 63) / 64), 64, sm, s>>>(a);
+    } else {
+        k_finalize<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(a);
+    }
     KJ_CUDA(cudaGetLastError());
     g_launches.fetch_add(1, std::memory_order_relaxed);
 }
@@ -1499,6 +1526,18 @@ void launch_rows_by(const double* X64, const uint32_t* A, uint64_t N, uint32_t n
 }
 
 // rows whose list is not yet globally exact (fine cascade: they go on to level 0)
+__global__ void k_miss_flags(const uint32_t* rows, uint64_t n, const uint8_t* st, uint8_t* flags) {
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x)
+        flags[i] = (st[rows[i]] & ST_MISS) ? 1 : 0;
+}
+void launch_miss_flags(const uint32_t* rows, uint64_t n, const uint8_t* st, uint8_t* flags,
+                       cudaStream_t s) {
+    if (!n) return;
+    k_miss_flags<<<(unsigned)std::min<uint64_t>((n + 255) / 256, 148 * 16), 256, 0, s>>>(rows, n, st, flags);
+    KJ_CUDA(cudaGetLastError());
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+}
 __global__ void k_uncert_flags(const uint32_t* rows, uint64_t n, const uint8_t* st, uint8_t* flags) {
     for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
          i += uint64_t(gridDim.x) * blockDim.x) {
@@ -1558,6 +1597,25 @@ void launch_gather_rows(const uint32_t* rows, uint64_t n, uint32_t K, const uint
                         const double* dist, uint32_t* oids, double* odist, cudaStream_t s) {
     if (!n || !K) return;
     k_gather_rows<<<2368, 256, 0, s>>>(rows, n, K, ids, dist, oids, odist);
+    KJ_CUDA(cudaGetLastError());
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+// rows[i] of (ids, dist) to the same rows of (oids, odist) (e.g. mapped host memory)
+__global__ void k_scatter_rows(const uint32_t* rows, uint64_t n, uint32_t K, const uint32_t* ids,
+                               const double* dist, uint32_t* oids, double* odist) {
+    const uint64_t total = n * K;
+    for (uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+         e += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t i = e / K, j = e - i * K;
+        const uint64_t at = (uint64_t)rows[i] * K + j;
+        oids[at] = ids[at];
+        odist[at] = dist[at];
+    }
+}
+void launch_scatter_rows(const uint32_t* rows, uint64_t n, uint32_t K, const uint32_t* ids,
+                         const double* dist, uint32_t* oids, double* odist, cudaStream_t s) {
+    if (!n || !K) return;
+    k_scatter_rows<<<1184, 256, 0, s>>>(rows, n, K, ids, dist, oids, odist);
     KJ_CUDA(cudaGetLastError());
     g_launches.fetch_add(1, std::memory_order_relaxed);
 }

@@ -133,6 +133,26 @@ __device__ __forceinline__ float tmem_ld1(uint32_t taddr) {
     return __uint_as_float(r);
 }
 
+// up to 8 single columns (any addresses) in flight, one wait
+__device__ __forceinline__ void tmem_ld8(const uint32_t (&ta)[8], float (&x)[8]) {
+    uint32_t r[8];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%8];\n\t"
+        "tcgen05.ld.sync.aligned.32x32b.x1.b32 {%1}, [%9];\n\t"
+        "tcgen05.ld.sync.aligned.32x32b.x1.b32 {%2}, [%10];\n\t"
+        "tcgen05.ld.sync.aligned.32x32b.x1.b32 {%3}, [%11];\n\t"
+        "tcgen05.ld.sync.aligned.32x32b.x1.b32 {%4}, [%12];\n\t"
+        "tcgen05.ld.sync.aligned.32x32b.x1.b32 {%5}, [%13];\n\t"
+        "tcgen05.ld.sync.aligned.32x32b.x1.b32 {%6}, [%14];\n\t"
+        "tcgen05.ld.sync.aligned.32x32b.x1.b32 {%7}, [%15];\n\t"
+        "tcgen05.wait::ld.sync.aligned;"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+        : "r"(ta[0]), "r"(ta[1]), "r"(ta[2]), "r"(ta[3]), "r"(ta[4]), "r"(ta[5]), "r"(ta[6]), "r"(ta[7])
+        : "memory");
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] = __uint_as_float(r[i]);
+}
+
 // K-th smallest (1-based k) of the 32*R values a[r] (element index r*32 + lane)
 // held across a warp: bitonic sort network, ascending.
 template <int R>
@@ -565,16 +585,29 @@ __global__ void __launch_bounds__(64 + 128 * G, 1)
                         mk[1] |= (v1[j] <= rhs ? 1u : 0u) << j;
                     }
                 }
+                // the columns any lane hit, 8 TMEM column loads in flight per batch
+                unsigned long long um = (unsigned long long)__reduce_or_sync(0xffffffffu, mk[0]) |
+                                        ((unsigned long long)__reduce_or_sync(0xffffffffu, mk[1]) << 32);
+                const unsigned long long mine = (unsigned long long)mk[0] | ((unsigned long long)mk[1] << 32);
+                while (um) {
+                    int jj[8];
+                    uint32_t ta[8];
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    unsigned um = __reduce_or_sync(0xffffffffu, mk[h]);
-                    while (um) {
-                        const int j = __ffs(um) - 1;
+                    for (int b = 0; b < 8; ++b) {
+                        jj[b] = um ? __ffsll((long long)um) - 1 : -1;
                         um &= um - 1;
+                        ta[b] = tbase + j0 + (uint32_t)(jj[b] < 0 ? 0 : jj[b]);
+                    }
+                    float xs[8];
+                    tmem_ld8(ta, xs);
+#pragma unroll
+                    for (int b = 0; b < 8; ++b) {
+                        const int j = jj[b];
+                        if (j < 0) break;
                         ++st_bits;
-                        const float x = tmem_ld1(tbase + j0 + h * 32 + j);
-                        const uint32_t pos = s + j0 + h * 32 + j;
-                        bool want = ((mk[h] >> j) & 1u) && x <= rhs && pos != qp;
+                        const float x = xs[b];
+                        const uint32_t pos = s + j0 + j;
+                        bool want = ((mine >> j) & 1ull) && x <= rhs && pos != qp;
                         // make room: cooperative compaction of every full buffer that needs it
                         unsigned full = __ballot_sync(0xffffffffu, want && cnt == LB);
                         while (full) {

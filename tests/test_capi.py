@@ -47,7 +47,7 @@ def test_python_binding_covers_header():
 
 def test_abi_version_without_gpu(lib):
     lib.knnj_abi_version.restype = ctypes.c_int
-    assert lib.knnj_abi_version() == 4
+    assert lib.knnj_abi_version() == 5
 
 
 def test_library_is_sm100a_only():

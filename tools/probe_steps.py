@@ -28,7 +28,8 @@ for o in a.opt:
 eng.set_points(X)
 keys = ["ms_total", "ms_eps_mean", "ms_histogram", "ms_hist_kernel", "ms_grid", "ms_join_build",
         "ms_join", "ms_join_kernel", "ms_fallback", "fallback_queries", "fallback_passes",
-        "slow_path_queries", "failed_count", "q_cpu", "hist_bins_counted", "join_candidate_pairs", "join_screened_pairs"]
+        "slow_path_queries", "failed_count", "q_cpu", "hist_bins_counted", "join_candidate_pairs", "join_screened_pairs",
+        "kth_bound2", "bound_retried", "eps_used"]
 for st in range(a.steps):
     t = time.time()
     r = eng.run(RunConfig(k=c["k"], mode="hybrid", seed=1), out=(0, 0, 0), want_hist=a.hist)
