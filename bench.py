@@ -35,6 +35,8 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "KNN self-join points/sec (end-to-end, K=32) at 1/2/4/8 B200 vs CPU ref"
+PHASES = ("ms_total", "ms_reorder", "ms_eps_mean", "ms_histogram", "ms_grid", "ms_split", "ms_join",
+          "ms_fallback", "ms_join_kernel", "ms_hist_kernel", "ms_join_build", "ms_download")
 UNIT = "points/s"
 
 
@@ -395,10 +397,9 @@ def run_ours(args, cfgd, X):
                                            "P_mean) against the measured FFMA peak, B against "
                                            "MEASURED_PEAKS hbm_gbs; above 1 = work the run "
                                            "avoids (capped histogram, box filter, tensor screen)"},
-            "phases_ms": {k2: statistics.mean(i[k2] for i in infos) for k2 in
-                          ("ms_reorder", "ms_eps_mean", "ms_histogram", "ms_grid", "ms_split",
-                           "ms_join", "ms_fallback", "ms_join_kernel", "ms_hist_kernel", "ms_join_build",
-                           "ms_download")},
+            "phases_ms": {k2: statistics.mean(i[k2] for i in infos) for k2 in PHASES},
+            "phases_ms_e2e": {k2: statistics.mean(i[k2] for i in infos_e2e) for k2 in PHASES},
+            "kth_bound": {"bound2": info["kth_bound2"], "rows_retried": info["bound_retried"]},
             "hist_pairs_per_s": hist_pairs / (hist_ms * 1e-3) if hist_ms > 0 else None,
             "gpu_launches": int(info["kernel_launches"]),
             "clocks": clk.summary(),

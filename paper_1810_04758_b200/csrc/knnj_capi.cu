@@ -220,6 +220,11 @@ Trace& trace() {
     return t;
 }
 
+// work items of at most 32 queries (the SIMT join's 32-thread blocks)
+struct SmallItem {
+    __device__ bool operator()(const uint4& it) const { return it.y - it.x <= 32u; }
+};
+
 // Device address of a host range in pinned (page-locked, mapped) memory, else null:
 // kernels may then store straight into it over PCIe.
 void* mapped_host(void* p, size_t bytes) {
@@ -295,6 +300,7 @@ struct knnj_ctx {
     DBuf<unsigned long long> d_u64a, d_u64b;
     DBuf<double> d_part;
 
+    DBuf<float> d_gbox;            // g rounded down [n], then up [n]
     cudaStream_t s_out = nullptr;  // result D2H overlapping the fallback (knnj_run)
     cudaEvent_t ev_out = nullptr;
     ~knnj_ctx() {
@@ -307,9 +313,14 @@ struct knnj_ctx {
     }
 
     void sync() { KJ_CUDA(cudaStreamSynchronize(s)); }
+    // the result stream runs at the highest priority: its finalize / copy blocks are
+    // dispatched ahead of the running join's next CTAs and then co-reside with them
+    bool out_priority = true;
     void ensure_out_stream() {
         if (!s_out) {
-            KJ_CUDA(cudaStreamCreateWithFlags(&s_out, cudaStreamNonBlocking));
+            int lo = 0, hi = 0;
+            KJ_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+            KJ_CUDA(cudaStreamCreateWithPriority(&s_out, cudaStreamNonBlocking, out_priority ? hi : lo));
             KJ_CUDA(cudaEventCreateWithFlags(&ev_out, cudaEventDisableTiming));
         }
     }
@@ -338,6 +349,16 @@ struct knnj_ctx {
         for (uint32_t j = 0; j < n; ++j) g[j] = mean0[order[j]];
         d_g.ensure(n);
         KJ_CUDA(cudaMemcpyAsync(d_g.p, g.data(), n * 8, cudaMemcpyHostToDevice, s));
+        {  // the centre rounded outward to FP32 (per-item screen radii, filter_items)
+            std::vector<float> gb(2 * n);
+            for (uint32_t j = 0; j < n; ++j) {
+                gb[j] = f32_round_down(g[j]);
+                gb[n + j] = f32_round_up(g[j]);
+            }
+            d_gbox.ensure(2 * n);
+            KJ_CUDA(cudaMemcpyAsync(d_gbox.p, gb.data(), 8 * n, cudaMemcpyHostToDevice, s));
+            sync();
+        }
         Npad = ((N + 127) / 128) * 128 + 128;
         Xf.ensure((uint64_t)n * Npad);
         d_u64a.ensure(1);
@@ -1136,14 +1157,16 @@ struct knnj_ctx {
     bool finalize_xj = true;      // finalize reads FP64 rows from a join-ordered copy
     bool early_d2h = true;        // knnj_run: result D2H overlaps classification + fallback
     bool stream_host = true;      // knnj_run into pinned outputs: rows written by the finalize
-    uint32_t join_chunks = 8;     // level-0 launches (finalize of one overlaps the next join)
+    uint32_t join_chunks = 16;    // level-0 launches (finalize of one overlaps the next join)
     uint32_t chunk_min_rows = 65536;  // ... each of at least this many query rows
+    uint32_t fin_blocks = 148 * 2;    // grid of a chunk's overlapped finalize (0: one warp per row)
+    uint32_t copy_blocks = 74;        // grid of a chunk's row copy to the host (0: one warp per row)
     // level-0 radius bound (run_impl): sample size, quantile (per mille) of the sample's
     // K-th sq, the largest bound worth using (fraction of the filter radius^2), and the
     // smallest pass it is tried on
     bool kth_bound = true;
     uint32_t bound_sample = 4096;
-    uint32_t kth_bound_q = 990;
+    uint32_t kth_bound_q = 999;
     double bound_max_frac = 0.8;
     uint64_t bound_min_rows = 200000;
 
@@ -1229,11 +1252,23 @@ struct knnj_ctx {
     //      |key| <= 4 R^2: 5 u24 R^2 (the cuts round up, __fadd_ru / __fsub_ru).
     //  (4) FP64: the scaled coordinates, |b|^2 and the reference's scalar-order sq64:
     //      (4n + 12) 4 U64 R^2.
-    double tc_delta() const {
+    double tc_delta() const { return tc_delta_at(Rg / tc_S()); }
+    // tc_delta_at(R) is a quadratic A R^2 + B R + C in the data radius R (every term
+    // below is): its coefficients, inflated slightly against the evaluation's rounding,
+    // for the per-item bound of items whose data lie within R of the centre
+    void tc_delta_poly(double& A, double& B, double& C) const {
+        const double f0 = tc_delta_at(0.0), f1 = tc_delta_at(1.0), f2 = tc_delta_at(2.0);
+        C = f0;
+        A = (f2 - 2.0 * f1 + f0) / 2.0;
+        B = f1 - A - f0;
+        A *= 1.0 + 1e-9;
+        B = std::max(0.0, B) * (1.0 + 1e-9) + 1e-9 * A;
+        C *= 1.0 + 1e-9;
+    }
+    double tc_delta_at(double R) const {
         const double u10 = std::ldexp(1.0, -10), u11 = std::ldexp(1.0, -11);
         const double u22 = std::ldexp(1.0, -22), u23 = std::ldexp(1.0, -23);
         const double u24 = std::ldexp(1.0, -24), u25 = std::ldexp(1.0, -25);
-        const double R = Rg / tc_S();
         const double R2 = R * R;
         const double rt = std::sqrt((double)n);
         const double rep = 6 * u22 * R2 + 2 * u24 * rt * R + 2 * u22 * R2 + 2 * u24;
@@ -1272,9 +1307,9 @@ struct knnj_ctx {
         const double S = tc_S();
         return 2.0 * tc_delta() * S * S <= 0.02 * w * w;
     }
-    TcJoinCfg tc_join_cfg(uint32_t K, double w) const {
+    TcJoinCfg tc_join_cfg(uint32_t K, double w, bool any_precision = false) const {
         TcJoinCfg c;
-        if (!use_tc() || K < 1 || !tc_precise_for(w)) return c;
+        if (!use_tc() || K < 1 || (!any_precision && !tc_precise_for(w))) return c;
         const uint32_t KB = tc_row_halfs() / 64;
         const uint32_t L0 = K + tc_slack;
         if (KB >= 3) {
@@ -1312,9 +1347,22 @@ struct knnj_ctx {
     // level lv and builds work items + candidate ranges.
     // the join kernel a pass will run on (decided before its items are built)
     bool pass_uses_tc(const Level& lv, uint32_t K) const { return tc_join_cfg(K, lv.w).ok; }
-    uint32_t pass_chunk(const Level& lv, uint32_t K) const {
+    // Mixed passes (item_tc): the global precision rule fails (data far from the centre
+    // somewhere), but items whose own data lie close enough to it pass the rule with a
+    // per-item bound; those run on the tensor cores, the rest on the SIMT kernel. Needs
+    // the box filter (it measures each item's radius) and 128-query items (G = 1).
+    bool item_tc = true;
+    uint32_t item_tc_min_q = 32;  // ... and items with at least this many queries
+    bool pass_mixed(const Level& lv, uint32_t K, double filter_r2) const {
+        if (!item_tc || !(filter_r2 > 0.0) || !box_filter || tc_join_cfg(K, lv.w).ok) return false;
+        const TcJoinCfg c = tc_join_cfg(K, lv.w, true);
+        return c.ok && c.sh.G == 1;
+    }
+    uint32_t pass_chunk(const Level& lv, uint32_t K, double filter_r2 = 0.0) const {
         const TcJoinCfg c = tc_join_cfg(K, lv.w);
-        return c.ok ? 128u * c.sh.G : (uint32_t)JB;
+        if (c.ok) return 128u * c.sh.G;
+        if (pass_mixed(lv, K, filter_r2)) return 128u;
+        return (uint32_t)JB;
     }
     // Sharded (nshard > 1): only a contiguous run of work items in cell order is kept
     // (SURVEY.md §8e), cut at equal shares of the estimated tile work; the pass then
@@ -1330,8 +1378,10 @@ struct knnj_ctx {
         P.nsplits = 0;
         P.row_begin = 0;
         P.candidates_dense = 0;
-        uint32_t chunk = K ? pass_chunk(lv, K) : (uint32_t)JB;
+        uint32_t chunk = K ? pass_chunk(lv, K, filter_r2) : (uint32_t)JB;
         P.chunk = chunk;
+        P.mixed = K && pass_mixed(lv, K, filter_r2);
+        P.has_r2 = false;
         P.nitems = P.nadj = P.candidates = 0;
         if (!nq) return;
         DBuf<uint32_t> pos_unsorted, qcell;
@@ -1367,7 +1417,7 @@ struct knnj_ctx {
         // 32-thread blocks instead of mostly idle 128-thread ones. (Not in the fallback
         // levels: few queries against huge neighbourhoods are tile-load bound there, and
         // 128 threads load a tile 4x faster; measured on C4.)
-        if (chunk == (uint32_t)JB && K && (&lv == &levels[0] || &lv >= &levels[40]) &&
+        if (chunk == (uint32_t)JB && K && !P.mixed && (&lv == &levels[0] || &lv >= &levels[40]) &&
             double(nq) / double(std::max<uint64_t>(nuc, 1)) < 48.0) {
             chunk = 32;
             P.chunk = 32;
@@ -1533,7 +1583,7 @@ struct knnj_ctx {
         // A streamed pass is cut into stream_chunks launches over contiguous row ranges
         // (items grouped by the chunk their first row falls in, LPT inside each), so one
         // chunk's finalize and result copy overlap the next chunk's join.
-        const uint32_t nch = (stream_chunks > 1 && P.nv == nq_own &&
+        const uint32_t nch = (stream_chunks > 1 && P.nv == nq_own && !P.mixed &&
                               nq_own >= (uint64_t)chunk_min_rows * stream_chunks)
                                  ? stream_chunks : 1;
         auto chunk_of = [&](const uint4& it) { return (uint32_t)((uint64_t)it.x * nch / nq_own); };
@@ -1598,7 +1648,7 @@ struct knnj_ctx {
         P.candidates = cand;
         P.screened = cand;
         if (filter_r2 > 0.0 && box_filter && P.nitems)
-            filter_ranges(lv, P, filter_r2, K > 0 && pass_uses_tc(lv, K));
+            filter_ranges(lv, P, filter_r2, K > 0 && (pass_uses_tc(lv, K) || P.mixed));
     }
 
     // launches a big level-0 pass is cut into (build_pass; 1 = one launch)
@@ -1629,8 +1679,26 @@ struct knnj_ctx {
             launch_block_boxes(X64.p, lv.J.p, N, n, lv.bbox.p, s);
             lv.bbox_ready = true;
         }
+        float* r2_out = nullptr;
+        if (P.mixed) {
+            P.item_r2.ensure(P.nitems);
+            r2_out = P.item_r2.p;
+        }
+        DBuf<float> dbox;  // the grid dims' data range, rounded outward
+        if (P.mixed) {
+            std::vector<float> hb(2 * lv.m);
+            for (uint32_t d = 0; d < lv.m; ++d) {
+                hb[d] = f32_round_down(lv.mins[d]);
+                hb[lv.m + d] = f32_round_up(lv.maxs[d]);
+            }
+            dbox.ensure(2 * lv.m);
+            KJ_CUDA(cudaMemcpyAsync(dbox.p, hb.data(), 8 * lv.m, cudaMemcpyHostToDevice, s));
+            sync();
+        }
         P.screened = filter_items(P.items.p, P.nitems, P.qpos.p, lv.J.p, lv.bbox.p, P.adj, P.nadj, r2,
-                                  sweep_order && tc_pass);
+                                  sweep_order && tc_pass, r2_out, lv.m,
+                                  f32_round_up(2.0 * lv.w * (1.0 + 1e-6)), dbox.p);
+        P.has_r2 = r2_out != nullptr;
     }
     // kept FB-blocks per item under the box filter (the filter's count pass only; items and
     // adj are left unchanged)
@@ -1660,7 +1728,8 @@ struct knnj_ctx {
     // sqrt(r2) of the item's query box; adj is replaced. Returns the kept candidate pairs.
     uint64_t filter_items(uint4* items, uint64_t nitems, const uint32_t* qpos, const uint32_t* J,
                           const float* bbox, DBuf<uint2>& adj, uint64_t& nadj, double r2,
-                          bool order = false) {
+                          bool order = false, float* item_r2 = nullptr, uint32_t r_m = 0,
+                          float r_2w = 0.f, const float* dbox = nullptr) {
         const uint64_t nblk = (N + FB - 1) / FB;
         // FP64 scalar sums can fall below the true sq: widen, then round up to FP32
         const float r2c = f32_round_up(r2 * (1.0 + 1e-9));
@@ -1705,7 +1774,7 @@ struct knnj_ctx {
         d_u64a.ensure(1);
         KJ_CUDA(cudaMemsetAsync(d_u64a.p, 0, 8, s));
         launch_filter_ranges(items, nitems, qbox.p, n, adj.p, bbox, nblk, r2c, nullptr, off.p,
-                             adj2.p, d_u64a.p, true, s, kp);
+                             adj2.p, d_u64a.p, true, s, kp, nullptr, d_gbox.p, item_r2, r_m, r_2w, dbox);
         if (order && total) {
             // nearest blocks first inside every item: the top-K cut converges early
             DBuf<uint2> adj3;
@@ -1732,6 +1801,7 @@ struct knnj_ctx {
 
     double last_join_kernel_ms = 0.0;
     bool last_join_tc = false;
+    unsigned long long last_mixed_tc_items = 0;
     // Runs the fused join over a pass, then the exact finalize (and the slow
     // path for overflowed lists). Writes rows of out_* (indexed by qrow).
     // With host_ids/host_dist (mapped pinned host memory) and a pass built in chunks, the
@@ -1745,14 +1815,16 @@ struct knnj_ctx {
                   double bound2 = 0.0) {
         if (!P.nq) return false;
         if (bound2 > 0.0 && P.nv != P.nq) throw Error(9, "a radius-bounded pass cannot hold split items");
-        const TcJoinCfg tcc = tc_join_cfg(K, lv.w);
-        const bool tc = tcc.ok && P.chunk == 128u * tcc.sh.G;
-        if (!tc && P.chunk != (uint32_t)JB && P.chunk != 32u)
+        const TcJoinCfg tcm = tc_join_cfg(K, lv.w, true);
+        const bool mixed = P.mixed && P.has_r2 && tcm.ok && tcm.sh.G == 1 && P.chunk == 128u;
+        const TcJoinCfg tcc = mixed ? tcm : tc_join_cfg(K, lv.w);
+        const bool tc = !mixed && tcc.ok && P.chunk == 128u * tcc.sh.G;
+        if (!tc && !mixed && P.chunk != (uint32_t)JB && P.chunk != 32u)
             throw Error(9, "pass built for a different kernel");
         // list capacity: K plus slack for near-ties inside the screen band (overflow -> exact slow path)
         // SIMT list slack: every extra slot costs shared memory (occupancy) and insertion
         // shifts; C4 (K=64) runs 11.8 s at K+32, 9.1 s at K+8 with no overflow rows
-        const uint32_t L = tc ? tcc.L : K + (simt_slack ? simt_slack : std::max<uint32_t>(8, K / 8));
+        const uint32_t L = (tc || mixed) ? tcc.L : K + (simt_slack ? simt_slack : std::max<uint32_t>(8, K / 8));
         if (L > 256)
             throw Error(1, "k = " + std::to_string(K) + " needs a near-tie list of " + std::to_string(L) +
                                " entries; the device join holds at most 256");
@@ -1760,10 +1832,11 @@ struct knnj_ctx {
         if (np < 0) throw Error(1, "dimension count above 128 is not supported by the device join");
         if (!tc && join_smem_bytes(np, L, P.chunk) > 227 * 1024)
             throw Error(1, "k too large for the device join");
+        bool mixed_tc_ran = false;
         const uint64_t nv = P.nv, nvv = P.nv - P.nq;  // launch rows; virtual (split-part) rows
         // chunk boundaries (one launch unless the pass was built in chunks)
         std::vector<uint64_t> ci = P.chunk_item, cr = P.chunk_row;
-        if (ci.size() < 2 || nvv) {
+        if (ci.size() < 2 || nvv || mixed) {
             ci = {0, P.nitems};
             cr = {0, P.nq};
         }
@@ -1816,10 +1889,6 @@ struct knnj_ctx {
         f.out_kth = out_kth;
         f.out_status = out_status;
         f.bound2 = bound2;
-        if (to_host) {
-            f.host_ids = host_ids;
-            f.host_dist = host_dist;
-        }
         // big passes (at least a quarter of the points: the copy is N rows) gather rows in
         // join order once
         if (finalize_xj && P.nq >= (1u << 16) && 4 * P.nq >= N) {
@@ -1830,16 +1899,39 @@ struct knnj_ctx {
             }
             f.XJ = lv.XJ.p;
         }
-        // the finalize of launch rows [cr[c], cr[c+1]) (on s_out behind chunk c's join)
-        auto finalize_chunk = [&](size_t c) {
+        // the finalize of launch rows [cr[c], cr[c+1]) (on s_out behind chunk c's join), on
+        // a bounded grid so it shares the SMs with the next chunk's join; rows that go to
+        // the host are taken in ascending output row (sorted per chunk on s_out)
+        uint64_t maxlen = 0;
+        for (size_t c = 0; c < nch; ++c) maxlen = std::max<uint64_t>(maxlen, cr[c + 1] - cr[c]);
+        DBuf<uint32_t> o_keys;
+        DBuf<unsigned char> o_tmpbuf;
+        void* o_tmp = nullptr;
+        size_t o_tmp_bytes = 0;
+        if (to_host) {
+            o_keys.ensure(maxlen);
+            KJ_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, o_tmp_bytes, P.qrow.p, o_keys.p,
+                                                   (int64_t)maxlen, 0, bits_for(N), s));
+            o_tmp = o_tmpbuf.ensure(o_tmp_bytes);
+        }
+        // the finalize of launch rows [cr[c], cr[c+1]) into the device rows, then (to_host)
+        // the chunk's rows to the host in ascending output row
+        auto finalize_chunk = [&](size_t c, cudaStream_t st) {
             FinalArgs fc = f;
             fc.qpos = P.qpos.p + cr[c];
             fc.qrow = P.qrow.p + cr[c];
             fc.cnt = cnt.p + cr[c];
             fc.pos = pos.p + cr[c] * L;
             fc.nrows = cr[c + 1] - cr[c];
-            KJ_CUDA(cudaStreamWaitEvent(s_out, ev_join[c], 0));
-            launch_finalize(fc, s_out);
+            if (st == s_out) KJ_CUDA(cudaStreamWaitEvent(s_out, ev_join[c], 0));
+            launch_finalize(fc, st, st == s_out ? fin_blocks : 0);
+            if (to_host && fc.nrows) {
+                size_t bytes = o_tmp_bytes;
+                KJ_CUDA(cub::DeviceRadixSort::SortKeys(o_tmp, bytes, P.qrow.p + cr[c], o_keys.p,
+                                                       (int64_t)fc.nrows, 0, bits_for(N), st));
+                launch_rows_to_host(o_keys.p, fc.nrows, K, out_ids, out_dist, host_ids, host_dist,
+                                    st == s_out ? copy_blocks : 0, st);
+            }
         };
         if (tc) {
             prep_tc(lv);
@@ -1878,7 +1970,7 @@ struct knnj_ctx {
                 launch_join_tc(ac, tcc.sh, ci[c + 1] - ci[c], N, s);
                 if (overlap) {
                     KJ_CUDA(cudaEventRecord(ev_join[c], s));
-                    finalize_chunk(c);
+                    finalize_chunk(c, s_out);
                 }
             }
             last_join_kernel_ms = t.ms();
@@ -1890,6 +1982,115 @@ struct knnj_ctx {
                         (unsigned long long)P.nitems, (unsigned long long)nv, h[0], h[1], h[2], h[3], h[4], last_join_kernel_ms);
             }
             last_join_tc = true;
+        } else if (mixed) {
+            // per-item screen bound and eligibility, then the two kernels over their items
+            DBuf<float> dlt, tc_dlt;
+            DBuf<uint8_t> okf;
+            DBuf<uint4> part;
+            dlt.ensure(P.nitems);
+            tc_dlt.ensure(P.nitems);
+            okf.ensure(P.nitems);
+            part.ensure(P.nitems);
+            double A = 0, B = 0, C = 0;
+            tc_delta_poly(A, B, C);
+            const double S = tc_S(), ws = lv.w / S;
+            launch_item_delta(P.items.p, P.item_r2.p, P.nitems, 1.0 / (S * S), A, B, C,
+                              0.02 * ws * ws, item_tc_min_q, dlt.p, okf.p, s);
+            d_u64a.ensure(2);
+            size_t bytes = 0;
+            KJ_CUDA(cub::DevicePartition::Flagged(nullptr, bytes, P.items.p, okf.p, part.p, d_u64a.p,
+                                                  (int64_t)P.nitems, s));
+            KJ_CUDA(cub::DevicePartition::Flagged(sc.get(bytes), bytes, P.items.p, okf.p, part.p,
+                                                  d_u64a.p, (int64_t)P.nitems, s));
+            bytes = 0;
+            KJ_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, dlt.p, okf.p, tc_dlt.p, d_u64a.p + 1,
+                                               (int64_t)P.nitems, s));
+            KJ_CUDA(cub::DeviceSelect::Flagged(sc.get(bytes), bytes, dlt.p, okf.p, tc_dlt.p,
+                                               d_u64a.p + 1, (int64_t)P.nitems, s));
+            unsigned long long ntc = 0;
+            KJ_CUDA(cudaMemcpyAsync(&ntc, d_u64a.p, 8, cudaMemcpyDeviceToHost, s));
+            sync();
+            last_mixed_tc_items = ntc;
+            Timer t(s);
+            if (ntc) {
+                prep_tc(lv);
+                TcJoinArgs a{};
+                a.Bh = lv.Bh.p;
+                a.row_halfs = lv.row_halfs;
+                a.ksteps = tc_ksteps();
+                a.n = n;
+                a.qpos = P.qpos.p;
+                a.items = part.p;
+                a.adj = P.adj.p;
+                DBuf<float> cut_scaled;
+                if (d_init_cut) {
+                    const double S2 = S * S;
+                    cut_scaled.ensure(nv);
+                    launch_scale_f32(d_init_cut, nv, (float)(1.0 / S2), cut_scaled.p, s);
+                    a.init_cut = cut_scaled.p;
+                }
+                a.K = K;
+                a.L = L;
+                a.out_cnt = cnt.p;
+                a.out_pos = pos.p;
+                a.delta = f32_round_up(tc_delta());
+                a.item_delta = tc_dlt.p;
+                static const bool want_stats = getenv("KNNJ_JOIN_STATS") != nullptr;
+                DBuf<unsigned long long> st;
+                if (want_stats) {
+                    st.ensure(8);
+                    KJ_CUDA(cudaMemsetAsync(st.p, 0, 64, s));
+                    a.stats = st.p;
+                }
+                Timer tt(s);
+                launch_join_tc(a, tcc.sh, ntc, N, s);
+                mixed_tc_ran = true;
+                if (want_stats) {
+                    const double ms_tc = tt.ms();
+                    unsigned long long h[8];
+                    KJ_CUDA(cudaMemcpyAsync(h, st.p, 64, cudaMemcpyDeviceToHost, s));
+                    sync();
+                    fprintf(stderr, "mixed tc part: items %llu slabs %llu rare %llu bits %llu inserts %llu compactions %llu ms %.1f\n",
+                            ntc, h[0], h[1], h[2], h[3], h[4], ms_tc);
+                }
+            }
+            if (ntc < P.nitems) {
+                // SIMT items: those of at most 32 queries on 32-thread blocks, the rest on 128
+                const uint64_t nsimt = P.nitems - ntc;
+                DBuf<uint4> part2;
+                part2.ensure(nsimt);
+                size_t b2 = 0;
+                KJ_CUDA(cub::DevicePartition::If(nullptr, b2, part.p + ntc, part2.p, d_u64a.p, (int64_t)nsimt,
+                                                 SmallItem{}, s));
+                KJ_CUDA(cub::DevicePartition::If(sc.get(b2), b2, part.p + ntc, part2.p, d_u64a.p,
+                                                 (int64_t)nsimt, SmallItem{}, s));
+                unsigned long long nsmall = 0;
+                KJ_CUDA(cudaMemcpyAsync(&nsmall, d_u64a.p, 8, cudaMemcpyDeviceToHost, s));
+                sync();
+                JoinArgs a{};
+                if (!lv.xs_ready) {
+                    lv.Xs.ensure((uint64_t)n * Npad);
+                    launch_gather_soa(Xf.p, lv.J.p, N, n, Npad, lv.Xs.p, s);
+                    lv.xs_ready = true;
+                }
+                a.Xs = lv.Xs.p;
+                a.Npad = Npad;
+                a.n = n;
+                a.qpos = P.qpos.p;
+                a.adj = P.adj.p;
+                a.init_cut = d_init_cut;
+                a.K = K;
+                a.L = L;
+                a.out_cnt = cnt.p;
+                a.out_pos = pos.p;
+                screen_consts(a.gam, a.erg, a.eab, a.e64);
+                a.items = part2.p;
+                if (nsmall) launch_join(a, nsmall, 32u, s);
+                a.items = part2.p + nsmall;
+                if (nsimt > nsmall) launch_join(a, nsimt - nsmall, P.chunk, s);
+            }
+            last_join_kernel_ms = t.ms();
+            last_join_tc = mixed_tc_ran;
         } else {
             JoinArgs a{};
             if (!lv.xs_ready) {
@@ -1916,21 +2117,23 @@ struct knnj_ctx {
                 launch_join(ac, ci[c + 1] - ci[c], P.chunk, s);
                 if (overlap) {
                     KJ_CUDA(cudaEventRecord(ev_join[c], s));
-                    finalize_chunk(c);
+                    finalize_chunk(c, s_out);
                 }
             }
             last_join_kernel_ms = t.ms();
             last_join_tc = false;
         }
         if (getenv("KNNJ_JOIN_STATS"))
-            fprintf(stderr, "pass: tc %d chunk %u items %llu rows %llu cand %llu screened %llu w %.6g cover2 %.6g K %u L %u ms %.1f\n",
-                    (int)tc, P.chunk, (unsigned long long)P.nitems, (unsigned long long)nv,
+            fprintf(stderr, "pass: tc %d mixed %d (tc items %llu) chunk %u items %llu rows %llu cand %llu screened %llu w %.6g cover2 %.6g K %u L %u ms %.1f\n",
+                    (int)tc, (int)mixed, (unsigned long long)(mixed ? last_mixed_tc_items : 0), P.chunk, (unsigned long long)P.nitems, (unsigned long long)nv,
                     (unsigned long long)P.candidates, (unsigned long long)P.screened, lv.w, cov2, K, L,
                     last_join_kernel_ms);
         trace().mark("pass: join kernel", s);
         if (overlap) {  // the chunks' finalizes ran on s_out; s continues after the last one
             KJ_CUDA(cudaEventRecord(ev_fin, s_out));
             KJ_CUDA(cudaStreamWaitEvent(s, ev_fin, 0));
+        } else if (to_host) {
+            finalize_chunk(0, s);
         } else {
             launch_finalize(f, s);
         }
@@ -2329,6 +2532,26 @@ int knnj_set_option(knnj_ctx* c, const char* name, int64_t value) {
         } else if (k == "bound_sample") {
             if (value < 16 || value > (1 << 20)) throw Error(1, "bound_sample must be in [16, 2^20]");
             c->bound_sample = (uint32_t)value;
+        } else if (k == "item_tc") {
+            c->item_tc = value != 0;
+        } else if (k == "item_tc_min_q") {
+            if (value < 1 || value > 128) throw Error(1, "item_tc_min_q must be in [1, 128]");
+            c->item_tc_min_q = (uint32_t)value;
+        } else if (k == "out_priority") {
+            c->out_priority = value != 0;
+            if (c->s_out) {  // recreated with the new priority on next use
+                KJ_CUDA(cudaStreamSynchronize(c->s_out));
+                KJ_CUDA(cudaStreamDestroy(c->s_out));
+                KJ_CUDA(cudaEventDestroy(c->ev_out));
+                c->s_out = nullptr;
+                c->ev_out = nullptr;
+            }
+        } else if (k == "copy_blocks") {
+            if (value < 0 || value > (1 << 24)) throw Error(1, "copy_blocks must be in [0, 2^24]");
+            c->copy_blocks = (uint32_t)value;
+        } else if (k == "fin_blocks") {
+            if (value < 0 || value > (1 << 24)) throw Error(1, "fin_blocks must be in [0, 2^24]");
+            c->fin_blocks = (uint32_t)value;
         } else if (k == "join_chunks") {
             if (value < 1 || value > 64) throw Error(1, "join_chunks must be in [1, 64]");
             c->join_chunks = (uint32_t)value;

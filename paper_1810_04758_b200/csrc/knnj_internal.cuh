@@ -161,6 +161,10 @@ struct Pass {
     // [chunk_row[c], chunk_row[c+1]); items are LPT-ordered inside each chunk. Empty: one
     // launch over everything.
     std::vector<uint64_t> chunk_item, chunk_row;
+    // mixed pass (knnj_capi.cu pass_mixed): items on the tensor cores where their own data
+    // radius (item_r2, absolute units, from the box filter) allows, the rest SIMT
+    bool mixed = false, has_r2 = false;
+    DBuf<float> item_r2;
 };
 
 struct JoinArgs {
@@ -192,6 +196,7 @@ struct TcJoinArgs {
     uint32_t* out_cnt;       // per launch row
     uint32_t* out_pos;       // per launch row * L
     float delta;             // |key - sq64/S^2| bound (scaled units)
+    const float* item_delta; // optional per work item bound (radius of the item's own data)
     float* dbg;              // test hook: block 0 dumps its first accumulator tile [128][128]
     unsigned long long* stats;  // dev hook (KNNJ_JOIN_STATS): slabs, rare slabs, bits, inserts, compactions
     // histogram epilogue (HIST kernels only)
@@ -226,8 +231,6 @@ struct FinalArgs {
     const double* XJ;        // optional: X64 rows in A order (row p = point A[p]); locality
     double bound2;           // > 0: radius-bounded pass (every candidate with sq <= bound2 was
                              // screened); rows whose K-th is not within it get ST_MISS only
-    uint32_t* host_ids;      // optional: the same rows also written straight to mapped host
-    double* host_dist;       //   memory (pinned), one coalesced store per row
 };
 
 struct HistArgs {
@@ -297,7 +300,7 @@ void launch_scale_f32(const float* in, uint64_t n, float scale, float* out, cuda
 int pick_np(uint32_t n);  // padded dimension count used by the templated kernels
 size_t join_smem_bytes(int np, uint32_t L, uint32_t qb);
 void launch_join(const JoinArgs& a, uint64_t nitems, uint32_t qb, cudaStream_t s);
-void launch_finalize(const FinalArgs& a, cudaStream_t s);
+void launch_finalize(const FinalArgs& a, cudaStream_t s, uint32_t max_blocks = 0);
 size_t hist_smem_bytes(int np, uint32_t n_bins);
 void launch_histogram(const HistArgs& a, uint64_t n_slabs, cudaStream_t s);
 
@@ -364,7 +367,9 @@ void launch_filter_ranges(uint4* items, uint64_t nitems, const float* qbox, uint
                           const uint2* adj, const float* box, uint64_t nblk, float r2,
                           uint32_t* out_cnt, const uint32_t* out_off, uint2* out_adj,
                           unsigned long long* screened, bool fill, cudaStream_t s,
-                          float* out_key = nullptr, unsigned long long* count_total = nullptr);
+                          float* out_key = nullptr, unsigned long long* count_total = nullptr,
+                          const float* gbox = nullptr, float* item_r2 = nullptr,
+                          uint32_t r_m = 0, float r_2w = 0.f, const float* dbox = nullptr);
 void launch_fill_u32(uint32_t* p, uint64_t n, uint32_t v, cudaStream_t s);
 void launch_merge_parts(const uint4* splits, uint64_t nsplits, uint32_t K, const uint32_t* t_ids,
                         const double* t_sq, const uint32_t* t_count, const uint32_t* qrow,
@@ -376,6 +381,12 @@ void launch_split_flags(const uint32_t* pids, uint64_t nq, const uint32_t* slot,
                         cudaStream_t s);
 void launch_rows_by(const double* X64, const uint32_t* A, uint64_t N, uint32_t n, double* out,
                     cudaStream_t s);
+// per work item: tensor-core screen bound delta(R) = (A R^2 + B R + C)(1 + 1e-6), rounded up,
+// from the item's squared data radius r2 (absolute units; scaled by inv_s2 = 1/S^2), and an
+// eligibility flag: 2 delta <= lim (the precision rule) and at least min_q queries
+void launch_item_delta(const uint4* items, const float* r2, uint64_t nitems, double inv_s2,
+                       double A, double B, double C, double lim, uint32_t min_q, float* delta,
+                       uint8_t* tc_ok, cudaStream_t s);
 void launch_miss_flags(const uint32_t* rows, uint64_t n, const uint8_t* st, uint8_t* flags,
                        cudaStream_t s);
 void launch_uncert_flags(const uint32_t* rows, uint64_t n, const uint8_t* st, uint8_t* flags,
@@ -389,6 +400,9 @@ void launch_find_ovf(const uint32_t* cnt, uint64_t n, uint32_t* rows, unsigned l
                      cudaStream_t s);
 void launch_gather_rows(const uint32_t* rows, uint64_t n, uint32_t K, const uint32_t* ids,
                         const double* dist, uint32_t* oids, double* odist, cudaStream_t s);
+void launch_rows_to_host(const uint32_t* rows, uint64_t n, uint32_t K, const uint32_t* ids,
+                         const double* dist, uint32_t* hids, double* hdist, uint32_t max_blocks,
+                         cudaStream_t s);
 void launch_scatter_rows(const uint32_t* rows, uint64_t n, uint32_t K, const uint32_t* ids,
                          const double* dist, uint32_t* oids, double* odist, cudaStream_t s);
 

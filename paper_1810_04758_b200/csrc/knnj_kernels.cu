@@ -305,15 +305,10 @@ __device__ __forceinline__ void rank_entries(const double (&sq)[EMAX], const uin
 }
 
 // ---------------------------------------------------------------- finalize
-// per-warp staging of one output row (K ids, pad, K doubles), 16-byte multiples
-__host__ __device__ __forceinline__ uint32_t fin_stage_words(uint32_t K) { return 4 * ((3 * K + 7) / 4); }
 
 // One warp per launch row: exact FP64 distances for the screened list, exact
 // (sq,id) ranks, first K written to the query's output row, status bits.
-__global__ void k_finalize(FinalArgs a) {
-    const uint64_t row = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (row >= a.nrows) return;
+__device__ __forceinline__ void finalize_row(const FinalArgs& a, uint64_t row, int lane) {
     const uint32_t c = a.cnt[row];
     if (c == SKIP) return;  // a split row: its parts are finalized and merged separately
     const uint32_t orow = a.qrow[row];
@@ -353,11 +348,6 @@ __global__ void k_finalize(FinalArgs a) {
         default: break;
     }
     double kth = CUDART_INF;
-    // mapped host rows: staged per warp, then one coalesced store per row (full PCIe lines)
-    extern __shared__ __align__(16) unsigned char fin_smem[];
-    const int wib = threadIdx.x >> 5;
-    uint32_t* s_ids = reinterpret_cast<uint32_t*>(fin_smem) + (size_t)wib * fin_stage_words(a.K);
-    double* s_dist = reinterpret_cast<double*>(s_ids + a.K + (a.K & 1));
 #pragma unroll
     for (int f = 0; f < EMAX; ++f) {
         const uint32_t i = f * 32 + lane;
@@ -366,18 +356,8 @@ __global__ void k_finalize(FinalArgs a) {
             a.out_ids[(uint64_t)orow * a.K + rk[f]] = id[f];
             a.out_dist[(uint64_t)orow * a.K + rk[f]] = d;
             if (a.out_sq) a.out_sq[(uint64_t)orow * a.K + rk[f]] = sq[f];
-            if (a.host_ids) {
-                s_ids[rk[f]] = id[f];
-                s_dist[rk[f]] = d;
-            }
             if (rk[f] == a.K - 1) kth = sq[f];
         }
-    }
-    if (a.host_ids) {
-        __syncwarp();
-        const uint32_t w = min(c, a.K);
-        for (uint32_t i = lane; i < w; i += 32) a.host_ids[(uint64_t)orow * a.K + i] = s_ids[i];
-        for (uint32_t i = lane; i < w; i += 32) a.host_dist[(uint64_t)orow * a.K + i] = s_dist[i];
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) kth = fmin(kth, __shfl_xor_sync(0xffffffffu, kth, o));
@@ -395,6 +375,14 @@ __global__ void k_finalize(FinalArgs a) {
         a.out_kth[orow] = c >= a.K ? kth : CUDART_INF;
         if (a.out_count) a.out_count[orow] = min(c, a.K);
     }
+}
+
+// Warps stride over the launch rows (a bounded grid shares the SMs with a running join).
+__global__ void k_finalize(FinalArgs a) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+    for (uint64_t w = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w < a.nrows; w += nw)
+        finalize_row(a, w, lane);
 }
 
 // ---------------------------------------------------------------- histogram
@@ -600,15 +588,11 @@ void launch_join(const JoinArgs& a, uint64_t nitems, uint32_t qb, cudaStream_t s
     }
 }
 
-void launch_finalize(const FinalArgs& a, cudaStream_t s) {
+void launch_finalize(const FinalArgs& a, cudaStream_t s, uint32_t max_blocks) {
     if (a.nrows == 0) return;
-    uint64_t threads = a.nrows * 32;
-    if (a.host_ids) {  // 2 warps per block, K x 12 B staging each (fits next to a join CTA)
-        const size_t sm = 2 * 4 * (size_t)fin_stage_words(a.K);
-        k_finalize<<<(unsigned)((threads + 63) / 64), 64, sm, s>>>(a);
-    } else {
-        k_finalize<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(a);
-    }
+    uint64_t blocks = (a.nrows * 32 + 255) / 256;
+    if (max_blocks) blocks = std::min<uint64_t>(blocks, max_blocks);
+    k_finalize<<<(unsigned)blocks, 256, 0, s>>>(a);
     KJ_CUDA(cudaGetLastError());
     g_launches.fetch_add(1, std::memory_order_relaxed);
 }
@@ -1526,6 +1510,28 @@ void launch_rows_by(const double* X64, const uint32_t* A, uint64_t N, uint32_t n
 }
 
 // rows whose list is not yet globally exact (fine cascade: they go on to level 0)
+__global__ void k_item_delta(const uint4* items, const float* r2, uint64_t nitems, double inv_s2,
+                             double A, double B, double C, double lim, uint32_t min_q, float* delta,
+                             uint8_t* tc_ok) {
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < nitems;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const double R2 = (double)r2[i] * inv_s2 * (1.0 + 1e-12);
+        const double d = (A * R2 + B * sqrt(R2) * (1.0 + 1e-15) + C) * (1.0 + 1e-6);
+        const float df = __double2float_ru(d);
+        delta[i] = df;
+        const uint4 it = items[i];
+        tc_ok[i] = (2.0 * (double)df <= lim && it.y - it.x >= min_q) ? 1 : 0;
+    }
+}
+void launch_item_delta(const uint4* items, const float* r2, uint64_t nitems, double inv_s2,
+                       double A, double B, double C, double lim, uint32_t min_q, float* delta,
+                       uint8_t* tc_ok, cudaStream_t s) {
+    if (!nitems) return;
+    k_item_delta<<<(unsigned)std::min<uint64_t>((nitems + 255) / 256, 148 * 16), 256, 0, s>>>(
+        items, r2, nitems, inv_s2, A, B, C, lim, min_q, delta, tc_ok);
+    KJ_CUDA(cudaGetLastError());
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+}
 __global__ void k_miss_flags(const uint32_t* rows, uint64_t n, const uint8_t* st, uint8_t* flags) {
     for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
          i += uint64_t(gridDim.x) * blockDim.x)
@@ -1597,6 +1603,30 @@ void launch_gather_rows(const uint32_t* rows, uint64_t n, uint32_t K, const uint
                         const double* dist, uint32_t* oids, double* odist, cudaStream_t s) {
     if (!n || !K) return;
     k_gather_rows<<<2368, 256, 0, s>>>(rows, n, K, ids, dist, oids, odist);
+    KJ_CUDA(cudaGetLastError());
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+// One warp per output row, rows taken in the given (ascending) order: the row's K ids and
+// K distances from device memory to the same row of mapped host memory, one coalesced
+// store per 128 bytes. Ascending rows keep the host stores sweeping the address space in
+// order (~49 GB/s over PCIe; random rows ~15 GB/s, tools/micro/pcie_write.cu).
+__global__ void k_rows_to_host(const uint32_t* rows, uint64_t n, uint32_t K, const uint32_t* ids,
+                               const double* dist, uint32_t* hids, double* hdist) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+    for (uint64_t w = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w < n; w += nw) {
+        const uint64_t base = (uint64_t)rows[w] * K;
+        for (uint32_t i = lane; i < K; i += 32) hids[base + i] = ids[base + i];
+        for (uint32_t i = lane; i < K; i += 32) hdist[base + i] = dist[base + i];
+    }
+}
+void launch_rows_to_host(const uint32_t* rows, uint64_t n, uint32_t K, const uint32_t* ids,
+                         const double* dist, uint32_t* hids, double* hdist, uint32_t max_blocks,
+                         cudaStream_t s) {
+    if (!n || !K) return;
+    uint64_t blocks = (n * 32 + 255) / 256;
+    if (max_blocks) blocks = std::min<uint64_t>(blocks, max_blocks);
+    k_rows_to_host<<<(unsigned)blocks, 256, 0, s>>>(rows, n, K, ids, dist, hids, hdist);
     KJ_CUDA(cudaGetLastError());
     g_launches.fetch_add(1, std::memory_order_relaxed);
 }
@@ -1814,11 +1844,25 @@ __global__ void k_item_boxes(const uint4* items, uint64_t nitems, const uint32_t
 // out_off[item], (abeg, aend) of the item rewritten, kept pairs summed into screened.
 // ORDER: one range per kept block plus a sweep-order key (squared distance between the
 // item box centre and the block box centre), for a per-item sort nearest-first.
+// FILL with item_r2: also the squared radius (rounded up) of the item's data about the
+// global centre, max over its query box and its kept blocks' boxes, from g rounded
+// outward (g_lo, g_hi): the per-item tensor-core screen bound.
+__device__ __forceinline__ float box_radius2(const float* lo, const float* hi, size_t stride,
+                                             const float* g_lo, const float* g_hi, uint32_t n,
+                                             uint32_t d0 = 0) {
+    float acc = 0.f;
+    for (uint32_t d = d0; d < n; ++d) {
+        const float r = fmaxf(fmaxf(__fsub_ru(g_hi[d], lo[d * stride]), __fsub_ru(hi[d * stride], g_lo[d])), 0.f);
+        acc = __fadd_ru(acc, __fmul_ru(r, r));
+    }
+    return acc;
+}
 template <bool FILL, bool ORDER>
 __global__ void k_filter_ranges(uint4* items, uint64_t nitems, const float* qbox, uint32_t n,
                                 const uint2* adj, const float* box, uint64_t nblk, float r2,
                                 uint32_t* out_cnt, const uint32_t* out_off, uint2* out_adj,
-                                unsigned long long* screened, float* out_key) {
+                                unsigned long long* screened, float* out_key, const float* gbox,
+                                float* item_r2, uint32_t r_m, float r_2w, const float* dbox) {
     const int lane = threadIdx.x & 31;
     const uint64_t item = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     if (item >= nitems) return;
@@ -1827,6 +1871,8 @@ __global__ void k_filter_ranges(uint4* items, uint64_t nitems, const float* qbox
     const float* qh = ql + n;
     uint32_t kept = 0;
     unsigned long long span = 0;
+    float rmax = 0.f;  // item_r2: max over kept blocks
+    const bool want_r = FILL && item_r2 != nullptr;
     const uint32_t base = FILL ? out_off[item] : 0;
     for (uint32_t ri = it.z; ri < it.w; ++ri) {
         const uint2 rg = adj[ri];
@@ -1851,6 +1897,9 @@ __global__ void k_filter_ranges(uint4* items, uint64_t nitems, const float* qbox
                     }
                 }
                 keep = acc <= r2;
+                if (want_r && keep && r_m < n)
+                    rmax = fmaxf(rmax, box_radius2(box + blk, box + (uint64_t)n * nblk + blk, nblk,
+                                                   gbox, gbox + n, n, r_m));
             }
             const unsigned m = __ballot_sync(0xffffffffu, keep);
             if (ORDER) {
@@ -1880,6 +1929,23 @@ __global__ void k_filter_ranges(uint4* items, uint64_t nitems, const float* qbox
         for (int o = 16; o > 0; o >>= 1) span += __shfl_xor_sync(0xffffffffu, span, o);
         if (lane == 0 && span) atomicAdd(screened, span * (unsigned long long)(it.y - it.x));
     }
+    if (want_r) {
+        // grid dims d < r_m: every candidate lies in the 3^m cells around the item's cell,
+        // i.e. within [qh - 2w, ql + 2w] (the cell holds the query box); the other dims:
+        // the kept blocks' boxes (and the query box)
+        for (int o = 16; o > 0; o >>= 1) rmax = fmaxf(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
+        if (lane == 0) {
+            float low = 0.f;
+            for (uint32_t d = 0; d < r_m; ++d) {  // ... and inside the data range (dbox)
+                const float lo = fmaxf(__fsub_rd(qh[d], r_2w), dbox[d]);
+                const float hi = fminf(__fadd_ru(ql[d], r_2w), dbox[r_m + d]);
+                const float r = fmaxf(fmaxf(__fsub_ru(gbox[n + d], lo), __fsub_ru(hi, gbox[d])), 0.f);
+                low = __fadd_ru(low, __fmul_ru(r, r));
+            }
+            const float high = r_m < n ? fmaxf(rmax, box_radius2(ql, qh, 1, gbox, gbox + n, n, r_m)) : 0.f;
+            item_r2[item] = __fadd_ru(low, high);
+        }
+    }
     if (lane == 0) {
         if (FILL) items[item] = make_uint4(it.x, it.y, base, base + kept);
         else out_cnt[item] = kept;
@@ -1898,13 +1964,15 @@ void launch_filter_ranges(uint4* items, uint64_t nitems, const float* qbox, uint
                           const uint2* adj, const float* box, uint64_t nblk, float r2,
                           uint32_t* out_cnt, const uint32_t* out_off, uint2* out_adj,
                           unsigned long long* screened, bool fill, cudaStream_t s,
-                          float* out_key, unsigned long long* count_total) {
+                          float* out_key, unsigned long long* count_total, const float* gbox,
+                          float* item_r2, uint32_t r_m, float r_2w, const float* dbox) {
     if (!nitems) return;
     const unsigned grid = (unsigned)((nitems * 32 + 255) / 256);
     if (!fill) screened = count_total;  // the count pass sums kept ranges there (if given)
 #define KJ_FR(F, O)                                                                       \
     k_filter_ranges<F, O><<<grid, 256, 0, s>>>(items, nitems, qbox, n, adj, box, nblk, r2, \
-                                               out_cnt, out_off, out_adj, screened, out_key)
+                                               out_cnt, out_off, out_adj, screened, out_key, gbox, \
+                                               item_r2, r_m, r_2w, dbox)
     if (out_key) {
         if (fill) KJ_FR(true, true);
         else KJ_FR(false, true);

@@ -133,24 +133,26 @@ __device__ __forceinline__ float tmem_ld1(uint32_t taddr) {
     return __uint_as_float(r);
 }
 
-// up to 8 single columns (any addresses) in flight, one wait
-__device__ __forceinline__ void tmem_ld8(const uint32_t (&ta)[8], float (&x)[8]) {
-    uint32_t r[8];
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%8];\n\t"
-        "tcgen05.ld.sync.aligned.32x32b.x1.b32 {%1}, [%9];\n\t"
-        "tcgen05.ld.sync.aligned.32x32b.x1.b32 {%2}, [%10];\n\t"
-        "tcgen05.ld.sync.aligned.32x32b.x1.b32 {%3}, [%11];\n\t"
-        "tcgen05.ld.sync.aligned.32x32b.x1.b32 {%4}, [%12];\n\t"
-        "tcgen05.ld.sync.aligned.32x32b.x1.b32 {%5}, [%13];\n\t"
-        "tcgen05.ld.sync.aligned.32x32b.x1.b32 {%6}, [%14];\n\t"
-        "tcgen05.ld.sync.aligned.32x32b.x1.b32 {%7}, [%15];\n\t"
-        "tcgen05.wait::ld.sync.aligned;"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
-        : "r"(ta[0]), "r"(ta[1]), "r"(ta[2]), "r"(ta[3]), "r"(ta[4]), "r"(ta[5]), "r"(ta[6]), "r"(ta[7])
-        : "memory");
+// 3-input FP32 min (FMNMX3 on sm_100; a NaN input is ignored like fminf)
+__device__ __forceinline__ float fmin3(float a, float b, float c) {
+    float d;
+    asm("min.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+    return d;
+}
+// minimum of a 64-column slab (NaN columns ignored): a 3-ary tree, 32 FMNMX3/FMNMX
+__device__ __forceinline__ float slab_min64(const float (&v0)[32], const float (&v1)[32]) {
+    float t[22];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) x[i] = __uint_as_float(r[i]);
+    for (int i = 0; i < 21; ++i) {
+        const int a = 3 * i, b = 3 * i + 1, c = 3 * i + 2;
+        t[i] = fmin3(a < 32 ? v0[a] : v1[a - 32], b < 32 ? v0[b] : v1[b - 32], c < 32 ? v0[c] : v1[c - 32]);
+    }
+    t[21] = v1[31];
+    float u[8];
+#pragma unroll
+    for (int i = 0; i < 7; ++i) u[i] = fmin3(t[3 * i], t[3 * i + 1], t[3 * i + 2]);
+    u[7] = t[21];
+    return fmin3(fmin3(u[0], u[1], u[2]), fmin3(u[3], u[4], u[5]), fminf(u[6], u[7]));
 }
 
 // K-th smallest (1-based k) of the 32*R values a[r] (element index r*32 + lane)
@@ -485,7 +487,7 @@ __global__ void __launch_bounds__(64 + 128 * G, 1)
         uint32_t cnt = 0;
         bool ovf = false;
         const float init_cut = (p.init_cut && has_q) ? p.init_cut[row] : CUDART_INF_F;
-        const float dl = p.delta;
+        const float dl = p.item_delta ? p.item_delta[blockIdx.x] : p.delta;
         const float cap = __fadd_ru(init_cut, dl);        // U + delta
         float cut = cap;
         float rhs = has_q ? __fsub_ru(cut, na) : -CUDART_INF_F;
@@ -559,20 +561,7 @@ __global__ void __launch_bounds__(64 + 128 * G, 1)
                         if ((uint32_t)(j + 32) >= lim) v1[j] = CUDART_NAN_F;
                     }
                 }
-                float m0[16], m1[16];
-#pragma unroll
-                for (int j = 0; j < 16; ++j) {
-                    m0[j] = fminf(v0[j], v0[j + 16]);
-                    m1[j] = fminf(v1[j], v1[j + 16]);
-                }
-#pragma unroll
-                for (int w = 8; w > 0; w >>= 1)
-#pragma unroll
-                    for (int j = 0; j < w; ++j) {
-                        m0[j] = fminf(m0[j], m0[j + w]);
-                        m1[j] = fminf(m1[j], m1[j + w]);
-                    }
-                const bool hit = has_q && !ovf && fminf(m0[0], m1[0]) <= rhs;
+                const bool hit = has_q && !ovf && slab_min64(v0, v1) <= rhs;
                 ++st_slab;
                 if (!__any_sync(0xffffffffu, hit)) continue;
                 ++st_rare;
@@ -585,29 +574,16 @@ __global__ void __launch_bounds__(64 + 128 * G, 1)
                         mk[1] |= (v1[j] <= rhs ? 1u : 0u) << j;
                     }
                 }
-                // the columns any lane hit, 8 TMEM column loads in flight per batch
-                unsigned long long um = (unsigned long long)__reduce_or_sync(0xffffffffu, mk[0]) |
-                                        ((unsigned long long)__reduce_or_sync(0xffffffffu, mk[1]) << 32);
-                const unsigned long long mine = (unsigned long long)mk[0] | ((unsigned long long)mk[1] << 32);
-                while (um) {
-                    int jj[8];
-                    uint32_t ta[8];
 #pragma unroll
-                    for (int b = 0; b < 8; ++b) {
-                        jj[b] = um ? __ffsll((long long)um) - 1 : -1;
+                for (int h = 0; h < 2; ++h) {
+                    unsigned um = __reduce_or_sync(0xffffffffu, mk[h]);
+                    while (um) {
+                        const int j = __ffs(um) - 1;
                         um &= um - 1;
-                        ta[b] = tbase + j0 + (uint32_t)(jj[b] < 0 ? 0 : jj[b]);
-                    }
-                    float xs[8];
-                    tmem_ld8(ta, xs);
-#pragma unroll
-                    for (int b = 0; b < 8; ++b) {
-                        const int j = jj[b];
-                        if (j < 0) break;
                         ++st_bits;
-                        const float x = xs[b];
-                        const uint32_t pos = s + j0 + j;
-                        bool want = ((mine >> j) & 1ull) && x <= rhs && pos != qp;
+                        const float x = tmem_ld1(tbase + j0 + h * 32 + j);
+                        const uint32_t pos = s + j0 + h * 32 + j;
+                        bool want = ((mk[h] >> j) & 1u) && x <= rhs && pos != qp;
                         // make room: cooperative compaction of every full buffer that needs it
                         unsigned full = __ballot_sync(0xffffffffu, want && cnt == LB);
                         while (full) {
@@ -701,20 +677,7 @@ __global__ void __launch_bounds__(64 + 128 * G, 1)
                             if ((uint32_t)(j + 32) >= lim) v[1][j] = CUDART_NAN_F;
                         }
                     }
-                    float m0[16], m1[16];
-#pragma unroll
-                    for (int j = 0; j < 16; ++j) {
-                        m0[j] = fminf(v[0][j], v[0][j + 16]);
-                        m1[j] = fminf(v[1][j], v[1][j + 16]);
-                    }
-#pragma unroll
-                    for (int w = 8; w > 0; w >>= 1)
-#pragma unroll
-                        for (int j = 0; j < w; ++j) {
-                            m0[j] = fminf(m0[j], m0[j + w]);
-                            m1[j] = fminf(m1[j], m1[j + w]);
-                        }
-                    const bool hit = fminf(m0[0], m1[0]) < skip_at;
+                    const bool hit = slab_min64(v[0], v[1]) < skip_at;
                     if (!__any_sync(0xffffffffu, hit)) continue;
                     unsigned mk[2] = {0u, 0u};
                     if (hit) {

@@ -1,0 +1,53 @@
+"""Mixed level passes (knnj_capi.cu pass_mixed / run_pass): when the tensor-core screen's
+global precision rule fails (data far from the centre somewhere, e.g. skewed Exp(1)
+coordinates), work items whose own data lie close to the centre run on the tcgen05 screen
+with a per-item error bound (tc_delta_poly at the item's radius, measured by the box
+filter), the rest on the SIMT screen. Neither screen may change an output bit: compared
+with an all-SIMT run and with the oracle."""
+import numpy as np
+import pytest
+
+from paper_1810_04758_b200 import RunConfig
+from paper_1810_04758_b200.synthetic import generate
+
+pytestmark = pytest.mark.gpu
+
+
+def _far_cluster(N, n, seed):
+    """A dense blob at the origin plus a sparse far shell: the global radius is large, the
+    blob's items are small."""
+    rng = np.random.default_rng(seed)
+    X = rng.standard_normal((N, n)) * 0.05
+    far = rng.standard_normal((N // 50, n))
+    far *= 40.0 / np.linalg.norm(far, axis=1)[:, None]
+    X[: far.shape[0]] = far
+    return X
+
+
+# mixed passes need 128-query items (G = 1): K > 40 for n <= 20, or n >= 21
+@pytest.mark.parametrize("spec,N,n,k,minq", [("exponential", 60000, 6, 64, 8), ("exponential", 50000, 5, 48, 16),
+                                             ("far", 40000, 4, 44, 1), ("far", 40000, 6, 64, 8),
+                                             ("exponential", 40000, 24, 16, 32), ("far", 30000, 22, 12, 1),
+                                             ("exponential", 80000, 6, 64, 64)])
+def test_mixed_pass_identical(engine, oracle, spec, N, n, k, minq):
+    X = _far_cluster(N, n, 5) if spec == "far" else generate(spec, N, n, 71)
+    cfg = RunConfig(k=k, mode="hybrid", seed=71)
+    engine.set_option("item_tc", 0)
+    engine.set_points(X)
+    a = engine.run(cfg, want_hist=False)
+    engine.set_option("item_tc", 1)
+    engine.set_option("item_tc_min_q", minq)
+    try:
+        engine.set_points(X)
+        b = engine.run(cfg, want_hist=False)
+    finally:
+        engine.set_option("item_tc_min_q", 32)
+    assert np.array_equal(b.ids, a.ids) and np.array_equal(b.dist, a.dist)
+    assert np.array_equal(b.provenance, a.provenance)
+    assert b.info["failed_count"] == a.info["failed_count"]
+    if minq == 1:
+        assert b.info["join_tensor_cores"] == 1, "no item ran on the tensor cores"
+    W = X[:, a.info["perm"]]
+    q = np.random.default_rng(3).choice(N, 40, replace=False).astype(np.uint32)
+    oi, od = oracle.brute_knn(W, q, k)
+    assert np.array_equal(b.ids[q], oi) and np.array_equal(b.dist[q], od)

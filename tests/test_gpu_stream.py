@@ -95,7 +95,7 @@ def test_radius_bounded_pass_identical(engine, oracle, spec, N, n, k, q):
     finally:
         engine.set_option("bound_min_rows", 200000)
         engine.set_option("bound_sample", 4096)
-        engine.set_option("kth_bound_q", 990)
+        engine.set_option("kth_bound_q", 999)
     assert np.array_equal(b.ids, a.ids) and np.array_equal(b.dist, a.dist)
     assert np.array_equal(b.provenance, a.provenance)
     assert b.info["failed_count"] == a.info["failed_count"]
