@@ -885,10 +885,11 @@ struct knnj_ctx {
     // >= target there, so lower_bound selects the same bin as with the full histogram.
     // If the capped counts fall short, the rest is re-binned in full.
     int hist_cap_mode = 1;  // 0: never cap, 1: cap when the histogram is large, 2: always
-    // The pilot first bins only the lowest tenth of the bins, then a quarter, then all
-    // (0: always in full; 1: all rounds; 2: the quarter round only for n <= 8). In 18-D
-    // the pair count below the radius grows ~8x per bin, so a quarter of the bins is
-    // already slower than binning in full; a tenth is not (C2's cap sits at bin 9).
+    // The pilot bins only the lowest 4% of the bins, then a tenth, then a quarter, then
+    // all, stopping at the first round whose counted bins reach 2x the target
+    // (0: always in full; 1: every round; 2: the 4% and quarter rounds only for n <= 8).
+    // In 18-D the pair count below the radius grows ~8x per bin, so a quarter of the bins
+    // is already slower than binning in full; a tenth is not (C2's cap sits at bin 9).
     int pilot_cap = 2;
     double last_hist_ms_pilot = 0.0;
     uint32_t hist_for_selection(const std::vector<uint64_t>& hq, uint32_t shard, uint32_t nshard,
@@ -1152,6 +1153,8 @@ struct knnj_ctx {
     // (K = 3n+2, ~22-bit products) padded to 64-half k-blocks (KB <= 5: n <= 106); wider
     // points use the SIMT kernels.
     bool tc_enabled = true;
+    bool tc_small_cta = false;
+    bool item_radius = true;  // fallback levels filter each item at its rows' K-th bound
     bool split_items = true;  // split oversized work items into candidate-range parts
     uint32_t tc_slack = 24;       // tcgen05 join list capacity K + slack (compaction when full)
     bool finalize_xj = true;      // finalize reads FP64 rows from a join-ordered copy
@@ -1341,7 +1344,9 @@ struct knnj_ctx {
             c.sh = TcShape{(int)KB, 1, KB == 5 ? 2 : 3, 64};
             c.L = std::min<uint32_t>(L0, 64);
         } else if (L0 <= 64) {
-            c.sh = KB == 1 ? TcShape{1, 2, 4} : TcShape{2, 1, 3};
+            // tc_small_cta: 128-query CTAs with a 2-stage ring (~106 KB): two per SM, twice
+            // the epilogue warps per SM sub-partition
+            c.sh = KB == 1 ? (tc_small_cta ? TcShape{1, 1, 2} : TcShape{1, 2, 4}) : TcShape{2, 1, 3};
             c.L = L0;
         } else {
             c.sh = KB == 1 ? TcShape{1, 1, 4} : TcShape{2, 1, 2};
@@ -1396,7 +1401,7 @@ struct knnj_ctx {
     void build_pass(Level& lv, const uint32_t* d_qpid, const uint32_t* d_qrow, uint64_t nq,
                     Pass& P, uint32_t K = 0, uint32_t shard = 0, uint32_t nshard = 1,
                     const uint8_t* d_dense = nullptr, double filter_r2 = 0.0, bool allow_split = true,
-                    bool all_points = false) {
+                    bool all_points = false, const float* d_cut_by_row = nullptr) {
         P.nq = nq;
         P.nq_all = nq;
         P.nv = nq;
@@ -1623,7 +1628,10 @@ struct knnj_ctx {
         const uint32_t nch = (stream_chunks > 1 && P.nv == nq_own && !P.mixed &&
                               nq_own >= (uint64_t)chunk_min_rows * stream_chunks)
                                  ? stream_chunks : 1;
-        auto chunk_of = [&](const uint4& it) { return (uint32_t)((uint64_t)it.x * nch / nq_own); };
+        // (split-part items run on virtual rows >= nq_own; chunking is off when they exist)
+        auto chunk_of = [&](const uint4& it) {
+            return nch == 1 ? 0u : (uint32_t)std::min<uint64_t>(nch - 1, (uint64_t)it.x * nch / nq_own);
+        };
         // (a stable counting sort on (chunk, weight class): 16 classes per doubling of the
         // item's pair count, heaviest first; O(items) where a comparison sort of C5's 470k
         // items cost tens of ms on the host)
@@ -1695,8 +1703,19 @@ struct knnj_ctx {
         sync();
         P.candidates = cand;
         P.screened = cand;
-        if (filter_r2 > 0.0 && box_filter && P.nitems)
-            filter_ranges(lv, P, filter_r2, K > 0 && (pass_uses_tc(lv, K) || P.mixed));
+        if (filter_r2 > 0.0 && box_filter && P.nitems) {
+            // rows that carry an upper bound U on their K-th sq (fallback levels: K points
+            // within sqrt(U) are known to exist) need no candidate beyond sqrt(U): an item
+            // filters at the largest bound among its rows
+            DBuf<float> irad;
+            if (d_cut_by_row) {
+                irad.ensure(P.nitems);
+                launch_item_max_cut(P.items.p, P.nitems, P.qrow.p, P.nq,
+                                    P.nv > P.nq ? P.vsrc.p : nullptr, d_cut_by_row, irad.p, s);
+            }
+            filter_ranges(lv, P, filter_r2, K > 0 && (pass_uses_tc(lv, K) || P.mixed),
+                          d_cut_by_row ? irad.p : nullptr);
+        }
     }
 
     // launches a big level-0 pass is cut into (build_pass; 1 = one launch)
@@ -1721,7 +1740,7 @@ struct knnj_ctx {
     double filter_radius2(const Level& lv) const { return cover2(lv) < kInf ? lv.w * lv.w : 0.0; }
     // order: the nearest-first sweep, for tcgen05 passes only (their epilogue's rare path
     // is what it cuts; a SIMT pass over tiny cells (C4) would sort billions of blocks)
-    void filter_ranges(Level& lv, Pass& P, double r2, bool tc_pass) {
+    void filter_ranges(Level& lv, Pass& P, double r2, bool tc_pass, const float* item_rad2 = nullptr) {
         if (!lv.bbox_ready) {
             lv.bbox.ensure(((N + FB - 1) / FB) * 2 * n);
             launch_block_boxes(X64.p, lv.J.p, N, n, lv.bbox.p, s);
@@ -1745,7 +1764,7 @@ struct knnj_ctx {
         }
         P.screened = filter_items(P.items.p, P.nitems, P.qpos.p, lv.J.p, lv.bbox.p, P.adj, P.nadj, r2,
                                   sweep_order && tc_pass, r2_out, lv.m,
-                                  f32_round_up(2.0 * lv.w * (1.0 + 1e-6)), dbox.p);
+                                  f32_round_up(2.0 * lv.w * (1.0 + 1e-6)), dbox.p, item_rad2);
         P.has_r2 = r2_out != nullptr;
     }
     // kept FB-blocks per item under the box filter (the filter's count pass only; items and
@@ -1777,7 +1796,7 @@ struct knnj_ctx {
     uint64_t filter_items(uint4* items, uint64_t nitems, const uint32_t* qpos, const uint32_t* J,
                           const float* bbox, DBuf<uint2>& adj, uint64_t& nadj, double r2,
                           bool order = false, float* item_r2 = nullptr, uint32_t r_m = 0,
-                          float r_2w = 0.f, const float* dbox = nullptr) {
+                          float r_2w = 0.f, const float* dbox = nullptr, const float* item_rad2 = nullptr) {
         const uint64_t nblk = (N + FB - 1) / FB;
         // FP64 scalar sums can fall below the true sq: widen, then round up to FP32
         const float r2c = f32_round_up(r2 * (1.0 + 1e-9));
@@ -1797,7 +1816,8 @@ struct knnj_ctx {
         d_u64a.ensure(1);
         KJ_CUDA(cudaMemsetAsync(d_u64a.p, 0, 8, s));
         launch_filter_ranges(items, nitems, qbox.p, n, adj.p, bbox, nblk, r2c, cnt.p, nullptr,
-                             nullptr, nullptr, false, s, kp, d_u64a.p);
+                             nullptr, nullptr, false, s, kp, d_u64a.p, nullptr, nullptr, 0, 0.f,
+                             nullptr, item_rad2);
         if (order) {  // one range per kept block: the total must fit the 32-bit range ids
             unsigned long long nr = 0;
             KJ_CUDA(cudaMemcpyAsync(&nr, d_u64a.p, 8, cudaMemcpyDeviceToHost, s));
@@ -1806,7 +1826,8 @@ struct knnj_ctx {
                 order = false;
                 kp = nullptr;
                 launch_filter_ranges(items, nitems, qbox.p, n, adj.p, bbox, nblk, r2c, cnt.p,
-                                     nullptr, nullptr, nullptr, false, s);
+                                     nullptr, nullptr, nullptr, false, s, nullptr, nullptr, nullptr,
+                                     nullptr, 0, 0.f, nullptr, item_rad2);
             }
         }
         exclusive_sum(sc, cnt.p, off.p, nitems + 1, s);
@@ -1822,7 +1843,8 @@ struct knnj_ctx {
         d_u64a.ensure(1);
         KJ_CUDA(cudaMemsetAsync(d_u64a.p, 0, 8, s));
         launch_filter_ranges(items, nitems, qbox.p, n, adj.p, bbox, nblk, r2c, nullptr, off.p,
-                             adj2.p, d_u64a.p, true, s, kp, nullptr, d_gbox.p, item_r2, r_m, r_2w, dbox);
+                             adj2.p, d_u64a.p, true, s, kp, nullptr, d_gbox.p, item_r2, r_m, r_2w, dbox,
+                             item_rad2);
         if (order && total) {
             // nearest blocks first inside every item: the top-K cut converges early
             DBuf<uint2> adj3;
@@ -2384,7 +2406,8 @@ struct knnj_ctx {
             KJ_CUDA(cudaMemcpyAsync(d_cut.p, scut.data(), 4 * np, cudaMemcpyHostToDevice, s));
             launch_scatter_f32(d_r.p, d_cut.p, np, d_cut_by_row.p, s);
             Pass P;
-            build_pass(lv, d_p.p, d_r.p, np, P, K, 0, 1, nullptr, filter_radius2(lv));
+            build_pass(lv, d_p.p, d_r.p, np, P, K, 0, 1, nullptr, filter_radius2(lv), true, false,
+                       item_radius ? d_cut_by_row.p : nullptr);
             trace().mark("levels: build_pass", s);
             launch_gather_f32(P.qrow.p, d_cut_by_row.p, np, d_cut.p, s);
             run_pass(lv, P, K, d_cut.p, -1.0, cov2, out_ids, out_dist, out_kth, out_status, n_slow);
@@ -2583,6 +2606,10 @@ int knnj_set_option(knnj_ctx* c, const char* name, int64_t value) {
         } else if (k == "bound_sample") {
             if (value < 16 || value > (1 << 20)) throw Error(1, "bound_sample must be in [16, 2^20]");
             c->bound_sample = (uint32_t)value;
+        } else if (k == "item_radius") {
+            c->item_radius = value != 0;
+        } else if (k == "tc_small_cta") {
+            c->tc_small_cta = value != 0;
         } else if (k == "item_tc") {
             c->item_tc = value != 0;
         } else if (k == "item_tc_min_q") {

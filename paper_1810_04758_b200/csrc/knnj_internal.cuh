@@ -369,7 +369,8 @@ void launch_filter_ranges(uint4* items, uint64_t nitems, const float* qbox, uint
                           unsigned long long* screened, bool fill, cudaStream_t s,
                           float* out_key = nullptr, unsigned long long* count_total = nullptr,
                           const float* gbox = nullptr, float* item_r2 = nullptr,
-                          uint32_t r_m = 0, float r_2w = 0.f, const float* dbox = nullptr);
+                          uint32_t r_m = 0, float r_2w = 0.f, const float* dbox = nullptr,
+                          const float* item_rad2 = nullptr);
 void launch_fill_u32(uint32_t* p, uint64_t n, uint32_t v, cudaStream_t s);
 void launch_merge_parts(const uint4* splits, uint64_t nsplits, uint32_t K, const uint32_t* t_ids,
                         const double* t_sq, const uint32_t* t_count, const uint32_t* qrow,
@@ -387,6 +388,8 @@ void launch_rows_by(const double* X64, const uint32_t* A, uint64_t N, uint32_t n
 void launch_item_delta(const uint4* items, const float* r2, uint64_t nitems, double inv_s2,
                        double A, double B, double C, double lim, uint32_t min_q, float* delta,
                        uint8_t* tc_ok, cudaStream_t s);
+void launch_item_max_cut(const uint4* items, uint64_t nitems, const uint32_t* qrow, uint64_t nq,
+                         const uint32_t* vsrc, const float* cut_by_row, float* out, cudaStream_t s);
 void launch_range_len(const uint2* r, uint64_t n, uint32_t* out, cudaStream_t s);  // out = y - x
 void launch_miss_flags(const uint32_t* rows, uint64_t n, const uint8_t* st, uint8_t* flags,
                        cudaStream_t s);

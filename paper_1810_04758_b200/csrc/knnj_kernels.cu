@@ -1532,6 +1532,31 @@ void launch_item_delta(const uint4* items, const float* r2, uint64_t nitems, dou
     KJ_CUDA(cudaGetLastError());
     g_launches.fetch_add(1, std::memory_order_relaxed);
 }
+// per work item: the largest per-row K-th bound (cut_by_row, by output row) over its launch
+// rows (virtual split-part rows map to their real row through vsrc)
+__global__ void k_item_max_cut(const uint4* items, uint64_t nitems, const uint32_t* qrow, uint64_t nq,
+                               const uint32_t* vsrc, const float* cut_by_row, float* out) {
+    const uint64_t item = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (item >= nitems) return;
+    const uint4 it = items[item];
+    float m = 0.f;
+    for (uint32_t r = it.x + lane; r < it.y; r += 32) {
+        const uint32_t rr = r < nq ? r : vsrc[r - nq];
+        m = fmaxf(m, cut_by_row[qrow[rr]]);
+    }
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    // widened like the scalar radius (an FP64 sum can sit below the true squared distance)
+    if (lane == 0) out[item] = it.y > it.x ? __fmul_ru(m, 1.0f + 0x1p-20f) : 0.f;
+}
+void launch_item_max_cut(const uint4* items, uint64_t nitems, const uint32_t* qrow, uint64_t nq,
+                         const uint32_t* vsrc, const float* cut_by_row, float* out, cudaStream_t s) {
+    if (!nitems) return;
+    k_item_max_cut<<<(unsigned)((nitems * 32 + 255) / 256), 256, 0, s>>>(items, nitems, qrow, nq, vsrc,
+                                                                         cut_by_row, out);
+    KJ_CUDA(cudaGetLastError());
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+}
 __global__ void k_range_len(const uint2* r, uint64_t n, uint32_t* out) {
     for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
          i += uint64_t(gridDim.x) * blockDim.x)
@@ -1873,13 +1898,15 @@ __global__ void k_filter_ranges(uint4* items, uint64_t nitems, const float* qbox
                                 const uint2* adj, const float* box, uint64_t nblk, float r2,
                                 uint32_t* out_cnt, const uint32_t* out_off, uint2* out_adj,
                                 unsigned long long* screened, float* out_key, const float* gbox,
-                                float* item_r2, uint32_t r_m, float r_2w, const float* dbox) {
+                                float* item_r2, uint32_t r_m, float r_2w, const float* dbox,
+                                const float* item_rad2) {
     const int lane = threadIdx.x & 31;
     const uint64_t item = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     if (item >= nitems) return;
     const uint4 it = items[item];
     const float* ql = qbox + item * 2 * n;
     const float* qh = ql + n;
+    if (item_rad2) r2 = fminf(r2, item_rad2[item]);  // the item's rows' K-th bound
     uint32_t kept = 0;
     unsigned long long span = 0;
     float rmax = 0.f;  // item_r2: max over kept blocks
@@ -1976,14 +2003,15 @@ void launch_filter_ranges(uint4* items, uint64_t nitems, const float* qbox, uint
                           uint32_t* out_cnt, const uint32_t* out_off, uint2* out_adj,
                           unsigned long long* screened, bool fill, cudaStream_t s,
                           float* out_key, unsigned long long* count_total, const float* gbox,
-                          float* item_r2, uint32_t r_m, float r_2w, const float* dbox) {
+                          float* item_r2, uint32_t r_m, float r_2w, const float* dbox,
+                          const float* item_rad2) {
     if (!nitems) return;
     const unsigned grid = (unsigned)((nitems * 32 + 255) / 256);
     if (!fill) screened = count_total;  // the count pass sums kept ranges there (if given)
 #define KJ_FR(F, O)                                                                       \
     k_filter_ranges<F, O><<<grid, 256, 0, s>>>(items, nitems, qbox, n, adj, box, nblk, r2, \
                                                out_cnt, out_off, out_adj, screened, out_key, gbox, \
-                                               item_r2, r_m, r_2w, dbox)
+                                               item_r2, r_m, r_2w, dbox, item_rad2)
     if (out_key) {
         if (fill) KJ_FR(true, true);
         else KJ_FR(false, true);

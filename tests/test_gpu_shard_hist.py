@@ -236,7 +236,8 @@ def test_early_d2h_identical(engine, spec, N, n, k):
 
 @pytest.mark.parametrize("opt,val,default", [("morton_dims", 6, 10), ("morton_bits", 5, 3),
                                              ("finalize_xj", 0, 1), ("tc_slack", 12, 24),
-                                             ("sweep_order", 0, 1)])
+                                             ("sweep_order", 0, 1), ("tc_small_cta", 1, 0),
+                                             ("item_radius", 0, 1)])
 def test_engine_knobs_identical(engine, oracle, opt, val, default):
     """The remaining engine knobs change only work order and layout, never an output bit
     (70k points so the finalize's join-ordered copy is in play)."""
