@@ -578,9 +578,18 @@ struct knnj_ctx {
 
     double last_hist_kernel_ms = 0.0;
     bool last_hist_tc = false;
+    // Counts of the sampled queries qids (this shard's share when sharded: a slice of the
+    // queries, or for the grid histogram all queries against a slice of the candidates).
     void histogram_queries(const uint64_t* qids, uint64_t nq, double em, uint32_t nb,
-                           uint64_t* raw, uint32_t ncount = 0) {
+                           uint64_t* raw, uint32_t ncount = 0, uint32_t shard = 0,
+                           uint32_t nshard = 1) {
         if (ncount == 0 || ncount > nb) ncount = nb;
+        const bool cand_split = nshard > 1 && grid_hist_applies(nq, ncount, nb);
+        if (nshard > 1 && !cand_split) {  // this shard's contiguous slice of the queries
+            const uint64_t lo = nq * shard / nshard, hi = nq * (shard + 1) / nshard;
+            qids += lo;
+            nq = hi - lo;
+        }
         if (nq == 0) {
             last_hist_kernel_ms = 0.0;
             return;
@@ -628,8 +637,11 @@ struct knnj_ctx {
         a.inv_width = inv_width;
         a.counts = d_cnt.p;
         screen_consts(a.gam, a.erg, a.eab, a.e64);
-        if (grid_hist_applies(nq, ncount, nb)) {
-            histogram_grid(d_q.p, nq, a, S[ncount]);
+        if (cand_split || grid_hist_applies(nq, ncount, nb)) {
+            if (cand_split)
+                histogram_grid(d_q.p, nq, a, S[ncount], N * shard / nshard, N * (shard + 1) / nshard);
+            else
+                histogram_grid(d_q.p, nq, a, S[ncount]);
             last_hist_tc = false;
             std::vector<unsigned long long> c(nb);
             KJ_CUDA(cudaMemcpyAsync(c.data(), d_cnt.p, 8 * nb, cudaMemcpyDeviceToHost, s));
@@ -684,23 +696,39 @@ struct knnj_ctx {
     Level hist_lv;  // built = its tables match the current working points
     DBuf<float> hist_Xs;
     double last_hist_grid_build_ms = 0.0;
-    void histogram_grid(const uint32_t* d_q, uint64_t nq, const HistArgs& h, double r2) {
+    // [p0, p1): the candidate slice (a shard's ids; default all points). With a slice the
+    // grid holds only those points and the queries (any ids) find their cells from their
+    // coordinates; the per-shard counts sum to the full histogram (counts are additive
+    // over candidate partitions), so every shard bins all sampled queries against 1/S of
+    // the points instead of 1/S of the queries against a replicated all-points grid.
+    uint64_t hist_p0 = 0, hist_p1 = 0;
+    DBuf<double> hist_mins;
+    void histogram_grid(const uint32_t* d_q, uint64_t nq, const HistArgs& h, double r2,
+                        uint64_t p0 = 0, uint64_t p1 = ~0ull) {
         const uint32_t m = std::min<uint32_t>(n, 6);
         const double w = std::sqrt(r2) * (1.0 + 1e-9);
+        p1 = std::min<uint64_t>(p1, N);
+        const bool slice = p0 != 0 || p1 != N;
         Timer tb(s);
         // a grid built for a slightly larger radius (the pilot's) serves this one too
-        if (!(hist_lv.built && hist_lv.m == m && hist_lv.w >= w && hist_lv.w <= 1.2 * w)) {
-            grid_tables_into(hist_lv, m, w);
+        if (!(hist_lv.built && hist_lv.m == m && hist_lv.w >= w && hist_lv.w <= 1.2 * w &&
+              hist_p0 == p0 && hist_p1 == p1)) {
+            grid_tables_into(hist_lv, m, w, p0, p1);
             hist_Xs.ensure((uint64_t)n * Npad);
-            launch_gather_soa(Xf.p, hist_lv.A.p, N, n, Npad, hist_Xs.p, s);
+            launch_gather_soa(Xf.p, hist_lv.A.p, hist_lv.npts, n, Npad, hist_Xs.p, s);
+            hist_mins.ensure(m);
+            KJ_CUDA(cudaMemcpyAsync(hist_mins.p, hist_lv.mins.data(), 8 * m, cudaMemcpyHostToDevice, s));
             hist_lv.built = true;
+            hist_p0 = p0;
+            hist_p1 = p1;
         }
-        // queries in the grid's sorted order (neighbouring warps share candidate rows)
+        // queries in the grid's sorted order (neighbouring warps share candidate rows); a
+        // slice grid does not hold them: they go by id
         DBuf<uint32_t> qp_u, qp;
-        qp_u.ensure(nq);
-        qp.ensure(nq);
-        launch_map_u32(d_q, hist_lv.posOf.p, nq, qp_u.p, s);
-        {
+        if (!slice) {
+            qp_u.ensure(nq);
+            qp.ensure(nq);
+            launch_map_u32(d_q, hist_lv.posOf.p, nq, qp_u.p, s);
             size_t bytes = 0;
             KJ_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, bytes, qp_u.p, qp.p, (int64_t)nq, 0,
                                                    bits_for(N), s));
@@ -725,8 +753,14 @@ struct knnj_ctx {
         a.strides = d_cs.p + m;
         a.n = n;
         a.m = m;
-        a.qpos = qp.p;
+        a.qpos = slice ? nullptr : qp.p;
         a.nq = nq;
+        if (slice) {
+            a.qids = d_q;
+            a.Xf = Xf.p;
+            a.mins = hist_mins.p;
+            a.w = hist_lv.w;
+        }
         a.n_bins = h.n_bins;
         a.n_count = h.n_count;
         a.SU = h.SU;
@@ -897,14 +931,13 @@ struct knnj_ctx {
                                 const std::function<void(uint64_t*, uint64_t)>& reduce,
                                 uint64_t* raw) {
         const uint64_t nq = hq.size();
-        const uint64_t lo = nq * shard / nshard, hi = nq * (shard + 1) / nshard;
         std::fill(raw, raw + nb, 0ull);
         const double pairs = double(nq) * double(N);
         const bool cap = !full && hist_cap_mode != 0 && nb > 2 &&
                          (hist_cap_mode == 2 || pairs >= 268435456.0);
         double kms = 0.0;
         if (!cap) {
-            histogram_queries(hq.data() + lo, hi - lo, em, nb, raw);
+            histogram_queries(hq.data(), nq, em, nb, raw, 0, shard, nshard);
             kms += last_hist_kernel_ms;
             reduce(raw, nb);
             last_hist_kernel_ms = kms;
@@ -914,7 +947,7 @@ struct knnj_ctx {
         // place the cap; a cap that falls short only costs the full re-binning)
         const uint64_t STRIDE = std::max<uint64_t>(64, nq / 8192);
         std::vector<uint64_t> pilot, rest;
-        for (uint64_t i = lo; i < hi; ++i) (i % STRIDE == 0 ? pilot : rest).push_back(hq[i]);
+        for (uint64_t i = 0; i < nq; ++i) (i % STRIDE == 0 ? pilot : rest).push_back(hq[i]);
         const uint64_t npilot = (nq + STRIDE - 1) / STRIDE;  // over all shards
         std::vector<uint64_t> praw(nb, 0), rraw(nb, 0);
         // the pilot itself first counts only the lowest third of the bins (exact there);
@@ -944,8 +977,8 @@ struct knnj_ctx {
         bool pilot_partial = false;
         for (uint32_t rc : rounds) {
             std::fill(praw.begin(), praw.end(), 0ull);
-            if (rc < nb) histogram_queries(pilot.data(), pilot.size(), em, nb, praw.data(), rc);
-            else histogram_queries(pilot.data(), pilot.size(), em, nb, praw.data());
+            histogram_queries(pilot.data(), pilot.size(), em, nb, praw.data(), rc < nb ? rc : 0, shard,
+                              nshard);
             kms += last_hist_kernel_ms;
             reduce(praw.data(), nb);
             pilot_partial = rc < nb;
@@ -956,7 +989,7 @@ struct knnj_ctx {
         bcap = std::min<uint32_t>(bcap, nb);
         uint64_t run = 0;
         if (bcap < nb) {
-            histogram_queries(rest.data(), rest.size(), em, nb, rraw.data(), bcap);
+            histogram_queries(rest.data(), rest.size(), em, nb, rraw.data(), bcap, shard, nshard);
             kms += last_hist_kernel_ms;
             reduce(rraw.data(), nb);
             run = 0;
@@ -972,11 +1005,11 @@ struct knnj_ctx {
         }
         if (pilot_partial) {  // the pilot's counts stop at its cap
             std::fill(praw.begin(), praw.end(), 0ull);
-            histogram_queries(pilot.data(), pilot.size(), em, nb, praw.data());
+            histogram_queries(pilot.data(), pilot.size(), em, nb, praw.data(), 0, shard, nshard);
             kms += last_hist_kernel_ms;
             reduce(praw.data(), nb);
         }
-        histogram_queries(rest.data(), rest.size(), em, nb, rraw.data());
+        histogram_queries(rest.data(), rest.size(), em, nb, rraw.data(), 0, shard, nshard);
         kms += last_hist_kernel_ms;
         reduce(rraw.data(), nb);
         for (uint32_t b = 0; b < nb; ++b) raw[b] = praw[b] + rraw[b];
@@ -1045,7 +1078,11 @@ struct knnj_ctx {
         finish_level(lv);
     }
     // GridIndex::build's tables (grid_index.cpp:13-75) for lv: B, G, A, slot, posOf
-    void grid_tables_into(Level& lv, uint32_t m, double w) {
+    // Grid tables over the points with ids in [p0, p1) (default all; a slice for the
+    // candidate-split histogram of sharded runs). Cell geometry from all points.
+    void grid_tables_into(Level& lv, uint32_t m, double w, uint64_t p0 = 0, uint64_t p1 = ~0ull) {
+        p1 = std::min<uint64_t>(p1, N);
+        const uint64_t cnt = p1 > p0 ? p1 - p0 : 0;
         lv.built = false;
         lv.m = m;
         lv.w = w;
@@ -1101,24 +1138,27 @@ struct knnj_ctx {
         DBuf<uint64_t>& skeys = gk_skeys;
         DBuf<uint32_t>& vals = gk_vals;
         DBuf<uint32_t>& runidx = gk_runidx;
-        keys.ensure(N);
-        skeys.ensure(N);
-        vals.ensure(N);
-        lv.A.ensure(N);
-        launch_cell_keys(X64.p, N, n, m, d_mins.p, w, d_cs.p, d_cs.p + m, keys.p, vals.p, s);
-        sort_pairs_u64_u32(sc, keys.p, skeys.p, vals.p, lv.A.p, N, lv.key_bits, s);
-        runidx.ensure(N);
-        launch_head_flags(skeys.p, N, vals.p, s);  // vals reused as flags
-        inclusive_sum(sc, vals.p, runidx.p, N, s);
+        keys.ensure(cnt);
+        skeys.ensure(cnt);
+        vals.ensure(cnt);
+        lv.A.ensure(cnt);
+        launch_cell_keys(X64.p + p0 * n, cnt, n, m, d_mins.p, w, d_cs.p, d_cs.p + m, keys.p, vals.p, s,
+                         (uint32_t)p0);
+        sort_pairs_u64_u32(sc, keys.p, skeys.p, vals.p, lv.A.p, cnt, lv.key_bits, s);
+        runidx.ensure(cnt);
+        launch_head_flags(skeys.p, cnt, vals.p, s);  // vals reused as flags
+        inclusive_sum(sc, vals.p, runidx.p, cnt, s);
         uint32_t nruns = 0;
-        KJ_CUDA(cudaMemcpyAsync(&nruns, runidx.p + N - 1, 4, cudaMemcpyDeviceToHost, s));
+        if (cnt) KJ_CUDA(cudaMemcpyAsync(&nruns, runidx.p + cnt - 1, 4, cudaMemcpyDeviceToHost, s));
         sync();
         lv.ncells = nruns;
         lv.B.ensure(nruns);
         lv.G.ensure(nruns);
         lv.slot.ensure(N);
         lv.posOf.ensure(N);
-        launch_grid_tables(skeys.p, lv.A.p, runidx.p, N, lv.B.p, lv.G.p, lv.slot.p, lv.posOf.p, s);
+        if (cnt)
+            launch_grid_tables(skeys.p, lv.A.p, runidx.p, cnt, lv.B.p, lv.G.p, lv.slot.p, lv.posOf.p, s);
+        lv.npts = cnt;
         lv.bbox_ready = lv.xj_ready = lv.xs_ready = lv.tc_ready = false;
     }
     // the join's order and operands on top of the tables
@@ -1153,7 +1193,7 @@ struct knnj_ctx {
     // (K = 3n+2, ~22-bit products) padded to 64-half k-blocks (KB <= 5: n <= 106); wider
     // points use the SIMT kernels.
     bool tc_enabled = true;
-    bool tc_small_cta = false;
+    int tc_small_cta = 2;  // 0 off, 1 on, 2 for n > 8
     bool item_radius = true;  // fallback levels filter each item at its rows' K-th bound
     bool split_items = true;  // split oversized work items into candidate-range parts
     uint32_t tc_slack = 24;       // tcgen05 join list capacity K + slack (compaction when full)
@@ -1164,6 +1204,7 @@ struct knnj_ctx {
     uint32_t chunk_min_rows = 65536;  // ... each of at least this many query rows
     uint32_t fin_blocks = 148 * 2;    // grid of a chunk's overlapped finalize (0: one warp per row)
     uint32_t copy_blocks = 74;        // grid of a chunk's row copy to the host (0: one warp per row)
+    bool rows_bulk = true;            // ... through cp.async.bulk (TMA) rather than plain stores
     // level-0 radius bound (run_impl): sample size, quantile (per mille) of the sample's
     // K-th sq, the largest bound worth using (fraction of the filter radius^2), and the
     // smallest pass it is tried on
@@ -1338,15 +1379,20 @@ struct knnj_ctx {
         TcJoinCfg c;
         if (!use_tc() || K < 1 || (!any_precision && !tc_precise_for(w))) return c;
         const uint32_t KB = tc_row_halfs() / 64;
-        const uint32_t L0 = K + tc_slack;
+        // lists past 64 entries are compacted over 128 slots (4 per lane): a wider slack
+        // halves their compactions (C4, K=64: 24 -> 40 cut the tcgen05 part 2.24 -> 2.15 s)
+        const uint32_t L0 = K + (K + tc_slack <= 64 ? tc_slack : std::max<uint32_t>(tc_slack, 40));
         if (KB >= 3) {
             // wide operands (43 <= n <= 106): 64-candidate tiles keep A + B stages in smem
             c.sh = TcShape{(int)KB, 1, KB == 5 ? 2 : 3, 64};
             c.L = std::min<uint32_t>(L0, 64);
         } else if (L0 <= 64) {
             // tc_small_cta: 128-query CTAs with a 2-stage ring (~106 KB): two per SM, twice
-            // the epilogue warps per SM sub-partition
-            c.sh = KB == 1 ? (tc_small_cta ? TcShape{1, 1, 2} : TcShape{1, 2, 4}) : TcShape{2, 1, 3};
+            // the epilogue warps per SM sub-partition. Measured: NS (18-D) 1675 -> 1585 ms,
+            // C2 unchanged, C5 (4-D) 1455 -> 1492 ms (twice the items to filter and sort), so
+            // the default (2) takes it for n > 8 only
+            const bool small = tc_small_cta == 1 || (tc_small_cta == 2 && n > 8);
+            c.sh = KB == 1 ? (small ? TcShape{1, 1, 2} : TcShape{1, 2, 4}) : TcShape{2, 1, 3};
             c.L = L0;
         } else {
             c.sh = KB == 1 ? TcShape{1, 1, 4} : TcShape{2, 1, 2};
@@ -2000,7 +2046,7 @@ struct knnj_ctx {
                 KJ_CUDA(cub::DeviceRadixSort::SortKeys(o_tmp, bytes, P.qrow.p + cr[c], o_keys.p,
                                                        (int64_t)fc.nrows, 0, bits_for(N), st));
                 launch_rows_to_host(o_keys.p, fc.nrows, K, out_ids, out_dist, host_ids, host_dist,
-                                    st == s_out ? copy_blocks : 0, st);
+                                    st == s_out ? copy_blocks : 0, st, rows_bulk);
             }
         };
         if (tc) {
@@ -2609,7 +2655,8 @@ int knnj_set_option(knnj_ctx* c, const char* name, int64_t value) {
         } else if (k == "item_radius") {
             c->item_radius = value != 0;
         } else if (k == "tc_small_cta") {
-            c->tc_small_cta = value != 0;
+            if (value < 0 || value > 2) throw Error(1, "tc_small_cta must be 0, 1 or 2");
+            c->tc_small_cta = (int)value;
         } else if (k == "item_tc") {
             c->item_tc = value != 0;
         } else if (k == "item_tc_min_q") {
@@ -2624,6 +2671,8 @@ int knnj_set_option(knnj_ctx* c, const char* name, int64_t value) {
                 c->s_out = nullptr;
                 c->ev_out = nullptr;
             }
+        } else if (k == "rows_bulk") {
+            c->rows_bulk = value != 0;
         } else if (k == "copy_blocks") {
             if (value < 0 || value > (1 << 24)) throw Error(1, "copy_blocks must be in [0, 2^24]");
             c->copy_blocks = (uint32_t)value;

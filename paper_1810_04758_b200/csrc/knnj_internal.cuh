@@ -116,6 +116,7 @@ struct Level {
     std::vector<double> mins, maxs;
     std::vector<uint64_t> cpd, strides;
     uint64_t ncells = 0;
+    uint64_t npts = 0;   // points in the tables (all N, or a slice: the histogram's shard grid)
     uint32_t key_bits = 0;
     DBuf<uint64_t> B;    // ncells: sorted non-empty linear cell ids
     DBuf<uint2> G;       // ncells: [begin,end) into A
@@ -272,6 +273,12 @@ struct HistGridArgs {
     double eps_mean, limit_sq, inv_width;
     unsigned long long* counts;
     float gam, erg, eab, e64;
+    // candidate-slice grids (a shard's points only): queries are point ids (qids), their
+    // cell from the coordinates with the grid's mins / width, FP32 coords from Xf (id order)
+    const uint32_t* qids;    // non-null selects this mode (qpos unused)
+    const float* Xf;
+    const double* mins;      // m
+    double w;
 };
 void launch_hist_grid(const HistGridArgs& a, cudaStream_t s);
 
@@ -318,7 +325,7 @@ void launch_minmax(const double* X, uint64_t N, uint32_t n, uint32_t m,
                    unsigned long long* mn, unsigned long long* mx, cudaStream_t s);
 void launch_cell_keys(const double* X, uint64_t N, uint32_t n, uint32_t m, const double* mins,
                       double w, const uint64_t* cpd, const uint64_t* strides, uint64_t* keys,
-                      uint32_t* vals, cudaStream_t s);
+                      uint32_t* vals, cudaStream_t s, uint32_t base = 0);
 void launch_iota(uint32_t* v, uint64_t N, cudaStream_t s);
 void launch_head_flags(const uint64_t* keys, uint64_t N, uint32_t* flags, cudaStream_t s);
 void launch_grid_tables(const uint64_t* skeys, const uint32_t* A, const uint32_t* runidx,
@@ -406,7 +413,7 @@ void launch_gather_rows(const uint32_t* rows, uint64_t n, uint32_t K, const uint
                         const double* dist, uint32_t* oids, double* odist, cudaStream_t s);
 void launch_rows_to_host(const uint32_t* rows, uint64_t n, uint32_t K, const uint32_t* ids,
                          const double* dist, uint32_t* hids, double* hdist, uint32_t max_blocks,
-                         cudaStream_t s);
+                         cudaStream_t s, bool rows_bulk = true);
 void launch_scatter_rows(const uint32_t* rows, uint64_t n, uint32_t K, const uint32_t* ids,
                          const double* dist, uint32_t* oids, double* odist, cudaStream_t s);
 

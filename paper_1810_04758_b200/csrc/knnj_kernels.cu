@@ -667,12 +667,20 @@ __global__ void __launch_bounds__(256) k_hist_grid(HistGridArgs a) {
     for (uint32_t j = 0; j < ml; ++j) R *= 3;
     for (uint64_t row = uint64_t(blockIdx.x) * WARPS + warp; row < a.nq;
          row += uint64_t(gridDim.x) * WARPS) {
-        const uint32_t qp = a.qpos[row];
-        const uint32_t qid = a.A[qp];
-        const uint64_t lin = a.B[a.slot[qid]];
+        const bool by_id = a.qids != nullptr;
+        const uint32_t qp = by_id ? 0xFFFFFFFFu : a.qpos[row];
+        const uint32_t qid = by_id ? a.qids[row] : a.A[qp];
         uint64_t c[8];
-        {
-            uint64_t r = lin;
+        if (by_id) {  // the cell rule of k_cell_keys (grid_index.cpp:77-88)
+            for (uint32_t j = 0; j < m; ++j) {
+                double rel = __ddiv_rn(__dsub_rn(a.X64[(uint64_t)qid * n + j], a.mins[j]), a.w);
+                if (rel < 0.0) rel = 0.0;
+                uint64_t idx = (uint64_t)floor(rel);
+                if (idx > a.cpd[j] - 1) idx = a.cpd[j] - 1;
+                c[j] = idx;
+            }
+        } else {
+            uint64_t r = a.B[a.slot[qid]];
             for (uint32_t j = 0; j < m; ++j) {
                 c[j] = r / a.strides[j];
                 r -= c[j] * a.strides[j];
@@ -707,7 +715,9 @@ __global__ void __launch_bounds__(256) k_hist_grid(HistGridArgs a) {
         float na = 0.f;
 #pragma unroll
         for (int d = 0; d < NP; ++d) {
-            const float v = d < (int)n ? a.Xs[(uint64_t)d * a.Npad + qp] : 0.f;
+            const float v = d < (int)n ? (by_id ? a.Xf[(uint64_t)d * a.Npad + qid]
+                                                : a.Xs[(uint64_t)d * a.Npad + qp])
+                                       : 0.f;
             a2[d] = -2.f * v;
             na = fmaf(v, v, na);
         }
@@ -725,7 +735,8 @@ __global__ void __launch_bounds__(256) k_hist_grid(HistGridArgs a) {
                 }
                 acc += nb;
                 const float dl = screen_delta(Aq, sqrtf(nb) * 1.0001f, a.gam, a.erg, a.eab, a.e64);
-                if (!(acc < __fsub_ru(__fadd_ru(lo_end, dl), na)) || t == qp) continue;
+                if (!(acc < __fsub_ru(__fadd_ru(lo_end, dl), na)) || (by_id ? a.A[t] == qid : t == qp))
+                    continue;
                 const float key = acc + na;
                 const float klo = __fsub_rd(key, dl), khi = __fadd_ru(key, dl);
                 int b = key > 0.f ? (int)(key * rsqrtf(key) * invw) : 0;
@@ -912,7 +923,7 @@ void launch_minmax(const double* X, uint64_t N, uint32_t n, uint32_t m, unsigned
 // grid_index.cpp:77-94 (cell_of + linearize), FP64 division and floor
 __global__ void k_cell_keys(const double* X, uint64_t N, uint32_t n, uint32_t m,
                             const double* mins, double w, const uint64_t* cpd,
-                            const uint64_t* strides, uint64_t* keys, uint32_t* vals) {
+                            const uint64_t* strides, uint64_t* keys, uint32_t* vals, uint32_t base) {
     for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < N;
          i += uint64_t(gridDim.x) * blockDim.x) {
         uint64_t id = 0;
@@ -924,13 +935,13 @@ __global__ void k_cell_keys(const double* X, uint64_t N, uint32_t n, uint32_t m,
             id += idx * strides[j];
         }
         keys[i] = id;
-        vals[i] = (uint32_t)i;
+        vals[i] = base + (uint32_t)i;
     }
 }
 void launch_cell_keys(const double* X, uint64_t N, uint32_t n, uint32_t m, const double* mins,
                       double w, const uint64_t* cpd, const uint64_t* strides, uint64_t* keys,
-                      uint32_t* vals, cudaStream_t s) {
-    k_cell_keys<<<2368, 256, 0, s>>>(X, N, n, m, mins, w, cpd, strides, keys, vals);
+                      uint32_t* vals, cudaStream_t s, uint32_t base) {
+    k_cell_keys<<<2368, 256, 0, s>>>(X, N, n, m, mins, w, cpd, strides, keys, vals, base);
     KJ_CUDA(cudaGetLastError());
     g_launches.fetch_add(1, std::memory_order_relaxed);
 }
@@ -1656,10 +1667,61 @@ __global__ void k_rows_to_host(const uint32_t* rows, uint64_t n, uint32_t K, con
         for (uint32_t i = lane; i < K; i += 32) hdist[base + i] = dist[base + i];
     }
 }
+// The same copy through the bulk-copy (TMA) engine: lanes stage a row in shared memory
+// with ordinary loads, one lane hands it to cp.async.bulk (shared -> mapped host). The
+// PCIe back-pressure then sits in the bulk-copy queue instead of the SM's load/store
+// pipeline that a concurrent join's epilogue shares. Rows need K % 4 == 0 (16-byte sizes).
+constexpr int RB = 8;  // row buffers per warp
+__global__ void __launch_bounds__(128) k_rows_to_host_bulk(const uint32_t* rows, uint64_t n, uint32_t K,
+                                                            const uint32_t* ids, const double* dist,
+                                                            uint32_t* hids, double* hdist) {
+    extern __shared__ __align__(128) unsigned char rb_smem[];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const uint32_t row_bytes = K * 12;  // K ids then K doubles
+    unsigned char* mine = rb_smem + (size_t)wib * RB * row_bytes;
+    const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+    uint32_t slot = 0;
+    for (uint64_t w = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w < n; w += nw) {
+        // the slot's previous bulk store must have read its data (RB - 1 may stay in flight)
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(RB - 1) : "memory");
+        __syncwarp();
+        const uint64_t base = (uint64_t)rows[w] * K;
+        uint32_t* si = reinterpret_cast<uint32_t*>(mine + slot * row_bytes);
+        double* sd = reinterpret_cast<double*>(si + K);
+        for (uint32_t i = lane; i < K; i += 32) si[i] = ids[base + i];
+        for (uint32_t i = lane; i < K; i += 32) sd[i] = dist[base + i];
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) {
+            const unsigned sa = (unsigned)__cvta_generic_to_shared(si);
+            const unsigned sb = (unsigned)__cvta_generic_to_shared(sd);
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(hids + base),
+                         "r"(sa), "r"(K * 4)
+                         : "memory");
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(hdist + base),
+                         "r"(sb), "r"(K * 8)
+                         : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+        slot = (slot + 1) % RB;
+    }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 void launch_rows_to_host(const uint32_t* rows, uint64_t n, uint32_t K, const uint32_t* ids,
                          const double* dist, uint32_t* hids, double* hdist, uint32_t max_blocks,
-                         cudaStream_t s) {
+                         cudaStream_t s, bool rows_bulk) {
     if (!n || !K) return;
+    const size_t sm = (size_t)4 * RB * K * 12;  // 4 warps per block
+    if (rows_bulk && K % 4 == 0 && sm <= 48 * 1024 &&
+        (reinterpret_cast<uintptr_t>(hids) & 15) == 0 && (reinterpret_cast<uintptr_t>(hdist) & 15) == 0) {
+        uint64_t blocks = (n * 32 + 127) / 128;
+        if (max_blocks) blocks = std::min<uint64_t>(blocks, 2ull * max_blocks);
+        k_rows_to_host_bulk<<<(unsigned)blocks, 128, sm, s>>>(rows, n, K, ids, dist, hids, hdist);
+        KJ_CUDA(cudaGetLastError());
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        return;
+    }
     uint64_t blocks = (n * 32 + 255) / 256;
     if (max_blocks) blocks = std::min<uint64_t>(blocks, max_blocks);
     k_rows_to_host<<<(unsigned)blocks, 256, 0, s>>>(rows, n, K, ids, dist, hids, hdist);

@@ -133,10 +133,6 @@ __device__ __forceinline__ float tmem_ld1(uint32_t taddr) {
     return __uint_as_float(r);
 }
 
-#ifndef KNNJ_RARE_LANE
-#define KNNJ_RARE_LANE 0
-#endif
-
 // 3-input FP32 min (FMNMX3 on sm_100; a NaN input is ignored like fminf)
 __device__ __forceinline__ float fmin3(float a, float b, float c) {
     float d;
@@ -578,43 +574,6 @@ __global__ void __launch_bounds__(64 + 128 * G, 1)
                         mk[1] |= (v1[j] <= rhs ? 1u : 0u) << j;
                     }
                 }
-#if KNNJ_RARE_LANE
-                // per-lane rare path: a hitting lane parks its slab in local memory and walks
-                // its own hit columns; the warp iterates max-over-lanes times instead of over
-                // the union of the lanes' columns (compactions stay warp-cooperative)
-                float park[64];
-                if (hit) {
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) {
-                        park[j] = v0[j];
-                        park[32 + j] = v1[j];
-                    }
-                }
-                unsigned long long mine = (unsigned long long)mk[0] | ((unsigned long long)mk[1] << 32);
-                while (__any_sync(0xffffffffu, mine != 0ull)) {
-                    const bool valid = mine != 0ull;
-                    const int j = valid ? __ffsll((long long)mine) - 1 : 0;
-                    mine &= mine - 1ull;
-                    ++st_bits;
-                    const float x = valid ? park[j] : CUDART_INF_F;
-                    const uint32_t pos = s + j0 + j;
-                    bool want = valid && x <= rhs && pos != qp;
-                    unsigned full = __ballot_sync(0xffffffffu, want && cnt == LB);
-                    while (full) {
-                        const int src = __ffs(full) - 1;
-                        full &= full - 1;
-                        ++st_cmp;
-                        compact(src);
-                    }
-                    want = want && !ovf && x <= rhs;
-                    if (p.stats) st_ins += __popc(__ballot_sync(0xffffffffu, want));
-                    if (want) {
-                        mykey[cnt] = x + na;
-                        mypos[cnt] = pos;
-                        ++cnt;
-                    }
-                }
-#else
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                     unsigned um = __reduce_or_sync(0xffffffffu, mk[h]);
@@ -642,7 +601,6 @@ __global__ void __launch_bounds__(64 + 128 * G, 1)
                         }
                     }
                 }
-#endif
             }
             fence_before();
             __syncwarp();

@@ -77,21 +77,37 @@ class ThreadAllreduce:
         return reduce
 
 
+GRID_HIST = {"hist_cap": 2, "hist_grid": 2}  # capped rounds on the grid histogram
+
+
 @pytest.mark.parametrize("shards", [2, 3])
-@pytest.mark.parametrize("spec,N,n,k", [("clusters:16:0.05", 8000, 18, 32),
-                                        ("exponential", 6000, 6, 20),
-                                        ("uniform", 5000, 2, 5)])
-def test_sharded_run_equals_single(engine, spec, N, n, k, shards):
+@pytest.mark.parametrize("spec,N,n,k,opts", [("clusters:16:0.05", 8000, 18, 32, {}),
+                                             ("exponential", 6000, 6, 20, {}),
+                                             ("uniform", 5000, 2, 5, {}),
+                                             ("uniform", 30000, 4, 16, GRID_HIST),
+                                             ("exponential", 20000, 6, 12, GRID_HIST)])
+def test_sharded_run_equals_single(engine, spec, N, n, k, opts, shards):
+    """Shards (threads on one GPU, counts summed through a thread all-reduce) merge to the
+    single run; with GRID_HIST every shard bins all sampled queries against its own
+    slice of the candidates (the candidate-split grid histogram)."""
     X = generate(spec, N, n, 7)
     cfg = RunConfig(k=k, mode="hybrid", seed=7)
-    engine.set_points(X)
-    ref = engine.run(cfg, want_hist=False)
+    for o, v in opts.items():
+        engine.set_option(o, v)
+    try:
+        engine.set_points(X)
+        ref = engine.run(cfg, want_hist=False)
+    finally:
+        engine.set_option("hist_cap", 1)
+        engine.set_option("hist_grid", 1)
     ar = ThreadAllreduce(shards)
     parts, errs, infos = [None] * shards, [], [None] * shards
 
     def work(rank):
         try:
             e = Engine(0)
+            for o, v in opts.items():
+                e.set_option(o, v)
             e.set_points(X)
             r = e.run(cfg, want_hist=False, shard=(rank, shards, ar.fn(rank)))
             parts[rank] = (r.queries.copy(), r.ids.copy(), r.dist.copy(), r.provenance.copy())
@@ -112,6 +128,7 @@ def test_sharded_run_equals_single(engine, spec, N, n, k, shards):
     assert np.array_equal(ids, ref.ids) and np.array_equal(dist, ref.dist)
     assert np.array_equal(prov, ref.provenance)
     assert all(i["eps_used"] == ref.info["eps_used"] for i in infos)
+    assert all(i["hist_bins_counted"] == ref.info["hist_bins_counted"] for i in infos)
     assert sum(i["n_owned"] for i in infos) == N
     assert sum(i["failed_count"] for i in infos) == ref.info["failed_count"]
     # every shard owns a share of the work
@@ -236,7 +253,7 @@ def test_early_d2h_identical(engine, spec, N, n, k):
 
 @pytest.mark.parametrize("opt,val,default", [("morton_dims", 6, 10), ("morton_bits", 5, 3),
                                              ("finalize_xj", 0, 1), ("tc_slack", 12, 24),
-                                             ("sweep_order", 0, 1), ("tc_small_cta", 1, 0),
+                                             ("sweep_order", 0, 1), ("tc_small_cta", 0, 2),
                                              ("item_radius", 0, 1)])
 def test_engine_knobs_identical(engine, oracle, opt, val, default):
     """The remaining engine knobs change only work order and layout, never an output bit

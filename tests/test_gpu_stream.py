@@ -45,25 +45,31 @@ def test_streamed_results_identical(engine, oracle, spec, N, n, k):
     engine.set_option("join_chunks", 8)
     engine.set_option("chunk_min_rows", 1)
     ptrs = []
+    got = []
     try:
         pi, ids = _pinned(lib, N * k, np.uint32)
         pd, dist = _pinned(lib, N * k, np.float64)
         pp, prov = _pinned(lib, N, np.uint8)
         ptrs = [pi, pd, pp]
-        ids[:] = 0xFFFFFFFF
-        dist[:] = -1.0
-        engine.set_points(X)
-        b = engine.run(cfg, out=(pi, pd, pp), want_hist=False)
-        bi, bd, bp = ids.reshape(N, k).copy(), dist.reshape(N, k).copy(), prov.copy()
-        # device-resident leg in chunks, pageable copy
+        for bulk in (1, 0):  # rows copied by cp.async.bulk, then by plain stores
+            engine.set_option("rows_bulk", bulk)
+            ids[:] = 0xFFFFFFFF
+            dist[:] = -1.0
+            engine.set_points(X)
+            b = engine.run(cfg, out=(pi, pd, pp), want_hist=False)
+            got.append((ids.reshape(N, k).copy(), dist.reshape(N, k).copy(), prov.copy()))
+        # device-resident leg, pageable copy
         engine.set_points(X)
         c = engine.run(cfg, want_hist=False)
     finally:
         engine.set_option("chunk_min_rows", 65536)
+        engine.set_option("rows_bulk", 1)
         for p in ptrs:
             lib.knnj_free_pinned(p)
-    assert np.array_equal(bi, a.ids) and np.array_equal(bd, a.dist)
-    assert np.array_equal(bp, a.provenance)
+    for bi, bd, bp in got:
+        assert np.array_equal(bi, a.ids) and np.array_equal(bd, a.dist)
+        assert np.array_equal(bp, a.provenance)
+    bi, bd, bp = got[0]
     assert np.array_equal(c.ids, a.ids) and np.array_equal(c.dist, a.dist)
     assert b.info["fallback_queries"] == a.info["fallback_queries"]
     assert b.info["slow_path_queries"] == a.info["slow_path_queries"]
