@@ -1086,6 +1086,7 @@ struct knnj_ctx {
         lv.built = false;
         lv.m = m;
         lv.w = w;
+        lv.prec_w = w;
         // min / max per indexed dim (exact)
         d_u64a.ensure(64);
         d_u64b.ensure(64);
@@ -1203,12 +1204,20 @@ struct knnj_ctx {
     uint32_t join_chunks = 16;    // level-0 launches (finalize of one overlaps the next join)
     uint32_t chunk_min_rows = 65536;  // ... each of at least this many query rows
     uint32_t fin_blocks = 148 * 2;    // grid of a chunk's overlapped finalize (0: one warp per row)
+    // (74 blocks of 8 warps: enough stores in flight for PCIe without slowing the join
+    // much; the same copy through cp.async.bulk (TMA) measured slower, 1.95 vs 1.73 s)
     uint32_t copy_blocks = 74;        // grid of a chunk's row copy to the host (0: one warp per row)
-    bool rows_bulk = true;            // ... through cp.async.bulk (TMA) rather than plain stores
     // level-0 radius bound (run_impl): sample size, quantile (per mille) of the sample's
     // K-th sq, the largest bound worth using (fraction of the filter radius^2), and the
     // smallest pass it is tried on
     bool kth_bound = true;
+    // the bounded pass on a grid of width ~B with cell runs (run_impl). Off by default: on C5
+    // it screens 3.3x fewer pairs (1.64e12 -> 4.96e11) yet runs slower (1.27 vs 1.05 s),
+    // because the epilogue's cost follows the items' 128-row tiles (the fine cells' runs fill
+    // them to ~60%) and the rare path, not the pair count
+    bool bound_grid = false;
+    double bound_grid_frac = 0.8;    // ... when B is below this fraction of level 0's width
+    uint32_t bound_group_span = 8;   // ... with cell runs of up to this many cells
     uint32_t bound_sample = 4096;
     uint32_t kth_bound_q = 999;
     double bound_max_frac = 0.8;
@@ -1421,7 +1430,7 @@ struct knnj_ctx {
     // Groups the queries (point ids + output rows, on device) by their cell in
     // level lv and builds work items + candidate ranges.
     // the join kernel a pass will run on (decided before its items are built)
-    bool pass_uses_tc(const Level& lv, uint32_t K) const { return tc_join_cfg(K, lv.w).ok; }
+    bool pass_uses_tc(const Level& lv, uint32_t K) const { return tc_join_cfg(K, lv.prec_w).ok; }
     // Mixed passes (item_tc): the global precision rule fails (data far from the centre
     // somewhere), but items whose own data lie close enough to it pass the rule with a
     // per-item bound; those run on the tensor cores, the rest on the SIMT kernel. Needs
@@ -1429,12 +1438,12 @@ struct knnj_ctx {
     bool item_tc = true;
     uint32_t item_tc_min_q = 32;  // ... and items with at least this many queries
     bool pass_mixed(const Level& lv, uint32_t K, double filter_r2) const {
-        if (!item_tc || !(filter_r2 > 0.0) || !box_filter || tc_join_cfg(K, lv.w).ok) return false;
-        const TcJoinCfg c = tc_join_cfg(K, lv.w, true);
+        if (!item_tc || !(filter_r2 > 0.0) || !box_filter || tc_join_cfg(K, lv.prec_w).ok) return false;
+        const TcJoinCfg c = tc_join_cfg(K, lv.prec_w, true);
         return c.ok && c.sh.G == 1;
     }
     uint32_t pass_chunk(const Level& lv, uint32_t K, double filter_r2 = 0.0) const {
-        const TcJoinCfg c = tc_join_cfg(K, lv.w);
+        const TcJoinCfg c = tc_join_cfg(K, lv.prec_w);
         if (c.ok) return 128u * c.sh.G;
         if (pass_mixed(lv, K, filter_r2)) return 128u;
         return (uint32_t)JB;
@@ -1447,7 +1456,8 @@ struct knnj_ctx {
     void build_pass(Level& lv, const uint32_t* d_qpid, const uint32_t* d_qrow, uint64_t nq,
                     Pass& P, uint32_t K = 0, uint32_t shard = 0, uint32_t nshard = 1,
                     const uint8_t* d_dense = nullptr, double filter_r2 = 0.0, bool allow_split = true,
-                    bool all_points = false, const float* d_cut_by_row = nullptr) {
+                    bool all_points = false, const float* d_cut_by_row = nullptr,
+                    uint32_t group_span = 0) {
         P.nq = nq;
         P.nq_all = nq;
         P.nv = nq;
@@ -1510,6 +1520,47 @@ struct knnj_ctx {
             chunk = 32;
             P.chunk = 32;
         }
+        // Cell runs (group_span > 1): consecutive query cells of one row of the grid (equal
+        // in all but the last dim, at most group_span cells apart) whose queries fit one
+        // work item share it; its candidates are the union of their neighbourhoods (rows
+        // over [c_first - 1, c_last + 1] in the last dim), a superset for each query. A
+        // fine grid holds few queries per cell; runs fill the item's 128-query tiles.
+        DBuf<uint32_t> uspan;
+        if (group_span > 1 && nuc > 1) {
+            std::vector<uint32_t> h_cell(nuc);
+            KJ_CUDA(cudaMemcpyAsync(h_cell.data(), ucell.p, 4 * nuc, cudaMemcpyDeviceToHost, s));
+            sync();
+            std::vector<uint64_t> h_lin(lv.ncells);
+            KJ_CUDA(cudaMemcpyAsync(h_lin.data(), lv.B.p, 8 * lv.ncells, cudaMemcpyDeviceToHost, s));
+            sync();
+            const uint64_t cl = lv.cpd[lv.m - 1];
+            std::vector<uint32_t> g_cell, g_cnt, g_span;
+            g_cell.reserve(nuc);
+            uint64_t row0 = 0, c0 = 0;
+            uint32_t q0 = 0;
+            for (uint64_t u = 0; u < nuc; ++u) {
+                const uint64_t lin = h_lin[h_cell[u]], row = lin / cl, cc = lin % cl;
+                if (!g_cell.empty() && row == row0 && cc - c0 < group_span && q0 + h_cnt[u] <= chunk) {
+                    q0 += h_cnt[u];
+                    g_cnt.back() = q0;
+                    g_span.back() = (uint32_t)(cc - c0 + 1);
+                    continue;
+                }
+                g_cell.push_back(h_cell[u]);
+                g_cnt.push_back(h_cnt[u]);
+                g_span.push_back(1);
+                row0 = row;
+                c0 = cc;
+                q0 = h_cnt[u];
+            }
+            nuc = g_cell.size();
+            KJ_CUDA(cudaMemcpyAsync(ucell.p, g_cell.data(), 4 * nuc, cudaMemcpyHostToDevice, s));
+            KJ_CUDA(cudaMemcpyAsync(ucnt.p, g_cnt.data(), 4 * nuc, cudaMemcpyHostToDevice, s));
+            uspan.ensure(nuc);
+            KJ_CUDA(cudaMemcpyAsync(uspan.p, g_span.data(), 4 * nuc, cudaMemcpyHostToDevice, s));
+            exclusive_sum(sc, ucnt.p, ufirst.p, nuc, s);
+            h_cnt.swap(g_cnt);
+        }
         std::vector<uint32_t> h_ioff(nuc + 1);
         uint64_t tot = 0;
         for (uint64_t u = 0; u < nuc; ++u) {
@@ -1527,7 +1578,8 @@ struct knnj_ctx {
         KJ_CUDA(cudaMemcpyAsync(d_cs.p + lv.m, lv.strides.data(), 8 * lv.m, cudaMemcpyHostToDevice, s));
         adj_cnt.ensure(nuc + 1);
         adj_off.ensure(nuc + 1);
-        launch_adj_count(lv.B.p, lv.ncells, ucell.p, nuc, lv.m, d_cs.p, d_cs.p + lv.m, adj_cnt.p, s);
+        launch_adj_count(lv.B.p, lv.ncells, ucell.p, nuc, lv.m, d_cs.p, d_cs.p + lv.m, adj_cnt.p, s,
+                         uspan.p);
         KJ_CUDA(cudaMemsetAsync(adj_cnt.p + nuc, 0, 4, s));
         exclusive_sum(sc, adj_cnt.p, adj_off.p, nuc + 1, s);
         uint32_t nadj = 0;
@@ -1538,7 +1590,7 @@ struct knnj_ctx {
         DBuf<unsigned long long> csize;
         csize.ensure(nuc);
         launch_adj_fill(lv.B.p, lv.G.p, lv.ncells, ucell.p, nuc, lv.m, d_cs.p, d_cs.p + lv.m,
-                        adj_off.p, P.adj.p, csize.p, s);
+                        adj_off.p, P.adj.p, csize.p, s, uspan.p);
         DBuf<uint4> items_unsorted;
         DBuf<unsigned long long> work;
         items_unsorted.ensure(tot);
@@ -1931,9 +1983,9 @@ struct knnj_ctx {
                   double bound2 = 0.0) {
         if (!P.nq) return false;
         if (bound2 > 0.0 && P.nv != P.nq) throw Error(9, "a radius-bounded pass cannot hold split items");
-        const TcJoinCfg tcm = tc_join_cfg(K, lv.w, true);
+        const TcJoinCfg tcm = tc_join_cfg(K, lv.prec_w, true);
         const bool mixed = P.mixed && P.has_r2 && tcm.ok && tcm.sh.G == 1 && P.chunk == 128u;
-        const TcJoinCfg tcc = mixed ? tcm : tc_join_cfg(K, lv.w);
+        const TcJoinCfg tcc = mixed ? tcm : tc_join_cfg(K, lv.prec_w);
         const bool tc = !mixed && tcc.ok && P.chunk == 128u * tcc.sh.G;
         if (!tc && !mixed && P.chunk != (uint32_t)JB && P.chunk != 32u)
             throw Error(9, "pass built for a different kernel");
@@ -2046,7 +2098,7 @@ struct knnj_ctx {
                 KJ_CUDA(cub::DeviceRadixSort::SortKeys(o_tmp, bytes, P.qrow.p + cr[c], o_keys.p,
                                                        (int64_t)fc.nrows, 0, bits_for(N), st));
                 launch_rows_to_host(o_keys.p, fc.nrows, K, out_ids, out_dist, host_ids, host_dist,
-                                    st == s_out ? copy_blocks : 0, st, rows_bulk);
+                                    st == s_out ? copy_blocks : 0, st);
             }
         };
         if (tc) {
@@ -2109,7 +2161,7 @@ struct knnj_ctx {
             part.ensure(P.nitems);
             double A = 0, B = 0, C = 0;
             tc_delta_poly(A, B, C);
-            const double S = tc_S(), ws = lv.w / S;
+            const double S = tc_S(), ws = lv.prec_w / S;
             launch_item_delta(P.items.p, P.item_r2.p, P.nitems, 1.0 / (S * S), A, B, C,
                               0.02 * ws * ws, item_tc_min_q, dlt.p, okf.p, s);
             d_u64a.ensure(2);
@@ -2640,6 +2692,11 @@ int knnj_set_option(knnj_ctx* c, const char* name, int64_t value) {
             c->chunk_min_rows = (uint32_t)value;
         } else if (k == "kth_bound") {
             c->kth_bound = value != 0;
+        } else if (k == "bound_grid") {
+            c->bound_grid = value != 0;
+        } else if (k == "bound_group_span") {
+            if (value < 1 || value > 64) throw Error(1, "bound_group_span must be in [1, 64]");
+            c->bound_group_span = (uint32_t)value;
         } else if (k == "kth_bound_q") {
             if (value < 1 || value > 1000) throw Error(1, "kth_bound_q must be in [1, 1000] per mille");
             c->kth_bound_q = (uint32_t)value;
@@ -2671,8 +2728,6 @@ int knnj_set_option(knnj_ctx* c, const char* name, int64_t value) {
                 c->s_out = nullptr;
                 c->ev_out = nullptr;
             }
-        } else if (k == "rows_bulk") {
-            c->rows_bulk = value != 0;
         } else if (k == "copy_blocks") {
             if (value < 0 || value > (1 << 24)) throw Error(1, "copy_blocks must be in [0, 2^24]");
             c->copy_blocks = (uint32_t)value;
@@ -3421,15 +3476,35 @@ static void run_impl(knnj_ctx* c, const knnj_config* cfg, uint32_t shard, uint32
                 else B2 = (double)f32_round_up(B2);
             }
             I.kth_bound2 = B2;
+            // The bounded pass runs on a grid of width ~B (bound_grid): every candidate within
+            // B of a query lies in its 3^m neighbourhood there, a (w0/B)^m times smaller
+            // volume than level 0's; cell runs refill the work items. Level 0's own walk is
+            // still built (unfiltered) for the reference's candidate counts.
+            Level* lvb = &lv0;
+            Pass P0;
+            const double wf = std::sqrt(B2) * (1.0 + 1e-9);
+            const bool fine_grid = B2 > 0.0 && c->bound_grid && wf < c->bound_grid_frac * lv0.w;
             {
                 Timer tb(s);
                 // chunked launches only pay for the streamed result copy (each chunk restarts
                 // the LPT schedule: on skewed data the tails cost more than the finalize
                 // overlap saves)
                 c->stream_chunks = (nshard == 1 && !fine && h_ids_dev) ? c->join_chunks : 1;
-                c->build_pass(lv0, d_q.p, d_rows.p, nq, P, k_eff, shard, nshard,
-                              have_dense ? d_dense.p : nullptr, B2 > 0.0 ? B2 : filt0, B2 <= 0.0,
-                              all_points);
+                if (fine_grid) {
+                    c->build_level(43, m, wf);
+                    lvb = &c->levels[43];
+                    lvb->prec_w = lv0.w;  // the screen band is judged against level 0's cells
+                    c->build_pass(*lvb, d_q.p, d_rows.p, nq, P, k_eff, shard, nshard,
+                                  have_dense ? d_dense.p : nullptr, B2, false, all_points, nullptr,
+                                  c->bound_group_span);
+                    c->stream_chunks = 1;
+                    c->build_pass(lv0, d_q.p, d_rows.p, nq, P0, k_eff, shard, nshard,
+                                  have_dense ? d_dense.p : nullptr, 0.0, true, all_points);
+                } else {
+                    c->build_pass(lv0, d_q.p, d_rows.p, nq, P, k_eff, shard, nshard,
+                                  have_dense ? d_dense.p : nullptr, B2 > 0.0 ? B2 : filt0, B2 <= 0.0,
+                                  all_points);
+                }
                 c->stream_chunks = 1;
                 I.ms_join_build = tb.ms();
             }
@@ -3439,7 +3514,7 @@ static void run_impl(knnj_ctx* c, const knnj_config* cfg, uint32_t shard, uint32
                     d_cut.ensure(P.nq);
                     launch_fill_f32(d_cut.p, P.nq, (float)B2, s);
                 }
-                streamed = c->run_pass(lv0, P, k_eff, B2 > 0.0 ? d_cut.p : nullptr, eps * eps,
+                streamed = c->run_pass(*lvb, P, k_eff, B2 > 0.0 ? d_cut.p : nullptr, eps * eps,
                                        c->cover2(lv0), o_ids.p, o_dist.p, o_kth.p, o_st.p, &slow,
                                        h_ids_dev, h_dist_dev, &patch_rows, B2);
                 I.ms_join_kernel = c->last_join_kernel_ms;
@@ -3487,9 +3562,10 @@ static void run_impl(knnj_ctx* c, const knnj_config* cfg, uint32_t shard, uint32
             I.ms_join = t.ms();
             trace().mark("run: join");
             I.join_tensor_cores = c->last_join_tc ? 1 : 0;
-            // candidates_examined counts dense queries only (DenseJoinStats)
-            I.candidates_examined = have_dense ? P.candidates_dense : P.candidates;
-            I.join_candidate_pairs = P.candidates;
+            // candidates_examined counts dense queries only (DenseJoinStats), over level 0's walk
+            const Pass& Pw = fine_grid ? P0 : P;
+            I.candidates_examined = have_dense ? Pw.candidates_dense : Pw.candidates;
+            I.join_candidate_pairs = Pw.candidates;
         }
         n_own = P.nq;
         // single-GPU runs with host outputs: copy every row now, on a second stream, while

@@ -113,6 +113,9 @@ struct Level {
     bool built = false;
     uint32_t m = 0;
     double w = 0.0;
+    double prec_w = 0.0;  // width the tcgen05 precision rule compares the screen band with
+                          // (w; a radius-bounded fine grid keeps level 0's: its cut is a
+                          // K-th distance, not a cell width)
     std::vector<double> mins, maxs;
     std::vector<uint64_t> cpd, strides;
     uint64_t ncells = 0;
@@ -337,11 +340,11 @@ void launch_map_u32(const uint32_t* idx, const uint32_t* table, uint64_t n, uint
                     cudaStream_t s);
 void launch_adj_count(const uint64_t* B, uint64_t ncells, const uint32_t* cells, uint64_t nc,
                       uint32_t m, const uint64_t* cpd, const uint64_t* strides,
-                      uint32_t* counts, cudaStream_t s);
+                      uint32_t* counts, cudaStream_t s, const uint32_t* spans = nullptr);
 void launch_adj_fill(const uint64_t* B, const uint2* G, uint64_t ncells, const uint32_t* cells,
                      uint64_t nc, uint32_t m, const uint64_t* cpd, const uint64_t* strides,
                      const uint32_t* offs, uint2* adj, unsigned long long* csize,
-                     cudaStream_t s);
+                     cudaStream_t s, const uint32_t* spans = nullptr);
 void launch_items(const uint32_t* ufirst, const uint32_t* ucnt, const uint32_t* item_off,
                   const uint32_t* adj_off, uint64_t nuc, const unsigned long long* csize,
                   uint4* items, unsigned long long* work, uint32_t chunk, cudaStream_t s);
@@ -413,7 +416,7 @@ void launch_gather_rows(const uint32_t* rows, uint64_t n, uint32_t K, const uint
                         const double* dist, uint32_t* oids, double* odist, cudaStream_t s);
 void launch_rows_to_host(const uint32_t* rows, uint64_t n, uint32_t K, const uint32_t* ids,
                          const double* dist, uint32_t* hids, double* hdist, uint32_t max_blocks,
-                         cudaStream_t s, bool rows_bulk = true);
+                         cudaStream_t s);
 void launch_scatter_rows(const uint32_t* rows, uint64_t n, uint32_t K, const uint32_t* ids,
                          const double* dist, uint32_t* oids, double* odist, cudaStream_t s);
 

@@ -308,6 +308,24 @@ __device__ __forceinline__ void rank_entries(const double (&sq)[EMAX], const uin
 
 // One warp per launch row: exact FP64 distances for the screened list, exact
 // (sq,id) ranks, first K written to the query's output row, status bits.
+// status bits and the K-th of one finalized row (lane 0 writes)
+__device__ __forceinline__ void finalize_status(const FinalArgs& a, uint32_t c, uint32_t orow, double kth,
+                                                int lane) {
+    if (lane != 0) return;
+    uint8_t st = 0;
+    if (c >= a.K) {
+        st |= ST_HAS_K;
+        if (kth <= a.eps2) st |= ST_IN_EPS;
+        if (kth < a.cover2) st |= ST_CERT;
+    }
+    // bounded pass: the listed top-K is the exact one only if its K-th lies within the
+    // bound (every candidate up to it was screened); otherwise re-run unbounded
+    if (a.bound2 > 0.0 && !(c >= a.K && kth <= a.bound2)) st = ST_MISS;
+    a.out_status[orow] = st;
+    a.out_kth[orow] = c >= a.K ? kth : CUDART_INF;
+    if (a.out_count) a.out_count[orow] = min(c, a.K);
+}
+
 __device__ __forceinline__ void finalize_row(const FinalArgs& a, uint64_t row, int lane) {
     const uint32_t c = a.cnt[row];
     if (c == SKIP) return;  // a split row: its parts are finalized and merged separately
@@ -361,20 +379,7 @@ __device__ __forceinline__ void finalize_row(const FinalArgs& a, uint64_t row, i
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) kth = fmin(kth, __shfl_xor_sync(0xffffffffu, kth, o));
-    if (lane == 0) {
-        uint8_t st = 0;
-        if (c >= a.K) {
-            st |= ST_HAS_K;
-            if (kth <= a.eps2) st |= ST_IN_EPS;
-            if (kth < a.cover2) st |= ST_CERT;
-        }
-        // bounded pass: the listed top-K is the exact one only if its K-th lies within the
-        // bound (every candidate up to it was screened); otherwise re-run unbounded
-        if (a.bound2 > 0.0 && !(c >= a.K && kth <= a.bound2)) st = ST_MISS;
-        a.out_status[orow] = st;
-        a.out_kth[orow] = c >= a.K ? kth : CUDART_INF;
-        if (a.out_count) a.out_count[orow] = min(c, a.K);
-    }
+    finalize_status(a, c, orow, kth, lane);
 }
 
 // Warps stride over the launch rows (a bounded grid shares the SMs with a running join).
@@ -1030,11 +1035,14 @@ void launch_map_u32(const uint32_t* idx, const uint32_t* table, uint64_t n, uint
 // the first m-1 indexed dims; each row is the contiguous B-range of linear ids
 // [row + lo_last, row + hi_last] (grid_index.cpp:114-147 enumerates exactly
 // these cells). The cell's own row is emitted first.
+// spans (optional): a work unit is a run of `span` cells along the last dim starting at
+// cells[w]; its rows then cover [c - 1, c + span] along that dim (the union of the cells'
+// neighbourhoods, a superset for every query of the run)
 template <bool FILL>
 __global__ void k_adj(const uint64_t* B, const uint2* G, uint64_t ncells, const uint32_t* cells,
                       uint64_t nc, uint32_t m, const uint64_t* cpd, const uint64_t* strides,
                       uint32_t* counts, const uint32_t* offs, uint2* adj,
-                      unsigned long long* csize) {
+                      unsigned long long* csize, const uint32_t* spans) {
     const uint64_t w = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (w >= nc) return;
@@ -1052,7 +1060,7 @@ __global__ void k_adj(const uint64_t* B, const uint2* G, uint64_t ncells, const 
     for (uint32_t j = 0; j < ml; ++j) R *= 3;
     const uint64_t own = (R - 1) / 2;
     const uint64_t lo_l = c[ml] > 0 ? c[ml] - 1 : 0;
-    const uint64_t hi_l = min(c[ml] + 1, cpd[ml] - 1);
+    const uint64_t hi_l = min(c[ml] + (spans ? spans[w] : 1u), cpd[ml] - 1);
     uint32_t written = 0;
     unsigned long long sz = 0;
     // process own row first (iteration -1), then all rows != own
@@ -1104,20 +1112,20 @@ __global__ void k_adj(const uint64_t* B, const uint2* G, uint64_t ncells, const 
 }
 void launch_adj_count(const uint64_t* B, uint64_t ncells, const uint32_t* cells, uint64_t nc,
                       uint32_t m, const uint64_t* cpd, const uint64_t* strides,
-                      uint32_t* counts, cudaStream_t s) {
+                      uint32_t* counts, cudaStream_t s, const uint32_t* spans) {
     if (!nc) return;
     k_adj<false><<<(unsigned)((nc * 32 + 255) / 256), 256, 0, s>>>(
-        B, nullptr, ncells, cells, nc, m, cpd, strides, counts, nullptr, nullptr, nullptr);
+        B, nullptr, ncells, cells, nc, m, cpd, strides, counts, nullptr, nullptr, nullptr, spans);
     KJ_CUDA(cudaGetLastError());
     g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 void launch_adj_fill(const uint64_t* B, const uint2* G, uint64_t ncells, const uint32_t* cells,
                      uint64_t nc, uint32_t m, const uint64_t* cpd, const uint64_t* strides,
                      const uint32_t* offs, uint2* adj, unsigned long long* csize,
-                     cudaStream_t s) {
+                     cudaStream_t s, const uint32_t* spans) {
     if (!nc) return;
     k_adj<true><<<(unsigned)((nc * 32 + 255) / 256), 256, 0, s>>>(
-        B, G, ncells, cells, nc, m, cpd, strides, nullptr, offs, adj, csize);
+        B, G, ncells, cells, nc, m, cpd, strides, nullptr, offs, adj, csize, spans);
     KJ_CUDA(cudaGetLastError());
     g_launches.fetch_add(1, std::memory_order_relaxed);
 }
@@ -1667,61 +1675,10 @@ __global__ void k_rows_to_host(const uint32_t* rows, uint64_t n, uint32_t K, con
         for (uint32_t i = lane; i < K; i += 32) hdist[base + i] = dist[base + i];
     }
 }
-// The same copy through the bulk-copy (TMA) engine: lanes stage a row in shared memory
-// with ordinary loads, one lane hands it to cp.async.bulk (shared -> mapped host). The
-// PCIe back-pressure then sits in the bulk-copy queue instead of the SM's load/store
-// pipeline that a concurrent join's epilogue shares. Rows need K % 4 == 0 (16-byte sizes).
-constexpr int RB = 8;  // row buffers per warp
-__global__ void __launch_bounds__(128) k_rows_to_host_bulk(const uint32_t* rows, uint64_t n, uint32_t K,
-                                                            const uint32_t* ids, const double* dist,
-                                                            uint32_t* hids, double* hdist) {
-    extern __shared__ __align__(128) unsigned char rb_smem[];
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const uint32_t row_bytes = K * 12;  // K ids then K doubles
-    unsigned char* mine = rb_smem + (size_t)wib * RB * row_bytes;
-    const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
-    uint32_t slot = 0;
-    for (uint64_t w = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w < n; w += nw) {
-        // the slot's previous bulk store must have read its data (RB - 1 may stay in flight)
-        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(RB - 1) : "memory");
-        __syncwarp();
-        const uint64_t base = (uint64_t)rows[w] * K;
-        uint32_t* si = reinterpret_cast<uint32_t*>(mine + slot * row_bytes);
-        double* sd = reinterpret_cast<double*>(si + K);
-        for (uint32_t i = lane; i < K; i += 32) si[i] = ids[base + i];
-        for (uint32_t i = lane; i < K; i += 32) sd[i] = dist[base + i];
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncwarp();
-        if (lane == 0) {
-            const unsigned sa = (unsigned)__cvta_generic_to_shared(si);
-            const unsigned sb = (unsigned)__cvta_generic_to_shared(sd);
-            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(hids + base),
-                         "r"(sa), "r"(K * 4)
-                         : "memory");
-            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(hdist + base),
-                         "r"(sb), "r"(K * 8)
-                         : "memory");
-            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-        }
-        slot = (slot + 1) % RB;
-    }
-    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-}
-
 void launch_rows_to_host(const uint32_t* rows, uint64_t n, uint32_t K, const uint32_t* ids,
                          const double* dist, uint32_t* hids, double* hdist, uint32_t max_blocks,
-                         cudaStream_t s, bool rows_bulk) {
+                         cudaStream_t s) {
     if (!n || !K) return;
-    const size_t sm = (size_t)4 * RB * K * 12;  // 4 warps per block
-    if (rows_bulk && K % 4 == 0 && sm <= 48 * 1024 &&
-        (reinterpret_cast<uintptr_t>(hids) & 15) == 0 && (reinterpret_cast<uintptr_t>(hdist) & 15) == 0) {
-        uint64_t blocks = (n * 32 + 127) / 128;
-        if (max_blocks) blocks = std::min<uint64_t>(blocks, 2ull * max_blocks);
-        k_rows_to_host_bulk<<<(unsigned)blocks, 128, sm, s>>>(rows, n, K, ids, dist, hids, hdist);
-        KJ_CUDA(cudaGetLastError());
-        g_launches.fetch_add(1, std::memory_order_relaxed);
-        return;
-    }
     uint64_t blocks = (n * 32 + 255) / 256;
     if (max_blocks) blocks = std::min<uint64_t>(blocks, max_blocks);
     k_rows_to_host<<<(unsigned)blocks, 256, 0, s>>>(rows, n, K, ids, dist, hids, hdist);

@@ -288,7 +288,11 @@ __global__ void __launch_bounds__(64 + 128 * G, 1)
     k_tc(const __grid_constant__ CUtensorMap tmB, TcJoinArgs p) {
     constexpr int NQ = 128 * G;                    // queries per block
     constexpr int BK = TN * 128;                   // bytes of one k-block of a candidate tile
-    constexpr int NB = (G == 2 ? 512 : 256) / (G * TN);  // accumulator buffers per group
+    // accumulator buffers per group: all 512 TMEM columns when the CTA has the SM to itself
+    // (G = 2, or a deep B ring whose shared memory admits one CTA); 256 for the two-per-SM
+    // shape (STAGES = 2). More buffers let a group's epilogue warps drift further apart
+    // (one warp's rare path no longer stalls the MMA into the next buffer).
+    constexpr int NB = (G == 2 || STAGES > 2 ? 512 : 256) / (G * TN);
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     // 1024-byte alignment for the 128B-swizzle atoms, staying in the shared state space
     unsigned char* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);

@@ -51,8 +51,8 @@ def test_streamed_results_identical(engine, oracle, spec, N, n, k):
         pd, dist = _pinned(lib, N * k, np.float64)
         pp, prov = _pinned(lib, N, np.uint8)
         ptrs = [pi, pd, pp]
-        for bulk in (1, 0):  # rows copied by cp.async.bulk, then by plain stores
-            engine.set_option("rows_bulk", bulk)
+        for cb in (74, 0):  # the row copy on a bounded grid, then one warp per row
+            engine.set_option("copy_blocks", cb)
             ids[:] = 0xFFFFFFFF
             dist[:] = -1.0
             engine.set_points(X)
@@ -63,7 +63,7 @@ def test_streamed_results_identical(engine, oracle, spec, N, n, k):
         c = engine.run(cfg, want_hist=False)
     finally:
         engine.set_option("chunk_min_rows", 65536)
-        engine.set_option("rows_bulk", 1)
+        engine.set_option("copy_blocks", 74)
         for p in ptrs:
             lib.knnj_free_pinned(p)
     for bi, bd, bp in got:
@@ -79,10 +79,14 @@ def test_streamed_results_identical(engine, oracle, spec, N, n, k):
     assert np.array_equal(bi[q], oi) and np.array_equal(bd[q], od)
 
 
-@pytest.mark.parametrize("spec,N,n,k,q", [("clusters:16:0.05", 40000, 18, 32, 990), ("uniform", 60000, 4, 32, 500),
-                                          ("exponential", 40000, 6, 40, 990), ("lattice", 30000, 4, 12, 900),
-                                          ("uniform", 50000, 2, 10, 300), ("mixture:8:0.05", 20000, 90, 16, 990)])
-def test_radius_bounded_pass_identical(engine, oracle, spec, N, n, k, q):
+@pytest.mark.parametrize("spec,N,n,k,q,grid", [("clusters:16:0.05", 40000, 18, 32, 990, 0),
+                                               ("uniform", 60000, 4, 32, 500, 0),
+                                               ("uniform", 60000, 4, 32, 500, 1),
+                                               ("exponential", 40000, 6, 40, 990, 1),
+                                               ("lattice", 30000, 4, 12, 900, 1),
+                                               ("uniform", 50000, 2, 10, 300, 1),
+                                               ("mixture:8:0.05", 20000, 90, 16, 990, 0)])
+def test_radius_bounded_pass_identical(engine, oracle, spec, N, n, k, q, grid):
     """The radius-bounded level-0 pass (the K-th of a query sample at quantile q bounds
     the box filter and the list cut; rows it misses are re-run without it) gives every
     row exactly the unbounded pass's output. Low quantiles force many misses."""
@@ -95,6 +99,7 @@ def test_radius_bounded_pass_identical(engine, oracle, spec, N, n, k, q):
     engine.set_option("bound_min_rows", 0)
     engine.set_option("bound_sample", 512)
     engine.set_option("kth_bound_q", q)
+    engine.set_option("bound_grid", grid)  # 1: the bounded pass on a grid of width ~B, cell runs
     try:
         engine.set_points(X)
         b = engine.run(cfg, want_hist=False)
@@ -102,6 +107,7 @@ def test_radius_bounded_pass_identical(engine, oracle, spec, N, n, k, q):
         engine.set_option("bound_min_rows", 200000)
         engine.set_option("bound_sample", 4096)
         engine.set_option("kth_bound_q", 999)
+        engine.set_option("bound_grid", 0)
     assert np.array_equal(b.ids, a.ids) and np.array_equal(b.dist, a.dist)
     assert np.array_equal(b.provenance, a.provenance)
     assert b.info["failed_count"] == a.info["failed_count"]
