@@ -1515,7 +1515,9 @@ struct knnj_ctx {
         // 32-thread blocks instead of mostly idle 128-thread ones. (Not in the fallback
         // levels: few queries against huge neighbourhoods are tile-load bound there, and
         // 128 threads load a tile 4x faster; measured on C4.)
-        if (chunk == (uint32_t)JB && K && !P.mixed && (&lv == &levels[0] || &lv >= &levels[40]) &&
+        // (SIMT passes only: a 128-query tensor-core shape, G = 1, also has chunk == JB)
+        if (chunk == (uint32_t)JB && K && !P.mixed && !tc_join_cfg(K, lv.prec_w).ok &&
+            (&lv == &levels[0] || &lv >= &levels[40]) &&
             double(nq) / double(std::max<uint64_t>(nuc, 1)) < 48.0) {
             chunk = 32;
             P.chunk = 32;
@@ -3519,6 +3521,7 @@ static void run_impl(knnj_ctx* c, const knnj_config* cfg, uint32_t shard, uint32
                                        h_ids_dev, h_dist_dev, &patch_rows, B2);
                 I.ms_join_kernel = c->last_join_kernel_ms;
                 I.join_screened_pairs = P.screened;
+                I.join_tensor_cores = c->last_join_tc ? 1 : 0;  // the main pass, not the retries
                 if (B2 > 0.0) {
                     // rows the bound missed: the unbounded level-0 pass over just those
                     DBuf<uint8_t> fl;
@@ -3561,7 +3564,7 @@ static void run_impl(knnj_ctx* c, const knnj_config* cfg, uint32_t shard, uint32
             }
             I.ms_join = t.ms();
             trace().mark("run: join");
-            I.join_tensor_cores = c->last_join_tc ? 1 : 0;
+            if (fine) I.join_tensor_cores = c->last_join_tc ? 1 : 0;
             // candidates_examined counts dense queries only (DenseJoinStats), over level 0's walk
             const Pass& Pw = fine_grid ? P0 : P;
             I.candidates_examined = have_dense ? Pw.candidates_dense : Pw.candidates;

@@ -284,7 +284,7 @@ __device__ __noinline__ uint32_t exact_bin(const double* X64, uint32_t n, uint32
 // warp issues just those (n = 4: one UMMA per tile instead of four).
 // TN = 64: wide operands (KB >= 3), so that A + the B ring fit in shared memory.
 template <int KB, int G, int STAGES, bool HIST, int LR, int TN = 128>
-__global__ void __launch_bounds__(64 + 128 * G, 1)
+__global__ void __launch_bounds__(32 * (1 + G) + 128 * G, 1)
     k_tc(const __grid_constant__ CUtensorMap tmB, TcJoinArgs p) {
     constexpr int NQ = 128 * G;                    // queries per block
     constexpr int BK = TN * 128;                   // bytes of one k-block of a candidate tile
@@ -328,7 +328,11 @@ __global__ void __launch_bounds__(64 + 128 * G, 1)
     }
 
     // epilogue identity
-    const int e = warp - 2;                      // epilogue warp index (valid if >= 0)
+    // warp 0: TMA producer; warps 1 .. G: MMA issuers (one per query group, so a group
+    // waiting on its epilogue never stalls the other's issue through lane divergence);
+    // then 4 epilogue warps per group (any 4 consecutive warps cover the 4 TMEM lane quarters)
+    constexpr int NSPEC = 1 + G;
+    const int e = warp - NSPEC;                  // epilogue warp index (valid if >= 0)
     const int g = e >= 0 ? e >> 2 : 0;           // query group
     const int quarter = warp & 3;                // TMEM lane quarter this warp may access
     const uint32_t r = quarter * 32 + lane;      // accumulator row (= TMEM lane)
@@ -449,12 +453,12 @@ __global__ void __launch_bounds__(64 + 128 * G, 1)
                     tma_load_2d(sB + (st * KB + kb) * BK, &tmB, &bar_full[st], kb * KBLK, (int)s);
             }
         }
-    } else if (warp == 1) {
+    } else if (warp <= G) {
         // ------------------------------------------------ MMA issuer
-        // one issuing lane per query group: a group whose epilogue is in its rare path
+        // one issuing warp per query group: a group whose epilogue is in its rare path
         // holds only its own accumulators; the other runs ahead within the stage ring
-        if (lane < G) {
-            const int gg = lane;
+        if (lane == 0) {
+            const int gg = warp - 1;
             uint32_t s, c;
             const uint32_t a0 = smem_u32(sA);
             for (uint32_t t = 0; next_tile(s, c); ++t) {
@@ -826,7 +830,7 @@ static void launch_tc_t(const TcJoinArgs& a, uint64_t nitems, uint64_t N, cudaSt
         const uint64_t cnt = std::min<uint64_t>(nitems - off, 2147483647ull);
         TcJoinArgs b = a;
         b.items = a.items + off;
-        k_tc<KB, G, STAGES, HIST, LR, TN><<<(unsigned)cnt, 64 + 128 * G, sm, s>>>(map, b);
+        k_tc<KB, G, STAGES, HIST, LR, TN><<<(unsigned)cnt, 32 * (1 + G) + 128 * G, sm, s>>>(map, b);
     }
     KJ_CUDA(cudaGetLastError());
     g_launches.fetch_add(1, std::memory_order_relaxed);
