@@ -1218,6 +1218,7 @@ struct knnj_ctx {
     bool bound_grid = false;
     double bound_grid_frac = 0.8;    // ... when B is below this fraction of level 0's width
     uint32_t bound_group_span = 8;   // ... with cell runs of up to this many cells
+    uint32_t level0_group_span = 0;  // cell runs in the level-0 pass (0/1: one cell per item)
     uint32_t bound_sample = 4096;
     uint32_t kth_bound_q = 999;
     double bound_max_frac = 0.8;
@@ -2696,6 +2697,9 @@ int knnj_set_option(knnj_ctx* c, const char* name, int64_t value) {
             c->kth_bound = value != 0;
         } else if (k == "bound_grid") {
             c->bound_grid = value != 0;
+        } else if (k == "level0_group_span") {
+            if (value < 0 || value > 64) throw Error(1, "level0_group_span must be in [0, 64]");
+            c->level0_group_span = (uint32_t)value;
         } else if (k == "bound_group_span") {
             if (value < 1 || value > 64) throw Error(1, "bound_group_span must be in [1, 64]");
             c->bound_group_span = (uint32_t)value;
@@ -3505,7 +3509,7 @@ static void run_impl(knnj_ctx* c, const knnj_config* cfg, uint32_t shard, uint32
                 } else {
                     c->build_pass(lv0, d_q.p, d_rows.p, nq, P, k_eff, shard, nshard,
                                   have_dense ? d_dense.p : nullptr, B2 > 0.0 ? B2 : filt0, B2 <= 0.0,
-                                  all_points);
+                                  all_points, nullptr, c->level0_group_span);
                 }
                 c->stream_chunks = 1;
                 I.ms_join_build = tb.ms();

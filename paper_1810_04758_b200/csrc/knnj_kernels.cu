@@ -326,6 +326,7 @@ __device__ __forceinline__ void finalize_status(const FinalArgs& a, uint32_t c, 
     if (a.out_count) a.out_count[orow] = min(c, a.K);
 }
 
+template <int EMAX>
 __device__ __forceinline__ void finalize_row(const FinalArgs& a, uint64_t row, int lane) {
     const uint32_t c = a.cnt[row];
     if (c == SKIP) return;  // a split row: its parts are finalized and merged separately
@@ -336,7 +337,6 @@ __device__ __forceinline__ void finalize_row(const FinalArgs& a, uint64_t row, i
     }
     const uint32_t qp = a.qpos[row];
     const double* qx = a.XJ ? a.XJ + (uint64_t)qp * a.n : a.X64 + (uint64_t)a.A[qp] * a.n;
-    constexpr int EMAX = 8;
     double sq[EMAX];
     uint32_t id[EMAX];
     uint32_t rk[EMAX];
@@ -361,7 +361,13 @@ __device__ __forceinline__ void finalize_row(const FinalArgs& a, uint64_t row, i
         case EE:                                           \
             rank_entries<EE, EMAX>(sq, id, rk, c);         \
             break;
-        KJ_RANK(1) KJ_RANK(2) KJ_RANK(3) KJ_RANK(4) KJ_RANK(5) KJ_RANK(6) KJ_RANK(7) KJ_RANK(8)
+        KJ_RANK(1) KJ_RANK(2)
+        case 3: if constexpr (EMAX >= 3) rank_entries<3, EMAX>(sq, id, rk, c); break;
+        case 4: if constexpr (EMAX >= 4) rank_entries<4, EMAX>(sq, id, rk, c); break;
+        case 5: if constexpr (EMAX >= 5) rank_entries<5, EMAX>(sq, id, rk, c); break;
+        case 6: if constexpr (EMAX >= 6) rank_entries<6, EMAX>(sq, id, rk, c); break;
+        case 7: if constexpr (EMAX >= 7) rank_entries<7, EMAX>(sq, id, rk, c); break;
+        case 8: if constexpr (EMAX >= 8) rank_entries<8, EMAX>(sq, id, rk, c); break;
 #undef KJ_RANK
         default: break;
     }
@@ -383,11 +389,14 @@ __device__ __forceinline__ void finalize_row(const FinalArgs& a, uint64_t row, i
 }
 
 // Warps stride over the launch rows (a bounded grid shares the SMs with a running join).
+// EMAX = list entries per lane: 2 for lists of at most 64 (fewer registers, more warps in
+// flight for the gathers), else 8.
+template <int EMAX>
 __global__ void k_finalize(FinalArgs a) {
     const int lane = threadIdx.x & 31;
     const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
     for (uint64_t w = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w < a.nrows; w += nw)
-        finalize_row(a, w, lane);
+        finalize_row<EMAX>(a, w, lane);
 }
 
 // ---------------------------------------------------------------- histogram
@@ -597,7 +606,8 @@ void launch_finalize(const FinalArgs& a, cudaStream_t s, uint32_t max_blocks) {
     if (a.nrows == 0) return;
     uint64_t blocks = (a.nrows * 32 + 255) / 256;
     if (max_blocks) blocks = std::min<uint64_t>(blocks, max_blocks);
-    k_finalize<<<(unsigned)blocks, 256, 0, s>>>(a);
+    if (a.L <= 64) k_finalize<2><<<(unsigned)blocks, 256, 0, s>>>(a);
+    else k_finalize<8><<<(unsigned)blocks, 256, 0, s>>>(a);
     KJ_CUDA(cudaGetLastError());
     g_launches.fetch_add(1, std::memory_order_relaxed);
 }
