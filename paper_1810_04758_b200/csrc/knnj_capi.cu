@@ -708,12 +708,13 @@ struct knnj_ctx {
         const uint32_t m = std::min<uint32_t>(n, 6);
         const double w = std::sqrt(r2) * (1.0 + 1e-9);
         p1 = std::min<uint64_t>(p1, N);
-        const bool slice = p0 != 0 || p1 != N;
+        // queries go by id (their cell from the coordinates): the grid then needs no
+        // point -> cell / position tables (two scattered N-element writes per build)
         Timer tb(s);
         // a grid built for a slightly larger radius (the pilot's) serves this one too
         if (!(hist_lv.built && hist_lv.m == m && hist_lv.w >= w && hist_lv.w <= 1.2 * w &&
               hist_p0 == p0 && hist_p1 == p1)) {
-            grid_tables_into(hist_lv, m, w, p0, p1);
+            grid_tables_into(hist_lv, m, w, p0, p1, false);
             hist_Xs.ensure((uint64_t)n * Npad);
             launch_gather_soa(Xf.p, hist_lv.A.p, hist_lv.npts, n, Npad, hist_Xs.p, s);
             hist_mins.ensure(m);
@@ -722,30 +723,27 @@ struct knnj_ctx {
             hist_p0 = p0;
             hist_p1 = p1;
         }
-        // queries in the grid's sorted order (neighbouring warps share candidate rows); a
-        // slice grid does not hold them: they go by id
-        DBuf<uint32_t> qp_u, qp;
-        if (!slice) {
-            qp_u.ensure(nq);
-            qp.ensure(nq);
-            launch_map_u32(d_q, hist_lv.posOf.p, nq, qp_u.p, s);
-            size_t bytes = 0;
-            KJ_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, bytes, qp_u.p, qp.p, (int64_t)nq, 0,
-                                                   bits_for(N), s));
-            KJ_CUDA(cub::DeviceRadixSort::SortKeys(sc.get(bytes), bytes, qp_u.p, qp.p, (int64_t)nq, 0,
-                                                   bits_for(N), s));
-        }
         DBuf<uint64_t> d_cs;
         d_cs.ensure(2 * m);
         KJ_CUDA(cudaMemcpyAsync(d_cs.p, hist_lv.cpd.data(), 8 * m, cudaMemcpyHostToDevice, s));
         KJ_CUDA(cudaMemcpyAsync(d_cs.p + m, hist_lv.strides.data(), 8 * m, cudaMemcpyHostToDevice, s));
+        // queries sorted by their cell (neighbouring warps share candidate rows)
+        DBuf<uint32_t> qs;
+        {
+            DBuf<uint64_t> kq, kq2;
+            kq.ensure(nq);
+            kq2.ensure(nq);
+            qs.ensure(nq);
+            launch_id_cell_keys(X64.p, d_q, nq, n, m, hist_mins.p, hist_lv.w, d_cs.p, d_cs.p + m, kq.p, s);
+            sort_pairs_u64_u32(sc, kq.p, kq2.p, d_q, qs.p, nq, hist_lv.key_bits, s);
+        }
         last_hist_grid_build_ms = tb.ms();
         HistGridArgs a{};
         a.Xs = hist_Xs.p;
         a.Npad = Npad;
         a.X64 = X64.p;
         a.A = hist_lv.A.p;
-        a.slot = hist_lv.slot.p;
+        a.slot = nullptr;
         a.B = hist_lv.B.p;
         a.G = hist_lv.G.p;
         a.ncells = hist_lv.ncells;
@@ -753,14 +751,12 @@ struct knnj_ctx {
         a.strides = d_cs.p + m;
         a.n = n;
         a.m = m;
-        a.qpos = slice ? nullptr : qp.p;
+        a.qpos = nullptr;
         a.nq = nq;
-        if (slice) {
-            a.qids = d_q;
-            a.Xf = Xf.p;
-            a.mins = hist_mins.p;
-            a.w = hist_lv.w;
-        }
+        a.qids = qs.p;
+        a.Xf = Xf.p;
+        a.mins = hist_mins.p;
+        a.w = hist_lv.w;
         a.n_bins = h.n_bins;
         a.n_count = h.n_count;
         a.SU = h.SU;
@@ -1080,7 +1076,8 @@ struct knnj_ctx {
     // GridIndex::build's tables (grid_index.cpp:13-75) for lv: B, G, A, slot, posOf
     // Grid tables over the points with ids in [p0, p1) (default all; a slice for the
     // candidate-split histogram of sharded runs). Cell geometry from all points.
-    void grid_tables_into(Level& lv, uint32_t m, double w, uint64_t p0 = 0, uint64_t p1 = ~0ull) {
+    void grid_tables_into(Level& lv, uint32_t m, double w, uint64_t p0 = 0, uint64_t p1 = ~0ull,
+                          bool point_tables = true) {
         p1 = std::min<uint64_t>(p1, N);
         const uint64_t cnt = p1 > p0 ? p1 - p0 : 0;
         lv.built = false;
@@ -1155,10 +1152,13 @@ struct knnj_ctx {
         lv.ncells = nruns;
         lv.B.ensure(nruns);
         lv.G.ensure(nruns);
-        lv.slot.ensure(N);
-        lv.posOf.ensure(N);
+        if (point_tables) {
+            lv.slot.ensure(N);
+            lv.posOf.ensure(N);
+        }
         if (cnt)
-            launch_grid_tables(skeys.p, lv.A.p, runidx.p, cnt, lv.B.p, lv.G.p, lv.slot.p, lv.posOf.p, s);
+            launch_grid_tables(skeys.p, lv.A.p, runidx.p, cnt, lv.B.p, lv.G.p,
+                               point_tables ? lv.slot.p : nullptr, point_tables ? lv.posOf.p : nullptr, s);
         lv.npts = cnt;
         lv.bbox_ready = lv.xj_ready = lv.xs_ready = lv.tc_ready = false;
     }
@@ -1218,7 +1218,8 @@ struct knnj_ctx {
     bool bound_grid = false;
     double bound_grid_frac = 0.8;    // ... when B is below this fraction of level 0's width
     uint32_t bound_group_span = 8;   // ... with cell runs of up to this many cells
-    uint32_t level0_group_span = 0;  // cell runs in the level-0 pass (0/1: one cell per item)
+    // cell runs in the level-0 pass when cells hold few queries (C4: 3.92 -> 3.47 s; 0/1 off)
+    uint32_t level0_group_span = 8;
     uint32_t bound_sample = 4096;
     uint32_t kth_bound_q = 999;
     double bound_max_frac = 0.8;
@@ -1529,7 +1530,24 @@ struct knnj_ctx {
         // over [c_first - 1, c_last + 1] in the last dim), a superset for each query. A
         // fine grid holds few queries per cell; runs fill the item's 128-query tiles.
         DBuf<uint32_t> uspan;
-        if (group_span > 1 && nuc > 1) {
+        DBuf<unsigned long long> rowwalk;  // cell runs: each row's own-cell walk (the counters)
+        if (group_span > 1 && nuc > 1 && 2 * nq < (uint64_t)chunk * nuc) {
+            // the reference's walk counters stay per cell: each launch row's own-cell
+            // neighbourhood size, before the cells are merged into runs
+            {
+                DBuf<uint64_t> d_cs0;
+                d_cs0.ensure(2 * lv.m);
+                KJ_CUDA(cudaMemcpyAsync(d_cs0.p, lv.cpd.data(), 8 * lv.m, cudaMemcpyHostToDevice, s));
+                KJ_CUDA(cudaMemcpyAsync(d_cs0.p + lv.m, lv.strides.data(), 8 * lv.m, cudaMemcpyHostToDevice, s));
+                DBuf<uint32_t> cnt0;
+                DBuf<unsigned long long> cs0;
+                cnt0.ensure(nuc);
+                cs0.ensure(nuc);
+                launch_adj_count(lv.B.p, lv.ncells, ucell.p, nuc, lv.m, d_cs0.p, d_cs0.p + lv.m, cnt0.p, s,
+                                 nullptr, lv.G.p, cs0.p);
+                rowwalk.ensure(nq);
+                launch_row_walk(ufirst.p, ucnt.p, nuc, cs0.p, rowwalk.p, s);
+            }
             std::vector<uint32_t> h_cell(nuc);
             KJ_CUDA(cudaMemcpyAsync(h_cell.data(), ucell.p, 4 * nuc, cudaMemcpyDeviceToHost, s));
             sync();
@@ -1625,7 +1643,18 @@ struct knnj_ctx {
         }
         const uint32_t r0 = i0 < i1 ? h_items[i0].x : 0;
         const uint32_t r1 = i0 < i1 ? h_items[i1 - 1].y : 0;
-        if (d_dense && i0 < i1) {
+        unsigned long long walk_all = 0;
+        if (rowwalk.p && i0 < i1) {  // cell runs: the per-cell walk of the owned rows
+            DBuf<unsigned long long> d_w;
+            d_w.ensure(2);
+            KJ_CUDA(cudaMemsetAsync(d_w.p, 0, 16, s));
+            launch_walk_sum(rowwalk.p + r0, P.qrow.p + r0, r1 - r0, d_dense, d_w.p, s);
+            unsigned long long hw[2] = {0, 0};
+            KJ_CUDA(cudaMemcpyAsync(hw, d_w.p, 16, cudaMemcpyDeviceToHost, s));
+            sync();
+            walk_all = hw[0];
+            if (d_dense) P.candidates_dense = hw[1];
+        } else if (d_dense && i0 < i1) {
             DBuf<unsigned long long> d_dc;
             d_dc.ensure(1);
             KJ_CUDA(cudaMemsetAsync(d_dc.p, 0, 8, s));
@@ -1645,6 +1674,8 @@ struct knnj_ctx {
             own[i].y -= r0;
             cand += own_w[i];
         }
+        const unsigned long long work_pairs = cand;  // pairs the items cover (runs: unions)
+        if (rowwalk.p) cand = walk_all;             // the reference walk's count
         const uint64_t nq_own = r1 - r0;
         // Split items whose candidate set is a large slice of the pass (few queries
         // against huge neighbourhoods: fallback passes, skewed cells) into parts over
@@ -1803,7 +1834,7 @@ struct knnj_ctx {
             KJ_CUDA(cudaMemcpyAsync(P.items.p, h_sorted.data(), 16 * P.nitems, cudaMemcpyHostToDevice, s));
         sync();
         P.candidates = cand;
-        P.screened = cand;
+        P.screened = work_pairs;
         if (filter_r2 > 0.0 && box_filter && P.nitems) {
             // rows that carry an upper bound U on their K-th sq (fallback levels: K points
             // within sqrt(U) are known to exist) need no candidate beyond sqrt(U): an item

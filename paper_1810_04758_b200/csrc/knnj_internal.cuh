@@ -340,7 +340,8 @@ void launch_map_u32(const uint32_t* idx, const uint32_t* table, uint64_t n, uint
                     cudaStream_t s);
 void launch_adj_count(const uint64_t* B, uint64_t ncells, const uint32_t* cells, uint64_t nc,
                       uint32_t m, const uint64_t* cpd, const uint64_t* strides,
-                      uint32_t* counts, cudaStream_t s, const uint32_t* spans = nullptr);
+                      uint32_t* counts, cudaStream_t s, const uint32_t* spans = nullptr,
+                      const uint2* G = nullptr, unsigned long long* csize = nullptr);
 void launch_adj_fill(const uint64_t* B, const uint2* G, uint64_t ncells, const uint32_t* cells,
                      uint64_t nc, uint32_t m, const uint64_t* cpd, const uint64_t* strides,
                      const uint32_t* offs, uint2* adj, unsigned long long* csize,
@@ -400,6 +401,13 @@ void launch_item_delta(const uint4* items, const float* r2, uint64_t nitems, dou
                        uint8_t* tc_ok, cudaStream_t s);
 void launch_item_max_cut(const uint4* items, uint64_t nitems, const uint32_t* qrow, uint64_t nq,
                          const uint32_t* vsrc, const float* cut_by_row, float* out, cudaStream_t s);
+void launch_row_walk(const uint32_t* ufirst, const uint32_t* ucnt, uint64_t nuc,
+                     const unsigned long long* csize, unsigned long long* rowwalk, cudaStream_t s);
+void launch_walk_sum(const unsigned long long* rowwalk, const uint32_t* qrow, uint64_t n,
+                     const uint8_t* dense, unsigned long long* out, cudaStream_t s);
+void launch_id_cell_keys(const double* X, const uint32_t* ids, uint64_t cnt, uint32_t n, uint32_t m,
+                         const double* mins, double w, const uint64_t* cpd, const uint64_t* strides,
+                         uint64_t* keys, cudaStream_t s);
 void launch_range_len(const uint2* r, uint64_t n, uint32_t* out, cudaStream_t s);  // out = y - x
 void launch_miss_flags(const uint32_t* rows, uint64_t n, const uint8_t* st, uint8_t* flags,
                        cudaStream_t s);

@@ -953,6 +953,33 @@ __global__ void k_cell_keys(const double* X, uint64_t N, uint32_t n, uint32_t m,
         vals[i] = base + (uint32_t)i;
     }
 }
+// cell keys of arbitrary points (ids), same rule as k_cell_keys
+__global__ void k_id_cell_keys(const double* X, const uint32_t* ids, uint64_t cnt, uint32_t n, uint32_t m,
+                               const double* mins, double w, const uint64_t* cpd,
+                               const uint64_t* strides, uint64_t* keys) {
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < cnt;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const double* x = X + (uint64_t)ids[i] * n;
+        uint64_t id = 0;
+        for (uint32_t j = 0; j < m; ++j) {
+            double rel = __ddiv_rn(__dsub_rn(x[j], mins[j]), w);
+            if (rel < 0.0) rel = 0.0;
+            uint64_t idx = (uint64_t)floor(rel);
+            if (idx > cpd[j] - 1) idx = cpd[j] - 1;
+            id += idx * strides[j];
+        }
+        keys[i] = id;
+    }
+}
+void launch_id_cell_keys(const double* X, const uint32_t* ids, uint64_t cnt, uint32_t n, uint32_t m,
+                         const double* mins, double w, const uint64_t* cpd, const uint64_t* strides,
+                         uint64_t* keys, cudaStream_t s) {
+    if (!cnt) return;
+    k_id_cell_keys<<<(unsigned)std::min<uint64_t>((cnt + 255) / 256, 2368), 256, 0, s>>>(
+        X, ids, cnt, n, m, mins, w, cpd, strides, keys);
+    KJ_CUDA(cudaGetLastError());
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+}
 void launch_cell_keys(const double* X, uint64_t N, uint32_t n, uint32_t m, const double* mins,
                       double w, const uint64_t* cpd, const uint64_t* strides, uint64_t* keys,
                       uint32_t* vals, cudaStream_t s, uint32_t base) {
@@ -996,8 +1023,8 @@ __global__ void k_grid_tables(const uint64_t* skeys, const uint32_t* A, const ui
             G[r].x = (uint32_t)i;
         }
         if (i == N - 1 || skeys[i + 1] != k) G[r].y = (uint32_t)(i + 1);
-        slot[A[i]] = r;
-        posOf[A[i]] = (uint32_t)i;
+        if (slot) slot[A[i]] = r;          // (scattered writes: skipped when not needed)
+        if (posOf) posOf[A[i]] = (uint32_t)i;
     }
 }
 void launch_grid_tables(const uint64_t* skeys, const uint32_t* A, const uint32_t* runidx,
@@ -1102,7 +1129,7 @@ __global__ void k_adj(const uint64_t* B, const uint2* G, uint64_t ncells, const 
                 const uint64_t s_hi = lower_bound_u64(B, ncells, row + hi_l + 1);
                 if (s_lo < s_hi) {
                     valid = true;
-                    rng = make_uint2(G[s_lo].x, G[s_hi - 1].y);
+                    if (G) rng = make_uint2(G[s_lo].x, G[s_hi - 1].y);  // (count pass: may be null)
                 }
             }
         }
@@ -1117,15 +1144,57 @@ __global__ void k_adj(const uint64_t* B, const uint2* G, uint64_t ncells, const 
     for (int o = 16; o > 0; o >>= 1) sz += __shfl_xor_sync(0xffffffffu, sz, o);
     if (lane == 0) {
         if (!FILL) counts[w] = written;
-        else if (csize) csize[w] = sz;
+        if (csize) csize[w] = sz;
     }
+}
+// Per launch row (cells' rows contiguous from ufirst): its cell's neighbourhood size.
+__global__ void k_row_walk(const uint32_t* ufirst, const uint32_t* ucnt, uint64_t nuc,
+                           const unsigned long long* csize, unsigned long long* rowwalk) {
+    for (uint64_t u = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; u < nuc;
+         u += uint64_t(gridDim.x) * blockDim.x)
+        for (uint32_t i = 0; i < ucnt[u]; ++i) rowwalk[ufirst[u] + i] = csize[u];
+}
+// sums of rowwalk over n rows: all (out[0]) and those whose output row is dense (out[1])
+__global__ void k_walk_sum(const unsigned long long* rowwalk, const uint32_t* qrow, uint64_t n,
+                           const uint8_t* dense, unsigned long long* out) {
+    unsigned long long a = 0, d = 0;
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        a += rowwalk[i];
+        if (dense && dense[qrow[i]]) d += rowwalk[i];
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        a += __shfl_xor_sync(0xffffffffu, a, o);
+        d += __shfl_xor_sync(0xffffffffu, d, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(out, a);
+        atomicAdd(out + 1, d);
+    }
+}
+void launch_row_walk(const uint32_t* ufirst, const uint32_t* ucnt, uint64_t nuc,
+                     const unsigned long long* csize, unsigned long long* rowwalk, cudaStream_t s) {
+    if (!nuc) return;
+    k_row_walk<<<(unsigned)std::min<uint64_t>((nuc + 255) / 256, 148 * 16), 256, 0, s>>>(ufirst, ucnt, nuc,
+                                                                                         csize, rowwalk);
+    KJ_CUDA(cudaGetLastError());
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+void launch_walk_sum(const unsigned long long* rowwalk, const uint32_t* qrow, uint64_t n,
+                     const uint8_t* dense, unsigned long long* out, cudaStream_t s) {
+    if (!n) return;
+    k_walk_sum<<<(unsigned)std::min<uint64_t>((n + 255) / 256, 148 * 8), 256, 0, s>>>(rowwalk, qrow, n,
+                                                                                      dense, out);
+    KJ_CUDA(cudaGetLastError());
+    g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 void launch_adj_count(const uint64_t* B, uint64_t ncells, const uint32_t* cells, uint64_t nc,
                       uint32_t m, const uint64_t* cpd, const uint64_t* strides,
-                      uint32_t* counts, cudaStream_t s, const uint32_t* spans) {
+                      uint32_t* counts, cudaStream_t s, const uint32_t* spans, const uint2* G,
+                      unsigned long long* csize) {
     if (!nc) return;
     k_adj<false><<<(unsigned)((nc * 32 + 255) / 256), 256, 0, s>>>(
-        B, nullptr, ncells, cells, nc, m, cpd, strides, counts, nullptr, nullptr, nullptr, spans);
+        B, G, ncells, cells, nc, m, cpd, strides, counts, nullptr, nullptr, csize, spans);
     KJ_CUDA(cudaGetLastError());
     g_launches.fetch_add(1, std::memory_order_relaxed);
 }
@@ -1997,15 +2066,18 @@ __global__ void k_filter_ranges(uint4* items, uint64_t nitems, const float* qbox
         if (lane == 0 && span) atomicAdd(screened, span * (unsigned long long)(it.y - it.x));
     }
     if (want_r) {
-        // grid dims d < r_m: every candidate lies in the 3^m cells around the item's cell,
-        // i.e. within [qh - 2w, ql + 2w] (the cell holds the query box); the other dims:
-        // the kept blocks' boxes (and the query box)
+        // grid dims d < r_m: every candidate lies in the cells next to a query's cell. In
+        // the dims where all the item's queries share one cell coordinate (all but the last:
+        // an item is one cell or a run of cells along the last dim) that is within
+        // [qh - 2w, ql + 2w]; along the last dim within [ql - 2w, qh + 2w]. The other dims:
+        // the kept blocks' boxes (and the query box). All clipped to the data range (dbox).
         for (int o = 16; o > 0; o >>= 1) rmax = fmaxf(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
         if (lane == 0) {
             float low = 0.f;
-            for (uint32_t d = 0; d < r_m; ++d) {  // ... and inside the data range (dbox)
-                const float lo = fmaxf(__fsub_rd(qh[d], r_2w), dbox[d]);
-                const float hi = fminf(__fadd_ru(ql[d], r_2w), dbox[r_m + d]);
+            for (uint32_t d = 0; d < r_m; ++d) {
+                const bool run_dim = d + 1 == r_m;
+                const float lo = fmaxf(__fsub_rd(run_dim ? ql[d] : qh[d], r_2w), dbox[d]);
+                const float hi = fminf(__fadd_ru(run_dim ? qh[d] : ql[d], r_2w), dbox[r_m + d]);
                 const float r = fmaxf(fmaxf(__fsub_ru(gbox[n + d], lo), __fsub_ru(hi, gbox[d])), 0.f);
                 low = __fadd_ru(low, __fmul_ru(r, r));
             }
