@@ -302,9 +302,15 @@ struct knnj_ctx {
 
     DBuf<float> d_gbox;            // g rounded down [n], then up [n]
     cudaStream_t s_out = nullptr;  // result D2H overlapping the fallback (knnj_run)
+    cudaEvent_t ev_copy = nullptr; // a streamed row copy on s_out still pending (copy_pending)
+    bool copy_pending = false;
+    DBuf<uint32_t> st_keys;        // its sorted rows and sort scratch
+    DBuf<unsigned char> st_tmp;
     cudaEvent_t ev_out = nullptr;
     ~knnj_ctx() {
         if (sample_work) sample_work_free(sample_work);
+        if (s_out) cudaStreamSynchronize(s_out);
+        if (ev_copy) cudaEventDestroy(ev_copy);
         if (ev_out) cudaEventDestroy(ev_out);
         if (s_out) cudaStreamDestroy(s_out);
         if (h_sq) cudaFreeHost(h_sq);
@@ -1220,6 +1226,7 @@ struct knnj_ctx {
     uint32_t bound_group_span = 8;   // ... with cell runs of up to this many cells
     // cell runs in the level-0 pass when cells hold few queries (C4: 3.92 -> 3.47 s; 0/1 off)
     uint32_t level0_group_span = 8;
+    uint32_t fallback_group_span = 8;  // ... and in the fallback levels (few rows per cell)
     uint32_t bound_sample = 4096;
     uint32_t kth_bound_q = 999;
     double bound_max_frac = 0.8;
@@ -2106,15 +2113,19 @@ struct knnj_ctx {
         // the host are taken in ascending output row (sorted per chunk on s_out)
         uint64_t maxlen = 0;
         for (size_t c = 0; c < nch; ++c) maxlen = std::max<uint64_t>(maxlen, cr[c + 1] - cr[c]);
-        DBuf<uint32_t> o_keys;
-        DBuf<unsigned char> o_tmpbuf;
+        // (context buffers: a copy may still run on s_out after this pass returns)
+        DBuf<uint32_t>& o_keys = st_keys;
         void* o_tmp = nullptr;
         size_t o_tmp_bytes = 0;
         if (to_host) {
+            if (copy_pending) {  // an earlier pass's copy still owns the buffers
+                KJ_CUDA(cudaStreamSynchronize(s_out));
+                copy_pending = false;
+            }
             o_keys.ensure(maxlen);
             KJ_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, o_tmp_bytes, P.qrow.p, o_keys.p,
                                                    (int64_t)maxlen, 0, bits_for(N), s));
-            o_tmp = o_tmpbuf.ensure(o_tmp_bytes);
+            o_tmp = st_tmp.ensure(o_tmp_bytes);
         }
         // the finalize of launch rows [cr[c], cr[c+1]) into the device rows, then (to_host)
         // the chunk's rows to the host in ascending output row
@@ -2335,7 +2346,20 @@ struct knnj_ctx {
             KJ_CUDA(cudaEventRecord(ev_fin, s_out));
             KJ_CUDA(cudaStreamWaitEvent(s, ev_fin, 0));
         } else if (to_host) {
-            finalize_chunk(0, s);
+            // one launch: the device finalize on s, then the sorted row copy on s_out so
+            // it overlaps whatever follows (the fallback); run_impl waits before patching
+            launch_finalize(f, s);
+            ensure_out_stream();
+            KJ_CUDA(cudaEventRecord(ev_out, s));
+            KJ_CUDA(cudaStreamWaitEvent(s_out, ev_out, 0));
+            size_t bytes = o_tmp_bytes;
+            KJ_CUDA(cub::DeviceRadixSort::SortKeys(o_tmp, bytes, P.qrow.p, o_keys.p, (int64_t)P.nq, 0,
+                                                   bits_for(N), s_out));
+            launch_rows_to_host(o_keys.p, P.nq, K, out_ids, out_dist, host_ids, host_dist, copy_blocks,
+                                s_out);
+            if (!ev_copy) KJ_CUDA(cudaEventCreateWithFlags(&ev_copy, cudaEventDisableTiming));
+            KJ_CUDA(cudaEventRecord(ev_copy, s_out));
+            copy_pending = true;
         } else {
             launch_finalize(f, s);
         }
@@ -2539,7 +2563,7 @@ struct knnj_ctx {
             launch_scatter_f32(d_r.p, d_cut.p, np, d_cut_by_row.p, s);
             Pass P;
             build_pass(lv, d_p.p, d_r.p, np, P, K, 0, 1, nullptr, filter_radius2(lv), true, false,
-                       item_radius ? d_cut_by_row.p : nullptr);
+                       item_radius ? d_cut_by_row.p : nullptr, fallback_group_span);
             trace().mark("levels: build_pass", s);
             launch_gather_f32(P.qrow.p, d_cut_by_row.p, np, d_cut.p, s);
             run_pass(lv, P, K, d_cut.p, -1.0, cov2, out_ids, out_dist, out_kth, out_status, n_slow);
@@ -2728,6 +2752,9 @@ int knnj_set_option(knnj_ctx* c, const char* name, int64_t value) {
             c->kth_bound = value != 0;
         } else if (k == "bound_grid") {
             c->bound_grid = value != 0;
+        } else if (k == "fallback_group_span") {
+            if (value < 0 || value > 64) throw Error(1, "fallback_group_span must be in [0, 64]");
+            c->fallback_group_span = (uint32_t)value;
         } else if (k == "level0_group_span") {
             if (value < 0 || value > 64) throw Error(1, "level0_group_span must be in [0, 64]");
             c->level0_group_span = (uint32_t)value;
@@ -3223,11 +3250,12 @@ static void run_impl(knnj_ctx* c, const knnj_config* cfg, uint32_t shard, uint32
     uint32_t* h_ids_dev = nullptr;       // device views of the mapped host outputs
     double* h_dist_dev = nullptr;
     std::vector<uint32_t> patch_rows;    // rows rewritten after the streamed finalize
-    struct OutSync {  // an early result copy never outlives the call (errors included)
+    struct OutSync {  // an early / streamed result copy never outlives the call (errors included)
         knnj_ctx* c;
         const bool& on;
         ~OutSync() {
-            if (on && c->s_out) cudaStreamSynchronize(c->s_out);
+            if ((on || c->copy_pending) && c->s_out) cudaStreamSynchronize(c->s_out);
+            c->copy_pending = false;
         }
     } out_sync{c, early_started};
     // host-side reference RNG streams (pairs for eps_mean, the histogram's query sample)
@@ -3691,6 +3719,10 @@ static void run_impl(knnj_ctx* c, const knnj_config* cfg, uint32_t shard, uint32
     {
         Timer t(s);
         if (nshard == 1 && streamed) {
+            if (c->copy_pending) {  // the level-0 row copy must land before the patch
+                KJ_CUDA(cudaStreamWaitEvent(s, c->ev_copy, 0));
+                c->copy_pending = false;
+            }
             // the level-0 rows are on the host already; patch what was rewritten after
             std::vector<uint32_t>& pr = patch_rows;
             pr.insert(pr.end(), fb_rows_host.begin(), fb_rows_host.end());

@@ -58,19 +58,22 @@ def test_mixed_pass_identical(engine, oracle, spec, N, n, k, minq):
                                         ("exponential", 50000, 5, 16), ("far", 40000, 4, 44),
                                         ("clusters:16:0.05", 40000, 18, 32)])
 def test_cell_runs_identical(engine, oracle, spec, N, n, k):
-    """Cell runs (level0_group_span): consecutive sparse cells of a grid row share a work
-    item whose candidates are the union of their neighbourhoods. Outputs, provenance and
-    the reference's per-cell walk counters (candidates_examined) are unchanged."""
+    """Cell runs (level0_group_span, fallback_group_span): consecutive sparse cells of a
+    grid row share a work item whose candidates are the union of their neighbourhoods.
+    Outputs, provenance and the reference's per-cell walk counters (candidates_examined)
+    are unchanged."""
     X = _far_cluster(N, n, 9) if spec == "far" else generate(spec, N, n, 73)
     cfg = RunConfig(k=k, mode="hybrid", seed=73)
     out = []
     try:
         for span in (0, 8):
             engine.set_option("level0_group_span", span)
+            engine.set_option("fallback_group_span", span)
             engine.set_points(X)
             out.append(engine.run(cfg, want_hist=False))
     finally:
         engine.set_option("level0_group_span", 8)
+        engine.set_option("fallback_group_span", 8)
     a, b = out
     assert np.array_equal(b.ids, a.ids) and np.array_equal(b.dist, a.dist)
     assert np.array_equal(b.provenance, a.provenance)
