@@ -1307,9 +1307,18 @@ struct knnj_ctx {
     }
     void prep_tc(Level& lv) {
         if (lv.tc_ready) return;
-        lv.row_halfs = tc_row_halfs();
-        lv.Bh.ensure(N * lv.row_halfs);
-        launch_prep_tc(X64.p, lv.J.p, N, n, d_g.p, 1.0 / tc_S(), lv.row_halfs, lv.Bh.p, s);
+        const uint32_t rh = tc_row_halfs();
+        lv.Bh.ensure(N * rh);
+        // the operand's non-zero prefix (3n+2 halfs, whole 16-byte chunks); the zero padding
+        // up to the 64-half k-block is written once per buffer and kept across rebuilds
+        const uint32_t nz = ((3 * n + 2 + 7) / 8) * 8;
+        const bool padded = lv.bh_zero_p == lv.Bh.p && lv.row_halfs == rh && lv.bh_zero_halfs == nz &&
+                            N <= lv.bh_zero_rows;
+        lv.row_halfs = rh;
+        launch_prep_tc(X64.p, lv.J.p, N, n, d_g.p, 1.0 / tc_S(), rh, lv.Bh.p, s, padded ? nz : rh);
+        if (!padded) lv.bh_zero_rows = N;
+        lv.bh_zero_p = lv.Bh.p;
+        lv.bh_zero_halfs = nz;
         lv.tc_ready = true;
     }
     // Bound delta on |key - sq64 / S^2| for the tensor-core screen. Scaled
@@ -1638,7 +1647,9 @@ struct knnj_ctx {
             // unfiltered count misjudges cells whose neighbourhood holds far clusters)
             std::vector<double> cost(tot);
             std::vector<uint32_t> kept;
-            if (filter_r2 > 0.0 && box_filter && tot)
+            // (when the grid indexes every dim the filter hardly changes an item's cost: the
+            // far blocks it drops are those of clusters close in the first m dims only)
+            if (filter_r2 > 0.0 && box_filter && tot && lv.m < n)
                 kept = filtered_blocks(lv, items_unsorted.p, tot, P.qpos.p, P.adj.p, filter_r2);
             for (uint64_t i = 0; i < tot; ++i) {
                 const uint32_t q = h_items[i].y - h_items[i].x;

@@ -133,6 +133,9 @@ struct Level {
     bool tc_ready = false;
     uint32_t row_halfs = 0, split = 0;
     DBuf<__half> Bh;     // N x row_halfs: tensor-core B operand (knnj_tc.cu)
+    const __half* bh_zero_p = nullptr;  // Bh block whose row padding an earlier build zeroed
+    uint32_t bh_zero_halfs = 0;         // ... beyond this many halfs, for rows of this width
+    uint64_t bh_zero_rows = 0;          // ... in its first this many rows
     DBuf<float> bbox;    // 2n x ceil(N/FB): FP32 boxes (outward) of FB-position blocks (J order)
     bool bbox_ready = false;
     DBuf<double> XJ;     // N x n: FP64 rows in join order (finalize gathers; lazy)
@@ -303,7 +306,8 @@ size_t tc_smem_bytes(const TcShape& sh, uint32_t L, uint32_t n_bins, bool hist);
 void launch_hist_tc(const TcJoinArgs& a, const TcShape& sh, uint64_t nitems, uint64_t N,
                     cudaStream_t s);
 void launch_prep_tc(const double* X64, const uint32_t* A, uint64_t N, uint32_t n, const double* g,
-                    double inv_S, uint32_t row_halfs, __half* Bh, cudaStream_t s);
+                    double inv_S, uint32_t row_halfs, __half* Bh, cudaStream_t s,
+                    uint32_t write_halfs = 0);
 void launch_join_tc(const TcJoinArgs& a, const TcShape& sh, uint64_t nitems, uint64_t N,
                     cudaStream_t s);
 void launch_scale_f32(const float* in, uint64_t n, float scale, float* out, cudaStream_t s);

@@ -205,7 +205,8 @@ __device__ __forceinline__ float warp_kth(float (&a)[R], uint32_t k) {
 // large hi x hi products and |b|^2 last, which keeps the accumulated partial sums small
 // for most of the UMMA chain (the accumulation term of tc_delta).
 __global__ void k_prep_tc(const double* X64, const uint32_t* A, uint64_t N, uint32_t n,
-                          const double* g, double inv_S, uint32_t row_halfs, __half* Bh) {
+                          const double* g, double inv_S, uint32_t row_halfs, __half* Bh,
+                          uint32_t write_halfs) {
     // one thread per row; the row is emitted as 16-byte chunks of 8 halfs, so a warp
     // writes whole 128-byte rows instead of scattered 2-byte stores
     for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < N;
@@ -220,7 +221,8 @@ __global__ void k_prep_tc(const double* X64, const uint32_t* A, uint64_t N, uint
         const __half nl = __double2half(nb - (double)__half2float(nh));
         const uint32_t o = 3 * n;
         uint4* row = reinterpret_cast<uint4*>(Bh + i * row_halfs);
-        for (uint32_t c0 = 0; c0 < row_halfs; c0 += 8) {
+        // (write_halfs < row_halfs: the rest of the row is known zero from an earlier build)
+        for (uint32_t c0 = 0; c0 < write_halfs; c0 += 8) {
             uint32_t w[4];
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
@@ -790,8 +792,9 @@ size_t tc_smem_bytes(const TcShape& sh, uint32_t L, uint32_t n_bins, bool hist) 
 }
 
 void launch_prep_tc(const double* X64, const uint32_t* A, uint64_t N, uint32_t n, const double* g,
-                    double inv_S, uint32_t row_halfs, __half* Bh, cudaStream_t s) {
-    k_prep_tc<<<2368, 256, 0, s>>>(X64, A, N, n, g, inv_S, row_halfs, Bh);
+                    double inv_S, uint32_t row_halfs, __half* Bh, cudaStream_t s, uint32_t write_halfs) {
+    if (write_halfs == 0 || write_halfs > row_halfs) write_halfs = row_halfs;
+    k_prep_tc<<<2368, 256, 0, s>>>(X64, A, N, n, g, inv_S, row_halfs, Bh, write_halfs);
     KJ_CUDA(cudaGetLastError());
     g_launches.fetch_add(1, std::memory_order_relaxed);
 }
