@@ -3288,7 +3288,11 @@ static void run_impl(knnj_ctx* c, const knnj_config* cfg, uint32_t shard, uint32
         eps_pin = pin;
         eps_pin_n = pin ? pairs : 0;
         hdrawer = std::thread([&] {
+            const auto t0 = std::chrono::steady_clock::now();
             hist_q = c->draw_histogram_sample(cfg->hist_query_fraction, derive_seed(cfg->seed, 2));
+            if (trace().on)
+                std::fprintf(stderr, "[knnj] host: histogram sample %zu   %9.3f ms\n", hist_q.size(),
+                             std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
         });
     }
     struct Joiner {
