@@ -2182,8 +2182,8 @@ struct knnj_ctx {
             static const bool want_stats = getenv("KNNJ_JOIN_STATS") != nullptr;
             DBuf<unsigned long long> st;
             if (want_stats) {
-                st.ensure(8);
-                KJ_CUDA(cudaMemsetAsync(st.p, 0, 64, s));
+                st.ensure(24);
+                KJ_CUDA(cudaMemsetAsync(st.p, 0, 24 * 8, s));
                 a.stats = st.p;
             }
             trace().mark("pass: pre-kernel", s);
@@ -2199,11 +2199,14 @@ struct knnj_ctx {
             }
             last_join_kernel_ms = t.ms();
             if (want_stats) {
-                unsigned long long h[8];
-                KJ_CUDA(cudaMemcpyAsync(h, st.p, 64, cudaMemcpyDeviceToHost, s));
+                unsigned long long h[24];
+                KJ_CUDA(cudaMemcpyAsync(h, st.p, 24 * 8, cudaMemcpyDeviceToHost, s));
                 KJ_CUDA(cudaStreamSynchronize(s));
                 fprintf(stderr, "join stats: items %llu rows %llu slabs %llu rare %llu bits %llu inserts %llu compactions %llu ms %.1f\n",
                         (unsigned long long)P.nitems, (unsigned long long)nv, h[0], h[1], h[2], h[3], h[4], last_join_kernel_ms);
+                if (h[23])  // -DKNNJ_TC_CLOCKS builds: cycles per role phase
+                    fprintf(stderr, "join clocks: epi warps %llu | epi accf-wait %llu ld64 %llu fast %llu rare %llu (compact %llu insert %llu) loop %llu prologue %llu total %llu | producer empty-wait %llu total %llu | mma full-wait %llu acce-wait %llu total %llu\n",
+                            h[23], h[8], h[9], h[10], h[11], h[13], h[14], h[12], h[19], h[20], h[16], h[21], h[17], h[18], h[22]);
             }
             last_join_tc = true;
         } else if (mixed) {
@@ -2262,8 +2265,8 @@ struct knnj_ctx {
                 static const bool want_stats = getenv("KNNJ_JOIN_STATS") != nullptr;
                 DBuf<unsigned long long> st;
                 if (want_stats) {
-                    st.ensure(8);
-                    KJ_CUDA(cudaMemsetAsync(st.p, 0, 64, s));
+                    st.ensure(24);
+                    KJ_CUDA(cudaMemsetAsync(st.p, 0, 24 * 8, s));
                     a.stats = st.p;
                 }
                 Timer tt(s);

@@ -133,6 +133,30 @@ __device__ __forceinline__ float tmem_ld1(uint32_t taddr) {
     return __uint_as_float(r);
 }
 
+// dev instrumentation (-DKNNJ_TC_CLOCKS, KNNJ_JOIN_STATS): cycles per role phase into stats[8..]
+#ifdef KNNJ_TC_CLOCKS
+#define TCK(v) const long long v = clock64()
+#define TCADD(i, a, b) (ck[i] += (unsigned long long)((b) - (a)))
+#else
+#define TCK(v)
+#define TCADD(i, a, b)
+#endif
+
+// v[j] for a warp-uniform runtime j, from registers: a 5-level select tree (31 SELs)
+// instead of a local-memory array or a TMEM re-read plus its wait
+__device__ __forceinline__ float pick32(const float (&v)[32], int j) {
+    float a[16], b[8], c[4], d[2];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) a[i] = (j & 16) ? v[i + 16] : v[i];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) b[i] = (j & 8) ? a[i + 8] : a[i];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) c[i] = (j & 4) ? b[i + 4] : b[i];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) d[i] = (j & 2) ? c[i + 2] : c[i];
+    return (j & 1) ? d[1] : d[0];
+}
+
 // 3-input FP32 min (FMNMX3 on sm_100; a NaN input is ignored like fminf)
 __device__ __forceinline__ float fmin3(float a, float b, float c) {
     float d;
@@ -306,6 +330,10 @@ __global__ void __launch_bounds__(32 * (1 + G) + 128 * G, 1)
     __shared__ uint32_t s_tmem;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+#ifdef KNNJ_TC_CLOCKS
+    unsigned long long ck[16] = {};
+    const long long ck_start = clock64();
+#endif
     const uint4 it = p.items[blockIdx.x];
     const uint32_t nq = it.y - it.x;
     constexpr uint32_t TMEM_COLS = G * NB * TN;
@@ -396,6 +424,10 @@ __global__ void __launch_bounds__(32 * (1 + G) + 128 * G, 1)
     __syncthreads();
     fence_after();
     const uint32_t tmem = s_tmem;
+#ifdef KNNJ_TC_CLOCKS
+    const long long ck_loop = clock64();
+    ck[11] += ck_loop - ck_start;
+#endif
 
     // Deterministic tile sequence over the item's ranges. In the first range (the
     // item's own cell row, where its queries live) the sweep starts at the tile
@@ -448,7 +480,10 @@ __global__ void __launch_bounds__(32 * (1 + G) + 128 * G, 1)
             uint32_t s, c;
             for (uint32_t t = 0; next_tile(s, c); ++t) {
                 const int st = t % STAGES;
+                TCK(w0);
                 mbar_wait(&bar_empty[st], ((t / STAGES) & 1) ^ 1);
+                TCK(w1);
+                TCADD(8, w0, w1);
                 mbar_expect_tx(&bar_full[st], KB * BK);
 #pragma unroll
                 for (int kb = 0; kb < KB; ++kb)
@@ -465,8 +500,13 @@ __global__ void __launch_bounds__(32 * (1 + G) + 128 * G, 1)
             const uint32_t a0 = smem_u32(sA);
             for (uint32_t t = 0; next_tile(s, c); ++t) {
                 const int st = t % STAGES, b = t % NB;
+                TCK(w0);
                 mbar_wait(&bar_full[st], (t / STAGES) & 1);
+                TCK(w1);
                 mbar_wait(&bar_acce[gg * NB + b], ((t / NB) & 1) ^ 1);
+                TCK(w2);
+                TCADD(9, w0, w1);
+                TCADD(10, w1, w2);
                 fence_after();
                 const uint32_t b0 = smem_u32(sB + st * KB * BK);
                 const uint32_t dcol = tmem + (gg * NB + b) * TN;
@@ -551,12 +591,18 @@ __global__ void __launch_bounds__(32 * (1 + G) + 128 * G, 1)
         unsigned long long st_slab = 0, st_rare = 0, st_bits = 0, st_ins = 0, st_cmp = 0;
         for (uint32_t t = 0; next_tile(s, c); ++t) {
             const int b = t % NB;
+            TCK(e0);
             mbar_wait(&bar_accf[g * NB + b], (t / NB) & 1);
+            TCK(e1);
+            TCADD(0, e0, e1);
             fence_after();
             const uint32_t tbase = tmem + ((uint32_t)(quarter * 32) << 16) + (g * NB + b) * TN;
             for (uint32_t j0 = 0; j0 < c; j0 += 64) {
                 float v0[32], v1[32];
+                TCK(l0);
                 tmem_ld64(tbase + j0, v0, v1);
+                TCK(l1);
+                TCADD(1, l0, l1);
                 if (p.dbg && blockIdx.x == 0 && t == 0 && g == 0)
 #pragma unroll
                     for (int j = 0; j < 32; ++j) {
@@ -573,9 +619,15 @@ __global__ void __launch_bounds__(32 * (1 + G) + 128 * G, 1)
                 }
                 const bool hit = has_q && !ovf && slab_min64(v0, v1) <= rhs;
                 ++st_slab;
-                if (!__any_sync(0xffffffffu, hit)) continue;
+                const bool any_hit = __any_sync(0xffffffffu, hit);
+                TCK(l2);
+                TCADD(2, l1, l2);
+                if (!any_hit) continue;
                 ++st_rare;
-                // rare path: warp-uniform loop over the columns any lane hit
+                // rare path: each lane walks its own hit columns, the values picked from
+                // registers; the warp loops max-over-lanes times, not once per column any
+                // lane hit. A lane's inserts keep their column order, so its list and cut
+                // evolve exactly as in a column-at-a-time walk.
                 unsigned mk[2] = {0u, 0u};
                 if (hit) {
 #pragma unroll
@@ -586,42 +638,52 @@ __global__ void __launch_bounds__(32 * (1 + G) + 128 * G, 1)
                 }
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
-                    unsigned um = __reduce_or_sync(0xffffffffu, mk[h]);
-                    while (um) {
-                        const int j = __ffs(um) - 1;
-                        um &= um - 1;
+                    unsigned m = mk[h];
+                    while (__any_sync(0xffffffffu, m != 0u)) {
+                        const bool act = m != 0u;
+                        const int j = act ? __ffs(m) - 1 : 0;
+                        m &= m - 1u;
                         ++st_bits;
-                        const float x = tmem_ld1(tbase + j0 + h * 32 + j);
+                        const float x = pick32(h ? v1 : v0, j);
                         const uint32_t pos = s + j0 + h * 32 + j;
-                        bool want = ((mk[h] >> j) & 1u) && x <= rhs && pos != qp;
+                        bool want = act && x <= rhs && pos != qp;
                         // make room: cooperative compaction of every full buffer that needs it
                         unsigned full = __ballot_sync(0xffffffffu, want && cnt == LB);
+                        TCK(r1);
                         while (full) {
                             const int src = __ffs(full) - 1;
                             full &= full - 1;
                             ++st_cmp;
                             compact(src);
                         }
+                        TCK(r2);
+                        TCADD(5, r1, r2);
                         want = want && !ovf && x <= rhs;  // cut may have tightened
-                        if (p.stats) st_ins += __popc(__ballot_sync(0xffffffffu, want));
                         if (want) {
                             mykey[cnt] = x + na;
                             mypos[cnt] = pos;
                             ++cnt;
+                            ++st_ins;
                         }
                     }
                 }
+                TCK(l3);
+                TCADD(3, l2, l3);
             }
             fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&bar_acce[g * NB + b]);
+            TCK(e2);
+            TCADD(4, e0, e2);
         }
-        if (p.stats && lane == 0) {
-            atomicAdd(p.stats + 0, st_slab);
-            atomicAdd(p.stats + 1, st_rare);
-            atomicAdd(p.stats + 2, st_bits);
+        if (p.stats) {  // bits: warp iterations of the rare loop; inserts: list appends
             atomicAdd(p.stats + 3, st_ins);
-            atomicAdd(p.stats + 4, st_cmp);
+            if (lane == 0) {
+                atomicAdd(p.stats + 2, st_bits);
+                atomicAdd(p.stats + 0, st_slab);
+                atomicAdd(p.stats + 1, st_rare);
+                atomicAdd(p.stats + 4, st_cmp);
+            }
         }
         if (has_q) {
             p.out_cnt[row] = ovf ? OVF : cnt;
@@ -765,6 +827,25 @@ __global__ void __launch_bounds__(32 * (1 + G) + 128 * G, 1)
         }
         flush();
     }
+#ifdef KNNJ_TC_CLOCKS
+    ck[12] += clock64() - ck_loop;
+    if (p.stats && lane == 0 && !HIST) {
+        // epilogue warps: 0 accf wait, 1 ld64, 2 fast, 3 rare, 4 loop total, 11 prologue,
+        // 12 role total; producer 8 (empty waits) + 13 total; MMA 9 full, 10 acce + 14 total
+        const int role = warp == 0 ? 0 : (warp <= G ? 1 : 2);
+        if (role == 2)
+            for (int i : {0, 1, 2, 3, 4, 5, 6, 11, 12}) atomicAdd(p.stats + 8 + i, ck[i]);
+        else if (role == 0) {
+            atomicAdd(p.stats + 8 + 8, ck[8]);
+            atomicAdd(p.stats + 8 + 13, ck[12]);
+        } else {
+            atomicAdd(p.stats + 8 + 9, ck[9]);
+            atomicAdd(p.stats + 8 + 10, ck[10]);
+            atomicAdd(p.stats + 8 + 14, ck[12]);
+        }
+        if (role == 2) atomicAdd(p.stats + 8 + 15, 1ull);  // epilogue warps
+    }
+#endif
     fence_before();
     __syncthreads();
     if (HIST) {

@@ -1,0 +1,5 @@
+mkdir -p gpurun_out
+export PYTHONUNBUFFERED=1
+T=${TAG:-r02clk2}
+KNNJ_JOIN_STATS=1 KNNJ_LIB_PATH=paper_1810_04758_b200/ab/clk/libknnj_b200.so timeout 600 python tools/probe_steps.py --config C5 --steps 2 > gpurun_out/${T}_C5_clk.log 2>&1
+echo done
