@@ -1201,6 +1201,8 @@ struct knnj_ctx {
     // points use the SIMT kernels.
     bool tc_enabled = true;
     int tc_small_cta = 2;  // 0 off, 1 on, 2 for n > 8
+    bool tc_item_halves = true;  // small CTAs over 256-query items (tc_halves)
+    bool grid_all_dims = false;  // this run's grid indexes every dim (m == n)
     bool item_radius = true;  // fallback levels filter each item at its rows' K-th bound
     bool split_items = true;  // split oversized work items into candidate-range parts
     uint32_t tc_slack = 24;       // tcgen05 join list capacity K + slack (compaction when full)
@@ -1416,9 +1418,11 @@ struct knnj_ctx {
         } else if (L0 <= 64) {
             // tc_small_cta: 128-query CTAs with a 2-stage ring (~106 KB): two per SM, twice
             // the epilogue warps per SM sub-partition. Measured: NS (18-D) 1675 -> 1585 ms,
-            // C2 unchanged, C5 (4-D) 1455 -> 1492 ms (twice the items to filter and sort), so
-            // the default (2) takes it for n > 8 only
-            const bool small = tc_small_cta == 1 || (tc_small_cta == 2 && n > 8);
+            // C2 unchanged; C5 (4-D) 1455 -> 1492 ms with 128-query items (twice the items
+            // to filter and sort), so the default (2) takes it for n > 8, and where the grid
+            // indexes every dim with the items built at 256 queries (tc_halves)
+            const bool small = tc_small_cta == 1 ||
+                               (tc_small_cta == 2 && (n > 8 || (tc_item_halves && grid_all_dims)));
             c.sh = KB == 1 ? (small ? TcShape{1, 1, 2} : TcShape{1, 2, 4}) : TcShape{2, 1, 3};
             c.L = L0;
         } else {
@@ -1460,9 +1464,17 @@ struct knnj_ctx {
         const TcJoinCfg c = tc_join_cfg(K, lv.prec_w, true);
         return c.ok && c.sh.G == 1;
     }
+    // 128-query CTAs over 256-query items: the items (their boxes, filter and sweep
+    // order) are built at 256 queries and each is launched as two 128-query halves over
+    // the same candidate ranges. Taken when the grid indexes every dim (the box filter
+    // gains little from the smaller query box there, while sorting twice the items'
+    // blocks cost C5 ~125 ms).
+    bool tc_halves(const Level& lv, const TcJoinCfg& c) const {
+        return c.ok && tc_item_halves && c.sh.KB == 1 && c.sh.G == 1 && c.sh.STAGES == 2 && lv.m == n;
+    }
     uint32_t pass_chunk(const Level& lv, uint32_t K, double filter_r2 = 0.0) const {
         const TcJoinCfg c = tc_join_cfg(K, lv.prec_w);
-        if (c.ok) return 128u * c.sh.G;
+        if (c.ok) return 128u * (tc_halves(lv, c) ? 2u : c.sh.G);
         if (pass_mixed(lv, K, filter_r2)) return 128u;
         return (uint32_t)JB;
     }
@@ -1522,6 +1534,7 @@ struct knnj_ctx {
             KJ_CUDA(cudaMemcpyAsync(&nuc, d_nruns.p, 8, cudaMemcpyDeviceToHost, s));
             sync();
         }
+        trace().mark("build: query cells", s);
         DBuf<uint32_t> ufirst, nit, item_off, adj_cnt, adj_off;
         ufirst.ensure(nuc + 1);
         exclusive_sum(sc, ucnt.p, ufirst.p, nuc, s);
@@ -1639,6 +1652,7 @@ struct knnj_ctx {
         KJ_CUDA(cudaMemcpyAsync(h_items.data(), items_unsorted.p, 16 * tot, cudaMemcpyDeviceToHost, s));
         KJ_CUDA(cudaMemcpyAsync(h_work.data(), work.p, 8 * tot, cudaMemcpyDeviceToHost, s));
         sync();
+        trace().mark("build: runs + adjacency + items", s);
         // items are in cell order here; a shard keeps a contiguous run of them
         uint64_t i0 = 0, i1 = tot;
         if (nshard > 1) {
@@ -1853,6 +1867,7 @@ struct knnj_ctx {
         sync();
         P.candidates = cand;
         P.screened = work_pairs;
+        trace().mark("build: shard, splits, LPT order", s);
         if (filter_r2 > 0.0 && box_filter && P.nitems) {
             // rows that carry an upper bound U on their K-th sq (fallback levels: K points
             // within sqrt(U) are known to exist) need no candidate beyond sqrt(U): an item
@@ -1865,6 +1880,31 @@ struct knnj_ctx {
             }
             filter_ranges(lv, P, filter_r2, K > 0 && (pass_uses_tc(lv, K) || P.mixed),
                           d_cut_by_row ? irad.p : nullptr);
+        }
+        if (K && !P.mixed && P.nitems && chunk == 256u && tc_halves(lv, tc_join_cfg(K, lv.prec_w))) {
+            // launch items: each 256-query item as 128-query halves, in the LPT order
+            std::vector<uint4> hi(P.nitems), ho;
+            KJ_CUDA(cudaMemcpyAsync(hi.data(), P.items.p, 16 * P.nitems, cudaMemcpyDeviceToHost, s));
+            sync();
+            ho.reserve(2 * P.nitems);
+            std::vector<uint64_t> at(P.nitems + 1);
+            for (uint64_t i = 0; i < P.nitems; ++i) {
+                at[i] = ho.size();
+                const uint4 it = hi[i];
+                if (it.y - it.x <= 128u) {
+                    ho.push_back(it);
+                    continue;
+                }
+                ho.push_back(make_uint4(it.x, it.x + 128u, it.z, it.w));
+                ho.push_back(make_uint4(it.x + 128u, it.y, it.z, it.w));
+            }
+            at[P.nitems] = ho.size();
+            for (auto& ci : P.chunk_item) ci = at[ci];
+            P.nitems = ho.size();
+            P.items.ensure(P.nitems);
+            KJ_CUDA(cudaMemcpyAsync(P.items.p, ho.data(), 16 * P.nitems, cudaMemcpyHostToDevice, s));
+            sync();
+            P.chunk = 128u;
         }
     }
 
@@ -2792,6 +2832,8 @@ int knnj_set_option(knnj_ctx* c, const char* name, int64_t value) {
         } else if (k == "tc_small_cta") {
             if (value < 0 || value > 2) throw Error(1, "tc_small_cta must be 0, 1 or 2");
             c->tc_small_cta = (int)value;
+        } else if (k == "tc_item_halves") {
+            c->tc_item_halves = value != 0;
         } else if (k == "item_tc") {
             c->item_tc = value != 0;
         } else if (k == "item_tc_min_q") {
@@ -2959,6 +3001,7 @@ int knnj_grid_build(knnj_ctx* c, uint32_t m, double eps, knnj_grid_info* info) {
         if (!(eps > 0.0)) throw Error(1, "grid eps must be positive");
         if (m < 1 || m > c->n) throw Error(1, "grid m must satisfy 1 <= m <= n");
         if (m > 64) throw Error(1, "grid m above 64 is not supported");
+        c->grid_all_dims = m == c->n;
         c->build_level(0, m, eps);
         c->eps0 = eps;
         c->m0 = m;
@@ -3472,7 +3515,8 @@ static void run_impl(knnj_ctx* c, const knnj_config* cfg, uint32_t shard, uint32
         {
             Nvtx nv("knnj: grid build");
             Timer t(s);
-            c->build_level(0, m, eps);
+            c->grid_all_dims = m == c->n;
+        c->build_level(0, m, eps);
             c->eps0 = eps;
             c->m0 = m;
             for (int L = 1; L < 40; ++L) c->levels[L].built = false;

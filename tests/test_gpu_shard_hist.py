@@ -278,6 +278,31 @@ def test_engine_knobs_identical(engine, oracle, opt, val, default):
     assert np.array_equal(b.ids[q], oi) and np.array_equal(b.dist[q], od)
 
 
+@pytest.mark.parametrize("small,halves", [(0, 1), (1, 0), (1, 1)])
+def test_item_halves_identical(engine, oracle, small, halves):
+    """128-query CTAs launched over 256-query items (tc_halves: 4-D, the grid indexes every
+    dim) and 128-query items give the same bits as the 256-query CTA shape."""
+    N, n, k = 300000, 4, 32
+    X = generate("uniform", N, n, 59)
+    cfg = RunConfig(k=k, mode="hybrid", seed=59)
+    out = []
+    for sm, hv in ((0, 1), (small, halves)):
+        engine.set_option("tc_small_cta", sm)
+        engine.set_option("tc_item_halves", hv)
+        engine.set_points(X)
+        out.append(engine.run(cfg, want_hist=False))
+    engine.set_option("tc_small_cta", 2)
+    engine.set_option("tc_item_halves", 1)
+    a, b = out
+    assert b.info["join_tensor_cores"] == 1
+    assert np.array_equal(a.ids, b.ids) and np.array_equal(a.dist, b.dist)
+    assert np.array_equal(a.provenance, b.provenance)
+    W = X[:, b.info["perm"]]
+    q = np.random.default_rng(5).choice(N, 32, replace=False).astype(np.uint32)
+    oi, od = oracle.brute_knn(W, q, k)
+    assert np.array_equal(b.ids[q], oi) and np.array_equal(b.dist[q], od)
+
+
 @pytest.mark.parametrize("spec,N,n,k", [("uniform", 40000, 4, 32), ("exponential", 30000, 6, 20),
                                         ("uniform", 50000, 2, 5), ("mixture", 30000, 3, 8),
                                         ("clusters:4:0.05", 20000, 8, 16)])
