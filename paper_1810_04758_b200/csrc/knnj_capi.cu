@@ -1640,7 +1640,7 @@ struct knnj_ctx {
         DBuf<unsigned long long> csize;
         csize.ensure(nuc);
         launch_adj_fill(lv.B.p, lv.G.p, lv.ncells, ucell.p, nuc, lv.m, d_cs.p, d_cs.p + lv.m,
-                        adj_off.p, P.adj.p, csize.p, s, uspan.p);
+                        adj_off.p, P.adj.p, csize.p, s, uspan.p, adj_order(lv.m));
         DBuf<uint4> items_unsorted;
         DBuf<unsigned long long> work;
         items_unsorted.ensure(tot);
@@ -1868,7 +1868,14 @@ struct knnj_ctx {
         P.candidates = cand;
         P.screened = work_pairs;
         trace().mark("build: shard, splits, LPT order", s);
-        if (filter_r2 > 0.0 && box_filter && P.nitems) {
+        // Level 0 on a grid over every dim with a radius of at least half the cell width:
+        // a 128-position block spans most of its cell, so hardly any block lies beyond the
+        // radius from an item's query box (C5: 0.4% of the pairs), and the nearer-rows-first
+        // adjacency order (adj_order) gives most of the per-block sweep's effect. C5: build
+        // 72 -> 20 ms, join kernel 855 -> 864 ms.
+        const bool filter_pays = !(filter_skip_all_dims && &lv == &levels[0] && lv.m == n &&
+                                   !P.mixed && !d_cut_by_row && filter_r2 >= 0.25 * lv.w * lv.w);
+        if (filter_r2 > 0.0 && box_filter && P.nitems && filter_pays) {
             // rows that carry an upper bound U on their K-th sq (fallback levels: K points
             // within sqrt(U) are known to exist) need no candidate beyond sqrt(U): an item
             // filters at the largest bound among its rows
@@ -1906,6 +1913,38 @@ struct knnj_ctx {
             sync();
             P.chunk = 128u;
         }
+    }
+
+    // The order of an item's neighbour rows (k_adj): own row first, then by the number of
+    // dims (of the first m-1) the row is offset in -- the nearer rows first, so the join's
+    // top-K cut tightens early when no per-block sweep order is built. Null: index order.
+    bool adj_norm_order = true;
+    bool filter_skip_all_dims = true;  // build_pass: filter_pays
+    DBuf<uint16_t> d_adj_order;
+    uint32_t adj_order_m = 0;
+    const uint16_t* adj_order(uint32_t m) {
+        if (!adj_norm_order || m < 2) return nullptr;
+        if (adj_order_m != m) {
+            uint32_t R = 1;
+            for (uint32_t j = 0; j + 1 < m; ++j) R *= 3;
+            if (R > 65535) return nullptr;
+            std::vector<uint16_t> ord(R);
+            std::vector<uint32_t> nz(R);
+            for (uint32_t r = 0; r < R; ++r) ord[r] = (uint16_t)r;
+            // digits of r: base 3 over the m-1 row dims, 1 = no offset (own row: all ones)
+            for (uint32_t r = 0; r < R; ++r) {
+                uint32_t z = 0;
+                uint32_t t = r;
+                for (uint32_t j = 0; j + 1 < m; ++j, t /= 3) z += t % 3 != 1;
+                nz[r] = z;
+            }
+            std::stable_sort(ord.begin(), ord.end(), [&](uint16_t a, uint16_t b) { return nz[a] < nz[b]; });
+            d_adj_order.ensure(R);
+            KJ_CUDA(cudaMemcpyAsync(d_adj_order.p, ord.data(), 2 * R, cudaMemcpyHostToDevice, s));
+            sync();
+            adj_order_m = m;
+        }
+        return d_adj_order.p;
     }
 
     // launches a big level-0 pass is cut into (build_pass; 1 = one launch)
@@ -2832,6 +2871,10 @@ int knnj_set_option(knnj_ctx* c, const char* name, int64_t value) {
         } else if (k == "tc_small_cta") {
             if (value < 0 || value > 2) throw Error(1, "tc_small_cta must be 0, 1 or 2");
             c->tc_small_cta = (int)value;
+        } else if (k == "filter_skip_all_dims") {
+            c->filter_skip_all_dims = value != 0;
+        } else if (k == "adj_norm_order") {
+            c->adj_norm_order = value != 0;
         } else if (k == "tc_item_halves") {
             c->tc_item_halves = value != 0;
         } else if (k == "item_tc") {

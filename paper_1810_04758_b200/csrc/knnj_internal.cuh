@@ -349,7 +349,8 @@ void launch_adj_count(const uint64_t* B, uint64_t ncells, const uint32_t* cells,
 void launch_adj_fill(const uint64_t* B, const uint2* G, uint64_t ncells, const uint32_t* cells,
                      uint64_t nc, uint32_t m, const uint64_t* cpd, const uint64_t* strides,
                      const uint32_t* offs, uint2* adj, unsigned long long* csize,
-                     cudaStream_t s, const uint32_t* spans = nullptr);
+                     cudaStream_t s, const uint32_t* spans = nullptr,
+                     const uint16_t* order = nullptr);
 void launch_items(const uint32_t* ufirst, const uint32_t* ucnt, const uint32_t* item_off,
                   const uint32_t* adj_off, uint64_t nuc, const unsigned long long* csize,
                   uint4* items, unsigned long long* work, uint32_t chunk, cudaStream_t s);

@@ -1079,7 +1079,7 @@ template <bool FILL>
 __global__ void k_adj(const uint64_t* B, const uint2* G, uint64_t ncells, const uint32_t* cells,
                       uint64_t nc, uint32_t m, const uint64_t* cpd, const uint64_t* strides,
                       uint32_t* counts, const uint32_t* offs, uint2* adj,
-                      unsigned long long* csize, const uint32_t* spans) {
+                      unsigned long long* csize, const uint32_t* spans, const uint16_t* order) {
     const uint64_t w = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (w >= nc) return;
@@ -1100,12 +1100,15 @@ __global__ void k_adj(const uint64_t* B, const uint2* G, uint64_t ncells, const 
     const uint64_t hi_l = min(c[ml] + (spans ? spans[w] : 1u), cpd[ml] - 1);
     uint32_t written = 0;
     unsigned long long sz = 0;
-    // process own row first (iteration -1), then all rows != own
-    for (int64_t base = -32; base < (int64_t)R; base += 32) {
+    // process own row first (iteration -1), then all rows != own; with `order` (own row
+    // first, then by the number of offset dims: the nearer rows first) in one sweep
+    for (int64_t base = order ? 0 : -32; base < (int64_t)R; base += 32) {
         int64_t r = base + lane;
         bool valid = false;
         uint2 rng = make_uint2(0, 0);
-        if (base < 0) {
+        if (order) {
+            r = r < (int64_t)R ? (int64_t)order[r] : -1;
+        } else if (base < 0) {
             if (lane == 0) r = (int64_t)own;
             else r = -1;
         } else if (r >= (int64_t)R || (uint64_t)r == own) {
@@ -1194,17 +1197,17 @@ void launch_adj_count(const uint64_t* B, uint64_t ncells, const uint32_t* cells,
                       unsigned long long* csize) {
     if (!nc) return;
     k_adj<false><<<(unsigned)((nc * 32 + 255) / 256), 256, 0, s>>>(
-        B, G, ncells, cells, nc, m, cpd, strides, counts, nullptr, nullptr, csize, spans);
+        B, G, ncells, cells, nc, m, cpd, strides, counts, nullptr, nullptr, csize, spans, nullptr);
     KJ_CUDA(cudaGetLastError());
     g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 void launch_adj_fill(const uint64_t* B, const uint2* G, uint64_t ncells, const uint32_t* cells,
                      uint64_t nc, uint32_t m, const uint64_t* cpd, const uint64_t* strides,
                      const uint32_t* offs, uint2* adj, unsigned long long* csize,
-                     cudaStream_t s, const uint32_t* spans) {
+                     cudaStream_t s, const uint32_t* spans, const uint16_t* order) {
     if (!nc) return;
     k_adj<true><<<(unsigned)((nc * 32 + 255) / 256), 256, 0, s>>>(
-        B, G, ncells, cells, nc, m, cpd, strides, nullptr, offs, adj, csize, spans);
+        B, G, ncells, cells, nc, m, cpd, strides, nullptr, offs, adj, csize, spans, order);
     KJ_CUDA(cudaGetLastError());
     g_launches.fetch_add(1, std::memory_order_relaxed);
 }

@@ -278,6 +278,30 @@ def test_engine_knobs_identical(engine, oracle, opt, val, default):
     assert np.array_equal(b.ids[q], oi) and np.array_equal(b.dist[q], od)
 
 
+@pytest.mark.parametrize("opt", ["filter_skip_all_dims", "adj_norm_order"])
+@pytest.mark.parametrize("spec,N,n,k", [("uniform", 200000, 4, 32), ("exponential", 60000, 6, 20),
+                                        ("mixture", 50000, 3, 8)])
+def test_all_dims_knobs_identical(engine, oracle, opt, spec, N, n, k):
+    """On grids over every dim: skipping the box filter at level 0 and the nearer-rows-first
+    adjacency order change only which pairs are screened and in what order."""
+    X = generate(spec, N, n, 61)
+    cfg = RunConfig(k=k, mode="hybrid", seed=61)
+    out = []
+    for v in (1, 0):
+        engine.set_option(opt, v)
+        engine.set_points(X)
+        out.append(engine.run(cfg, want_hist=False))
+    engine.set_option(opt, 1)
+    a, b = out
+    assert np.array_equal(a.ids, b.ids) and np.array_equal(a.dist, b.dist)
+    assert np.array_equal(a.provenance, b.provenance)
+    assert a.info["failed_count"] == b.info["failed_count"]
+    W = X[:, a.info["perm"]]
+    q = np.random.default_rng(8).choice(N, 32, replace=False).astype(np.uint32)
+    oi, od = oracle.brute_knn(W, q, k)
+    assert np.array_equal(a.ids[q], oi) and np.array_equal(a.dist[q], od)
+
+
 @pytest.mark.parametrize("small,halves", [(0, 1), (1, 0), (1, 1)])
 def test_item_halves_identical(engine, oracle, small, halves):
     """128-query CTAs launched over 256-query items (tc_halves: 4-D, the grid indexes every

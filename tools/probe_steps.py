@@ -41,5 +41,5 @@ for st in range(a.steps):
     w = time.time() - t
     i = r.info
     print(f"[{a.config} N={N} step {st}] wall={w*1e3:.1f}ms " +
-          " ".join(f"{k}={i[k]:.2f}" if isinstance(i[k], float) else f"{k}={i[k]}" for k in keys),
+          " ".join(f"{k}={i[k]:.4g}" if isinstance(i[k], float) else f"{k}={i[k]}" for k in keys),
           flush=True)
