@@ -1,0 +1,9 @@
+mkdir -p gpurun_out
+export PYTHONUNBUFFERED=1
+T=${TAG:-r02cp2}
+for cb in 37 56; do
+timeout 900 python tools/probe_steps.py --config C5 --steps 3 --pinned --opt copy_blocks=$cb > gpurun_out/${T}_C5_cb$cb.log 2>&1
+done
+timeout 900 python tools/probe_steps.py --config C5 --steps 3 --pinned --opt fin_blocks=148 > gpurun_out/${T}_C5_fb148.log 2>&1
+timeout 900 python tools/probe_steps.py --config C5 --steps 3 --pinned --opt join_chunks=8 > gpurun_out/${T}_C5_ch8.log 2>&1
+echo done
