@@ -304,6 +304,30 @@ __device__ __forceinline__ void rank_entries(const double (&sq)[EMAX], const uin
     }
 }
 
+// The same ranks with the row's entries staged in shared memory: one broadcast 16-byte
+// load per source entry instead of three shuffles (the finalize is bound by its LSU /
+// shuffle issue: ncu r02fin, 46% LSU, 80% SM throughput).
+template <int E, int EMAX>
+__device__ __forceinline__ void rank_entries_smem(const double (&sq)[EMAX], const uint32_t (&id)[EMAX],
+                                                  uint32_t (&rk)[EMAX], uint32_t c, uint4* ent) {
+    const int lane = threadIdx.x & 31;
+    __syncwarp();  // the previous row's reads are done
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        const unsigned long long b = (unsigned long long)__double_as_longlong(sq[e]);
+        ent[e * 32 + lane] = make_uint4((uint32_t)b, (uint32_t)(b >> 32), id[e], 0u);
+    }
+    __syncwarp();
+#pragma unroll 4
+    for (uint32_t src = 0; src < c; ++src) {
+        const uint4 v = ent[src];
+        const double sv = __longlong_as_double((long long)(((unsigned long long)v.y << 32) | v.x));
+#pragma unroll
+        for (int f = 0; f < E; ++f)
+            if (pair_less(sv, v.z, sq[f], id[f])) ++rk[f];
+    }
+}
+
 // ---------------------------------------------------------------- finalize
 
 // One warp per launch row: exact FP64 distances for the screened list, exact
@@ -327,7 +351,8 @@ __device__ __forceinline__ void finalize_status(const FinalArgs& a, uint32_t c, 
 }
 
 template <int EMAX>
-__device__ __forceinline__ void finalize_row(const FinalArgs& a, uint64_t row, int lane) {
+__device__ __forceinline__ void finalize_row(const FinalArgs& a, uint64_t row, int lane,
+                                             uint4* ent = nullptr) {
     const uint32_t c = a.cnt[row];
     if (c == SKIP) return;  // a split row: its parts are finalized and merged separately
     const uint32_t orow = a.qrow[row];
@@ -356,7 +381,10 @@ __device__ __forceinline__ void finalize_row(const FinalArgs& a, uint64_t row, i
     }
     // exact (sq, id) rank of every entry: compile-time entry count per lane, so the
     // inner comparisons are not issued for empty register slots
-    switch (E) {
+    if (ent) {  // staged ranks (lists of at most 64 entries)
+        if (E == 1) rank_entries_smem<1, EMAX>(sq, id, rk, c, ent);
+        else if (E == 2) rank_entries_smem<2, EMAX>(sq, id, rk, c, ent);
+    } else switch (E) {
 #define KJ_RANK(EE)                                        \
         case EE:                                           \
             rank_entries<EE, EMAX>(sq, id, rk, c);         \
@@ -395,8 +423,10 @@ template <int EMAX>
 __global__ void k_finalize(FinalArgs a) {
     const int lane = threadIdx.x & 31;
     const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+    __shared__ uint4 s_ent[EMAX == 2 ? 8 * 64 : 1];  // 256-thread blocks: 8 warps x 64 entries
+    uint4* ent = EMAX == 2 ? s_ent + (threadIdx.x >> 5) * 64 : nullptr;
     for (uint64_t w = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w < a.nrows; w += nw)
-        finalize_row<EMAX>(a, w, lane);
+        finalize_row<EMAX>(a, w, lane, ent);
 }
 
 // ---------------------------------------------------------------- histogram
