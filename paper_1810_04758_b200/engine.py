@@ -104,6 +104,7 @@ class Engine:
         self.device = device
         self.N = 0
         self.n = 0
+        self._all_queries = None
 
     def close(self) -> None:
         if getattr(self, "h", None):
@@ -299,7 +300,12 @@ class Engine:
         if info.eps_fallback:
             warnings.append("beta target unreachable within eps_mean; clamped to the histogram maximum")
         if queries is None:
-            queries = np.arange(N, dtype=np.uint32)
+            # every point is a query: one read-only 0..N-1 array per point set (a fresh
+            # 4N-byte array per run costs the host ~50 ms at 100M points)
+            if self._all_queries is None or self._all_queries.size != N:
+                self._all_queries = np.arange(N, dtype=np.uint32)
+                self._all_queries.flags.writeable = False
+            queries = self._all_queries
         rows = nq
         if owned is not None:
             rows = int(info.n_owned)
