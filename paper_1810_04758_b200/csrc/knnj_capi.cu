@@ -722,7 +722,7 @@ struct knnj_ctx {
               hist_p0 == p0 && hist_p1 == p1)) {
             grid_tables_into(hist_lv, m, w, p0, p1, false);
             hist_Xs.ensure((uint64_t)n * Npad);
-            launch_gather_soa(Xf.p, hist_lv.A.p, hist_lv.npts, n, Npad, hist_Xs.p, s);
+            launch_gather_x64(X64.p, d_g.p, hist_lv.A.p, hist_lv.npts, n, Npad, hist_Xs.p, s);
             hist_mins.ensure(m);
             KJ_CUDA(cudaMemcpyAsync(hist_mins.p, hist_lv.mins.data(), 8 * m, cudaMemcpyHostToDevice, s));
             hist_lv.built = true;
@@ -2376,7 +2376,7 @@ struct knnj_ctx {
                 JoinArgs a{};
                 if (!lv.xs_ready) {
                     lv.Xs.ensure((uint64_t)n * Npad);
-                    launch_gather_soa(Xf.p, lv.J.p, N, n, Npad, lv.Xs.p, s);
+                    launch_gather_x64(X64.p, d_g.p, lv.J.p, N, n, Npad, lv.Xs.p, s);
                     lv.xs_ready = true;
                 }
                 a.Xs = lv.Xs.p;
@@ -2401,7 +2401,7 @@ struct knnj_ctx {
             JoinArgs a{};
             if (!lv.xs_ready) {
                 lv.Xs.ensure((uint64_t)n * Npad);
-                launch_gather_soa(Xf.p, lv.J.p, N, n, Npad, lv.Xs.p, s);
+                launch_gather_x64(X64.p, d_g.p, lv.J.p, N, n, Npad, lv.Xs.p, s);
                 lv.xs_ready = true;
             }
             a.Xs = lv.Xs.p;

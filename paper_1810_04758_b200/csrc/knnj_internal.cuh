@@ -338,7 +338,7 @@ void launch_head_flags(const uint64_t* keys, uint64_t N, uint32_t* flags, cudaSt
 void launch_grid_tables(const uint64_t* skeys, const uint32_t* A, const uint32_t* runidx,
                         uint64_t N, uint64_t* B, uint2* G, uint32_t* slot, uint32_t* posOf,
                         cudaStream_t s);
-void launch_gather_soa(const float* Xf, const uint32_t* A, uint64_t N, uint32_t n,
+void launch_gather_x64(const double* X, const double* g, const uint32_t* A, uint64_t N, uint32_t n,
                        uint64_t Npad, float* Xs, cudaStream_t s);
 void launch_map_u32(const uint32_t* idx, const uint32_t* table, uint64_t n, uint32_t* out,
                     cudaStream_t s);

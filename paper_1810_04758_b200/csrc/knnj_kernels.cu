@@ -1065,21 +1065,25 @@ void launch_grid_tables(const uint64_t* skeys, const uint32_t* A, const uint32_t
     g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
-__global__ void k_gather_soa(const float* Xf, const uint32_t* A, uint64_t N, uint32_t n,
-                             uint64_t Npad, float* Xs) {
+// FP32 SoA rows in a grid's position order (A: position -> point), gathered from the
+// FP64 point rows: (float)(x - g), the value k_to_float_soa stores, from one contiguous
+// 8n-byte row per point instead of n scattered 4-byte reads of the SoA copy (one sector
+// instead of four at n = 4)
+__global__ void k_gather_x64(const double* X, const double* g, const uint32_t* A, uint64_t N,
+                             uint32_t n, uint64_t Npad, float* Xs) {
     for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < Npad;
          i += uint64_t(gridDim.x) * blockDim.x) {
         if (i < N) {
-            const uint32_t src = A[i];
-            for (uint32_t d = 0; d < n; ++d) Xs[uint64_t(d) * Npad + i] = Xf[uint64_t(d) * Npad + src];
+            const double* x = X + (uint64_t)A[i] * n;
+            for (uint32_t d = 0; d < n; ++d) Xs[uint64_t(d) * Npad + i] = (float)(x[d] - g[d]);
         } else {
             for (uint32_t d = 0; d < n; ++d) Xs[uint64_t(d) * Npad + i] = 0.f;
         }
     }
 }
-void launch_gather_soa(const float* Xf, const uint32_t* A, uint64_t N, uint32_t n,
+void launch_gather_x64(const double* X, const double* g, const uint32_t* A, uint64_t N, uint32_t n,
                        uint64_t Npad, float* Xs, cudaStream_t s) {
-    k_gather_soa<<<2368, 256, 0, s>>>(Xf, A, N, n, Npad, Xs);
+    k_gather_x64<<<2368, 256, 0, s>>>(X, g, A, N, n, Npad, Xs);
     KJ_CUDA(cudaGetLastError());
     g_launches.fetch_add(1, std::memory_order_relaxed);
 }
