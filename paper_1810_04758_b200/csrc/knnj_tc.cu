@@ -872,10 +872,64 @@ size_t tc_smem_bytes(const TcShape& sh, uint32_t L, uint32_t n_bins, bool hist) 
     return b;
 }
 
+// k_prep_tc for a compile-time n <= 8: the row's halfs from registers (no per-half
+// division by n, no re-reads of the point row); the same values, bit for bit
+template <int NN>
+__global__ void k_prep_tc_n(const double* X64, const uint32_t* A, uint64_t N, const double* g,
+                            double inv_S, uint32_t row_halfs, __half* Bh, uint32_t write_halfs) {
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < N;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const double* x = X64 + (uint64_t)A[i] * NN;
+        double nb = 0.0;
+        __half hi[NN], lo[NN];
+#pragma unroll
+        for (int d = 0; d < NN; ++d) {
+            const double v = (x[d] - g[d]) * inv_S;
+            nb += v * v;
+            hi[d] = __double2half(v);
+            lo[d] = __double2half(v - (double)__half2float(hi[d]));
+        }
+        const __half nh = __double2half(nb);
+        const __half nl = __double2half(nb - (double)__half2float(nh));
+        constexpr int O = 3 * NN;
+        constexpr int NZ = ((O + 2 + 7) / 8) * 8;  // the 16-byte chunks holding non-zeros
+        uint4* row = reinterpret_cast<uint4*>(Bh + i * row_halfs);
+#pragma unroll
+        for (int c0 = 0; c0 < NZ; c0 += 8) {
+            uint32_t w[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                uint32_t pair = 0;
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int k = c0 + 2 * e + h;  // lo | hi | hi | nb_hi | nb_lo | 0...
+                    const __half hv = k < NN ? lo[k < NN ? k : 0]
+                                      : k < 2 * NN ? hi[k < 2 * NN ? k - NN : 0]
+                                      : k < O ? hi[k < O ? k - 2 * NN : 0]
+                                      : k == O ? nh : k == O + 1 ? nl : __float2half(0.f);
+                    pair |= (uint32_t)__half_as_ushort(hv) << (16 * h);
+                }
+                w[e] = pair;
+            }
+            row[c0 / 8] = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+        // (write_halfs < row_halfs: the rest of the row is known zero from an earlier build)
+        for (uint32_t c0 = NZ; c0 < write_halfs; c0 += 8) row[c0 / 8] = make_uint4(0u, 0u, 0u, 0u);
+    }
+}
+
 void launch_prep_tc(const double* X64, const uint32_t* A, uint64_t N, uint32_t n, const double* g,
                     double inv_S, uint32_t row_halfs, __half* Bh, cudaStream_t s, uint32_t write_halfs) {
     if (write_halfs == 0 || write_halfs > row_halfs) write_halfs = row_halfs;
-    k_prep_tc<<<2368, 256, 0, s>>>(X64, A, N, n, g, inv_S, row_halfs, Bh, write_halfs);
+    switch (n) {
+#define KJ_PREP(NN)                                                                            \
+    case NN:                                                                                   \
+        k_prep_tc_n<NN><<<2368, 256, 0, s>>>(X64, A, N, g, inv_S, row_halfs, Bh, write_halfs); \
+        break;
+        KJ_PREP(1) KJ_PREP(2) KJ_PREP(3) KJ_PREP(4) KJ_PREP(5) KJ_PREP(6) KJ_PREP(7) KJ_PREP(8)
+#undef KJ_PREP
+        default: k_prep_tc<<<2368, 256, 0, s>>>(X64, A, N, n, g, inv_S, row_halfs, Bh, write_halfs);
+    }
     KJ_CUDA(cudaGetLastError());
     g_launches.fetch_add(1, std::memory_order_relaxed);
 }
