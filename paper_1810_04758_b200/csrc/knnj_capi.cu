@@ -1919,6 +1919,7 @@ struct knnj_ctx {
     // dims (of the first m-1) the row is offset in -- the nearer rows first, so the join's
     // top-K cut tightens early when no per-block sweep order is built. Null: index order.
     bool adj_norm_order = true;
+    bool chunk_device_out = false;  // chunked level-0 pass (finalize overlapped) for device outputs too
     bool filter_skip_all_dims = true;  // build_pass: filter_pays
     DBuf<uint16_t> d_adj_order;
     uint32_t adj_order_m = 0;
@@ -2873,6 +2874,8 @@ int knnj_set_option(knnj_ctx* c, const char* name, int64_t value) {
             c->tc_small_cta = (int)value;
         } else if (k == "filter_skip_all_dims") {
             c->filter_skip_all_dims = value != 0;
+        } else if (k == "chunk_device_out") {
+            c->chunk_device_out = value != 0;
         } else if (k == "adj_norm_order") {
             c->adj_norm_order = value != 0;
         } else if (k == "tc_item_halves") {
@@ -3659,7 +3662,8 @@ static void run_impl(knnj_ctx* c, const knnj_config* cfg, uint32_t shard, uint32
                 // chunked launches only pay for the streamed result copy (each chunk restarts
                 // the LPT schedule: on skewed data the tails cost more than the finalize
                 // overlap saves)
-                c->stream_chunks = (nshard == 1 && !fine && h_ids_dev) ? c->join_chunks : 1;
+                c->stream_chunks = (nshard == 1 && !fine && (h_ids_dev || c->chunk_device_out))
+                                    ? c->join_chunks : 1;
                 if (fine_grid) {
                     c->build_level(43, m, wf);
                     lvb = &c->levels[43];
